@@ -1,0 +1,288 @@
+#!/usr/bin/env python3
+"""Benchmark: full PF-SMC particle-steps/s of the per-observation update
+(BASELINE.json metric) on BASELINE config 2 — Lotka-Volterra, N = 2^20
+particles per GPU, FP64, h = 0.1 (one LMM step per observation), a = 0.98,
+synthetic RK4 observations.
+
+One bench "step" = one pf_step (filter.cpp:292-394) over the whole resident
+ensemble for the next observation. Timing: per-step CUDA events on the
+sampler's stream, W >= 3 warm-up steps, the L2 flushed (256 MiB write)
+between timed steps outside the events; max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation of the path
+(oracle/_ref: the unmodified C++ pf_step, Backend::parallel(all host
+threads)) on the same workload, each step a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec (full PF-SMC step)"
+UNIT = "particle-steps/s"
+N_PER_GPU = 1 << 20
+T_OBS = 1000
+# Algorithmic bytes per particle, F = d + p + 1.
+D, P = 2, 2
+F = D + P + 1
+STEP_BYTES = 24 * F + 56                     # whole step, minimal fused pipeline
+KERNEL_BYTES = {                              # per particle per launch
+    "k_predict": 8 * (D + P) + 8 + 8 + 8,     # record + lw in; ll_bar + lg out
+    "k_scan_sums": 8,                         # lg in
+    "k_scan_pieces": 8,                       # lg in
+    "k_scan_cdf": 8 + 8 + 2,                  # lg in; cdf + local guide out
+    "k_update": 8 * (D + P) + 8 + 8 * (D + P) + 8 + 4,  # gather rec + ll_bar; rec + lw + anc out
+}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(n, steps, seconds_cap, workers, prob, use_ref=True):
+    """Times the reference (oracle/_ref) or the C port on a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ctypes import REF_SO, Oracle, Reference, StepConfig
+    kind = "reference" if (use_ref and os.path.exists(REF_SO)) else "port"
+    O = Oracle()
+    sc = StepConfig(model="lv", family=prob.cfg.family, order=prob.cfg.order, h=0.1, a=0.98,
+                    seed=prob.cfg.seed, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, prob.cfg.seed, **prob.prior)
+    done, secs = 0, 0.0
+    tp = 0.0
+    while done < steps and (secs < seconds_cap or done < 1):
+        j = done + 1
+        t1 = prob.times[j - 1]
+        if kind == "reference":
+            secs += Reference().time_steps(sc, ens, prob.ys[j - 1:j], [t1], j, tp, workers)
+        else:
+            t0 = time.perf_counter()
+            O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1)
+            secs += time.perf_counter() - t0
+        tp = t1
+        done += 1
+    return {"value": n * done / secs, "unit": UNIT, "cores": workers if kind == "reference" else 1,
+            "kind": kind, "steps": done, "seconds": secs,
+            "sample": f"LV N={n}, observations 1..{done}, "
+                      + (f"reference pf_step Backend::parallel({workers})" if kind == "reference"
+                         else "C restatement, 1 thread")}
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    from paper_1411_1702_b200 import problems
+    workers = len(os.sched_getaffinity(0))
+    prob = problems.lotka_volterra(particles=N_PER_GPU, T=max(args.steps + args.warmup, 4), seed=1)
+    # each step: one reference pf_step at the full N = 2^20 (bounded: <= 30 s total)
+    cb = cpu_reference(N_PER_GPU, args.steps, 30.0, workers, prob)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": cb["steps"],
+            "warmup": 0, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded RK4 LV)",
+            "impl": "reference",
+            "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles": N_PER_GPU,
+                       "h": 0.1, "shrink_a": 0.98, "integrator": "am2 (m=1)"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--particles", type=int, default=N_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    args = ap.parse_args()
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import numpy as np
+    import torch
+
+    from paper_1411_1702_b200 import problems
+    from paper_1411_1702_b200.sampler import GpuSampler
+
+    if args.warmup < 3:
+        args.warmup = 3
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    n = args.particles
+    T = min(T_OBS, args.steps + args.warmup + args.e2e_steps + 1)
+    prob = problems.lotka_volterra(particles=n, T=T_OBS, seed=1)
+    # replicas: every rank filters its own N-particle ensemble
+    cfg = prob.cfg
+    gpu = GpuSampler("lv", cfg, prob.obs, device=local)
+    gpu.initialize_uniform(**prob.prior)
+    gpu.upload_observations(prob.ys[:T], prob.times[:T], 0.0)
+    stream = torch.cuda.ExternalStream(gpu.stream_handle, device=local)
+
+    j = 0
+    for _ in range(args.warmup):
+        j += 1
+        gpu.step_resident(j)
+    gpu.synchronize()
+    gpu.set_kernel_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            gpu.flush_l2()
+            j += 1
+            with torch.cuda.stream(stream):
+                ev[k][0].record(stream)
+            gpu.step_resident(j)
+            with torch.cuda.stream(stream):
+                ev[k][1].record(stream)
+        last = gpu.synchronize()
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kt = gpu.kernel_times()
+    gpu.set_kernel_timing(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n * world * args.steps / (total_ms / 1e3)
+
+    # e2e: the drop-in C-ABI pf_step with host buffers (y in, trace row out)
+    ys_pinned = torch.tensor(prob.ys[:T], dtype=torch.float64).pin_memory().numpy()
+    e2e_s = 0.0
+    e2e_steps = max(1, min(args.e2e_steps, T - j))
+    for _ in range(e2e_steps):
+        j += 1
+        gpu.flush_l2()
+        gpu.synchronize()
+        t0 = time.perf_counter()
+        gpu.pf_step(ys_pinned[j - 1], j, prob.times[j - 2], prob.times[j - 1])
+        e2e_s += time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": n * world * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * 2,
+           "d2h_bytes_per_step": 8 * (2 * P + D + 1), "steps": e2e_steps,
+           "path": "pfsmc_gpu_step (C ABI drop-in for filter::pf_step), blocking"}
+
+    peaks, peak_kind = _peaks()
+    hbm = float(peaks["hbm_gbs"])
+    names = list(kt.keys())
+    dom = max(names, key=lambda k: kt[k])
+    avg_ms = kt[dom] / args.steps
+    achieved = KERNEL_BYTES[dom] * n / (avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_gbs = STEP_BYTES * n / (total_ms / args.steps / 1e3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RK4 Lotka-Volterra observations, uniform priors)",
+            "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles_per_gpu": n,
+                       "global_particles": n * world, "d": D, "p": P, "h": 0.1, "shrink_a": 0.98,
+                       "integrator": "am2 (reference semantics: m=1 => AM1 corrector, AB1 predictor)",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind},
+            "step_roofline": {"bytes_per_particle": STEP_BYTES, "achieved": step_gbs, "peak": hbm,
+                              "frac": step_gbs / hbm},
+            "kernel_ms_per_step": {k: v / args.steps for k, v in kt.items()},
+            "gpu_launches": 5 * args.steps,
+            "e2e": e2e, "clocks": clk.summary(),
+            "final_trace": {"theta_mean": list(map(float, last[:P])), "ess": float(last[-1])}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(N_PER_GPU, 20, 15.0, len(os.sched_getaffinity(0)), prob)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line))
+    gpu.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

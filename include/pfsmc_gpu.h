@@ -1,0 +1,163 @@
+/* pfsmc_gpu — B200-native drop-in for the reference per-observation update
+ * `pfsmc::filter::pf_step` of the LMM PF-SMC sampler (arXiv 1411.1702).
+ *
+ * Plain C ABI: opaque handles, plain pointers and sizes, integer status
+ * codes plus a thread-local last-error string — the same conventions as the
+ * reference's C ABI (/root/reference/proj/include/pfsmc.h:12-25,
+ * src/capi.cpp:13-37). The reference's own C ABI is experiment-level only
+ * (config / generate / run / bench / report, pfsmc.h:27-59) and has no
+ * per-step entry point; the calls below are what a caller of
+ *   StepResult pf_step(Ensemble&, std::span<const double> y, size_t j,
+ *                      double t_prev, double t_obs, const PfConfig&,
+ *                      exec::Backend&, const models::OdeModel&,
+ *                      const ObservationModel&, PhaseTimings*)
+ * (filter.hpp:151-155, filter.cpp:292-394) binds instead. Each entry point
+ * names the reference interface it replaces.
+ *
+ * Handles are not re-entrant; several handles may coexist (one per GPU).
+ * Ensembles cross this boundary as the reference stores them: row-major AoS
+ * (states N x d, params_u N x p, unconstrained = log space), normalised
+ * logw, mean_u (p), cov_u (p x p) — filter.hpp:19-28.
+ */
+#ifndef PFSMC_GPU_H
+#define PFSMC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same values as pfsmc_status (pfsmc.h:12-18). NUMERICAL is raised at the
+ * same step j as the reference raises NumericalError (total degeneracy in
+ * fitness_weights / update_weights, chol_psd failure); CONFIG where it
+ * raises ConfigError (PfConfig::validate, interval_step_count). */
+typedef enum pfsmc_gpu_status {
+  PFSMC_GPU_OK = 0,
+  PFSMC_GPU_ERR_INTERNAL = 1,
+  PFSMC_GPU_ERR_CONFIG = 2,
+  PFSMC_GPU_ERR_NUMERICAL = 3,
+  PFSMC_GPU_ERR_IO = 4
+} pfsmc_gpu_status;
+
+/* Compiled-in OdeModel plugins (device functors; models.hpp:20-55 contract). */
+enum {
+  PFSMC_GPU_MODEL_DECAY = 0,      /* x' = -theta x (reference test model) */
+  PFSMC_GPU_MODEL_LOTKA_VOLTERRA = 1,
+  PFSMC_GPU_MODEL_ROBERTSON = 2,
+  PFSMC_GPU_MODEL_CHAIN8 = 3
+};
+/* lmm::Family (lmm.hpp:12) */
+enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
+/* Observation noise. GAUSSIAN is filter::log_likelihood (filter.cpp:124-141);
+ * LOGNORMAL is an extension for BASELINE config 3 (no reference counterpart). */
+enum { PFSMC_GPU_LIK_GAUSSIAN = 0, PFSMC_GPU_LIK_LOGNORMAL = 1 };
+
+typedef struct pfsmc_gpu_sampler pfsmc_gpu_sampler;
+
+/* The fields of filter::PfConfig + ObservationModel that pf_step reads
+ * (filter.hpp:30-65), plus the device placement. */
+typedef struct pfsmc_gpu_config {
+  int model;               /* PFSMC_GPU_MODEL_* */
+  int family;              /* PFSMC_GPU_AB / AM / BDF  (IntegratorSpec.family) */
+  int order;               /* 1..3                      (IntegratorSpec.order)  */
+  double shrink_a;         /* PfConfig.shrink_a, in (0, 1) */
+  uint64_t seed;           /* PfConfig.seed */
+  double newton_tol;       /* NewtonOpts.tol (reference default 1e-9) */
+  int newton_max_iter;     /* NewtonOpts.max_iter (reference default 20) */
+  uint64_t particles;      /* PfConfig.particles (global N) */
+  const uint64_t* obs_indices; /* ObservationModel.indices */
+  uint64_t n_obs;          /* m_y <= 8 */
+  double sigma;            /* ObservationModel.sigma */
+  int likelihood;          /* PFSMC_GPU_LIK_* */
+  int device;              /* CUDA ordinal */
+} pfsmc_gpu_config;
+
+const char* pfsmc_gpu_version(void);
+/* Thread-local message of the most recent failure (pfsmc_last_error). */
+const char* pfsmc_gpu_last_error(void);
+
+/* Validates like PfConfig::validate (filter.cpp:45-74) and allocates the
+ * device-resident ensemble (SoA-of-records, double buffered). */
+pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler** out);
+void pfsmc_gpu_destroy(pfsmc_gpu_sampler* s);
+
+/* Inject / read back a filter::Ensemble (host AoS arrays, sizes from cfg).
+ * set: the shrink mean is recomputed from (params_u, exp(logw)) on the
+ * device exactly as filter::shrink does each step (filter.cpp:107-122);
+ * cov_u is used as given for the next proliferation (filter.cpp:343). */
+pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* states,
+                                        const double* params_u, const double* logw,
+                                        const double* mean_u, const double* cov_u);
+pfsmc_gpu_status pfsmc_gpu_get_ensemble(pfsmc_gpu_sampler* s, double* states,
+                                        double* params_u, double* logw, double* mean_u,
+                                        double* cov_u);
+
+/* Device-side initialisation (replaces filter::initialize, filter.cpp:76-105).
+ * gaussian: the reference prior (theta_u ~ N(mu, sigma), x ~ N(mean, std),
+ * optional clamp at 0), stream (seed, 0, i, init), theta then x.
+ * uniform: the BASELINE box prior U[lo, hi] in natural space, same stream
+ * and order, theta_u = log U. Moments with equal weights. */
+pfsmc_gpu_status pfsmc_gpu_init_gaussian(pfsmc_gpu_sampler* s, const double* th_mu,
+                                         const double* th_sigma, const double* x_mean,
+                                         const double* x_std, const int* x_clamp);
+pfsmc_gpu_status pfsmc_gpu_init_uniform(pfsmc_gpu_sampler* s, const double* th_lo,
+                                        const double* th_hi, const double* x_lo,
+                                        const double* x_hi);
+
+/* THE DROP-IN: one assimilation step, replacing filter::pf_step
+ * (filter.cpp:292-394). y: n_obs host doubles; j: 1-based time index;
+ * [t_prev, t_obs] with fixed LMM step h (PfConfig.h). trace_out (host,
+ * optional) receives the TraceRow: theta_mean[p] (natural space),
+ * theta_var[p], state_mean[d], ess — 2p + d + 1 doubles. Blocking. */
+pfsmc_gpu_status pfsmc_gpu_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
+                                double t_prev, double t_obs, double h, double* trace_out);
+
+/* Non-blocking variant for resident observation streams: enqueues the step
+ * on the sampler's stream, observations taken from pfsmc_gpu_upload_observations
+ * row (j - 1). Errors surface at the next pfsmc_gpu_synchronize. */
+pfsmc_gpu_status pfsmc_gpu_upload_observations(pfsmc_gpu_sampler* s, const double* ys,
+                                               const double* t_obs, uint64_t T, double t0,
+                                               double h);
+pfsmc_gpu_status pfsmc_gpu_step_resident(pfsmc_gpu_sampler* s, uint64_t j);
+pfsmc_gpu_status pfsmc_gpu_synchronize(pfsmc_gpu_sampler* s, double* trace_out);
+
+/* filter::run (filter.cpp:396-443) on resident observations: rows (T+1) x
+ * (2p + d + 1) of the PosteriorTrace, row 0 from the current ensemble;
+ * degeneracy streak flags in warn_out (T+1 ints, optional). */
+pfsmc_gpu_status pfsmc_gpu_run(pfsmc_gpu_sampler* s, double* trace_rows, int* warn_out);
+
+/* Diagnostics of the last step (lock-step parity, FLOP counting):
+ * ancestors (uint32, N), predictor log-likelihoods before reshuffle (N),
+ * total Newton iterations of the step. Any pointer may be NULL. */
+pfsmc_gpu_status pfsmc_gpu_get_step_diagnostics(pfsmc_gpu_sampler* s, uint32_t* ancestors,
+                                                double* loglik_bar, uint64_t* newton_iters);
+
+/* Kernel-level parity for resample_multinomial (filter.cpp:158-178): the
+ * device CDF + ancestor search fed an injected fitness vector g (host, N
+ * doubles, N = cfg.particles); ancestors_out (host, N). Also returns the
+ * device CDF (optional). */
+pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g,
+                                           uint64_t j, uint32_t* ancestors_out,
+                                           double* cdf_out);
+
+/* The CUDA stream every launch of this handle goes to (cudaStream_t). */
+void* pfsmc_gpu_stream(pfsmc_gpu_sampler* s);
+
+/* Per-kernel device time accounting (CUDA events around each launch of the
+ * step's kernels, on the sampler's stream). While enabled, steps launch
+ * kernels directly instead of replaying the CUDA graph. names_out receives a
+ * static, comma-separated kernel list. */
+pfsmc_gpu_status pfsmc_gpu_set_kernel_timing(pfsmc_gpu_sampler* s, int enable);
+pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, int* n_kernels,
+                                        const char** names_out);
+
+/* L2 flush helper for benchmarks: writes a device buffer larger than L2 on
+ * the sampler's stream. */
+pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

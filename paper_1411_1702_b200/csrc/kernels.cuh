@@ -1,0 +1,591 @@
+// Device side shared by every translation unit of the sampler: launch
+// context, per-step parameters, device state, the templated K1 (k_predict),
+// K3 (k_update), moments / init kernels, the ancestor search, and the
+// KernelSet interface the host driver dispatches through (sampler.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <memory>
+
+#include "../../include/pfsmc_gpu.h"
+#include "exact_cdf.cuh"
+#include "lmm.cuh"
+#include "reduce.cuh"
+
+namespace pfsmc_gpu {
+
+constexpr int kMaxObs = 8;
+constexpr int kTile = 4096;              // exact-CDF tile (elements)
+constexpr int kItems = kTile / kThreads;  // 16 per thread
+constexpr int kMaxWin = 64;              // windows per tile before serial fallback
+constexpr double kNegInf = -INFINITY;
+
+enum ErrBits : int { kErrPredict = 1, kErrChol = 2, kErrUpdate = 4, kErrInternal = 8 };
+
+// Per-step scalars, copied host->device before each step (graph memcpy node).
+struct StepParams {
+  unsigned long long j;
+  double t_prev, h;
+  int m;
+  int pad;
+  double y[kMaxObs];  // observations (log y for the lognormal kind)
+  double ll_const;    // -0.5 m (log 2pi + log s2)   (filter.cpp:140, host glibc log)
+  double sly;         // sum log y (lognormal extension only)
+};
+
+// Device-resident sampler state.
+struct DevState {
+  int cur;            // which record buffer holds the ensemble
+  int error;          // ErrBits of the current step
+  int chol_failed;    // chol_psd of cov failed (raised at the next proliferation)
+  int pad;
+  double lse_w;       // logw_n = lw_n - lse_w
+  double lse_g;       // fitness log-normaliser of the current step
+  double mu[4];       // shrink mean = weighted mean of the current params
+  double cov[16];     // cov_u (p x p)
+  double L[16];       // chol_psd(cov_u), consumed by the next proliferation
+  double jitter;
+  double trace[2 * 4 + 8 + 1];
+  unsigned long long newton_iters;
+  double total_mass;  // exact CDF total (diagnostic)
+};
+
+struct TileHdr {
+  int nwin;  // -1: overflow (serial tile)
+  int tail_e;
+  long long tail_d0, tail_d1;
+};
+struct TileWin {
+  double g;
+  int e;
+  int local;  // element index inside the tile
+  long long d0, d1;
+};
+
+// Immutable launch context (pointers + constants), passed by value.
+struct Ctx {
+  int N, R, ntiles;
+  int m_y, likelihood;
+  int obs_idx[kMaxObs];
+  double a, one_minus_a, s_prolif;  // s = sqrt(1 - a^2)
+  double tol;
+  int max_iter;
+  unsigned long long seed;
+  double two_s2;
+  int coarse_bits;  // coarse guide has 2^coarse_bits buckets
+  double* rec[2];
+  double* lw;
+  double* llbar;
+  double* lg;
+  double* cdf;
+  unsigned* anc;
+  unsigned short* lguide;  // per-tile local guide (kTile entries per tile)
+  unsigned* coarse;
+  double* tile_start;  // exact CDF value before each tile (0 for tile 0)
+  double* tile_end;    // exact CDF value at each tile's last element (guarded at the end)
+  DD* tile_sum;
+  long long* tile_cnt;
+  DD* tile_pre;
+  long long* tile_cnt_pre;
+  TileHdr* hdr;
+  TileWin* win;        // kMaxWin per tile
+  double* win_after;   // exact sum after each window (kMaxWin per tile)
+  double* part;        // block partials
+  double* gpart;       // group partials
+  unsigned* cnt_pred;  // last-block counters of k_predict (ngroups + 1)
+  unsigned* cnt_upd;   // ... of k_update / k_moments (ngroups + 1)
+  unsigned* cnt_scan;  // [0] k_scan_sums, [1] k_scan_pieces
+  const double* gin;   // injected fitness (parity mode) or null
+  DevState* st;
+  const StepParams* sp;
+};
+
+// ---------------------------------------------------------------- helpers
+template <class M>
+__device__ __forceinline__ void load_record(const double* __restrict__ rec, int R, long long n,
+                                            double (&x)[M::D], double (&th)[M::P]) {
+  const double2* p = reinterpret_cast<const double2*>(rec + n * R);
+  double v[M::D + M::P + 1];
+#pragma unroll
+  for (int i = 0; i < (M::D + M::P + 1) / 2; ++i) {
+    const double2 q = __ldg(p + i);
+    v[2 * i] = q.x;
+    v[2 * i + 1] = q.y;
+  }
+#pragma unroll
+  for (int i = 0; i < M::D; ++i) x[i] = v[i];
+#pragma unroll
+  for (int i = 0; i < M::P; ++i) th[i] = v[M::D + i];
+}
+
+template <class M>
+__device__ __forceinline__ void store_record(double* __restrict__ rec, int R, long long n,
+                                             const double (&x)[M::D], const double (&th)[M::P]) {
+  double2* p = reinterpret_cast<double2*>(rec + n * R);
+  double v[M::D + M::P + 1];
+#pragma unroll
+  for (int i = 0; i < M::D; ++i) v[i] = x[i];
+#pragma unroll
+  for (int i = 0; i < M::P; ++i) v[M::D + i] = th[i];
+  v[M::D + M::P] = 0.0;
+#pragma unroll
+  for (int i = 0; i < (M::D + M::P + 1) / 2; ++i) p[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+
+// filter::log_likelihood (filter.cpp:124-141): ll_const - ss / (2 s2);
+// lognormal extension: (ll_const' - ss/(2 s2)) with r = log y - log x, -inf for x <= 0.
+template <class M>
+__device__ __forceinline__ double loglik(const Ctx& c, const StepParams& sp,
+                                         const double (&x)[M::D]) {
+  double ss = 0.0;
+  if (c.likelihood == PFSMC_GPU_LIK_LOGNORMAL) {
+    for (int k = 0; k < c.m_y; ++k) {
+      double xv = 0.0;
+#pragma unroll
+      for (int i = 0; i < M::D; ++i)
+        if (i == c.obs_idx[k]) xv = x[i];
+      if (!(xv > 0.0)) return kNegInf;
+      const double r = sp.y[k] - log(xv);
+      ss += r * r;
+    }
+  } else {
+    for (int k = 0; k < c.m_y; ++k) {
+      double xv = 0.0;
+#pragma unroll
+      for (int i = 0; i < M::D; ++i)
+        if (i == c.obs_idx[k]) xv = x[i];
+      const double r = sp.y[k] - xv;
+      ss += r * r;
+    }
+  }
+  if (c.likelihood == PFSMC_GPU_LIK_LOGNORMAL) return (sp.ll_const - ss / c.two_s2) - sp.sly;
+  return sp.ll_const - ss / c.two_s2;
+}
+
+__device__ __forceinline__ bool grid_error(const Ctx& c) {
+  return *reinterpret_cast<volatile int*>(&c.st->error) != 0;
+}
+
+// ---------------------------------------------------------------- K1
+template <class M, int FAM, int ORD>
+__global__ void __launch_bounds__(kThreads) k_predict(Ctx c) {
+  constexpr int D = M::D, P = M::P;
+  __shared__ double scratch[kWarps * 2];
+  __shared__ double fin[2];
+  if (grid_error(c)) return;
+  const StepParams& sp = *c.sp;  // read fields in place (no local copy)
+  const DevState& st = *c.st;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  double lgv = kNegInf;
+  int iters = 0;
+  if (n < c.N) {
+    double x[D], tu[P], th[P], gamma[D];
+    load_record<M>(c.rec[st.cur], c.R, n, x, tu);
+    const double logw = c.lw[n] - st.lse_w;
+    // shrink (filter.cpp:118) + natural_params (models.cpp:18-25)
+#pragma unroll
+    for (int k = 0; k < P; ++k) th[k] = exp(c.a * tu[k] + c.one_minus_a * st.mu[k]);
+    Propagator<M, FAM, ORD> prop;
+    const int status = prop.run(th, x, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    const double ll = status == kOk ? loglik<M>(c, sp, x) : kNegInf;
+    c.llbar[n] = ll;
+    lgv = logw + ll;
+    c.lg[n] = lgv;
+  }
+  if (FAM != kAB) {
+    int it = iters;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(0xffffffffu, it, o);
+    if ((threadIdx.x & 31) == 0 && it) atomicAdd(&c.st->newton_iters, static_cast<unsigned long long>(it));
+  }
+  const double one[1] = {1.0};
+  block_partial<1, false>(lgv, one, c.part + blockIdx.x * 2, scratch);
+  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch)) {
+    if (threadIdx.x == 0) {
+      // logsumexp (filter.cpp:16-23) + the degeneracy check (filter.cpp:149-152)
+      const double mx = fin[0];
+      const double lse = isfinite(mx) ? mx + log(fin[1]) : kNegInf;
+      c.st->lse_g = lse;
+      if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+    }
+  }
+}
+
+// Ancestor search: first k with cdf_k > u (std::upper_bound), clamped.
+__device__ __forceinline__ unsigned find_ancestor(const Ctx& c, double u) {
+  const double B1 = ldexp(1.0, c.coarse_bits);
+  int t = static_cast<int>(__ldg(&c.coarse[static_cast<long long>(u * B1)]));
+  while (t < c.ntiles - 1 && __ldg(&c.tile_end[t]) <= u) ++t;
+  const double c_start = __ldg(&c.tile_start[t]);
+  const double c_end = __ldg(&c.tile_end[t]);
+  const double wdt = (c_end - c_start) * (1.0 / kTile);
+  double fi = floor((u - c_start) / wdt);
+  fi = fmin(fmax(fi, 0.0), static_cast<double>(kTile - 1));
+  int i = static_cast<int>(fi);
+  while (i > 0 && c_start + static_cast<double>(i) * wdt > u) --i;
+  while (i + 1 < kTile && c_start + static_cast<double>(i + 1) * wdt <= u) ++i;
+  const long long base = static_cast<long long>(t) * kTile;
+  long long k = base + __ldg(&c.lguide[base + i]);
+  while (k < c.N - 1 && __ldg(&c.cdf[k]) <= u) ++k;
+  return static_cast<unsigned>(k);
+}
+
+// ---------------------------------------------------------------- K3
+template <class M>
+struct MomentLayout {
+  static constexpr int P = M::P, D = M::D;
+  static constexpr int NA = P, NB = P * (P + 1) / 2, NX = D;
+  static constexpr int V = 1 + NA + NB + NX + 1;  // values: S, A, B, X, Q (partial = M + V)
+};
+
+// Finalise (M, S, A, B, X, Q) into lse_w, mean, cov, trace, chol for the
+// next step; K is the shift the partials were taken about.
+template <class M>
+__device__ void finalize_moments(const Ctx& c, const double* fin, const double (&K)[M::P],
+                                 bool set_lse, bool set_cov) {
+  using ML = MomentLayout<M>;
+  constexpr int P = M::P, D = M::D;
+  DevState& st = *c.st;
+  const double Mx = fin[0];
+  const double S = fin[1];
+  const double lse = isfinite(Mx) ? Mx + log(S) : kNegInf;
+  if (set_lse) {
+    // update_weights degeneracy check (filter.cpp:215-219)
+    if (!isfinite(lse)) {
+      atomicOr(&st.error, kErrUpdate);
+      return;
+    }
+    st.lse_w = lse;
+  }
+  double mu[P], dm[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    dm[k] = fin[2 + k] / S;
+    mu[k] = K[k] + dm[k];
+    st.mu[k] = mu[k];
+  }
+  if (set_cov) {
+    int idx = 0;
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int q = r; q < P; ++q) {
+        const double v = fin[2 + ML::NA + idx] / S - dm[r] * dm[q];
+        st.cov[r * P + q] = v;
+        st.cov[q * P + r] = v;
+        ++idx;
+      }
+  }
+  // TraceRow (filter.cpp:379-391)
+#pragma unroll
+  for (int k = 0; k < P; ++k) st.trace[k] = exp(mu[k]);
+#pragma unroll
+  for (int k = 0; k < P; ++k) st.trace[P + k] = st.cov[k * P + k];
+#pragma unroll
+  for (int k = 0; k < D; ++k) st.trace[2 * P + k] = fin[2 + ML::NA + ML::NB + k] / S;
+  st.trace[2 * P + D] = S * S / fin[2 + ML::NA + ML::NB + ML::NX];
+}
+
+// chol_psd with the jitter ladder (linalg.cpp:439-500), one thread. Same
+// operation order as the reference; sqrt and division are IEEE-exact, so L
+// is bitwise the reference's for the same C.
+template <int P>
+__device__ void chol_psd_device(DevState& st) {
+  const double* C = st.cov;
+  double trace = 0.0;
+  for (int i = 0; i < P; ++i) trace += C[i * P + i];
+  const double unit = trace / static_cast<double>(P);
+  const double au = fabs(unit);
+  const double pivot_tol = 1e-14 * ((1.0 < au) ? au : 1.0);
+  const double ladder[6] = {0.0, 1e-12, 1e-10, 1e-8, 1e-6, 1e-4};
+  for (int r = 0; r < 6; ++r) {
+    const double eps = ladder[r] * unit;
+    double A[P * P], L[P * P];
+    for (int i = 0; i < P * P; ++i) {
+      A[i] = C[i];
+      L[i] = 0.0;
+    }
+    if (eps != 0.0)
+      for (int i = 0; i < P; ++i) A[i * P + i] += eps;
+    bool ok = true;
+    for (int i = 0; i < P && ok; ++i) {
+      double d = A[i * P + i];
+      for (int k = 0; k < i; ++k) d -= L[i * P + k] * L[i * P + k];
+      if (d < -pivot_tol) {
+        ok = false;
+        break;
+      }
+      if (d <= pivot_tol) {
+        for (int j = i + 1; j < P; ++j) {
+          double s = A[j * P + i];
+          for (int k = 0; k < i; ++k) s -= L[j * P + k] * L[i * P + k];
+          if (fabs(s) > pivot_tol) ok = false;
+        }
+        L[i * P + i] = 0.0;
+        continue;
+      }
+      const double root = sqrt(d);
+      L[i * P + i] = root;
+      for (int j = i + 1; j < P; ++j) {
+        double s = A[j * P + i];
+        for (int k = 0; k < i; ++k) s -= L[j * P + k] * L[i * P + k];
+        L[j * P + i] = s / root;
+      }
+    }
+    if (ok) {
+      for (int i = 0; i < P * P; ++i) st.L[i] = L[i];
+      st.jitter = eps;
+      st.chol_failed = 0;
+      return;
+    }
+  }
+  st.chol_failed = 1;
+}
+
+template <class M, int FAM, int ORD>
+__global__ void __launch_bounds__(kThreads) k_update(Ctx c) {
+  constexpr int D = M::D, P = M::P;
+  using ML = MomentLayout<M>;
+  constexpr int V = ML::V;
+  __shared__ double scratch[kWarps * V];
+  __shared__ double fin[V + 1];  // M + V values
+  __shared__ double sL[P * P], sK[P];
+  if (grid_error(c)) return;
+  DevState& st = *c.st;
+  if (st.chol_failed) {
+    // proliferate's chol_psd throws (linalg.cpp:499) after the resample phase
+    if (threadIdx.x == 0) atomicOr(&st.error, kErrChol);
+    return;
+  }
+  if (threadIdx.x < P * P) sL[threadIdx.x] = st.L[threadIdx.x];
+  if (threadIdx.x < P) sK[threadIdx.x] = st.mu[threadIdx.x];
+  __syncthreads();
+  const StepParams& sp = *c.sp;  // read fields in place (no local copy)
+  const int cur = st.cur;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  double lwv = kNegInf;
+  double vals[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) vals[k] = 0.0;
+  int iters = 0;
+  if (n < c.N) {
+    // survival of the fittest (filter.cpp:169-176)
+    const double u = resample_uniform(c.seed, sp.j, n);
+    const unsigned anc = find_ancestor(c, u);
+    c.anc[n] = anc;
+    double x[D], tu[P], tb[P], th[P], gamma[D];
+    load_record<M>(c.rec[cur], c.R, anc, x, tu);
+    const double llb = __ldg(&c.llbar[anc]);
+    // shrink of the ancestor (filter.cpp:118), proliferation (filter.cpp:185-196)
+    double z[P];
+    stream_normals<P>(c.seed, sp.j, n, kProliferate, z);
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      tb[r] = c.a * tu[r] + c.one_minus_a * sK[r];
+      double dot = 0.0;
+#pragma unroll
+      for (int q = 0; q <= r; ++q) dot += sL[r * P + q] * z[q];
+      tb[r] += c.s_prolif * dot;
+      th[r] = exp(tb[r]);
+    }
+    // repropagate + innovate + log-lik (filter.cpp:351-365)
+    double xr[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) xr[k] = x[k];
+    Propagator<M, FAM, ORD> prop;
+    const int status = prop.run(th, xr, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    double ll = kNegInf;
+    if (status == kOk) {
+      double zi[D];
+      stream_normals<D>(c.seed, sp.j, n, kInnovate, zi);
+#pragma unroll
+      for (int k = 0; k < D; ++k) xr[k] += sqrt(gamma[k]) * zi[k];
+      ll = loglik<M>(c, sp, xr);
+    } else {
+#pragma unroll
+      for (int k = 0; k < D; ++k) xr[k] = x[k];
+    }
+    lwv = ll - llb;  // update_weights (filter.cpp:214)
+    store_record<M>(c.rec[cur ^ 1], c.R, n, xr, tb);
+    c.lw[n] = lwv;
+    // moment leaf: theta about K, outer product, state, ESS
+    double dv[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) dv[k] = tb[k] - sK[k];
+    vals[0] = 1.0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) vals[1 + k] = dv[k];
+    int idx = 0;
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int q = r; q < P; ++q) vals[1 + ML::NA + idx++] = dv[r] * dv[q];
+#pragma unroll
+    for (int k = 0; k < D; ++k) vals[1 + ML::NA + ML::NB + k] = xr[k];
+    vals[V - 1] = 1.0;
+  }
+  if (FAM != kAB) {
+    int it = iters;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(0xffffffffu, it, o);
+    if ((threadIdx.x & 31) == 0 && it) atomicAdd(&st.newton_iters, static_cast<unsigned long long>(it));
+  }
+  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
+  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+    if (threadIdx.x == 0) {
+      double K[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) K[k] = sK[k];
+      finalize_moments<M>(c, fin, K, true, true);
+      if (!(st.error & kErrUpdate)) {
+        chol_psd_device<P>(st);
+        st.cur = cur ^ 1;
+      }
+    }
+  }
+}
+
+// Moments of the resident ensemble (after injection / initialisation):
+// refreshes the shrink mean (and, for init, cov + chol); lse_w untouched.
+template <class M>
+__global__ void __launch_bounds__(kThreads) k_moments(Ctx c, int set_cov) {
+  constexpr int D = M::D, P = M::P;
+  using ML = MomentLayout<M>;
+  constexpr int V = ML::V;
+  __shared__ double scratch[kWarps * V];
+  __shared__ double fin[V + 1];  // M + V values
+  DevState& st = *c.st;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  double lwv = kNegInf;
+  double vals[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) vals[k] = 0.0;
+  double K[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) K[k] = st.mu[k];  // shift: caller-provided guess
+  if (n < c.N) {
+    double x[D], tu[P];
+    load_record<M>(c.rec[st.cur], c.R, n, x, tu);
+    lwv = c.lw[n] - st.lse_w;
+    vals[0] = 1.0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) vals[1 + k] = tu[k] - K[k];
+    int idx = 0;
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int q = r; q < P; ++q) vals[1 + ML::NA + idx++] = (tu[r] - K[r]) * (tu[q] - K[q]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) vals[1 + ML::NA + ML::NB + k] = x[k];
+    vals[V - 1] = 1.0;
+  }
+  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
+  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+    if (threadIdx.x == 0) {
+      finalize_moments<M>(c, fin, K, false, set_cov != 0);
+      chol_psd_device<P>(st);
+    }
+  }
+}
+
+template <int P>
+__global__ void k_chol(DevState* st) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) chol_psd_device<P>(*st);
+}
+
+// Initialisation: stream (seed, 0, i, init), theta then x (filter.cpp:87-100).
+template <class M>
+__global__ void __launch_bounds__(kThreads) k_init(Ctx c, int kind, const double* prm, double lw0) {
+  constexpr int D = M::D, P = M::P;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  // prm: gaussian: th_mu[P], th_sigma[P], x_mean[D], x_std[D], x_clamp[D]
+  //      uniform : th_lo[P], th_hi[P], x_lo[D], x_hi[D]
+  Stream s(c.seed, 0, n, kInit);
+  double x[D], tu[P];
+  if (kind == 0) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) tu[k] = prm[k] + prm[P + k] * s.next_normal();
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double v = prm[2 * P + k] + prm[2 * P + D + k] * s.next_normal();
+      if (prm[2 * P + 2 * D + k] != 0.0 && v < 0.0) v = 0.0;
+      x[k] = v;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < P; ++k) tu[k] = log(prm[k] + (prm[P + k] - prm[k]) * s.next_uniform());
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = prm[2 * P + k] + (prm[2 * P + D + k] - prm[2 * P + k]) * s.next_uniform();
+  }
+  store_record<M>(c.rec[c.st->cur], c.R, n, x, tu);
+  c.lw[n] = lw0;
+}
+
+// ---------------------------------------------------------------- host side
+struct KernelSet {
+  virtual ~KernelSet() = default;
+  virtual void predict(const Ctx& c, int grid, cudaStream_t s) = 0;
+  virtual void update(const Ctx& c, int grid, cudaStream_t s) = 0;
+  virtual void moments(const Ctx& c, int grid, cudaStream_t s, int set_cov) = 0;
+  virtual void chol(const Ctx& c, cudaStream_t s) = 0;
+  virtual void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) = 0;
+  int d = 0, p = 0;
+};
+
+template <class M, int FAM, int ORD>
+struct KernelSetT final : KernelSet {
+  KernelSetT() {
+    d = M::D;
+    p = M::P;
+  }
+  void predict(const Ctx& c, int grid, cudaStream_t s) override {
+    k_predict<M, FAM, ORD><<<grid, kThreads, 0, s>>>(c);
+  }
+  void update(const Ctx& c, int grid, cudaStream_t s) override {
+    k_update<M, FAM, ORD><<<grid, kThreads, 0, s>>>(c);
+  }
+  void moments(const Ctx& c, int grid, cudaStream_t s, int set_cov) override {
+    k_moments<M><<<grid, kThreads, 0, s>>>(c, set_cov);
+  }
+  void chol(const Ctx& c, cudaStream_t s) override { k_chol<M::P><<<1, 32, 0, s>>>(c.st); }
+  void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) override {
+    k_init<M><<<grid, kThreads, 0, s>>>(c, kind, prm, lw0);
+  }
+};
+
+template <class M, int FAM>
+std::unique_ptr<KernelSet> make_order(int order) {
+  switch (order) {
+    case 1: return std::make_unique<KernelSetT<M, FAM, 1>>();
+    case 2: return std::make_unique<KernelSetT<M, FAM, 2>>();
+    case 3: return std::make_unique<KernelSetT<M, FAM, 3>>();
+  }
+  return nullptr;
+}
+template <class M>
+std::unique_ptr<KernelSet> make_family(int fam, int order) {
+  switch (fam) {
+    case kAB: return make_order<M, kAB>(order);
+    case kAM: return make_order<M, kAM>(order);
+    case kBDF: return make_order<M, kBDF>(order);
+  }
+  return nullptr;
+}
+// One translation unit per model instantiates its 9 (family, order) kernel
+// sets (kernels_<model>.cu), so the builds run in parallel.
+std::unique_ptr<KernelSet> make_kernels_decay(int fam, int order);
+std::unique_ptr<KernelSet> make_kernels_lv(int fam, int order);
+std::unique_ptr<KernelSet> make_kernels_robertson(int fam, int order);
+std::unique_ptr<KernelSet> make_kernels_chain(int fam, int order);
+
+inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
+  switch (model) {
+    case DecayModel::ID: return make_kernels_decay(fam, order);
+    case LotkaVolterraModel::ID: return make_kernels_lv(fam, order);
+    case RobertsonModel::ID: return make_kernels_robertson(fam, order);
+    case ChainModel::ID: return make_kernels_chain(fam, order);
+  }
+  return nullptr;
+}
+
+}  // namespace pfsmc_gpu

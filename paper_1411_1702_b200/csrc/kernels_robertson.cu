@@ -1,0 +1,9 @@
+// Kernel instantiations for RobertsonModel: every (family, order) of the reference's
+// fixed-step integrator set (lmm.cpp:64-77: AB/AM/BDF x orders 1-3).
+#include "kernels.cuh"
+
+namespace pfsmc_gpu {
+std::unique_ptr<KernelSet> make_kernels_robertson(int fam, int order) {
+  return make_family<RobertsonModel>(fam, order);
+}
+}  // namespace pfsmc_gpu

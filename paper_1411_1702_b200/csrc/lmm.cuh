@@ -1,0 +1,335 @@
+// Psi: fixed-step LMM interval propagation for ONE particle, entirely in
+// registers (state history, f history, Newton iterate and the d x d LU).
+//
+// Restates /root/reference/proj/src/lmm.cpp:
+//   coefficient tables          lmm.cpp:18-60   (same decimal-rational literals)
+//   explicit / implicit terms   lmm.cpp:108-144 (alpha terms first, then h*beta_i f)
+//   extrapolation predictor     lmm.cpp:146-165
+//   DenseLu factor / solve      linalg.cpp:201-258 (first strict max pivot,
+//                                inv = 1/pivot, zero-multiplier skip)
+//   newton_solve                lmm.cpp:219-266 (J rebuilt each iteration;
+//                                ||dx|| <= tol (1 + ||x||) after the update)
+//   LTE factors / finish_step   lmm.cpp:307-342, 438-452
+//   ramped interval loop        lmm.cpp:468-503 (order p = min(k, order),
+//                                fresh history every interval)
+// The order ramp makes steps k = 1, 2, 3 special (avail = min(k, 4) history
+// entries); each is a separate compile-time instantiation, so every history
+// index is static and nothing touches local memory.
+#pragma once
+#include "models.cuh"
+
+namespace pfsmc_gpu {
+
+enum Family : int { kAB = 0, kAM = 1, kBDF = 2 };
+enum ParticleStatus : int { kOk = 0, kInvalidRhs = 1, kNewtonDivergence = 2, kSingular = 3 };
+
+// ---- coefficient tables (lmm.cpp:18-60) ----------------------------------
+__host__ __device__ constexpr double ab_beta(int order, int i) {
+  return order == 1   ? (i == 1 ? 1.0 : 0.0)
+         : order == 2 ? (i == 1 ? 3.0 / 2.0 : i == 2 ? -1.0 / 2.0 : 0.0)
+         : order == 3 ? (i == 1 ? 23.0 / 12.0 : i == 2 ? -16.0 / 12.0 : i == 3 ? 5.0 / 12.0 : 0.0)
+                      : (i == 1 ? 55.0 / 24.0 : i == 2 ? -59.0 / 24.0 : i == 3 ? 37.0 / 24.0
+                                                : i == 4 ? -9.0 / 24.0 : 0.0);
+}
+__host__ __device__ constexpr double ab_C(int order) {
+  return order == 1 ? 1.0 / 2.0 : order == 2 ? 5.0 / 12.0 : order == 3 ? 3.0 / 8.0 : 251.0 / 720.0;
+}
+__host__ __device__ constexpr double am_beta(int order, int i) {
+  return order == 1   ? (i == 0 ? 1.0 : 0.0)
+         : order == 2 ? (i == 0 ? 1.0 / 2.0 : i == 1 ? 1.0 / 2.0 : 0.0)
+                      : (i == 0 ? 5.0 / 12.0 : i == 1 ? 8.0 / 12.0 : i == 2 ? -1.0 / 12.0 : 0.0);
+}
+__host__ __device__ constexpr double am_C(int order) {
+  return order == 1 ? -1.0 / 2.0 : order == 2 ? -1.0 / 12.0 : -1.0 / 24.0;
+}
+__host__ __device__ constexpr double bdf_alpha(int order, int i) {
+  return order == 1   ? (i == 0 ? 1.0 : 0.0)
+         : order == 2 ? (i == 0 ? 4.0 / 3.0 : i == 1 ? -1.0 / 3.0 : 0.0)
+                      : (i == 0 ? 18.0 / 11.0 : i == 1 ? -9.0 / 11.0 : i == 2 ? 2.0 / 11.0 : 0.0);
+}
+__host__ __device__ constexpr double bdf_beta0(int order) {
+  return order == 1 ? 1.0 : order == 2 ? 2.0 / 3.0 : 6.0 / 11.0;
+}
+__host__ __device__ constexpr double bdf_C(int order) {
+  return order == 1 ? -1.0 / 2.0 : order == 2 ? -2.0 / 9.0 : -3.0 / 22.0;
+}
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+// std::max as the reference uses it: (a < b) ? b : a (NaN never wins).
+__device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
+
+// ---- LU with partial pivoting, in registers (linalg.cpp:201-258) --------
+template <int D>
+__device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[D]) {
+  int piv[D];
+#pragma unroll
+  for (int col = 0; col < D; ++col) {
+    int pivot = col;
+    double best = fabs(A[col][col]);
+#pragma unroll
+    for (int r = col + 1; r < D; ++r) {
+      const double v = fabs(A[r][col]);
+      if (v > best) {
+        best = v;
+        pivot = r;
+      }
+    }
+    if (best == 0.0) return false;
+    piv[col] = pivot;
+#pragma unroll
+    for (int r = col + 1; r < D; ++r) {
+      if (pivot == r) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double t = A[col][j];
+          A[col][j] = A[r][j];
+          A[r][j] = t;
+        }
+      }
+    }
+    const double inv = 1.0 / A[col][col];
+#pragma unroll
+    for (int r = col + 1; r < D; ++r) {
+      const double f = A[r][col] * inv;
+      A[r][col] = f;
+      if (f != 0.0) {
+#pragma unroll
+        for (int j = col + 1; j < D; ++j) A[r][j] -= f * A[col][j];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+#pragma unroll
+    for (int r = i + 1; r < D; ++r) {
+      if (piv[i] == r) {
+        const double t = b[i];
+        b[i] = b[r];
+        b[r] = t;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < i; ++j) b[i] -= A[i][j] * b[j];
+  }
+#pragma unroll
+  for (int ii = D - 1; ii >= 0; --ii) {
+#pragma unroll
+    for (int j = ii + 1; j < D; ++j) b[ii] -= A[ii][j] * b[j];
+    b[ii] /= A[ii][ii];
+  }
+  return true;
+}
+
+// ---- Newton on G(x) = x - h b0 f(x) - c (lmm.cpp:219-266) ---------------
+template <class M>
+__device__ __forceinline__ int newton_solve(const double (&th)[M::P], double hb0,
+                                            const double (&c)[M::D], double (&x)[M::D],
+                                            double tol, int max_iter, int& iters) {
+  constexpr int D = M::D;
+  for (int iter = 1; iter <= max_iter; ++iter) {
+    double f[D], r[D], A[D][D];
+    if (!M::rhs(th, x, f)) {
+      iters += iter;
+      return kInvalidRhs;
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) r[j] = x[j] - hb0 * f[j] - c[j];
+    if (!M::jac(th, x, A)) {
+      iters += iter;
+      return kInvalidRhs;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) A[i][j] = -hb0 * A[i][j];
+#pragma unroll
+    for (int i = 0; i < D; ++i) A[i][i] += 1.0;
+    if (!lu_solve_inplace<D>(A, r)) {
+      iters += iter;
+      return kSingular;
+    }
+    double dn = 0.0, xn = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      x[j] -= r[j];
+      dn = ref_max(dn, fabs(r[j]));
+      xn = ref_max(xn, fabs(x[j]));
+    }
+    if (!isfinite(xn) || !isfinite(dn)) {
+      iters += iter;
+      return kInvalidRhs;
+    }
+    if (dn <= tol * (1.0 + xn)) {
+      iters += iter;
+      return kOk;
+    }
+  }
+  iters += max_iter;
+  return kNewtonDivergence;
+}
+
+// ---- the ramped interval propagator ------------------------------------
+template <class M, int FAM, int ORD>
+struct Propagator {
+  static constexpr int D = M::D;
+  static constexpr int P = M::P;
+  static constexpr int SD = FAM == kBDF ? ORD + 1 : 1;  // states kept
+  static constexpr int FD = FAM == kAB ? ORD + 1 : ORD;  // f values kept
+
+  double xs[SD][D];
+  double fs[FD][D];
+
+  // AB(q) explicit combination: 0 + 1.0*x_n, then (h*beta_i) f_{n+1-i}.
+  template <int Q>
+  __device__ __forceinline__ void ab_step(double h, double (&out)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * xs[0][j];
+#pragma unroll
+    for (int i = 1; i <= Q; ++i) {
+      const double hb = h * ab_beta(Q, i);
+#pragma unroll
+      for (int j = 0; j < D; ++j) out[j] += hb * fs[i - 1][j];
+    }
+  }
+
+  // implicit_history_terms for AM(p) / BDF(p) (lmm.cpp:130-144).
+  template <int PA>
+  __device__ __forceinline__ void implicit_terms(double h, double (&c)[D]) const {
+    if constexpr (FAM == kAM) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * xs[0][j];
+#pragma unroll
+      for (int i = 1; i < PA; ++i) {
+        const double hb = h * am_beta(PA, i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) c[j] += hb * fs[i - 1][j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) c[j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < PA; ++i) {
+        const double a = bdf_alpha(PA, i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) c[j] += a * xs[i][j];
+      }
+    }
+  }
+
+  // extrapolate_predictor(q) (lmm.cpp:146-165); the binomials are exact.
+  template <int Q>
+  __device__ __forceinline__ void extrapolate(double (&out)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = 0.0;
+    double binom = static_cast<double>(Q) + 1.0;
+    double sign = 1.0;
+#pragma unroll
+    for (int i = 0; i <= Q; ++i) {
+      const double coef = sign * binom;
+#pragma unroll
+      for (int j = 0; j < D; ++j) out[j] += coef * xs[i][j];
+      sign = -sign;
+      binom = binom * static_cast<double>(Q + 1 - (i + 1)) / static_cast<double>(i + 2);
+    }
+  }
+
+  __device__ __forceinline__ void push(const double (&x)[D], const double (&f)[D]) {
+#pragma unroll
+    for (int i = SD - 1; i > 0; --i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) xs[i][j] = xs[i - 1][j];
+#pragma unroll
+    for (int i = FD - 1; i > 0; --i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) fs[i][j] = fs[i - 1][j];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      xs[0][j] = x[j];
+      fs[0][j] = f[j];
+    }
+  }
+
+  // One ramp step at compile-time active order PA with AV history entries.
+  // Returns the particle status (kOk keeps going).
+  template <int PA, int AV>
+  __device__ __forceinline__ int step(const double (&th)[P], double h, double tol, int max_iter,
+                                      double (&gamma)[D], int& iters) {
+    double xnew[D], ref[D];
+    double factor;
+    if constexpr (FAM == kAB) {
+      ab_step<PA>(h, xnew);
+      if constexpr (AV >= PA + 1) {
+        ab_step<PA + 1>(h, ref);
+      } else if constexpr (PA >= 2) {
+        ab_step<PA - 1>(h, ref);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) ref[j] = xs[0][j];
+      }
+      factor = 1.0;
+    } else {
+      double c[D];
+      implicit_terms<PA>(h, c);
+      ab_step<PA>(h, xnew);  // Newton's initial guess: explicit AB(q), q = PA
+      if constexpr (FAM == kAM) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) ref[j] = xnew[j];
+        factor = fabs(am_C(PA)) / fabs(ab_C(PA) - am_C(PA));
+      } else if constexpr (AV >= PA + 1) {
+        extrapolate<PA>(ref);
+        factor = fabs(bdf_C(PA)) / fabs(1.0 - bdf_C(PA));
+      } else if constexpr (AV < 2) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) ref[j] = xnew[j];
+        factor = fabs(bdf_C(PA)) / fabs(ab_C(PA) - bdf_C(PA));
+      } else {
+        extrapolate<AV - 1>(ref);
+        factor = fabs(bdf_C(PA)) / fabs(1.0 - bdf_C(PA));
+      }
+      const double b0 = FAM == kAM ? am_beta(PA, 0) : bdf_beta0(PA);
+      const int st = newton_solve<M>(th, h * b0, c, xnew, tol, max_iter, iters);
+      if (st != kOk) return st;
+    }
+    // finish_step (lmm.cpp:438-452)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double est = factor * fabs(xnew[j] - ref[j]);
+      gamma[j] += est * est;
+    }
+    double fnew[D];
+    if (!M::rhs(th, xnew, fnew)) return kInvalidRhs;
+    push(xnew, fnew);
+    return kOk;
+  }
+
+  // propagate_interval (lmm.cpp:468-503): m fixed steps of size h from x.
+  // On return x holds the last accepted state (the reference's run.x).
+  __device__ __forceinline__ int run(const double (&th)[P], double (&x)[D], double h, int m,
+                                     double tol, int max_iter, double (&gamma)[D], int& iters) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) gamma[j] = 0.0;
+    double f0[D];
+    if (!M::rhs(th, x, f0)) return kInvalidRhs;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      xs[0][j] = x[j];
+      fs[0][j] = f0[j];
+    }
+    int st = kOk;
+    for (int k = 1; k <= m && st == kOk; ++k) {
+      if (k == 1)
+        st = step<1, 1>(th, h, tol, max_iter, gamma, iters);
+      else if (k == 2)
+        st = step<cmin(2, ORD), 2>(th, h, tol, max_iter, gamma, iters);
+      else if (k == 3)
+        st = step<cmin(3, ORD), 3>(th, h, tol, max_iter, gamma, iters);
+      else
+        st = step<ORD, 4>(th, h, tol, max_iter, gamma, iters);
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = xs[0][j];
+    return st;
+  }
+};
+
+}  // namespace pfsmc_gpu

@@ -1,0 +1,168 @@
+// Deterministic reductions for the log-sum-exp and weighted-moment epilogues.
+//
+// A "weighted partial" is (M, v[V]): M the max of the leaf log-weights
+// (NaN excluded, as the reference's std::max pass, filter.cpp:18), v the sums
+// of leaf quantities weighted by e = exp(x - M); the last value may be
+// weighted by e^2 (the ESS sum). NaN leaves poison the sums exactly as a NaN
+// poisons the reference's exp-sum (filter.cpp:21). Every tree below has a
+// fixed shape, so results are bitwise reproducible run to run; no FP atomics.
+//
+// Cross-block combination uses the "last block done" pattern in two levels
+// (groups of kGroup blocks, then the groups), so no launch is spent on it.
+#pragma once
+#include <cstdint>
+
+namespace pfsmc_gpu {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kGroup = 64;
+
+__device__ __forceinline__ double nan_free_max(double a, double b) {
+  // operands already NaN-free; (a < b) ? b : a like std::max
+  return (a < b) ? b : a;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nan_free_max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide max (all threads get the result). scratch >= kWarps doubles.
+__device__ __forceinline__ double block_max(double v, double* scratch) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  double r = scratch[0];
+#pragma unroll
+  for (int i = 1; i < kWarps; ++i) r = nan_free_max(r, scratch[i]);
+  return r;
+}
+
+// Block-wide sums of V values; result valid in thread 0. scratch >= kWarps*V.
+template <int V>
+__device__ __forceinline__ void block_sums(double (&v)[V], double* scratch) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < V; ++k) scratch[w * V + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double s = scratch[k];
+      for (int i = 1; i < kWarps; ++i) s += scratch[i * V + k];
+      v[k] = s;
+    }
+  }
+}
+
+// Leaf -> block partial. x: leaf log-weight; vals: leaf quantities (weighted
+// by e = exp(x - M) inside, the last one by e^2 when SQ). Thread 0 writes
+// (M, sums[V]) to out[0..V].
+template <int V, bool SQ>
+__device__ __forceinline__ void block_partial(double x, const double (&vals)[V], double* out,
+                                              double* scratch) {
+  const bool is_nan = isnan(x);
+  const double leaf_max = is_nan ? -INFINITY : x;
+  const double M = block_max(leaf_max, scratch);
+  double e;
+  if (is_nan)
+    e = NAN;
+  else if (x == -INFINITY)
+    e = 0.0;
+  else
+    e = exp(x - M);  // M finite here unless every leaf is -inf (then x==-inf)
+  double v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = ((SQ && k == V - 1) ? e * e : e) * vals[k];
+  block_sums<V>(v, scratch);
+  if (threadIdx.x == 0) {
+    out[0] = M;
+#pragma unroll
+    for (int k = 0; k < V; ++k) out[1 + k] = v[k];
+  }
+}
+
+// Combine `count` partials (stride V+1) into one, by one block, fixed order:
+// thread t folds partials t, t+256, ... sequentially (rescaled), then a fixed
+// warp/block tree. Result in out[0..V] (thread 0 writes).
+template <int V, bool SQ>
+__device__ __forceinline__ void combine_partials(const double* in, int count, double* out,
+                                                 double* scratch) {
+  double m = -INFINITY;
+  for (int i = threadIdx.x; i < count; i += kThreads) m = nan_free_max(m, __ldcg(in + i * (V + 1)));
+  const double M = block_max(m, scratch);
+  double v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = 0.0;
+  for (int i = threadIdx.x; i < count; i += kThreads) {
+    const double mi = __ldcg(in + i * (V + 1));
+    const double c = (mi == -INFINITY) ? 0.0 : exp(mi - M);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const double w = (SQ && k == V - 1) ? c * c : c;
+      v[k] += w * __ldcg(in + i * (V + 1) + 1 + k);
+    }
+  }
+  block_sums<V>(v, scratch);
+  if (threadIdx.x == 0) {
+    out[0] = M;
+#pragma unroll
+    for (int k = 0; k < V; ++k) out[1 + k] = v[k];
+  }
+}
+
+// Two-level last-block-done tree. Every block calls this after writing its
+// partial at part[blockIdx.x*(V+1)]; returns true in exactly one block (the
+// last), where `final_out` holds the grand partial (thread 0 wrote it, and a
+// __syncthreads() has been issued). counters: [0..ngroups) group counters,
+// [ngroups] the final counter; all reset to 0 by their last user.
+template <int V, bool SQ>
+__device__ __forceinline__ bool tree_reduce_last(double* part, double* group_part,
+                                                 unsigned* counters, double* final_out,
+                                                 double* scratch) {
+  __shared__ int s_flag;
+  const int nblocks = gridDim.x;
+  const int ngroups = (nblocks + kGroup - 1) / kGroup;
+  const int g = blockIdx.x / kGroup;
+  const int gsize = min(kGroup, nblocks - g * kGroup);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd(&counters[g], 1u);
+    s_flag = (old == static_cast<unsigned>(gsize - 1));
+    if (s_flag) counters[g] = 0;
+  }
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  combine_partials<V, SQ>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
+                          group_part + g * (V + 1), scratch);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd(&counters[ngroups], 1u);
+    s_flag = (old == static_cast<unsigned>(ngroups - 1));
+    if (s_flag) counters[ngroups] = 0;
+  }
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  combine_partials<V, SQ>(group_part, ngroups, final_out, scratch);
+  __syncthreads();
+  return true;
+}
+
+}  // namespace pfsmc_gpu

@@ -1,0 +1,196 @@
+"""The BASELINE.json workloads: model, priors, integrator choice and seeded
+synthetic observations (no dataset exists for them).
+
+Conventions (documented in DESIGN.md):
+* observation noise for row r uses the keyed stream (seed, r + 1, 0, init),
+  components drawn in order — the reference generator's convention
+  (bench.cpp:370-376);
+* Lotka-Volterra truth is RK4 at h = 1e-3 (BASELINE config 1); the chain and
+  Robertson truths use scipy's Radau at rtol 1e-10 (the reference generator
+  is its own adaptive BDF at rtol 1e-8, bench.cpp:298-317);
+* the reference ramps the LMM order up from 1 in every observation interval
+  (lmm.cpp:478-481), so a configured order only engages with >= order
+  sub-steps per interval (m = (t_obs - t_prev) / h).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .sampler import ObservationModel, PfConfig
+
+# ---------------------------------------------------------------- host Philox
+_M0, _M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+_W0, _W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+_KC = 0x7066736D632D3031
+_MASK = (1 << 64) - 1
+
+
+def philox4x64(ctr, key):
+    """Philox4x64-10 (rng.cpp:28-41), Python integers."""
+    c0, c1, c2, c3 = ctr
+    k0, k1 = key
+    for r in range(10):
+        if r:
+            k0 = (k0 + _W0) & _MASK
+            k1 = (k1 + _W1) & _MASK
+        p0 = _M0 * c0
+        p1 = _M1 * c2
+        c0, c1, c2, c3 = ((p1 >> 64) ^ c1 ^ k0) & _MASK, p1 & _MASK, ((p0 >> 64) ^ c3 ^ k1) & _MASK, p0 & _MASK
+    return c0, c1, c2, c3
+
+
+class HostStream:
+    """RngStream (rng.cpp:43-75) on the host; used for observation noise."""
+
+    def __init__(self, seed, j, n, purpose):
+        self.key = (seed & _MASK, _KC)
+        self.ctr = [0, j, n, purpose]
+        self.block_index = 0
+        self.lane = 4
+        self.block = None
+        self.spare = None
+
+    def next_u64(self):
+        if self.lane == 4:
+            self.ctr[0] = self.block_index
+            self.block_index += 1
+            self.block = philox4x64(self.ctr, self.key)
+            self.lane = 0
+        w = self.block[self.lane]
+        self.lane += 1
+        return w
+
+    def next_uniform(self):
+        return float(self.next_u64() >> 11) * 2.0 ** -53
+
+    def next_normal(self):
+        if self.spare is not None:
+            s, self.spare = self.spare, None
+            return s
+        u1 = (float(self.next_u64() >> 11) + 1.0) * 2.0 ** -53
+        u2 = self.next_uniform()
+        r = math.sqrt(-2.0 * math.log(u1))
+        ang = 2.0 * 3.14159265358979323846 * u2
+        self.spare = r * math.sin(ang)
+        return r * math.cos(ang)
+
+
+# ---------------------------------------------------------------- truths
+def _lv_rhs(x, th):
+    return np.array([th[0] * x[0] - x[0] * x[1], x[0] * x[1] - th[1] * x[1]])
+
+
+def rk4_path(rhs, x0, th, times, h):
+    x = np.array(x0, dtype=float)
+    t = 0.0
+    out = []
+    for to in times:
+        n = int(round((to - t) / h))
+        for _ in range(n):
+            k1 = rhs(x, th)
+            k2 = rhs(x + 0.5 * h * k1, th)
+            k3 = rhs(x + 0.5 * h * k2, th)
+            k4 = rhs(x + h * k3, th)
+            x = x + (h / 6.0) * (k1 + 2 * k2 + 2 * k3 + k4)
+        t = to
+        out.append(x.copy())
+    return np.array(out)
+
+
+def _robertson_rhs(t, x, k):
+    return [-k[0] * x[0] + k[2] * x[1] * x[2], k[0] * x[0] - k[1] * x[1] ** 2 - k[2] * x[1] * x[2],
+            k[1] * x[1] ** 2]
+
+
+def _chain_rhs(t, x, th):
+    f = th[0] * x[:7] / (1.0 + x[:7])
+    o = np.empty(8)
+    o[0] = 1.0 - f[0]
+    o[1:7] = f[:6] - th[1] * x[1:7] - th[2] * x[1:7] ** 2
+    o[7] = th[1] * x[6] - th[3] * x[7]
+    return o
+
+
+def radau_path(rhs, x0, th, times):
+    from scipy.integrate import solve_ivp
+    sol = solve_ivp(rhs, (0.0, float(times[-1])), x0, method="Radau", t_eval=times, args=(th,),
+                    rtol=1e-10, atol=1e-14)
+    return sol.y.T
+
+
+# ---------------------------------------------------------------- problems
+@dataclass
+class Problem:
+    name: str
+    model: str
+    cfg: PfConfig
+    obs: ObservationModel
+    truth: np.ndarray
+    x0_truth: np.ndarray
+    prior_kind: str          # "uniform" (natural box) or "gaussian" (unconstrained)
+    prior: dict
+    t0: float = 0.0
+    substeps: int = 1        # m: LMM steps per observation interval
+    times: np.ndarray = field(default=None)
+    ys: np.ndarray = field(default=None)
+
+    def h_for(self, t_prev, t_obs):
+        return (t_obs - t_prev) / self.substeps
+
+    def init(self, sampler):
+        if self.prior_kind == "uniform":
+            sampler.initialize_uniform(**self.prior)
+        else:
+            sampler.initialize_gaussian(**self.prior)
+
+
+def lotka_volterra(particles=1024, T=200, seed=1, family="am", order=2) -> Problem:
+    """BASELINE configs 1-2."""
+    th = np.array([1.0, 0.8])
+    x0 = np.array([1.2, 0.9])
+    times = 0.1 * np.arange(1, T + 1)
+    path = rk4_path(_lv_rhs, x0, th, times, 1e-3)
+    ys = np.empty_like(path)
+    for r in range(T):
+        s = HostStream(seed, r + 1, 0, 0)
+        ys[r] = [path[r, k] + 0.05 * s.next_normal() for k in range(2)]
+    cfg = PfConfig(particles=particles, shrink_a=0.98, h=0.1, family=family, order=order, seed=seed)
+    obs = ObservationModel([0, 1], 0.05)
+    prior = dict(th_lo=[0.5, 0.5], th_hi=[1.5, 1.5], x_lo=[0.5, 0.5], x_hi=[1.5, 1.5])
+    return Problem("lotka_volterra", "lv", cfg, obs, th, x0, "uniform", prior, 0.0, 1, times, ys)
+
+
+def robertson(particles=1 << 22, T=400, seed=1, substeps=2, max_iter=4) -> Problem:
+    """BASELINE config 3 (lognormal noise is an extension of the reference)."""
+    k = np.array([0.04, 3e7, 1e4])
+    x0 = np.array([1.0, 0.0, 0.0])
+    times = np.logspace(-4, 3, T)
+    path = radau_path(_robertson_rhs, x0, k, times)
+    ys = np.empty((T, 2))
+    for r in range(T):
+        s = HostStream(seed, r + 1, 0, 0)
+        ys[r] = [path[r, i] * math.exp(0.02 * s.next_normal()) for i in (0, 2)]
+    cfg = PfConfig(particles=particles, shrink_a=0.99, h=times[0] / substeps, family="bdf", order=2,
+                   seed=seed, newton_max_iter=max_iter)
+    obs = ObservationModel([0, 2], 0.02, "lognormal")
+    prior = dict(th_mu=list(np.log(k) + 0.5), th_sigma=[1.0] * 3, x_mean=list(x0), x_std=[0.0] * 3)
+    return Problem("robertson", "robertson", cfg, obs, k, x0, "gaussian", prior, 0.0, substeps, times, ys)
+
+
+def chain8(particles=1 << 24, T=500, seed=1, substeps=3) -> Problem:
+    """BASELINE config 4 (x(0) = 0: not specified by BASELINE.json)."""
+    th = np.array([2.0, 50.0, 5.0, 0.5])
+    x0 = np.zeros(8)
+    times = 0.1 * np.arange(1, T + 1)
+    path = radau_path(_chain_rhs, x0, th, times)
+    ys = np.empty((T, 3))
+    for r in range(T):
+        s = HostStream(seed, r + 1, 0, 0)
+        ys[r] = [path[r, i] + 0.01 * s.next_normal() for i in (0, 3, 7)]
+    cfg = PfConfig(particles=particles, shrink_a=0.98, h=0.1 / substeps, family="bdf", order=3, seed=seed)
+    obs = ObservationModel([0, 3, 7], 0.01)
+    prior = dict(th_lo=list(0.5 * th), th_hi=list(2.0 * th), x_lo=[0.0] * 8, x_hi=[0.0] * 8)
+    return Problem("chain8", "chain", cfg, obs, th, x0, "uniform", prior, 0.0, substeps, times, ys)

@@ -1,0 +1,332 @@
+"""GPU parity: the sm_100a kernels through the C ABI against the CPU oracle
+(oracle/pfsmc_oracle.c, itself pinned bitwise to the reference in
+test_oracle.py) and the reference-generated golden fixtures.
+
+Bars (BASELINE.json north_star):
+* ancestors: bit-exact (integer index work);
+* states / params / weights: 1e-10 relative;
+* posterior mean / covariance trace: 1e-8 relative.
+The only device/host differences are CUDA's exp/log/sin/cos vs glibc
+(<= 2 ulp), so every floating comparison below carries its tolerance.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle_ctypes import Ensemble as OEns
+from oracle_ctypes import Oracle, StepConfig
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+O = Oracle()
+REL_STATE = 1e-10
+REL_TRACE = 1e-8
+
+
+def _sampler(sc: StepConfig, n, likelihood="gaussian"):
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    cfg = PfConfig(particles=n, shrink_a=sc.a, h=sc.h, family=sc.family, order=sc.order, seed=sc.seed,
+                   newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter)
+    return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood))
+
+
+def _to_gpu_ens(e):
+    from paper_1411_1702_b200.sampler import Ensemble
+    return Ensemble(e.states, e.params_u, e.logw, e.mean_u, e.cov_u)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    fin = np.isfinite(a) & np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    assert np.array_equal(a[~fin], b[~fin])
+    if not fin.any():
+        return 0.0
+    return float(np.max(np.abs(a[fin] - b[fin]) / np.maximum(np.abs(b[fin]), 1e-300)))
+
+
+def _rel_scaled(a, b):
+    """Normwise relative error per column, max_i |a - b| / max_i |b| — the
+    meaningful "relative" for quantities that cross zero (log-space params,
+    log-weights, covariances)."""
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    if a.ndim == 1:
+        a, b = a[:, None], b[:, None]
+    a, b = a.reshape(a.shape[0], -1), b.reshape(b.shape[0], -1)
+    return float(np.max(np.max(np.abs(a - b), axis=0) / np.maximum(np.max(np.abs(b), axis=0), 1e-300)))
+
+
+# ---------------------------------------------------------------- resampling
+def _g_cases(rng):
+    out = {}
+    for n in (1, 3, 4095, 4096, 4097, 65536, 1 << 20):
+        g = np.exp(rng.standard_normal(n))
+        out[f"lognormal1_{n}"] = g / g.sum()
+    for s in (0.1, 4.0):
+        g = np.exp(s * rng.standard_normal(1 << 16))
+        out[f"lognormal{s}_65536"] = g / g.sum()
+    out["uniform_1e5"] = np.full(100000, 1e-5)
+    oh = np.zeros(1 << 18)
+    oh[123457] = 1.0
+    out["onehot_262144"] = oh
+    two = np.zeros(10000)
+    two[[10, 9000]] = 0.5
+    out["twohot_exact"] = two
+    short = np.full(5000, 0.9 / 5000)
+    out["short_mass_guard"] = short
+    z = np.exp(rng.standard_normal(50000))
+    z[:20000] = 0.0
+    z[30000:30100] = 0.0
+    out["zeros_prefix"] = z / z.sum()
+    tiny = np.exp(rng.standard_normal(20000))
+    tiny[0] = 1e-300
+    tiny[1] = 5e-324
+    out["subnormal_head"] = tiny / tiny.sum()
+    return out
+
+
+def test_resample_from_injected_g_is_bit_exact():
+    """Kernel-level parity of resample_multinomial (filter.cpp:158-178): the
+    device CDF equals the reference's sequential sum bit for bit, so the
+    ancestors are identical for every fitness vector."""
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    rng = np.random.default_rng(11)
+    for name, g in _g_cases(rng).items():
+        n = len(g)
+        s = GpuSampler("lv", PfConfig(particles=n, seed=99), ObservationModel([0, 1], 0.05))
+        anc, cdf = s.resample_from_g(g, 4, with_cdf=True)
+        ref_cdf = np.cumsum(g)
+        ref_cdf[-1] = max(ref_cdf[-1], 1.0)
+        assert np.array_equal(cdf, ref_cdf), (name, np.flatnonzero(cdf != ref_cdf)[:5])
+        want = O.resample(g, 99, 4)
+        assert np.array_equal(anc.astype(np.int64), want), (name, np.flatnonzero(anc != want)[:5])
+        s.close()
+
+
+def test_resample_golden_fixture():
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    d = np.load(os.path.join(GOLD, "resample.npz"))
+    for k in [x[:-2] for x in d.files if x.endswith("_g")]:
+        g = d[f"{k}_g"]
+        s = GpuSampler("lv", PfConfig(particles=len(g), seed=99), ObservationModel([0, 1], 0.05))
+        assert np.array_equal(s.resample_from_g(g, 4).astype(np.int64), d[f"{k}_anc"]), k
+        s.close()
+
+
+def test_cumsum_is_sequential():
+    # the check above relies on np.cumsum being the left-to-right sum
+    g = np.random.default_rng(0).random(1000)
+    acc, out = 0.0, []
+    for v in g:
+        acc += v
+        out.append(acc)
+    assert np.array_equal(np.cumsum(g), np.array(out))
+
+
+# ---------------------------------------------------------------- lock-step
+def _compare_step(gpu, ens_o, trace_o, dg, row):
+    anc_g, llb_g, _ = gpu.step_diagnostics()
+    got = gpu.get_ensemble()
+    mism = np.flatnonzero(anc_g.astype(np.int64) != dg["ancestors"])
+    assert mism.size == 0, f"ancestor mismatch at slots {mism[:10]}"
+    assert _rel(llb_g, dg["loglik_bar"]) < REL_STATE
+    assert _rel(got.states, ens_o.states) < REL_STATE
+    assert _rel_scaled(got.params_u, ens_o.params_u) < REL_STATE
+    w_g, w_o = np.exp(got.logw), np.exp(ens_o.logw)
+    assert _rel_scaled(w_g, w_o) < REL_STATE
+    assert _rel(got.mean_u, ens_o.mean_u) < REL_TRACE
+    assert _rel_scaled(got.cov_u, ens_o.cov_u) < REL_TRACE
+    tr = np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]])
+    assert _rel(tr, trace_o) < REL_TRACE
+
+
+LOCKSTEP = [
+    ("lv_am2_m1", dict(model="lv", family="am", order=2, h=0.1, seed=21), 1 << 16, 8, 1),
+    ("lv_ab2_m1", dict(model="lv", family="ab", order=2, h=0.1, seed=22), 1 << 14, 6, 1),
+    ("lv_bdf3_m4", dict(model="lv", family="bdf", order=3, h=0.025, seed=23), 1 << 13, 5, 4),
+    ("lv_am3_m4", dict(model="lv", family="am", order=3, h=0.025, seed=24), 1 << 13, 5, 4),
+    ("lv_ab3_m4", dict(model="lv", family="ab", order=3, h=0.025, seed=25), 1 << 13, 5, 4),
+]
+
+
+@pytest.mark.parametrize("name,kw,n,steps,m", LOCKSTEP, ids=[c[0] for c in LOCKSTEP])
+def test_lockstep_lotka_volterra(name, kw, n, steps, m):
+    """Both sides start every step from the same (oracle) ensemble."""
+    from paper_1411_1702_b200 import problems
+    sc = StepConfig(**kw, obs_idx=(0, 1), sigma=0.05)
+    prob = problems.lotka_volterra(particles=n, T=steps, seed=kw["seed"])
+    ens = O.init_uniform("lv", n, kw["seed"], **prob.prior)
+    gpu = _sampler(sc, n)
+    tp = 0.0
+    for j in range(1, steps + 1):
+        gpu.set_ensemble(_to_gpu_ens(ens))
+        t1 = prob.times[j - 1]
+        row = gpu.pf_step(prob.ys[j - 1], j, tp, t1, h=(t1 - tp) / m)
+        sc.h = (t1 - tp) / m
+        trace_o, dg = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1, diag=True)
+        _compare_step(gpu, ens, trace_o, dg, row)
+        tp = t1
+    gpu.close()
+
+
+def _golden_cases():
+    return sorted(f[3:-4] for f in os.listdir(GOLD) if f.startswith("pf_") and f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("case", _golden_cases())
+def test_against_reference_fixtures(case):
+    """Lock-step against fixtures written by the unmodified reference."""
+    d = np.load(os.path.join(GOLD, f"pf_{case}.npz"))
+    kw = json.loads(str(d["config"]))
+    sc = StepConfig(**kw)
+    n = int(d["n"])
+    gpu = _sampler(sc, n)
+    ens = OEns(d["init_states"], d["init_params_u"], d["init_logw"], d["init_mean_u"], d["init_cov_u"])
+    for j, (t0, t1, h) in enumerate(d["steps"], 1):
+        gpu.set_ensemble(_to_gpu_ens(ens))
+        row = gpu.pf_step(d["ys"][j - 1], j, float(t0), float(t1), h=float(h))
+        nxt = OEns(d[f"s{j}_states"], d[f"s{j}_params_u"], d[f"s{j}_logw"], d[f"s{j}_mean_u"], d[f"s{j}_cov_u"])
+        dg = {"ancestors": d[f"s{j}_anc"], "loglik_bar": d[f"s{j}_llbar"]}
+        _compare_step(gpu, nxt, d[f"s{j}_trace"], dg, row)
+        ens = nxt
+    gpu.close()
+
+
+def test_free_running_lotka_volterra():
+    """No re-injection: GPU and oracle run 30 steps independently."""
+    from paper_1411_1702_b200 import problems
+    n, steps = 1 << 14, 30
+    prob = problems.lotka_volterra(particles=n, T=steps, seed=5)
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=5, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 5, **prob.prior)
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    tp = 0.0
+    for j in range(1, steps + 1):
+        t1 = prob.times[j - 1]
+        row = gpu.pf_step(prob.ys[j - 1], j, tp, t1)
+        trace_o, dg = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1, diag=True)
+        anc_g, _, _ = gpu.step_diagnostics()
+        assert np.array_equal(anc_g.astype(np.int64), dg["ancestors"]), f"step {j}"
+        tr = np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]])
+        assert _rel(tr, trace_o) < REL_TRACE, j
+        tp = t1
+    got = gpu.get_ensemble()
+    assert _rel(got.states, ens.states) < 1e-8
+    gpu.close()
+
+
+# ---------------------------------------------------------------- stiff models
+def test_lockstep_chain_bdf3():
+    th = np.array([2.0, 50.0, 5.0, 0.5])
+    n = 4096
+    sc = StepConfig(model="chain", family="bdf", order=3, h=0.1 / 3, a=0.98, seed=8, obs_idx=(0, 3, 7), sigma=0.01)
+    ens = O.init_uniform("chain", n, 8, 0.5 * th, 2 * th, [0] * 8, [0] * 8)
+    gpu = _sampler(sc, n)
+    rng = np.random.default_rng(3)
+    tp = 0.0
+    for j in range(1, 5):
+        y = np.array([0.09 * j, 0.001 * j, 0.0]) + 0.01 * rng.standard_normal(3)
+        gpu.set_ensemble(_to_gpu_ens(ens))
+        row = gpu.pf_step(y, j, tp, tp + 0.1)
+        trace_o, dg = O.pf_step(sc, ens, y, j, tp, tp + 0.1, diag=True)
+        _compare_step(gpu, ens, trace_o, dg, row)
+        tp += 0.1
+    gpu.close()
+
+
+def test_lockstep_robertson_lognormal():
+    from paper_1411_1702_b200 import problems
+    n = 4096
+    prob = problems.robertson(particles=n, T=6, seed=4)
+    sc = StepConfig(model="robertson", family="bdf", order=2, a=0.99, seed=4, obs_idx=(0, 2), sigma=0.02,
+                    newton_max_iter=4, likelihood="lognormal")
+    ens = O.init_gaussian("robertson", n, 4, prob.prior["th_mu"], prob.prior["th_sigma"], prob.prior["x_mean"],
+                          prob.prior["x_std"], [0, 0, 0])
+    gpu = _sampler(sc, n, likelihood="lognormal")
+    tp = 0.0
+    for j in range(1, 7):
+        t1 = prob.times[j - 1]
+        sc.h = (t1 - tp) / 2
+        gpu.set_ensemble(_to_gpu_ens(ens))
+        row = gpu.pf_step(prob.ys[j - 1], j, tp, t1, h=sc.h)
+        trace_o, dg = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1, diag=True)
+        _compare_step(gpu, ens, trace_o, dg, row)
+        tp = t1
+    gpu.close()
+
+
+# ---------------------------------------------------------------- init / errors
+def test_device_initialisation_matches_oracle():
+    from paper_1411_1702_b200 import problems
+    n = 10000
+    prob = problems.lotka_volterra(particles=n, T=1, seed=9)
+    gpu = _sampler(StepConfig(model="lv", seed=9), n)
+    gpu.initialize_uniform(**prob.prior)
+    got = gpu.get_ensemble()
+    ens = O.init_uniform("lv", n, 9, **prob.prior)
+    assert np.array_equal(got.states, ens.states)        # uniforms are integer-exact
+    assert _rel_scaled(got.params_u, ens.params_u) < 1e-14  # log: CUDA vs glibc
+    assert np.array_equal(got.logw, ens.logw)
+    assert _rel(got.mean_u, ens.mean_u) < 1e-12
+    assert _rel_scaled(got.cov_u, ens.cov_u) < 1e-10
+    gpu.close()
+    sc = StepConfig(model="robertson", seed=9, obs_idx=(0, 2), sigma=0.02)
+    gpu = _sampler(sc, n)
+    mu = list(np.log([0.04, 3e7, 1e4]) + 0.5)
+    gpu.initialize_gaussian(mu, [1, 1, 1], [1, 0, 0], [0, 0, 0])
+    got = gpu.get_ensemble()
+    ens = O.init_gaussian("robertson", n, 9, mu, [1, 1, 1], [1, 0, 0], [0, 0, 0], [0, 0, 0])
+    assert _rel_scaled(got.params_u, ens.params_u) < 1e-13  # normals: CUDA log/sin/cos
+    assert np.array_equal(got.states, ens.states)
+    gpu.close()
+
+
+def test_total_degeneracy_raises_numerical_at_same_step():
+    from paper_1411_1702_b200.sampler import NumericalError
+    n = 2048
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=2, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 2, [0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    with pytest.raises(NumericalError, match="total degeneracy"):
+        gpu.pf_step(np.array([1e200, 1e200]), 1, 0.0, 0.1)
+    gpu.close()
+
+
+def test_config_errors():
+    from paper_1411_1702_b200.sampler import ConfigError
+    with pytest.raises(ConfigError):
+        _sampler(StepConfig(model="lv", a=1.0), 16)
+    with pytest.raises(ConfigError):
+        _sampler(StepConfig(model="lv", obs_idx=(0, 0)), 16)
+    gpu = _sampler(StepConfig(model="lv"), 16)
+    gpu.initialize_uniform([0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+    with pytest.raises(ConfigError, match="integer step count"):
+        gpu.pf_step([1.0, 1.0], 1, 0.0, 0.1, h=0.03)
+    gpu.close()
+
+
+def test_run_matches_oracle_loop():
+    """filter::run semantics: row 0 + T rows, degeneracy streak flags."""
+    from paper_1411_1702_b200 import problems
+    n, T = 1024, 20
+    prob = problems.lotka_volterra(particles=n, T=T, seed=1)
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=1, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 1, **prob.prior)
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    rows = gpu.run(prob.ys, prob.times)
+    assert len(rows) == T + 1 and rows[0].j == 0 and rows[-1].j == T
+    tp = 0.0
+    for j in range(1, T + 1):
+        trace_o, _ = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, prob.times[j - 1])
+        r = rows[j]
+        tr = np.concatenate([r.theta_mean, r.theta_var, r.state_mean, [r.ess]])
+        assert _rel(tr, trace_o) < REL_TRACE, j
+        tp = prob.times[j - 1]
+    gpu.close()
