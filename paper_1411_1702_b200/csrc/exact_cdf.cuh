@@ -12,51 +12,41 @@
 // run of elements composes exactly in the monoid
 //   (A then B)(b) = A(b) + B((b + A(b)) mod 2),
 // represented by the pair (delta(0), delta(1)) -- a parallel scan.
-// Binade crossings (where rounding changes scale) are located with a
-// double-double approximate prefix P_k and a rigorous bound E_k >= |s_k - P_k|
-// (<= cnt_k ulp/2, cnt_k = inexact additions so far). Every element whose
-// before/after values are not certainly in one binade becomes a "window":
-// the resolver applies it with a real IEEE add, fl(s + g), in order. Windows
-// are ~log2(N) per scan (one per binade crossing), so the serial part is tiny.
-// Elements with g == 0 are the identity and never need a window.
+//
+// Binade crossings (where rounding changes scale) are located with an
+// approximate parallel prefix P_k (plain doubles, any summation tree) and a
+// rigorous bound |s_k - P_k| <= E_k: a floating-point sum of nonnegative
+// terms by any tree has at most (cnt - 1) rounding nodes (nodes adding a zero
+// are exact), each off by <= 2^-53 of a value <= the total, so both s_k and
+// P_k are within (cnt_k - 1) 2^-53 P_k(1 + tiny) of the true sum. Every
+// element whose before/after values are not CERTAINLY in one binade becomes a
+// "window": the resolver applies it with a real IEEE add, fl(s + g), in
+// order. Windows are ~log2(N) per scan (one per binade crossing), so the
+// serial part is tiny. Elements with g == 0 are the identity.
 #pragma once
 #include <cstdint>
 
 namespace pfsmc_gpu {
 
-// ---------------- double-double helpers (error-free transforms) ----------
-struct DD {
-  double hi, lo;
-};
-__device__ __forceinline__ DD two_sum(double a, double b) {
-  const double s = __dadd_rn(a, b);
-  const double bb = __dsub_rn(s, a);
-  const double err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-  return {s, err};
-}
-__device__ __forceinline__ DD dd_add(DD a, double b) {
-  DD s = two_sum(a.hi, b);
-  s.lo = __dadd_rn(s.lo, a.lo);
-  return two_sum(s.hi, s.lo);
-}
-__device__ __forceinline__ DD dd_add(DD a, DD b) {
-  DD s = two_sum(a.hi, b.hi);
-  s.lo = __dadd_rn(s.lo, __dadd_rn(a.lo, b.lo));
-  return two_sum(s.hi, s.lo);
-}
-
 // Binade index with the subnormal range folded into e = -1022
 // (ulp 2^-1074 on [0, 2^-1021)).
 __device__ __forceinline__ int binade_of(double v) {
   if (!(v >= 0x1.0p-1021)) return -1022;
-  return ilogb(v);
+  return static_cast<int>((__double_as_longlong(v) >> 52) & 0x7ff) - 1023;
+}
+
+// x * 2^k, exact whenever the result is representable: a single multiply by
+// a bit-built power of two on the normal range, ldexp() beyond it.
+__device__ __forceinline__ double scale2(double x, int k) {
+  if (k >= -1000 && k <= 1000) return x * __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+  return ldexp(x, k);
 }
 
 constexpr int kNoBinade = -100000;
 
-// Monoid element for the segmented scan. flag = segment head (a window or
-// the element right after one starts a new segment); e = the binade of the
-// segment (kNoBinade while the segment holds only g == 0 elements).
+// Monoid element for the segmented scan. flag = segment head (a window
+// starts a new segment); e = the binade of the segment (kNoBinade while the
+// segment holds only g == 0 elements).
 struct Piece {
   long long d0, d1;
   int e;
@@ -69,37 +59,41 @@ __device__ __forceinline__ Piece piece_identity() { return {0, 0, kNoBinade, 0};
 __device__ __forceinline__ Piece piece_combine(const Piece& a, const Piece& b) {
   if (b.flag) return b;
   Piece r;
-  r.d0 = a.d0 + (((a.d0) & 1) ? b.d1 : b.d0);
+  r.d0 = a.d0 + ((a.d0 & 1) ? b.d1 : b.d0);
   r.d1 = a.d1 + (((1 + a.d1) & 1) ? b.d1 : b.d0);
   r.e = b.e != kNoBinade ? b.e : a.e;
   r.flag = a.flag;
   return r;
 }
 
-// Rigorous |s - P| bound. cnt = nonzero g's so far; the first nonzero add
-// (onto 0) is exact, and a one-term double-double sum is exact, so cnt <= 1
-// gives 0. Otherwise (cnt - 1) roundings of <= 2^-53 s each, doubled plus a
-// margin that also covers rounding P.hi +- E itself.
-__device__ __forceinline__ double sum_bound(double p_hi, long long cnt) {
+__device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
+  Piece r;
+  r.d0 = __shfl_up_sync(0xffffffffu, p.d0, o);
+  r.d1 = __shfl_up_sync(0xffffffffu, p.d1, o);
+  r.e = __shfl_up_sync(0xffffffffu, p.e, o);
+  r.flag = __shfl_up_sync(0xffffffffu, p.flag, o);
+  return r;
+}
+
+// Rigorous |s - P| bound (see header). cnt <= 1: both sums are exact.
+__device__ __forceinline__ double sum_bound(double p, long long cnt) {
   if (cnt <= 1) return 0.0;
-  return (static_cast<double>(cnt - 1) + 4.0) * 0x1.0p-51 * p_hi + 0x1.0p-1060;
+  return (2.0 * static_cast<double>(cnt) + 8.0) * 0x1.0p-53 * p + 0x1.0p-1060;
 }
 
 // Per-element kind: 0 = neutral (g == 0), 1 = run element, 2 = window.
 // For run elements fills the monoid piece at binade e.
-__device__ __forceinline__ int classify(double g, DD p_prev, long long cnt_prev, DD p_cur,
+__device__ __forceinline__ int classify(double g, double p_prev, long long cnt_prev, double p_cur,
                                         long long cnt_cur, Piece& out) {
   out = piece_identity();
   if (g == 0.0) return 0;
-  const double lo = p_prev.hi - sum_bound(p_prev.hi, cnt_prev);
-  const double hi = p_cur.hi + sum_bound(p_cur.hi, cnt_cur);
-  const int e_lo = binade_of(lo);
-  const int e_hi = binade_of(hi);
+  const int e_lo = binade_of(p_prev - sum_bound(p_prev, cnt_prev));
+  const int e_hi = binade_of(p_cur + sum_bound(p_cur, cnt_cur));
   if (e_lo != e_hi) {
     out.flag = 1;
     return 2;
   }
-  const double v = ldexp(g, 52 - e_lo);  // exact scaling, v < 2^53
+  const double v = scale2(g, 52 - e_lo);  // exact scaling, v < 2^53
   const double q = floor(v);
   const double f = v - q;
   const long long qi = static_cast<long long>(q);
@@ -108,7 +102,7 @@ __device__ __forceinline__ int classify(double g, DD p_prev, long long cnt_prev,
   } else if (f > 0.5) {
     out.d0 = out.d1 = qi + 1;
   } else {  // exact tie: round half to even on m + q
-    out.d0 = qi + ((0 + qi) & 1);
+    out.d0 = qi + (qi & 1);
     out.d1 = qi + ((1 + qi) & 1);
   }
   out.e = e_lo;
@@ -121,12 +115,11 @@ __device__ __forceinline__ int classify(double g, DD p_prev, long long cnt_prev,
 __device__ __forceinline__ bool piece_apply(const Piece& a, double& s) {
   if (a.e == kNoBinade) return true;
   if (binade_of(s) != a.e) return false;
-  const double ms = ldexp(s, 52 - a.e);
+  const double ms = scale2(s, 52 - a.e);
   const long long m = static_cast<long long>(ms);
-  if (static_cast<double>(m) != ms) return false;
   const long long m2 = m + ((m & 1) ? a.d1 : a.d0);
-  s = ldexp(static_cast<double>(m2), a.e - 52);
-  return true;
+  s = scale2(static_cast<double>(m2), a.e - 52);
+  return static_cast<double>(m) == ms;
 }
 
 }  // namespace pfsmc_gpu

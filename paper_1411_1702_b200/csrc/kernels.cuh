@@ -14,8 +14,6 @@
 namespace pfsmc_gpu {
 
 constexpr int kMaxObs = 8;
-constexpr int kTile = 4096;              // exact-CDF tile (elements)
-constexpr int kItems = kTile / kThreads;  // 16 per thread
 constexpr int kMaxWin = 64;              // windows per tile before serial fallback
 constexpr double kNegInf = -INFINITY;
 
@@ -37,7 +35,7 @@ struct DevState {
   int cur;            // which record buffer holds the ensemble
   int error;          // ErrBits of the current step
   int chol_failed;    // chol_psd of cov failed (raised at the next proliferation)
-  int pad;
+  int scan_epoch;     // tags this step's look-back descriptors
   double lse_w;       // logw_n = lw_n - lse_w
   double lse_g;       // fitness log-normaliser of the current step
   double mu[4];       // shrink mean = weighted mean of the current params
@@ -72,19 +70,20 @@ struct Ctx {
   unsigned long long seed;
   double two_s2;
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
+  int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
   double* rec[2];
   double* lw;
   double* llbar;
   double* lg;
   double* cdf;
   unsigned* anc;
-  unsigned short* lguide;  // per-tile local guide (kTile entries per tile)
+  unsigned short* lguide;  // per-tile local guide (one entry per tile element)
   unsigned* coarse;
-  double* tile_start;  // exact CDF value before each tile (0 for tile 0)
-  double* tile_end;    // exact CDF value at each tile's last element (guarded at the end)
-  DD* tile_sum;
-  long long* tile_cnt;
-  DD* tile_pre;
+  double2* tile_info;  // exact CDF (value before the tile, value at its last element;
+                       // the last tile's end carries the guard, filter.cpp:168)
+  double* g;           // fitness of the current step (k_scan_tiles writes it)
+  struct LookBack* lookback;  // decoupled look-back descriptors (approx. tile sums)
+  double* tile_pre;    // approximate exclusive tile prefixes
   long long* tile_cnt_pre;
   TileHdr* hdr;
   TileWin* win;        // kMaxWin per tile
@@ -93,7 +92,7 @@ struct Ctx {
   double* gpart;       // group partials
   unsigned* cnt_pred;  // last-block counters of k_predict (ngroups + 1)
   unsigned* cnt_upd;   // ... of k_update / k_moments (ngroups + 1)
-  unsigned* cnt_scan;  // [0] k_scan_sums, [1] k_scan_pieces
+  unsigned* cnt_scan;  // [1] k_scan_pieces done counter, [2] its dynamic tile id
   const double* gin;   // injected fitness (parity mode) or null
   DevState* st;
   const StepParams* sp;
@@ -136,28 +135,28 @@ __device__ __forceinline__ void store_record(double* __restrict__ rec, int R, lo
 template <class M>
 __device__ __forceinline__ double loglik(const Ctx& c, const StepParams& sp,
                                          const double (&x)[M::D]) {
+  // all indices compile-time (no local-memory copies of c / sp)
   double ss = 0.0;
-  if (c.likelihood == PFSMC_GPU_LIK_LOGNORMAL) {
-    for (int k = 0; k < c.m_y; ++k) {
-      double xv = 0.0;
+  const bool lognormal = c.likelihood == PFSMC_GPU_LIK_LOGNORMAL;
+  bool dead = false;
 #pragma unroll
-      for (int i = 0; i < M::D; ++i)
-        if (i == c.obs_idx[k]) xv = x[i];
-      if (!(xv > 0.0)) return kNegInf;
-      const double r = sp.y[k] - log(xv);
-      ss += r * r;
-    }
-  } else {
-    for (int k = 0; k < c.m_y; ++k) {
-      double xv = 0.0;
+  for (int k = 0; k < kMaxObs; ++k) {
+    if (k < c.m_y) {
+      const int idx = c.obs_idx[k];
+      double xv = x[0];
 #pragma unroll
-      for (int i = 0; i < M::D; ++i)
-        if (i == c.obs_idx[k]) xv = x[i];
-      const double r = sp.y[k] - xv;
+      for (int i = 1; i < M::D; ++i) xv = (i == idx) ? x[i] : xv;
+      double r;
+      if (lognormal) {
+        dead |= !(xv > 0.0);
+        r = sp.y[k] - log(xv);
+      } else {
+        r = sp.y[k] - xv;
+      }
       ss += r * r;
     }
   }
-  if (c.likelihood == PFSMC_GPU_LIK_LOGNORMAL) return (sp.ll_const - ss / c.two_s2) - sp.sly;
+  if (lognormal) return dead ? kNegInf : (sp.ll_const - ss / c.two_s2) - sp.sly;
   return sp.ll_const - ss / c.two_s2;
 }
 
@@ -167,7 +166,7 @@ __device__ __forceinline__ bool grid_error(const Ctx& c) {
 
 // ---------------------------------------------------------------- K1
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads) k_predict(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 4) k_predict(Ctx c) {
   constexpr int D = M::D, P = M::P;
   __shared__ double scratch[kWarps * 2];
   __shared__ double fin[2];
@@ -210,20 +209,22 @@ __global__ void __launch_bounds__(kThreads) k_predict(Ctx c) {
   }
 }
 
-// Ancestor search: first k with cdf_k > u (std::upper_bound), clamped.
+// Ancestor search: first k with cdf_k > u (std::upper_bound, filter.cpp:173),
+// clamped to N-1 (filter.cpp:175). coarse guide -> tile -> per-tile local
+// guide -> short forward walk over the exact CDF.
 __device__ __forceinline__ unsigned find_ancestor(const Ctx& c, double u) {
-  const double B1 = ldexp(1.0, c.coarse_bits);
+  const double B1 = scale2(1.0, c.coarse_bits);
   int t = static_cast<int>(__ldg(&c.coarse[static_cast<long long>(u * B1)]));
-  while (t < c.ntiles - 1 && __ldg(&c.tile_end[t]) <= u) ++t;
-  const double c_start = __ldg(&c.tile_start[t]);
-  const double c_end = __ldg(&c.tile_end[t]);
-  const double wdt = (c_end - c_start) * (1.0 / kTile);
-  double fi = floor((u - c_start) / wdt);
-  fi = fmin(fmax(fi, 0.0), static_cast<double>(kTile - 1));
+  double2 ti = __ldg(&c.tile_info[t]);
+  while (t < c.ntiles - 1 && ti.y <= u) ti = __ldg(&c.tile_info[++t]);
+  const int tile = 1 << c.tile_log2;
+  const double wdt = (ti.y - ti.x) * scale2(1.0, -c.tile_log2);
+  double fi = floor((u - ti.x) / wdt);
+  fi = fmin(fmax(fi, 0.0), static_cast<double>(tile - 1));
   int i = static_cast<int>(fi);
-  while (i > 0 && c_start + static_cast<double>(i) * wdt > u) --i;
-  while (i + 1 < kTile && c_start + static_cast<double>(i + 1) * wdt <= u) ++i;
-  const long long base = static_cast<long long>(t) * kTile;
+  while (i > 0 && ti.x + static_cast<double>(i) * wdt > u) --i;
+  while (i + 1 < tile && ti.x + static_cast<double>(i + 1) * wdt <= u) ++i;
+  const long long base = static_cast<long long>(t) << c.tile_log2;
   long long k = base + __ldg(&c.lguide[base + i]);
   while (k < c.N - 1 && __ldg(&c.cdf[k]) <= u) ++k;
   return static_cast<unsigned>(k);
@@ -342,13 +343,15 @@ __device__ void chol_psd_device(DevState& st) {
 }
 
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads) k_update(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 3) k_update(Ctx c) {
   constexpr int D = M::D, P = M::P;
   using ML = MomentLayout<M>;
   constexpr int V = ML::V;
   __shared__ double scratch[kWarps * V];
   __shared__ double fin[V + 1];  // M + V values
   __shared__ double sL[P * P], sK[P];
+  constexpr int kTsc = V <= 12 ? V * kThreads : 1;
+  __shared__ double tsc[kTsc];
   if (grid_error(c)) return;
   DevState& st = *c.st;
   if (st.chol_failed) {
@@ -429,7 +432,8 @@ __global__ void __launch_bounds__(kThreads) k_update(Ctx c) {
     for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(0xffffffffu, it, o);
     if ((threadIdx.x & 31) == 0 && it) atomicAdd(&st.newton_iters, static_cast<unsigned long long>(it));
   }
-  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
+  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch,
+                         V <= 12 ? tsc : nullptr);
   if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
     if (threadIdx.x == 0) {
       double K[P];

@@ -68,12 +68,44 @@ __device__ __forceinline__ void block_sums(double (&v)[V], double* scratch) {
   }
 }
 
+// Block-wide sums through a shared-memory transpose (fewer instructions
+// than V shuffle trees): each thread stores its V values, then V*8 threads
+// each fold 32 entries of one value in order, then V threads fold the 8
+// chunk sums in order. Fixed shape => bitwise reproducible. Result in
+// thread 0's v[]. tsc >= V * kThreads doubles.
+template <int V>
+__device__ __forceinline__ void block_sums_smem(double (&v)[V], double* tsc) {
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < V; ++k) tsc[k * kThreads + threadIdx.x] = v[k];
+  __syncthreads();
+  double part = 0.0;
+  if (threadIdx.x < V * kWarps) {
+    const int k = threadIdx.x / kWarps, ch = threadIdx.x % kWarps;
+    const double* src = tsc + k * kThreads + ch * 32;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) part += src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < V * kWarps) tsc[threadIdx.x] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double s = tsc[k * kWarps];
+      for (int i = 1; i < kWarps; ++i) s += tsc[k * kWarps + i];
+      v[k] = s;
+    }
+  }
+}
+
 // Leaf -> block partial. x: leaf log-weight; vals: leaf quantities (weighted
 // by e = exp(x - M) inside, the last one by e^2 when SQ). Thread 0 writes
-// (M, sums[V]) to out[0..V].
+// (M, sums[V]) to out[0..V]. tsc: V * kThreads doubles of shared scratch
+// (null: shuffle trees, scratch >= kWarps * V).
 template <int V, bool SQ>
 __device__ __forceinline__ void block_partial(double x, const double (&vals)[V], double* out,
-                                              double* scratch) {
+                                              double* scratch, double* tsc = nullptr) {
   const bool is_nan = isnan(x);
   const double leaf_max = is_nan ? -INFINITY : x;
   const double M = block_max(leaf_max, scratch);
@@ -87,7 +119,10 @@ __device__ __forceinline__ void block_partial(double x, const double (&vals)[V],
   double v[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) v[k] = ((SQ && k == V - 1) ? e * e : e) * vals[k];
-  block_sums<V>(v, scratch);
+  if (tsc)
+    block_sums_smem<V>(v, tsc);
+  else
+    block_sums<V>(v, scratch);
   if (threadIdx.x == 0) {
     out[0] = M;
 #pragma unroll

@@ -3,7 +3,7 @@
 //
 // One step (reference: filter::pf_step, filter.cpp:292-394) is five launches:
 //   K1 k_predict      shrink + Psi + log-lik + fitness lse   (filter.cpp:300-324, 143-156)
-//   S1 k_scan_sums    fitness g, per-tile double-double sums  \
+//   S1 (merged into S2: fitness g, look-back approximate tile prefixes)     \
 //   S2 k_scan_pieces  exact-CDF run/window decomposition,      > exact sequential CDF
 //                     last block resolves the serial chain    /  (filter.cpp:158-168)
 //   S3 k_scan_cdf     exact CDF + per-tile guide tables
@@ -31,419 +31,641 @@
 
 namespace pfsmc_gpu {
 // ---------------------------------------------------------------- exact CDF
-__device__ __forceinline__ double fitness_of(const Ctx& c, long long k, double lse) {
-  if (k >= c.N) return 0.0;
-  if (c.gin) return c.gin[k];
-  return exp(c.lg[k] - lse);  // fitness_weights (filter.cpp:154)
-}
-
-// smem layout with one pad double per 16 to keep the per-thread contiguous
-// reads conflict-free.
-__device__ __forceinline__ int sidx(int e) { return e + (e >> 4); }
-constexpr int kSmemTile = kTile + kTile / 16;
-
-__device__ __forceinline__ void load_tile_g(const Ctx& c, int t, double* sg) {
-  const double lse = c.st->lse_g;
-  const long long base = static_cast<long long>(t) * kTile;
-#pragma unroll 4
-  for (int i = 0; i < kItems; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    sg[sidx(e)] = fitness_of(c, base + e, lse);
-  }
-  __syncthreads();
-}
-
-// Block exclusive scan of (DD, count) pairs: approximate prefix only.
-__device__ __forceinline__ void block_excl_scan_dd(DD v, long long cnt, DD& excl, long long& cexcl,
-                                                   DD* sdd, long long* scnt) {
-  sdd[threadIdx.x] = v;
-  scnt[threadIdx.x] = cnt;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    // warp 0 scans 8 chunks of 32 sequentially in dd (deterministic)
-    const int l = threadIdx.x;
-    DD run = {0.0, 0.0};
-    long long crun = 0;
-    for (int chunk = 0; chunk < kThreads / 32; ++chunk) {
-      const int i = chunk * 32 + l;
-      DD x = sdd[i];
-      long long cx = scnt[i];
-      // inclusive warp scan (Hillis-Steele)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        DD y;
-        y.hi = __shfl_up_sync(0xffffffffu, x.hi, o);
-        y.lo = __shfl_up_sync(0xffffffffu, x.lo, o);
-        const long long cy = __shfl_up_sync(0xffffffffu, cx, o);
-        if (l >= o) {
-          x = dd_add(y, x);
-          cx += cy;
-        }
-      }
-      DD ex;
-      ex.hi = __shfl_up_sync(0xffffffffu, x.hi, 1);
-      ex.lo = __shfl_up_sync(0xffffffffu, x.lo, 1);
-      long long cex = __shfl_up_sync(0xffffffffu, cx, 1);
-      if (l == 0) {
-        ex = {0.0, 0.0};
-        cex = 0;
-      }
-      sdd[i] = dd_add(run, ex);
-      scnt[i] = crun + cex;
-      DD tot;
-      tot.hi = __shfl_sync(0xffffffffu, x.hi, 31);
-      tot.lo = __shfl_sync(0xffffffffu, x.lo, 31);
-      run = dd_add(run, tot);
-      crun += __shfl_sync(0xffffffffu, cx, 31);
-    }
-  }
-  __syncthreads();
-  excl = sdd[threadIdx.x];
-  cexcl = scnt[threadIdx.x];
-  __syncthreads();
-}
-
-// S1: per-tile double-double sums + nonzero counts; last block: exclusive
-// prefix over tiles.
-__global__ void __launch_bounds__(kThreads) k_scan_sums(Ctx c) {
-  __shared__ double sg[kSmemTile];
-  __shared__ DD sdd[kThreads];
-  __shared__ long long scnt[kThreads];
-  __shared__ int s_last;
-  if (grid_error(c)) return;
-  const int t = blockIdx.x;
-  load_tile_g(c, t, sg);
-  DD s = {0.0, 0.0};
-  long long cnt = 0;
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const double g = sg[sidx(threadIdx.x * kItems + i)];
-    s = dd_add(s, g);
-    cnt += (g != 0.0);
-  }
-  DD ex;
-  long long cex;
-  block_excl_scan_dd(s, cnt, ex, cex, sdd, scnt);
-  if (threadIdx.x == kThreads - 1) {
-    c.tile_sum[t] = dd_add(ex, s);
-    c.tile_cnt[t] = cex + cnt;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned old = atomicAdd(&c.cnt_scan[0], 1u);
-    s_last = (old == gridDim.x - 1);
-    if (s_last) c.cnt_scan[0] = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // exclusive prefix over tiles: thread-contiguous chunks, then block scan
-  const int per = (c.ntiles + kThreads - 1) / kThreads;
-  const int t0 = threadIdx.x * per;
-  DD ts = {0.0, 0.0};
-  long long tc = 0;
-  for (int k = t0; k < min(t0 + per, c.ntiles); ++k) {
-    DD v;
-    v.hi = __ldcg(&c.tile_sum[k].hi);
-    v.lo = __ldcg(&c.tile_sum[k].lo);
-    ts = dd_add(ts, v);
-    tc += __ldcg(&c.tile_cnt[k]);
-  }
-  block_excl_scan_dd(ts, tc, ex, cex, sdd, scnt);
-  for (int k = t0; k < min(t0 + per, c.ntiles); ++k) {
-    c.tile_pre[k] = ex;
-    c.tile_cnt_pre[k] = cex;
-    DD v;
-    v.hi = __ldcg(&c.tile_sum[k].hi);
-    v.lo = __ldcg(&c.tile_sum[k].lo);
-    ex = dd_add(ex, v);
-    cex += __ldcg(&c.tile_cnt[k]);
-  }
-}
-
-// Block-wide exclusive segmented scan of Piece (Hillis-Steele, fixed shape).
-__device__ __forceinline__ Piece block_excl_scan_piece(Piece v, Piece* sp) {
-  sp[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = 1; o < kThreads; o <<= 1) {
-    Piece mine = sp[threadIdx.x];
-    Piece left = threadIdx.x >= o ? sp[threadIdx.x - o] : piece_identity();
-    __syncthreads();
-    if (threadIdx.x >= o) sp[threadIdx.x] = piece_combine(left, mine);
-    __syncthreads();
-  }
-  Piece ex = threadIdx.x ? sp[threadIdx.x - 1] : piece_identity();
-  __syncthreads();
-  return ex;
-}
-
-__device__ __forceinline__ int block_excl_scan_int(int v, int* si, int& total) {
-  si[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = 1; o < kThreads; o <<= 1) {
-    const int x = si[threadIdx.x];
-    const int y = threadIdx.x >= o ? si[threadIdx.x - o] : 0;
-    __syncthreads();
-    si[threadIdx.x] = x + y;
-    __syncthreads();
-  }
-  total = si[kThreads - 1];
-  const int ex = threadIdx.x ? si[threadIdx.x - 1] : 0;
-  __syncthreads();
-  return ex;
-}
-
-// Shared per-tile analysis used by S2 and S3 (identical code => identical
-// classification in both).
-struct TileScan {
-  Piece carry;      // exclusive segmented prefix for this thread
-  int win_excl;     // windows before this thread's first element
-  int win_total;    // windows in the tile
-  DD p0;            // approximate prefix before this thread's first element
-  long long c0;
+// Tiles of ITEMS * 256 elements (thread t owns elements ITEMS*t .. +ITEMS-1).
+// ITEMS = 4 (1024-element tiles) keeps the per-thread serial chains short
+// and the grid wide for N <= 2^22; ITEMS = 16 bounds the tile count (and the
+// resolver's work) at larger N. One pad double per thread chunk keeps the
+// per-thread contiguous shared-memory reads conflict-free.
+template <int ITEMS>
+struct TileCfg {
+  static constexpr int kTileT = ITEMS * kThreads;
+  static constexpr int kSmem = kTileT + kThreads;
+  __device__ static __forceinline__ int sidx(int e) { return e + e / ITEMS; }
 };
 
-__device__ __forceinline__ void analyse_tile(const Ctx& c, int t, const double* sg, TileScan& ts,
-                                             DD* sdd, long long* scnt, Piece* spc, int* si) {
-  DD s = {0.0, 0.0};
-  long long cnt = 0;
+// Per-thread running values for a block-wide scan.
+struct SumCnt {
+  double s;
+  long long c;
+};
+
+// Block-wide exclusive scan of (sum, count) in a fixed shape: warp shuffle
+// scan, warp totals through smem, scanned by warp 0. Approximate sums only
+// (the bound in exact_cdf.cuh covers any tree); counts exact.
+__device__ __forceinline__ SumCnt block_excl_scan_sc(SumCnt v, SumCnt& total, SumCnt* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SumCnt x = v;
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const double g = sg[sidx(threadIdx.x * kItems + i)];
-    s = dd_add(s, g);
-    cnt += (g != 0.0);
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ys = __shfl_up_sync(0xffffffffu, x.s, o);
+    const long long yc = __shfl_up_sync(0xffffffffu, x.c, o);
+    if (lane >= o) {
+      x.s = ys + x.s;
+      x.c += yc;
+    }
   }
-  DD ex;
-  long long cex;
-  block_excl_scan_dd(s, cnt, ex, cex, sdd, scnt);
-  DD tp;
-  tp.hi = __ldcg(&c.tile_pre[t].hi);
-  tp.lo = __ldcg(&c.tile_pre[t].lo);
-  ts.p0 = dd_add(tp, ex);
-  ts.c0 = __ldcg(&c.tile_cnt_pre[t]) + cex;
-  // thread-local pass: aggregate piece + window count
-  DD P = ts.p0;
-  long long C = ts.c0;
-  Piece agg = piece_identity();
-  int nw = 0;
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    SumCnt t = lane < kWarps ? sw[lane] : SumCnt{0.0, 0};
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const double g = sg[sidx(threadIdx.x * kItems + i)];
-    const DD pp = P;
-    const long long cp = C;
-    P = dd_add(P, g);
-    C += (g != 0.0);
-    Piece pc;
-    const int kind = classify(g, pp, cp, P, C, pc);
-    nw += (kind == 2);
-    agg = piece_combine(agg, pc);
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const double ys = __shfl_up_sync(0xffffffffu, t.s, o);
+      const long long yc = __shfl_up_sync(0xffffffffu, t.c, o);
+      if (lane >= o) {
+        t.s = ys + t.s;
+        t.c += yc;
+      }
+    }
+    if (lane < kWarps) sw[kWarps + lane] = t;  // inclusive warp prefixes
   }
-  ts.carry = block_excl_scan_piece(agg, spc);
-  ts.win_excl = block_excl_scan_int(nw, si, ts.win_total);
+  __syncthreads();
+  const SumCnt pre = w ? sw[kWarps + w - 1] : SumCnt{0.0, 0};
+  total = sw[2 * kWarps - 1];
+  const double es = __shfl_up_sync(0xffffffffu, x.s, 1);
+  const long long ec = __shfl_up_sync(0xffffffffu, x.c, 1);
+  SumCnt ex = lane ? SumCnt{es, ec} : SumCnt{0.0, 0};
+  ex.s = pre.s + ex.s;
+  ex.c += pre.c;
+  __syncthreads();
+  return ex;
 }
 
-// S2: tile records (window list + segment aggregates); last block resolves
-// the exact chain over tiles (serial over windows, exact integer runs).
-__global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
-  __shared__ double sg[kSmemTile];
-  __shared__ DD sdd[kThreads];
-  __shared__ long long scnt[kThreads];
-  __shared__ Piece spc[kThreads];
-  __shared__ int si[kThreads];
-  __shared__ int s_last;
-  if (grid_error(c)) return;
-  const int t = blockIdx.x;
-  load_tile_g(c, t, sg);
-  TileScan ts;
-  analyse_tile(c, t, sg, ts, sdd, scnt, spc, si);
-  const bool overflow = ts.win_total > kMaxWin;
-  // second local pass: emit windows with the aggregate preceding each
-  DD P = ts.p0;
-  long long C = ts.c0;
-  Piece acc = ts.carry;
-  int w = ts.win_excl;
-  for (int i = 0; i < kItems; ++i) {
-    const int e = threadIdx.x * kItems + i;
-    const double g = sg[sidx(e)];
-    const DD pp = P;
-    const long long cp = C;
-    P = dd_add(P, g);
-    C += (g != 0.0);
-    Piece pc;
-    const int kind = classify(g, pp, cp, P, C, pc);
-    if (kind == 2 && !overflow) {
-      TileWin tw;
-      tw.g = g;
-      tw.e = acc.e;
-      tw.local = e;
-      tw.d0 = acc.d0;
-      tw.d1 = acc.d1;
-      c.win[static_cast<size_t>(t) * kMaxWin + w] = tw;
-      ++w;
+// Block-wide exclusive segmented scan of Piece, fixed shape.
+__device__ __forceinline__ Piece block_excl_scan_piece(Piece v, Piece* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Piece x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Piece y = shfl_up_piece(x, o);
+    if (lane >= o) x = piece_combine(y, x);
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    Piece t = lane < kWarps ? sw[lane] : piece_identity();
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const Piece y = shfl_up_piece(t, o);
+      if (lane >= o) t = piece_combine(y, t);
     }
-    acc = piece_combine(acc, pc);
+    if (lane < kWarps) sw[kWarps + lane] = t;
+  }
+  __syncthreads();
+  Piece ex = shfl_up_piece(x, 1);
+  if (lane == 0) ex = piece_identity();
+  if (w) ex = piece_combine(sw[kWarps + w - 1], ex);
+  __syncthreads();
+  return ex;
+}
+
+// Block-wide exclusive scan of ints.
+__device__ __forceinline__ int block_excl_scan_int(int v, int& total, int* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kWarps ? sw[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kWarps) sw[kWarps + lane] = t;
+  }
+  __syncthreads();
+  total = sw[2 * kWarps - 1];
+  const int ex = x - v + (w ? sw[kWarps + w - 1] : 0);
+  __syncthreads();
+  return ex;
+}
+
+// Per-thread view of one tile, shared by S2 and S3 (identical code =>
+// identical classification in both).
+template <int ITEMS>
+struct ThreadTile {
+  double g[ITEMS];
+  double p[ITEMS + 1];  // approximate prefix before each element (p[ITEMS]: after the last)
+  int lc[ITEMS + 1];    // nonzero count before each element, relative to cnt0
+  long long cnt0;       // nonzero count before the first element
+  int uniform_e;        // binade of the whole chunk (fast path) or kNoBinade
+  Piece agg;            // the chunk's aggregate piece
+  int nwin;             // windows in the chunk
+  Piece carry;          // exclusive segmented prefix for this thread
+  int win_excl;         // windows before this thread's first element
+  int win_total;        // windows in the tile
+};
+
+struct ScanScratch {
+  SumCnt sc[2 * kWarps];
+  Piece pc[2 * kWarps];
+  int si[2 * kWarps];
+};
+
+// Fast-path rounding of one element in a known binade: delta for even /
+// odd m (identical unless g/u ends in exactly one half).
+__device__ __forceinline__ void run_delta(double g, double scale, long long& d0, long long& d1) {
+  const double v = g * scale;
+  const double q = floor(v);
+  const double f = v - q;
+  const long long qi = static_cast<long long>(q);
+  if (f < 0.5) {
+    d0 = d1 = qi;
+  } else if (f > 0.5) {
+    d0 = d1 = qi + 1;
+  } else {
+    d0 = qi + (qi & 1);
+    d1 = qi + ((1 + qi) & 1);
+  }
+}
+
+// Classification of element i against the approximate prefix (general path).
+template <int ITEMS>
+__device__ __forceinline__ int classify_at(const ThreadTile<ITEMS>& tt, int i, Piece& pc) {
+  return classify(tt.g[i], tt.p[i], tt.cnt0 + tt.lc[i], tt.p[i + 1], tt.cnt0 + tt.lc[i + 1], pc);
+}
+
+// Chunk analysis given p[0] and cnt0: prefix, fast-path test, aggregate.
+// Fast path: when [p0 - E, p_end + E] lies in one binade, every nonzero
+// element is a run element of that binade (the per-element bounds are
+// nested inside), so the per-element classification would agree.
+template <int ITEMS>
+__device__ __forceinline__ void chunk_analyse(ThreadTile<ITEMS>& tt) {
+  tt.lc[0] = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    tt.p[i + 1] = tt.p[i] + tt.g[i];
+    tt.lc[i + 1] = tt.lc[i] + (tt.g[i] != 0.0);
+  }
+  tt.uniform_e = kNoBinade;
+  tt.agg = piece_identity();
+  tt.nwin = 0;
+  if (tt.lc[ITEMS] == 0) return;  // all zero: identity
+  const double E = sum_bound(tt.p[ITEMS], tt.cnt0 + tt.lc[ITEMS]);
+  const int e_lo = binade_of(tt.p[0] - E);
+  const int e_hi = binade_of(tt.p[ITEMS] + E);
+  if (e_lo == e_hi) {
+    tt.uniform_e = e_lo;
+    const double scale = scale2(1.0, 52 - e_lo);
+    long long s0 = 0, s1 = 0;
+    bool tie = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      long long d0, d1;
+      run_delta(tt.g[i], scale, d0, d1);
+      tie |= (d0 != d1);
+      s0 += d0;
+      s1 += d1;
+    }
+    if (!tie) {
+      tt.agg = Piece{s0, s1, e_lo, 0};
+      return;
+    }
+    Piece a = piece_identity();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      Piece pc = piece_identity();
+      if (tt.g[i] != 0.0) {
+        run_delta(tt.g[i], scale, pc.d0, pc.d1);
+        pc.e = e_lo;
+      }
+      a = piece_combine(a, pc);
+    }
+    tt.agg = a;
+    return;
+  }
+  Piece a = piece_identity();
+  int nw = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    Piece pc;
+    nw += (classify_at(tt, i, pc) == 2);
+    a = piece_combine(a, pc);
+  }
+  tt.agg = a;
+  tt.nwin = nw;
+}
+
+// One 16-byte look-back descriptor per tile: {approx sum, count:30 | kind:2
+// | epoch}. 16-byte aligned accesses are single-copy atomic.
+struct __align__(16) LookBack {
+  double s;
+  unsigned cnt;
+  unsigned tag;  // (epoch << 2) | kind, kind 1 = aggregate, 2 = inclusive
+};
+
+__device__ __forceinline__ void lb_store(LookBack* p, double s, unsigned cnt, unsigned tag) {
+  const unsigned long long lo = static_cast<unsigned long long>(__double_as_longlong(s));
+  const unsigned long long hi = (static_cast<unsigned long long>(tag) << 32) | cnt;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ LookBack lb_load(const LookBack* p) {
+  unsigned long long lo, hi;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+  LookBack r;
+  r.s = __longlong_as_double(static_cast<long long>(lo));
+  r.cnt = static_cast<unsigned>(hi & 0xffffffffu);
+  r.tag = static_cast<unsigned>(hi >> 32);
+  return r;
+}
+
+constexpr int kResolveWin = 512;  // windows staged in smem by the resolver
+
+struct ResolverSmem {
+  TileWin win[kResolveWin];
+  TileHdr hdr[kThreads];
+  Piece excl[kThreads];
+  double out[kThreads];
+  double in[kThreads];
+  int wlist[kThreads];
+  double carry, next;
+  int bad;
+};
+
+template <int ITEMS>
+union PiecesSmem {
+  double g[TileCfg<ITEMS>::kSmem];
+  ResolverSmem rs;
+};
+
+// S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
+// once; approximate tile prefix by decoupled look-back; classification and
+// tile records (window list + segment aggregates). The last block resolves
+// the exact chain over all tiles: a segmented monoid scan across window-free
+// tiles and an in-order IEEE walk over the windows only, with everything the
+// walk touches staged in shared memory.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
+  using TC = TileCfg<ITEMS>;
+  __shared__ PiecesSmem<ITEMS> sm;
+  __shared__ ScanScratch sw;
+  __shared__ int s_tile, s_last;
+  __shared__ double s_pre;
+  __shared__ long long s_cpre;
+  if (grid_error(c)) return;
+  const unsigned epoch = static_cast<unsigned>(c.st->scan_epoch);
+  if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&c.cnt_scan[2], 1u));
+  __syncthreads();
+  const int t = s_tile;  // dynamic tile id: predecessors are already running
+  const long long base = static_cast<long long>(t) * TC::kTileT;
+  const double lse = c.st->lse_g;
+  ThreadTile<ITEMS> tt;
+#pragma unroll 4
+  for (int i = 0; i < ITEMS; ++i) {
+    const int e = i * kThreads + threadIdx.x;
+    const long long k = base + e;
+    double g = 0.0;
+    if (k < c.N) {
+      g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
+      c.g[k] = g;
+    }
+    sm.g[TC::sidx(e)] = g;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) tt.g[i] = sm.g[TC::sidx(threadIdx.x * ITEMS + i)];
+  SumCnt mine{0.0, 0};
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    mine.s += tt.g[i];
+    mine.c += (tt.g[i] != 0.0);
+  }
+  SumCnt tot;
+  const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
+  if (threadIdx.x == 0) {
+    // decoupled look-back over approximate (any-order) tile sums
+    LookBack* lb = c.lookback;
+    double pre = 0.0;
+    long long cpre = 0;
+    if (t == 0) {
+      lb_store(lb + t, tot.s, static_cast<unsigned>(tot.c), ((epoch + 1) << 2) | 2u);
+    } else {
+      lb_store(lb + t, tot.s, static_cast<unsigned>(tot.c), ((epoch + 1) << 2) | 1u);
+      int k = t - 1;
+      while (true) {
+        const LookBack v = lb_load(lb + k);
+        if ((v.tag >> 2) != epoch + 1) continue;  // not yet published this step
+        pre += v.s;
+        cpre += v.cnt;
+        if ((v.tag & 3u) == 2u) break;
+        --k;
+      }
+      lb_store(lb + t, pre + tot.s, static_cast<unsigned>(cpre + tot.c), ((epoch + 1) << 2) | 2u);
+    }
+    s_pre = pre;
+    s_cpre = cpre;
+  }
+  __syncthreads();
+  tt.p[0] = s_pre + ex.s;
+  tt.cnt0 = s_cpre + ex.c;
+  chunk_analyse<ITEMS>(tt);
+  tt.carry = block_excl_scan_piece(tt.agg, sw.pc);
+  tt.win_excl = block_excl_scan_int(tt.nwin, tt.win_total, sw.si);
+  const bool overflow = tt.win_total > kMaxWin;
+  if (tt.nwin > 0 && !overflow) {
+    Piece acc = tt.carry;
+    int w = tt.win_excl;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      Piece pc;
+      const int kind = classify_at(tt, i, pc);
+      if (kind == 2) {
+        TileWin tw;
+        tw.g = tt.g[i];
+        tw.e = acc.e;
+        tw.local = threadIdx.x * ITEMS + i;
+        tw.d0 = acc.d0;
+        tw.d1 = acc.d1;
+        c.win[static_cast<size_t>(t) * kMaxWin + w] = tw;
+        ++w;
+      }
+      acc = piece_combine(acc, pc);
+    }
   }
   if (threadIdx.x == kThreads - 1) {
+    const Piece acc = piece_combine(tt.carry, tt.agg);
     TileHdr h;
-    h.nwin = overflow ? -1 : ts.win_total;
+    h.nwin = overflow ? -1 : tt.win_total;
     h.tail_e = acc.e;
     h.tail_d0 = acc.d0;
     h.tail_d1 = acc.d1;
     c.hdr[t] = h;
+    c.tile_pre[t] = s_pre;
+    c.tile_cnt_pre[t] = s_cpre;
   }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
     s_last = (old == gridDim.x - 1);
-    if (s_last) c.cnt_scan[1] = 0;
+    if (s_last) {
+      c.cnt_scan[1] = 0;
+      c.cnt_scan[2] = 0;
+    }
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ---- resolver: one thread walks the tiles in order -----------------
+
+  // ---------------- resolver (one block), chunks of kThreads tiles --------
+  ResolverSmem& rs = sm.rs;
   if (threadIdx.x == 0) {
-    const double lse = c.st->lse_g;
-    double s = 0.0;
-    bool ok = true;
-    for (int tt = 0; tt < c.ntiles; ++tt) {
-      c.tile_start[tt] = s;
-      const int nwin = __ldcg(&c.hdr[tt].nwin);
-      if (nwin < 0) {
-        // serial tile: plain IEEE sequential sum, writes the CDF directly
-        const long long base = static_cast<long long>(tt) * kTile;
-        for (int e = 0; e < kTile && base + e < c.N; ++e) {
-          s = s + fitness_of(c, base + e, lse);
-          c.cdf[base + e] = s;
-        }
-      } else {
-        for (int wi = 0; wi < nwin; ++wi) {
-          const TileWin* tw = c.win + static_cast<size_t>(tt) * kMaxWin + wi;
-          Piece a;
-          a.e = __ldcg(&tw->e);
-          a.d0 = __ldcg(&tw->d0);
-          a.d1 = __ldcg(&tw->d1);
-          a.flag = 0;
-          ok &= piece_apply(a, s);
-          s = s + __ldcg(&tw->g);
-          c.win_after[static_cast<size_t>(tt) * kMaxWin + wi] = s;
-        }
-        Piece a;
-        a.e = __ldcg(&c.hdr[tt].tail_e);
-        a.d0 = __ldcg(&c.hdr[tt].tail_d0);
-        a.d1 = __ldcg(&c.hdr[tt].tail_d1);
-        a.flag = 0;
-        ok &= piece_apply(a, s);
-      }
-      c.tile_end[tt] = s;
+    rs.carry = 0.0;
+    rs.bad = 0;
+  }
+  __syncthreads();
+  for (int b0 = 0; b0 < c.ntiles; b0 += kThreads) {
+    const int ti = b0 + threadIdx.x;
+    const bool valid = ti < c.ntiles;
+    TileHdr h{0, kNoBinade, 0, 0};
+    if (valid) {
+      h.nwin = __ldcg(&c.hdr[ti].nwin);
+      h.tail_e = __ldcg(&c.hdr[ti].tail_e);
+      h.tail_d0 = __ldcg(&c.hdr[ti].tail_d0);
+      h.tail_d1 = __ldcg(&c.hdr[ti].tail_d1);
     }
-    c.st->total_mass = s;
-    // guard the last bin (filter.cpp:168)
-    c.tile_end[c.ntiles - 1] = (s < 1.0) ? 1.0 : s;
-    if (!ok) atomicOr(&c.st->error, kErrInternal);
+    const bool windowed = valid && h.nwin != 0;
+    const Piece agg{h.tail_d0, h.tail_d1, h.tail_e, 0};
+    const Piece mine_p = windowed ? Piece{0, 0, kNoBinade, 1} : agg;
+    const Piece excl = block_excl_scan_piece(mine_p, sw.pc);
+    int nwt, nws;
+    const int rank = block_excl_scan_int(windowed ? 1 : 0, nwt, sw.si);
+    const int wofs = block_excl_scan_int(windowed && h.nwin > 0 ? h.nwin : 0, nws, sw.si);
+    if (windowed) {
+      rs.wlist[rank] = ti;
+      rs.excl[rank] = excl;
+      rs.hdr[rank] = h;
+      for (int k = 0; k < h.nwin && wofs + k < kResolveWin; ++k)
+        rs.win[wofs + k] = c.win[static_cast<size_t>(ti) * kMaxWin + k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // in-order IEEE walk over the windowed tiles of this chunk
+      double seg = rs.carry;
+      int wo = 0;
+      bool ok = true;
+      for (int r = 0; r < nwt; ++r) {
+        const int wt = rs.wlist[r];
+        const TileHdr wh = rs.hdr[r];
+        double s = seg;
+        ok &= piece_apply(rs.excl[r], s);
+        rs.in[r] = s;
+        if (wh.nwin < 0) {
+          // serial tile (window overflow): plain sequential sum, CDF written here
+          const long long tb = static_cast<long long>(wt) * TC::kTileT;
+          for (int e = 0; e < TC::kTileT && tb + e < c.N; ++e) {
+            s = s + __ldcg(&c.g[tb + e]);
+            c.cdf[tb + e] = s;
+          }
+        } else {
+          for (int k = 0; k < wh.nwin; ++k, ++wo) {
+            TileWin tw;
+            if (wo < kResolveWin) {
+              tw = rs.win[wo];
+            } else {
+              const TileWin* gw = c.win + static_cast<size_t>(wt) * kMaxWin + k;
+              tw.g = __ldcg(&gw->g);
+              tw.e = __ldcg(&gw->e);
+              tw.d0 = __ldcg(&gw->d0);
+              tw.d1 = __ldcg(&gw->d1);
+            }
+            ok &= piece_apply(Piece{tw.d0, tw.d1, tw.e, 0}, s);
+            s = s + tw.g;  // the window element: a real IEEE add, as acc += g[i]
+            c.win_after[static_cast<size_t>(wt) * kMaxWin + k] = s;
+          }
+          ok &= piece_apply(Piece{wh.tail_d0, wh.tail_d1, wh.tail_e, 0}, s);
+        }
+        rs.out[r] = s;
+        seg = s;
+      }
+      if (!ok) rs.bad = 1;
+    }
+    __syncthreads();
+    if (valid) {
+      double s_in, s_end;
+      if (windowed) {
+        s_in = rs.in[rank];
+        s_end = rs.out[rank];
+      } else {
+        s_in = rank > 0 ? rs.out[rank - 1] : rs.carry;
+        bool ok = piece_apply(excl, s_in);
+        s_end = s_in;
+        ok &= piece_apply(agg, s_end);
+        if (!ok) rs.bad = 1;
+      }
+      if (ti == c.ntiles - 1) {
+        c.st->total_mass = s_end;
+        s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
+      }
+      c.tile_info[ti] = make_double2(s_in, s_end);
+      if (threadIdx.x == min(kThreads, c.ntiles - b0) - 1) rs.next = s_end;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rs.carry = rs.next;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (rs.bad) atomicOr(&c.st->error, kErrInternal);
+    c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
   }
 }
 
 // S3: exact per-element CDF, per-tile local guide and the coarse guide.
+template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
-  __shared__ double sg[kSmemTile];
-  __shared__ DD sdd[kThreads];
-  __shared__ long long scnt[kThreads];
-  __shared__ Piece spc[kThreads];
-  __shared__ int si[kThreads];
+  using TC = TileCfg<ITEMS>;
+  __shared__ double sg[TC::kSmem];
+  __shared__ ScanScratch sw;
   if (grid_error(c)) return;
   const int t = blockIdx.x;
-  const long long base = static_cast<long long>(t) * kTile;
-  load_tile_g(c, t, sg);
+  const long long base = static_cast<long long>(t) * TC::kTileT;
   const int nwin = __ldcg(&c.hdr[t].nwin);
-  const double c_start = __ldcg(&c.tile_start[t]);
-  const double c_end = __ldcg(&c.tile_end[t]);
-  if (nwin >= 0) {
-    TileScan ts;
-    analyse_tile(c, t, sg, ts, sdd, scnt, spc, si);
-    DD P = ts.p0;
-    long long C = ts.c0;
-    Piece acc = ts.carry;
-    int w = ts.win_excl;
-    double seg = w > 0 ? __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w - 1]) : c_start;
-    double vals[kItems];
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const int e = threadIdx.x * kItems + i;
-      const double g = sg[sidx(e)];
-      const DD pp = P;
-      const long long cp = C;
-      P = dd_add(P, g);
-      C += (g != 0.0);
-      Piece pc;
-      const int kind = classify(g, pp, cp, P, C, pc);
-      acc = piece_combine(acc, pc);
-      double sk;
-      if (kind == 2) {
-        seg = __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w]);
-        ++w;
-        sk = seg;
-      } else {
-        sk = seg;
-        piece_apply(acc, sk);
-      }
-      vals[i] = sk;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) sg[sidx(threadIdx.x * kItems + i)] = vals[i];
-    __syncthreads();
-  } else {
-    __syncthreads();
+  const double2 ti = __ldcg(&c.tile_info[t]);
+  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
+  ThreadTile<ITEMS> tt;
 #pragma unroll 4
-    for (int i = 0; i < kItems; ++i) {
-      const int e = i * kThreads + threadIdx.x;
-      sg[sidx(e)] = base + e < c.N ? __ldcg(&c.cdf[base + e]) : 0.0;
-    }
-    __syncthreads();
-  }
-  // guard + padding beyond N, then write the CDF (coalesced)
-  const int valid = static_cast<int>(min(static_cast<long long>(kTile), c.N - base));
-#pragma unroll 4
-  for (int i = 0; i < kItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int e = i * kThreads + threadIdx.x;
-    double v = sg[sidx(e)];
+    sg[TC::sidx(e)] = e < valid ? __ldcg(&c.g[base + e]) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) tt.g[i] = sg[TC::sidx(threadIdx.x * ITEMS + i)];
+  double vals[ITEMS];
+  if (nwin >= 0) {
+    SumCnt mine{0.0, 0};
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      mine.s += tt.g[i];
+      mine.c += (tt.g[i] != 0.0);
+    }
+    SumCnt tot;
+    const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
+    tt.p[0] = __ldcg(&c.tile_pre[t]) + ex.s;
+    tt.cnt0 = __ldcg(&c.tile_cnt_pre[t]) + ex.c;
+    chunk_analyse<ITEMS>(tt);
+    tt.carry = block_excl_scan_piece(tt.agg, sw.pc);
+    tt.win_excl = block_excl_scan_int(tt.nwin, tt.win_total, sw.si);
+    int w = tt.win_excl;
+    double seg = w > 0 ? __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w - 1]) : ti.x;
+    if (tt.uniform_e != kNoBinade || tt.lc[ITEMS] == 0) {
+      // no window in this chunk: one exact base value, then integer steps
+      double s0 = seg;
+      piece_apply(tt.carry, s0);
+      if (tt.lc[ITEMS] == 0) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
+      } else {
+        const int e = tt.uniform_e;
+        const double scale = scale2(1.0, 52 - e);
+        long long m = static_cast<long long>(scale2(s0, 52 - e));
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (tt.g[i] != 0.0) {
+            long long d0, d1;
+            run_delta(tt.g[i], scale, d0, d1);
+            m += (m & 1) ? d1 : d0;
+          }
+          vals[i] = scale2(static_cast<double>(m), e - 52);
+        }
+      }
+    } else {
+      Piece acc = tt.carry;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        Piece pc;
+        const int kind = classify_at(tt, i, pc);
+        acc = piece_combine(acc, pc);
+        double sk = seg;
+        if (kind == 2) {
+          seg = __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w]);
+          ++w;
+          sk = seg;
+        } else {
+          piece_apply(acc, sk);
+        }
+        vals[i] = sk;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = threadIdx.x * ITEMS + i;
+      vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int e = threadIdx.x * ITEMS + i;
+    double v = vals[i];
     if (base + e == c.N - 1) v = (v < 1.0) ? 1.0 : v;  // filter.cpp:168
     if (e >= valid) v = INFINITY;
-    sg[sidx(e)] = v;
+    sg[TC::sidx(e)] = v;
   }
   __syncthreads();
 #pragma unroll 4
-  for (int i = 0; i < kItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int e = i * kThreads + threadIdx.x;
-    if (e < valid) c.cdf[base + e] = sg[sidx(e)];
+    if (e < valid) c.cdf[base + e] = sg[TC::sidx(e)];
   }
-  // local guide: bucket i edge x_i = c_start + i*w; first local k with cdf > x_i
-  const double wdt = (c_end - c_start) * (1.0 / kTile);
-  for (int i = threadIdx.x; i < kTile; i += kThreads) {
-    const double x = c_start + static_cast<double>(i) * wdt;
+  // local guide: bucket i edge x_i = start + i*w; first local k with cdf > x_i.
+  // Thread t owns ITEMS consecutive buckets: one binary search, then a walk.
+  const double wdt = (ti.y - ti.x) * (1.0 / TC::kTileT);
+  {
+    const int i0 = threadIdx.x * ITEMS;
+    const double x0 = ti.x + static_cast<double>(i0) * wdt;
     int lo = 0, len = valid;
     while (len > 0) {
       const int half = len >> 1;
-      if (!(x < sg[sidx(lo + half)])) {
+      if (!(x0 < sg[TC::sidx(lo + half)])) {
         lo += half + 1;
         len -= half + 1;
       } else {
         len = half;
       }
     }
-    c.lguide[base + i] = static_cast<unsigned short>(min(lo, valid - 1));
+    unsigned packed[ITEMS / 2];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const double x = ti.x + static_cast<double>(i0 + i) * wdt;
+      while (lo < valid && !(x < sg[TC::sidx(lo)])) ++lo;
+      const unsigned v = static_cast<unsigned>(min(lo, valid - 1));
+      if (i & 1)
+        packed[i >> 1] |= v << 16;
+      else
+        packed[i >> 1] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < ITEMS / 8; ++q)
+      reinterpret_cast<uint4*>(c.lguide + base + i0)[q] =
+          make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
   }
-  // coarse guide: buckets b with c_start <= b/B1 < c_end point at this tile
-  const double B1 = ldexp(1.0, c.coarse_bits);
+  // coarse guide: buckets b with start <= b/B1 < end point at this tile
+  const double B1 = scale2(1.0, c.coarse_bits);
   const long long nb = 1LL << c.coarse_bits;
-  long long b_lo = static_cast<long long>(ceil(c_start * B1));
-  long long b_hi = static_cast<long long>(ceil(fmin(c_end, 1.0) * B1)) - 1;
-  if (c_end >= 1.0) b_hi = nb - 1;
+  long long b_lo = static_cast<long long>(ceil(ti.x * B1));
+  long long b_hi = ti.y >= 1.0 ? nb - 1 : static_cast<long long>(ceil(ti.y * B1)) - 1;
   b_lo = max(b_lo, 0LL);
   b_hi = min(b_hi, nb - 1);
   for (long long b = b_lo + threadIdx.x; b <= b_hi; b += kThreads) c.coarse[b] = t;
+}
+
+void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
+  const bool small = c.tile_log2 == 11;
+  if (which == 1) {
+    if (small) k_scan_pieces<8><<<ntiles, kThreads, 0, st>>>(c);
+    else k_scan_pieces<16><<<ntiles, kThreads, 0, st>>>(c);
+  } else {
+    if (small) k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
+    else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
@@ -492,8 +714,8 @@ struct NumericalError : std::runtime_error {
                                #x);                                                      \
   } while (0)
 
-static const char* kKernelNames = "k_predict,k_scan_sums,k_scan_pieces,k_scan_cdf,k_update";
-constexpr int kNumKernels = 5;
+static const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_update";
+constexpr int kNumKernels = 4;
 
 }  // namespace pfsmc_gpu
 
@@ -629,14 +851,12 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   }
   s->ks->predict(c, s->grid, st);
   if (timed) CK(cudaEventRecord(ev[1], st));
-  k_scan_sums<<<s->ntiles, kThreads, 0, st>>>(c);
+  launch_scan(c, s->ntiles, st, 1);
   if (timed) CK(cudaEventRecord(ev[2], st));
-  k_scan_pieces<<<s->ntiles, kThreads, 0, st>>>(c);
+  launch_scan(c, s->ntiles, st, 2);
   if (timed) CK(cudaEventRecord(ev[3], st));
-  k_scan_cdf<<<s->ntiles, kThreads, 0, st>>>(c);
-  if (timed) CK(cudaEventRecord(ev[4], st));
   s->ks->update(c, s->grid, st);
-  if (timed) CK(cudaEventRecord(ev[5], st));
+  if (timed) CK(cudaEventRecord(ev[4], st));
   CK(cudaGetLastError());
 }
 
@@ -733,7 +953,8 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->N = static_cast<long long>(cfg->particles);
     s->grid = static_cast<int>((s->N + kThreads - 1) / kThreads);
-    s->ntiles = static_cast<int>((s->N + kTile - 1) / kTile);
+    const int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
+    s->ntiles = static_cast<int>((s->N + (1LL << tile_log2) - 1) >> tile_log2);
     Ctx& c = s->ctx;
     c.N = static_cast<int>(s->N);
     c.R = ((s->d + s->p + 1) / 2) * 2;
@@ -760,13 +981,14 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     c.lg = s->dalloc<double>(N);
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
-    c.lguide = s->dalloc<unsigned short>(NT * kTile);
+    c.tile_log2 = tile_log2;
+    c.lguide = s->dalloc<unsigned short>(NT << tile_log2);
     c.coarse = s->dalloc<unsigned>(size_t(1) << cb);
-    c.tile_start = s->dalloc<double>(NT);
-    c.tile_end = s->dalloc<double>(NT);
-    c.tile_sum = s->dalloc<DD>(NT);
-    c.tile_cnt = s->dalloc<long long>(NT);
-    c.tile_pre = s->dalloc<DD>(NT);
+    c.tile_info = s->dalloc<double2>(NT);
+    c.g = s->dalloc<double>(N);
+    c.lookback = s->dalloc<LookBack>(NT);
+    CK(cudaMemset(c.lookback, 0, sizeof(LookBack) * NT));
+    c.tile_pre = s->dalloc<double>(NT);
     c.tile_cnt_pre = s->dalloc<long long>(NT);
     c.hdr = s->dalloc<TileHdr>(NT);
     c.win = s->dalloc<TileWin>(NT * kMaxWin);
@@ -1023,9 +1245,8 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
     Ctx c = s->ctx;
     c.gin = dg;
-    k_scan_sums<<<s->ntiles, kThreads, 0, s->stream>>>(c);
-    k_scan_pieces<<<s->ntiles, kThreads, 0, s->stream>>>(c);
-    k_scan_cdf<<<s->ntiles, kThreads, 0, s->stream>>>(c);
+    launch_scan(c, s->ntiles, s->stream, 1);
+    launch_scan(c, s->ntiles, s->stream, 2);
     k_search_only<<<s->grid, kThreads, 0, s->stream>>>(c);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ancestors_out, c.anc, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, s->stream));

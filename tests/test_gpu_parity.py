@@ -242,7 +242,7 @@ def test_lockstep_chain_bdf3():
 def test_lockstep_robertson_lognormal():
     from paper_1411_1702_b200 import problems
     n = 4096
-    prob = problems.robertson(particles=n, T=6, seed=4)
+    prob = problems.robertson(particles=n, T=400, seed=4)  # first 6 of the 400 log-spaced times
     sc = StepConfig(model="robertson", family="bdf", order=2, a=0.99, seed=4, obs_idx=(0, 2), sigma=0.02,
                     newton_max_iter=4, likelihood="lognormal")
     ens = O.init_gaussian("robertson", n, 4, prob.prior["th_mu"], prob.prior["th_sigma"], prob.prior["x_mean"],
