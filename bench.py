@@ -37,12 +37,13 @@ T_OBS = 1000
 D, P = 2, 2
 F = D + P + 1
 STEP_BYTES = 24 * F + 56                     # whole step, minimal fused pipeline
+R = D + P                                     # record doubles (x, theta_u)
 KERNEL_BYTES = {                              # per particle per launch
-    "k_predict": 8 * (D + P) + 8 + 8 + 8,     # record + lw in; ll_bar + lg out
-    "k_scan_sums": 8,                         # lg in
-    "k_scan_pieces": 8,                       # lg in
-    "k_scan_cdf": 8 + 8 + 2,                  # lg in; cdf + local guide out
-    "k_update": 8 * (D + P) + 8 + 8 * (D + P) + 8 + 4,  # gather rec + ll_bar; rec + lw + anc out
+    "k_predict": 8 * R + 8 + 8 + 8,           # record + lw in; ll_bar + lg out
+    "k_scan_pieces": 8 + 8,                   # lg in; g out
+    "k_scan_cdf": 8 + 8 + 2,                  # g in; cdf + local guide out
+    "k_serve": 8 * R + 8 + 8 * (R + 2) + 4,   # ancestor record + ll_bar gathered; payload + anc out
+    "k_update": 8 * (R + 2) + 8 * R + 8,      # payload in; record + lw out
 }
 
 
@@ -270,7 +271,7 @@ def main():
             "step_roofline": {"bytes_per_particle": STEP_BYTES, "achieved": step_gbs, "peak": hbm,
                               "frac": step_gbs / hbm},
             "kernel_ms_per_step": {k: v / args.steps for k, v in kt.items()},
-            "gpu_launches": 5 * args.steps,
+            "gpu_launches": len(kt) * args.steps,
             "e2e": e2e, "clocks": clk.summary(),
             "final_trace": {"theta_mean": list(map(float, last[:P])), "ess": float(last[-1])}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

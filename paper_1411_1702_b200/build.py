@@ -58,6 +58,18 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    # the C++ drop-in example over include/pfsmc_gpu.hpp (exercised by a GPU test)
+    root = os.path.dirname(HERE)
+    ex_src = os.path.join(root, "examples", "drop_in_lv.cpp")
+    ex_bin = os.path.join(root, "examples", "drop_in_lv")
+    if os.path.exists(ex_src) and (not os.path.exists(ex_bin)
+                                   or os.path.getmtime(ex_bin) < max(os.path.getmtime(ex_src),
+                                                                     os.path.getmtime(LIB))):
+        cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"), ex_src, "-o", ex_bin,
+               "-L", HERE, "-lpfsmc_gpu", "-Wl,-rpath,$ORIGIN/../paper_1411_1702_b200"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed:\n{r.stderr}")
     if verbose:
         print(f"[build] {LIB}")
     return LIB

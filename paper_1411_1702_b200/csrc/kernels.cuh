@@ -72,6 +72,7 @@ struct Ctx {
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
   double* rec[2];
+  double* payload;     // slot-ordered ancestor payloads {record, ll_bar, index} (R + 2 doubles)
   double* lw;
   double* llbar;
   double* lg;
@@ -366,18 +367,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_update(Ctx c) {
   const int cur = st.cur;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
   double lwv = kNegInf;
-  double vals[V];
+  double vals[V];  // moment leaf
 #pragma unroll
   for (int k = 0; k < V; ++k) vals[k] = 0.0;
   int iters = 0;
   if (n < c.N) {
-    // survival of the fittest (filter.cpp:169-176)
-    const double u = resample_uniform(c.seed, sp.j, n);
-    const unsigned anc = find_ancestor(c, u);
-    c.anc[n] = anc;
+    // survival of the fittest (filter.cpp:169-176): the ancestor's record and
+    // ll_bar were gathered into slot order by k_serve (coalesced read here)
     double x[D], tu[P], tb[P], th[P], gamma[D];
-    load_record<M>(c.rec[cur], c.R, anc, x, tu);
-    const double llb = __ldg(&c.llbar[anc]);
+    load_record<M>(c.payload, c.R + 2, n, x, tu);
+    const double llb = __ldg(&c.payload[n * (c.R + 2) + c.R]);
     // shrink of the ancestor (filter.cpp:118), proliferation (filter.cpp:185-196)
     double z[P];
     stream_normals<P>(c.seed, sp.j, n, kProliferate, z);

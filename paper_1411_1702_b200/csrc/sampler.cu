@@ -668,6 +668,25 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
   }
 }
 
+// Survival of the fittest (filter.cpp:169-176, 330-335): slot n draws its
+// uniform, finds its ancestor in the exact CDF and gathers the ancestor's
+// record and predictor log-likelihood into slot order, so K3 streams them
+// coalesced. Latency-bound (dependent random loads), so it runs as its own
+// small-footprint, high-occupancy kernel.
+__global__ void __launch_bounds__(kThreads) k_serve(Ctx c) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const double u = resample_uniform(c.seed, c.sp->j, n);
+  const unsigned a = find_ancestor(c, u);
+  c.anc[n] = a;
+  const int W = c.R + 2;
+  const double2* src = reinterpret_cast<const double2*>(c.rec[c.st->cur] + static_cast<long long>(a) * c.R);
+  double2* dst = reinterpret_cast<double2*>(c.payload + n * W);
+  for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
+  dst[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(a));
+}
+
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
@@ -714,8 +733,8 @@ struct NumericalError : std::runtime_error {
                                #x);                                                      \
   } while (0)
 
-static const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_update";
-constexpr int kNumKernels = 4;
+static const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_serve,k_update";
+constexpr int kNumKernels = 5;
 
 }  // namespace pfsmc_gpu
 
@@ -855,8 +874,10 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   if (timed) CK(cudaEventRecord(ev[2], st));
   launch_scan(c, s->ntiles, st, 2);
   if (timed) CK(cudaEventRecord(ev[3], st));
-  s->ks->update(c, s->grid, st);
+  k_serve<<<s->grid, kThreads, 0, st>>>(c);
   if (timed) CK(cudaEventRecord(ev[4], st));
+  s->ks->update(c, s->grid, st);
+  if (timed) CK(cudaEventRecord(ev[5], st));
   CK(cudaGetLastError());
 }
 
@@ -976,6 +997,7 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     const size_t NT = static_cast<size_t>(s->ntiles);
     c.rec[0] = s->dalloc<double>(N * c.R);
     c.rec[1] = s->dalloc<double>(N * c.R);
+    c.payload = s->dalloc<double>(N * (c.R + 2));
     c.lw = s->dalloc<double>(N);
     c.llbar = s->dalloc<double>(N);
     c.lg = s->dalloc<double>(N);

@@ -330,3 +330,25 @@ def test_run_matches_oracle_loop():
         assert _rel(tr, trace_o) < REL_TRACE, j
         tp = prob.times[j - 1]
     gpu.close()
+
+
+def test_cpp_drop_in_example_matches_oracle():
+    """The C++ mirror (include/pfsmc_gpu.hpp) used as a pf_step call-site
+    replacement: trace rows agree with the oracle run from the same prior."""
+    import subprocess
+    from paper_1411_1702_b200 import problems
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "drop_in_lv")
+    n, T, seed = 4096, 5, 7
+    prob = problems.lotka_volterra(particles=n, T=T, seed=seed)
+    inp = "\n".join(f"{float(a)!r} {float(b)!r}" for a, b in prob.ys) + "\n"
+    out = subprocess.run([exe, str(n), str(T), str(seed)], input=inp, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    rows = [list(map(float, ln.split()[1:])) for ln in out.stdout.strip().splitlines()]
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=seed, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, seed, **prob.prior)
+    tp = 0.0
+    for j in range(1, T + 1):
+        trace_o, _ = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, prob.times[j - 1])
+        assert _rel(np.array(rows[j - 1]), trace_o) < REL_TRACE, j
+        tp = prob.times[j - 1]
