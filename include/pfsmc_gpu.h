@@ -157,6 +157,40 @@ pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, in
  * the sampler's stream. */
 pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s);
 
+/* ------------------------------------------------------------------------
+ * Multi-GPU sharding. One handle per GPU owns the global
+ * slots [rank*N/world, (rank+1)*N/world) of the N = cfg.particles global
+ * particles (N a multiple of world * 16384); every keyed stream uses the
+ * global slot, so the sharded filter draws exactly the single-handle numbers
+ * and reproduces its results bit for bit. The host orchestrator
+ * (paper_1411_1702_b200/sharded.py) runs, per step:
+ *   shard_predict -> allgather buf 0 into 1 -> shard_finish_lse
+ *   shard_scan_sums -> allgather buf 2 into 3 -> shard_scan_records
+ *   allgather the own slices of bufs 4, 5 -> shard_resolve
+ *   shard_serve (counts) -> exchange payloads buf 8 -> buf 9 -> shard_update
+ *   allgather buf 6 into 7 -> shard_finish_moments(7)
+ * i.e. the only cross-GPU traffic is the global log-sum-exp, the tile records
+ * of the exact CDF, the ancestor payloads and the moment partials. */
+pfsmc_gpu_status pfsmc_gpu_create_shard(const pfsmc_gpu_config* cfg, int rank, int world,
+                                        pfsmc_gpu_sampler** out);
+/* Device pointer + size of exchange buffer `which` (see the sequence above;
+ * 4/5 are global arrays whose own slice starts at rank * bytes / world). */
+pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** ptr,
+                                        uint64_t* bytes);
+pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
+                                         double t_prev, double t_obs, double h);
+pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_scan_sums(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s);
+/* counts_out: world send counts then world receive counts (payloads of
+ * (record, ll_bar, ancestor, slot) doubles); blocking. */
+pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out);
+pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
+pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
+/* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */
+pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out);
+
 #ifdef __cplusplus
 }
 #endif

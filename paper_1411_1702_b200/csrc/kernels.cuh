@@ -97,6 +97,19 @@ struct Ctx {
   const double* gin;   // injected fitness (parity mode) or null
   DevState* st;
   const StepParams* sp;
+  // ---- sharding (one handle = one contiguous range of global slots) ----
+  long long n0;        // global index of this shard's first slot (keys every stream)
+  long long n_glob;    // global particle count
+  int sharded;         // 0: the handle is the whole filter
+  int rank, world;
+  int gntiles;         // tiles over all shards
+  int tile0;           // global index of this shard's first tile
+  TileHdr* ghdr;       // all shards' tile headers (allgathered)
+  TileWin* gwin;       // all shards' tile windows (allgathered, kMaxWin per tile)
+  double* gwin_after;  // exact sums after every window (global resolver)
+  double2* gtile_info; // exact (start, end) of every global tile
+  double* shard_sum;   // [2]: this shard's approximate g total and nonzero count (sums mode)
+  double* shard_off;   // [2]: global approximate offset and count before this shard
 };
 
 // ---------------------------------------------------------------- helpers
@@ -199,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_predict(Ctx c) {
   }
   const double one[1] = {1.0};
   block_partial<1, false>(lgv, one, c.part + blockIdx.x * 2, scratch);
-  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch)) {
+  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, !c.sharded)) {
     if (threadIdx.x == 0) {
       // logsumexp (filter.cpp:16-23) + the degeneracy check (filter.cpp:149-152)
       const double mx = fin[0];
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_update(Ctx c) {
     const double llb = __ldg(&c.payload[n * (c.R + 2) + c.R]);
     // shrink of the ancestor (filter.cpp:118), proliferation (filter.cpp:185-196)
     double z[P];
-    stream_normals<P>(c.seed, sp.j, n, kProliferate, z);
+    stream_normals<P>(c.seed, sp.j, c.n0 + n, kProliferate, z);
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       tb[r] = c.a * tu[r] + c.one_minus_a * sK[r];
@@ -398,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_update(Ctx c) {
     double ll = kNegInf;
     if (status == kOk) {
       double zi[D];
-      stream_normals<D>(c.seed, sp.j, n, kInnovate, zi);
+      stream_normals<D>(c.seed, sp.j, c.n0 + n, kInnovate, zi);
 #pragma unroll
       for (int k = 0; k < D; ++k) xr[k] += sqrt(gamma[k]) * zi[k];
       ll = loglik<M>(c, sp, xr);
@@ -433,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_update(Ctx c) {
   }
   block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch,
                          V <= 12 ? tsc : nullptr);
-  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
     if (threadIdx.x == 0) {
       double K[P];
 #pragma unroll
@@ -482,10 +495,39 @@ __global__ void __launch_bounds__(kThreads) k_moments(Ctx c, int set_cov) {
     vals[V - 1] = 1.0;
   }
   block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
-  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
     if (threadIdx.x == 0) {
       finalize_moments<M>(c, fin, K, false, set_cov != 0);
       chol_psd_device<P>(st);
+    }
+  }
+}
+
+// Sharded finishers: the same final combine as the single-handle tree
+// (combine_partials over the group partials in global order), over the
+// allgathered group partials of every shard => bitwise identical results.
+// flags: 1 = set lse_w (+ degeneracy check), 2 = set cov, 4 = chol + flip the
+// record buffer (a completed step); 0/2 are the injection / init refreshes.
+template <class M>
+__global__ void __launch_bounds__(kThreads) k_finish_moments(Ctx c, const double* gp, int ngroups,
+                                                             int flags) {
+  constexpr int P = M::P;
+  constexpr int V = MomentLayout<M>::V;
+  __shared__ double scratch[kWarps * V];
+  __shared__ double fin[V + 1];
+  if (grid_error(c)) return;
+  DevState& st = *c.st;
+  double K[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) K[k] = st.mu[k];
+  __syncthreads();
+  combine_partials<V, true>(gp, ngroups, fin, scratch);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    finalize_moments<M>(c, fin, K, (flags & 1) != 0, (flags & 2) != 0);
+    if (!(st.error & kErrUpdate)) {
+      chol_psd_device<P>(st);
+      if (flags & 4) st.cur ^= 1;
     }
   }
 }
@@ -503,7 +545,7 @@ __global__ void __launch_bounds__(kThreads) k_init(Ctx c, int kind, const double
   if (n >= c.N) return;
   // prm: gaussian: th_mu[P], th_sigma[P], x_mean[D], x_std[D], x_clamp[D]
   //      uniform : th_lo[P], th_hi[P], x_lo[D], x_hi[D]
-  Stream s(c.seed, 0, n, kInit);
+  Stream s(c.seed, 0, c.n0 + n, kInit);
   double x[D], tu[P];
   if (kind == 0) {
 #pragma unroll
@@ -532,6 +574,8 @@ struct KernelSet {
   virtual void moments(const Ctx& c, int grid, cudaStream_t s, int set_cov) = 0;
   virtual void chol(const Ctx& c, cudaStream_t s) = 0;
   virtual void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) = 0;
+  virtual void finish_moments(const Ctx& c, const double* gp, int ngroups, int flags, cudaStream_t s) = 0;
+  virtual int moment_width() const = 0;
   int d = 0, p = 0;
 };
 
@@ -554,6 +598,10 @@ struct KernelSetT final : KernelSet {
   void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) override {
     k_init<M><<<grid, kThreads, 0, s>>>(c, kind, prm, lw0);
   }
+  void finish_moments(const Ctx& c, const double* gp, int ngroups, int flags, cudaStream_t s) override {
+    k_finish_moments<M><<<1, kThreads, 0, s>>>(c, gp, ngroups, flags);
+  }
+  int moment_width() const override { return MomentLayout<M>::V + 1; }
 };
 
 template <class M, int FAM>

@@ -167,7 +167,7 @@ __device__ __forceinline__ void combine_partials(const double* in, int count, do
 template <int V, bool SQ>
 __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_part,
                                                  unsigned* counters, double* final_out,
-                                                 double* scratch) {
+                                                 double* scratch, bool final_level = true) {
   __shared__ int s_flag;
   const int nblocks = gridDim.x;
   const int ngroups = (nblocks + kGroup - 1) / kGroup;
@@ -185,6 +185,7 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __threadfence();
   combine_partials<V, SQ>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
                           group_part + g * (V + 1), scratch);
+  if (!final_level) return false;  // sharded: the group partials are exported
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -294,13 +294,128 @@ union PiecesSmem {
   ResolverSmem rs;
 };
 
+// The exact chain over tiles, one block: a segmented monoid scan across
+// window-free tiles and an in-order IEEE walk over the windows only, with
+// everything the walk touches staged in shared memory. Used for the single
+// handle (own tiles) and, sharded, for all shards' tiles on every rank.
+template <int ITEMS>
+__device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
+                              double2* tile_info, int ntiles, bool own_g, ResolverSmem& rs,
+                              ScanScratch& sw) {
+  using TC = TileCfg<ITEMS>;
+  if (threadIdx.x == 0) {
+    rs.carry = 0.0;
+    rs.bad = 0;
+  }
+  __syncthreads();
+  for (int b0 = 0; b0 < ntiles; b0 += kThreads) {
+    const int ti = b0 + threadIdx.x;
+    const bool valid = ti < ntiles;
+    TileHdr h{0, kNoBinade, 0, 0};
+    if (valid) {
+      h.nwin = __ldcg(&hdr[ti].nwin);
+      h.tail_e = __ldcg(&hdr[ti].tail_e);
+      h.tail_d0 = __ldcg(&hdr[ti].tail_d0);
+      h.tail_d1 = __ldcg(&hdr[ti].tail_d1);
+    }
+    const bool windowed = valid && h.nwin != 0;
+    const Piece agg{h.tail_d0, h.tail_d1, h.tail_e, 0};
+    const Piece mine_p = windowed ? Piece{0, 0, kNoBinade, 1} : agg;
+    const Piece excl = block_excl_scan_piece(mine_p, sw.pc);
+    int nwt, nws;
+    const int rank = block_excl_scan_int(windowed ? 1 : 0, nwt, sw.si);
+    const int wofs = block_excl_scan_int(windowed && h.nwin > 0 ? h.nwin : 0, nws, sw.si);
+    if (windowed) {
+      rs.wlist[rank] = ti;
+      rs.excl[rank] = excl;
+      rs.hdr[rank] = h;
+      for (int k = 0; k < h.nwin && wofs + k < kResolveWin; ++k)
+        rs.win[wofs + k] = win[static_cast<size_t>(ti) * kMaxWin + k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // in-order IEEE walk over the windowed tiles of this chunk
+      double seg = rs.carry;
+      int wo = 0;
+      bool ok = true;
+      for (int r = 0; r < nwt; ++r) {
+        const int wt = rs.wlist[r];
+        const TileHdr wh = rs.hdr[r];
+        double s = seg;
+        ok &= piece_apply(rs.excl[r], s);
+        rs.in[r] = s;
+        if (wh.nwin < 0 && !own_g) {
+          ok = false;  // window overflow in a remote tile: unsupported when sharded
+        } else if (wh.nwin < 0) {
+          // serial tile (window overflow): plain sequential sum, CDF written here
+          const long long tb = static_cast<long long>(wt) * TC::kTileT;
+          for (int e = 0; e < TC::kTileT && tb + e < c.N; ++e) {
+            s = s + __ldcg(&c.g[tb + e]);
+            c.cdf[tb + e] = s;
+          }
+        } else {
+          for (int k = 0; k < wh.nwin; ++k, ++wo) {
+            TileWin tw;
+            if (wo < kResolveWin) {
+              tw = rs.win[wo];
+            } else {
+              const TileWin* gw = win + static_cast<size_t>(wt) * kMaxWin + k;
+              tw.g = __ldcg(&gw->g);
+              tw.e = __ldcg(&gw->e);
+              tw.d0 = __ldcg(&gw->d0);
+              tw.d1 = __ldcg(&gw->d1);
+            }
+            ok &= piece_apply(Piece{tw.d0, tw.d1, tw.e, 0}, s);
+            s = s + tw.g;  // the window element: a real IEEE add, as acc += g[i]
+            win_after[static_cast<size_t>(wt) * kMaxWin + k] = s;
+          }
+          ok &= piece_apply(Piece{wh.tail_d0, wh.tail_d1, wh.tail_e, 0}, s);
+        }
+        rs.out[r] = s;
+        seg = s;
+      }
+      if (!ok) rs.bad = 1;
+    }
+    __syncthreads();
+    if (valid) {
+      double s_in, s_end;
+      if (windowed) {
+        s_in = rs.in[rank];
+        s_end = rs.out[rank];
+      } else {
+        s_in = rank > 0 ? rs.out[rank - 1] : rs.carry;
+        bool ok = piece_apply(excl, s_in);
+        s_end = s_in;
+        ok &= piece_apply(agg, s_end);
+        if (!ok) rs.bad = 1;
+      }
+      if (ti == ntiles - 1) {
+        c.st->total_mass = s_end;
+        s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
+      }
+      tile_info[ti] = make_double2(s_in, s_end);
+      if (threadIdx.x == min(kThreads, ntiles - b0) - 1) rs.next = s_end;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rs.carry = rs.next;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && rs.bad) atomicOr(&c.st->error, kErrInternal);
+}
+
 // S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
 // once; approximate tile prefix by decoupled look-back; classification and
 // tile records (window list + segment aggregates). The last block resolves
 // the exact chain over all tiles: a segmented monoid scan across window-free
 // tiles and an in-order IEEE walk over the windows only, with everything the
 // walk touches staged in shared memory.
-template <int ITEMS>
+// MODE 0: single handle (look-back + records + resolver).
+// MODE 1 (sharded, phase A): g, shard-local look-back prefixes, shard total.
+// MODE 2 (sharded, phase B): records against the global approximate offset
+//         (written straight into the allgather buffers); no resolver.
+enum ScanMode { kScanFull = 0, kScanSums = 1, kScanRecords = 2 };
+
+template <int ITEMS, int MODE>
 __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   using TC = TileCfg<ITEMS>;
   __shared__ PiecesSmem<ITEMS> sm;
@@ -310,9 +425,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   __shared__ long long s_cpre;
   if (grid_error(c)) return;
   const unsigned epoch = static_cast<unsigned>(c.st->scan_epoch);
-  if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&c.cnt_scan[2], 1u));
-  __syncthreads();
-  const int t = s_tile;  // dynamic tile id: predecessors are already running
+  if (MODE != kScanRecords) {
+    if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&c.cnt_scan[2], 1u));
+    __syncthreads();
+  }
+  // dynamic tile id for the look-back modes: predecessors are already running
+  const int t = MODE != kScanRecords ? s_tile : static_cast<int>(blockIdx.x);
   const long long base = static_cast<long long>(t) * TC::kTileT;
   const double lse = c.st->lse_g;
   ThreadTile<ITEMS> tt;
@@ -322,8 +440,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
     const long long k = base + e;
     double g = 0.0;
     if (k < c.N) {
-      g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
-      c.g[k] = g;
+      if (MODE == kScanRecords) {
+        g = __ldcg(&c.g[k]);
+      } else {
+        g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
+        c.g[k] = g;
+      }
     }
     sm.g[TC::sidx(e)] = g;
   }
@@ -338,7 +460,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   }
   SumCnt tot;
   const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
-  if (threadIdx.x == 0) {
+  if (MODE == kScanRecords) {
+    if (threadIdx.x == 0) {
+      s_pre = c.shard_off[0] + __ldcg(&c.tile_pre[t]);  // (off + tile) + thread, as S3
+      s_cpre = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
+    }
+  } else if (threadIdx.x == 0) {
     // decoupled look-back over approximate (any-order) tile sums
     LookBack* lb = c.lookback;
     double pre = 0.0;
@@ -362,6 +489,27 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
     s_cpre = cpre;
   }
   __syncthreads();
+  if (MODE == kScanSums) {
+    if (threadIdx.x == 0) {
+      c.tile_pre[t] = s_pre;
+      c.tile_cnt_pre[t] = s_cpre;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
+      if (old == gridDim.x - 1) {
+        c.cnt_scan[1] = 0;
+        c.cnt_scan[2] = 0;
+        __threadfence();
+        const LookBack v = lb_load(c.lookback + (c.ntiles - 1));
+        c.shard_sum[0] = v.s;
+        c.shard_sum[1] = static_cast<double>(v.cnt);
+        c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
+      }
+    }
+    return;
+  }
   tt.p[0] = s_pre + ex.s;
   tt.cnt0 = s_cpre + ex.c;
   chunk_analyse<ITEMS>(tt);
@@ -396,9 +544,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
     h.tail_d0 = acc.d0;
     h.tail_d1 = acc.d1;
     c.hdr[t] = h;
-    c.tile_pre[t] = s_pre;
-    c.tile_cnt_pre[t] = s_cpre;
+    if (MODE == kScanFull) {
+      c.tile_pre[t] = s_pre;
+      c.tile_cnt_pre[t] = s_cpre;
+    }
   }
+  if (MODE == kScanRecords) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -413,107 +564,17 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   if (!s_last) return;
   __threadfence();
 
-  // ---------------- resolver (one block), chunks of kThreads tiles --------
-  ResolverSmem& rs = sm.rs;
-  if (threadIdx.x == 0) {
-    rs.carry = 0.0;
-    rs.bad = 0;
-  }
-  __syncthreads();
-  for (int b0 = 0; b0 < c.ntiles; b0 += kThreads) {
-    const int ti = b0 + threadIdx.x;
-    const bool valid = ti < c.ntiles;
-    TileHdr h{0, kNoBinade, 0, 0};
-    if (valid) {
-      h.nwin = __ldcg(&c.hdr[ti].nwin);
-      h.tail_e = __ldcg(&c.hdr[ti].tail_e);
-      h.tail_d0 = __ldcg(&c.hdr[ti].tail_d0);
-      h.tail_d1 = __ldcg(&c.hdr[ti].tail_d1);
-    }
-    const bool windowed = valid && h.nwin != 0;
-    const Piece agg{h.tail_d0, h.tail_d1, h.tail_e, 0};
-    const Piece mine_p = windowed ? Piece{0, 0, kNoBinade, 1} : agg;
-    const Piece excl = block_excl_scan_piece(mine_p, sw.pc);
-    int nwt, nws;
-    const int rank = block_excl_scan_int(windowed ? 1 : 0, nwt, sw.si);
-    const int wofs = block_excl_scan_int(windowed && h.nwin > 0 ? h.nwin : 0, nws, sw.si);
-    if (windowed) {
-      rs.wlist[rank] = ti;
-      rs.excl[rank] = excl;
-      rs.hdr[rank] = h;
-      for (int k = 0; k < h.nwin && wofs + k < kResolveWin; ++k)
-        rs.win[wofs + k] = c.win[static_cast<size_t>(ti) * kMaxWin + k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // in-order IEEE walk over the windowed tiles of this chunk
-      double seg = rs.carry;
-      int wo = 0;
-      bool ok = true;
-      for (int r = 0; r < nwt; ++r) {
-        const int wt = rs.wlist[r];
-        const TileHdr wh = rs.hdr[r];
-        double s = seg;
-        ok &= piece_apply(rs.excl[r], s);
-        rs.in[r] = s;
-        if (wh.nwin < 0) {
-          // serial tile (window overflow): plain sequential sum, CDF written here
-          const long long tb = static_cast<long long>(wt) * TC::kTileT;
-          for (int e = 0; e < TC::kTileT && tb + e < c.N; ++e) {
-            s = s + __ldcg(&c.g[tb + e]);
-            c.cdf[tb + e] = s;
-          }
-        } else {
-          for (int k = 0; k < wh.nwin; ++k, ++wo) {
-            TileWin tw;
-            if (wo < kResolveWin) {
-              tw = rs.win[wo];
-            } else {
-              const TileWin* gw = c.win + static_cast<size_t>(wt) * kMaxWin + k;
-              tw.g = __ldcg(&gw->g);
-              tw.e = __ldcg(&gw->e);
-              tw.d0 = __ldcg(&gw->d0);
-              tw.d1 = __ldcg(&gw->d1);
-            }
-            ok &= piece_apply(Piece{tw.d0, tw.d1, tw.e, 0}, s);
-            s = s + tw.g;  // the window element: a real IEEE add, as acc += g[i]
-            c.win_after[static_cast<size_t>(wt) * kMaxWin + k] = s;
-          }
-          ok &= piece_apply(Piece{wh.tail_d0, wh.tail_d1, wh.tail_e, 0}, s);
-        }
-        rs.out[r] = s;
-        seg = s;
-      }
-      if (!ok) rs.bad = 1;
-    }
-    __syncthreads();
-    if (valid) {
-      double s_in, s_end;
-      if (windowed) {
-        s_in = rs.in[rank];
-        s_end = rs.out[rank];
-      } else {
-        s_in = rank > 0 ? rs.out[rank - 1] : rs.carry;
-        bool ok = piece_apply(excl, s_in);
-        s_end = s_in;
-        ok &= piece_apply(agg, s_end);
-        if (!ok) rs.bad = 1;
-      }
-      if (ti == c.ntiles - 1) {
-        c.st->total_mass = s_end;
-        s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
-      }
-      c.tile_info[ti] = make_double2(s_in, s_end);
-      if (threadIdx.x == min(kThreads, c.ntiles - b0) - 1) rs.next = s_end;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) rs.carry = rs.next;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (rs.bad) atomicOr(&c.st->error, kErrInternal);
-    c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
-  }
+  resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs, sw);
+  if (threadIdx.x == 0) c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
+}
+
+// Sharded: every rank resolves the exact chain over ALL shards' tiles.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c) {
+  __shared__ ResolverSmem rs;
+  __shared__ ScanScratch sw;
+  if (grid_error(c)) return;
+  resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, rs, sw);
 }
 
 // S3: exact per-element CDF, per-tile local guide and the coarse guide.
@@ -547,8 +608,9 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
     }
     SumCnt tot;
     const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
-    tt.p[0] = __ldcg(&c.tile_pre[t]) + ex.s;
-    tt.cnt0 = __ldcg(&c.tile_cnt_pre[t]) + ex.c;
+    // same prefix as the records phase: global offset (sharded) + tile + thread
+    tt.p[0] = (c.shard_off[0] + __ldcg(&c.tile_pre[t])) + ex.s;
+    tt.cnt0 = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]) + ex.c;
     chunk_analyse<ITEMS>(tt);
     tt.carry = block_excl_scan_piece(tt.agg, sw.pc);
     tt.win_excl = block_excl_scan_int(tt.nwin, tt.win_total, sw.si);
@@ -605,7 +667,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x * ITEMS + i;
     double v = vals[i];
-    if (base + e == c.N - 1) v = (v < 1.0) ? 1.0 : v;  // filter.cpp:168
+    if (c.n0 + base + e == c.n_glob - 1) v = (v < 1.0) ? 1.0 : v;  // filter.cpp:168
     if (e >= valid) v = INFINITY;
     sg[TC::sidx(e)] = v;
   }
@@ -654,17 +716,34 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
   long long b_hi = ti.y >= 1.0 ? nb - 1 : static_cast<long long>(ceil(ti.y * B1)) - 1;
   b_lo = max(b_lo, 0LL);
   b_hi = min(b_hi, nb - 1);
+  if (t == 0) b_lo = static_cast<long long>(floor(ti.x * B1));  // a shard's first tile also owns
+                                                              // the bucket its range starts in
   for (long long b = b_lo + threadIdx.x; b <= b_hi; b += kThreads) c.coarse[b] = t;
 }
 
 void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
   const bool small = c.tile_log2 == 11;
-  if (which == 1) {
-    if (small) k_scan_pieces<8><<<ntiles, kThreads, 0, st>>>(c);
-    else k_scan_pieces<16><<<ntiles, kThreads, 0, st>>>(c);
-  } else {
-    if (small) k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
-    else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
+  switch (which) {
+    case 1:
+      if (small) k_scan_pieces<8, kScanFull><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_pieces<16, kScanFull><<<ntiles, kThreads, 0, st>>>(c);
+      break;
+    case 2:
+      if (small) k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
+      break;
+    case 3:
+      if (small) k_scan_pieces<8, kScanSums><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_pieces<16, kScanSums><<<ntiles, kThreads, 0, st>>>(c);
+      break;
+    case 4:
+      if (small) k_scan_pieces<8, kScanRecords><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_pieces<16, kScanRecords><<<ntiles, kThreads, 0, st>>>(c);
+      break;
+    case 5:
+      if (small) k_resolve_global<8><<<1, kThreads, 0, st>>>(c);
+      else k_resolve_global<16><<<1, kThreads, 0, st>>>(c);
+      break;
   }
 }
 
@@ -685,6 +764,92 @@ __global__ void __launch_bounds__(kThreads) k_serve(Ctx c) {
   double2* dst = reinterpret_cast<double2*>(c.payload + n * W);
   for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
   dst[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(a));
+}
+
+__global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp, int ngroups) {
+  __shared__ double scratch[kWarps * 2];
+  __shared__ double fin[2];
+  if (grid_error(c)) return;
+  combine_partials<1, false>(gp, ngroups, fin, scratch);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double mx = fin[0];
+    const double lse = isfinite(mx) ? mx + log(fin[1]) : kNegInf;
+    c.st->lse_g = lse;
+    if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+  }
+}
+
+// ---- sharded ancestor migration (pull model) ---------------------------
+// Rank r owns the exact-CDF range [start_r, end_r) of its tiles; the global
+// upper_bound(cdf, u) lands on rank r iff u is in that range. Every rank draws
+// the uniforms of ALL global slots (keyed streams: identical numbers on every
+// rank), serves those in its range from its own exact CDF, and ships
+// {record, ll_bar, ancestor, destination slot} to the slot's owner.
+constexpr int kShardPW = 4;  // extra doubles of a migration payload beyond the record
+
+__device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
+  const int ntl = c.ntiles;
+  for (int r = 0; r < c.world; ++r) {
+    const double lo = c.gtile_info[r * ntl].x;
+    const double hi = c.gtile_info[(r + 1) * ntl - 1].y;
+    if (u >= lo && u < hi) return r;
+  }
+  return c.world - 1;  // unreachable: the last range ends at the guarded cdf >= 1 > u
+}
+
+__global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendbuf, unsigned* send_cnt) {
+  if (grid_error(c)) return;
+  const int W = c.R + kShardPW;
+  const double lo = c.tile_info[0].x;
+  const double hi = c.tile_info[c.ntiles - 1].y;
+  const long long cap = c.N;  // per destination: at most its N_local slots
+  for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
+       ng += static_cast<long long>(gridDim.x) * kThreads) {
+    const double u = resample_uniform(c.seed, c.sp->j, ng);
+    if (!(u >= lo && u < hi)) continue;
+    const unsigned a = find_ancestor(c, u);
+    const int dest = static_cast<int>(ng / c.N);
+    const unsigned pos = atomicAdd(&send_cnt[dest], 1u);
+    const double2* src = reinterpret_cast<const double2*>(c.rec[c.st->cur] + static_cast<long long>(a) * c.R);
+    double2* dst = reinterpret_cast<double2*>(sendbuf + (dest * cap + pos) * W);
+    for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
+    dst[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(c.n0 + a));
+    dst[c.R / 2 + 1] = make_double2(static_cast<double>(ng - dest * c.N), 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_recv_counts(Ctx c, unsigned* recv_cnt) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const double u = resample_uniform(c.seed, c.sp->j, c.n0 + n);
+  atomicAdd(&recv_cnt[serving_rank(c, u)], 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) k_place(Ctx c, const double* recvbuf, long long count) {
+  if (grid_error(c)) return;
+  const long long i = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (i >= count) return;
+  const int W = c.R + kShardPW;
+  const double2* src = reinterpret_cast<const double2*>(recvbuf + i * W);
+  const long long slot = static_cast<long long>(recvbuf[i * W + c.R + 2]);
+  double2* dst = reinterpret_cast<double2*>(c.payload + slot * (c.R + 2));
+  for (int k = 0; k < c.R / 2 + 1; ++k) dst[k] = src[k];
+  c.anc[slot] = static_cast<unsigned>(recvbuf[i * W + c.R + 1]);
+}
+
+// Global approximate offset of this shard (rank order) from the allgathered
+// (sum, count) pairs.
+__global__ void k_shard_offset(Ctx c, const double* gathered) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0, n = 0.0;
+  for (int r = 0; r < c.rank; ++r) {
+    s += gathered[2 * r];
+    n += gathered[2 * r + 1];
+  }
+  c.shard_off[0] = s;
+  c.shard_off[1] = n;
 }
 
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
@@ -769,6 +934,16 @@ struct pfsmc_gpu_sampler {
   double kernel_ms[kNumKernels] = {};
   std::vector<cudaEvent_t> pending;  // (kNumKernels+1) per timed step
   bool have_ensemble = false;
+  // sharding (pfsmc_gpu_create_shard)
+  int rank = 0, world = 1;
+  int ngroups_pred = 0, ngroups_upd = 0;
+  double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
+  double* gp_mom_all = nullptr;    // allgathered K3 group partials (world * ngroups * W)
+  double* sums_all = nullptr;      // allgathered shard (sum, count) pairs
+  double* sendbuf = nullptr;       // world * N_local payloads
+  double* recvbuf = nullptr;       // N_local payloads
+  unsigned* counts_dev = nullptr;  // [world] send + [world] recv
+  unsigned* counts_host = nullptr; // pinned mirror
 
   template <typename T>
   T* dalloc(size_t count) {
@@ -786,6 +961,7 @@ struct pfsmc_gpu_sampler {
     if (sp_host) cudaFreeHost(sp_host);
     if (trace_host) cudaFreeHost(trace_host);
     if (st_host) cudaFreeHost(st_host);
+    if (counts_host) cudaFreeHost(counts_host);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -941,9 +1117,13 @@ extern "C" {
 const char* pfsmc_gpu_version(void) { return "pfsmc_gpu 0.1 (sm_100a)"; }
 const char* pfsmc_gpu_last_error(void) { return g_last_error.c_str(); }
 
-pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler** out) {
+static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int world,
+                                    pfsmc_gpu_sampler** out) {
   return guarded([&] {
     *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) throw ConfigError("shard: need 0 <= rank < world");
+    if (world > 1 && cfg && cfg->particles % (static_cast<uint64_t>(world) * kGroup * kThreads) != 0)
+      throw ConfigError("shard: particles must be a multiple of world * 16384");
     if (!cfg) throw ConfigError("null config");
     // PfConfig::validate (filter.cpp:45-74)
     if (cfg->particles == 0) throw ConfigError("config: particles must be >= 1");
@@ -972,7 +1152,9 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     s->cfg.obs_indices = s->obs.data();
     CK(cudaSetDevice(cfg->device));
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    s->N = static_cast<long long>(cfg->particles);
+    s->rank = rank;
+    s->world = world;
+    s->N = static_cast<long long>(cfg->particles / world);
     s->grid = static_cast<int>((s->N + kThreads - 1) / kThreads);
     const int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
     s->ntiles = static_cast<int>((s->N + (1LL << tile_log2) - 1) >> tile_log2);
@@ -1006,15 +1188,30 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     c.tile_log2 = tile_log2;
     c.lguide = s->dalloc<unsigned short>(NT << tile_log2);
     c.coarse = s->dalloc<unsigned>(size_t(1) << cb);
-    c.tile_info = s->dalloc<double2>(NT);
+    const size_t GNT = NT * world;  // tile arrays cover every shard (aliased at tile0)
+    c.n0 = static_cast<long long>(rank) * s->N;
+    c.n_glob = static_cast<long long>(cfg->particles);
+    c.sharded = world > 1;
+    c.rank = rank;
+    c.world = world;
+    c.gntiles = static_cast<int>(GNT);
+    c.tile0 = static_cast<int>(NT) * rank;
+    c.gtile_info = s->dalloc<double2>(GNT);
+    c.tile_info = c.gtile_info + c.tile0;
     c.g = s->dalloc<double>(N);
     c.lookback = s->dalloc<LookBack>(NT);
     CK(cudaMemset(c.lookback, 0, sizeof(LookBack) * NT));
     c.tile_pre = s->dalloc<double>(NT);
     c.tile_cnt_pre = s->dalloc<long long>(NT);
-    c.hdr = s->dalloc<TileHdr>(NT);
-    c.win = s->dalloc<TileWin>(NT * kMaxWin);
-    c.win_after = s->dalloc<double>(NT * kMaxWin);
+    c.ghdr = s->dalloc<TileHdr>(GNT);
+    c.gwin = s->dalloc<TileWin>(GNT * kMaxWin);
+    c.gwin_after = s->dalloc<double>(GNT * kMaxWin);
+    c.hdr = c.ghdr + c.tile0;
+    c.win = c.gwin + static_cast<size_t>(c.tile0) * kMaxWin;
+    c.win_after = c.gwin_after + static_cast<size_t>(c.tile0) * kMaxWin;
+    c.shard_sum = s->dalloc<double>(2);
+    c.shard_off = s->dalloc<double>(2);
+    CK(cudaMemset(c.shard_off, 0, 2 * sizeof(double)));
     const int vmax = 1 + 4 + 10 + 8 + 1 + 1;
     c.part = s->dalloc<double>(static_cast<size_t>(s->grid) * vmax + 64);
     c.gpart = s->dalloc<double>(static_cast<size_t>(s->grid / kGroup + 2) * vmax + 64);
@@ -1033,10 +1230,31 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
     CK(cudaMallocHost(&s->sp_host, sizeof(StepParams)));
     CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
     CK(cudaMallocHost(&s->trace_host, 64 * sizeof(double)));
+    s->ngroups_pred = (s->grid + kGroup - 1) / kGroup;
+    s->ngroups_upd = s->ngroups_pred;
+    if (world > 1) {
+      const int W = s->ks->moment_width();
+      s->gp_pred_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_pred * 2);
+      s->gp_mom_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_upd * W);
+      s->sums_all = s->dalloc<double>(2 * world);
+      s->sendbuf = s->dalloc<double>(static_cast<size_t>(world) * N * (c.R + kShardPW));
+      s->recvbuf = s->dalloc<double>(N * (c.R + kShardPW));
+      s->counts_dev = s->dalloc<unsigned>(2 * world);
+      CK(cudaMallocHost(&s->counts_host, 2 * world * sizeof(unsigned)));
+    }
     build_graph(s.get());
     *out = s.release();
     return PFSMC_GPU_OK;
   });
+}
+
+pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler** out) {
+  return create_impl(cfg, 0, 1, out);
+}
+
+pfsmc_gpu_status pfsmc_gpu_create_shard(const pfsmc_gpu_config* cfg, int rank, int world,
+                                        pfsmc_gpu_sampler** out) {
+  return create_impl(cfg, rank, world, out);
 }
 
 void pfsmc_gpu_destroy(pfsmc_gpu_sampler* s) { delete s; }
@@ -1064,7 +1282,9 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     for (int k = 0; k < p * p; ++k) h.cov[k] = cov_u[k];
     CK(cudaMemcpyAsync(s->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, s->stream));
     k_pack<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, d, p, tmp_x, tmp_t, 0);
-    s->ks->moments(s->ctx, s->grid, s->stream, 0);  // shrink mean + chol(cov_u)
+    // shrink mean + chol(cov_u); sharded: the caller finishes it globally
+    // (pfsmc_gpu_shard_moments + allgather + pfsmc_gpu_shard_finish_moments(0))
+    if (s->world == 1) s->ks->moments(s->ctx, s->grid, s->stream, 0);
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     cudaFree(tmp_x);
@@ -1114,11 +1334,14 @@ static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vecto
     h.chol_failed = 0;
     for (int k = 0; k < 4; ++k) h.mu[k] = 0.0;
     CK(cudaMemcpyAsync(s->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, s->stream));
-    const double lw0 = -std::log(static_cast<double>(s->N));  // filter.cpp:86
+    const double lw0 = -std::log(static_cast<double>(s->cfg.particles));  // filter.cpp:86
     s->ks->init(s->ctx, s->grid, s->stream, kind, dprm, lw0);
-    // first pass: mean about 0; second pass: cov about that mean
-    s->ks->moments(s->ctx, s->grid, s->stream, 1);
-    s->ks->moments(s->ctx, s->grid, s->stream, 1);
+    // first pass: mean about 0; second pass: cov about that mean (sharded:
+    // the caller runs both passes globally)
+    if (s->world == 1) {
+      s->ks->moments(s->ctx, s->grid, s->stream, 1);
+      s->ks->moments(s->ctx, s->grid, s->stream, 1);
+    }
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     cudaFree(dprm);
@@ -1311,6 +1534,140 @@ pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s) {
     }
     k_flush<<<148 * 4, 256, 0, s->stream>>>(s->flush_buf, s->flush_n);
     CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+
+// ---------------------------------------------------------------- sharded phases
+// One handle per GPU, each owning global slots [rank*N/world, (rank+1)*N/world).
+// The host orchestrator (paper_1411_1702_b200/sharded.py) runs the phases in
+// order and performs the collectives on the exposed buffers between them.
+
+pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** ptr, uint64_t* bytes) {
+  return guarded([&] {
+    const Ctx& c = s->ctx;
+    const size_t W = static_cast<size_t>(s->ks->moment_width());
+    const size_t PW = static_cast<size_t>(c.R + kShardPW);
+    switch (which) {
+      case 0: *ptr = c.gpart; *bytes = sizeof(double) * 2 * s->ngroups_pred; break;
+      case 1: *ptr = s->gp_pred_all; *bytes = sizeof(double) * 2 * s->ngroups_pred * s->world; break;
+      case 2: *ptr = c.shard_sum; *bytes = sizeof(double) * 2; break;
+      case 3: *ptr = s->sums_all; *bytes = sizeof(double) * 2 * s->world; break;
+      case 4: *ptr = c.ghdr; *bytes = sizeof(TileHdr) * c.gntiles; break;
+      case 5: *ptr = c.gwin; *bytes = sizeof(TileWin) * static_cast<size_t>(c.gntiles) * kMaxWin; break;
+      case 6: *ptr = c.gpart; *bytes = sizeof(double) * W * s->ngroups_upd; break;
+      case 7: *ptr = s->gp_mom_all; *bytes = sizeof(double) * W * s->ngroups_upd * s->world; break;
+      case 8: *ptr = s->sendbuf; *bytes = sizeof(double) * PW * s->N * s->world; break;
+      case 9: *ptr = s->recvbuf; *bytes = sizeof(double) * PW * s->N; break;
+      default: throw ConfigError("shard_buffer: unknown buffer id");
+    }
+    if (s->world == 1 && (which == 1 || which == 3 || which >= 7)) throw ConfigError("not a sharded handle");
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
+                                         double t_prev, double t_obs, double h) {
+  return guarded([&] {
+    if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+    const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
+    CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
+    *s->sp_host = sp;
+    CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+    enqueue_prologue(s);
+    s->ks->predict(s->ctx, s->grid, s->stream);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    k_finish_lse<<<1, kThreads, 0, s->stream>>>(s->ctx, s->gp_pred_all, s->ngroups_pred * s->world);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_scan_sums(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    launch_scan(s->ctx, s->ntiles, s->stream, 3);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    k_shard_offset<<<1, 32, 0, s->stream>>>(s->ctx, s->sums_all);
+    launch_scan(s->ctx, s->ntiles, s->stream, 4);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    launch_scan(s->ctx, s->ntiles, s->stream, 5);
+    launch_scan(s->ctx, s->ntiles, s->stream, 2);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// counts_out: [world] payloads this rank sends to each rank, then [world]
+// payloads it receives from each rank. Blocking (the exchange needs them).
+pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  return guarded([&] {
+    const int W = s->world;
+    CK(cudaMemsetAsync(s->counts_dev, 0, 2 * W * sizeof(unsigned), s->stream));
+    const long long nglob = s->ctx.n_glob;
+    const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
+    k_serve_sharded<<<g, kThreads, 0, s->stream>>>(s->ctx, s->sendbuf, s->counts_dev);
+    k_recv_counts<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->counts_dev + W);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->counts_host, s->counts_dev, 2 * W * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    check_error(s);
+    for (int i = 0; i < 2 * W; ++i) counts_out[i] = s->counts_host[i];
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv) {
+  return guarded([&] {
+    if (n_recv != static_cast<uint64_t>(s->N)) throw std::runtime_error("shard_update: payload count mismatch");
+    k_place<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->recvbuf, static_cast<long long>(n_recv));
+    s->ks->update(s->ctx, s->grid, s->stream);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    s->ks->moments(s->ctx, s->grid, s->stream, 1);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// flags: 7 = a completed step (lse_w, cov, chol, flip); 2 = init refresh;
+// 0 = injection (shrink mean only). Blocking; trace_out optional.
+pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out) {
+  return guarded([&] {
+    s->ks->finish_moments(s->ctx, s->gp_mom_all, s->ngroups_upd * s->world, flags, s->stream);
+    CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaGetLastError());
+    check_error(s);
+    if (trace_out) {
+      const int n = 2 * s->p + s->d + 1;
+      for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
+    }
     return PFSMC_GPU_OK;
   });
 }

@@ -1,0 +1,325 @@
+"""Multi-GPU PF-SMC: particle sharding with the per-step collectives
+(SURVEY.md §8(e)).
+
+Each shard owns a contiguous range of GLOBAL slots and keys every Philox
+stream by the global slot (filter.cpp:88, 171, 190, 204), so a sharded step
+draws exactly the numbers of the single-handle step. Per step
+(`ShardedFilter.pf_step`) the only exchanges are:
+
+  A  allgather of the predict-kernel group partials  -> global log-sum-exp
+     (combined in the single-handle order: bitwise the same lse)
+  B  allgather of shard (approximate g total, nonzero count) -> global
+     approximate prefix for the exact-CDF classification
+  C  allgather of the tile records (headers + windows) -> every rank resolves
+     the exact sequential CDF chain over all shards (exact_cdf.cuh)
+  D  personalised exchange of ancestor payloads: rank r serves the global
+     slots whose uniform falls in its exact-CDF range and ships
+     {record, ll_bar, ancestor, slot} to the slot's owner (the migration)
+  E  allgather of the update-kernel moment partials -> global lse_w, mean,
+     covariance, trace row, chol (same combine as the single handle)
+
+The orchestration is backend-agnostic: a shard exposes phases and exchange
+buffers (torch tensors); a communicator moves the bytes. `GpuShard` drives
+the sm_100a kernels through the C ABI (include/pfsmc_gpu.h); `TorchComm`
+uses torch.distributed (NCCL across GPUs, or gloo), `LocalComm` moves bytes
+between shards living in one process (used to check on ONE GPU that R
+shards reproduce the single-handle run bit for bit; the phases run strictly
+one after another, no kernel ever waits on another shard's kernel).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional
+
+import numpy as np
+
+from .sampler import MODEL_DIMS, MODELS, GpuSampler, ObservationModel, PfConfig, TraceRow, _f64, _ptr
+
+BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV = range(10)
+STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
+
+
+class _CudaArray:
+    """Zero-copy view of a raw device allocation for torch.as_tensor."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3}
+
+
+class GpuShard(GpuSampler):
+    """One shard of the global filter on one GPU (pfsmc_gpu_create_shard)."""
+
+    def __init__(self, model: str, cfg: PfConfig, obs: ObservationModel, rank: int, world: int,
+                 device: int = 0):
+        from .sampler import FAMILIES, LIKELIHOODS, _Config, load_library
+        self.lib = load_library()
+        self.model, self.cfg, self.obs = model, cfg, obs
+        self.d, self.p = MODEL_DIMS[MODELS[model]]
+        self.rank, self.world, self.device = rank, world, device
+        self._idx = np.ascontiguousarray(list(obs.indices), dtype=np.uint64)
+        c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed, cfg.newton_tol,
+                    cfg.newton_max_iter, cfg.particles, _ptr(self._idx, C.POINTER(C.c_uint64)), len(self._idx),
+                    obs.sigma, LIKELIHOODS[obs.likelihood], device)
+        L = self.lib
+        for name in ("pfsmc_gpu_create_shard", "pfsmc_gpu_shard_buffer", "pfsmc_gpu_shard_predict",
+                     "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_sums", "pfsmc_gpu_shard_scan_records",
+                     "pfsmc_gpu_shard_resolve", "pfsmc_gpu_shard_serve", "pfsmc_gpu_shard_update",
+                     "pfsmc_gpu_shard_moments", "pfsmc_gpu_shard_finish_moments"):
+            getattr(L, name).restype = C.c_int
+        h = C.c_void_p()
+        self._check(L.pfsmc_gpu_create_shard(C.byref(c), rank, world, C.byref(h)))
+        self.h = h
+        self.n = cfg.particles // world
+        self.n0 = rank * self.n
+        self.row_width = 2 * self.p + self.d + 1
+        self._bufs = {}
+
+    # -- exchange buffers ------------------------------------------------
+    def buffer(self, which: int):
+        if which not in self._bufs:
+            import torch
+            ptr, nb = C.c_void_p(), C.c_uint64()
+            self._check(self.lib.pfsmc_gpu_shard_buffer(self.h, which, C.byref(ptr), C.byref(nb)))
+            self._bufs[which] = torch.as_tensor(_CudaArray(ptr.value, nb.value), device=f"cuda:{self.device}")
+        return self._bufs[which]
+
+    def stream(self):
+        import torch
+        return torch.cuda.ExternalStream(self.stream_handle, device=f"cuda:{self.device}")
+
+    # -- phases ------------------------------------------------------------
+    def predict(self, y, j, t_prev, t_obs, h):
+        y = _f64(y)
+        self._check(self.lib.pfsmc_gpu_shard_predict(self.h, _ptr(y), C.c_uint64(j), C.c_double(t_prev),
+                                                      C.c_double(t_obs), C.c_double(h)))
+
+    def finish_lse(self):
+        self._check(self.lib.pfsmc_gpu_shard_finish_lse(self.h))
+
+    def scan_sums(self):
+        self._check(self.lib.pfsmc_gpu_shard_scan_sums(self.h))
+
+    def scan_records(self):
+        self._check(self.lib.pfsmc_gpu_shard_scan_records(self.h))
+
+    def resolve(self):
+        self._check(self.lib.pfsmc_gpu_shard_resolve(self.h))
+
+    def serve(self) -> np.ndarray:
+        counts = np.zeros(2 * self.world, dtype=np.uint32)
+        self._check(self.lib.pfsmc_gpu_shard_serve(self.h, counts.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return counts
+
+    def update(self, n_recv: int):
+        self._check(self.lib.pfsmc_gpu_shard_update(self.h, C.c_uint64(n_recv)))
+
+    def moments(self):
+        self._check(self.lib.pfsmc_gpu_shard_moments(self.h))
+
+    def finish_moments(self, flags: int) -> np.ndarray:
+        out = np.zeros(self.row_width)
+        self._check(self.lib.pfsmc_gpu_shard_finish_moments(self.h, flags, _ptr(out)))
+        return out
+
+    def payload_doubles(self) -> int:
+        return (self.d + self.p + 1) // 2 * 2 + 4
+
+    def sync(self):
+        self.synchronize()
+
+
+# ------------------------------------------------------------------ comms
+class LocalComm:
+    """Collectives among shards that all live in this process."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def _fence(self, shards):
+        import torch
+        for s in shards:
+            s.sync()
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.synchronize()
+
+    def allgather(self, shards, src: int, dst: int):
+        """dst buffer of every shard <- concat over ranks of src buffers."""
+        self._fence(shards)
+        parts = [s.buffer(src) for s in sorted(shards, key=lambda s: s.rank)]
+        for s in shards:
+            out = s.buffer(dst)
+            n = parts[0].numel()
+            for r, p in enumerate(parts):
+                out[r * n:(r + 1) * n].copy_(p)
+        self._fence(shards)
+
+    def allgather_slices(self, shards, buf: int):
+        """Each shard's global buffer carries its slice at rank * size; share them."""
+        self._fence(shards)
+        bufs = {s.rank: s.buffer(buf) for s in shards}
+        n = bufs[0].numel() // self.world
+        for r, b in bufs.items():
+            for s in shards:
+                if s.rank != r:
+                    s.buffer(buf)[r * n:(r + 1) * n].copy_(b[r * n:(r + 1) * n])
+        self._fence(shards)
+
+    def exchange(self, shards, counts: dict, item_bytes: int):
+        """Send region of rank r for dest d lives at d * cap (cap = N_local items)."""
+        self._fence(shards)
+        by_rank = {s.rank: s for s in shards}
+        for d, sd in by_rank.items():
+            off = 0
+            cap = sd.n
+            for r in range(self.world):
+                k = int(counts[r][d])
+                if k:
+                    src = by_rank[r].buffer(BUF_SEND)[(d * cap) * item_bytes:(d * cap + k) * item_bytes]
+                    sd.buffer(BUF_RECV)[off * item_bytes:(off + k) * item_bytes].copy_(src)
+                off += k
+        self._fence(shards)
+
+    def gather_counts(self, shards, local_counts: dict) -> dict:
+        return local_counts
+
+
+class TorchComm:
+    """One shard per process; torch.distributed (NCCL for GPUs, gloo on CPU)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+
+    def _ctx(self, s):
+        import contextlib
+        import torch
+        if hasattr(s, "stream_handle"):
+            return torch.cuda.stream(s.stream())
+        return contextlib.nullcontext()
+
+    def allgather(self, shards, src: int, dst: int):
+        (s,) = shards
+        with self._ctx(s):
+            self.dist.all_gather_into_tensor(s.buffer(dst), s.buffer(src))
+
+    def allgather_slices(self, shards, buf: int):
+        (s,) = shards
+        b = s.buffer(buf)
+        n = b.numel() // self.world
+        with self._ctx(s):
+            mine = b[self.rank * n:(self.rank + 1) * n].clone()
+            self.dist.all_gather_into_tensor(b, mine)
+
+    def gather_counts(self, shards, local_counts: dict) -> dict:
+        import torch
+        (s,) = shards
+        t = torch.as_tensor(local_counts[s.rank].astype(np.int64))
+        if hasattr(s, "stream_handle"):
+            t = t.to(f"cuda:{s.device}")
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        with self._ctx(s):
+            self.dist.all_gather(out, t)
+        return {r: out[r].cpu().numpy() for r in range(self.world)}
+
+    def exchange(self, shards, counts: dict, item_bytes: int):
+        (s,) = shards
+        me, W = self.rank, self.world
+        send, recv = s.buffer(BUF_SEND), s.buffer(BUF_RECV)
+        cap = s.n
+        ops = []
+        off = 0
+        for r in range(W):
+            k_in = int(counts[r][me])          # rank r sends k_in payloads to me
+            k_out = int(counts[me][r])         # I send k_out payloads to rank r
+            rbuf = recv[off * item_bytes:(off + k_in) * item_bytes]
+            sbuf = send[(r * cap) * item_bytes:(r * cap + k_out) * item_bytes]
+            if r == me:
+                with self._ctx(s):
+                    rbuf.copy_(sbuf)
+            else:
+                if k_out:
+                    ops.append(self.dist.P2POp(self.dist.isend, sbuf, r))
+                if k_in:
+                    ops.append(self.dist.P2POp(self.dist.irecv, rbuf, r))
+            off += k_in
+        if ops:
+            with self._ctx(s):
+                for w in self.dist.batch_isend_irecv(ops):
+                    w.wait()
+
+
+# ------------------------------------------------------------------ the filter
+class ShardedFilter:
+    """The global filter over `shards` (this process's shards) and `comm`."""
+
+    def __init__(self, shards: List, comm):
+        self.shards = sorted(shards, key=lambda s: s.rank)
+        self.comm = comm
+        s0 = self.shards[0]
+        self.d, self.p, self.world = s0.d, s0.p, s0.world
+
+    def _each(self, fn):
+        return [fn(s) for s in self.shards]
+
+    def _refresh(self, flags):
+        self._each(lambda s: s.moments())
+        self.comm.allgather(self.shards, BUF_MOM, BUF_MOM_ALL)
+        return self._each(lambda s: s.finish_moments(flags))[0]
+
+    def initialize_uniform(self, **prior):
+        self._each(lambda s: s.initialize_uniform(**prior))
+        self._refresh(INIT_FLAGS)   # equal-weight mean
+        self._refresh(INIT_FLAGS)   # covariance about it
+
+    def initialize_gaussian(self, **prior):
+        self._each(lambda s: s.initialize_gaussian(**prior))
+        self._refresh(INIT_FLAGS)
+        self._refresh(INIT_FLAGS)
+
+    def set_ensemble(self, ens):
+        """Global filter::Ensemble; each shard takes its slot range."""
+        from .sampler import Ensemble
+        for s in self.shards:
+            sl = slice(s.n0, s.n0 + s.n)
+            s.set_ensemble(Ensemble(ens.states[sl], ens.params_u[sl], ens.logw[sl], ens.mean_u, ens.cov_u))
+        self._refresh(INJECT_FLAGS)
+
+    def pf_step(self, y, j: int, t_prev: float, t_obs: float, h: float) -> TraceRow:
+        sh, comm = self.shards, self.comm
+        self._each(lambda s: s.predict(y, j, t_prev, t_obs, h))
+        comm.allgather(sh, BUF_PRED, BUF_PRED_ALL)                       # A
+        self._each(lambda s: s.finish_lse())
+        self._each(lambda s: s.scan_sums())
+        comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # B
+        self._each(lambda s: s.scan_records())
+        comm.allgather_slices(sh, BUF_HDR)                               # C
+        comm.allgather_slices(sh, BUF_WIN)
+        self._each(lambda s: s.resolve())
+        served = {s.rank: s.serve() for s in sh}
+        counts = comm.gather_counts(sh, {r: c[:self.world] for r, c in served.items()})  # send matrix
+        for r, c in served.items():   # each rank also derived its receive counts independently
+            if [int(counts[q][r]) for q in range(self.world)] != [int(v) for v in c[self.world:]]:
+                raise RuntimeError("sharded exchange: send/receive count mismatch")
+        item = 8 * sh[0].payload_doubles()
+        comm.exchange(sh, counts, item)                                  # D: migration
+        for s in sh:
+            s.update(int(sum(counts[r][s.rank] for r in range(self.world))))
+        comm.allgather(sh, BUF_MOM, BUF_MOM_ALL)                         # E
+        rows = self._each(lambda s: s.finish_moments(STEP_FLAGS))
+        out = rows[0]
+        p, d = self.p, self.d
+        return TraceRow(j, t_obs, out[:p].copy(), out[p:2 * p].copy(), out[2 * p:2 * p + d].copy(),
+                        float(out[2 * p + d]))
+
+    def get_ensemble(self):
+        """Local shards' slices concatenated (rank order)."""
+        from .sampler import Ensemble
+        parts = [s.get_ensemble() for s in self.shards]
+        return Ensemble(np.concatenate([e.states for e in parts]), np.concatenate([e.params_u for e in parts]),
+                        np.concatenate([e.logw for e in parts]), parts[0].mean_u, parts[0].cov_u)
+
+    def ancestors(self) -> np.ndarray:
+        return np.concatenate([s.step_diagnostics()[0] for s in self.shards])
