@@ -142,6 +142,10 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
                                            uint64_t j, uint32_t* ancestors_out,
                                            double* cdf_out);
 
+/* %globaltimer probes of the last step (ns): [0] exact-CDF kernel start,
+ * [1] resolver start, [2] resolver end. Diagnostics for profiling. */
+pfsmc_gpu_status pfsmc_gpu_debug_timestamps(pfsmc_gpu_sampler* s, uint64_t* out8);
+
 /* The CUDA stream every launch of this handle goes to (cudaStream_t). */
 void* pfsmc_gpu_stream(pfsmc_gpu_sampler* s);
 
@@ -165,7 +169,7 @@ pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s);
  * and reproduces its results bit for bit. The host orchestrator
  * (paper_1411_1702_b200/sharded.py) runs, per step:
  *   shard_predict -> allgather buf 0 into 1 -> shard_finish_lse
- *   shard_scan_sums -> allgather buf 2 into 3 -> shard_scan_records
+ *   allgather buf 2 into 3 -> shard_scan_records
  *   allgather the own slices of bufs 4, 5 -> shard_resolve
  *   shard_serve (counts) -> exchange payloads buf 8 -> buf 9 -> shard_update
  *   allgather buf 6 into 7 -> shard_finish_moments(7)
@@ -180,7 +184,6 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
 pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
                                          double t_prev, double t_obs, double h);
 pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s);
-pfsmc_gpu_status pfsmc_gpu_shard_scan_sums(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s);
 /* counts_out: world send counts then world receive counts (payloads of

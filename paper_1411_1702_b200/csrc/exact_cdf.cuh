@@ -14,11 +14,9 @@
 // represented by the pair (delta(0), delta(1)) -- a parallel scan.
 //
 // Binade crossings (where rounding changes scale) are located with an
-// approximate parallel prefix P_k (plain doubles, any summation tree) and a
-// rigorous bound |s_k - P_k| <= E_k: a floating-point sum of nonnegative
-// terms by any tree has at most (cnt - 1) rounding nodes (nodes adding a zero
-// are exact), each off by <= 2^-53 of a value <= the total, so both s_k and
-// P_k are within (cnt_k - 1) 2^-53 P_k(1 + tiny) of the true sum. Every
+// approximate parallel prefix P_k (any summation tree, tile offsets from the
+// predict kernel's block partials) and a rigorous bound |s_k - P_k| <= E_k
+// (sum_bound below). Every
 // element whose before/after values are not CERTAINLY in one binade becomes a
 // "window": the resolver applies it with a real IEEE add, fl(s + g), in
 // order. Windows are ~log2(N) per scan (one per binade crossing), so the
@@ -75,10 +73,21 @@ __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
   return r;
 }
 
-// Rigorous |s - P| bound (see header). cnt <= 1: both sums are exact.
+// Rigorous |s - P| bound. P = (tile prefix from the K1 block partials) +
+// (in-tile tree prefix of the exact g). Error sources, u = 2^-53, cnt =
+// nonzero (finite) terms so far:
+//  * the sequential s and every tree/partial sum: <= cnt rounding nodes each
+//    (nodes adding a zero are exact), each <= u of a value <= P(1+tiny);
+//  * tile sums = sum_b S_b exp(M_b - lse): per-block product and sum
+//    roundings (<= cnt), CUDA exp <= 2 ulp on S_b terms and the scale;
+//  * argument roundings fl(lg - M_b), fl(M_b - lse), fl(lg - lse): absolute
+//    <= u * 3 * g |ln g| <= u * 3/e per nonzero term (g |ln g| <= 1/e).
+// => |s - P| <= u ((5 cnt + 16) P + 2 cnt); used with a 2x margin. cnt <= 1:
+// a one-term sum is exact on every path (exp(0) = 1), so both are exact.
 __device__ __forceinline__ double sum_bound(double p, long long cnt) {
   if (cnt <= 1) return 0.0;
-  return (2.0 * static_cast<double>(cnt) + 8.0) * 0x1.0p-53 * p + 0x1.0p-1060;
+  const double n = static_cast<double>(cnt);
+  return ((12.0 * n + 64.0) * p + 4.0 * n) * 0x1.0p-53 + 0x1.0p-1060;
 }
 
 // Per-element kind: 0 = neutral (g == 0), 1 = run element, 2 = window.

@@ -35,7 +35,7 @@ struct DevState {
   int cur;            // which record buffer holds the ensemble
   int error;          // ErrBits of the current step
   int chol_failed;    // chol_psd of cov failed (raised at the next proliferation)
-  int scan_epoch;     // tags this step's look-back descriptors
+  int pad;
   double lse_w;       // logw_n = lw_n - lse_w
   double lse_g;       // fitness log-normaliser of the current step
   double mu[4];       // shrink mean = weighted mean of the current params
@@ -45,7 +45,14 @@ struct DevState {
   double trace[2 * 4 + 8 + 1];
   unsigned long long newton_iters;
   double total_mass;  // exact CDF total (diagnostic)
+  unsigned long long tstamp[8];  // %globaltimer probes (diagnostics)
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct TileHdr {
   int nwin;  // -1: overflow (serial tile)
@@ -57,6 +64,16 @@ struct TileWin {
   int e;
   int local;  // element index inside the tile
   long long d0, d1;
+};
+
+// Per-thread handoff from the records phase to the CDF phase of the exact
+// scan: the thread's approximate prefix and the exact segment carry.
+struct ThreadRec {
+  double p0;
+  long long cnt0;
+  long long d0, d1;
+  int e, flag;
+  int win_excl, pad;
 };
 
 // Immutable launch context (pointers + constants), passed by value.
@@ -83,8 +100,10 @@ struct Ctx {
   double2* tile_info;  // exact CDF (value before the tile, value at its last element;
                        // the last tile's end carries the guard, filter.cpp:168)
   double* g;           // fitness of the current step (k_scan_tiles writes it)
-  struct LookBack* lookback;  // decoupled look-back descriptors (approx. tile sums)
-  double* tile_pre;    // approximate exclusive tile prefixes
+  double* tile_pre;    // approximate exclusive tile prefixes (from the K1 block partials)
+  int* blk_cnt;        // K1 blocks: number of finite fitness log-weights
+  double* trel;        // per tile: fitness mass relative to its K1 group max
+  struct ThreadRec* trec;  // S2 -> S3 handoff: per-thread prefix and segment carry
   long long* tile_cnt_pre;
   TileHdr* hdr;
   TileWin* win;        // kMaxWin per tile
@@ -108,7 +127,7 @@ struct Ctx {
   TileWin* gwin;       // all shards' tile windows (allgathered, kMaxWin per tile)
   double* gwin_after;  // exact sums after every window (global resolver)
   double2* gtile_info; // exact (start, end) of every global tile
-  double* shard_sum;   // [2]: this shard's approximate g total and nonzero count (sums mode)
+  double* shard_sum;   // [2]: this shard's approximate g total and nonzero count (K1 tail)
   double* shard_off;   // [2]: global approximate offset and count before this shard
 };
 
@@ -178,6 +197,87 @@ __device__ __forceinline__ bool grid_error(const Ctx& c) {
   return *reinterpret_cast<volatile int*>(&c.st->error) != 0;
 }
 
+// Approximate fitness mass per exact-CDF tile, straight from the K1 block
+// partials (M_b, S_b = sum exp(lg - M_b)), in two levels so no single block
+// walks every partial:
+//  * group hook (last block of each 64-block group, before lse is known):
+//    trel_t = sum_b S_b exp(M_b - M_g) and the finite count of each tile in
+//    the group (a tile is 8 or 16 K1 blocks; groups hold whole tiles);
+//  * tile_prefixes (final block): T_t = trel_t exp(M_g - lse), exclusive
+//    prefix over tiles.
+// Only the exact scan's classification reads these, through the rigorous
+// bound of exact_cdf.cuh (sum_bound); no pass over the fitness vector and no
+// look-back is needed.
+struct TileGroupHook {
+  const Ctx* c;
+  __device__ void operator()(int g, int gsize) const {
+    const int bpt_log2 = c->tile_log2 - 8;  // K1 blocks per tile
+    const double mg = __ldcg(&c->gpart[2 * g]);
+    const int b0 = g * kGroup;
+    double w = 0.0;
+    int n = 0;
+    if (threadIdx.x < gsize) {
+      const int b = b0 + threadIdx.x;
+      const double mb = __ldcg(&c->part[2 * b]);
+      if (mb != -INFINITY) w = __ldcg(&c->part[2 * b + 1]) * exp(mb - mg);
+      n = __ldcg(&c->blk_cnt[b]);
+    }
+    // fixed-order sums over the bpt lanes of each tile (butterfly inside aligned lane groups)
+    for (int o = 1; o < (1 << bpt_log2); o <<= 1) {
+      w += __shfl_xor_sync(0xffffffffu, w, o);
+      n += __shfl_xor_sync(0xffffffffu, n, o);
+    }
+    if (threadIdx.x < gsize && (threadIdx.x & ((1 << bpt_log2) - 1)) == 0) {
+      const int t = (b0 + threadIdx.x) >> bpt_log2;
+      c->trel[t] = w;
+      c->tile_cnt_pre[t] = n;  // per-tile count; tile_prefixes turns it into the prefix
+    }
+  }
+};
+
+__device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse) {
+  __shared__ SumCnt sw[2 * kWarps];
+  const int tpg_log2 = 6 - (c.tile_log2 - 8);  // tiles per group
+  const int per = (c.ntiles + kThreads - 1) / kThreads;
+  const int t0 = threadIdx.x * per, t1 = min(t0 + per, c.ntiles);
+  double s[8];
+  long long n[8];
+  SumCnt acc{0.0, 0};
+  for (int t = t0; t < t1; ++t) {
+    const double mg = __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
+    const double v = mg == -INFINITY ? 0.0 : __ldcg(&c.trel[t]) * exp(mg - lse);
+    const long long k = __ldcg(&c.tile_cnt_pre[t]);
+    if (t - t0 < 8) {
+      s[t - t0] = v;
+      n[t - t0] = k;
+    }
+    acc.s += v;
+    acc.c += k;
+  }
+  SumCnt tot;
+  SumCnt ex = block_excl_scan_sc(acc, tot, sw);
+  for (int t = t0; t < t1; ++t) {
+    double v;
+    long long k;
+    if (t - t0 < 8) {
+      v = s[t - t0];
+      k = n[t - t0];
+    } else {
+      const double mg = __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
+      v = mg == -INFINITY ? 0.0 : __ldcg(&c.trel[t]) * exp(mg - lse);
+      k = __ldcg(&c.tile_cnt_pre[t]);
+    }
+    c.tile_pre[t] = ex.s;
+    c.tile_cnt_pre[t] = ex.c;
+    ex.s += v;
+    ex.c += k;
+  }
+  if (threadIdx.x == kThreads - 1) {
+    c.shard_sum[0] = tot.s;
+    c.shard_sum[1] = static_cast<double>(tot.c);
+  }
+}
+
 // ---------------------------------------------------------------- K1
 template <class M, int FAM, int ORD>
 __global__ void __launch_bounds__(kThreads, 4) k_predict(Ctx c) {
@@ -211,15 +311,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_predict(Ctx c) {
     if ((threadIdx.x & 31) == 0 && it) atomicAdd(&c.st->newton_iters, static_cast<unsigned long long>(it));
   }
   const double one[1] = {1.0};
+  const int nfin = __syncthreads_count(isfinite(lgv) != 0);
+  if (threadIdx.x == 0) c.blk_cnt[blockIdx.x] = nfin;
   block_partial<1, false>(lgv, one, c.part + blockIdx.x * 2, scratch);
-  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, !c.sharded)) {
+  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, !c.sharded,
+                                 TileGroupHook{&c})) {
+    __shared__ double s_lse;
     if (threadIdx.x == 0) {
       // logsumexp (filter.cpp:16-23) + the degeneracy check (filter.cpp:149-152)
       const double mx = fin[0];
       const double lse = isfinite(mx) ? mx + log(fin[1]) : kNegInf;
       c.st->lse_g = lse;
       if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+      s_lse = lse;
     }
+    __syncthreads();
+    if (isfinite(s_lse)) tile_prefixes(c, s_lse);
   }
 }
 

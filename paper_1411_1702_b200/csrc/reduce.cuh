@@ -164,10 +164,17 @@ __device__ __forceinline__ void combine_partials(const double* in, int count, do
 // last), where `final_out` holds the grand partial (thread 0 wrote it, and a
 // __syncthreads() has been issued). counters: [0..ngroups) group counters,
 // [ngroups] the final counter; all reset to 0 by their last user.
-template <int V, bool SQ>
+struct NoGroupHook {
+  __device__ void operator()(int, int) const {}
+};
+
+// hook(g, gsize) runs in the last block of group g after its group partial
+// is written (all of the group's block partials are visible).
+template <int V, bool SQ, class Hook = NoGroupHook>
 __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_part,
                                                  unsigned* counters, double* final_out,
-                                                 double* scratch, bool final_level = true) {
+                                                 double* scratch, bool final_level = true,
+                                                 const Hook& hook = Hook()) {
   __shared__ int s_flag;
   const int nblocks = gridDim.x;
   const int ngroups = (nblocks + kGroup - 1) / kGroup;
@@ -185,6 +192,8 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __threadfence();
   combine_partials<V, SQ>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
                           group_part + g * (V + 1), scratch);
+  __syncthreads();
+  hook(g, gsize);
   if (!final_level) return false;  // sharded: the group partials are exported
   __threadfence();
   __syncthreads();
@@ -199,6 +208,54 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   combine_partials<V, SQ>(group_part, ngroups, final_out, scratch);
   __syncthreads();
   return true;
+}
+
+// Per-thread running values for a block-wide scan.
+struct SumCnt {
+  double s;
+  long long c;
+};
+
+// Block-wide exclusive scan of (sum, count) in a fixed shape: warp shuffle
+// scan, warp totals through smem, scanned by warp 0. Approximate sums only
+// (the bound in exact_cdf.cuh covers any tree); counts exact.
+__device__ __forceinline__ SumCnt block_excl_scan_sc(SumCnt v, SumCnt& total, SumCnt* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SumCnt x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ys = __shfl_up_sync(0xffffffffu, x.s, o);
+    const long long yc = __shfl_up_sync(0xffffffffu, x.c, o);
+    if (lane >= o) {
+      x.s = ys + x.s;
+      x.c += yc;
+    }
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    SumCnt t = lane < kWarps ? sw[lane] : SumCnt{0.0, 0};
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const double ys = __shfl_up_sync(0xffffffffu, t.s, o);
+      const long long yc = __shfl_up_sync(0xffffffffu, t.c, o);
+      if (lane >= o) {
+        t.s = ys + t.s;
+        t.c += yc;
+      }
+    }
+    if (lane < kWarps) sw[kWarps + lane] = t;  // inclusive warp prefixes
+  }
+  __syncthreads();
+  const SumCnt pre = w ? sw[kWarps + w - 1] : SumCnt{0.0, 0};
+  total = sw[2 * kWarps - 1];
+  const double es = __shfl_up_sync(0xffffffffu, x.s, 1);
+  const long long ec = __shfl_up_sync(0xffffffffu, x.c, 1);
+  SumCnt ex = lane ? SumCnt{es, ec} : SumCnt{0.0, 0};
+  ex.s = pre.s + ex.s;
+  ex.c += pre.c;
+  __syncthreads();
+  return ex;
 }
 
 }  // namespace pfsmc_gpu

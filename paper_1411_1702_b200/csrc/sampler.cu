@@ -43,54 +43,6 @@ struct TileCfg {
   __device__ static __forceinline__ int sidx(int e) { return e + e / ITEMS; }
 };
 
-// Per-thread running values for a block-wide scan.
-struct SumCnt {
-  double s;
-  long long c;
-};
-
-// Block-wide exclusive scan of (sum, count) in a fixed shape: warp shuffle
-// scan, warp totals through smem, scanned by warp 0. Approximate sums only
-// (the bound in exact_cdf.cuh covers any tree); counts exact.
-__device__ __forceinline__ SumCnt block_excl_scan_sc(SumCnt v, SumCnt& total, SumCnt* sw) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  SumCnt x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double ys = __shfl_up_sync(0xffffffffu, x.s, o);
-    const long long yc = __shfl_up_sync(0xffffffffu, x.c, o);
-    if (lane >= o) {
-      x.s = ys + x.s;
-      x.c += yc;
-    }
-  }
-  if (lane == 31) sw[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    SumCnt t = lane < kWarps ? sw[lane] : SumCnt{0.0, 0};
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const double ys = __shfl_up_sync(0xffffffffu, t.s, o);
-      const long long yc = __shfl_up_sync(0xffffffffu, t.c, o);
-      if (lane >= o) {
-        t.s = ys + t.s;
-        t.c += yc;
-      }
-    }
-    if (lane < kWarps) sw[kWarps + lane] = t;  // inclusive warp prefixes
-  }
-  __syncthreads();
-  const SumCnt pre = w ? sw[kWarps + w - 1] : SumCnt{0.0, 0};
-  total = sw[2 * kWarps - 1];
-  const double es = __shfl_up_sync(0xffffffffu, x.s, 1);
-  const long long ec = __shfl_up_sync(0xffffffffu, x.c, 1);
-  SumCnt ex = lane ? SumCnt{es, ec} : SumCnt{0.0, 0};
-  ex.s = pre.s + ex.s;
-  ex.c += pre.c;
-  __syncthreads();
-  return ex;
-}
-
 // Block-wide exclusive segmented scan of Piece, fixed shape.
 __device__ __forceinline__ Piece block_excl_scan_piece(Piece v, Piece* sw) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -157,9 +109,6 @@ struct ThreadTile {
   int uniform_e;        // binade of the whole chunk (fast path) or kNoBinade
   Piece agg;            // the chunk's aggregate piece
   int nwin;             // windows in the chunk
-  Piece carry;          // exclusive segmented prefix for this thread
-  int win_excl;         // windows before this thread's first element
-  int win_total;        // windows in the tile
 };
 
 struct ScanScratch {
@@ -252,27 +201,50 @@ __device__ __forceinline__ void chunk_analyse(ThreadTile<ITEMS>& tt) {
   tt.nwin = nw;
 }
 
-// One 16-byte look-back descriptor per tile: {approx sum, count:30 | kind:2
-// | epoch}. 16-byte aligned accesses are single-copy atomic.
-struct __align__(16) LookBack {
-  double s;
-  unsigned cnt;
-  unsigned tag;  // (epoch << 2) | kind, kind 1 = aggregate, 2 = inclusive
+// Composite resolver scan element: the segmented piece over window-free
+// tiles, the windowed-tile rank and the staged-window offset, in one scan.
+struct ResScan {
+  Piece pc;
+  int rank, wofs;
 };
 
-__device__ __forceinline__ void lb_store(LookBack* p, double s, unsigned cnt, unsigned tag) {
-  const unsigned long long lo = static_cast<unsigned long long>(__double_as_longlong(s));
-  const unsigned long long hi = (static_cast<unsigned long long>(tag) << 32) | cnt;
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(lo), "l"(hi) : "memory");
+__device__ __forceinline__ ResScan res_combine(const ResScan& a, const ResScan& b) {
+  return ResScan{piece_combine(a.pc, b.pc), a.rank + b.rank, a.wofs + b.wofs};
 }
-__device__ __forceinline__ LookBack lb_load(const LookBack* p) {
-  unsigned long long lo, hi;
-  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
-  LookBack r;
-  r.s = __longlong_as_double(static_cast<long long>(lo));
-  r.cnt = static_cast<unsigned>(hi & 0xffffffffu);
-  r.tag = static_cast<unsigned>(hi >> 32);
-  return r;
+
+__device__ __forceinline__ ResScan shfl_up_res(const ResScan& v, int o) {
+  return ResScan{shfl_up_piece(v.pc, o), __shfl_up_sync(0xffffffffu, v.rank, o),
+                 __shfl_up_sync(0xffffffffu, v.wofs, o)};
+}
+
+// Block-wide exclusive scan of ResScan (fixed shape); total in `tot`.
+__device__ __forceinline__ ResScan block_excl_scan_res(ResScan v, ResScan& tot, ResScan* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const ResScan id{piece_identity(), 0, 0};
+  ResScan x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const ResScan y = shfl_up_res(x, o);
+    if (lane >= o) x = res_combine(y, x);
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    ResScan t = lane < kWarps ? sw[lane] : id;
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const ResScan y = shfl_up_res(t, o);
+      if (lane >= o) t = res_combine(y, t);
+    }
+    if (lane < kWarps) sw[kWarps + lane] = t;
+  }
+  __syncthreads();
+  ResScan ex = shfl_up_res(x, 1);
+  if (lane == 0) ex = id;
+  if (w) ex = res_combine(sw[kWarps + w - 1], ex);
+  tot = sw[2 * kWarps - 1];
+  __syncthreads();
+  return ex;
 }
 
 constexpr int kResolveWin = 512;  // windows staged in smem by the resolver
@@ -284,14 +256,9 @@ struct ResolverSmem {
   double out[kThreads];
   double in[kThreads];
   int wlist[kThreads];
+  ResScan rsw[2 * kWarps];
   double carry, next;
   int bad;
-};
-
-template <int ITEMS>
-union PiecesSmem {
-  double g[TileCfg<ITEMS>::kSmem];
-  ResolverSmem rs;
 };
 
 // The exact chain over tiles, one block: a segmented monoid scan across
@@ -300,8 +267,7 @@ union PiecesSmem {
 // handle (own tiles) and, sharded, for all shards' tiles on every rank.
 template <int ITEMS>
 __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
-                              double2* tile_info, int ntiles, bool own_g, ResolverSmem& rs,
-                              ScanScratch& sw) {
+                              double2* tile_info, int ntiles, bool own_g, ResolverSmem& rs) {
   using TC = TileCfg<ITEMS>;
   if (threadIdx.x == 0) {
     rs.carry = 0.0;
@@ -320,17 +286,18 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
     }
     const bool windowed = valid && h.nwin != 0;
     const Piece agg{h.tail_d0, h.tail_d1, h.tail_e, 0};
-    const Piece mine_p = windowed ? Piece{0, 0, kNoBinade, 1} : agg;
-    const Piece excl = block_excl_scan_piece(mine_p, sw.pc);
-    int nwt, nws;
-    const int rank = block_excl_scan_int(windowed ? 1 : 0, nwt, sw.si);
-    const int wofs = block_excl_scan_int(windowed && h.nwin > 0 ? h.nwin : 0, nws, sw.si);
+    ResScan mine{windowed ? Piece{0, 0, kNoBinade, 1} : agg, windowed ? 1 : 0,
+                 windowed && h.nwin > 0 ? h.nwin : 0};
+    ResScan tot;
+    const ResScan ex = block_excl_scan_res(mine, tot, rs.rsw);
+    const int nwt = tot.rank;
+    const int rank = ex.rank;
     if (windowed) {
       rs.wlist[rank] = ti;
-      rs.excl[rank] = excl;
+      rs.excl[rank] = ex.pc;
       rs.hdr[rank] = h;
-      for (int k = 0; k < h.nwin && wofs + k < kResolveWin; ++k)
-        rs.win[wofs + k] = win[static_cast<size_t>(ti) * kMaxWin + k];
+      for (int k = 0; k < h.nwin && ex.wofs + k < kResolveWin; ++k)
+        rs.win[ex.wofs + k] = win[static_cast<size_t>(ti) * kMaxWin + k];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -384,7 +351,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
         s_end = rs.out[rank];
       } else {
         s_in = rank > 0 ? rs.out[rank - 1] : rs.carry;
-        bool ok = piece_apply(excl, s_in);
+        bool ok = piece_apply(ex.pc, s_in);
         s_end = s_in;
         ok &= piece_apply(agg, s_end);
         if (!ok) rs.bad = 1;
@@ -403,36 +370,31 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
   if (threadIdx.x == 0 && rs.bad) atomicOr(&c.st->error, kErrInternal);
 }
 
-// S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
-// once; approximate tile prefix by decoupled look-back; classification and
-// tile records (window list + segment aggregates). The last block resolves
-// the exact chain over all tiles: a segmented monoid scan across window-free
-// tiles and an in-order IEEE walk over the windows only, with everything the
-// walk touches staged in shared memory.
-// MODE 0: single handle (look-back + records + resolver).
-// MODE 1 (sharded, phase A): g, shard-local look-back prefixes, shard total.
-// MODE 2 (sharded, phase B): records against the global approximate offset
-//         (written straight into the allgather buffers); no resolver.
-enum ScanMode { kScanFull = 0, kScanSums = 1, kScanRecords = 2 };
+template <int ITEMS>
+union PiecesSmem {
+  double g[TileCfg<ITEMS>::kSmem];
+  ResolverSmem rs;
+};
 
-template <int ITEMS, int MODE>
+// S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
+// once; the approximate prefix from the tile offsets computed in the predict
+// kernel's tail (no look-back); classification, windows and tile records;
+// the per-thread handoff for S3. SHARDED = 0: the last block resolves the
+// exact chain (single handle); 1: records only (every rank resolves all
+// shards' records after the allgather, k_resolve_global).
+template <int ITEMS, int SHARDED>
 __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   using TC = TileCfg<ITEMS>;
   __shared__ PiecesSmem<ITEMS> sm;
   __shared__ ScanScratch sw;
-  __shared__ int s_tile, s_last;
-  __shared__ double s_pre;
-  __shared__ long long s_cpre;
+  __shared__ int s_last;
   if (grid_error(c)) return;
-  const unsigned epoch = static_cast<unsigned>(c.st->scan_epoch);
-  if (MODE != kScanRecords) {
-    if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&c.cnt_scan[2], 1u));
-    __syncthreads();
-  }
-  // dynamic tile id for the look-back modes: predecessors are already running
-  const int t = MODE != kScanRecords ? s_tile : static_cast<int>(blockIdx.x);
+  if (!SHARDED && threadIdx.x == 0 && blockIdx.x == 0) c.st->tstamp[0] = global_ns();
+  const int t = blockIdx.x;
   const long long base = static_cast<long long>(t) * TC::kTileT;
   const double lse = c.st->lse_g;
+  const double pre = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
+  const long long cpre = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
   ThreadTile<ITEMS> tt;
 #pragma unroll 4
   for (int i = 0; i < ITEMS; ++i) {
@@ -440,12 +402,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
     const long long k = base + e;
     double g = 0.0;
     if (k < c.N) {
-      if (MODE == kScanRecords) {
-        g = __ldcg(&c.g[k]);
-      } else {
-        g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
-        c.g[k] = g;
-      }
+      g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
+      c.g[k] = g;
     }
     sm.g[TC::sidx(e)] = g;
   }
@@ -460,65 +418,18 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   }
   SumCnt tot;
   const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
-  if (MODE == kScanRecords) {
-    if (threadIdx.x == 0) {
-      s_pre = c.shard_off[0] + __ldcg(&c.tile_pre[t]);  // (off + tile) + thread, as S3
-      s_cpre = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
-    }
-  } else if (threadIdx.x == 0) {
-    // decoupled look-back over approximate (any-order) tile sums
-    LookBack* lb = c.lookback;
-    double pre = 0.0;
-    long long cpre = 0;
-    if (t == 0) {
-      lb_store(lb + t, tot.s, static_cast<unsigned>(tot.c), ((epoch + 1) << 2) | 2u);
-    } else {
-      lb_store(lb + t, tot.s, static_cast<unsigned>(tot.c), ((epoch + 1) << 2) | 1u);
-      int k = t - 1;
-      while (true) {
-        const LookBack v = lb_load(lb + k);
-        if ((v.tag >> 2) != epoch + 1) continue;  // not yet published this step
-        pre += v.s;
-        cpre += v.cnt;
-        if ((v.tag & 3u) == 2u) break;
-        --k;
-      }
-      lb_store(lb + t, pre + tot.s, static_cast<unsigned>(cpre + tot.c), ((epoch + 1) << 2) | 2u);
-    }
-    s_pre = pre;
-    s_cpre = cpre;
-  }
-  __syncthreads();
-  if (MODE == kScanSums) {
-    if (threadIdx.x == 0) {
-      c.tile_pre[t] = s_pre;
-      c.tile_cnt_pre[t] = s_cpre;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
-      if (old == gridDim.x - 1) {
-        c.cnt_scan[1] = 0;
-        c.cnt_scan[2] = 0;
-        __threadfence();
-        const LookBack v = lb_load(c.lookback + (c.ntiles - 1));
-        c.shard_sum[0] = v.s;
-        c.shard_sum[1] = static_cast<double>(v.cnt);
-        c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
-      }
-    }
-    return;
-  }
-  tt.p[0] = s_pre + ex.s;
-  tt.cnt0 = s_cpre + ex.c;
+  tt.p[0] = pre + ex.s;
+  tt.cnt0 = cpre + ex.c;
   chunk_analyse<ITEMS>(tt);
-  tt.carry = block_excl_scan_piece(tt.agg, sw.pc);
-  tt.win_excl = block_excl_scan_int(tt.nwin, tt.win_total, sw.si);
-  const bool overflow = tt.win_total > kMaxWin;
+  const Piece carry = block_excl_scan_piece(tt.agg, sw.pc);
+  int win_total;
+  const int win_excl = block_excl_scan_int(tt.nwin, win_total, sw.si);
+  const bool overflow = win_total > kMaxWin;
+  c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x] =
+      ThreadRec{tt.p[0], tt.cnt0, carry.d0, carry.d1, carry.e, carry.flag, win_excl, 0};
   if (tt.nwin > 0 && !overflow) {
-    Piece acc = tt.carry;
-    int w = tt.win_excl;
+    Piece acc = carry;
+    int w = win_excl;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       Piece pc;
@@ -537,89 +448,68 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
     }
   }
   if (threadIdx.x == kThreads - 1) {
-    const Piece acc = piece_combine(tt.carry, tt.agg);
-    TileHdr h;
-    h.nwin = overflow ? -1 : tt.win_total;
-    h.tail_e = acc.e;
-    h.tail_d0 = acc.d0;
-    h.tail_d1 = acc.d1;
-    c.hdr[t] = h;
-    if (MODE == kScanFull) {
-      c.tile_pre[t] = s_pre;
-      c.tile_cnt_pre[t] = s_cpre;
-    }
+    const Piece acc = piece_combine(carry, tt.agg);
+    c.hdr[t] = TileHdr{overflow ? -1 : win_total, acc.e, acc.d0, acc.d1};
   }
-  if (MODE == kScanRecords) return;
+  if (SHARDED) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
     s_last = (old == gridDim.x - 1);
-    if (s_last) {
-      c.cnt_scan[1] = 0;
-      c.cnt_scan[2] = 0;
-    }
+    if (s_last) c.cnt_scan[1] = 0;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-
-  resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs, sw);
-  if (threadIdx.x == 0) c.st->scan_epoch = static_cast<int>((epoch + 1) & 0x3fffffffu);
+  if (threadIdx.x == 0) c.st->tstamp[1] = global_ns();
+  resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
+  if (threadIdx.x == 0) c.st->tstamp[2] = global_ns();
 }
 
 // Sharded: every rank resolves the exact chain over ALL shards' tiles.
 template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c) {
   __shared__ ResolverSmem rs;
-  __shared__ ScanScratch sw;
   if (grid_error(c)) return;
-  resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, rs, sw);
+  resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, rs);
 }
 
-// S3: exact per-element CDF, per-tile local guide and the coarse guide.
+// S3: exact per-element CDF (from the S2 per-thread handoff: no block
+// scans), per-tile local guide and the coarse guide.
 template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
   using TC = TileCfg<ITEMS>;
   __shared__ double sg[TC::kSmem];
-  __shared__ ScanScratch sw;
   if (grid_error(c)) return;
   const int t = blockIdx.x;
   const long long base = static_cast<long long>(t) * TC::kTileT;
   const int nwin = __ldcg(&c.hdr[t].nwin);
   const double2 ti = __ldcg(&c.tile_info[t]);
   const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
-  ThreadTile<ITEMS> tt;
-#pragma unroll 4
-  for (int i = 0; i < ITEMS; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    sg[TC::sidx(e)] = e < valid ? __ldcg(&c.g[base + e]) : 0.0;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) tt.g[i] = sg[TC::sidx(threadIdx.x * ITEMS + i)];
   double vals[ITEMS];
   if (nwin >= 0) {
-    SumCnt mine{0.0, 0};
+    ThreadTile<ITEMS> tt;
+    const double2* gsrc = reinterpret_cast<const double2*>(c.g + base + threadIdx.x * ITEMS);
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      mine.s += tt.g[i];
-      mine.c += (tt.g[i] != 0.0);
+    for (int i = 0; i < ITEMS / 2; ++i) {
+      const double2 v = __ldcg(gsrc + i);
+      const int e = threadIdx.x * ITEMS + 2 * i;
+      tt.g[2 * i] = e < valid ? v.x : 0.0;
+      tt.g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
     }
-    SumCnt tot;
-    const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
-    // same prefix as the records phase: global offset (sharded) + tile + thread
-    tt.p[0] = (c.shard_off[0] + __ldcg(&c.tile_pre[t])) + ex.s;
-    tt.cnt0 = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]) + ex.c;
+    const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
+    tt.p[0] = tr.p0;
+    tt.cnt0 = tr.cnt0;
     chunk_analyse<ITEMS>(tt);
-    tt.carry = block_excl_scan_piece(tt.agg, sw.pc);
-    tt.win_excl = block_excl_scan_int(tt.nwin, tt.win_total, sw.si);
-    int w = tt.win_excl;
+    const Piece carry{tr.d0, tr.d1, tr.e, tr.flag};
+    int w = tr.win_excl;
     double seg = w > 0 ? __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w - 1]) : ti.x;
+    bool ok = true;
     if (tt.uniform_e != kNoBinade || tt.lc[ITEMS] == 0) {
       // no window in this chunk: one exact base value, then integer steps
       double s0 = seg;
-      piece_apply(tt.carry, s0);
+      ok &= piece_apply(carry, s0);
       if (tt.lc[ITEMS] == 0) {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
@@ -627,6 +517,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
         const int e = tt.uniform_e;
         const double scale = scale2(1.0, 52 - e);
         long long m = static_cast<long long>(scale2(s0, 52 - e));
+        const long long m_hi = 1LL << 53;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           if (tt.g[i] != 0.0) {
@@ -636,9 +527,10 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
           }
           vals[i] = scale2(static_cast<double>(m), e - 52);
         }
+        ok &= m < m_hi && binade_of(s0) == e;  // self-check of the bound
       }
     } else {
-      Piece acc = tt.carry;
+      Piece acc = carry;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         Piece pc;
@@ -650,11 +542,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
           ++w;
           sk = seg;
         } else {
-          piece_apply(acc, sk);
+          ok &= piece_apply(acc, sk);
         }
         vals[i] = sk;
       }
     }
+    if (!ok) atomicOr(&c.st->error, kErrInternal);
   } else {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -662,7 +555,6 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
       vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
     }
   }
-  __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x * ITEMS + i;
@@ -725,20 +617,16 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
   const bool small = c.tile_log2 == 11;
   switch (which) {
     case 1:
-      if (small) k_scan_pieces<8, kScanFull><<<ntiles, kThreads, 0, st>>>(c);
-      else k_scan_pieces<16, kScanFull><<<ntiles, kThreads, 0, st>>>(c);
+      if (small) k_scan_pieces<8, 0><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_pieces<16, 0><<<ntiles, kThreads, 0, st>>>(c);
       break;
     case 2:
       if (small) k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
       else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
       break;
-    case 3:
-      if (small) k_scan_pieces<8, kScanSums><<<ntiles, kThreads, 0, st>>>(c);
-      else k_scan_pieces<16, kScanSums><<<ntiles, kThreads, 0, st>>>(c);
-      break;
     case 4:
-      if (small) k_scan_pieces<8, kScanRecords><<<ntiles, kThreads, 0, st>>>(c);
-      else k_scan_pieces<16, kScanRecords><<<ntiles, kThreads, 0, st>>>(c);
+      if (small) k_scan_pieces<8, 1><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_pieces<16, 1><<<ntiles, kThreads, 0, st>>>(c);
       break;
     case 5:
       if (small) k_resolve_global<8><<<1, kThreads, 0, st>>>(c);
@@ -770,6 +658,7 @@ __global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp
   __shared__ double scratch[kWarps * 2];
   __shared__ double fin[2];
   if (grid_error(c)) return;
+  __shared__ double s_lse;
   combine_partials<1, false>(gp, ngroups, fin, scratch);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -777,7 +666,11 @@ __global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp
     const double lse = isfinite(mx) ? mx + log(fin[1]) : kNegInf;
     c.st->lse_g = lse;
     if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+    s_lse = lse;
   }
+  __syncthreads();
+  // local tile prefixes + this shard's total (allgathered next, phase B)
+  if (isfinite(s_lse)) tile_prefixes(c, s_lse);
 }
 
 // ---- sharded ancestor migration (pull model) ---------------------------
@@ -850,6 +743,36 @@ __global__ void k_shard_offset(Ctx c, const double* gathered) {
   }
   c.shard_off[0] = s;
   c.shard_off[1] = n;
+}
+
+// Injected-fitness parity path (pfsmc_gpu_resample_from_g): tile sums of
+// the given g (in place of the predict kernel's block partials), then the
+// same tile prefixes with lse = 0.
+__global__ void __launch_bounds__(kThreads) k_gin_tiles(Ctx c) {
+  __shared__ double scratch[kWarps * 2];
+  const long long base = static_cast<long long>(blockIdx.x) << c.tile_log2;
+  const int tile = 1 << c.tile_log2;
+  double s = 0.0;
+  int n = 0;
+  for (int e = threadIdx.x; e < tile; e += kThreads) {
+    const long long k = base + e;
+    const double g = k < c.N ? c.gin[k] : 0.0;
+    s += g;
+    n += (g != 0.0);
+  }
+  double v[2] = {s, static_cast<double>(n)};
+  block_sums<2>(v, scratch);  // fixed-order tree; counts are exact small integers
+  if (threadIdx.x == 0) {
+    c.trel[blockIdx.x] = v[0];
+    c.tile_cnt_pre[blockIdx.x] = static_cast<long long>(v[1]);
+  }
+  const int ngroups = (c.ntiles * (tile / kThreads) + kGroup - 1) / kGroup;
+  for (int g = blockIdx.x * kThreads + threadIdx.x; g < ngroups; g += gridDim.x * kThreads) c.gpart[2 * g] = 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_gin_prefix(Ctx c) {
+  if (threadIdx.x == 0) c.st->lse_g = 0.0;
+  tile_prefixes(c, 0.0);
 }
 
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
@@ -1199,8 +1122,9 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.gtile_info = s->dalloc<double2>(GNT);
     c.tile_info = c.gtile_info + c.tile0;
     c.g = s->dalloc<double>(N);
-    c.lookback = s->dalloc<LookBack>(NT);
-    CK(cudaMemset(c.lookback, 0, sizeof(LookBack) * NT));
+    c.blk_cnt = s->dalloc<int>(static_cast<size_t>(s->grid));
+    c.trel = s->dalloc<double>(NT);
+    c.trec = s->dalloc<ThreadRec>(NT * kThreads);
     c.tile_pre = s->dalloc<double>(NT);
     c.tile_cnt_pre = s->dalloc<long long>(NT);
     c.ghdr = s->dalloc<TileHdr>(GNT);
@@ -1475,6 +1399,16 @@ pfsmc_gpu_status pfsmc_gpu_get_step_diagnostics(pfsmc_gpu_sampler* s, uint32_t* 
   });
 }
 
+pfsmc_gpu_status pfsmc_gpu_debug_timestamps(pfsmc_gpu_sampler* s, uint64_t* out8) {
+  return guarded([&] {
+    DevState h{};
+    CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    for (int i = 0; i < 8; ++i) out8[i] = h.tstamp[i];
+    return PFSMC_GPU_OK;
+  });
+}
+
 pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g, uint64_t j,
                                            uint32_t* ancestors_out, double* cdf_out) {
   return guarded([&] {
@@ -1490,6 +1424,8 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
     Ctx c = s->ctx;
     c.gin = dg;
+    k_gin_tiles<<<s->ntiles, kThreads, 0, s->stream>>>(c);
+    k_gin_prefix<<<1, kThreads, 0, s->stream>>>(c);
     launch_scan(c, s->ntiles, s->stream, 1);
     launch_scan(c, s->ntiles, s->stream, 2);
     k_search_only<<<s->grid, kThreads, 0, s->stream>>>(c);
@@ -1585,14 +1521,6 @@ pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, 
 pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     k_finish_lse<<<1, kThreads, 0, s->stream>>>(s->ctx, s->gp_pred_all, s->ngroups_pred * s->world);
-    CK(cudaGetLastError());
-    return PFSMC_GPU_OK;
-  });
-}
-
-pfsmc_gpu_status pfsmc_gpu_shard_scan_sums(pfsmc_gpu_sampler* s) {
-  return guarded([&] {
-    launch_scan(s->ctx, s->ntiles, s->stream, 3);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });

@@ -63,7 +63,7 @@ class GpuShard(GpuSampler):
                     obs.sigma, LIKELIHOODS[obs.likelihood], device)
         L = self.lib
         for name in ("pfsmc_gpu_create_shard", "pfsmc_gpu_shard_buffer", "pfsmc_gpu_shard_predict",
-                     "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_sums", "pfsmc_gpu_shard_scan_records",
+                     "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_records",
                      "pfsmc_gpu_shard_resolve", "pfsmc_gpu_shard_serve", "pfsmc_gpu_shard_update",
                      "pfsmc_gpu_shard_moments", "pfsmc_gpu_shard_finish_moments"):
             getattr(L, name).restype = C.c_int
@@ -96,9 +96,6 @@ class GpuShard(GpuSampler):
 
     def finish_lse(self):
         self._check(self.lib.pfsmc_gpu_shard_finish_lse(self.h))
-
-    def scan_sums(self):
-        self._check(self.lib.pfsmc_gpu_shard_scan_sums(self.h))
 
     def scan_records(self):
         self._check(self.lib.pfsmc_gpu_shard_scan_records(self.h))
@@ -291,8 +288,7 @@ class ShardedFilter:
         sh, comm = self.shards, self.comm
         self._each(lambda s: s.predict(y, j, t_prev, t_obs, h))
         comm.allgather(sh, BUF_PRED, BUF_PRED_ALL)                       # A
-        self._each(lambda s: s.finish_lse())
-        self._each(lambda s: s.scan_sums())
+        self._each(lambda s: s.finish_lse())                             # (+ local tile prefixes)
         comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # B
         self._each(lambda s: s.scan_records())
         comm.allgather_slices(sh, BUF_HDR)                               # C

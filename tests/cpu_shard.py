@@ -144,8 +144,6 @@ class CpuShard:
         if not np.isfinite(lse):
             raise NumericalError("total degeneracy: every particle has zero predictive likelihood")
         self.lse_g = lse
-
-    def scan_sums(self):
         self.g = np.exp(self.lg - self.lse_g)
         self.bufs[2][:] = [self.g.sum(), np.count_nonzero(self.g)]
 

@@ -391,3 +391,27 @@ def test_sharded_shards_reproduce_single_handle_bitwise(world):
     single.close()
     for s in shards:
         s.close()
+
+
+def test_free_running_full_size_lv():
+    """BASELINE config 2 size (N = 2^20): 10 free-running steps, ancestors
+    bit-exact against the oracle and the trace within 1e-8."""
+    from paper_1411_1702_b200 import problems
+    n, steps = 1 << 20, 10
+    prob = problems.lotka_volterra(particles=n, T=steps, seed=1)
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=1, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 1, **prob.prior)
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    tp = 0.0
+    for j in range(1, steps + 1):
+        t1 = prob.times[j - 1]
+        row = gpu.pf_step(prob.ys[j - 1], j, tp, t1)
+        trace_o, dg = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1, diag=True)
+        anc_g, _, _ = gpu.step_diagnostics()
+        mism = np.count_nonzero(anc_g.astype(np.int64) != dg["ancestors"])
+        assert mism == 0, f"step {j}: {mism} ancestors differ"
+        tr = np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]])
+        assert _rel(tr, trace_o) < REL_TRACE, j
+        tp = t1
+    gpu.close()
