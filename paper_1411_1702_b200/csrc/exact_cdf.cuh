@@ -119,16 +119,17 @@ __device__ __forceinline__ int classify(double g, double p_prev, long long cnt_p
 }
 
 // Apply a segment aggregate to the exact running sum s (which the
-// classification guarantees lies in binade a.e). Returns false on an
-// internal inconsistency (never expected; reported as INTERNAL).
+// classification guarantees lies in binade a.e). In that binade s = m u with
+// u = 2^(e-52), and the parity of m is the lowest significand bit of s, so
+// the update is one exact IEEE add: s + delta u is representable (it stays in
+// the binade, or lands exactly on 2^(e+1)). Returns false on an internal
+// inconsistency (never expected; reported as INTERNAL).
 __device__ __forceinline__ bool piece_apply(const Piece& a, double& s) {
   if (a.e == kNoBinade) return true;
   if (binade_of(s) != a.e) return false;
-  const double ms = scale2(s, 52 - a.e);
-  const long long m = static_cast<long long>(ms);
-  const long long m2 = m + ((m & 1) ? a.d1 : a.d0);
-  s = scale2(static_cast<double>(m2), a.e - 52);
-  return static_cast<double>(m) == ms;
+  const long long delta = (__double_as_longlong(s) & 1) ? a.d1 : a.d0;
+  s = s + scale2(static_cast<double>(delta), a.e - 52);
+  return true;
 }
 
 }  // namespace pfsmc_gpu

@@ -180,9 +180,10 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   const int ngroups = (nblocks + kGroup - 1) / kGroup;
   const int g = blockIdx.x / kGroup;
   const int gsize = min(kGroup, nblocks - g * kGroup);
-  __threadfence();
+  // the block partial was written by thread 0 only: it alone fences
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned old = atomicAdd(&counters[g], 1u);
     s_flag = (old == static_cast<unsigned>(gsize - 1));
     if (s_flag) counters[g] = 0;
@@ -195,7 +196,7 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   hook(g, gsize);
   if (!final_level) return false;  // sharded: the group partials are exported
-  __threadfence();
+  __threadfence();  // the hook's writes (any thread) and the group partial
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned old = atomicAdd(&counters[ngroups], 1u);

@@ -247,124 +247,163 @@ __device__ __forceinline__ ResScan block_excl_scan_res(ResScan v, ResScan& tot, 
   return ex;
 }
 
-constexpr int kResolveWin = 512;  // windows staged in smem by the resolver
+constexpr int kResolveWin = 256;    // windows staged in smem by the resolver
+constexpr int kMaxSuper = 16;       // tiles per resolver thread (super-tile)
+constexpr int kStageSuper = 32;     // windowed super-tiles whose headers are staged
 
 struct ResolverSmem {
   TileWin win[kResolveWin];
-  TileHdr hdr[kThreads];
+  const TileWin* wsrc[kResolveWin];
+  TileHdr hdr[kStageSuper * kMaxSuper];
   Piece excl[kThreads];
   double out[kThreads];
-  double in[kThreads];
   int wlist[kThreads];
   ResScan rsw[2 * kWarps];
-  double carry, next;
+  double carry;
   int bad;
 };
 
-// The exact chain over tiles, one block: a segmented monoid scan across
-// window-free tiles and an in-order IEEE walk over the windows only, with
-// everything the walk touches staged in shared memory. Used for the single
-// handle (own tiles) and, sharded, for all shards' tiles on every rank.
+// The exact chain over tiles, one block. Each thread owns a run of K
+// consecutive tiles (a super-tile); window-free super-tiles compose in a
+// segmented monoid scan, the windowed ones are walked in order by one
+// thread with real IEEE adds at the windows; everything that walk touches
+// is staged in shared memory. Used for the single handle (own tiles) and,
+// sharded, for all shards' tiles on every rank.
 template <int ITEMS>
 __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
                               double2* tile_info, int ntiles, bool own_g, ResolverSmem& rs) {
   using TC = TileCfg<ITEMS>;
+  const int K = min(kMaxSuper, (ntiles + kThreads - 1) / kThreads);
   if (threadIdx.x == 0) {
     rs.carry = 0.0;
     rs.bad = 0;
   }
   __syncthreads();
-  for (int b0 = 0; b0 < ntiles; b0 += kThreads) {
-    const int ti = b0 + threadIdx.x;
-    const bool valid = ti < ntiles;
-    TileHdr h{0, kNoBinade, 0, 0};
-    if (valid) {
-      h.nwin = __ldcg(&hdr[ti].nwin);
-      h.tail_e = __ldcg(&hdr[ti].tail_e);
-      h.tail_d0 = __ldcg(&hdr[ti].tail_d0);
-      h.tail_d1 = __ldcg(&hdr[ti].tail_d1);
+  auto load_hdr = [&](int ti) {
+    TileHdr h;
+    h.nwin = __ldcg(&hdr[ti].nwin);
+    h.tail_e = __ldcg(&hdr[ti].tail_e);
+    h.tail_d0 = __ldcg(&hdr[ti].tail_d0);
+    h.tail_d1 = __ldcg(&hdr[ti].tail_d1);
+    return h;
+  };
+  for (int b0 = 0; b0 < ntiles; b0 += kThreads * K) {
+    const int tb = b0 + threadIdx.x * K;
+    const int te = min(tb + K, ntiles);
+    // compose the super-tile (pure if none of its tiles has a window)
+    Piece agg = piece_identity();
+    bool windowed = false;
+    int nw = 0;
+    for (int ti = tb; ti < te; ++ti) {
+      const TileHdr h = load_hdr(ti);
+      if (h.nwin != 0) {
+        windowed = true;
+        nw += h.nwin > 0 ? h.nwin : 0;
+      } else {
+        agg = piece_combine(agg, Piece{h.tail_d0, h.tail_d1, h.tail_e, 0});
+      }
     }
-    const bool windowed = valid && h.nwin != 0;
-    const Piece agg{h.tail_d0, h.tail_d1, h.tail_e, 0};
-    ResScan mine{windowed ? Piece{0, 0, kNoBinade, 1} : agg, windowed ? 1 : 0,
-                 windowed && h.nwin > 0 ? h.nwin : 0};
+    ResScan mine{windowed ? Piece{0, 0, kNoBinade, 1} : agg, windowed ? 1 : 0, windowed ? nw : 0};
     ResScan tot;
+    if (threadIdx.x == 0 && b0 == 0) c.st->tstamp[3] = global_ns();
     const ResScan ex = block_excl_scan_res(mine, tot, rs.rsw);
     const int nwt = tot.rank;
-    const int rank = ex.rank;
+    if (threadIdx.x == 0 && b0 == 0) {
+      c.st->tstamp[4] = global_ns();
+      c.st->tstamp[7] = static_cast<unsigned long long>(nwt) * 100000ull + tot.wofs;
+    }
     if (windowed) {
-      rs.wlist[rank] = ti;
-      rs.excl[rank] = ex.pc;
-      rs.hdr[rank] = h;
-      for (int k = 0; k < h.nwin && ex.wofs + k < kResolveWin; ++k)
-        rs.win[ex.wofs + k] = win[static_cast<size_t>(ti) * kMaxWin + k];
+      rs.wlist[ex.rank] = threadIdx.x;
+      rs.excl[ex.rank] = ex.pc;
+      if (ex.rank < kStageSuper)
+        for (int ti = tb; ti < te; ++ti) rs.hdr[ex.rank * kMaxSuper + (ti - tb)] = load_hdr(ti);
+      int w = ex.wofs;  // record where the windows live; loaded cooperatively below
+      for (int ti = tb; ti < te; ++ti) {
+        const int n = __ldcg(&hdr[ti].nwin);
+        for (int k = 0; k < n && w < kResolveWin; ++k, ++w) rs.wsrc[w] = win + static_cast<size_t>(ti) * kMaxWin + k;
+      }
     }
     __syncthreads();
+    for (int w = threadIdx.x; w < min(tot.wofs, kResolveWin); w += kThreads) rs.win[w] = *rs.wsrc[w];
+    __syncthreads();
+    if (threadIdx.x == 0 && b0 == 0) c.st->tstamp[5] = global_ns();
     if (threadIdx.x == 0) {
-      // in-order IEEE walk over the windowed tiles of this chunk
+      // in-order walk over the windowed super-tiles of this chunk
       double seg = rs.carry;
       int wo = 0;
       bool ok = true;
       for (int r = 0; r < nwt; ++r) {
-        const int wt = rs.wlist[r];
-        const TileHdr wh = rs.hdr[r];
+        const int st0 = b0 + rs.wlist[r] * K;
+        const int st1 = min(st0 + K, ntiles);
         double s = seg;
         ok &= piece_apply(rs.excl[r], s);
-        rs.in[r] = s;
-        if (wh.nwin < 0 && !own_g) {
-          ok = false;  // window overflow in a remote tile: unsupported when sharded
-        } else if (wh.nwin < 0) {
-          // serial tile (window overflow): plain sequential sum, CDF written here
-          const long long tb = static_cast<long long>(wt) * TC::kTileT;
-          for (int e = 0; e < TC::kTileT && tb + e < c.N; ++e) {
-            s = s + __ldcg(&c.g[tb + e]);
-            c.cdf[tb + e] = s;
-          }
-        } else {
-          for (int k = 0; k < wh.nwin; ++k, ++wo) {
-            TileWin tw;
-            if (wo < kResolveWin) {
-              tw = rs.win[wo];
-            } else {
-              const TileWin* gw = win + static_cast<size_t>(wt) * kMaxWin + k;
-              tw.g = __ldcg(&gw->g);
-              tw.e = __ldcg(&gw->e);
-              tw.d0 = __ldcg(&gw->d0);
-              tw.d1 = __ldcg(&gw->d1);
+        for (int ti = st0; ti < st1; ++ti) {
+          const TileHdr wh = r < kStageSuper ? rs.hdr[r * kMaxSuper + (ti - st0)] : load_hdr(ti);
+          const double s_in = s;
+          if (wh.nwin < 0 && !own_g) {
+            ok = false;  // window overflow in a remote tile: unsupported when sharded
+          } else if (wh.nwin < 0) {
+            // serial tile (window overflow): plain sequential sum, CDF written here
+            const long long tbase = static_cast<long long>(ti) * TC::kTileT;
+            for (int e = 0; e < TC::kTileT && tbase + e < c.N; ++e) {
+              s = s + __ldcg(&c.g[tbase + e]);
+              c.cdf[tbase + e] = s;
             }
-            ok &= piece_apply(Piece{tw.d0, tw.d1, tw.e, 0}, s);
-            s = s + tw.g;  // the window element: a real IEEE add, as acc += g[i]
-            win_after[static_cast<size_t>(wt) * kMaxWin + k] = s;
+          } else {
+            for (int k = 0; k < wh.nwin; ++k, ++wo) {
+              TileWin tw;
+              if (wo < kResolveWin) {
+                tw = rs.win[wo];
+              } else {
+                const TileWin* gw = win + static_cast<size_t>(ti) * kMaxWin + k;
+                tw.g = __ldcg(&gw->g);
+                tw.e = __ldcg(&gw->e);
+                tw.d0 = __ldcg(&gw->d0);
+                tw.d1 = __ldcg(&gw->d1);
+              }
+              ok &= piece_apply(Piece{tw.d0, tw.d1, tw.e, 0}, s);
+              s = s + tw.g;  // the window element: a real IEEE add, as acc += g[i]
+              win_after[static_cast<size_t>(ti) * kMaxWin + k] = s;
+            }
+            ok &= piece_apply(Piece{wh.tail_d0, wh.tail_d1, wh.tail_e, 0}, s);
           }
-          ok &= piece_apply(Piece{wh.tail_d0, wh.tail_d1, wh.tail_e, 0}, s);
+          double s_end = s;
+          if (ti == ntiles - 1) {
+            c.st->total_mass = s_end;
+            s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
+          }
+          tile_info[ti] = make_double2(s_in, s_end);
         }
         rs.out[r] = s;
         seg = s;
       }
       if (!ok) rs.bad = 1;
+      if (b0 == 0) c.st->tstamp[6] = global_ns();
     }
     __syncthreads();
-    if (valid) {
-      double s_in, s_end;
-      if (windowed) {
-        s_in = rs.in[rank];
-        s_end = rs.out[rank];
-      } else {
-        s_in = rank > 0 ? rs.out[rank - 1] : rs.carry;
-        bool ok = piece_apply(ex.pc, s_in);
-        s_end = s_in;
-        ok &= piece_apply(agg, s_end);
-        if (!ok) rs.bad = 1;
+    if (tb < te && !windowed) {
+      double s = ex.rank > 0 ? rs.out[ex.rank - 1] : rs.carry;
+      bool ok = piece_apply(ex.pc, s);
+      for (int ti = tb; ti < te; ++ti) {
+        const TileHdr h = load_hdr(ti);
+        const double s_in = s;
+        ok &= piece_apply(Piece{h.tail_d0, h.tail_d1, h.tail_e, 0}, s);
+        double s_end = s;
+        if (ti == ntiles - 1) {
+          c.st->total_mass = s_end;
+          s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
+        }
+        tile_info[ti] = make_double2(s_in, s_end);
       }
-      if (ti == ntiles - 1) {
-        c.st->total_mass = s_end;
-        s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
-      }
-      tile_info[ti] = make_double2(s_in, s_end);
-      if (threadIdx.x == min(kThreads, ntiles - b0) - 1) rs.next = s_end;
+      if (!ok) rs.bad = 1;
     }
     __syncthreads();
-    if (threadIdx.x == 0) rs.carry = rs.next;
+    // the chunk's exact end value: the last super-tile's end
+    if (threadIdx.x == 0) {
+      const int last = min(b0 + kThreads * K, ntiles) - 1;
+      const double2 v = __ldcg(&tile_info[last]);
+      rs.carry = (last == ntiles - 1) ? c.st->total_mass : v.y;
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0 && rs.bad) atomicOr(&c.st->error, kErrInternal);

@@ -9,4 +9,6 @@ tp=0.0
 for j in range(1,11):
     g.pf_step(prob.ys[j-1],j,tp,prob.times[j-1]); tp=prob.times[j-1]
     g.lib.pfsmc_gpu_debug_timestamps(g.h,ts)
-    print(j, "scan->resolver start %.1f us, resolver %.1f us"%((ts[1]-ts[0])/1e3,(ts[2]-ts[1])/1e3))
+    print(j, "scan->resolver start %.1f us, resolver %.1f us"%((ts[1]-ts[0])/1e3,(ts[2]-ts[1])/1e3),
+          "| hdr+compose %.1f, scan %.1f, stage %.1f, walk %.1f us; windowed super-tiles %d, windows %d" % (
+          (ts[3]-ts[1])/1e3, (ts[4]-ts[3])/1e3, (ts[5]-ts[4])/1e3, (ts[6]-ts[5])/1e3, ts[7]//100000, ts[7]%100000))
