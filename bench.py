@@ -156,6 +156,107 @@ def run_reference_arm(args, world, rank):
     return 0
 
 
+def fp64_peak(device):
+    import ctypes
+    from paper_1411_1702_b200.sampler import load_library
+    lib = load_library()
+    lib.pfsmc_gpu_fp64_peak.restype = ctypes.c_int
+    v = ctypes.c_double()
+    rc = lib.pfsmc_gpu_fp64_peak(device, ctypes.byref(v))
+    return v.value if rc == 0 else None
+
+
+def _timed_steps(gpu, prob, steps, warmup, stream):
+    """Blocking drop-in steps with per-step events (L2 flushed between)."""
+    import torch
+    ms, j, tp = [], 0, 0.0
+    iters = []
+    for k in range(warmup + steps):
+        j += 1
+        t1 = prob.times[j - 1]
+        gpu.flush_l2()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+        gpu.pf_step(prob.ys[j - 1], j, tp, t1, h=prob.h_for(tp, t1))
+        with torch.cuda.stream(stream):
+            b.record(stream)
+        torch.cuda.synchronize()
+        if k >= warmup:
+            ms.append(a.elapsed_time(b))
+            iters.append(gpu.step_diagnostics()[2])
+        tp = t1
+    return ms, iters
+
+
+def bench_workloads(local, fp64):
+    """BASELINE configs 3-5 on one GPU (extra lines of the report; the
+    headline metric is config 2)."""
+    import numpy as np
+    import torch
+    from paper_1411_1702_b200 import problems
+    from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
+    peaks, _ = _peaks()
+    hbm = float(peaks["hbm_gbs"])
+    out = {}
+    # config 5: resample / reduction bandwidth, 2^25 x 64-byte records
+    n5 = 1 << 25
+    s = GpuSampler("payload64", PfConfig(particles=n5, seed=5), ObservationModel([0], 1.0), device=local)
+    rng = np.random.default_rng(0)
+    s.set_ensemble(Ensemble(rng.standard_normal((n5, 6)), rng.standard_normal((n5, 2)), np.zeros(n5),
+                            np.zeros(2), np.eye(2)))
+    stream = torch.cuda.ExternalStream(s.stream_handle, device=local)
+    c5 = {}
+    for sigma in (0.1, 1.0, 4.0):
+        s.c5_set_logweights(sigma, 1)
+        ms = []
+        for it in range(7):
+            s.flush_l2()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+            s.c5_iteration(it + 1)
+            with torch.cuda.stream(stream):
+                b.record(stream)
+            s.synchronize()
+            if it >= 2:
+                ms.append(a.elapsed_time(b))
+        t = sum(ms) / len(ms)
+        gbs = 184.0 * n5 / (t / 1e3) / 1e9
+        c5[f"sigma={sigma}"] = {"ms_per_iteration": t, "particle_iterations_per_s": n5 / (t / 1e3),
+                               "hbm_gbs_algorithmic": gbs, "frac_of_measured_hbm": gbs / hbm}
+    s.close()
+    out["c5_resample_bandwidth"] = {"particles": n5, "record_bytes": 64, "bytes_per_particle_iteration": 184,
+                                    "results": c5}
+    # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal (first log-spaced intervals)
+    n3 = 1 << 22
+    prob = problems.robertson(particles=n3, T=400, seed=1)
+    g = GpuSampler("robertson", prob.cfg, prob.obs, device=local)
+    prob.init(g)
+    ms, it = _timed_steps(g, prob, 5, 2, torch.cuda.ExternalStream(g.stream_handle, device=local))
+    t = sum(ms) / len(ms)
+    out["c3_robertson"] = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4", "steps": len(ms),
+                           "ms_per_step": t, "particle_steps_per_s": n3 / (t / 1e3),
+                           "newton_iterations_per_particle_step": float(np.mean(it)) / n3}
+    g.close()
+    # config 4: 8-compartment chain, 2^24, BDF3 m=3
+    n4 = 1 << 24
+    prob = problems.chain8(particles=n4, T=10, seed=1)
+    g = GpuSampler("chain", prob.cfg, prob.obs, device=local)
+    prob.init(g)
+    ms, it = _timed_steps(g, prob, 2, 1, torch.cuda.ExternalStream(g.stream_handle, device=local))
+    t = sum(ms) / len(ms)
+    newton = float(np.mean(it)) / n4
+    flops = 2 * 643 * newton  # survey §8(d): N_it(8) = 643 flops per Newton iteration (dominant term)
+    tfl = flops * n4 / (t / 1e3) / 1e12
+    out["c4_chain8"] = {"particles": n4, "integrator": "bdf3, m=3", "steps": len(ms), "ms_per_step": t,
+                        "particle_steps_per_s": n4 / (t / 1e3), "newton_iterations_per_particle_step": newton,
+                        "fp64_tflops_newton_only": tfl, "fp64_peak_tflops_measured": fp64,
+                        "frac_of_fp64_peak": (tfl / fp64) if fp64 else None}
+    g.close()
+    return out
+
+
 def run_sharded(args, world, rank, local):
     """N > 1: ONE global filter of n * world particles sharded over the GPUs
     (weak scaling), NCCL collectives + ancestor migration.
@@ -235,6 +336,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
+    ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")
     args = ap.parse_args()
     world, rank, local = _dist()
     if args.impl == "reference":
@@ -346,6 +448,13 @@ def main():
             "gpu_launches": len(kt) * args.steps,
             "e2e": e2e, "clocks": clk.summary(),
             "final_trace": {"theta_mean": list(map(float, last[:P])), "ess": float(last[-1])}}
+    fp64 = fp64_peak(local)
+    line["fp64_peak_tflops_measured"] = fp64
+    if world == 1 and not args.no_workloads:
+        try:
+            line["workloads"] = bench_workloads(local, fp64)
+        except Exception as e:  # the headline line must still print
+            line["workloads"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(N_PER_GPU, 20, 15.0, len(os.sched_getaffinity(0)), prob)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

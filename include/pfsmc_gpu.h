@@ -46,7 +46,8 @@ enum {
   PFSMC_GPU_MODEL_DECAY = 0,      /* x' = -theta x (reference test model) */
   PFSMC_GPU_MODEL_LOTKA_VOLTERRA = 1,
   PFSMC_GPU_MODEL_ROBERTSON = 2,
-  PFSMC_GPU_MODEL_CHAIN8 = 3
+  PFSMC_GPU_MODEL_CHAIN8 = 3,
+  PFSMC_GPU_MODEL_PAYLOAD64 = 4   /* 64-byte record, resample microbenchmark only */
 };
 /* lmm::Family (lmm.hpp:12) */
 enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
@@ -156,6 +157,17 @@ void* pfsmc_gpu_stream(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_set_kernel_timing(pfsmc_gpu_sampler* s, int enable);
 pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, int* n_kernels,
                                         const char** names_out);
+
+/* BASELINE config 5 (resample / reduction bandwidth), PAYLOAD64 handles:
+ * draw i.i.d. N(0, sigma^2) log-weights (keyed stream (seed, key, n, init)),
+ * then enqueue iterations of: log-sum-exp, weighted 2x2 covariance of
+ * theta, exact multinomial resampling, gather of the 64-byte records. */
+pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key);
+pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
+
+/* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop; the FP64
+ * roofline denominator the benchmarks report against). */
+pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops);
 
 /* L2 flush helper for benchmarks: writes a device buffer larger than L2 on
  * the sampler's stream. */

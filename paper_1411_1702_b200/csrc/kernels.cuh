@@ -735,6 +735,7 @@ std::unique_ptr<KernelSet> make_kernels_decay(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_lv(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_robertson(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_chain(int fam, int order);
+std::unique_ptr<KernelSet> make_kernels_payload(int fam, int order);
 
 inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
   switch (model) {
@@ -742,6 +743,7 @@ inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
     case LotkaVolterraModel::ID: return make_kernels_lv(fam, order);
     case RobertsonModel::ID: return make_kernels_robertson(fam, order);
     case ChainModel::ID: return make_kernels_chain(fam, order);
+    case Payload64Model::ID: return make_kernels_payload(fam, order);
   }
   return nullptr;
 }

@@ -814,6 +814,111 @@ __global__ void __launch_bounds__(kThreads) k_gin_prefix(Ctx c) {
   tile_prefixes(c, 0.0);
 }
 
+// ---- BASELINE config 5: resample / reduction bandwidth microbenchmark ----
+// One iteration over the resident 64-byte records {x[4], h[2], theta[2]}:
+// log-sum-exp of lw (+ the exact scan's tile offsets), the weighted 2x2
+// parameter covariance, the exact multinomial resampling and the gather of
+// the ancestors' records into the next buffer.
+__global__ void __launch_bounds__(kThreads) k_c5_weights(Ctx c, double sigma, unsigned long long key) {
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  double z[1];
+  stream_normals<1>(c.seed, key, c.n0 + n, kInit, z);
+  c.lw[n] = sigma * z[0];
+}
+
+__global__ void __launch_bounds__(kThreads) k_c5_lse(Ctx c) {
+  __shared__ double scratch[kWarps * 2];
+  __shared__ double fin[2];
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const double x = n < c.N ? c.lw[n] : -INFINITY;
+  const double one[1] = {1.0};
+  const int nfin = __syncthreads_count(isfinite(x) != 0);
+  if (threadIdx.x == 0) c.blk_cnt[blockIdx.x] = nfin;
+  block_partial<1, false>(x, one, c.part + blockIdx.x * 2, scratch);
+  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, true, TileGroupHook{&c})) {
+    __shared__ double s_lse;
+    if (threadIdx.x == 0) {
+      const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
+      c.st->lse_g = lse;
+      if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+      s_lse = lse;
+    }
+    __syncthreads();
+    if (isfinite(s_lse)) tile_prefixes(c, s_lse);
+  }
+}
+
+// weighted mean / covariance of theta (weighted_mean_cov, linalg.cpp:389-432)
+// with w = exp(lw - lse): plain block sums about the previous mean.
+__global__ void __launch_bounds__(kThreads) k_c5_moments(Ctx c) {
+  __shared__ double scratch[kWarps * 6];
+  __shared__ double fin[7];
+  if (grid_error(c)) return;
+  DevState& st = *c.st;
+  const double lse = st.lse_g;
+  const double k0 = st.mu[0], k1 = st.mu[1];
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double x = -INFINITY;
+  if (n < c.N) {
+    const double2 th = __ldg(reinterpret_cast<const double2*>(c.rec[st.cur] + n * c.R + 6));
+    x = c.lw[n] - lse;
+    const double d0 = th.x - k0, d1 = th.y - k1;
+    v[0] = d0;
+    v[1] = d1;
+    v[2] = d0 * d0;
+    v[3] = d0 * d1;
+    v[4] = d1 * d1;
+  }
+  double vals[6] = {1.0, v[0], v[1], v[2], v[3], v[4]};
+  block_partial<6, false>(x, vals, c.part + static_cast<size_t>(blockIdx.x) * 7, scratch);
+  if (tree_reduce_last<6, false>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+    if (threadIdx.x == 0) {
+      const double S = fin[1];
+      const double m0 = fin[2] / S, m1 = fin[3] / S;
+      st.mu[0] = k0 + m0;
+      st.mu[1] = k1 + m1;
+      st.cov[0] = fin[4] / S - m0 * m0;
+      st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
+      st.cov[3] = fin[6] / S - m1 * m1;
+    }
+  }
+}
+
+// Survival of the fittest straight into the next record buffer.
+__global__ void __launch_bounds__(kThreads) k_c5_serve(Ctx c, unsigned long long j) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const double u = resample_uniform(c.seed, j, c.n0 + n);
+  const unsigned a = find_ancestor(c, u);
+  c.anc[n] = a;
+  const int cur = c.st->cur;
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur] + static_cast<long long>(a) * c.R);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1] + n * c.R);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = __ldg(src + i);
+}
+
+__global__ void k_flip(DevState* st) { st->cur ^= 1; }
+
+// FP64 roofline denominator: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(kThreads) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += x[i];
+  if (acc == 12345.678) out[0] = acc;  // keeps the chains live
+}
+
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
@@ -1635,6 +1740,64 @@ pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags,
       const int n = 2 * s->p + s->d + 1;
       for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
     }
+    return PFSMC_GPU_OK;
+  });
+}
+
+
+// ---- BASELINE config 5 microbenchmark entry points (model PAYLOAD64) -----
+pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key) {
+  return guarded([&] {
+    if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    k_c5_weights<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, sigma, key);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// One resample/reduction iteration (enqueue only): LSE + tile offsets, the
+// weighted 2x2 covariance, the exact CDF, the ancestor search and gather.
+pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
+  return guarded([&] {
+    if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    Ctx c = s->ctx;
+    c.lg = c.lw;  // the fitness log-weights are the log-weights here
+    CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
+    k_c5_lse<<<s->grid, kThreads, 0, s->stream>>>(c);
+    k_c5_moments<<<s->grid, kThreads, 0, s->stream>>>(c);
+    launch_scan(c, s->ntiles, s->stream, 1);
+    launch_scan(c, s->ntiles, s->stream, 2);
+    k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
+    k_flip<<<1, 1, 0, s->stream>>>(s->st);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+
+// Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA).
+pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* out;
+    CK(cudaMalloc(&out, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8, iters = 4096;
+    k_dfma_peak<<<blocks, kThreads>>>(out, 256, 0.999999, 1e-7);  // warm-up
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, kThreads>>>(out, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *tflops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * kThreads / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
     return PFSMC_GPU_OK;
   });
 }

@@ -27,8 +27,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpfsmc_gpu.so")
 
-MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3}
-MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4)}
+MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4}
+MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 4: (6, 2)}
 FAMILIES = {"ab": 0, "am": 1, "bdf": 2}
 LIKELIHOODS = {"gaussian": 0, "lognormal": 1}
 
@@ -81,7 +81,8 @@ def load_library(path: str = LIB_PATH):
                      "pfsmc_gpu_init_uniform", "pfsmc_gpu_step", "pfsmc_gpu_upload_observations",
                      "pfsmc_gpu_step_resident", "pfsmc_gpu_synchronize", "pfsmc_gpu_run",
                      "pfsmc_gpu_get_step_diagnostics", "pfsmc_gpu_resample_from_g",
-                     "pfsmc_gpu_set_kernel_timing", "pfsmc_gpu_kernel_times", "pfsmc_gpu_flush_l2"):
+                     "pfsmc_gpu_set_kernel_timing", "pfsmc_gpu_kernel_times", "pfsmc_gpu_flush_l2",
+                     "pfsmc_gpu_c5_set_logweights", "pfsmc_gpu_c5_iteration"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
     return _lib
@@ -282,6 +283,13 @@ class GpuSampler:
         names = C.c_char_p()
         self._check(self.lib.pfsmc_gpu_kernel_times(self.h, _ptr(ms), C.byref(n), C.byref(names)))
         return dict(zip(names.value.decode().split(","), ms[:n.value].tolist()))
+
+    # -- BASELINE config 5 microbenchmark (model "payload64") ------------
+    def c5_set_logweights(self, sigma: float, key: int):
+        self._check(self.lib.pfsmc_gpu_c5_set_logweights(self.h, C.c_double(sigma), C.c_uint64(key)))
+
+    def c5_iteration(self, j: int):
+        self._check(self.lib.pfsmc_gpu_c5_iteration(self.h, C.c_uint64(j)))
 
     def flush_l2(self):
         self._check(self.lib.pfsmc_gpu_flush_l2(self.h))

@@ -415,3 +415,31 @@ def test_free_running_full_size_lv():
         assert _rel(tr, trace_o) < REL_TRACE, j
         tp = t1
     gpu.close()
+
+
+def test_c5_resample_iteration_matches_oracle():
+    """BASELINE config 5 iteration on 64-byte records: LSE, weighted 2x2
+    covariance, exact multinomial resampling and the gather, vs the oracle's
+    fitness_weights / weighted_mean_cov / resample_multinomial."""
+    from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
+    n = 1 << 16
+    rng = np.random.default_rng(3)
+    for sigma in (0.1, 1.0, 4.0):
+        s = GpuSampler("payload64", PfConfig(particles=n, seed=77), ObservationModel([0], 1.0))
+        states = rng.standard_normal((n, 6))
+        params = rng.standard_normal((n, 2))
+        s.set_ensemble(Ensemble(states, params, np.zeros(n), np.zeros(2), np.eye(2)))
+        s.c5_set_logweights(sigma, 5)
+        lw = s.get_ensemble().logw.copy()
+        s.c5_iteration(1)
+        s.synchronize()
+        anc, _, _ = s.step_diagnostics()
+        g = O.fitness(lw, np.zeros(n))
+        want = O.resample(g, 77, 1)
+        assert np.array_equal(anc.astype(np.int64), want), sigma
+        e = s.get_ensemble()
+        assert np.array_equal(e.states, states[want]) and np.array_equal(e.params_u, params[want])
+        mean, cov = O.weighted_mean_cov(params, g)
+        np.testing.assert_allclose(e.mean_u, mean, rtol=1e-10, atol=1e-13)
+        np.testing.assert_allclose(e.cov_u, cov, rtol=1e-8, atol=1e-13)
+        s.close()
