@@ -13,8 +13,9 @@
 //   ramped interval loop        lmm.cpp:468-503 (order p = min(k, order),
 //                                fresh history every interval)
 // The order ramp makes steps k = 1, 2, 3 special (avail = min(k, 4) history
-// entries); each is a separate compile-time instantiation, so every history
-// index is static and nothing touches local memory.
+// entries); for small d each is a separate compile-time instantiation, so
+// every history index is static and nothing touches local memory; for large d
+// (the 8-species chain) one runtime-order body keeps the code in the I-cache.
 #pragma once
 #include "models.cuh"
 
@@ -120,6 +121,60 @@ __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[
   return true;
 }
 
+// Structured path for models whose Jacobian (hence I - h b0 J) is lower
+// bidiagonal (M::jac_band gives the diagonal and subdiagonal). When no
+// partial-pivoting swap is triggered (the reference's rule: first strictly
+// larger |.|) and every band entry is finite with a normal diagonal, the
+// dense elimination (linalg.cpp:201-258) performs on the band exactly the
+// operations done here; the ones it adds only combine structural zeros (+-0)
+// with finite values, leaving every band entry bit-identical. Anything else
+// takes the dense path below, which rebuilds J with M::jac; it is kept out of
+// line so the 8x8 matrix never lives in the hot loop's registers.
+template <class M>
+__device__ __forceinline__ bool dense_newton_solve(const double* th_p, const double* x_p, double hb0,
+                                                double* r_p) {
+  constexpr int D = M::D;
+  double th[M::P], x[D], r[D], A[D][D];
+  for (int j = 0; j < M::P; ++j) th[j] = th_p[j];
+  for (int j = 0; j < D; ++j) x[j] = x_p[j], r[j] = r_p[j];
+  M::jac(th, x, A);  // finite: jac_band (same entries) was checked
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) A[i][j] = -hb0 * A[i][j];
+  for (int i = 0; i < D; ++i) A[i][i] += 1.0;
+  const bool ok = lu_solve_inplace<D>(A, r);
+  for (int j = 0; j < D; ++j) r_p[j] = r[j];
+  return ok;
+}
+
+template <class M>
+__device__ __forceinline__ bool band_solve(const double (&th)[M::P], const double (&x)[M::D],
+                                           double hb0, const double (&jd)[M::D],
+                                           const double (&js)[M::D - 1], double (&b)[M::D]) {
+  constexpr int D = M::D;
+  double dg[D], sb[D - 1];
+  bool fast = true;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    dg[i] = -hb0 * jd[i];
+    dg[i] += 1.0;
+    fast &= fabs(dg[i]) >= 2.2250738585072014e-308 && fabs(dg[i]) <= 1.7976931348623157e308;
+  }
+#pragma unroll
+  for (int c = 0; c + 1 < D; ++c) {
+    sb[c] = -hb0 * js[c];
+    fast &= !(fabs(sb[c]) > fabs(dg[c]));
+  }
+  if (!fast) return dense_newton_solve<M>(th, x, hb0, b);
+#pragma unroll
+  for (int i = 1; i < D; ++i) {
+    const double l = sb[i - 1] * (1.0 / dg[i - 1]);
+    b[i] -= l * b[i - 1];
+  }
+#pragma unroll
+  for (int ii = D - 1; ii >= 0; --ii) b[ii] /= dg[ii];
+  return true;
+}
+
 // ---- Newton on G(x) = x - h b0 f(x) - c (lmm.cpp:219-266) ---------------
 template <class M>
 __device__ __forceinline__ int newton_solve(const double (&th)[M::P], double hb0,
@@ -127,24 +182,36 @@ __device__ __forceinline__ int newton_solve(const double (&th)[M::P], double hb0
                                             double tol, int max_iter, int& iters) {
   constexpr int D = M::D;
   for (int iter = 1; iter <= max_iter; ++iter) {
-    double f[D], r[D], A[D][D];
+    double f[D], r[D];
     if (!M::rhs(th, x, f)) {
       iters += iter;
       return kInvalidRhs;
     }
 #pragma unroll
     for (int j = 0; j < D; ++j) r[j] = x[j] - hb0 * f[j] - c[j];
-    if (!M::jac(th, x, A)) {
-      iters += iter;
-      return kInvalidRhs;
+    bool solved;
+    if constexpr (M::kLowerBidiagonal) {
+      double jd[D], js[D - 1];
+      if (!M::jac_band(th, x, jd, js)) {
+        iters += iter;
+        return kInvalidRhs;
+      }
+      solved = band_solve<M>(th, x, hb0, jd, js, r);
+    } else {
+      double A[D][D];
+      if (!M::jac(th, x, A)) {
+        iters += iter;
+        return kInvalidRhs;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) A[i][j] = -hb0 * A[i][j];
+#pragma unroll
+      for (int i = 0; i < D; ++i) A[i][i] += 1.0;
+      solved = lu_solve_inplace<D>(A, r);
     }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) A[i][j] = -hb0 * A[i][j];
-#pragma unroll
-    for (int i = 0; i < D; ++i) A[i][i] += 1.0;
-    if (!lu_solve_inplace<D>(A, r)) {
+    if (!solved) {
       iters += iter;
       return kSingular;
     }
@@ -302,6 +369,117 @@ struct Propagator {
     return kOk;
   }
 
+  // ---- runtime-order forms (large d) -------------------------------------
+  // For large state dimensions the four compile-time ramp instantiations
+  // (each with its own inlined Newton + LU) blow the kernel past the
+  // instruction cache. These forms run ONE step body for every ramp step:
+  // loops go to the compile-time maximum under a warp-uniform predicate, so
+  // history indices stay static (registers) and the floating-point operation
+  // sequence is exactly that of the templates above.
+  __device__ __forceinline__ void ab_step_rt(int q, double h, double (&out)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * xs[0][j];
+#pragma unroll
+    for (int i = 1; i <= FD; ++i) {
+      if (i <= q) {
+        const double hb = h * ab_beta(q, i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] += hb * fs[i - 1][j];
+      }
+    }
+  }
+  __device__ __forceinline__ void implicit_terms_rt(int pa, double h, double (&c)[D]) const {
+    if constexpr (FAM == kAM) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * xs[0][j];
+#pragma unroll
+      for (int i = 1; i < FD + 1; ++i) {
+        if (i < pa) {
+          const double hb = h * am_beta(pa, i);
+#pragma unroll
+          for (int j = 0; j < D; ++j) c[j] += hb * fs[i - 1][j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) c[j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < SD; ++i) {
+        if (i < pa) {
+          const double a = bdf_alpha(pa, i);
+#pragma unroll
+          for (int j = 0; j < D; ++j) c[j] += a * xs[i][j];
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void extrapolate_rt(int q, double (&out)[D]) const {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = 0.0;
+    double binom = static_cast<double>(q) + 1.0;
+    double sign = 1.0;
+#pragma unroll
+    for (int i = 0; i < SD; ++i) {
+      if (i <= q) {
+        const double coef = sign * binom;
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] += coef * xs[i][j];
+        sign = -sign;
+        binom = binom * static_cast<double>(q + 1 - (i + 1)) / static_cast<double>(i + 2);
+      }
+    }
+  }
+  __device__ __forceinline__ int step_rt(int pa, int av, const double (&th)[P], double h, double tol,
+                                         int max_iter, double (&gamma)[D], int& iters) {
+    double xnew[D], ref[D];
+    double factor;
+    if constexpr (FAM == kAB) {
+      ab_step_rt(pa, h, xnew);
+      if (av >= pa + 1) {
+        ab_step_rt(pa + 1, h, ref);
+      } else if (pa >= 2) {
+        ab_step_rt(pa - 1, h, ref);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) ref[j] = xs[0][j];
+      }
+      factor = 1.0;
+    } else {
+      double c[D];
+      implicit_terms_rt(pa, h, c);
+      ab_step_rt(pa, h, xnew);
+      if constexpr (FAM == kAM) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) ref[j] = xnew[j];
+        factor = fabs(am_C(pa)) / fabs(ab_C(pa) - am_C(pa));
+      } else {
+        if (av >= pa + 1) {
+          extrapolate_rt(pa, ref);
+          factor = fabs(bdf_C(pa)) / fabs(1.0 - bdf_C(pa));
+        } else if (av < 2) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) ref[j] = xnew[j];
+          factor = fabs(bdf_C(pa)) / fabs(ab_C(pa) - bdf_C(pa));
+        } else {
+          extrapolate_rt(av - 1, ref);
+          factor = fabs(bdf_C(pa)) / fabs(1.0 - bdf_C(pa));
+        }
+      }
+      const double b0 = FAM == kAM ? am_beta(pa, 0) : bdf_beta0(pa);
+      const int st = newton_solve<M>(th, h * b0, c, xnew, tol, max_iter, iters);
+      if (st != kOk) return st;
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double est = factor * fabs(xnew[j] - ref[j]);
+      gamma[j] += est * est;
+    }
+    double fnew[D];
+    if (!M::rhs(th, xnew, fnew)) return kInvalidRhs;
+    push(xnew, fnew);
+    return kOk;
+  }
+
   // propagate_interval (lmm.cpp:468-503): m fixed steps of size h from x.
   // On return x holds the last accepted state (the reference's run.x).
   __device__ __forceinline__ int run(const double (&th)[P], double (&x)[D], double h, int m,
@@ -316,6 +494,15 @@ struct Propagator {
       fs[0][j] = f0[j];
     }
     int st = kOk;
+    if constexpr (D >= 6) {
+      for (int k = 1; k <= m && st == kOk; ++k)
+        st = step_rt(cmin(k, ORD), cmin(k, 4), th, h, tol, max_iter, gamma, iters);
+      if (true) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = xs[0][j];
+        return st;
+      }
+    }
     for (int k = 1; k <= m && st == kOk; ++k) {
       if (k == 1)
         st = step<1, 1>(th, h, tol, max_iter, gamma, iters);
