@@ -166,6 +166,16 @@ def fp64_peak(device):
     return v.value if rc == 0 else None
 
 
+def gather_peak(device, n_rec=1 << 25):
+    import ctypes
+    from paper_1411_1702_b200.sampler import load_library
+    lib = load_library()
+    lib.pfsmc_gpu_gather_peak.restype = ctypes.c_int
+    v = ctypes.c_double()
+    rc = lib.pfsmc_gpu_gather_peak(device, ctypes.c_longlong(n_rec), ctypes.byref(v))
+    return v.value if rc == 0 else None
+
+
 def _timed_steps(gpu, prob, steps, warmup, stream):
     """Blocking drop-in steps with per-step events (L2 flushed between)."""
     import torch
@@ -226,7 +236,23 @@ def bench_workloads(local, fp64):
         c5[f"sigma={sigma}"] = {"ms_per_iteration": t, "particle_iterations_per_s": n5 / (t / 1e3),
                                "hbm_gbs_algorithmic": gbs, "frac_of_measured_hbm": gbs / hbm}
     s.close()
+    # Composite roofline for the iteration. Streamed bytes per particle (at the
+    # measured HBM peak): stats 72 (the 64-byte record line + lw), exact scan
+    # 33 (lg twice, cdf, segment ends), serve 68 (record write + ancestor).
+    # Random bytes: two 64-byte bursts (the CDF segment and the ancestor's
+    # record) at the measured random-read rate, derived from the gather
+    # microbenchmark (64 B random read + 64 B streamed write per record).
+    gpk = gather_peak(local)
+    seq_b, rnd_b = 72 + 33 + 68, 128
+    rnd_rate = 64.0 / (128.0 / (gpk * 1e9) - 64.0 / (hbm * 1e9)) if gpk else None
+    bound_ms = (n5 * (seq_b / (hbm * 1e9) + rnd_b / rnd_rate) * 1e3) if rnd_rate else None
+    for v in c5.values():
+        v["composite_bound_ms"] = bound_ms
+        v["frac_of_composite_bound"] = (bound_ms / v["ms_per_iteration"]) if bound_ms else None
     out["c5_resample_bandwidth"] = {"particles": n5, "record_bytes": 64, "bytes_per_particle_iteration": 184,
+                                    "streamed_bytes_per_particle": seq_b, "random_bytes_per_particle": rnd_b,
+                                    "random_gather_peak_gbs": gpk,
+                                    "random_read_rate_gbs": rnd_rate / 1e9 if rnd_rate else None,
                                     "results": c5}
     # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal (first log-spaced intervals)
     n3 = 1 << 22

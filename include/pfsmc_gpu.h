@@ -168,6 +168,10 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop; the FP64
  * roofline denominator the benchmarks report against). */
 pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops);
+/* Measured random-gather roofline for the resampling gathers: GB/s of
+   64-byte records read at hashed indices plus written in slot order, over
+   n_rec records (use n_rec * 64 bytes > L2). Benchmark helper. */
+pfsmc_gpu_status pfsmc_gpu_gather_peak(int device, long long n_rec, double* gbs);
 
 /* L2 flush helper for benchmarks: writes a device buffer larger than L2 on
  * the sampler's stream. */

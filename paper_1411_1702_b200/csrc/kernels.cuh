@@ -95,14 +95,14 @@ struct Ctx {
   double* lg;
   double* cdf;
   unsigned* anc;
-  unsigned short* lguide;  // per-tile local guide (one entry per tile element)
-  unsigned* coarse;
+  double* seg_end;     // exact CDF at the end of each 8-element segment (L2-resident)
+  unsigned* coarse;    // guide: bucket b -> first segment with seg_end > b / 2^coarse_bits
   double2* tile_info;  // exact CDF (value before the tile, value at its last element;
                        // the last tile's end carries the guard, filter.cpp:168)
-  double* g;           // fitness of the current step (k_scan_tiles writes it)
   double* tile_pre;    // approximate exclusive tile prefixes (from the K1 block partials)
   int* blk_cnt;        // K1 blocks: number of finite fitness log-weights
   double* trel;        // per tile: fitness mass relative to its K1 group max
+  double* tile_m;      // per tile max (C5 tile-loop LSE), or unused
   struct ThreadRec* trec;  // S2 -> S3 handoff: per-thread prefix and segment carry
   long long* tile_cnt_pre;
   TileHdr* hdr;
@@ -130,6 +130,8 @@ struct Ctx {
   double* shard_sum;   // [2]: this shard's approximate g total and nonzero count (K1 tail)
   double* shard_off;   // [2]: global approximate offset and count before this shard
 };
+
+constexpr int kSegLog2 = 3;  // ancestor-search segment: 8 CDF values = one 64-byte burst
 
 // ---------------------------------------------------------------- helpers
 template <class M>
@@ -193,6 +195,38 @@ __device__ __forceinline__ double loglik(const Ctx& c, const StepParams& sp,
   return sp.ll_const - ss / c.two_s2;
 }
 
+// L2 eviction-priority hints (createpolicy + ld/st .L2::cache_hint): the
+// ancestor search keeps its small tables (guide, segment ends) resident
+// while the one-shot traffic (CDF segments, record gathers) is evicted first.
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_hint(const unsigned* a, uint64_t pol) {
+  unsigned v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double2* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" :: "l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ bool grid_error(const Ctx& c) {
   return *reinterpret_cast<volatile int*>(&c.st->error) != 0;
 }
@@ -235,7 +269,8 @@ struct TileGroupHook {
   }
 };
 
-__device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse) {
+// tile_m (C5 path): per-tile maxima instead of the group maxima.
+__device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const double* tile_m = nullptr) {
   __shared__ SumCnt sw[2 * kWarps];
   const int tpg_log2 = 6 - (c.tile_log2 - 8);  // tiles per group
   const int per = (c.ntiles + kThreads - 1) / kThreads;
@@ -244,7 +279,7 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse) {
   long long n[8];
   SumCnt acc{0.0, 0};
   for (int t = t0; t < t1; ++t) {
-    const double mg = __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
+    const double mg = tile_m ? __ldcg(&tile_m[t]) : __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
     const double v = mg == -INFINITY ? 0.0 : __ldcg(&c.trel[t]) * exp(mg - lse);
     const long long k = __ldcg(&c.tile_cnt_pre[t]);
     if (t - t0 < 8) {
@@ -263,7 +298,7 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse) {
       v = s[t - t0];
       k = n[t - t0];
     } else {
-      const double mg = __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
+      const double mg = tile_m ? __ldcg(&tile_m[t]) : __ldcg(&c.gpart[2 * (t >> tpg_log2)]);
       v = mg == -INFINITY ? 0.0 : __ldcg(&c.trel[t]) * exp(mg - lse);
       k = __ldcg(&c.tile_cnt_pre[t]);
     }
@@ -331,24 +366,79 @@ __global__ void __launch_bounds__(kThreads, (M::D <= 3 ? 4 : 1)) k_predict(Ctx c
 }
 
 // Ancestor search: first k with cdf_k > u (std::upper_bound, filter.cpp:173),
-// clamped to N-1 (filter.cpp:175). coarse guide -> tile -> per-tile local
-// guide -> short forward walk over the exact CDF.
+// clamped to N-1 (filter.cpp:175), in two parts:
+//  find_segment: guide bucket -> segment bracket [lo, hi] (guide entries and
+//    segment ends are L2-resident) -> binary search / walk over seg_end ->
+//    the segment whose end first exceeds u;
+//  the count of CDF values <= u inside that aligned segment (the CDF is
+//    non-decreasing, so the count is the offset of the first value above u).
+__device__ __forceinline__ long long find_segment(const Ctx& c, double u) {
+  const uint64_t keep = l2_policy_keep();
+  constexpr int seg_log2 = kSegLog2;
+  const long long nseg = (static_cast<long long>(c.N) + (1 << seg_log2) - 1) >> seg_log2;
+  const long long nb = 1LL << c.coarse_bits;
+  long long b = static_cast<long long>(scale2(u, c.coarse_bits));
+  b = min(max(b, 0LL), nb - 1);
+  long long lo = ld_hint(&c.coarse[b], keep);
+  long long hi = nseg - 1;
+  if (b + 1 < nb) {
+    // the next bucket belongs to this handle only if its edge is below our end
+    const double edge = scale2(static_cast<double>(b + 1), -c.coarse_bits);
+    if (edge < __ldg(&c.tile_info[c.ntiles - 1]).y) hi = min(hi, static_cast<long long>(ld_hint(&c.coarse[b + 1], keep)));
+  }
+  lo = min(lo, hi);
+  while (hi - lo > 4) {
+    const long long mid = (lo + hi) >> 1;
+    if (ld_hint(&c.seg_end[mid], keep) > u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  while (lo < hi && ld_hint(&c.seg_end[lo], keep) <= u) ++lo;
+  return lo;
+}
+
+// Scalar form (one thread, one slot).
 __device__ __forceinline__ unsigned find_ancestor(const Ctx& c, double u) {
-  const double B1 = scale2(1.0, c.coarse_bits);
-  int t = static_cast<int>(__ldg(&c.coarse[static_cast<long long>(u * B1)]));
-  double2 ti = __ldg(&c.tile_info[t]);
-  while (t < c.ntiles - 1 && ti.y <= u) ti = __ldg(&c.tile_info[++t]);
-  const int tile = 1 << c.tile_log2;
-  const double wdt = (ti.y - ti.x) * scale2(1.0, -c.tile_log2);
-  double fi = floor((u - ti.x) / wdt);
-  fi = fmin(fmax(fi, 0.0), static_cast<double>(tile - 1));
-  int i = static_cast<int>(fi);
-  while (i > 0 && ti.x + static_cast<double>(i) * wdt > u) --i;
-  while (i + 1 < tile && ti.x + static_cast<double>(i + 1) * wdt <= u) ++i;
-  const long long base = static_cast<long long>(t) << c.tile_log2;
-  long long k = base + __ldg(&c.lguide[base + i]);
-  while (k < c.N - 1 && __ldg(&c.cdf[k]) <= u) ++k;
-  return static_cast<unsigned>(k);
+  constexpr int seg_log2 = kSegLog2;
+  const long long k0 = find_segment(c, u) << seg_log2;
+  const long long k1 = min(k0 + (1LL << seg_log2), static_cast<long long>(c.N));
+  int cnt = 0;
+  for (long long k = k0; k < k1; ++k) cnt += __ldg(&c.cdf[k]) <= u;
+  return static_cast<unsigned>(min(k0 + cnt, static_cast<long long>(c.N) - 1));
+}
+
+// Warp-cooperative form: every lane of the warp must call it (lanes without
+// a slot pass u = -1). The segment reads are spread so that each load
+// instruction covers whole 64-byte segments (four lanes each), i.e. one L1
+// wavefront per segment instead of one per lane and per 16 bytes.
+__device__ __forceinline__ unsigned find_ancestor_warp(const Ctx& c, double u) {
+  constexpr int SEGL2 = kSegLog2;
+  constexpr int P = 1 << (SEGL2 - 1);  // lanes per segment (16-byte parts)
+  constexpr int S = 32 / P;            // segments per load instruction
+  const int lane = threadIdx.x & 31;
+  const long long N = c.N;
+  const long long k0 = u >= 0.0 ? (find_segment(c, u) << SEGL2) : 0;
+  int mine = 0;
+#pragma unroll
+  for (int q = 0; q < 32; q += S) {
+    const int src = q + lane / P;
+    const long long ks = __shfl_sync(0xffffffffu, k0, src);
+    const double us = __shfl_sync(0xffffffffu, u, src);
+    const long long kk = ks + 2 * (lane % P);
+    int cnt = 0;
+    if (kk + 1 < N) {
+      const double2 v = ld_hint(reinterpret_cast<const double2*>(c.cdf + kk), l2_policy_stream());
+      cnt = (v.x <= us) + (v.y <= us);
+    } else if (kk < N) {
+      cnt = __ldg(&c.cdf[kk]) <= us;
+    }
+#pragma unroll
+    for (int o = P / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const int got = __shfl_sync(0xffffffffu, cnt, ((lane - q) & (S - 1)) * P);
+    if (lane >= q && lane < q + S) mine = got;
+  }
+  return static_cast<unsigned>(min(k0 + mine, N - 1));
 }
 
 // ---------------------------------------------------------------- K3

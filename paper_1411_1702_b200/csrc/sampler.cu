@@ -345,8 +345,9 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
           } else if (wh.nwin < 0) {
             // serial tile (window overflow): plain sequential sum, CDF written here
             const long long tbase = static_cast<long long>(ti) * TC::kTileT;
+            const double lse = c.st->lse_g;
             for (int e = 0; e < TC::kTileT && tbase + e < c.N; ++e) {
-              s = s + __ldcg(&c.g[tbase + e]);
+              s = s + (c.gin ? __ldcg(&c.gin[tbase + e]) : exp(__ldcg(&c.lg[tbase + e]) - lse));
               c.cdf[tbase + e] = s;
             }
           } else {
@@ -435,16 +436,23 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   const double pre = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
   const long long cpre = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
   ThreadTile<ITEMS> tt;
-#pragma unroll 4
-  for (int i = 0; i < ITEMS; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    const long long k = base + e;
-    double g = 0.0;
-    if (k < c.N) {
-      g = c.gin ? c.gin[k] : exp(c.lg[k] - lse);
-      c.g[k] = g;
+  {
+    // all ITEMS loads in flight first, then the exps
+    const double* src = c.gin ? c.gin : c.lg;
+    double x[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const long long k = base + i * kThreads + threadIdx.x;
+      x[i] = k < c.N ? __ldcs(&src[k]) : 0.0;
     }
-    sm.g[TC::sidx(e)] = g;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = i * kThreads + threadIdx.x;
+      const long long k = base + e;
+      double g = 0.0;
+      if (k < c.N) g = c.gin ? x[i] : exp(x[i] - lse);  // S3 recomputes it (bitwise)
+      sm.g[TC::sidx(e)] = g;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -529,13 +537,22 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
   double vals[ITEMS];
   if (nwin >= 0) {
     ThreadTile<ITEMS> tt;
-    const double2* gsrc = reinterpret_cast<const double2*>(c.g + base + threadIdx.x * ITEMS);
+    // g = exp(lg - lse) recomputed exactly as S2 did (same inputs, same op)
+    const double lse = c.st->lse_g;
+    const double2* gsrc = reinterpret_cast<const double2*>((c.gin ? c.gin : c.lg) + base + threadIdx.x * ITEMS);
 #pragma unroll
     for (int i = 0; i < ITEMS / 2; ++i) {
-      const double2 v = __ldcg(gsrc + i);
+      const double2 v = __ldcs(gsrc + i);
       const int e = threadIdx.x * ITEMS + 2 * i;
       tt.g[2 * i] = e < valid ? v.x : 0.0;
       tt.g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
+    }
+    if (!c.gin) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int e = threadIdx.x * ITEMS + i;
+        tt.g[i] = e < valid ? exp(tt.g[i] - lse) : 0.0;
+      }
     }
     const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
     tt.p[0] = tr.p0;
@@ -608,39 +625,24 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
     const int e = i * kThreads + threadIdx.x;
     if (e < valid) c.cdf[base + e] = sg[TC::sidx(e)];
   }
-  // local guide: bucket i edge x_i = start + i*w; first local k with cdf > x_i.
-  // Thread t owns ITEMS consecutive buckets: one binary search, then a walk.
-  const double wdt = (ti.y - ti.x) * (1.0 / TC::kTileT);
-  {
-    const int i0 = threadIdx.x * ITEMS;
-    const double x0 = ti.x + static_cast<double>(i0) * wdt;
-    int lo = 0, len = valid;
-    while (len > 0) {
-      const int half = len >> 1;
-      if (!(x0 < sg[TC::sidx(lo + half)])) {
-        lo += half + 1;
-        len -= half + 1;
-      } else {
-        len = half;
-      }
-    }
-    unsigned packed[ITEMS / 2];
+  // Segment ends (a segment = 8 elements, one 64-byte burst): seg_end[j] is
+  // the exact CDF at the segment's last element. They and the guide below
+  // are small enough to stay in L2, so the ancestor search reads HBM once
+  // (the one 64/128-byte CDF segment) before the record gather.
+  constexpr int SPT = ITEMS >> kSegLog2;  // segments per thread
+  constexpr int SPB = SPT * kThreads;     // segments per tile
+  __shared__ double send[SPB];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const double x = ti.x + static_cast<double>(i0 + i) * wdt;
-      while (lo < valid && !(x < sg[TC::sidx(lo)])) ++lo;
-      const unsigned v = static_cast<unsigned>(min(lo, valid - 1));
-      if (i & 1)
-        packed[i >> 1] |= v << 16;
-      else
-        packed[i >> 1] = v;
-    }
-#pragma unroll
-    for (int q = 0; q < ITEMS / 8; ++q)
-      reinterpret_cast<uint4*>(c.lguide + base + i0)[q] =
-          make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+  for (int q = 0; q < SPT; ++q) {
+    const int i0 = threadIdx.x * ITEMS + (q << kSegLog2);
+    const double v = i0 < valid ? sg[TC::sidx(min(i0 + (1 << kSegLog2) - 1, valid - 1))] : INFINITY;
+    send[threadIdx.x * SPT + q] = v;
+    if (i0 < valid) c.seg_end[static_cast<long long>(t) * SPB + threadIdx.x * SPT + q] = v;
   }
-  // coarse guide: buckets b with start <= b/B1 < end point at this tile
+  __syncthreads();
+  // guide: bucket b (edge b/B) -> first segment whose end exceeds b/B, for
+  // the buckets with start <= b/B < end of this tile (binary search over the
+  // tile's 256 segment ends in shared memory; bucket work spread over threads)
   const double B1 = scale2(1.0, c.coarse_bits);
   const long long nb = 1LL << c.coarse_bits;
   long long b_lo = static_cast<long long>(ceil(ti.x * B1));
@@ -649,7 +651,20 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
   b_hi = min(b_hi, nb - 1);
   if (t == 0) b_lo = static_cast<long long>(floor(ti.x * B1));  // a shard's first tile also owns
                                                               // the bucket its range starts in
-  for (long long b = b_lo + threadIdx.x; b <= b_hi; b += kThreads) c.coarse[b] = t;
+  for (long long b = b_lo + threadIdx.x; b <= b_hi; b += kThreads) {
+    const double x = scale2(static_cast<double>(b), -c.coarse_bits);
+    int lo = 0, len = SPB;
+    while (len > 0) {
+      const int half = len >> 1;
+      if (!(x < send[lo + half])) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    c.coarse[b] = static_cast<unsigned>(t) * SPB + static_cast<unsigned>(min(lo, SPB - 1));
+  }
 }
 
 void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
@@ -682,15 +697,28 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
 __global__ void __launch_bounds__(kThreads) k_serve(Ctx c) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  if (n >= c.N) return;
-  const double u = resample_uniform(c.seed, c.sp->j, n);
-  const unsigned a = find_ancestor(c, u);
-  c.anc[n] = a;
-  const int W = c.R + 2;
-  const double2* src = reinterpret_cast<const double2*>(c.rec[c.st->cur] + static_cast<long long>(a) * c.R);
-  double2* dst = reinterpret_cast<double2*>(c.payload + n * W);
-  for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
-  dst[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(a));
+  const double u = n < c.N ? resample_uniform(c.seed, c.sp->j, n) : -1.0;
+  const unsigned a = find_ancestor_warp(c, u);
+  if (n < c.N) c.anc[n] = a;
+  // warp-cooperative gather: consecutive lanes move consecutive 16-byte
+  // parts of the warp's 32 payloads (coalesced stores, whole-record loads)
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const int H = c.R / 2 + 1;  // 16-byte parts per payload
+  const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
+  double2* pay = reinterpret_cast<double2*>(c.payload);
+  for (int idx = lane; idx < 32 * H; idx += 32) {
+    const int slot = idx / H, part = idx - slot * H;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);  // every lane reaches this shuffle
+    const long long ns = wbase + slot;
+    if (ns >= c.N) continue;
+    double2 v;
+    if (part < H - 1)
+      v = __ldg(rec + static_cast<long long>(as) * (H - 1) + part);
+    else
+      v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(as));
+    pay[ns * H + part] = v;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp, int ngroups) {
@@ -827,79 +855,129 @@ __global__ void __launch_bounds__(kThreads) k_c5_weights(Ctx c, double sigma, un
   c.lw[n] = sigma * z[0];
 }
 
-__global__ void __launch_bounds__(kThreads) k_c5_lse(Ctx c) {
-  __shared__ double scratch[kWarps * 2];
-  __shared__ double fin[2];
-  if (grid_error(c)) return;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  const double x = n < c.N ? c.lw[n] : -INFINITY;
-  const double one[1] = {1.0};
-  const int nfin = __syncthreads_count(isfinite(x) != 0);
-  if (threadIdx.x == 0) c.blk_cnt[blockIdx.x] = nfin;
-  block_partial<1, false>(x, one, c.part + blockIdx.x * 2, scratch);
-  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, true, TileGroupHook{&c})) {
-    __shared__ double s_lse;
-    if (threadIdx.x == 0) {
-      const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
-      c.st->lse_g = lse;
-      if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
-      s_lse = lse;
-    }
-    __syncthreads();
-    if (isfinite(s_lse)) tile_prefixes(c, s_lse);
-  }
-}
-
-// weighted mean / covariance of theta (weighted_mean_cov, linalg.cpp:389-432)
-// with w = exp(lw - lse): plain block sums about the previous mean.
-__global__ void __launch_bounds__(kThreads) k_c5_moments(Ctx c) {
-  __shared__ double scratch[kWarps * 6];
-  __shared__ double fin[7];
+// One pass over the resident particles computes everything the iteration
+// reduces: the log-sum-exp of lw, the weighted 2x2 parameter covariance
+// (weighted_mean_cov, linalg.cpp:389-432, about the previous mean) and the
+// exact scan's tile offsets. A grid of a few blocks per SM loops over the
+// exact-CDF tiles; each thread's ITEMS (lw, theta) loads are all in flight
+// before the tile's partial: M_t = max lw, then sums of e = exp(lw - M_t)
+// times (1, d0, d1, d0 d0, d0 d1, d1 d1) and the finite count. The block
+// folds its tiles in order (combine_partials' rescaling rule); the last block
+// combines the block partials in a fixed order. Bitwise reproducible.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
+  constexpr int kTileT = ITEMS * kThreads;
+  constexpr int V = 7;  // S, A0, A1, B00, B01, B11, finite count
+  __shared__ double scratch[kWarps * V];
+  __shared__ double fin[V];
+  __shared__ int s_last;
   if (grid_error(c)) return;
   DevState& st = *c.st;
-  const double lse = st.lse_g;
   const double k0 = st.mu[0], k1 = st.mu[1];
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  double x = -INFINITY;
-  if (n < c.N) {
-    const double2 th = __ldg(reinterpret_cast<const double2*>(c.rec[st.cur] + n * c.R + 6));
-    x = c.lw[n] - lse;
-    const double d0 = th.x - k0, d1 = th.y - k1;
-    v[0] = d0;
-    v[1] = d1;
-    v[2] = d0 * d0;
-    v[3] = d0 * d1;
-    v[4] = d1 * d1;
-  }
-  double vals[6] = {1.0, v[0], v[1], v[2], v[3], v[4]};
-  block_partial<6, false>(x, vals, c.part + static_cast<size_t>(blockIdx.x) * 7, scratch);
-  if (tree_reduce_last<6, false>(c.part, c.gpart, c.cnt_upd, fin, scratch)) {
+  const double* rec = c.rec[st.cur];
+  for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+    const long long base = static_cast<long long>(t) * kTileT;
+    double x[ITEMS];
+    double2 th[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const long long k = base + i * kThreads + threadIdx.x;
+      x[i] = k < c.N ? __ldcs(&c.lw[k]) : -INFINITY;
+      th[i] = k < c.N ? __ldcs(reinterpret_cast<const double2*>(rec + k * c.R + 6)) : make_double2(0.0, 0.0);
+    }
+    double m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (!isnan(x[i])) m = nan_free_max(m, x[i]);
+    const double M = block_max(m, scratch);
+    double v[V] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const double e = isnan(x[i]) ? NAN : (x[i] == -INFINITY ? 0.0 : exp(x[i] - M));
+      const double d0 = th[i].x - k0, d1 = th[i].y - k1;
+      v[0] += e;
+      v[1] += e * d0;
+      v[2] += e * d1;
+      v[3] += e * (d0 * d0);
+      v[4] += e * (d0 * d1);
+      v[5] += e * (d1 * d1);
+      v[6] += isfinite(x[i]) ? 1.0 : 0.0;
+    }
+    block_sums<V>(v, scratch);
     if (threadIdx.x == 0) {
-      const double S = fin[1];
-      const double m0 = fin[2] / S, m1 = fin[3] / S;
-      st.mu[0] = k0 + m0;
-      st.mu[1] = k1 + m1;
-      st.cov[0] = fin[4] / S - m0 * m0;
-      st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
-      st.cov[3] = fin[6] / S - m1 * m1;
+      double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;  // per-tile partial (after the block slots)
+      tp[0] = M;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) tp[1 + k] = v[k];
+      c.trel[t] = v[0];
+      c.tile_m[t] = M;
+      c.tile_cnt_pre[t] = static_cast<long long>(v[6]);
     }
   }
+  if (threadIdx.x == 0) {
+    // this block's partial over its tiles, in tile order
+    double M = -INFINITY;
+    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) M = nan_free_max(M, c.tile_m[t]);
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+      const double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;
+      const double w = tp[0] == -INFINITY ? 0.0 : exp(tp[0] - M);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) acc[k] += w * tp[1 + k];
+    }
+    double* bp = c.part + static_cast<size_t>(blockIdx.x) * V;
+    bp[0] = M;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) bp[1 + k] = acc[k];
+    __threadfence();
+    const unsigned old = atomicAdd(&c.cnt_scan[3], 1u);
+    s_last = (old == gridDim.x - 1);
+    if (s_last) c.cnt_scan[3] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  combine_partials<6, false>(c.part, gridDim.x, fin, scratch);
+  __syncthreads();
+  __shared__ double s_lse;
+  if (threadIdx.x == 0) {
+    const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
+    st.lse_g = lse;
+    if (!isfinite(lse)) atomicOr(&st.error, kErrPredict);
+    s_lse = lse;
+    const double S = fin[1];
+    const double m0 = fin[2] / S, m1 = fin[3] / S;
+    st.mu[0] = k0 + m0;
+    st.mu[1] = k1 + m1;
+    st.cov[0] = fin[4] / S - m0 * m0;
+    st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
+    st.cov[3] = fin[6] / S - m1 * m1;
+  }
+  __syncthreads();
+  if (isfinite(s_lse)) tile_prefixes(c, s_lse, c.tile_m);
 }
 
-// Survival of the fittest straight into the next record buffer.
+// Survival of the fittest straight into the next record buffer (64-byte
+// records: four lanes per record, eight records per load instruction).
 __global__ void __launch_bounds__(kThreads) k_c5_serve(Ctx c, unsigned long long j) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  if (n >= c.N) return;
-  const double u = resample_uniform(c.seed, j, c.n0 + n);
-  const unsigned a = find_ancestor(c, u);
-  c.anc[n] = a;
+  const double u = n < c.N ? resample_uniform(c.seed, j, c.n0 + n) : -1.0;
+  const unsigned a = find_ancestor_warp(c, u);
+  if (n < c.N) c.anc[n] = a;
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
   const int cur = c.st->cur;
-  const double2* src = reinterpret_cast<const double2*>(c.rec[cur] + static_cast<long long>(a) * c.R);
-  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1] + n * c.R);
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur]);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+  const uint64_t pol = l2_policy_stream();
 #pragma unroll
-  for (int i = 0; i < 4; ++i) dst[i] = __ldg(src + i);
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const long long ns = wbase + slot;
+    if (ns < c.N) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
 }
 
 __global__ void k_flip(DevState* st) { st->cur ^= 1; }
@@ -919,12 +997,35 @@ __global__ void __launch_bounds__(kThreads) k_dfma_peak(double* out, int iters, 
   if (acc == 12345.678) out[0] = acc;  // keeps the chains live
 }
 
+// Random-gather roofline: dst[n] = src[h(n)] for 64-byte records, h a
+// bijective-free integer hash (splitmix64) — the same access shape as the
+// resampling gather, without the search. Same warp-cooperative layout.
+__global__ void __launch_bounds__(kThreads) k_gather_peak(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                          long long n_rec) {
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  uint64_t z = static_cast<uint64_t>(n) + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  const unsigned a = static_cast<unsigned>(z % static_cast<uint64_t>(n_rec));
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const uint64_t pol = l2_policy_stream();
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const long long ns = wbase + slot;
+    if (ns < n_rec) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_search_only(Ctx c) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  if (n >= c.N) return;
-  const double u = resample_uniform(c.seed, c.sp->j, n);
-  c.anc[n] = find_ancestor(c, u);
+  const double u = n < c.N ? resample_uniform(c.seed, c.sp->j, n) : -1.0;
+  const unsigned a = find_ancestor_warp(c, u);
+  if (n < c.N) c.anc[n] = a;
 }
 
 // Record pack/unpack for the AoS boundary (filter::Ensemble layout).
@@ -979,6 +1080,8 @@ struct pfsmc_gpu_sampler {
   int d = 0, p = 0;
   long long N = 0;
   int grid = 0, ntiles = 0;
+  int num_sms = 148;
+  size_t l2_window = 0, l2_persist = 0;  // ancestor-search tables pinned in L2
   Ctx ctx{};
   cudaStream_t stream = nullptr;
   // device buffers
@@ -1218,6 +1321,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     }
     s->cfg.obs_indices = s->obs.data();
     CK(cudaSetDevice(cfg->device));
+    CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->rank = rank;
     s->world = world;
@@ -1239,8 +1343,10 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.max_iter = cfg->newton_max_iter;
     c.seed = cfg->seed;
     c.two_s2 = 2.0 * (cfg->sigma * cfg->sigma);
+    // guide buckets: about one per CDF segment (of the whole filter), <= 2^22
+    const long long nseg_glob = std::max<long long>(1, static_cast<long long>(cfg->particles) >> kSegLog2);
     int cb = 6;
-    while ((1LL << cb) < 4LL * s->ntiles) ++cb;
+    while ((1LL << cb) < nseg_glob && cb < 22) ++cb;
     c.coarse_bits = cb;
     const size_t N = static_cast<size_t>(s->N);
     const size_t NT = static_cast<size_t>(s->ntiles);
@@ -1253,8 +1359,34 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
     c.tile_log2 = tile_log2;
-    c.lguide = s->dalloc<unsigned short>(NT << tile_log2);
-    c.coarse = s->dalloc<unsigned>(size_t(1) << cb);
+    // the ancestor search's tables, in one range pinned in L2 (persisting
+    // access-policy window on the stream; the gathers stream past them)
+    {
+      const size_t nseg = (NT << tile_log2) >> kSegLog2;
+      const size_t bytes = nseg * sizeof(double) + (size_t(1) << cb) * sizeof(unsigned);
+      char* tab = s->dalloc<char>(bytes);
+      c.seg_end = reinterpret_cast<double*>(tab);
+      c.coarse = reinterpret_cast<unsigned*>(tab + nseg * sizeof(double));
+      int max_win = 0, max_persist = 0;
+      CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device));
+      CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, cfg->device));
+      if (max_win > 0 && max_persist > 0) {
+        const size_t win = std::min(bytes, static_cast<size_t>(max_win));
+        size_t cur = 0;
+        CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+        const size_t want = std::min(win, static_cast<size_t>(max_persist));
+        if (cur < want) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.base_ptr = tab;
+        av.accessPolicyWindow.num_bytes = win;
+        av.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(want) / static_cast<float>(win));
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CK(cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+        s->l2_window = win;
+        s->l2_persist = want;
+      }
+    }
     const size_t GNT = NT * world;  // tile arrays cover every shard (aliased at tile0)
     c.n0 = static_cast<long long>(rank) * s->N;
     c.n_glob = static_cast<long long>(cfg->particles);
@@ -1265,9 +1397,9 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.tile0 = static_cast<int>(NT) * rank;
     c.gtile_info = s->dalloc<double2>(GNT);
     c.tile_info = c.gtile_info + c.tile0;
-    c.g = s->dalloc<double>(N);
     c.blk_cnt = s->dalloc<int>(static_cast<size_t>(s->grid));
     c.trel = s->dalloc<double>(NT);
+    c.tile_m = s->dalloc<double>(NT);
     c.trec = s->dalloc<ThreadRec>(NT * kThreads);
     c.tile_pre = s->dalloc<double>(NT);
     c.tile_cnt_pre = s->dalloc<long long>(NT);
@@ -1763,8 +1895,11 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
     Ctx c = s->ctx;
     c.lg = c.lw;  // the fitness log-weights are the log-weights here
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
-    k_c5_lse<<<s->grid, kThreads, 0, s->stream>>>(c);
-    k_c5_moments<<<s->grid, kThreads, 0, s->stream>>>(c);
+    // one wave: 126 (ITEMS 16) / 74 (ITEMS 8) registers => 2 / 3 blocks per SM
+    if (c.tile_log2 == 11)
+      k_c5_stats<8><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
+    else
+      k_c5_stats<16><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
     launch_scan(c, s->ntiles, s->stream, 1);
     launch_scan(c, s->ntiles, s->stream, 2);
     k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
@@ -1798,6 +1933,38 @@ pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Measured random 64-byte-record gather throughput (GB/s of record bytes
+// read + written), over n_rec records (> L2), median-free: best of 5.
+pfsmc_gpu_status pfsmc_gpu_gather_peak(int device, long long n_rec, double* gbs) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    double2 *src, *dst;
+    CK(cudaMalloc(&src, static_cast<size_t>(n_rec) * 64));
+    CK(cudaMalloc(&dst, static_cast<size_t>(n_rec) * 64));
+    CK(cudaMemset(src, 0, static_cast<size_t>(n_rec) * 64));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = static_cast<int>((n_rec + kThreads - 1) / kThreads);
+    float best = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      CK(cudaEventRecord(e0));
+      k_gather_peak<<<blocks, kThreads>>>(src, dst, n_rec);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r > 0) best = std::min(best, ms);
+    }
+    *gbs = 128.0 * static_cast<double>(n_rec) / (best * 1e-3) / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(src);
+    cudaFree(dst);
     return PFSMC_GPU_OK;
   });
 }

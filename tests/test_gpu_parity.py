@@ -221,8 +221,11 @@ def test_free_running_lotka_volterra():
 
 
 # ---------------------------------------------------------------- stiff models
-def test_lockstep_chain_bdf3():
-    th = np.array([2.0, 50.0, 5.0, 0.5])
+@pytest.mark.parametrize("th0", [2.0, 120.0])
+def test_lockstep_chain_bdf3(th0):
+    # th0 = 120: h b0 dflux beats the diagonal, so the Newton LU pivots and
+    # the banded solve must hand over to the dense one (lmm.cuh band_solve)
+    th = np.array([th0, 50.0, 5.0, 0.5])
     n = 4096
     sc = StepConfig(model="chain", family="bdf", order=3, h=0.1 / 3, a=0.98, seed=8, obs_idx=(0, 3, 7), sigma=0.01)
     ens = O.init_uniform("chain", n, 8, 0.5 * th, 2 * th, [0] * 8, [0] * 8)
@@ -417,14 +420,15 @@ def test_free_running_full_size_lv():
     gpu.close()
 
 
-def test_c5_resample_iteration_matches_oracle():
+@pytest.mark.parametrize("n,sigmas", [(1 << 16, (0.1, 1.0, 4.0)), ((1 << 22) + 4097 * 3 + 5, (1.0,))])
+def test_c5_resample_iteration_matches_oracle(n, sigmas):
     """BASELINE config 5 iteration on 64-byte records: LSE, weighted 2x2
     covariance, exact multinomial resampling and the gather, vs the oracle's
-    fitness_weights / weighted_mean_cov / resample_multinomial."""
+    fitness_weights / weighted_mean_cov / resample_multinomial. The second
+    case is ragged and uses the 4096-element tiles."""
     from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
-    n = 1 << 16
     rng = np.random.default_rng(3)
-    for sigma in (0.1, 1.0, 4.0):
+    for sigma in sigmas:
         s = GpuSampler("payload64", PfConfig(particles=n, seed=77), ObservationModel([0], 1.0))
         states = rng.standard_normal((n, 6))
         params = rng.standard_normal((n, 2))
@@ -436,9 +440,29 @@ def test_c5_resample_iteration_matches_oracle():
         anc, _, _ = s.step_diagnostics()
         g = O.fitness(lw, np.zeros(n))
         want = O.resample(g, 77, 1)
-        assert np.array_equal(anc.astype(np.int64), want), sigma
+        anc = anc.astype(np.int64)
+        # The reference's lse is a sequential sum (relative error up to ~n eps);
+        # ours is a tree. Every g therefore moves by that much and a slot whose
+        # uniform sits that close to a CDF edge may legitimately flip: such
+        # classified near-ties are the only mismatches allowed.
+        bad = np.nonzero(anc != want)[0]
+        if len(bad):
+            cdf = np.cumsum(g)
+            cdf[-1] = max(cdf[-1], 1.0)
+            tol = 4.0 * n * 2.0 ** -53
+            for b in bad:
+                u = O.draws(77, 1, int(b), 3, 1, 1)[0]
+                edge = cdf[min(anc[b], want[b])]
+                assert abs(u - edge) <= tol * edge, (sigma, b, u, edge)
+            assert len(bad) <= 8, (sigma, len(bad))
+        # exactness of the device CDF itself: the oracle's own g injected
+        a2, cdf2 = s.resample_from_g(g, 1, with_cdf=True)
+        assert np.array_equal(a2.astype(np.int64), want), sigma
+        cdf_o = np.cumsum(g)
+        cdf_o[-1] = max(cdf_o[-1], 1.0)
+        assert np.array_equal(cdf2, cdf_o), sigma
         e = s.get_ensemble()
-        assert np.array_equal(e.states, states[want]) and np.array_equal(e.params_u, params[want])
+        assert np.array_equal(e.states, states[anc]) and np.array_equal(e.params_u, params[anc])
         mean, cov = O.weighted_mean_cov(params, g)
         np.testing.assert_allclose(e.mean_u, mean, rtol=1e-10, atol=1e-13)
         np.testing.assert_allclose(e.cov_u, cov, rtol=1e-8, atol=1e-13)
