@@ -694,6 +694,7 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
 // record and predictor log-likelihood into slot order, so K3 streams them
 // coalesced. Latency-bound (dependent random loads), so it runs as its own
 // small-footprint, high-occupancy kernel.
+template <int H>  // 16-byte parts per payload (R / 2 + 1)
 __global__ void __launch_bounds__(kThreads) k_serve(Ctx c) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
@@ -704,20 +705,33 @@ __global__ void __launch_bounds__(kThreads) k_serve(Ctx c) {
   // parts of the warp's 32 payloads (coalesced stores, whole-record loads)
   const int lane = threadIdx.x & 31;
   const long long wbase = n - lane;
-  const int H = c.R / 2 + 1;  // 16-byte parts per payload
   const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
   double2* pay = reinterpret_cast<double2*>(c.payload);
-  for (int idx = lane; idx < 32 * H; idx += 32) {
+#pragma unroll
+  for (int it = 0; it < H; ++it) {
+    const int idx = lane + 32 * it;
     const int slot = idx / H, part = idx - slot * H;
-    const unsigned as = __shfl_sync(0xffffffffu, a, slot);  // every lane reaches this shuffle
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
     const long long ns = wbase + slot;
-    if (ns >= c.N) continue;
-    double2 v;
-    if (part < H - 1)
-      v = __ldg(rec + static_cast<long long>(as) * (H - 1) + part);
-    else
-      v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(as));
-    pay[ns * H + part] = v;
+    if (ns < c.N) {
+      double2 v;
+      if (part < H - 1)
+        v = __ldg(rec + static_cast<long long>(as) * (H - 1) + part);
+      else
+        v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(as));
+      pay[ns * H + part] = v;
+    }
+  }
+}
+
+void launch_serve(const Ctx& c, int grid, cudaStream_t st) {
+  switch (c.R / 2 + 1) {
+    case 2: k_serve<2><<<grid, kThreads, 0, st>>>(c); break;
+    case 3: k_serve<3><<<grid, kThreads, 0, st>>>(c); break;
+    case 4: k_serve<4><<<grid, kThreads, 0, st>>>(c); break;
+    case 5: k_serve<5><<<grid, kThreads, 0, st>>>(c); break;
+    case 7: k_serve<7><<<grid, kThreads, 0, st>>>(c); break;
+    default: break;
   }
 }
 
@@ -1220,7 +1234,7 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   if (timed) CK(cudaEventRecord(ev[2], st));
   launch_scan(c, s->ntiles, st, 2);
   if (timed) CK(cudaEventRecord(ev[3], st));
-  k_serve<<<s->grid, kThreads, 0, st>>>(c);
+  launch_serve(c, s->grid, st);
   if (timed) CK(cudaEventRecord(ev[4], st));
   s->ks->update(c, s->grid, st);
   if (timed) CK(cudaEventRecord(ev[5], st));
