@@ -1095,7 +1095,6 @@ struct pfsmc_gpu_sampler {
   long long N = 0;
   int grid = 0, ntiles = 0;
   int num_sms = 148;
-  size_t l2_window = 0, l2_persist = 0;  // ancestor-search tables pinned in L2
   Ctx ctx{};
   cudaStream_t stream = nullptr;
   // device buffers
@@ -1373,34 +1372,12 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
     c.tile_log2 = tile_log2;
-    // the ancestor search's tables, in one range pinned in L2 (persisting
-    // access-policy window on the stream; the gathers stream past them)
-    {
-      const size_t nseg = (NT << tile_log2) >> kSegLog2;
-      const size_t bytes = nseg * sizeof(double) + (size_t(1) << cb) * sizeof(unsigned);
-      char* tab = s->dalloc<char>(bytes);
-      c.seg_end = reinterpret_cast<double*>(tab);
-      c.coarse = reinterpret_cast<unsigned*>(tab + nseg * sizeof(double));
-      int max_win = 0, max_persist = 0;
-      CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, cfg->device));
-      CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, cfg->device));
-      if (max_win > 0 && max_persist > 0) {
-        const size_t win = std::min(bytes, static_cast<size_t>(max_win));
-        size_t cur = 0;
-        CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-        const size_t want = std::min(win, static_cast<size_t>(max_persist));
-        if (cur < want) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-        cudaStreamAttrValue av{};
-        av.accessPolicyWindow.base_ptr = tab;
-        av.accessPolicyWindow.num_bytes = win;
-        av.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(want) / static_cast<float>(win));
-        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        CK(cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &av));
-        s->l2_window = win;
-        s->l2_persist = want;
-      }
-    }
+    // the ancestor search's tables (segment ends, guide): small, read with
+    // an L2 evict-last policy so the one-shot gathers stream past them. (A
+    // persisting access-policy window was measured: it cost the streaming
+    // kernels more than it saved, profiles/r01_notes.md.)
+    c.seg_end = s->dalloc<double>((NT << tile_log2) >> kSegLog2);
+    c.coarse = s->dalloc<unsigned>(size_t(1) << cb);
     const size_t GNT = NT * world;  // tile arrays cover every shard (aliased at tile0)
     c.n0 = static_cast<long long>(rank) * s->N;
     c.n_glob = static_cast<long long>(cfg->particles);
