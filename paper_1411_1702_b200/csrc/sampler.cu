@@ -263,7 +263,125 @@ struct ResolverSmem {
   int bad;
 };
 
-// The exact chain over tiles, one block. Each thread owns a run of K
+__device__ __forceinline__ TileHdr load_hdr(const TileHdr* hdr, int ti) {
+  TileHdr h;
+  h.nwin = __ldcg(&hdr[ti].nwin);
+  h.tail_e = __ldcg(&hdr[ti].tail_e);
+  h.tail_d0 = __ldcg(&hdr[ti].tail_d0);
+  h.tail_d1 = __ldcg(&hdr[ti].tail_d1);
+  return h;
+}
+
+struct WinSmem {
+  Piece wp[kResolveWin];   // piece from the previous window (or chain start) to this window
+  double wg[kResolveWin];  // the window element
+  double sa[kResolveWin];  // exact sum after the window
+  int wt[kResolveWin], wk[kResolveWin];
+  ResScan rsw[2 * kWarps];
+  int bad;
+};
+
+// The exact chain at WINDOW granularity, one block (the common case). Each
+// thread owns K consecutive tiles; a tile is the segmented element
+// (tail piece, head flag = has windows), so one block scan gives every
+// thread the piece from the last window before its tiles. Then: (1) threads
+// lay out every window's piece-since-the-previous-window in shared memory,
+// in global order; (2) ONE thread applies the windows serially (one exact
+// piece application and one real IEEE add each, ~log2 N of them); (3) every
+// thread derives its tiles' exact (start, end) from the window sums. Returns
+// false, having written nothing, when a tile overflowed its window list or
+// the windows exceed the staging area: the caller then runs resolve_chain.
+template <int ITEMS>
+__device__ bool resolve_windows(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
+                                double2* tile_info, int ntiles, WinSmem& ws) {
+  const int K = (ntiles + kThreads - 1) / kThreads;
+  const int tb = min(static_cast<int>(threadIdx.x) * K, ntiles), te = min(tb + K, ntiles);
+  Piece agg = piece_identity();
+  int nw = 0, ovf = 0;
+  for (int t0 = tb; t0 < te; t0 += 8) {
+    TileHdr h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (t0 + i < te) h[i] = load_hdr(hdr, t0 + i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (t0 + i < te) {
+        ovf += h[i].nwin < 0;
+        nw += max(h[i].nwin, 0);
+        agg = piece_combine(agg, Piece{h[i].tail_d0, h[i].tail_d1, h[i].tail_e, h[i].nwin != 0});
+      }
+    }
+  }
+  ResScan tot;
+  const ResScan ex = block_excl_scan_res(ResScan{agg, ovf, nw}, tot, ws.rsw);
+  if (tot.rank > 0 || tot.wofs > kResolveWin) return false;  // uniform
+  if (threadIdx.x == 0) {
+    ws.bad = 0;
+    c.st->tstamp[3] = c.st->tstamp[4] = global_ns();
+    c.st->tstamp[7] = static_cast<unsigned long long>(tot.wofs);
+  }
+  {
+    Piece E = ex.pc;
+    int wo = ex.wofs;
+    for (int t = tb; t < te; ++t) {
+      const TileHdr h = load_hdr(hdr, t);
+      for (int k = 0; k < h.nwin; ++k) {
+        const TileWin* gw = win + static_cast<size_t>(t) * kMaxWin + k;
+        Piece pc{__ldcg(&gw->d0), __ldcg(&gw->d1), __ldcg(&gw->e), 0};
+        if (k == 0) pc = piece_combine(E, pc);
+        ws.wp[wo] = pc;
+        ws.wg[wo] = __ldcg(&gw->g);
+        ws.wt[wo] = t;
+        ws.wk[wo] = k;
+        ++wo;
+      }
+      E = piece_combine(E, Piece{h.tail_d0, h.tail_d1, h.tail_e, h.nwin != 0});
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.st->tstamp[5] = global_ns();
+    double s = 0.0;
+    bool ok = true;
+    for (int w = 0; w < tot.wofs; ++w) {
+      ok &= piece_apply(ws.wp[w], s);
+      s = s + ws.wg[w];  // the window element: a real IEEE add, as acc += g[i]
+      ws.sa[w] = s;
+    }
+    if (!ok) ws.bad = 1;
+    c.st->tstamp[6] = global_ns();
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < tot.wofs; w += kThreads)
+    win_after[static_cast<size_t>(ws.wt[w]) * kMaxWin + ws.wk[w]] = ws.sa[w];
+  {
+    double s = ex.wofs > 0 ? ws.sa[ex.wofs - 1] : 0.0;
+    bool ok = piece_apply(ex.pc, s);
+    int wo = ex.wofs;
+    for (int t = tb; t < te; ++t) {
+      const TileHdr h = load_hdr(hdr, t);
+      const double s_in = s;
+      if (h.nwin > 0) {
+        wo += h.nwin;
+        s = ws.sa[wo - 1];
+      }
+      ok &= piece_apply(Piece{h.tail_d0, h.tail_d1, h.tail_e, 0}, s);
+      double s_end = s;
+      if (t == ntiles - 1) {
+        c.st->total_mass = s_end;
+        s_end = (s_end < 1.0) ? 1.0 : s_end;  // guard the last bin (filter.cpp:168)
+      }
+      tile_info[t] = make_double2(s_in, s_end);
+    }
+    if (!ok) ws.bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ws.bad) atomicOr(&c.st->error, kErrInternal);
+  return true;
+}
+
+// Fallback (a tile overflowed its window list, or > kResolveWin windows):
+// the exact chain over tiles, one block. Each thread owns a run of K
 // consecutive tiles (a super-tile); window-free super-tiles compose in a
 // segmented monoid scan, the windowed ones are walked in order by one
 // thread with real IEEE adds at the windows; everything that walk touches
@@ -279,14 +397,6 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
     rs.bad = 0;
   }
   __syncthreads();
-  auto load_hdr = [&](int ti) {
-    TileHdr h;
-    h.nwin = __ldcg(&hdr[ti].nwin);
-    h.tail_e = __ldcg(&hdr[ti].tail_e);
-    h.tail_d0 = __ldcg(&hdr[ti].tail_d0);
-    h.tail_d1 = __ldcg(&hdr[ti].tail_d1);
-    return h;
-  };
   for (int b0 = 0; b0 < ntiles; b0 += kThreads * K) {
     const int tb = b0 + threadIdx.x * K;
     const int te = min(tb + K, ntiles);
@@ -295,7 +405,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
     bool windowed = false;
     int nw = 0;
     for (int ti = tb; ti < te; ++ti) {
-      const TileHdr h = load_hdr(ti);
+      const TileHdr h = load_hdr(hdr, ti);
       if (h.nwin != 0) {
         windowed = true;
         nw += h.nwin > 0 ? h.nwin : 0;
@@ -316,7 +426,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
       rs.wlist[ex.rank] = threadIdx.x;
       rs.excl[ex.rank] = ex.pc;
       if (ex.rank < kStageSuper)
-        for (int ti = tb; ti < te; ++ti) rs.hdr[ex.rank * kMaxSuper + (ti - tb)] = load_hdr(ti);
+        for (int ti = tb; ti < te; ++ti) rs.hdr[ex.rank * kMaxSuper + (ti - tb)] = load_hdr(hdr, ti);
       int w = ex.wofs;  // record where the windows live; loaded cooperatively below
       for (int ti = tb; ti < te; ++ti) {
         const int n = __ldcg(&hdr[ti].nwin);
@@ -338,7 +448,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
         double s = seg;
         ok &= piece_apply(rs.excl[r], s);
         for (int ti = st0; ti < st1; ++ti) {
-          const TileHdr wh = r < kStageSuper ? rs.hdr[r * kMaxSuper + (ti - st0)] : load_hdr(ti);
+          const TileHdr wh = r < kStageSuper ? rs.hdr[r * kMaxSuper + (ti - st0)] : load_hdr(hdr, ti);
           const double s_in = s;
           if (wh.nwin < 0 && !own_g) {
             ok = false;  // window overflow in a remote tile: unsupported when sharded
@@ -386,7 +496,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
       double s = ex.rank > 0 ? rs.out[ex.rank - 1] : rs.carry;
       bool ok = piece_apply(ex.pc, s);
       for (int ti = tb; ti < te; ++ti) {
-        const TileHdr h = load_hdr(ti);
+        const TileHdr h = load_hdr(hdr, ti);
         const double s_in = s;
         ok &= piece_apply(Piece{h.tail_d0, h.tail_d1, h.tail_e, 0}, s);
         double s_end = s;
@@ -414,6 +524,7 @@ template <int ITEMS>
 union PiecesSmem {
   double g[TileCfg<ITEMS>::kSmem];
   ResolverSmem rs;
+  WinSmem ws;
 };
 
 // S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
@@ -510,16 +621,21 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) c.st->tstamp[1] = global_ns();
-  resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
+  if (!resolve_windows<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, sm.ws))
+    resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
   if (threadIdx.x == 0) c.st->tstamp[2] = global_ns();
 }
 
 // Sharded: every rank resolves the exact chain over ALL shards' tiles.
 template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c) {
-  __shared__ ResolverSmem rs;
+  __shared__ union {
+    ResolverSmem rs;
+    WinSmem ws;
+  } sm;
   if (grid_error(c)) return;
-  resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, rs);
+  if (!resolve_windows<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, sm.ws))
+    resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, sm.rs);
 }
 
 // S3: exact per-element CDF (from the S2 per-thread handoff: no block
