@@ -119,8 +119,18 @@ struct ScanScratch {
 
 // Fast-path rounding of one element in a known binade: delta for even /
 // odd m (identical unless g/u ends in exactly one half).
-__device__ __forceinline__ void run_delta(double g, double scale, long long& d0, long long& d1) {
-  const double v = g * scale;
+// The scale 2^(52-e) is passed as two exact factors: for the subnormal
+// binade (e = -1022) 2^1074 itself overflows, 2^537 * 2^537 does not.
+struct UlpScale {
+  double s1, s2;
+};
+__device__ __forceinline__ UlpScale ulp_scale(int e) {
+  const int k = 52 - e;
+  return k <= 1000 ? UlpScale{scale2(1.0, k), 1.0} : UlpScale{scale2(1.0, k - k / 2), scale2(1.0, k / 2)};
+}
+
+__device__ __forceinline__ void run_delta(double g, UlpScale scale, long long& d0, long long& d1) {
+  const double v = (g * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
   const double q = floor(v);
   const double f = v - q;
   const long long qi = static_cast<long long>(q);
@@ -161,7 +171,7 @@ __device__ __forceinline__ void chunk_analyse(ThreadTile<ITEMS>& tt) {
   const int e_hi = binade_of(tt.p[ITEMS] + E);
   if (e_lo == e_hi) {
     tt.uniform_e = e_lo;
-    const double scale = scale2(1.0, 52 - e_lo);
+    const UlpScale scale = ulp_scale(e_lo);
     long long s0 = 0, s1 = 0;
     bool tie = false;
 #pragma unroll
@@ -687,7 +697,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
         for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
       } else {
         const int e = tt.uniform_e;
-        const double scale = scale2(1.0, 52 - e);
+        const UlpScale scale = ulp_scale(e);
         long long m = static_cast<long long>(scale2(s0, 52 - e));
         const long long m_hi = 1LL << 53;
 #pragma unroll

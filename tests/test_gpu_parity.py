@@ -86,6 +86,20 @@ def _g_cases(rng):
     tiny[0] = 1e-300
     tiny[1] = 5e-324
     out["subnormal_head"] = tiny / tiny.sum()
+    # every element doubles the running sum: one binade crossing (window) per
+    # element, > kMaxWin in one tile -> serial tile + super-tile resolver
+    stair = np.zeros(4096)
+    stair[:1100] = 2.0 ** (np.arange(1100) - 1070.0)
+    out["staircase_overflow"] = stair
+    # > kResolveWin windows in total, <= kMaxWin per tile -> super-tile resolver
+    spread = np.zeros(1 << 16)
+    spread[np.arange(300) * 200 + 7] = 2.0 ** (np.arange(300) - 1070.0)
+    out["staircase_spread"] = spread
+    # ~120 windows spread over many tiles -> window-granular resolver
+    mid = np.zeros(1 << 17)
+    mid[np.arange(120) * 1000 + 3] = 2.0 ** (np.arange(120) - 110.0)
+    mid[mid == 0] = 1e-40
+    out["staircase_windows"] = mid
     return out
 
 
