@@ -121,6 +121,35 @@ def test_resample_from_injected_g_is_bit_exact():
         s.close()
 
 
+def test_resample_randomized_structures_bit_exact():
+    """Property check over 40 seeded random fitness structures (sizes from 1
+    to ~3e5, zero runs, σ up to 8 log-normal mass, subnormal and huge
+    values): the device CDF is the sequential sum bit for bit and the
+    ancestors are the reference's."""
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    rng = np.random.default_rng(2024)
+    for case in range(40):
+        n = int(rng.choice([1, 2, 7, 255, 2048, 2049, 4096 * 3 + 1, int(rng.integers(1, 300000))]))
+        g = np.exp(rng.uniform(0, 8) * rng.standard_normal(n) - rng.uniform(0, 700))
+        if rng.random() < 0.5:
+            z0 = int(rng.integers(0, n))
+            g[z0:z0 + int(rng.integers(0, n))] = 0.0
+        if rng.random() < 0.3:
+            g[rng.integers(0, n, size=max(1, n // 50))] = 5e-324 * rng.integers(1, 1000)
+        if rng.random() < 0.2:
+            g[int(rng.integers(0, n))] = 2.0 ** int(rng.integers(-60, 60))
+        if rng.random() < 0.5 and g.sum() > 0:
+            g = g / g.sum()
+        s = GpuSampler("lv", PfConfig(particles=n, seed=7 + case), ObservationModel([0, 1], 0.05))
+        anc, cdf = s.resample_from_g(g, 3, with_cdf=True)
+        ref = np.cumsum(g)
+        ref[-1] = max(ref[-1], 1.0)
+        assert np.array_equal(cdf, ref), (case, n, np.flatnonzero(cdf != ref)[:5])
+        want = O.resample(g, 7 + case, 3)
+        assert np.array_equal(anc.astype(np.int64), want), (case, n)
+        s.close()
+
+
 def test_resample_golden_fixture():
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     d = np.load(os.path.join(GOLD, "resample.npz"))
