@@ -383,7 +383,7 @@ def main():
         if not args.replicas:
             return run_sharded(args, world, rank, local)
     n = args.particles
-    T = min(T_OBS, args.steps + args.warmup + args.e2e_steps + 1)
+    T = min(T_OBS, 2 * args.steps + args.warmup + args.e2e_steps + 1)
     prob = problems.lotka_volterra(particles=n, T=T_OBS, seed=1)
     # replicas: every rank filters its own N-particle ensemble
     cfg = prob.cfg
@@ -397,11 +397,12 @@ def main():
         j += 1
         gpu.step_resident(j)
     gpu.synchronize()
-    gpu.set_kernel_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    # headline: the production path (one CUDA graph per step, programmatic
+    # dependent launches between the five kernels), events around each step
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             gpu.flush_l2()
@@ -414,6 +415,14 @@ def main():
         last = gpu.synchronize()
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    # per-kernel breakdown (and the roofline's kernel duration): a second pass
+    # of the same steps with events between the kernels (no graph, no PDL)
+    gpu.set_kernel_timing(True)
+    for k in range(args.steps):
+        gpu.flush_l2()
+        j += 1
+        gpu.step_resident(j)
+    gpu.synchronize()
     kt = gpu.kernel_times()
     gpu.set_kernel_timing(False)
     total_ms = sum(step_ms)
