@@ -193,6 +193,11 @@ LOCKSTEP = [
     ("lv_bdf3_m4", dict(model="lv", family="bdf", order=3, h=0.025, seed=23), 1 << 13, 5, 4),
     ("lv_am3_m4", dict(model="lv", family="am", order=3, h=0.025, seed=24), 1 << 13, 5, 4),
     ("lv_ab3_m4", dict(model="lv", family="ab", order=3, h=0.025, seed=25), 1 << 13, 5, 4),
+    # ragged sizes: partial warps / blocks / tiles / segments
+    ("lv_am2_n5003", dict(model="lv", family="am", order=2, h=0.1, seed=26), 5003, 5, 1),
+    ("lv_bdf2_n257", dict(model="lv", family="bdf", order=2, h=0.05, seed=27), 257, 5, 2),
+    ("lv_am1_n3", dict(model="lv", family="am", order=1, h=0.1, seed=28), 3, 4, 1),
+    ("lv_ab2_n70001", dict(model="lv", family="ab", order=2, h=0.1, seed=29), 70001, 3, 1),
 ]
 
 
