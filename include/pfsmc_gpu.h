@@ -47,7 +47,9 @@ enum {
   PFSMC_GPU_MODEL_LOTKA_VOLTERRA = 1,
   PFSMC_GPU_MODEL_ROBERTSON = 2,
   PFSMC_GPU_MODEL_CHAIN8 = 3,
-  PFSMC_GPU_MODEL_PAYLOAD64 = 4   /* 64-byte record, resample microbenchmark only */
+  PFSMC_GPU_MODEL_PAYLOAD64 = 4,  /* 64-byte record, resample microbenchmark only */
+  PFSMC_GPU_MODEL_METABOLIC = 5   /* the reference's problem 1, models::MetabolicModel
+                                     (models.cpp:37-119): d = 3, p = 4, time-dependent input */
 };
 /* lmm::Family (lmm.hpp:12) */
 enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
@@ -73,6 +75,9 @@ typedef struct pfsmc_gpu_config {
   double sigma;            /* ObservationModel.sigma */
   int likelihood;          /* PFSMC_GPU_LIK_* */
   int device;              /* CUDA ordinal */
+  double model_consts[8];  /* the bound model's constants; METABOLIC: (lambda, c0, A0, A,
+                              t0_input, tau) = MetabolicConstants (models.hpp:67-74),
+                              reference defaults (1, 1, 1, 5, 2, 1); others: unused */
 } pfsmc_gpu_config;
 
 const char* pfsmc_gpu_version(void);

@@ -67,6 +67,9 @@ struct PfConfig {
   double newton_tol = 1e-9;
   int newton_max_iter = 20;
   int device = 0;
+  // the bound model's constants; METABOLIC: models::MetabolicConstants
+  // (lambda, c0, A0, A, t0_input, tau), reference defaults (models.hpp:67-74)
+  double model_consts[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
 };
 
 // filter::TraceRow (filter.hpp:67-75).
@@ -95,6 +98,7 @@ class Sampler {
     c.sigma = obs.sigma;
     c.likelihood = obs.likelihood;
     c.device = cfg.device;
+    for (int k = 0; k < 8; ++k) c.model_consts[k] = cfg.model_consts[k];
     check(pfsmc_gpu_create(&c, &h_));
   }
   ~Sampler() { pfsmc_gpu_destroy(h_); }

@@ -120,6 +120,7 @@ int or_model_dims(int model, int* d, int* p) {
     case OR_MODEL_LV: *d = 2; *p = 2; return OR_OK;
     case OR_MODEL_ROBERTSON: *d = 3; *p = 3; return OR_OK;
     case OR_MODEL_CHAIN: *d = 8; *p = 4; return OR_OK;
+    case OR_MODEL_METABOLIC: *d = 3; *p = 4; return OR_OK;
   }
   return fail(OR_CONFIG, "unknown model id");
 }
@@ -130,9 +131,35 @@ static int all_finite(const double* v, int n) {
   return 1;
 }
 
+/* Constants of the bound model (MetabolicConstants, models.hpp:67-74:
+ * lambda, c0, A0, A, t0_input, tau), set with or_set_model_consts. */
+static double g_mk[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
+
+void or_set_model_consts(const double* k) {
+  for (int i = 0; i < 8; ++i) g_mk[i] = k[i];
+}
+
+/* input_phi (models.cpp:37-42) */
+static double input_phi(double t, double A0, double A, double t0_input, double tau) {
+  const double dt = t - t0_input;
+  if (dt <= 0.0) return A0;
+  return A0 + A * dt * exp(-dt / tau);
+}
+
 /* rhs(t, x) -> f; returns 0 when undefined/non-finite (models.hpp:24-27). */
-static int model_rhs(int model, const double* th, const double* x, double* o) {
+static int model_rhs(int model, double t, const double* th, const double* x, double* o) {
   switch (model) {
+    case OR_MODEL_METABOLIC: { /* metabolic_rhs (models.cpp:44-57) */
+      const double den1 = x[0] + th[1];
+      const double den2 = x[1] + th[3];
+      if (den1 <= 0.0 || den2 <= 0.0) return 0;
+      const double flux1 = th[0] * x[0] / den1;
+      const double flux2 = th[2] * x[1] / den2;
+      o[0] = input_phi(t, g_mk[2], g_mk[3], g_mk[4], g_mk[5]) - flux1;
+      o[1] = flux1 - flux2;
+      o[2] = flux2 - g_mk[0] * (x[2] - g_mk[1]);
+      return all_finite(o, 3);
+    }
     case OR_MODEL_DECAY:
       o[0] = -th[0] * x[0];
       return 1;
@@ -166,12 +193,27 @@ static int model_rhs(int model, const double* th, const double* x, double* o) {
 }
 
 int or_rhs(int model, const double* theta_nat, const double* x, double* f) {
-  return model_rhs(model, theta_nat, x, f);
+  return model_rhs(model, 0.0, theta_nat, x, f);
 }
 
 /* Dense Jacobian, row-major d x d. */
-static int model_jac(int model, const double* th, const double* x, double* J) {
+static int model_jac(int model, double t, const double* th, const double* x, double* J) {
+  (void)t;
   switch (model) {
+    case OR_MODEL_METABOLIC: { /* metabolic_jacobian (models.cpp:59-76) */
+      const double den1 = x[0] + th[1];
+      const double den2 = x[1] + th[3];
+      if (den1 <= 0.0 || den2 <= 0.0) return 0;
+      const double d1 = th[0] * th[1] / (den1 * den1);
+      const double d2 = th[2] * th[3] / (den2 * den2);
+      for (int i = 0; i < 9; ++i) J[i] = 0.0;
+      J[0] = -d1;
+      J[3] = d1;
+      J[4] = -d2;
+      J[7] = d2;
+      J[8] = -g_mk[0];
+      return isfinite(d1) && isfinite(d2);
+    }
     case OR_MODEL_DECAY:
       J[0] = -th[0];
       return 1;
@@ -344,7 +386,7 @@ static void lu_solve(int n, const double* lu, const int* piv, double* x) {
 }
 
 /* newton_solve (lmm.cpp:219-266), dense path. Returns status, iterations. */
-static int newton_solve(int model, const double* th, int d, double hb0,
+static int newton_solve(int model, double t_next, const double* th, int d, double hb0,
                         const double* c, const double* guess, double tol,
                         int max_iter, double* out, int* iters) {
   double f[OR_MAX_D], r[OR_MAX_D], J[OR_MAX_D * OR_MAX_D];
@@ -352,9 +394,9 @@ static int newton_solve(int model, const double* th, int d, double hb0,
   memcpy(out, guess, sizeof(double) * d);
   for (int iter = 1; iter <= max_iter; ++iter) {
     *iters = iter;
-    if (!model_rhs(model, th, out, f)) return OR_ST_INVALID_RHS;
+    if (!model_rhs(model, t_next, th, out, f)) return OR_ST_INVALID_RHS;
     for (int j = 0; j < d; ++j) r[j] = out[j] - hb0 * f[j] - c[j];
-    if (!model_jac(model, th, out, J)) return OR_ST_INVALID_RHS;
+    if (!model_jac(model, t_next, th, out, J)) return OR_ST_INVALID_RHS;
     for (int i = 0; i < d * d; ++i) J[i] = -hb0 * J[i];
     for (int i = 0; i < d; ++i) J[i * d + i] += 1.0;
     if (!lu_factor(d, J, piv)) return OR_ST_SINGULAR;
@@ -406,7 +448,7 @@ static int propagate(int model, int d, const double* th, const double* x0,
   for (int j = 0; j < d; ++j) gamma[j] = 0.0;
   *status = OR_ST_OK;
   *iters = 0;
-  if (!model_rhs(model, th, x, fnew)) {
+  if (!model_rhs(model, t0, th, x, fnew)) {
     *status = OR_ST_INVALID_RHS;
     memcpy(state, x, sizeof(double) * d);
     return OR_OK;
@@ -455,7 +497,7 @@ static int propagate(int model, int d, const double* th, const double* x0,
       }
       ref = pred;
       int it = 0;
-      const int st = newton_solve(model, th, d, h * act.beta[0], c, guess, tol,
+      const int st = newton_solve(model, t_next, th, d, h * act.beta[0], c, guess, tol,
                                   max_iter, xnew, &it);
       *iters += it;
       if (st != OR_ST_OK) {
@@ -468,7 +510,7 @@ static int propagate(int model, int d, const double* th, const double* x0,
       const double est = factor * fabs(xnew[j] - ref[j]);
       gamma[j] += est * est;
     }
-    if (!model_rhs(model, th, xnew, fnew)) {
+    if (!model_rhs(model, t_next, th, xnew, fnew)) {
       *status = OR_ST_INVALID_RHS;
       break;
     }

@@ -24,7 +24,8 @@ enum { OR_OK = 0, OR_INTERNAL = 1, OR_CONFIG = 2, OR_NUMERICAL = 3 };
 enum { OR_PURPOSE_INIT = 0, OR_PURPOSE_PROLIFERATE = 1, OR_PURPOSE_INNOVATE = 2,
        OR_PURPOSE_RESAMPLE = 3 };
 enum { OR_AB = 0, OR_AM = 1, OR_BDF = 2 };
-enum { OR_MODEL_DECAY = 0, OR_MODEL_LV = 1, OR_MODEL_ROBERTSON = 2, OR_MODEL_CHAIN = 3 };
+enum { OR_MODEL_DECAY = 0, OR_MODEL_LV = 1, OR_MODEL_ROBERTSON = 2, OR_MODEL_CHAIN = 3,
+       OR_MODEL_METABOLIC = 5 /* the reference's models::MetabolicModel (models.cpp:37-119) */ };
 enum { OR_LIK_GAUSSIAN = 0, OR_LIK_LOGNORMAL = 1 };
 enum { OR_ST_OK = 0, OR_ST_INVALID_RHS = 1, OR_ST_NEWTON_DIVERGENCE = 2,
        OR_ST_SINGULAR = 3 };
@@ -73,6 +74,8 @@ int or_stream_draws(uint64_t seed, uint64_t j, uint64_t n, int purpose, int kind
                     uint64_t count, void* out);
 int or_model_dims(int model, int* d, int* p);
 int or_rhs(int model, const double* theta_nat, const double* x, double* f);
+/* Constants of the bound model (METABOLIC: lambda, c0, A0, A, t0_input, tau). */
+void or_set_model_consts(const double* k);
 int or_propagate_interval(int model, const double* theta_nat, const double* x0,
                           double t0, double t1, double h, int family, int order,
                           double tol, int max_iter, double* state_out,

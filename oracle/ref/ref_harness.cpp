@@ -73,7 +73,7 @@ extern "C" {
 // Mirrors the fields of filter::PfConfig / ObservationModel that pf_step
 // reads (filter.hpp:30-65), flattened to plain C.
 typedef struct ref_cfg {
-  int model;        // 0 decay, 1 Lotka-Volterra, 2 Robertson, 3 chain
+  int model;        // 0 decay, 1 Lotka-Volterra, 2 Robertson, 3 chain, 5 metabolic
   int family;       // 0 ab, 1 am, 2 bdf
   int order;        // 1..3
   double h;         // fixed LMM step
@@ -97,6 +97,11 @@ typedef struct ref_ens {
 } ref_ens;
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// Constants of the bound MetabolicModel for the next model construction.
+void ref_set_model_consts(const double* k) {
+  for (int i = 0; i < 8; ++i) pfsmc_oracle_ref::g_model_consts[i] = k[i];
+}
 
 int ref_philox(const uint64_t* ctr, const uint64_t* key, uint64_t* out) {
   return guarded([&] {

@@ -196,10 +196,24 @@ class ChainModel : public OdeModel {
   }
 };
 
-enum ModelId { kDecay = 0, kLotkaVolterra = 1, kRobertson = 2, kChain = 3 };
+enum ModelId { kDecay = 0, kLotkaVolterra = 1, kRobertson = 2, kChain = 3, kMetabolic = 5 };
+
+// Constants for the reference's own MetabolicModel (models.hpp:67-74), set
+// through the harness (ref_set_model_consts): lambda, c0, A0, A, t0_input, tau.
+inline double g_model_consts[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
 
 inline std::unique_ptr<OdeModel> make_model(int id) {
   switch (id) {
+    case kMetabolic: {  // the reference's own plugin, unmodified (models.cpp:37-119)
+      pfsmc::models::MetabolicConstants k;
+      k.lambda = g_model_consts[0];
+      k.c0 = g_model_consts[1];
+      k.A0 = g_model_consts[2];
+      k.A = g_model_consts[3];
+      k.t0_input = g_model_consts[4];
+      k.tau = g_model_consts[5];
+      return std::make_unique<pfsmc::models::MetabolicModel>(k);
+    }
     case kDecay:
       return std::make_unique<DecayModel>();
     case kLotkaVolterra:

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-diag-suppress", "497", "-Xptxas", "-warn-spills"]
 SOURCES = ["sampler.cu", "kernels_decay.cu", "kernels_lv.cu", "kernels_robertson.cu",
-           "kernels_chain.cu", "kernels_payload.cu"]
+           "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu"]
 
 
 def _stale(obj: str, src: str) -> bool:

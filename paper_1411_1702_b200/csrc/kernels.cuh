@@ -86,6 +86,7 @@ struct Ctx {
   int max_iter;
   unsigned long long seed;
   double two_s2;
+  double mconst[8];  // model constants (METABOLIC: lambda, c0, A0, A, t0_input, tau)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
   double* rec[2];
@@ -333,7 +334,8 @@ __global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 4 : M::D <= 3 ? 4 : 1))
 #pragma unroll
     for (int k = 0; k < P; ++k) th[k] = exp(c.a * tu[k] + c.one_minus_a * st.mu[k]);
     Propagator<M, FAM, ORD> prop;
-    const int status = prop.run(th, x, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    prop.mk = M::load_k(c.mconst);
+    const int status = prop.run(th, x, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
     const double ll = status == kOk ? loglik<M>(c, sp, x) : kNegInf;
     c.llbar[n] = ll;
     lgv = logw + ll;
@@ -604,7 +606,8 @@ __global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1))
 #pragma unroll
     for (int k = 0; k < D; ++k) xr[k] = x[k];
     Propagator<M, FAM, ORD> prop;
-    const int status = prop.run(th, xr, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    prop.mk = M::load_k(c.mconst);
+    const int status = prop.run(th, xr, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
     double ll = kNegInf;
     if (status == kOk) {
       double zi[D];
@@ -826,6 +829,7 @@ std::unique_ptr<KernelSet> make_kernels_lv(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_robertson(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_chain(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_payload(int fam, int order);
+std::unique_ptr<KernelSet> make_kernels_metabolic(int fam, int order);
 
 inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
   switch (model) {
@@ -834,6 +838,7 @@ inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
     case RobertsonModel::ID: return make_kernels_robertson(fam, order);
     case ChainModel::ID: return make_kernels_chain(fam, order);
     case Payload64Model::ID: return make_kernels_payload(fam, order);
+    case MetabolicModel::ID: return make_kernels_metabolic(fam, order);
   }
   return nullptr;
 }

@@ -1,0 +1,10 @@
+// Kernel instantiations for MetabolicModel (the reference's problem 1,
+// models.cpp:37-119): every (family, order) of the fixed-step integrator set
+// (lmm.cpp:64-77: AB/AM/BDF x orders 1-3).
+#include "kernels.cuh"
+
+namespace pfsmc_gpu {
+std::unique_ptr<KernelSet> make_kernels_metabolic(int fam, int order) {
+  return make_family<MetabolicModel>(fam, order);
+}
+}  // namespace pfsmc_gpu

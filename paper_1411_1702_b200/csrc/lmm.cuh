@@ -131,13 +131,13 @@ __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[
 // takes the dense path below, which rebuilds J with M::jac; it is kept out of
 // line so the 8x8 matrix never lives in the hot loop's registers.
 template <class M>
-__device__ __forceinline__ bool dense_newton_solve(const double* th_p, const double* x_p, double hb0,
-                                                double* r_p) {
+__device__ __forceinline__ bool dense_newton_solve(const typename M::K& mk, double tn, const double* th_p,
+                                                   const double* x_p, double hb0, double* r_p) {
   constexpr int D = M::D;
   double th[M::P], x[D], r[D], A[D][D];
   for (int j = 0; j < M::P; ++j) th[j] = th_p[j];
   for (int j = 0; j < D; ++j) x[j] = x_p[j], r[j] = r_p[j];
-  M::jac(th, x, A);  // finite: jac_band (same entries) was checked
+  M::jac(mk, tn, th, x, A);  // finite: jac_band (same entries) was checked
   for (int i = 0; i < D; ++i)
     for (int j = 0; j < D; ++j) A[i][j] = -hb0 * A[i][j];
   for (int i = 0; i < D; ++i) A[i][i] += 1.0;
@@ -147,7 +147,8 @@ __device__ __forceinline__ bool dense_newton_solve(const double* th_p, const dou
 }
 
 template <class M>
-__device__ __forceinline__ bool band_solve(const double (&th)[M::P], const double (&x)[M::D],
+__device__ __forceinline__ bool band_solve(const typename M::K& mk, double tn, const double (&th)[M::P],
+                                           const double (&x)[M::D],
                                            double hb0, const double (&jd)[M::D],
                                            const double (&js)[M::D - 1], double (&b)[M::D]) {
   constexpr int D = M::D;
@@ -164,7 +165,7 @@ __device__ __forceinline__ bool band_solve(const double (&th)[M::P], const doubl
     sb[c] = -hb0 * js[c];
     fast &= !(fabs(sb[c]) > fabs(dg[c]));
   }
-  if (!fast) return dense_newton_solve<M>(th, x, hb0, b);
+  if (!fast) return dense_newton_solve<M>(mk, tn, th, x, hb0, b);
 #pragma unroll
   for (int i = 1; i < D; ++i) {
     const double l = sb[i - 1] * (1.0 / dg[i - 1]);
@@ -177,13 +178,14 @@ __device__ __forceinline__ bool band_solve(const double (&th)[M::P], const doubl
 
 // ---- Newton on G(x) = x - h b0 f(x) - c (lmm.cpp:219-266) ---------------
 template <class M>
-__device__ __forceinline__ int newton_solve(const double (&th)[M::P], double hb0,
+__device__ __forceinline__ int newton_solve(const typename M::K& mk, double tn, const double (&th)[M::P],
+                                            double hb0,
                                             const double (&c)[M::D], double (&x)[M::D],
                                             double tol, int max_iter, int& iters) {
   constexpr int D = M::D;
   for (int iter = 1; iter <= max_iter; ++iter) {
     double f[D], r[D];
-    if (!M::rhs(th, x, f)) {
+    if (!M::rhs(mk, tn, th, x, f)) {
       iters += iter;
       return kInvalidRhs;
     }
@@ -192,14 +194,14 @@ __device__ __forceinline__ int newton_solve(const double (&th)[M::P], double hb0
     bool solved;
     if constexpr (M::kLowerBidiagonal) {
       double jd[D], js[D - 1];
-      if (!M::jac_band(th, x, jd, js)) {
+      if (!M::jac_band(mk, tn, th, x, jd, js)) {
         iters += iter;
         return kInvalidRhs;
       }
-      solved = band_solve<M>(th, x, hb0, jd, js, r);
+      solved = band_solve<M>(mk, tn, th, x, hb0, jd, js, r);
     } else {
       double A[D][D];
-      if (!M::jac(th, x, A)) {
+      if (!M::jac(mk, tn, th, x, A)) {
         iters += iter;
         return kInvalidRhs;
       }
@@ -245,6 +247,7 @@ struct Propagator {
 
   double xs[SD][D];
   double fs[FD][D];
+  typename M::K mk;  // model constants (the bound OdeModel's state, models.hpp:20-55)
 
   // AB(q) explicit combination: 0 + 1.0*x_n, then (h*beta_i) f_{n+1-i}.
   template <int Q>
@@ -319,7 +322,7 @@ struct Propagator {
   // One ramp step at compile-time active order PA with AV history entries.
   // Returns the particle status (kOk keeps going).
   template <int PA, int AV>
-  __device__ __forceinline__ int step(const double (&th)[P], double h, double tol, int max_iter,
+  __device__ __forceinline__ int step(const double (&th)[P], double tn, double h, double tol, int max_iter,
                                       double (&gamma)[D], int& iters) {
     double xnew[D], ref[D];
     double factor;
@@ -354,7 +357,7 @@ struct Propagator {
         factor = fabs(bdf_C(PA)) / fabs(1.0 - bdf_C(PA));
       }
       const double b0 = FAM == kAM ? am_beta(PA, 0) : bdf_beta0(PA);
-      const int st = newton_solve<M>(th, h * b0, c, xnew, tol, max_iter, iters);
+      const int st = newton_solve<M>(mk, tn, th, h * b0, c, xnew, tol, max_iter, iters);
       if (st != kOk) return st;
     }
     // finish_step (lmm.cpp:438-452)
@@ -364,7 +367,7 @@ struct Propagator {
       gamma[j] += est * est;
     }
     double fnew[D];
-    if (!M::rhs(th, xnew, fnew)) return kInvalidRhs;
+    if (!M::rhs(mk, tn, th, xnew, fnew)) return kInvalidRhs;
     push(xnew, fnew);
     return kOk;
   }
@@ -429,7 +432,7 @@ struct Propagator {
       }
     }
   }
-  __device__ __forceinline__ int step_rt(int pa, int av, const double (&th)[P], double h, double tol,
+  __device__ __forceinline__ int step_rt(int pa, int av, const double (&th)[P], double tn, double h, double tol,
                                          int max_iter, double (&gamma)[D], int& iters) {
     double xnew[D], ref[D];
     double factor;
@@ -466,7 +469,7 @@ struct Propagator {
         }
       }
       const double b0 = FAM == kAM ? am_beta(pa, 0) : bdf_beta0(pa);
-      const int st = newton_solve<M>(th, h * b0, c, xnew, tol, max_iter, iters);
+      const int st = newton_solve<M>(mk, tn, th, h * b0, c, xnew, tol, max_iter, iters);
       if (st != kOk) return st;
     }
 #pragma unroll
@@ -475,19 +478,20 @@ struct Propagator {
       gamma[j] += est * est;
     }
     double fnew[D];
-    if (!M::rhs(th, xnew, fnew)) return kInvalidRhs;
+    if (!M::rhs(mk, tn, th, xnew, fnew)) return kInvalidRhs;
     push(xnew, fnew);
     return kOk;
   }
 
   // propagate_interval (lmm.cpp:468-503): m fixed steps of size h from x.
   // On return x holds the last accepted state (the reference's run.x).
-  __device__ __forceinline__ int run(const double (&th)[P], double (&x)[D], double h, int m,
+  // t_next = t0 + k h (lmm.cpp:482), not an accumulated sum.
+  __device__ __forceinline__ int run(const double (&th)[P], double (&x)[D], double t0, double h, int m,
                                      double tol, int max_iter, double (&gamma)[D], int& iters) {
 #pragma unroll
     for (int j = 0; j < D; ++j) gamma[j] = 0.0;
     double f0[D];
-    if (!M::rhs(th, x, f0)) return kInvalidRhs;
+    if (!M::rhs(mk, t0, th, x, f0)) return kInvalidRhs;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       xs[0][j] = x[j];
@@ -496,7 +500,8 @@ struct Propagator {
     int st = kOk;
     if constexpr (D >= 6) {
       for (int k = 1; k <= m && st == kOk; ++k)
-        st = step_rt(cmin(k, ORD), cmin(k, 4), th, h, tol, max_iter, gamma, iters);
+        st = step_rt(cmin(k, ORD), cmin(k, 4), th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma,
+                     iters);
       if (true) {
 #pragma unroll
         for (int j = 0; j < D; ++j) x[j] = xs[0][j];
@@ -505,13 +510,13 @@ struct Propagator {
     }
     for (int k = 1; k <= m && st == kOk; ++k) {
       if (k == 1)
-        st = step<1, 1>(th, h, tol, max_iter, gamma, iters);
+        st = step<1, 1>(th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma, iters);
       else if (k == 2)
-        st = step<cmin(2, ORD), 2>(th, h, tol, max_iter, gamma, iters);
+        st = step<cmin(2, ORD), 2>(th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma, iters);
       else if (k == 3)
-        st = step<cmin(3, ORD), 3>(th, h, tol, max_iter, gamma, iters);
+        st = step<cmin(3, ORD), 3>(th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma, iters);
       else
-        st = step<ORD, 4>(th, h, tol, max_iter, gamma, iters);
+        st = step<ORD, 4>(th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma, iters);
     }
 #pragma unroll
     for (int j = 0; j < D; ++j) x[j] = xs[0][j];

@@ -1448,6 +1448,8 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     s->cfg = *cfg;
     s->ks = make_kernels(cfg->model, cfg->family, cfg->order);
     if (!s->ks) throw ConfigError("unknown model id");
+    if (cfg->model == MetabolicModel::ID && !(cfg->model_consts[5] > 0.0))
+      throw ConfigError("metabolic model: tau must be positive");  // MetabolicModel ctor, models.cpp:104-108
     s->d = s->ks->d;
     s->p = s->ks->p;
     std::vector<bool> seen(s->d, false);
@@ -1482,6 +1484,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.max_iter = cfg->newton_max_iter;
     c.seed = cfg->seed;
     c.two_s2 = 2.0 * (cfg->sigma * cfg->sigma);
+    for (int k = 0; k < 8; ++k) c.mconst[k] = cfg->model_consts[k];
     // guide buckets: about one per CDF segment (of the whole filter), <= 2^22
     const long long nseg_glob = std::max<long long>(1, static_cast<long long>(cfg->particles) >> kSegLog2);
     int cb = 6;

@@ -27,8 +27,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpfsmc_gpu.so")
 
-MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4}
-MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 4: (6, 2)}
+MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4, "metabolic": 5}
+MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 4: (6, 2), 5: (3, 4)}
+# models::MetabolicConstants defaults (models.hpp:67-74): lambda, c0, A0, A, t0_input, tau
+METABOLIC_DEFAULTS = (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
 FAMILIES = {"ab": 0, "am": 1, "bdf": 2}
 LIKELIHOODS = {"gaussian": 0, "lognormal": 1}
 
@@ -57,7 +59,15 @@ class _Config(C.Structure):
                 ("shrink_a", C.c_double), ("seed", C.c_uint64), ("newton_tol", C.c_double),
                 ("newton_max_iter", C.c_int), ("particles", C.c_uint64),
                 ("obs_indices", _u64p), ("n_obs", C.c_uint64), ("sigma", C.c_double),
-                ("likelihood", C.c_int), ("device", C.c_int)]
+                ("likelihood", C.c_int), ("device", C.c_int), ("model_consts", C.c_double * 8)]
+
+
+def model_consts_array(model: str, consts=None):
+    """The C ABI's model_consts[8] (METABOLIC: MetabolicConstants order)."""
+    if consts is None:
+        consts = METABOLIC_DEFAULTS if model == "metabolic" else ()
+    v = list(map(float, consts)) + [0.0] * (8 - len(consts))
+    return (C.c_double * 8)(*v[:8])
 
 
 _lib = None
@@ -153,7 +163,8 @@ class TraceRow:
 class GpuSampler:
     """One device-resident ensemble on one B200 behind the C ABI."""
 
-    def __init__(self, model: str, cfg: PfConfig, obs: ObservationModel, device: int = 0):
+    def __init__(self, model: str, cfg: PfConfig, obs: ObservationModel, device: int = 0,
+                 model_consts=None):
         self.lib = load_library()
         self.model = model
         self.cfg = cfg
@@ -163,7 +174,7 @@ class GpuSampler:
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed,
                     cfg.newton_tol, cfg.newton_max_iter, cfg.particles,
                     _ptr(self._idx, _u64p), len(self._idx), obs.sigma,
-                    LIKELIHOODS[obs.likelihood], device)
+                    LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts))
         h = C.c_void_p()
         self._check(self.lib.pfsmc_gpu_create(C.byref(c), C.byref(h)))
         self.h = h

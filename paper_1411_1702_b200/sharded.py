@@ -51,8 +51,8 @@ class GpuShard(GpuSampler):
     """One shard of the global filter on one GPU (pfsmc_gpu_create_shard)."""
 
     def __init__(self, model: str, cfg: PfConfig, obs: ObservationModel, rank: int, world: int,
-                 device: int = 0):
-        from .sampler import FAMILIES, LIKELIHOODS, _Config, load_library
+                 device: int = 0, model_consts=None):
+        from .sampler import FAMILIES, LIKELIHOODS, _Config, load_library, model_consts_array
         self.lib = load_library()
         self.model, self.cfg, self.obs = model, cfg, obs
         self.d, self.p = MODEL_DIMS[MODELS[model]]
@@ -60,7 +60,7 @@ class GpuShard(GpuSampler):
         self._idx = np.ascontiguousarray(list(obs.indices), dtype=np.uint64)
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed, cfg.newton_tol,
                     cfg.newton_max_iter, cfg.particles, _ptr(self._idx, C.POINTER(C.c_uint64)), len(self._idx),
-                    obs.sigma, LIKELIHOODS[obs.likelihood], device)
+                    obs.sigma, LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts))
         L = self.lib
         for name in ("pfsmc_gpu_create_shard", "pfsmc_gpu_shard_buffer", "pfsmc_gpu_shard_predict",
                      "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_records",

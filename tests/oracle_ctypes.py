@@ -20,8 +20,10 @@ ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libpfsmc_ref.so")
 
 FAMILIES = {"ab": 0, "am": 1, "bdf": 2}
-MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3}
-DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4)}
+MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "metabolic": 5}
+DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 5: (3, 4)}
+# models::MetabolicConstants defaults (models.hpp:67-74): lambda, c0, A0, A, t0_input, tau
+METABOLIC_DEFAULTS = (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
 LIKELIHOODS = {"gaussian": 0, "lognormal": 1}
 
 _dp = C.POINTER(C.c_double)
@@ -155,6 +157,11 @@ class Oracle(_Base):
         self.lib.or_philox4x64(_ptr(c, _u64p), _ptr(k, _u64p), _ptr(o, _u64p))
         return o
 
+    def set_model_consts(self, k=METABOLIC_DEFAULTS):
+        v = np.zeros(8)
+        v[:len(k)] = k
+        self.lib.or_set_model_consts(_ptr(v))
+
     def draws(self, seed, j, n, purpose, kind, count):
         out = np.zeros(count, dtype=np.uint64 if kind == 0 else np.float64)
         self._check(self.lib.or_stream_draws(C.c_uint64(seed), C.c_uint64(j), C.c_uint64(n),
@@ -268,6 +275,11 @@ class Reference(_Base):
         o = np.zeros(4, dtype=np.uint64)
         self._check(self.lib.ref_philox(_ptr(c, _u64p), _ptr(k, _u64p), _ptr(o, _u64p)))
         return o
+
+    def set_model_consts(self, k=METABOLIC_DEFAULTS):
+        v = np.zeros(8)
+        v[:len(k)] = k
+        self.lib.ref_set_model_consts(_ptr(v))
 
     def draws(self, seed, j, n, purpose, kind, count):
         out = np.zeros(count, dtype=np.uint64 if kind == 0 else np.float64)

@@ -27,11 +27,12 @@ REL_STATE = 1e-10
 REL_TRACE = 1e-8
 
 
-def _sampler(sc: StepConfig, n, likelihood="gaussian"):
+def _sampler(sc: StepConfig, n, likelihood="gaussian", model_consts=None):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     cfg = PfConfig(particles=n, shrink_a=sc.a, h=sc.h, family=sc.family, order=sc.order, seed=sc.seed,
                    newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter)
-    return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood))
+    return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood),
+                      model_consts=model_consts)
 
 
 def _to_gpu_ens(e):
@@ -288,6 +289,44 @@ def test_lockstep_chain_bdf3(th0):
         _compare_step(gpu, ens, trace_o, dg, row)
         tp += 0.1
     gpu.close()
+
+
+@pytest.mark.parametrize("family,order,consts", [("bdf", 2, None), ("am", 3, None),
+                                                 ("bdf", 3, (0.7, 0.5, 1.2, 3.0, 1.9, 0.6))])
+def test_lockstep_metabolic(family, order, consts):
+    """The reference's own problem-1 model (models.cpp:37-119): time-dependent
+    input flux, constants bound at creation, Gaussian prior with clamped x0;
+    intervals straddle the input switch-on at t0_input, m = 4 sub-steps."""
+    n = 6000
+    k = consts or (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
+    O.set_model_consts(k)
+    try:
+        sc = StepConfig(model="metabolic", family=family, order=order, h=0.05, a=0.98, seed=12,
+                        obs_idx=(0, 1, 2), sigma=0.1)
+        mu = np.log([1.5, 0.7, 1.5, 0.5])
+        ens = O.init_gaussian("metabolic", n, 12, mu, [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+        gpu = _sampler(sc, n, model_consts=k)
+        rng = np.random.default_rng(8)
+        tp = 1.6
+        for j in range(1, 6):
+            y = np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3)
+            gpu.set_ensemble(_to_gpu_ens(ens))
+            row = gpu.pf_step(y, j, tp, tp + 0.2)
+            trace_o, dg = O.pf_step(sc, ens, y, j, tp, tp + 0.2, diag=True)
+            _compare_step(gpu, ens, trace_o, dg, row)
+            tp += 0.2
+        gpu.close()
+    finally:
+        O.set_model_consts((1.0, 1.0, 1.0, 5.0, 2.0, 1.0))
+
+
+def test_metabolic_config_error():
+    """tau <= 0 is a ConfigError at model construction (models.cpp:104-108)."""
+    from paper_1411_1702_b200.sampler import NumericalError
+    sc = StepConfig(model="metabolic", family="bdf", order=2, h=0.05, obs_idx=(0, 1, 2), sigma=0.1)
+    with pytest.raises(Exception) as e:
+        _sampler(sc, 64, model_consts=(1.0, 1.0, 1.0, 5.0, 2.0, 0.0))
+    assert "tau" in str(e.value) and not isinstance(e.value, NumericalError)
 
 
 def test_lockstep_robertson_lognormal():

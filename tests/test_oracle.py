@@ -184,6 +184,39 @@ def test_oracle_matches_live_reference(family, order, h):
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("family,order,consts", [("bdf", 2, None), ("am", 3, None), ("ab", 2, None),
+                                                 ("bdf", 3, (0.7, 0.5, 1.2, 3.0, 1.9, 0.6))])
+def test_oracle_matches_live_reference_metabolic(family, order, consts):
+    """The reference's own MetabolicModel (time-dependent input flux) through
+    the reference's initialize (Gaussian prior, clamped x0) and pf_step; the
+    steps straddle the input switch-on at t0_input so both branches of
+    input_phi (models.cpp:37-42) run, with m = 4 sub-steps per interval."""
+    R = Reference()
+    k = consts or (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
+    O.set_model_consts(k)
+    R.set_model_consts(k)
+    try:
+        sc = StepConfig(model="metabolic", family=family, order=order, h=0.05, seed=5, obs_idx=(0, 1, 2),
+                        sigma=0.1)
+        mu = np.log([1.5, 0.7, 1.5, 0.5])
+        e = O.init_gaussian("metabolic", 400, 5, mu, [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+        e2 = R.init_gaussian(sc, 400, mu, [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+        assert np.array_equal(e.states, e2.states) and np.array_equal(e.params_u, e2.params_u)
+        rng = np.random.default_rng(3)
+        tp = 1.6
+        for j in range(1, 6):
+            y = np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3)
+            t1, _ = O.pf_step(sc, e, y, j, tp, tp + 0.2)
+            t2 = R.pf_step(sc, e2, y, j, tp, tp + 0.2)
+            tp += 0.2
+            assert np.array_equal(t1, t2), j
+            assert np.array_equal(e.states, e2.states) and np.array_equal(e.logw, e2.logw)
+    finally:
+        O.set_model_consts((1.0, 1.0, 1.0, 5.0, 2.0, 1.0))
+        R.set_model_consts((1.0, 1.0, 1.0, 5.0, 2.0, 1.0))
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built (needs /root/reference)")
 def test_degeneracy_error_parity():
     """Both raise NUMERICAL at the same step (total degeneracy)."""
     R = Reference()
