@@ -56,6 +56,10 @@ CASES = {
                                sigma=0.02, newton_max_iter=4), 48, "gauss_rob", None),
     "decay_bdf1": (dict(model="decay", family="bdf", order=1, h=0.5, a=0.95, seed=31415, obs_idx=(0,), sigma=0.5),
                    3, "gauss_decay", [(0.0, 0.5, 0.5)]),
+    # the reference's own MetabolicModel (default MetabolicConstants), across the input switch-on
+    "metabolic_bdf2_m4": (dict(model="metabolic", family="bdf", order=2, h=0.05, a=0.98, seed=21,
+                               obs_idx=(0, 1, 2), sigma=0.1), 80, "gauss_metabolic",
+                          [(1.6 + 0.2 * k, 1.6 + 0.2 * (k + 1), 0.05) for k in range(5)]),
 }
 
 
@@ -67,6 +71,8 @@ def init_ens(kind, n, seed, O, R, sc):
         return O.init_uniform("chain", n, seed, 0.5 * th, 2 * th, [0] * 8, [0] * 8)
     if kind == "gauss_rob":
         return R.init_gaussian(sc, n, np.log([0.04, 3e7, 1e4]) + 0.5, [1, 1, 1], [1, 0, 0], [0, 0, 0], [0, 0, 0])
+    if kind == "gauss_metabolic":  # bench.cpp:214-237 defaults
+        return R.init_gaussian(sc, n, np.log([1.5, 0.7, 1.5, 0.5]), [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
     if kind == "gauss_decay":
         return R.init_gaussian(sc, n, [np.log(0.8)], [0.4], [2.0], [0.1], [0])
     raise KeyError(kind)
@@ -93,6 +99,8 @@ def pf_cases():
                 y = np.array([1.2, 0.9]) + 0.05 * rng.standard_normal(2)
             elif kw["model"] == "chain":
                 y = np.array([0.09 * j, 0.001 * j, 0.0]) + 0.01 * rng.standard_normal(3)
+            elif kw["model"] == "metabolic":
+                y = np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3)
             elif kw["model"] == "robertson":
                 y = np.array([1 - 0.04 * t1, 0.04 * t1 * 1e-3]) + 1e-3 * rng.standard_normal(2)
             else:
