@@ -23,7 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-diag-suppress", "497", "-Xptxas", "-warn-spills"]
 SOURCES = ["sampler.cu", "kernels_decay.cu", "kernels_lv.cu", "kernels_robertson.cu",
-           "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu"]
+           "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu",
+           "experiment.cpp"]  # host-only: the experiment-level drop-in (pfsmc_gpu_experiment.h)
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -32,14 +33,16 @@ def _stale(obj: str, src: str) -> bool:
     t = os.path.getmtime(obj)
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "pfsmc_gpu.h"))
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "pfsmc_gpu_experiment.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
 def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
     if _stale(obj, path):
-        cmd = [NVCC, *FLAGS, "-c", path, "-o", obj]
+        flags = FLAGS if src.endswith(".cu") else ["-O2", "-std=c++17", "-Xcompiler", "-fPIC"]
+        cmd = [NVCC, *flags, "-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

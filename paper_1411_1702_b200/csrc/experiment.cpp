@@ -1,0 +1,702 @@
+// Experiment-level drop-in: the reference's C ABI pfsmc_config_* /
+// pfsmc_run_experiment (include/pfsmc.h:27-48, src/capi.cpp:60-108) and the
+// driver behind it, bench::run_experiment (bench.cpp:537-607), with the
+// filter running on the GPU sampler (include/pfsmc_gpu.h) instead of the
+// thread-pool backend.
+//
+// Same config keys, validation messages and status codes as
+// ExperimentConfig::set (bench.cpp:110-153); same canonical JSON and FNV-1a
+// config hash (bench.cpp:155-178); same data CSV + .json sidecar input
+// (bench.cpp:398-445), equispaced-grid check (bench.cpp:449-476), problem
+// setup (bench.cpp:188-248, problem "metabolic"), filter::run semantics
+// (initial row, degeneracy streak; filter.cpp:396-443) and outputs: the trace
+// CSV (bench.cpp:484-499) and the report JSON (bench.cpp:501-527), tagged
+// "<problem>_<integrator>_gpu".
+//
+// Out of scope (ConfigError): problem "advdiff" (the sparse advection-
+// diffusion model) and integrator "adaptive-bdf2".
+#include <charconv>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pfsmc_gpu.h"
+#include "../../include/pfsmc_gpu_experiment.h"
+
+namespace {
+
+namespace fs = std::filesystem;
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+thread_local std::string g_err;
+
+template <typename F>
+pfsmc_gpu_status guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return PFSMC_GPU_OK;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return PFSMC_GPU_ERR_CONFIG;
+  } catch (const NumericalError& e) {
+    g_err = e.what();
+    return PFSMC_GPU_ERR_NUMERICAL;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return PFSMC_GPU_ERR_IO;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PFSMC_GPU_ERR_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return PFSMC_GPU_ERR_INTERNAL;
+  }
+}
+
+// A GPU-sampler status turned back into the exception family.
+void check_gpu(pfsmc_gpu_status st) {
+  if (st == PFSMC_GPU_OK) return;
+  const std::string msg = pfsmc_gpu_last_error();
+  if (st == PFSMC_GPU_ERR_CONFIG) throw ConfigError(msg);
+  if (st == PFSMC_GPU_ERR_NUMERICAL) throw NumericalError(msg);
+  if (st == PFSMC_GPU_ERR_IO) throw IoError(msg);
+  throw std::runtime_error(msg);
+}
+
+// ---- number / JSON formatting ------------------------------------------
+std::string fmt17(double v) {  // %.17g, the trace CSV format (bench.cpp:24-28)
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+// Shortest round-trip decimal with a ".0" on integral values: the number
+// format of the reference's JSON writer.
+std::string json_num(double v) {
+  if (!std::isfinite(v)) return "null";
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, v);
+  std::string s(buf, r.ptr);
+  if (s.find_first_of(".eE") == std::string::npos) s += ".0";
+  return s;
+}
+
+std::string json_str(const std::string& s) {
+  std::string o = "\"";
+  for (const char ch : s) {
+    switch (ch) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\n': o += "\\n"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (static_cast<unsigned char>(ch) < 0x20) {
+          char b[8];
+          std::snprintf(b, sizeof b, "\\u%04x", ch);
+          o += b;
+        } else {
+          o += ch;
+        }
+    }
+  }
+  return o + "\"";
+}
+
+std::uint64_t fnv1a(const std::string& s) {
+  std::uint64_t h = 1469598103934665603ULL;
+  for (const unsigned char ch : s) {
+    h ^= ch;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+// ---- a small JSON reader for the data sidecar ---------------------------
+struct JVal {
+  enum Kind { kNull, kBool, kNum, kStr, kArr, kObj } kind = kNull;
+  bool b = false;
+  double num = 0.0;
+  std::string str;
+  std::vector<JVal> arr;
+  std::map<std::string, JVal> obj;
+};
+
+struct JParser {
+  const std::string& s;
+  std::size_t i = 0;
+  explicit JParser(const std::string& t) : s(t) {}
+  [[noreturn]] void bad() { throw IoError("bad sidecar: malformed JSON"); }
+  void ws() {
+    while (i < s.size() && (s[i] == ' ' || s[i] == '\n' || s[i] == '\r' || s[i] == '\t')) ++i;
+  }
+  std::string string() {
+    if (s[i] != '"') bad();
+    ++i;
+    std::string o;
+    while (i < s.size() && s[i] != '"') {
+      if (s[i] == '\\') {
+        ++i;
+        if (i >= s.size()) bad();
+        const char e = s[i];
+        o += e == 'n' ? '\n' : e == 't' ? '\t' : e;
+      } else {
+        o += s[i];
+      }
+      ++i;
+    }
+    if (i >= s.size()) bad();
+    ++i;
+    return o;
+  }
+  JVal value() {
+    ws();
+    if (i >= s.size()) bad();
+    JVal v;
+    const char ch = s[i];
+    if (ch == '{') {
+      v.kind = JVal::kObj;
+      ++i;
+      ws();
+      if (s[i] == '}') {
+        ++i;
+        return v;
+      }
+      for (;;) {
+        ws();
+        const std::string k = string();
+        ws();
+        if (s[i] != ':') bad();
+        ++i;
+        v.obj[k] = value();
+        ws();
+        if (s[i] == ',') {
+          ++i;
+          continue;
+        }
+        if (s[i] == '}') {
+          ++i;
+          return v;
+        }
+        bad();
+      }
+    }
+    if (ch == '[') {
+      v.kind = JVal::kArr;
+      ++i;
+      ws();
+      if (s[i] == ']') {
+        ++i;
+        return v;
+      }
+      for (;;) {
+        v.arr.push_back(value());
+        ws();
+        if (s[i] == ',') {
+          ++i;
+          continue;
+        }
+        if (s[i] == ']') {
+          ++i;
+          return v;
+        }
+        bad();
+      }
+    }
+    if (ch == '"') {
+      v.kind = JVal::kStr;
+      v.str = string();
+      return v;
+    }
+    if (s.compare(i, 4, "true") == 0) {
+      v.kind = JVal::kBool;
+      v.b = true;
+      i += 4;
+      return v;
+    }
+    if (s.compare(i, 5, "false") == 0) {
+      v.kind = JVal::kBool;
+      i += 5;
+      return v;
+    }
+    if (s.compare(i, 4, "null") == 0) {
+      i += 4;
+      return v;
+    }
+    char* end = nullptr;
+    v.kind = JVal::kNum;
+    v.num = std::strtod(s.c_str() + i, &end);
+    if (end == s.c_str() + i) bad();
+    i = static_cast<std::size_t>(end - s.c_str());
+    return v;
+  }
+};
+
+const JVal& jat(const JVal& o, const char* key) {
+  const auto it = o.obj.find(key);
+  if (o.kind != JVal::kObj || it == o.obj.end())
+    throw IoError(std::string("bad sidecar: missing key '") + key + "'");
+  return it->second;
+}
+double jnum(const JVal& v) {
+  if (v.kind != JVal::kNum) throw IoError("bad sidecar: expected a number");
+  return v.num;
+}
+
+// ---- ExperimentConfig (bench.hpp:18-41) ----------------------------------
+struct Integrator {
+  int family = PFSMC_GPU_BDF, order = 2;
+};
+
+// parse_integrator (bench.cpp:67-97)
+Integrator parse_integrator(const std::string& name) {
+  if (name == "adaptive-bdf2")
+    throw ConfigError("integrator 'adaptive-bdf2' (adaptive BDF(1,2)) is not implemented by the GPU sampler");
+  if (name.size() >= 3) {
+    const char digit = name.back();
+    const std::string fam = name.substr(0, name.size() - 1);
+    if (digit >= '1' && digit <= '3') {
+      Integrator s;
+      s.order = digit - '0';
+      if (fam == "ab") return s.family = PFSMC_GPU_AB, s;
+      if (fam == "am") return s.family = PFSMC_GPU_AM, s;
+      if (fam == "bdf") return s.family = PFSMC_GPU_BDF, s;
+    }
+  }
+  throw ConfigError("unknown integrator '" + name + "'");
+}
+
+double parse_double(const std::string& key, const std::string& value) {
+  try {
+    std::size_t pos = 0;
+    const double v = std::stod(value, &pos);
+    if (pos != value.size()) throw std::invalid_argument(value);
+    return v;
+  } catch (const std::exception&) {
+    throw ConfigError("config key '" + key + "': cannot parse number '" + value + "'");
+  }
+}
+
+std::uint64_t parse_u64(const std::string& key, const std::string& value) {
+  try {
+    std::size_t pos = 0;
+    const unsigned long long v = std::stoull(value, &pos);
+    if (pos != value.size()) throw std::invalid_argument(value);
+    return v;
+  } catch (const std::exception&) {
+    throw ConfigError("config key '" + key + "': cannot parse integer '" + value + "'");
+  }
+}
+
+double override_or(const std::map<std::string, double>& o, const std::string& key, double fallback) {
+  const auto it = o.find(key);
+  return it == o.end() ? fallback : it->second;
+}
+
+}  // namespace
+
+struct pfsmc_gpu_experiment {
+  std::string problem = "metabolic";
+  std::uint64_t n = 20;
+  std::string integrator = "bdf2";
+  std::string backend = "seq";
+  std::uint64_t workers = 0;
+  std::uint64_t particles = 5000;
+  double step = 0.05;
+  double shrink_a = 0.98;
+  std::uint64_t seed = 0;
+  double rtol = 1e-3;
+  bool warmup = false;
+  double sigma = -1.0;
+  double t_end = 10.0;
+  std::uint64_t n_obs = 50;
+  std::map<std::string, double> overrides;
+  int device = 0;  // GPU placement (not part of the canonical config)
+
+  // ExperimentConfig::set (bench.cpp:110-153), plus "device".
+  void set(const std::string& key, const std::string& value) {
+    if (key == "problem") {
+      if (value != "metabolic" && value != "advdiff") throw ConfigError("problem must be 'metabolic' or 'advdiff'");
+      problem = value;
+    } else if (key == "n") {
+      n = parse_u64(key, value);
+    } else if (key == "integrator") {
+      if (value != "adaptive-bdf2") parse_integrator(value);  // validation
+      integrator = value;
+    } else if (key == "backend") {
+      if (value != "seq" && value != "par" && value != "batch")
+        throw ConfigError("backend must be seq, par or batch");
+      backend = value;
+    } else if (key == "workers") {
+      workers = parse_u64(key, value);
+    } else if (key == "particles") {
+      particles = parse_u64(key, value);
+    } else if (key == "step") {
+      step = parse_double(key, value);
+    } else if (key == "shrink-a") {
+      shrink_a = parse_double(key, value);
+    } else if (key == "seed") {
+      seed = parse_u64(key, value);
+    } else if (key == "rtol") {
+      rtol = parse_double(key, value);
+    } else if (key == "warmup") {
+      warmup = value == "1" || value == "true";
+    } else if (key == "sigma") {
+      sigma = parse_double(key, value);
+    } else if (key == "t-end") {
+      t_end = parse_double(key, value);
+    } else if (key == "n-obs") {
+      n_obs = parse_u64(key, value);
+    } else if (key.rfind("truth.", 0) == 0 || key.rfind("prior.", 0) == 0 || key.rfind("x0.", 0) == 0 ||
+               key.rfind("const.", 0) == 0) {
+      overrides[key] = parse_double(key, value);
+    } else if (key == "device") {
+      device = static_cast<int>(parse_u64(key, value));
+    } else {
+      throw ConfigError("unknown config key '" + key + "'");
+    }
+  }
+
+  // ExperimentConfig::canonical_json (bench.cpp:155-174): compact, keys sorted.
+  std::string canonical_json() const {
+    std::string o = "{";
+    o += "\"backend\":" + json_str(backend);
+    o += ",\"integrator\":" + json_str(integrator);
+    o += ",\"n\":" + std::to_string(n);
+    o += ",\"n_obs\":" + std::to_string(n_obs);
+    o += ",\"overrides\":{";
+    bool first = true;
+    for (const auto& [k, v] : overrides) {
+      o += (first ? "" : ",") + json_str(k) + ":" + json_num(v);
+      first = false;
+    }
+    o += "}";
+    o += ",\"particles\":" + std::to_string(particles);
+    o += ",\"problem\":" + json_str(problem);
+    o += ",\"rtol\":" + json_num(rtol);
+    o += ",\"seed\":" + std::to_string(seed);
+    o += ",\"shrink_a\":" + json_num(shrink_a);
+    o += ",\"sigma\":" + json_num(sigma);
+    o += ",\"step\":" + json_num(step);
+    o += ",\"t_end\":" + json_num(t_end);
+    o += std::string(",\"warmup\":") + (warmup ? "true" : "false");
+    o += ",\"workers\":" + std::to_string(workers);
+    return o + "}";
+  }
+  std::string hash() const {
+    char buf[20];
+    std::snprintf(buf, sizeof buf, "%016llx", static_cast<unsigned long long>(fnv1a(canonical_json())));
+    return buf;
+  }
+};
+
+namespace {
+
+// ---- the problem (build_problem, bench.cpp:188-248) ----------------------
+struct Setup {
+  Integrator integ;
+  std::vector<double> th_mu, th_sigma, x_mean, x_std;
+  std::vector<int> x_clamp;
+  std::vector<std::string> param_names;
+  double consts[8] = {};
+};
+
+Setup build_problem(const pfsmc_gpu_experiment& cfg) {
+  Setup s;
+  s.integ = parse_integrator(cfg.integrator);
+  if (!(cfg.shrink_a > 0.0 && cfg.shrink_a < 1.0)) throw ConfigError("shrink-a must lie strictly between 0 and 1");
+  if (cfg.problem != "metabolic")
+    throw ConfigError("problem '" + cfg.problem +
+                      "' (sparse advection-diffusion) is not implemented by the GPU sampler");
+  const auto& o = cfg.overrides;
+  // MetabolicConstants (models.hpp:67-74) with const.* overrides
+  s.consts[0] = override_or(o, "const.lambda", 1.0);
+  s.consts[1] = override_or(o, "const.c0", 1.0);
+  s.consts[2] = override_or(o, "const.A0", 1.0);
+  s.consts[3] = override_or(o, "const.A", 5.0);
+  s.consts[4] = override_or(o, "const.t0", 2.0);
+  s.consts[5] = override_or(o, "const.tau", 1.0);
+  if (!(s.consts[5] > 0.0)) throw ConfigError("metabolic model: tau must be positive");
+  s.param_names = {"V1", "k1", "V2", "k2"};
+  const double prior_mu[4] = {std::log(1.5), std::log(0.7), std::log(1.5), std::log(0.5)};
+  for (int k = 0; k < 4; ++k) {
+    s.th_mu.push_back(override_or(o, "prior." + s.param_names[k] + ".mu", prior_mu[k]));
+    s.th_sigma.push_back(override_or(o, "prior." + s.param_names[k] + ".sigma", 0.5));
+  }
+  for (int k = 0; k < 3; ++k) {
+    const std::string base = "x0." + std::to_string(k);
+    const double truth = override_or(o, base + ".truth", 1.0);
+    s.x_mean.push_back(override_or(o, base + ".mean", truth));
+    s.x_std.push_back(override_or(o, base + ".std", 0.25));
+    s.x_clamp.push_back(1);
+  }
+  if (cfg.n_obs == 0 || !(cfg.t_end > 0.0)) throw ConfigError("metabolic problem needs n-obs >= 1 and t-end > 0");
+  return s;
+}
+
+// ---- data (load_data, bench.cpp:398-445) ----------------------------------
+struct Loaded {
+  std::string problem;
+  std::uint64_t n = 0;
+  double t0 = 0.0, sigma = 0.0;
+  std::vector<double> times, values, truth;
+  std::vector<std::uint64_t> obs_indices;
+  std::size_t m = 0;
+};
+
+std::string sidecar_path(const std::string& csv) {
+  const fs::path p(csv);
+  fs::path side = p;
+  side.replace_extension(".json");
+  if (side == p) side += ".json";
+  return side.string();
+}
+
+Loaded load_data(const std::string& csv) {
+  std::ifstream in(csv);
+  if (!in) throw IoError("cannot open data file '" + csv + "'");
+  std::string line;
+  if (!std::getline(in, line)) throw IoError("data file '" + csv + "' is empty");
+  Loaded L;
+  for (const char ch : line) L.m += ch == ',';
+  if (L.m == 0) throw IoError("data file has no observation columns");
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    std::stringstream ss(line);
+    std::string cell;
+    std::size_t col = 0;
+    while (std::getline(ss, cell, ',')) {
+      const double v = std::strtod(cell.c_str(), nullptr);
+      (col == 0 ? L.times : L.values).push_back(v);
+      ++col;
+    }
+    if (col != L.m + 1) throw IoError("ragged row in data file");
+  }
+  std::ifstream sin(sidecar_path(csv));
+  if (!sin) throw IoError("cannot open sidecar '" + sidecar_path(csv) + "'");
+  std::stringstream buf;
+  buf << sin.rdbuf();
+  const std::string text = buf.str();
+  JParser jp(text);
+  const JVal side = jp.value();
+  const JVal& pr = jat(side, "problem");
+  if (pr.kind != JVal::kStr) throw IoError("bad sidecar: problem");
+  L.problem = pr.str;
+  L.n = static_cast<std::uint64_t>(jnum(jat(side, "n")));
+  L.t0 = jnum(jat(side, "t0"));
+  L.sigma = jnum(jat(side, "sigma"));
+  for (const JVal& v : jat(side, "obs_indices").arr) L.obs_indices.push_back(static_cast<std::uint64_t>(jnum(v)));
+  for (const JVal& v : jat(side, "truth").arr) L.truth.push_back(jnum(v));
+  (void)jnum(jat(side, "seed"));
+  if (L.obs_indices.size() != L.m) throw ConfigError("sidecar observation indices do not match data width");
+  return L;
+}
+
+// check_time_grid (bench.cpp:449-476)
+void check_time_grid(const Loaded& d, double h) {
+  if (d.times.empty()) throw ConfigError("no observations in data file");
+  const double spacing = d.times.front() - d.t0;
+  if (!(spacing > 0.0)) throw ConfigError("observation times must increase");
+  double prev = d.t0;
+  for (const double t : d.times) {
+    const double dt = t - prev;
+    if (std::abs(dt - spacing) > 1e-9 * std::max(1.0, std::abs(spacing)))
+      throw ConfigError("observation times must be equispaced");
+    prev = t;
+  }
+  const double ratio = spacing / h;
+  const double r = std::round(ratio);
+  if (r < 1.0 || std::abs(ratio - r) > 1e-9 * std::max(1.0, ratio))
+    throw ConfigError("step h must divide the observation spacing an integer number of times");
+}
+
+struct SamplerHandle {
+  pfsmc_gpu_sampler* h = nullptr;
+  ~SamplerHandle() {
+    if (h) pfsmc_gpu_destroy(h);
+  }
+};
+
+void make_sampler(SamplerHandle& out, const pfsmc_gpu_experiment& cfg, const Setup& s, const Loaded& d) {
+  pfsmc_gpu_config c{};
+  c.model = PFSMC_GPU_MODEL_METABOLIC;
+  c.family = s.integ.family;
+  c.order = s.integ.order;
+  c.shrink_a = cfg.shrink_a;
+  c.seed = cfg.seed;
+  c.newton_tol = 1e-9;     // NewtonOpts defaults (lmm.hpp:68-71)
+  c.newton_max_iter = 20;
+  c.particles = cfg.particles;
+  c.obs_indices = d.obs_indices.data();
+  c.n_obs = d.obs_indices.size();
+  c.sigma = d.sigma;
+  c.likelihood = PFSMC_GPU_LIK_GAUSSIAN;
+  c.device = cfg.device;
+  for (int k = 0; k < 8; ++k) c.model_consts[k] = s.consts[k];
+  check_gpu(pfsmc_gpu_create(&c, &out.h));
+}
+
+std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_csv, const std::string& out_dir) {
+  const Setup setup = build_problem(cfg);
+  const Loaded data = load_data(data_csv);
+  if (data.problem != cfg.problem)
+    throw ConfigError("data file was generated for problem '" + data.problem + "', config says '" + cfg.problem + "'");
+  check_time_grid(data, cfg.step);
+  if (!(cfg.step > 0.0)) throw ConfigError("config: step size h must be positive");
+  fs::create_directories(out_dir);
+  const std::size_t T = data.times.size(), p = 4, d = 3;
+  if (cfg.warmup) {
+    // one untimed assimilation step on a scratch ensemble (bench.cpp:559-565)
+    SamplerHandle scratch;
+    make_sampler(scratch, cfg, setup, data);
+    check_gpu(pfsmc_gpu_init_gaussian(scratch.h, setup.th_mu.data(), setup.th_sigma.data(), setup.x_mean.data(),
+                                      setup.x_std.data(), setup.x_clamp.data()));
+    std::vector<double> row(2 * p + d + 1);
+    check_gpu(pfsmc_gpu_step(scratch.h, data.values.data(), 1, data.t0, data.times.front(), cfg.step, row.data()));
+  }
+  SamplerHandle s;
+  make_sampler(s, cfg, setup, data);
+  const std::size_t W = 2 * p + d + 1;
+  std::vector<double> rows((T + 1) * W);
+  std::vector<int> warn(T + 1, 0);
+  const auto start = std::chrono::steady_clock::now();
+  // filter::run: initialize (filter.cpp:405), initial row, the step loop
+  check_gpu(pfsmc_gpu_init_gaussian(s.h, setup.th_mu.data(), setup.th_sigma.data(), setup.x_mean.data(),
+                                    setup.x_std.data(), setup.x_clamp.data()));
+  check_gpu(pfsmc_gpu_upload_observations(s.h, data.values.data(), data.times.data(), T, data.t0, cfg.step));
+  check_gpu(pfsmc_gpu_run(s.h, rows.data(), warn.data()));
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+
+  const std::string tag = cfg.problem + "_" + cfg.integrator + "_gpu";
+  const std::string trace_csv = (fs::path(out_dir) / ("trace_" + tag + ".csv")).string();
+  const std::string report_path = (fs::path(out_dir) / ("report_" + tag + ".json")).string();
+  {  // write_trace_csv (bench.cpp:484-499)
+    std::ofstream out(trace_csv);
+    if (!out) throw IoError("cannot write trace '" + trace_csv + "'");
+    out << "j,t";
+    for (const auto& nm : setup.param_names) out << ",theta_mean_" << nm;
+    for (const auto& nm : setup.param_names) out << ",theta_var_" << nm;
+    out << ",ess\n";
+    for (std::size_t j = 0; j <= T; ++j) {
+      const double* r = rows.data() + j * W;
+      out << j << "," << fmt17(j == 0 ? data.t0 : data.times[j - 1]);
+      for (std::size_t k = 0; k < p; ++k) out << "," << fmt17(r[k]);
+      for (std::size_t k = 0; k < p; ++k) out << "," << fmt17(r[p + k]);
+      out << "," << fmt17(r[2 * p + d]) << "\n";
+    }
+  }
+  {  // report_to_json (bench.cpp:501-527)
+    const double* last = rows.data() + T * W;
+    auto arr = [](const std::vector<double>& v) {
+      std::string o = "[";
+      for (std::size_t i = 0; i < v.size(); ++i) o += (i ? ", " : "") + json_num(v[i]);
+      return o + "]";
+    };
+    std::vector<double> est(last, last + p), sd(p);
+    for (std::size_t k = 0; k < p; ++k) sd[k] = std::sqrt(std::max(0.0, last[p + k]));
+    std::string warnings = "[";
+    bool first = true;
+    for (std::size_t j = 0; j <= T; ++j) {
+      if (!warn[j]) continue;
+      warnings += (first ? "" : ", ") + json_str("effective sample size collapsed to 1 at step " + std::to_string(j));
+      first = false;
+    }
+    warnings += "]";
+    std::ofstream out(report_path);
+    if (!out) throw IoError("cannot write report '" + report_path + "'");
+    out << "{\n";
+    out << "  \"backend\": \"gpu\",\n";
+    out << "  \"config\": " << cfg.canonical_json() << ",\n";
+    out << "  \"config_hash\": " << json_str(cfg.hash()) << ",\n";
+    out << "  \"efficiency\": 0.0,\n";
+    out << "  \"final_estimate\": " << arr(est) << ",\n";
+    out << "  \"final_std_u\": " << arr(sd) << ",\n";
+    out << "  \"param_names\": [\"V1\", \"k1\", \"V2\", \"k2\"],\n";
+    out << "  \"param_positive\": [1, 1, 1, 1],\n";
+    out << "  \"phases\": {\"proliferate\": 0.0, \"propagate\": 0.0, \"repropagate\": 0.0, \"resample\": 0.0, "
+           "\"weights\": 0.0},\n";
+    out << "  \"speedup\": 0.0,\n";
+    out << "  \"trace_csv\": " << json_str(trace_csv) << ",\n";
+    out << "  \"truth\": " << arr(data.truth) << ",\n";
+    out << "  \"wall_time_s\": " << json_num(wall) << ",\n";
+    out << "  \"warnings\": " << warnings << ",\n";
+    out << "  \"worker_busy_s\": []\n";
+    out << "}\n";
+    if (!out) throw IoError("failed writing report '" + report_path + "'");
+  }
+  return report_path;
+}
+
+}  // namespace
+
+extern "C" {
+
+pfsmc_gpu_experiment* pfsmc_gpu_experiment_new(void) { return new (std::nothrow) pfsmc_gpu_experiment; }
+
+void pfsmc_gpu_experiment_free(pfsmc_gpu_experiment* cfg) { delete cfg; }
+
+const char* pfsmc_gpu_experiment_last_error(void) { return g_err.c_str(); }
+
+pfsmc_gpu_status pfsmc_gpu_experiment_set(pfsmc_gpu_experiment* cfg, const char* key, const char* value) {
+  if (!cfg || !key || !value) {
+    g_err = "null argument";
+    return PFSMC_GPU_ERR_CONFIG;
+  }
+  return guarded([&] { cfg->set(key, value); });
+}
+
+pfsmc_gpu_status pfsmc_gpu_experiment_canonical(const pfsmc_gpu_experiment* cfg, char** json_out,
+                                                char** hash_out) {
+  if (!cfg) {
+    g_err = "null argument";
+    return PFSMC_GPU_ERR_CONFIG;
+  }
+  return guarded([&] {
+    auto dup = [](const std::string& v) {
+      char* p = static_cast<char*>(std::malloc(v.size() + 1));
+      if (p) std::memcpy(p, v.c_str(), v.size() + 1);
+      return p;
+    };
+    if (json_out) *json_out = dup(cfg->canonical_json());
+    if (hash_out) *hash_out = dup(cfg->hash());
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_run_experiment(const pfsmc_gpu_experiment* cfg, const char* data_csv,
+                                          const char* out_dir, char** report_path_out) {
+  if (!cfg || !data_csv || !out_dir) {
+    g_err = "null argument";
+    return PFSMC_GPU_ERR_CONFIG;
+  }
+  return guarded([&] {
+    const std::string path = run_impl(*cfg, data_csv, out_dir);
+    if (report_path_out) {
+      char* p = static_cast<char*>(std::malloc(path.size() + 1));
+      if (p) std::memcpy(p, path.c_str(), path.size() + 1);
+      *report_path_out = p;
+    }
+  });
+}
+
+void pfsmc_gpu_string_free(char* s) { std::free(s); }
+
+}  // extern "C"

@@ -11,11 +11,11 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
-HEADER = os.path.join(ROOT, "include", "pfsmc_gpu.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("pfsmc_gpu.h", "pfsmc_gpu_experiment.h")]
 
 
 def declared_symbols():
-    txt = open(HEADER).read()
+    txt = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"\b(pfsmc_gpu_[a-z_0-9]+)\s*\(", txt)))
 
 
