@@ -78,6 +78,10 @@ typedef struct pfsmc_gpu_config {
   double model_consts[8];  /* the bound model's constants; METABOLIC: (lambda, c0, A0, A,
                               t0_input, tau) = MetabolicConstants (models.hpp:67-74),
                               reference defaults (1, 1, 1, 5, 2, 1); others: unused */
+  int adaptive;            /* IntegratorSpec.adaptive: variable-step BDF(1,2)
+                              (lmm::adaptive_bdf_interval, lmm.cpp:894-1019); family,
+                              order and the step h are then unused */
+  double rtol;             /* IntegratorSpec.rtol (adaptive only; reference default 1e-3) */
 } pfsmc_gpu_config;
 
 const char* pfsmc_gpu_version(void);

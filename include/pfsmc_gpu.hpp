@@ -70,6 +70,8 @@ struct PfConfig {
   // the bound model's constants; METABOLIC: models::MetabolicConstants
   // (lambda, c0, A0, A, t0_input, tau), reference defaults (models.hpp:67-74)
   double model_consts[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
+  bool adaptive = false;  // IntegratorSpec.adaptive (variable-step BDF(1,2))
+  double rtol = 1e-3;     // IntegratorSpec.rtol
 };
 
 // filter::TraceRow (filter.hpp:67-75).
@@ -99,6 +101,8 @@ class Sampler {
     c.likelihood = obs.likelihood;
     c.device = cfg.device;
     for (int k = 0; k < 8; ++k) c.model_consts[k] = cfg.model_consts[k];
+    c.adaptive = cfg.adaptive ? 1 : 0;
+    c.rtol = cfg.rtol;
     check(pfsmc_gpu_create(&c, &h_));
   }
   ~Sampler() { pfsmc_gpu_destroy(h_); }

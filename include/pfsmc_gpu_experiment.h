@@ -19,8 +19,9 @@
  * (= pfsmc_status values); the message is pfsmc_gpu_experiment_last_error().
  *
  * Scope: problem "metabolic" (models::MetabolicModel on the device) with the
- * fixed-step integrators ab1-3 / am1-3 / bdf1-3. "advdiff" and
- * "adaptive-bdf2" return PFSMC_GPU_ERR_CONFIG (not implemented on the GPU).
+ * fixed-step integrators ab1-3 / am1-3 / bdf1-3 and "adaptive-bdf2" (the
+ * variable-step BDF(1,2), rtol from the config). "advdiff" returns
+ * PFSMC_GPU_ERR_CONFIG (the sparse model is not implemented on the GPU).
  */
 #ifndef PFSMC_GPU_EXPERIMENT_H
 #define PFSMC_GPU_EXPERIMENT_H

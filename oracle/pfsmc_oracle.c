@@ -521,6 +521,126 @@ static int propagate(int model, int d, const double* th, const double* x0,
   return OR_OK;
 }
 
+/* adaptive_bdf_interval (lmm.cpp:894-1019): variable-step BDF(1,2) with a
+ * Newton corrector, predictor-based error control, gamma = rtol * steps. */
+static double clampd(double v, double lo, double hi) { return (v < lo) ? lo : (hi < v) ? hi : v; }
+static double dmin(double a, double b) { return (b < a) ? b : a; }
+
+static int adaptive_bdf(int model, int d, const double* th, const double* x0, double t0, double t1,
+                        double rtol, double tol, int max_iter, double* state, double* gamma,
+                        int* status, int* iters) {
+  if (!(rtol > 0.0)) return fail(OR_CONFIG, "adaptive_bdf_interval: rtol must be positive");
+  if (!(t1 > t0)) return fail(OR_CONFIG, "adaptive_bdf_interval: need t1 > t0");
+  const double total = t1 - t0;
+  const double h_min = total * 1e-10;
+  double x[OR_MAX_D], fcur[OR_MAX_D], c[OR_MAX_D], pred[OR_MAX_D], xnew[OR_MAX_D], xm1[OR_MAX_D],
+      xm2[OR_MAX_D];
+  double tm1 = 0.0, tm2 = 0.0;
+  int npoints = 1;
+  long steps_taken = 0;
+  memcpy(x, x0, sizeof(double) * d);
+  memset(xm1, 0, sizeof xm1);
+  memset(xm2, 0, sizeof xm2);
+  for (int j = 0; j < d; ++j) gamma[j] = 0.0;
+  *status = OR_ST_OK;
+  *iters = 0;
+  if (!model_rhs(model, t0, th, x, fcur)) {
+    *status = OR_ST_INVALID_RHS;
+    memcpy(state, x, sizeof(double) * d);
+    return OR_OK;
+  }
+  double t = t0;
+  double h = total * 1e-2;
+  while (t < t1 - total * 1e-12) {
+    h = dmin(h, t1 - t);
+    if (h < h_min) {
+      *status = OR_ST_STIFFNESS;
+      memcpy(state, x, sizeof(double) * d);
+      return OR_OK;
+    }
+    const int p = npoints >= 2 ? 2 : 1;
+    const double t_next = t + h;
+    double hb0, factor;
+    if (p == 1) {
+      for (int j = 0; j < d; ++j) {
+        c[j] = x[j];
+        pred[j] = x[j] + h * fcur[j];
+      }
+      hb0 = h;
+      factor = 0.5;
+    } else {
+      const double h_prev = t - tm1;
+      const double omega = h / h_prev;
+      const double a2 = -(omega * omega) / (1.0 + 2.0 * omega);
+      hb0 = h * (1.0 + omega) / (1.0 + 2.0 * omega);
+      for (int j = 0; j < d; ++j) c[j] = x[j] + a2 * (xm1[j] - x[j]);
+      if (npoints >= 3) {
+        const double dt1 = t - tm1;
+        const double dt2 = tm1 - tm2;
+        for (int j = 0; j < d; ++j) {
+          const double dd1 = (x[j] - xm1[j]) / dt1;
+          const double dd1p = (xm1[j] - xm2[j]) / dt2;
+          const double dd2 = (dd1 - dd1p) / (t - tm2);
+          pred[j] = x[j] + h * dd1 + h * (h + dt1) * dd2;
+        }
+      } else {
+        for (int j = 0; j < d; ++j) pred[j] = x[j] + omega * (x[j] - xm1[j]);
+      }
+      factor = 2.0 / 11.0;
+    }
+    int it = 0;
+    const int st = newton_solve(model, t_next, th, d, hb0, c, pred, tol, max_iter, xnew, &it);
+    *iters += it;
+    if (st != OR_ST_OK) {
+      h *= 0.25;
+      continue;
+    }
+    double err = 0.0, xn = 0.0;
+    for (int j = 0; j < d; ++j) {
+      err = dmax(err, factor * fabs(xnew[j] - pred[j]));
+      xn = dmax(xn, fabs(xnew[j]));
+    }
+    const double est_rel = err / (1.0 + xn);
+    double growth;
+    if (est_rel == 0.0) {
+      growth = 4.0;
+    } else {
+      growth = 0.9 * pow(rtol / est_rel, 1.0 / ((double)p + 1.0));
+      growth = clampd(growth, 0.25, 4.0);
+    }
+    if (est_rel <= rtol) {
+      if (!model_rhs(model, t_next, th, xnew, fcur)) {
+        *status = OR_ST_INVALID_RHS;
+        memcpy(state, x, sizeof(double) * d);
+        return OR_OK;
+      }
+      memcpy(xm2, xm1, sizeof(double) * d);
+      tm2 = tm1;
+      memcpy(xm1, x, sizeof(double) * d);
+      tm1 = t;
+      memcpy(x, xnew, sizeof(double) * d);
+      t = t_next;
+      npoints = npoints + 1 < 3 ? npoints + 1 : 3;
+      ++steps_taken;
+    }
+    h *= growth;
+  }
+  const double g = rtol * (double)steps_taken;
+  for (int j = 0; j < d; ++j) gamma[j] = g;
+  memcpy(state, x, sizeof(double) * d);
+  return OR_OK;
+}
+
+/* the integrator the config selects (filter.cpp:242-264) */
+static int propagate_cfg(const or_cfg* c, int d, const double* th, const double* x0, double t0,
+                         double t1, double* state, double* gamma, int* status, int* iters) {
+  if (c->adaptive)
+    return adaptive_bdf(c->model, d, th, x0, t0, t1, c->rtol, c->newton_tol, c->newton_max_iter, state,
+                        gamma, status, iters);
+  return propagate(c->model, d, th, x0, t0, t1, c->h, c->family, c->order, c->newton_tol,
+                   c->newton_max_iter, state, gamma, status, iters);
+}
+
 int or_propagate_interval(int model, const double* theta_nat, const double* x0,
                           double t0, double t1, double h, int family, int order,
                           double tol, int max_iter, double* state_out,
@@ -735,9 +855,7 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
     double nat[OR_MAX_P], xb[OR_MAX_D], gam[OR_MAX_D];
     int st, it;
     to_natural((int)p, tb + i * p, nat);
-    if ((rc = propagate(c->model, (int)d, nat, e->states + i * d, t_prev, t_obs,
-                        c->h, c->family, c->order, c->newton_tol,
-                        c->newton_max_iter, xb, gam, &st, &it)))
+    if ((rc = propagate_cfg(c, (int)d, nat, e->states + i * d, t_prev, t_obs, xb, gam, &st, &it)))
       goto done;
     if (out && out->newton_iters) out->newton_iters[i] = it;
     ll_bar[i] = st == OR_ST_OK ? or_log_likelihood(c, y, xb) : kNegInf;
@@ -779,9 +897,7 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
     double nat[OR_MAX_P], xr[OR_MAX_D], gam[OR_MAX_D];
     int st, it;
     to_natural((int)p, tnew + i * p, nat);
-    if ((rc = propagate(c->model, (int)d, nat, xs + i * d, t_prev, t_obs, c->h,
-                        c->family, c->order, c->newton_tol, c->newton_max_iter,
-                        xr, gam, &st, &it)))
+    if ((rc = propagate_cfg(c, (int)d, nat, xs + i * d, t_prev, t_obs, xr, gam, &st, &it)))
       goto done;
     if (out && out->newton_iters) out->newton_iters[i] += it;
     if (out && out->status_new) out->status_new[i] = st;

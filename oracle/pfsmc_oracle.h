@@ -28,7 +28,7 @@ enum { OR_MODEL_DECAY = 0, OR_MODEL_LV = 1, OR_MODEL_ROBERTSON = 2, OR_MODEL_CHA
        OR_MODEL_METABOLIC = 5 /* the reference's models::MetabolicModel (models.cpp:37-119) */ };
 enum { OR_LIK_GAUSSIAN = 0, OR_LIK_LOGNORMAL = 1 };
 enum { OR_ST_OK = 0, OR_ST_INVALID_RHS = 1, OR_ST_NEWTON_DIVERGENCE = 2,
-       OR_ST_SINGULAR = 3 };
+       OR_ST_SINGULAR = 3, OR_ST_STIFFNESS = 4 };
 
 #define OR_MAX_D 8
 #define OR_MAX_P 4
@@ -46,6 +46,8 @@ typedef struct or_cfg {
   uint64_t m_y;
   double sigma;
   int likelihood; /* OR_LIK_* ; lognormal is an extension */
+  int adaptive;   /* IntegratorSpec.adaptive: variable-step BDF(1,2) (lmm.cpp:894-1019) */
+  double rtol;    /* IntegratorSpec.rtol (adaptive only) */
 } or_cfg;
 
 typedef struct or_ens {

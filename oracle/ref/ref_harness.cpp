@@ -85,6 +85,8 @@ typedef struct ref_cfg {
   uint64_t m_y;
   double sigma;
   int workers;      // 0 sequential, >0 parallel(workers), <0 batched(-workers)
+  int adaptive;     // IntegratorSpec.adaptive (variable-step BDF(1,2))
+  double rtol;      // IntegratorSpec.rtol
 } ref_cfg;
 
 typedef struct ref_ens {
@@ -136,9 +138,10 @@ filter::PfConfig to_pf(const ref_cfg& c, std::size_t n, const models::OdeModel& 
   cfg.particles = n;
   cfg.shrink_a = c.a;
   cfg.h = c.h;
-  cfg.integrator.adaptive = false;
+  cfg.integrator.adaptive = c.adaptive != 0;
   cfg.integrator.family = family_of(c.family);
   cfg.integrator.order = c.order;
+  cfg.integrator.rtol = c.rtol;
   cfg.seed = c.seed;
   cfg.newton.tol = c.newton_tol;
   cfg.newton.max_iter = c.newton_max_iter;

@@ -14,7 +14,8 @@
 // "<problem>_<integrator>_gpu".
 //
 // Out of scope (ConfigError): problem "advdiff" (the sparse advection-
-// diffusion model) and integrator "adaptive-bdf2".
+// diffusion model). Integrator "adaptive-bdf2" runs the
+// device adaptive BDF(1,2) (lmm.cpp:894-1019) with the config's rtol.
 #include <charconv>
 #include <chrono>
 #include <cmath>
@@ -90,15 +91,33 @@ std::string fmt17(double v) {  // %.17g, the trace CSV format (bench.cpp:24-28)
   return buf;
 }
 
-// Shortest round-trip decimal with a ".0" on integral values: the number
-// format of the reference's JSON writer.
+// The number format of the reference's JSON writer (nlohmann::json dump):
+// the shortest round-trip digits D with value = D x 10^k, n = |D| + k, laid out
+// as D000.0 (k >= 0, n <= 15), DD.DD (0 < n <= 15), 0.000D (-4 < n <= 0),
+// else D.DDDe+XX (exponent sign always, at least two digits).
 std::string json_num(double v) {
   if (!std::isfinite(v)) return "null";
+  if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
   char buf[64];
-  const auto r = std::to_chars(buf, buf + sizeof buf, v);
-  std::string s(buf, r.ptr);
-  if (s.find_first_of(".eE") == std::string::npos) s += ".0";
-  return s;
+  const auto r = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::scientific);
+  const std::string sci(buf, r.ptr);  // [-]d[.ddd]e[+-]XX
+  std::string out = v < 0 ? "-" : "";
+  const std::size_t epos = sci.find('e');
+  std::string digits;
+  for (std::size_t i = v < 0 ? 1 : 0; i < epos; ++i)
+    if (sci[i] != '.') digits += sci[i];
+  const int x = std::atoi(sci.c_str() + epos + 1);  // value = d.ddd x 10^x
+  const int len = static_cast<int>(digits.size());
+  const int k = x - (len - 1);                       // value = digits x 10^k
+  const int n = len + k;
+  if (k >= 0 && n <= 15) return out + digits + std::string(k, '0') + ".0";
+  if (0 < n && n <= 15) return out + digits.substr(0, n) + "." + digits.substr(n);
+  if (-4 < n && n <= 0) return out + "0." + std::string(-n, '0') + digits;
+  std::string m = len == 1 ? digits : digits.substr(0, 1) + "." + digits.substr(1);
+  const int e = n - 1;
+  char eb[8];
+  std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+  return out + m + eb;
 }
 
 std::string json_str(const std::string& s) {
@@ -265,12 +284,16 @@ double jnum(const JVal& v) {
 // ---- ExperimentConfig (bench.hpp:18-41) ----------------------------------
 struct Integrator {
   int family = PFSMC_GPU_BDF, order = 2;
+  bool adaptive = false;
 };
 
 // parse_integrator (bench.cpp:67-97)
 Integrator parse_integrator(const std::string& name) {
-  if (name == "adaptive-bdf2")
-    throw ConfigError("integrator 'adaptive-bdf2' (adaptive BDF(1,2)) is not implemented by the GPU sampler");
+  if (name == "adaptive-bdf2") {
+    Integrator s;
+    s.adaptive = true;
+    return s;
+  }
   if (name.size() >= 3) {
     const char digit = name.back();
     const std::string fam = name.substr(0, name.size() - 1);
@@ -340,7 +363,7 @@ struct pfsmc_gpu_experiment {
     } else if (key == "n") {
       n = parse_u64(key, value);
     } else if (key == "integrator") {
-      if (value != "adaptive-bdf2") parse_integrator(value);  // validation
+      parse_integrator(value);  // validation
       integrator = value;
     } else if (key == "backend") {
       if (value != "seq" && value != "par" && value != "batch")
@@ -512,7 +535,7 @@ Loaded load_data(const std::string& csv) {
 }
 
 // check_time_grid (bench.cpp:449-476)
-void check_time_grid(const Loaded& d, double h) {
+void check_time_grid(const Loaded& d, bool adaptive, double h) {
   if (d.times.empty()) throw ConfigError("no observations in data file");
   const double spacing = d.times.front() - d.t0;
   if (!(spacing > 0.0)) throw ConfigError("observation times must increase");
@@ -523,6 +546,7 @@ void check_time_grid(const Loaded& d, double h) {
       throw ConfigError("observation times must be equispaced");
     prev = t;
   }
+  if (adaptive) return;
   const double ratio = spacing / h;
   const double r = std::round(ratio);
   if (r < 1.0 || std::abs(ratio - r) > 1e-9 * std::max(1.0, ratio))
@@ -552,6 +576,8 @@ void make_sampler(SamplerHandle& out, const pfsmc_gpu_experiment& cfg, const Set
   c.likelihood = PFSMC_GPU_LIK_GAUSSIAN;
   c.device = cfg.device;
   for (int k = 0; k < 8; ++k) c.model_consts[k] = s.consts[k];
+  c.adaptive = s.integ.adaptive ? 1 : 0;
+  c.rtol = cfg.rtol;
   check_gpu(pfsmc_gpu_create(&c, &out.h));
 }
 
@@ -560,8 +586,8 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
   const Loaded data = load_data(data_csv);
   if (data.problem != cfg.problem)
     throw ConfigError("data file was generated for problem '" + data.problem + "', config says '" + cfg.problem + "'");
-  check_time_grid(data, cfg.step);
-  if (!(cfg.step > 0.0)) throw ConfigError("config: step size h must be positive");
+  check_time_grid(data, setup.integ.adaptive, cfg.step);
+  if (!setup.integ.adaptive && !(cfg.step > 0.0)) throw ConfigError("config: step size h must be positive");
   fs::create_directories(out_dir);
   const std::size_t T = data.times.size(), p = 4, d = 3;
   if (cfg.warmup) {

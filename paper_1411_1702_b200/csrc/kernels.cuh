@@ -25,6 +25,7 @@ struct StepParams {
   double t_prev, h;
   int m;
   int pad;
+  double t_obs;       // interval end (the adaptive integrator's t1)
   double y[kMaxObs];  // observations (log y for the lognormal kind)
   double ll_const;    // -0.5 m (log 2pi + log s2)   (filter.cpp:140, host glibc log)
   double sly;         // sum log y (lognormal extension only)
@@ -87,6 +88,7 @@ struct Ctx {
   unsigned long long seed;
   double two_s2;
   double mconst[8];  // model constants (METABOLIC: lambda, c0, A0, A, t0_input, tau)
+  double rtol;       // adaptive BDF(1,2) tolerance (IntegratorSpec.rtol)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
   double* rec[2];
@@ -335,7 +337,11 @@ __global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 4 : M::D <= 3 ? 4 : 1))
     for (int k = 0; k < P; ++k) th[k] = exp(c.a * tu[k] + c.one_minus_a * st.mu[k]);
     Propagator<M, FAM, ORD> prop;
     prop.mk = M::load_k(c.mconst);
-    const int status = prop.run(th, x, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    int status;
+    if constexpr (ORD == 0)
+      status = prop.run_adaptive(th, x, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
+    else
+      status = prop.run(th, x, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
     const double ll = status == kOk ? loglik<M>(c, sp, x) : kNegInf;
     c.llbar[n] = ll;
     lgv = logw + ll;
@@ -607,7 +613,11 @@ __global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1))
     for (int k = 0; k < D; ++k) xr[k] = x[k];
     Propagator<M, FAM, ORD> prop;
     prop.mk = M::load_k(c.mconst);
-    const int status = prop.run(th, xr, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+    int status;
+    if constexpr (ORD == 0)
+      status = prop.run_adaptive(th, xr, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
+    else
+      status = prop.run(th, xr, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
     double ll = kNegInf;
     if (status == kOk) {
       double zi[D];
@@ -806,6 +816,8 @@ struct KernelSetT final : KernelSet {
 
 template <class M, int FAM>
 std::unique_ptr<KernelSet> make_order(int order) {
+  if constexpr (FAM == kBDF)
+    if (order == 0) return std::make_unique<KernelSetT<M, FAM, 0>>();  // adaptive BDF(1,2)
   switch (order) {
     case 1: return std::make_unique<KernelSetT<M, FAM, 1>>();
     case 2: return std::make_unique<KernelSetT<M, FAM, 2>>();

@@ -22,7 +22,7 @@
 namespace pfsmc_gpu {
 
 enum Family : int { kAB = 0, kAM = 1, kBDF = 2 };
-enum ParticleStatus : int { kOk = 0, kInvalidRhs = 1, kNewtonDivergence = 2, kSingular = 3 };
+enum ParticleStatus : int { kOk = 0, kInvalidRhs = 1, kNewtonDivergence = 2, kSingular = 3, kStiffness = 4 };
 
 // ---- coefficient tables (lmm.cpp:18-60) ----------------------------------
 __host__ __device__ constexpr double ab_beta(int order, int i) {
@@ -56,8 +56,12 @@ __host__ __device__ constexpr double bdf_C(int order) {
 }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
-// std::max as the reference uses it: (a < b) ? b : a (NaN never wins).
+// std::max / std::min / std::clamp as the reference uses them.
 __device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double ref_min(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double ref_clamp(double v, double lo, double hi) {
+  return (v < lo) ? lo : (hi < v) ? hi : v;
+}
 
 // ---- LU with partial pivoting, in registers (linalg.cpp:201-258) --------
 template <int D>
@@ -242,8 +246,9 @@ template <class M, int FAM, int ORD>
 struct Propagator {
   static constexpr int D = M::D;
   static constexpr int P = M::P;
-  static constexpr int SD = FAM == kBDF ? ORD + 1 : 1;  // states kept
-  static constexpr int FD = FAM == kAB ? ORD + 1 : ORD;  // f values kept
+  // ORD == 0: the adaptive BDF(1,2) integrator (run_adaptive only)
+  static constexpr int SD = FAM == kBDF ? ORD + 1 : 1;              // states kept
+  static constexpr int FD = ORD == 0 ? 1 : FAM == kAB ? ORD + 1 : ORD;  // f values kept
 
   double xs[SD][D];
   double fs[FD][D];
@@ -485,6 +490,106 @@ struct Propagator {
 
   // propagate_interval (lmm.cpp:468-503): m fixed steps of size h from x.
   // On return x holds the last accepted state (the reference's run.x).
+  // adaptive_bdf_interval (lmm.cpp:894-1019): variable-step BDF(1,2), the
+  // step size driven per particle by the predictor error estimate; Newton as
+  // in the fixed-step path; gamma = rtol * accepted steps in every component.
+  // The history is three accepted points (x, x_{-1}, x_{-2}) in registers.
+  __device__ __forceinline__ int run_adaptive(const double (&th)[P], double (&x)[D], double t0, double t1,
+                                              double rtol, double tol, int max_iter, double (&gamma)[D],
+                                              int& iters) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) gamma[j] = 0.0;
+    const double total = t1 - t0;
+    const double h_min = total * 1e-10;
+    double fcur[D], xm1[D], xm2[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) xm1[j] = xm2[j] = 0.0;
+    double tm1 = 0.0, tm2 = 0.0;
+    int npoints = 1;
+    long long steps = 0;
+    if (!M::rhs(mk, t0, th, x, fcur)) return kInvalidRhs;
+    double t = t0;
+    double h = total * 1e-2;
+    while (t < t1 - total * 1e-12) {
+      h = ref_min(h, t1 - t);
+      if (h < h_min) return kStiffness;
+      const int p = npoints >= 2 ? 2 : 1;
+      const double t_next = t + h;
+      double hb0, factor, c[D], pred[D];
+      if (p == 1) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          c[j] = x[j];
+          pred[j] = x[j] + h * fcur[j];
+        }
+        hb0 = h;
+        factor = 0.5;
+      } else {
+        const double h_prev = t - tm1;
+        const double omega = h / h_prev;
+        const double a2 = -(omega * omega) / (1.0 + 2.0 * omega);
+        hb0 = h * (1.0 + omega) / (1.0 + 2.0 * omega);
+#pragma unroll
+        for (int j = 0; j < D; ++j) c[j] = x[j] + a2 * (xm1[j] - x[j]);
+        if (npoints >= 3) {
+          const double dt1 = t - tm1;
+          const double dt2 = tm1 - tm2;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const double dd1 = (x[j] - xm1[j]) / dt1;
+            const double dd1p = (xm1[j] - xm2[j]) / dt2;
+            const double dd2 = (dd1 - dd1p) / (t - tm2);
+            pred[j] = x[j] + h * dd1 + h * (h + dt1) * dd2;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) pred[j] = x[j] + omega * (x[j] - xm1[j]);
+        }
+        factor = 2.0 / 11.0;
+      }
+      double xnew[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) xnew[j] = pred[j];
+      if (newton_solve<M>(mk, t_next, th, hb0, c, xnew, tol, max_iter, iters) != kOk) {
+        h *= 0.25;
+        continue;
+      }
+      double err = 0.0, xn = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        err = ref_max(err, factor * fabs(xnew[j] - pred[j]));
+        xn = ref_max(xn, fabs(xnew[j]));
+      }
+      const double est_rel = err / (1.0 + xn);
+      double growth;
+      if (est_rel == 0.0) {
+        growth = 4.0;
+      } else {
+        growth = 0.9 * pow(rtol / est_rel, 1.0 / (static_cast<double>(p) + 1.0));
+        growth = ref_clamp(growth, 0.25, 4.0);
+      }
+      if (est_rel <= rtol) {
+        if (!M::rhs(mk, t_next, th, xnew, fcur)) return kInvalidRhs;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          xm2[j] = xm1[j];
+          xm1[j] = x[j];
+          x[j] = xnew[j];
+        }
+        tm2 = tm1;
+        tm1 = t;
+        t = t_next;
+        npoints = npoints + 1 < 3 ? npoints + 1 : 3;
+        ++steps;
+      }
+      h *= growth;
+    }
+    const double g = rtol * static_cast<double>(steps);
+#pragma unroll
+    for (int j = 0; j < D; ++j) gamma[j] = g;
+    return kOk;
+  }
+
   // t_next = t0 + k h (lmm.cpp:482), not an accumulated sum.
   __device__ __forceinline__ int run(const double (&th)[P], double (&x)[D], double t0, double h, int m,
                                      double tol, int max_iter, double (&gamma)[D], int& iters) {

@@ -1310,8 +1310,14 @@ StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double
   StepParams sp{};
   sp.j = j;
   sp.t_prev = t_prev;
+  sp.t_obs = t_obs;
   sp.h = h;
-  sp.m = step_count(t_prev, t_obs, h);
+  if (s->cfg.adaptive) {
+    if (!(t_obs > t_prev)) throw ConfigError("adaptive_bdf_interval: need t1 > t0");  // lmm.cpp:902-904
+    sp.m = 0;
+  } else {
+    sp.m = step_count(t_prev, t_obs, h);
+  }
   const double m = static_cast<double>(s->cfg.n_obs);
   const double s2 = s->cfg.sigma * s->cfg.sigma;
   constexpr double kLog2Pi = 1.8378770664093453;
@@ -1440,13 +1446,19 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     if (!(cfg->shrink_a > 0.0 && cfg->shrink_a < 1.0))
       throw ConfigError("config: shrink factor a must lie in (0, 1)");
     if (!(cfg->sigma > 0.0)) throw ConfigError("config: observation noise sigma must be positive");
-    if (cfg->order < 1 || cfg->order > 3)
-      throw ConfigError("scheme_coefficients: order must be 1, 2 or 3");
-    if (cfg->family < 0 || cfg->family > 2) throw ConfigError("scheme_coefficients: unknown family");
+    if (cfg->adaptive) {
+      if (!(cfg->rtol > 0.0)) throw ConfigError("config: rtol must be positive");  // filter.cpp:54-56
+    } else {
+      if (cfg->order < 1 || cfg->order > 3)
+        throw ConfigError("scheme_coefficients: order must be 1, 2 or 3");
+      if (cfg->family < 0 || cfg->family > 2) throw ConfigError("scheme_coefficients: unknown family");
+    }
     if (cfg->n_obs > static_cast<uint64_t>(kMaxObs)) throw ConfigError("config: at most 8 observed components");
     auto s = std::make_unique<pfsmc_gpu_sampler>();
     s->cfg = *cfg;
-    s->ks = make_kernels(cfg->model, cfg->family, cfg->order);
+    // adaptive: the variable-step BDF(1,2) kernels (order slot 0)
+    s->ks = cfg->adaptive ? make_kernels(cfg->model, PFSMC_GPU_BDF, 0)
+                          : make_kernels(cfg->model, cfg->family, cfg->order);
     if (!s->ks) throw ConfigError("unknown model id");
     if (cfg->model == MetabolicModel::ID && !(cfg->model_consts[5] > 0.0))
       throw ConfigError("metabolic model: tau must be positive");  // MetabolicModel ctor, models.cpp:104-108
@@ -1485,6 +1497,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.seed = cfg->seed;
     c.two_s2 = 2.0 * (cfg->sigma * cfg->sigma);
     for (int k = 0; k < 8; ++k) c.mconst[k] = cfg->model_consts[k];
+    c.rtol = cfg->rtol;
     // guide buckets: about one per CDF segment (of the whole filter), <= 2^22
     const long long nseg_glob = std::max<long long>(1, static_cast<long long>(cfg->particles) >> kSegLog2);
     int cb = 6;

@@ -59,7 +59,8 @@ class _Config(C.Structure):
                 ("shrink_a", C.c_double), ("seed", C.c_uint64), ("newton_tol", C.c_double),
                 ("newton_max_iter", C.c_int), ("particles", C.c_uint64),
                 ("obs_indices", _u64p), ("n_obs", C.c_uint64), ("sigma", C.c_double),
-                ("likelihood", C.c_int), ("device", C.c_int), ("model_consts", C.c_double * 8)]
+                ("likelihood", C.c_int), ("device", C.c_int), ("model_consts", C.c_double * 8),
+                ("adaptive", C.c_int), ("rtol", C.c_double)]
 
 
 def model_consts_array(model: str, consts=None):
@@ -128,6 +129,8 @@ class PfConfig:
     seed: int = 0
     newton_tol: float = 1e-9
     newton_max_iter: int = 20
+    adaptive: bool = False  # IntegratorSpec.adaptive: variable-step BDF(1,2) (lmm.cpp:894-1019)
+    rtol: float = 1e-3      # IntegratorSpec.rtol (adaptive only)
 
 
 @dataclass
@@ -174,7 +177,8 @@ class GpuSampler:
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed,
                     cfg.newton_tol, cfg.newton_max_iter, cfg.particles,
                     _ptr(self._idx, _u64p), len(self._idx), obs.sigma,
-                    LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts))
+                    LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts),
+                    int(cfg.adaptive), cfg.rtol)
         h = C.c_void_p()
         self._check(self.lib.pfsmc_gpu_create(C.byref(c), C.byref(h)))
         self.h = h

@@ -60,7 +60,8 @@ class GpuShard(GpuSampler):
         self._idx = np.ascontiguousarray(list(obs.indices), dtype=np.uint64)
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed, cfg.newton_tol,
                     cfg.newton_max_iter, cfg.particles, _ptr(self._idx, C.POINTER(C.c_uint64)), len(self._idx),
-                    obs.sigma, LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts))
+                    obs.sigma, LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts),
+                    int(cfg.adaptive), cfg.rtol)
         L = self.lib
         for name in ("pfsmc_gpu_create_shard", "pfsmc_gpu_shard_buffer", "pfsmc_gpu_shard_predict",
                      "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_records",

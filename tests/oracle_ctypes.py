@@ -43,7 +43,7 @@ class OrCfg(C.Structure):
                 ("h", C.c_double), ("a", C.c_double), ("seed", C.c_uint64),
                 ("newton_tol", C.c_double), ("newton_max_iter", C.c_int),
                 ("obs_idx", _u64p), ("m_y", C.c_uint64), ("sigma", C.c_double),
-                ("likelihood", C.c_int)]
+                ("likelihood", C.c_int), ("adaptive", C.c_int), ("rtol", C.c_double)]
 
 
 class RefCfg(C.Structure):
@@ -51,7 +51,7 @@ class RefCfg(C.Structure):
                 ("h", C.c_double), ("a", C.c_double), ("seed", C.c_uint64),
                 ("newton_tol", C.c_double), ("newton_max_iter", C.c_int),
                 ("obs_idx", _u64p), ("m_y", C.c_uint64), ("sigma", C.c_double),
-                ("workers", C.c_int)]
+                ("workers", C.c_int), ("adaptive", C.c_int), ("rtol", C.c_double)]
 
 
 class Ens(C.Structure):
@@ -117,6 +117,8 @@ class StepConfig:
     obs_idx: tuple = (0, 1)
     sigma: float = 0.05
     likelihood: str = "gaussian"
+    adaptive: bool = False   # IntegratorSpec.adaptive (variable-step BDF(1,2))
+    rtol: float = 1e-3       # IntegratorSpec.rtol
 
     @property
     def dims(self):
@@ -147,7 +149,7 @@ class Oracle(_Base):
         idx = np.ascontiguousarray(sc.obs_idx, dtype=np.uint64)
         cfg = OrCfg(MODELS[sc.model], FAMILIES[sc.family], sc.order, sc.h, sc.a,
                     sc.seed, sc.newton_tol, sc.newton_max_iter, _ptr(idx, _u64p),
-                    len(idx), sc.sigma, LIKELIHOODS[sc.likelihood])
+                    len(idx), sc.sigma, LIKELIHOODS[sc.likelihood], int(sc.adaptive), sc.rtol)
         return cfg, idx
 
     def philox(self, ctr, key):
@@ -266,7 +268,8 @@ class Reference(_Base):
             raise ValueError("the reference has only the Gaussian likelihood")
         idx = np.ascontiguousarray(sc.obs_idx, dtype=np.uint64)
         cfg = RefCfg(MODELS[sc.model], FAMILIES[sc.family], sc.order, sc.h, sc.a, sc.seed,
-                     sc.newton_tol, sc.newton_max_iter, _ptr(idx, _u64p), len(idx), sc.sigma, workers)
+                     sc.newton_tol, sc.newton_max_iter, _ptr(idx, _u64p), len(idx), sc.sigma, workers,
+                     int(sc.adaptive), sc.rtol)
         return cfg, idx
 
     def philox(self, ctr, key):

@@ -38,6 +38,8 @@ def _rows(path):
      ("seed", "11")],
     [("particles", "1500"), ("integrator", "am2"), ("step", "0.025"), ("n-obs", "12"), ("t-end", "3"),
      ("seed", "4"), ("const.tau", "0.8"), ("prior.k2.sigma", "0.3"), ("warmup", "1")],
+    [("particles", "1000"), ("integrator", "adaptive-bdf2"), ("rtol", "1e-4"), ("n-obs", "15"), ("t-end", "3"),
+     ("seed", "8")],
 ])
 def test_run_experiment_matches_reference(kv, tmp_path):
     G, R = _libs()

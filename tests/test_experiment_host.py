@@ -35,6 +35,10 @@ CONFIGS = [
      ("seed", "3"), ("prior.V1.sigma", "0.4"), ("const.tau", "0.7"), ("x0.1.mean", "1.3"), ("warmup", "true")],
     [("shrink-a", "0.95"), ("sigma", "0.125"), ("rtol", "1e-05"), ("backend", "par"), ("workers", "8"),
      ("truth.V1", "2.5"), ("n", "7")],
+    # number layouts of the JSON writer: fixed / 0.000d / scientific boundaries
+    # (unused override names carry the extreme values into the canonical JSON only)
+    [("rtol", "1e-4"), ("truth.Za", "0.0001234"), ("truth.Zb", "1e15"), ("truth.Zc", "123456789012345678"),
+     ("truth.Zd", "-2.5e-300"), ("truth.Ze", "1e16"), ("truth.Zf", "-0.0"), ("integrator", "adaptive-bdf2")],
 ]
 
 

@@ -30,7 +30,8 @@ REL_TRACE = 1e-8
 def _sampler(sc: StepConfig, n, likelihood="gaussian", model_consts=None):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     cfg = PfConfig(particles=n, shrink_a=sc.a, h=sc.h, family=sc.family, order=sc.order, seed=sc.seed,
-                   newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter)
+                   newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter, adaptive=sc.adaptive,
+                   rtol=sc.rtol)
     return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood),
                       model_consts=model_consts)
 
@@ -318,6 +319,41 @@ def test_lockstep_metabolic(family, order, consts):
         gpu.close()
     finally:
         O.set_model_consts((1.0, 1.0, 1.0, 5.0, 2.0, 1.0))
+
+
+@pytest.mark.parametrize("model,rtol", [("metabolic", 1e-3), ("metabolic", 1e-5), ("lv", 1e-4),
+                                        ("robertson", 1e-3)])
+def test_lockstep_adaptive_bdf(model, rtol):
+    """Variable-step BDF(1,2) (adaptive_bdf_interval, lmm.cpp:894-1019): per-
+    particle step-size control, Newton corrector, gamma = rtol * steps."""
+    rng = np.random.default_rng(9)
+    n = 5000
+    if model == "metabolic":
+        sc = StepConfig(model=model, family="bdf", order=2, seed=6, obs_idx=(0, 1, 2), sigma=0.1,
+                        adaptive=True, rtol=rtol)
+        mu = np.log([1.5, 0.7, 1.5, 0.5])
+        ens = O.init_gaussian(model, n, 6, mu, [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+        ys = [np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3) for _ in range(4)]
+        ts = [1.6 + 0.2 * k for k in range(5)]
+    elif model == "lv":
+        sc = StepConfig(model=model, family="bdf", order=2, seed=6, adaptive=True, rtol=rtol)
+        ens = O.init_uniform("lv", n, 6, [0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+        ys = [np.array([1.2, 0.9]) + 0.05 * rng.standard_normal(2) for _ in range(4)]
+        ts = [0.1 * k for k in range(5)]
+    else:
+        sc = StepConfig(model=model, family="bdf", order=2, a=0.99, seed=6, obs_idx=(0, 2), sigma=0.02,
+                        newton_max_iter=4, adaptive=True, rtol=rtol)
+        ens = O.init_gaussian(model, n, 6, np.log([0.04, 3e7, 1e4]) + 0.5, [1, 1, 1], [1, 0, 0], [0, 0, 0],
+                              [0, 0, 0])
+        ts = [0.0] + list(np.logspace(-4, 3, 400)[:4])
+        ys = [np.array([1 - 0.04 * t, 0.04 * t * 1e-3]) + 1e-3 * rng.standard_normal(2) for t in ts[1:]]
+    gpu = _sampler(sc, n)
+    for j in range(1, len(ts)):
+        gpu.set_ensemble(_to_gpu_ens(ens))
+        row = gpu.pf_step(ys[j - 1], j, ts[j - 1], ts[j])
+        trace_o, dg = O.pf_step(sc, ens, ys[j - 1], j, ts[j - 1], ts[j], diag=True)
+        _compare_step(gpu, ens, trace_o, dg, row)
+    gpu.close()
 
 
 def test_metabolic_config_error():

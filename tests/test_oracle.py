@@ -217,6 +217,41 @@ def test_oracle_matches_live_reference_metabolic(family, order, consts):
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("model,rtol", [("metabolic", 1e-3), ("metabolic", 1e-5), ("lv", 1e-4),
+                                        ("robertson", 1e-3)])
+def test_oracle_matches_live_reference_adaptive(model, rtol):
+    """Variable-step BDF(1,2) (adaptive_bdf_interval, lmm.cpp:894-1019) through
+    pf_step: oracle == unmodified reference, every field, bitwise."""
+    R = Reference()
+    rng = np.random.default_rng(9)
+    if model == "metabolic":
+        sc = StepConfig(model=model, family="bdf", order=2, seed=6, obs_idx=(0, 1, 2), sigma=0.1,
+                        adaptive=True, rtol=rtol)
+        mu = np.log([1.5, 0.7, 1.5, 0.5])
+        e = O.init_gaussian(model, 300, 6, mu, [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+        ys = [np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3) for _ in range(4)]
+        ts = [1.6 + 0.2 * k for k in range(5)]
+    elif model == "lv":
+        sc = StepConfig(model=model, family="bdf", order=2, seed=6, adaptive=True, rtol=rtol)
+        e = O.init_uniform("lv", 300, 6, [0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+        ys = [np.array([1.2, 0.9]) + 0.05 * rng.standard_normal(2) for _ in range(4)]
+        ts = [0.1 * k for k in range(5)]
+    else:
+        sc = StepConfig(model=model, family="bdf", order=2, a=0.99, seed=6, obs_idx=(0, 2), sigma=0.02,
+                        newton_max_iter=4, likelihood="gaussian", adaptive=True, rtol=rtol)
+        e = R.init_gaussian(sc, 200, np.log([0.04, 3e7, 1e4]) + 0.5, [1, 1, 1], [1, 0, 0], [0, 0, 0], [0, 0, 0])
+        ts = [0.0] + list(np.logspace(-4, 3, 400)[:4])
+        ys = [np.array([1 - 0.04 * t, 0.04 * t * 1e-3]) + 1e-3 * rng.standard_normal(2) for t in ts[1:]]
+    e2 = e.copy()
+    for j in range(1, len(ts)):
+        t1, _ = O.pf_step(sc, e, ys[j - 1], j, ts[j - 1], ts[j])
+        t2 = R.pf_step(sc, e2, ys[j - 1], j, ts[j - 1], ts[j])
+        assert np.array_equal(t1, t2), j
+        assert np.array_equal(e.states, e2.states) and np.array_equal(e.logw, e2.logw)
+        assert np.array_equal(e.params_u, e2.params_u)
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built (needs /root/reference)")
 def test_degeneracy_error_parity():
     """Both raise NUMERICAL at the same step (total degeneracy)."""
     R = Reference()
