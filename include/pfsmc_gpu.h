@@ -177,6 +177,15 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop; the FP64
  * roofline denominator the benchmarks report against). */
 pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops);
+/* One noise-free trajectory of a compiled-in model through times[0..T) from
+ * (t0, x0) with the adaptive BDF(1,2) integrator at rtol (the data
+ * generator's truth path: bench.cpp:296-317 over lmm::adaptive_bdf_interval,
+ * NewtonOpts defaults); states_out is T x d. NUMERICAL if the integration
+ * fails, like the reference generator. */
+pfsmc_gpu_status pfsmc_gpu_model_trajectory(int model, const double* model_consts, const double* theta_nat,
+                                            const double* x0, const double* times, uint64_t T, double t0,
+                                            double rtol, int device, double* states_out);
+
 /* Measured random-gather roofline for the resampling gathers: GB/s of
    64-byte records read at hashed indices plus written in slot order, over
    n_rec records (use n_rec * 64 bytes > L2). Benchmark helper. */

@@ -12,6 +12,7 @@
  *                                         .json sidecar input, same trace CSV
  *                                         and report JSON outputs, run tag
  *                                         "<problem>_<integrator>_gpu")
+ *   pfsmc_gpu_generate_data            <- pfsmc_generate_data (truth path on the GPU)
  *   pfsmc_gpu_string_free              <- pfsmc_string_free
  *
  * pfsmc_gpu_experiment_canonical exposes ExperimentConfig::canonical_json /
@@ -42,6 +43,10 @@ pfsmc_gpu_status pfsmc_gpu_experiment_canonical(const pfsmc_gpu_experiment* cfg,
                                                 char** hash_out);
 pfsmc_gpu_status pfsmc_gpu_run_experiment(const pfsmc_gpu_experiment* cfg, const char* data_csv,
                                           const char* out_dir, char** report_path_out);
+/* pfsmc_generate_data (pfsmc.h:35-37, bench.cpp:321-396): the truth trajectory
+ * integrated on the GPU (pfsmc_gpu_model_trajectory, adaptive BDF(1,2), rtol
+ * 1e-8), the noise from the same keyed streams, the CSV + .json sidecar. */
+pfsmc_gpu_status pfsmc_gpu_generate_data(const pfsmc_gpu_experiment* cfg, const char* csv_path);
 void pfsmc_gpu_string_free(char* s);
 
 #ifdef __cplusplus

@@ -33,6 +33,7 @@
 
 #include "../../include/pfsmc_gpu.h"
 #include "../../include/pfsmc_gpu_experiment.h"
+#include "philox.cuh"  // host Philox4x64-10 streams (bitwise the reference's RngStream)
 
 namespace {
 
@@ -672,9 +673,76 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
   return report_path;
 }
 
+// generate_data (bench.cpp:321-396): the truth path on the GPU (adaptive
+// BDF(1,2) at rtol 1e-8), then per observation row r the stream
+// (seed, r + 1, 0, init) of normals on the host, the CSV and the sidecar.
+void generate_impl(const pfsmc_gpu_experiment& cfg, const std::string& csv_path) {
+  const Setup setup = build_problem(cfg);
+  const auto& o = cfg.overrides;
+  const std::vector<double> truth = {override_or(o, "truth.V1", 2.0), override_or(o, "truth.k1", 0.5),
+                                     override_or(o, "truth.V2", 1.0), override_or(o, "truth.k2", 0.8)};
+  std::vector<double> x0;
+  for (int k = 0; k < 3; ++k) x0.push_back(override_or(o, "x0." + std::to_string(k) + ".truth", 1.0));
+  std::vector<double> times;
+  for (std::uint64_t i = 1; i <= cfg.n_obs; ++i)
+    times.push_back(cfg.t_end * static_cast<double>(i) / static_cast<double>(cfg.n_obs));
+  const std::size_t d = 3, T = times.size();
+  std::vector<double> traj(T * d);
+  check_gpu(pfsmc_gpu_model_trajectory(PFSMC_GPU_MODEL_METABOLIC, setup.consts, truth.data(), x0.data(),
+                                       times.data(), T, 0.0, 1e-8, cfg.device, traj.data()));
+  const std::vector<std::uint64_t> indices = {0, 1, 2};  // problem 1 observes everything
+  double sigma = cfg.sigma;
+  if (!(sigma > 0.0)) {
+    double mx = 0.0;
+    for (const double v : traj) mx = std::max(mx, std::abs(v));
+    sigma = 0.05 * mx;
+  }
+  if (!(sigma >= 1e-12)) throw ConfigError("observation noise sigma must be >= 1e-12");
+  std::ofstream out(csv_path);
+  if (!out) throw IoError("cannot write data file '" + csv_path + "'");
+  out << "t";
+  for (std::size_t k = 1; k <= indices.size(); ++k) out << ",y" << k;
+  out << "\n";
+  for (std::size_t r = 0; r < T; ++r) {
+    pfsmc_gpu::Stream noise(cfg.seed, r + 1, 0, pfsmc_gpu::kInit);
+    out << fmt17(times[r]);
+    for (const std::uint64_t idx : indices) out << "," << fmt17(traj[r * d + idx] + sigma * noise.next_normal());
+    out << "\n";
+  }
+  if (!out) throw IoError("failed writing data file '" + csv_path + "'");
+  out.close();
+  const std::string side = sidecar_path(csv_path);
+  std::ofstream sout(side);
+  if (!sout) throw IoError("cannot write sidecar '" + side + "'");
+  auto arr = [](const std::vector<double>& v) {
+    std::string a = "[";
+    for (std::size_t i = 0; i < v.size(); ++i) a += (i ? ", " : "") + json_num(v[i]);
+    return a + "]";
+  };
+  sout << "{\n";
+  sout << "  \"n\": " << cfg.n << ",\n";
+  sout << "  \"obs_indices\": [0, 1, 2],\n";
+  sout << "  \"param_names\": [\"V1\", \"k1\", \"V2\", \"k2\"],\n";
+  sout << "  \"problem\": " << json_str(cfg.problem) << ",\n";
+  sout << "  \"seed\": " << cfg.seed << ",\n";
+  sout << "  \"sigma\": " << json_num(sigma) << ",\n";
+  sout << "  \"t0\": 0.0,\n";
+  sout << "  \"truth\": " << arr(truth) << "\n";
+  sout << "}\n";
+}
+
 }  // namespace
 
 extern "C" {
+
+pfsmc_gpu_status pfsmc_gpu_generate_data(const pfsmc_gpu_experiment* cfg, const char* csv_path) {
+  if (!cfg || !csv_path) {
+    g_err = "null argument";
+    return PFSMC_GPU_ERR_CONFIG;
+  }
+  return guarded([&] { generate_impl(*cfg, csv_path); });
+}
+
 
 pfsmc_gpu_experiment* pfsmc_gpu_experiment_new(void) { return new (std::nothrow) pfsmc_gpu_experiment; }
 

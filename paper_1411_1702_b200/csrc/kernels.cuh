@@ -777,8 +777,40 @@ __global__ void __launch_bounds__(kThreads) k_init(Ctx c, int kind, const double
 }
 
 // ---------------------------------------------------------------- host side
+// One noise-free truth trajectory (the data generator's reference_observations,
+// bench.cpp:296-317): adaptive BDF(1,2) at rtol from x0 through every
+// observation time, one thread. prm = model constants[8], theta_nat[P], x0[D];
+// out = T x D states; status[0] = first non-ok particle status (0 if none).
+template <class M>
+__global__ void k_trajectory(const double* prm, const double* times, int T, double t0, double rtol,
+                             double tol, int max_iter, double* out, int* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Propagator<M, kBDF, 0> prop;
+  prop.mk = M::load_k(prm);
+  double th[M::P], x[M::D], gamma[M::D];
+#pragma unroll
+  for (int k = 0; k < M::P; ++k) th[k] = prm[8 + k];
+#pragma unroll
+  for (int k = 0; k < M::D; ++k) x[k] = prm[8 + M::P + k];
+  double tp = t0;
+  int iters = 0;
+  status[0] = 0;
+  for (int r = 0; r < T; ++r) {
+    const int st = prop.run_adaptive(th, x, tp, times[r], rtol, tol, max_iter, gamma, iters);
+    if (st != kOk) {
+      status[0] = st;
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < M::D; ++k) out[static_cast<long long>(r) * M::D + k] = x[k];
+    tp = times[r];
+  }
+}
+
 struct KernelSet {
   virtual ~KernelSet() = default;
+  virtual void trajectory(const double* prm, const double* times, int T, double t0, double rtol, double tol,
+                          int max_iter, double* out, int* status, cudaStream_t s) = 0;
   virtual void predict(const Ctx& c, int grid, cudaStream_t s) = 0;
   virtual void update(const Ctx& c, int grid, cudaStream_t s) = 0;
   virtual void moments(const Ctx& c, int grid, cudaStream_t s, int set_cov) = 0;
@@ -794,6 +826,10 @@ struct KernelSetT final : KernelSet {
   KernelSetT() {
     d = M::D;
     p = M::P;
+  }
+  void trajectory(const double* prm, const double* times, int T, double t0, double rtol, double tol,
+                  int max_iter, double* out, int* status, cudaStream_t s) override {
+    k_trajectory<M><<<1, 32, 0, s>>>(prm, times, T, t0, rtol, tol, max_iter, out, status);
   }
   void predict(const Ctx& c, int grid, cudaStream_t s) override {
     k_predict<M, FAM, ORD><<<grid, kThreads, 0, s>>>(c);

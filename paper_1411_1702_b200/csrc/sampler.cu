@@ -2070,6 +2070,52 @@ pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops) {
   });
 }
 
+// One noise-free trajectory of a compiled-in model through the observation
+// times with the adaptive BDF(1,2) integrator (the data generator's truth
+// path, bench.cpp:296-317 with lmm::adaptive_bdf_interval). Blocking.
+pfsmc_gpu_status pfsmc_gpu_model_trajectory(int model, const double* model_consts, const double* theta_nat,
+                                            const double* x0, const double* times, uint64_t T, double t0,
+                                            double rtol, int device, double* states_out) {
+  return guarded([&] {
+    auto ks = make_kernels(model, PFSMC_GPU_BDF, 0);
+    if (!ks) throw ConfigError("unknown model id");
+    if (!(rtol > 0.0)) throw ConfigError("adaptive_bdf_interval: rtol must be positive");
+    if (T == 0) return PFSMC_GPU_OK;
+    double tp = t0;
+    for (uint64_t r = 0; r < T; ++r) {
+      if (!(times[r] > tp)) throw ConfigError("adaptive_bdf_interval: need t1 > t0");
+      tp = times[r];
+    }
+    if (model == MetabolicModel::ID && !(model_consts[5] > 0.0))
+      throw ConfigError("metabolic model: tau must be positive");
+    CK(cudaSetDevice(device));
+    const int d = ks->d, p = ks->p;
+    std::vector<double> prm(8 + p + d);
+    for (int k = 0; k < 8; ++k) prm[k] = model_consts ? model_consts[k] : 0.0;
+    for (int k = 0; k < p; ++k) prm[8 + k] = theta_nat[k];
+    for (int k = 0; k < d; ++k) prm[8 + p + k] = x0[k];
+    double *dprm, *dt, *dout;
+    int* dst;
+    CK(cudaMalloc(&dprm, sizeof(double) * prm.size()));
+    CK(cudaMalloc(&dt, sizeof(double) * T));
+    CK(cudaMalloc(&dout, sizeof(double) * T * d));
+    CK(cudaMalloc(&dst, sizeof(int)));
+    CK(cudaMemcpy(dprm, prm.data(), sizeof(double) * prm.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dt, times, sizeof(double) * T, cudaMemcpyHostToDevice));
+    ks->trajectory(dprm, dt, static_cast<int>(T), t0, rtol, 1e-9, 20, dout, dst, nullptr);  // NewtonOpts{}
+    CK(cudaGetLastError());
+    int st = 0;
+    CK(cudaMemcpy(&st, dst, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(states_out, dout, sizeof(double) * T * d, cudaMemcpyDeviceToHost));
+    cudaFree(dprm);
+    cudaFree(dt);
+    cudaFree(dout);
+    cudaFree(dst);
+    if (st != 0) throw NumericalError("reference trajectory integration failed (stiffness)");
+    return PFSMC_GPU_OK;
+  });
+}
+
 // Measured random 64-byte-record gather throughput (GB/s of record bytes
 // read + written), over n_rec records (> L2), median-free: best of 5.
 pfsmc_gpu_status pfsmc_gpu_gather_peak(int device, long long n_rec, double* gbs) {

@@ -88,3 +88,36 @@ def test_run_experiment_errors_match_reference(tmp_path):
         f.write("9.0,1.0\n")
     o = C.c_char_p()
     assert G.pfsmc_gpu_run_experiment(g, data.encode(), str(tmp_path / "g").encode(), C.byref(o)) == 4
+
+
+@pytest.mark.parametrize("kv", [[("n-obs", "30"), ("t-end", "6"), ("seed", "21")],
+                                [("n-obs", "10"), ("t-end", "4"), ("seed", "2"), ("const.A", "3.5"),
+                                 ("truth.V1", "1.7"), ("x0.0.truth", "0.6"), ("sigma", "0.05")]])
+def test_generate_data_matches_reference(kv, tmp_path):
+    """pfsmc_gpu_generate_data vs the reference's pfsmc_generate_data: the truth
+    path is integrated on the GPU (adaptive BDF(1,2), rtol 1e-8) and the noise
+    comes from the same keyed streams, so every value agrees to rounding."""
+    G, R = _libs()
+    g, r = C.c_void_p(G.pfsmc_gpu_experiment_new()), C.c_void_p(R.pfsmc_config_new())
+    for k, v in kv:
+        assert R.pfsmc_config_set(r, k.encode(), v.encode()) == 0
+        assert G.pfsmc_gpu_experiment_set(g, k.encode(), v.encode()) == 0
+    dr, dg = str(tmp_path / "ref.csv"), str(tmp_path / "gpu.csv")
+    assert R.pfsmc_generate_data(r, dr.encode()) == 0
+    assert G.pfsmc_gpu_generate_data(g, dg.encode()) == 0, G.pfsmc_gpu_experiment_last_error()
+    hr, vr = _rows(dr)
+    hg, vg = _rows(dg)
+    assert hr == hg and vr.shape == vg.shape
+    assert np.array_equal(vr[:, 0], vg[:, 0])
+    np.testing.assert_allclose(vg[:, 1:], vr[:, 1:], rtol=1e-10, atol=1e-12)
+    sr, sg = json.load(open(dr[:-4] + ".json")), json.load(open(dg[:-4] + ".json"))
+    assert set(sr) == set(sg)
+    for key in sr:
+        if key == "sigma":
+            assert abs(sg[key] - sr[key]) <= 1e-10 * sr[key]
+        else:
+            assert sg[key] == sr[key], key
+    # the GPU-generated file drives the reference's own experiment (format compatibility)
+    o = C.c_char_p()
+    assert R.pfsmc_run_experiment(r, dg.encode(), str(tmp_path / "o").encode(), C.byref(o)) == 0, \
+        R.pfsmc_last_error()
