@@ -280,6 +280,42 @@ def bench_workloads(local, fp64):
                         "fp64_tflops_newton_only": tfl, "fp64_peak_tflops_measured": fp64,
                         "frac_of_fp64_peak": (tfl / fp64) if fp64 else None}
     g.close()
+    # the reference's own problem 1 (models::MetabolicModel), BDF2 with m = 4 sub-steps,
+    # N = 2^20, beside the unmodified reference pf_step on a bounded sample
+    nm = 1 << 20
+    prob = problems.metabolic(particles=nm, n_obs=50, seed=1)
+    g = GpuSampler("metabolic", prob.cfg, prob.obs, device=local)
+    prob.init(g)
+    ms, it = _timed_steps(g, prob, 5, 3, torch.cuda.ExternalStream(g.stream_handle, device=local))
+    g.close()
+    t = sum(ms) / len(ms)
+    met = {"particles": nm, "integrator": "bdf2, h = 0.05, m = 4 per observation", "steps": len(ms),
+           "ms_per_step": t, "particle_steps_per_s": nm / (t / 1e3),
+           "newton_iterations_per_particle_step": float(np.mean(it)) / nm}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_ctypes import REF_SO, Oracle, Reference, StepConfig
+        if os.path.exists(REF_SO):
+            workers = len(os.sched_getaffinity(0))
+            O, R = Oracle(), Reference()
+            n_cpu = 1 << 16
+            sc = StepConfig(model="metabolic", family="bdf", order=2, h=0.05, a=0.98, seed=1, obs_idx=(0, 1, 2),
+                            sigma=prob.obs.sigma)
+            ens = R.init_gaussian(sc, n_cpu, prob.prior["th_mu"], prob.prior["th_sigma"], prob.prior["x_mean"],
+                                  prob.prior["x_std"], prob.prior["x_clamp"])
+            secs, done, tp = 0.0, 0, 0.0
+            while done < 4 and secs < 10.0:
+                j = done + 1
+                secs += R.time_steps(sc, ens, prob.ys[j - 1:j], [prob.times[j - 1]], j, tp, workers)
+                tp = prob.times[j - 1]
+                done += 1
+            met["cpu_reference"] = {"value": n_cpu * done / secs, "unit": UNIT, "cores": workers,
+                                    "kind": "reference",
+                                    "sample": f"metabolic N={n_cpu}, observations 1..{done}, reference pf_step "
+                                              f"Backend::parallel({workers})"}
+    except Exception as e:  # the GPU line stands on its own
+        met["cpu_reference"] = {"error": repr(e)[:200]}
+    out["reference_problem1_metabolic"] = met
     return out
 
 

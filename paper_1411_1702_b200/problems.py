@@ -194,3 +194,40 @@ def chain8(particles=1 << 24, T=500, seed=1, substeps=3) -> Problem:
     obs = ObservationModel([0, 3, 7], 0.01)
     prior = dict(th_lo=list(0.5 * th), th_hi=list(2.0 * th), x_lo=[0.0] * 8, x_hi=[0.0] * 8)
     return Problem("chain8", "chain", cfg, obs, th, x0, "uniform", prior, 0.0, substeps, times, ys)
+
+
+def _metabolic_rhs(t, x, th, k=(1.0, 1.0, 1.0, 5.0, 2.0, 1.0)):
+    lam, c0, A0, A, t0, tau = k
+    dt = t - t0
+    phi = A0 if dt <= 0.0 else A0 + A * dt * math.exp(-dt / tau)
+    f1 = th[0] * x[0] / (x[0] + th[1])
+    f2 = th[2] * x[1] / (x[1] + th[3])
+    return [phi - f1, f1 - f2, f2 - lam * (x[2] - c0)]
+
+
+def metabolic(particles=1 << 20, n_obs=50, t_end=10.0, seed=1, step=0.05, integrator=("bdf", 2)) -> Problem:
+    """The reference's own problem 1 (bench.cpp:201-248 defaults): models::
+    MetabolicModel with the default MetabolicConstants, truth (2, 0.5, 1, 0.8),
+    x0 = (1, 1, 1), log-normal prior N(log(1.5, 0.7, 1.5, 0.5), 0.5^2), x0 ~
+    N(1, 0.25^2) clamped at 0, every state observed at t_end i / n_obs with the
+    generator's noise rule sigma = 0.05 max|x| (bench.cpp:346-355). The truth
+    path is scipy Radau at rtol 1e-10 (the reference generator: its adaptive
+    BDF at rtol 1e-8; pfsmc_gpu_generate_data reproduces that one)."""
+    from scipy.integrate import solve_ivp
+    th = np.array([2.0, 0.5, 1.0, 0.8])
+    x0 = np.array([1.0, 1.0, 1.0])
+    times = t_end * np.arange(1, n_obs + 1) / n_obs
+    sol = solve_ivp(_metabolic_rhs, (0.0, float(times[-1])), x0, method="Radau", t_eval=times, args=(th,),
+                    rtol=1e-10, atol=1e-14)
+    path = sol.y.T
+    sigma = 0.05 * float(np.max(np.abs(path)))
+    ys = np.empty((n_obs, 3))
+    for r in range(n_obs):
+        s = HostStream(seed, r + 1, 0, 0)
+        ys[r] = [path[r, i] + sigma * s.next_normal() for i in range(3)]
+    substeps = int(round((times[0] - 0.0) / step))
+    cfg = PfConfig(particles=particles, shrink_a=0.98, h=step, family=integrator[0], order=integrator[1], seed=seed)
+    obs = ObservationModel([0, 1, 2], sigma)
+    prior = dict(th_mu=list(np.log([1.5, 0.7, 1.5, 0.5])), th_sigma=[0.5] * 4, x_mean=[1.0] * 3,
+                 x_std=[0.25] * 3, x_clamp=[1, 1, 1])
+    return Problem("metabolic", "metabolic", cfg, obs, th, x0, "gaussian", prior, 0.0, substeps, times, ys)
