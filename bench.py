@@ -398,6 +398,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the sharded path (NCCL collectives + migration) even at N = 1 (a check of that path)")
     ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")
     args = ap.parse_args()
     world, rank, local = _dist()
@@ -413,8 +415,15 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
+        if "MASTER_ADDR" not in os.environ:  # a plain single-process run with --force-sharded
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
+                              WORLD_SIZE="1")
+            sk.close()
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         if not args.replicas:
             return run_sharded(args, world, rank, local)

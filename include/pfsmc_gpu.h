@@ -221,8 +221,12 @@ pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s);
 /* counts_out: world send counts then world receive counts (payloads of
- * (record, ll_bar, ancestor, slot) doubles); blocking. */
+ * (record, ll_bar, ancestor, slot) doubles); blocking. Every rank derives the
+ * whole migration count matrix locally (same keyed uniforms, same exact shard
+ * ranges), so no count exchange is needed: */
 pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out);
+/* ... the world x world matrix of the last serve (row r = rank r's sends). */
+pfsmc_gpu_status pfsmc_gpu_shard_count_matrix(pfsmc_gpu_sampler* s, uint32_t* out);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */

@@ -898,19 +898,31 @@ __device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
   return c.world - 1;  // unreachable: the last range ends at the guarded cdf >= 1 > u
 }
 
+// Every rank walks all global slots (a warp = 32 consecutive slots, all of one
+// destination since N_local is a multiple of 16384) and serves those whose
+// uniform falls in its exact-CDF range. Send positions: one atomic per warp
+// (ballot + popc), slot order inside the warp.
 __global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendbuf, unsigned* send_cnt) {
   if (grid_error(c)) return;
   const int W = c.R + kShardPW;
   const double lo = c.tile_info[0].x;
   const double hi = c.tile_info[c.ntiles - 1].y;
   const long long cap = c.N;  // per destination: at most its N_local slots
+  const int lane = threadIdx.x & 31;
   for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
        ng += static_cast<long long>(gridDim.x) * kThreads) {
     const double u = resample_uniform(c.seed, c.sp->j, ng);
-    if (!(u >= lo && u < hi)) continue;
-    const unsigned a = find_ancestor(c, u);
+    const bool mine = u >= lo && u < hi;
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    if (!m) continue;
     const int dest = static_cast<int>(ng / c.N);
-    const unsigned pos = atomicAdd(&send_cnt[dest], 1u);
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(&send_cnt[dest], static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!mine) continue;
+    const unsigned pos = base + static_cast<unsigned>(__popc(m & ((1u << lane) - 1u)));
+    const unsigned a = find_ancestor(c, u);
     const double2* src = reinterpret_cast<const double2*>(c.rec[c.st->cur] + static_cast<long long>(a) * c.R);
     double2* dst = reinterpret_cast<double2*>(sendbuf + (dest * cap + pos) * W);
     for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
@@ -919,12 +931,19 @@ __global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendb
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_recv_counts(Ctx c, unsigned* recv_cnt) {
+// The whole migration count matrix, computed identically on every rank from
+// the keyed uniforms and the allgathered exact shard ranges: cnt[r * W + d] =
+// slots of rank d served by rank r. One atomic per group of lanes with the
+// same serving rank (match_any); a warp's 32 slots share the destination.
+__global__ void __launch_bounds__(kThreads) k_count_matrix(Ctx c, unsigned* cnt) {
   if (grid_error(c)) return;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  if (n >= c.N) return;
-  const double u = resample_uniform(c.seed, c.sp->j, c.n0 + n);
-  atomicAdd(&recv_cnt[serving_rank(c, u)], 1u);
+  for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
+       ng += static_cast<long long>(gridDim.x) * kThreads) {
+    const int r = serving_rank(c, resample_uniform(c.seed, c.sp->j, ng));
+    const int dest = static_cast<int>(ng / c.N);
+    const unsigned grp = __match_any_sync(0xffffffffu, r);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&cnt[r * c.world + dest], static_cast<unsigned>(__popc(grp)));
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_place(Ctx c, const double* recvbuf, long long count) {
@@ -1245,6 +1264,7 @@ struct pfsmc_gpu_sampler {
   bool have_ensemble = false;
   // sharding (pfsmc_gpu_create_shard)
   int rank = 0, world = 1;
+  bool shard_api = false;  // created by pfsmc_gpu_create_shard
   int ngroups_pred = 0, ngroups_upd = 0;
   double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
   double* gp_mom_all = nullptr;    // allgathered K3 group partials (world * ngroups * W)
@@ -1252,6 +1272,7 @@ struct pfsmc_gpu_sampler {
   double* sendbuf = nullptr;       // world * N_local payloads
   double* recvbuf = nullptr;       // N_local payloads
   unsigned* counts_dev = nullptr;  // [world] send + [world] recv
+  unsigned* counts_all = nullptr;  // the W x W migration count matrix (k_count_matrix)
   unsigned* counts_host = nullptr; // pinned mirror
 
   template <typename T>
@@ -1433,11 +1454,11 @@ const char* pfsmc_gpu_version(void) { return "pfsmc_gpu 0.1 (sm_100a)"; }
 const char* pfsmc_gpu_last_error(void) { return g_last_error.c_str(); }
 
 static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int world,
-                                    pfsmc_gpu_sampler** out) {
+                                    pfsmc_gpu_sampler** out, bool shard_api = false) {
   return guarded([&] {
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) throw ConfigError("shard: need 0 <= rank < world");
-    if (world > 1 && cfg && cfg->particles % (static_cast<uint64_t>(world) * kGroup * kThreads) != 0)
+    if (shard_api && cfg && cfg->particles % (static_cast<uint64_t>(world) * kGroup * kThreads) != 0)
       throw ConfigError("shard: particles must be a multiple of world * 16384");
     if (!cfg) throw ConfigError("null config");
     // PfConfig::validate (filter.cpp:45-74)
@@ -1523,7 +1544,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     const size_t GNT = NT * world;  // tile arrays cover every shard (aliased at tile0)
     c.n0 = static_cast<long long>(rank) * s->N;
     c.n_glob = static_cast<long long>(cfg->particles);
-    c.sharded = world > 1;
+    c.sharded = shard_api;  // a shard handle (any world size, 1 included) exports its partials
     c.rank = rank;
     c.world = world;
     c.gntiles = static_cast<int>(GNT);
@@ -1565,7 +1586,8 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     CK(cudaMallocHost(&s->trace_host, 64 * sizeof(double)));
     s->ngroups_pred = (s->grid + kGroup - 1) / kGroup;
     s->ngroups_upd = s->ngroups_pred;
-    if (world > 1) {
+    s->shard_api = shard_api;
+    if (shard_api) {
       const int W = s->ks->moment_width();
       s->gp_pred_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_pred * 2);
       s->gp_mom_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_upd * W);
@@ -1573,7 +1595,8 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
       s->sendbuf = s->dalloc<double>(static_cast<size_t>(world) * N * (c.R + kShardPW));
       s->recvbuf = s->dalloc<double>(N * (c.R + kShardPW));
       s->counts_dev = s->dalloc<unsigned>(2 * world);
-      CK(cudaMallocHost(&s->counts_host, 2 * world * sizeof(unsigned)));
+      s->counts_all = s->dalloc<unsigned>(static_cast<size_t>(world) * world);
+      CK(cudaMallocHost(&s->counts_host, (2 * world + world * world) * sizeof(unsigned)));
     }
     build_graph(s.get());
     *out = s.release();
@@ -1587,7 +1610,7 @@ pfsmc_gpu_status pfsmc_gpu_create(const pfsmc_gpu_config* cfg, pfsmc_gpu_sampler
 
 pfsmc_gpu_status pfsmc_gpu_create_shard(const pfsmc_gpu_config* cfg, int rank, int world,
                                         pfsmc_gpu_sampler** out) {
-  return create_impl(cfg, rank, world, out);
+  return create_impl(cfg, rank, world, out, true);
 }
 
 void pfsmc_gpu_destroy(pfsmc_gpu_sampler* s) { delete s; }
@@ -1617,7 +1640,7 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     k_pack<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, d, p, tmp_x, tmp_t, 0);
     // shrink mean + chol(cov_u); sharded: the caller finishes it globally
     // (pfsmc_gpu_shard_moments + allgather + pfsmc_gpu_shard_finish_moments(0))
-    if (s->world == 1) s->ks->moments(s->ctx, s->grid, s->stream, 0);
+    if (!s->shard_api) s->ks->moments(s->ctx, s->grid, s->stream, 0);
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     cudaFree(tmp_x);
@@ -1671,7 +1694,7 @@ static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vecto
     s->ks->init(s->ctx, s->grid, s->stream, kind, dprm, lw0);
     // first pass: mean about 0; second pass: cov about that mean (sharded:
     // the caller runs both passes globally)
-    if (s->world == 1) {
+    if (!s->shard_api) {
       s->ks->moments(s->ctx, s->grid, s->stream, 1);
       s->ks->moments(s->ctx, s->grid, s->stream, 1);
     }
@@ -1905,9 +1928,11 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
       case 7: *ptr = s->gp_mom_all; *bytes = sizeof(double) * W * s->ngroups_upd * s->world; break;
       case 8: *ptr = s->sendbuf; *bytes = sizeof(double) * PW * s->N * s->world; break;
       case 9: *ptr = s->recvbuf; *bytes = sizeof(double) * PW * s->N; break;
+      case 10: *ptr = s->counts_dev; *bytes = sizeof(unsigned) * 2 * s->world; break;
+      case 11: *ptr = s->counts_all; *bytes = sizeof(unsigned) * s->world * s->world; break;
       default: throw ConfigError("shard_buffer: unknown buffer id");
     }
-    if (s->world == 1 && (which == 1 || which == 3 || which >= 7)) throw ConfigError("not a sharded handle");
+    if (!s->shard_api && (which == 1 || which == 3 || which >= 7)) throw ConfigError("not a sharded handle");
     return PFSMC_GPU_OK;
   });
 }
@@ -1958,18 +1983,35 @@ pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
 pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
   return guarded([&] {
     const int W = s->world;
+    // counts_dev: [W] actual sends of this rank; counts_all: the W x W matrix
     CK(cudaMemsetAsync(s->counts_dev, 0, 2 * W * sizeof(unsigned), s->stream));
+    CK(cudaMemsetAsync(s->counts_all, 0, static_cast<size_t>(W) * W * sizeof(unsigned), s->stream));
     const long long nglob = s->ctx.n_glob;
     const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
     k_serve_sharded<<<g, kThreads, 0, s->stream>>>(s->ctx, s->sendbuf, s->counts_dev);
-    k_recv_counts<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->counts_dev + W);
+    k_count_matrix<<<g, kThreads, 0, s->stream>>>(s->ctx, s->counts_all);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(s->counts_host, s->counts_dev, 2 * W * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                       s->stream));
+    CK(cudaMemcpyAsync(s->counts_host, s->counts_dev, W * sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->counts_host + 2 * W, s->counts_all, static_cast<size_t>(W) * W * sizeof(unsigned),
+                       cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     check_error(s);
-    for (int i = 0; i < 2 * W; ++i) counts_out[i] = s->counts_host[i];
+    const unsigned* mat = s->counts_host + 2 * W;
+    for (int d = 0; d < W; ++d)  // the served counts must be the matrix row (self-check)
+      if (s->counts_host[d] != mat[s->rank * W + d]) throw std::runtime_error("shard_serve: count mismatch");
+    for (int i = 0; i < W; ++i) counts_out[i] = mat[s->rank * W + i];      // sends
+    for (int i = 0; i < W; ++i) counts_out[W + i] = mat[i * W + s->rank];  // receives
+    return PFSMC_GPU_OK;
+  });
+}
+
+// The W x W migration count matrix of the last shard_serve (row r: rank r's sends).
+pfsmc_gpu_status pfsmc_gpu_shard_count_matrix(pfsmc_gpu_sampler* s, uint32_t* out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    const int W = s->world;
+    for (int i = 0; i < W * W; ++i) out[i] = s->counts_host[2 * W + i];
     return PFSMC_GPU_OK;
   });
 }

@@ -35,7 +35,8 @@ import numpy as np
 
 from .sampler import MODEL_DIMS, MODELS, GpuSampler, ObservationModel, PfConfig, TraceRow, _f64, _ptr
 
-BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV = range(10)
+(BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
+ BUF_CNT, BUF_CNT_ALL) = range(12)
 STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
 
 
@@ -68,6 +69,7 @@ class GpuShard(GpuSampler):
                      "pfsmc_gpu_shard_resolve", "pfsmc_gpu_shard_serve", "pfsmc_gpu_shard_update",
                      "pfsmc_gpu_shard_moments", "pfsmc_gpu_shard_finish_moments"):
             getattr(L, name).restype = C.c_int
+        L.pfsmc_gpu_shard_count_matrix.restype = C.c_int
         h = C.c_void_p()
         self._check(L.pfsmc_gpu_create_shard(C.byref(c), rank, world, C.byref(h)))
         self.h = h
@@ -108,6 +110,13 @@ class GpuShard(GpuSampler):
         counts = np.zeros(2 * self.world, dtype=np.uint32)
         self._check(self.lib.pfsmc_gpu_shard_serve(self.h, counts.ctypes.data_as(C.POINTER(C.c_uint32))))
         return counts
+
+    def count_matrix(self) -> np.ndarray:
+        """The world x world migration counts of the last serve (row r = rank r's sends),
+        derived locally on every rank."""
+        out = np.zeros(self.world * self.world, dtype=np.uint32)
+        self._check(self.lib.pfsmc_gpu_shard_count_matrix(self.h, out.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return out.reshape(self.world, self.world)
 
     def update(self, n_recv: int):
         self._check(self.lib.pfsmc_gpu_shard_update(self.h, C.c_uint64(n_recv)))
@@ -208,19 +217,21 @@ class TorchComm:
         b = s.buffer(buf)
         n = b.numel() // self.world
         with self._ctx(s):
-            mine = b[self.rank * n:(self.rank + 1) * n].clone()
-            self.dist.all_gather_into_tensor(b, mine)
+            # in place: the input is this rank's slice of the output (NCCL in-place allgather)
+            self.dist.all_gather_into_tensor(b, b[self.rank * n:(self.rank + 1) * n])
 
     def gather_counts(self, shards, local_counts: dict) -> dict:
         import torch
         (s,) = shards
-        t = torch.as_tensor(local_counts[s.rank].astype(np.int64))
-        if hasattr(s, "stream_handle"):
-            t = t.to(f"cuda:{s.device}")
-        out = [torch.zeros_like(t) for _ in range(self.world)]
+        # every copy and the collective on the shard's stream: NCCL orders itself
+        # after the current stream, and the host reads wait for it
         with self._ctx(s):
+            t = torch.as_tensor(local_counts[s.rank].astype(np.int64))
+            if hasattr(s, "stream_handle"):
+                t = t.to(f"cuda:{s.device}")
+            out = [torch.zeros_like(t) for _ in range(self.world)]
             self.dist.all_gather(out, t)
-        return {r: out[r].cpu().numpy() for r in range(self.world)}
+            return {r: out[r].cpu().numpy() for r in range(self.world)}
 
     def exchange(self, shards, counts: dict, item_bytes: int):
         (s,) = shards
@@ -296,10 +307,11 @@ class ShardedFilter:
         comm.allgather_slices(sh, BUF_WIN)
         self._each(lambda s: s.resolve())
         served = {s.rank: s.serve() for s in sh}
-        counts = comm.gather_counts(sh, {r: c[:self.world] for r, c in served.items()})  # send matrix
-        for r, c in served.items():   # each rank also derived its receive counts independently
-            if [int(counts[q][r]) for q in range(self.world)] != [int(v) for v in c[self.world:]]:
-                raise RuntimeError("sharded exchange: send/receive count mismatch")
+        mat = sh[0].count_matrix()                                       # same on every rank: no exchange
+        counts = {r: mat[r] for r in range(self.world)}                  # counts[r][d]: r sends to d
+        for r, c in served.items():
+            if [int(v) for v in c[:self.world]] != [int(v) for v in mat[r]]:
+                raise RuntimeError("sharded exchange: send count mismatch")
         item = 8 * sh[0].payload_doubles()
         comm.exchange(sh, counts, item)                                  # D: migration
         for s in sh:

@@ -39,7 +39,8 @@ class CpuShard:
         self.V = V
         self.bufs = {0: np.zeros(2), 1: np.zeros(2 * world), 2: np.zeros(2), 3: np.zeros(2 * world),
                      4: np.zeros(n_glob), 5: np.zeros(world), 6: np.zeros(V + 1), 7: np.zeros((V + 1) * world),
-                     8: np.zeros(world * self.n * self.W), 9: np.zeros(self.n * self.W)}
+                     8: np.zeros(world * self.n * self.W), 9: np.zeros(self.n * self.W),
+                     10: np.zeros(2 * world, dtype=np.uint32), 11: np.zeros(2 * world * world, dtype=np.uint32)}
         self._tens = {k: _t(v) for k, v in self.bufs.items()}
         self.lse_w = 0.0
         self.mu = np.zeros(self.p)
@@ -55,6 +56,15 @@ class CpuShard:
 
     def payload_doubles(self):
         return self.W
+
+    def count_matrix(self):
+        """world x world migration counts, derived from the keyed uniforms and ranges."""
+        m = np.zeros((self.world, self.world), dtype=np.uint32)
+        u_all = np.array([O.draws(self.sc.seed, self.j, ng, 3, 1, 1)[0] for ng in range(self.n_glob)])
+        for ng, u in enumerate(u_all):
+            r = next(r for r, (a, b) in enumerate(self.ranges) if a <= u < b)
+            m[r, ng // self.n] += 1
+        return m
 
     # ---------------------------------------------------------- ensemble
     def initialize_uniform(self, th_lo, th_hi, x_lo, x_hi):
@@ -180,6 +190,7 @@ class CpuShard:
             u = u_all[self.n0 + n]
             r = next(r for r, (a, b) in enumerate(self.ranges) if a <= u < b)
             cnt[self.world + r] += 1
+        self.bufs[10][:] = cnt
         return cnt
 
     def update(self, n_recv):

@@ -519,6 +519,49 @@ def test_sharded_shards_reproduce_single_handle_bitwise(world):
         s.close()
 
 
+def test_sharded_torchcomm_nccl_world1_bitwise():
+    """The multi-GPU orchestration path as bench.py --gpus N runs it (GpuShard +
+    TorchComm over NCCL, collectives on the shard's stream), at world size 1 on
+    this one GPU: every collective / exchange code path executes and the run
+    equals the single handle bit for bit."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1411_1702_b200 import problems
+    from paper_1411_1702_b200.sampler import GpuSampler
+    from paper_1411_1702_b200.sharded import GpuShard, ShardedFilter, TorchComm
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        n, T = 1 << 15, 4
+        prob = problems.lotka_volterra(particles=n, T=T, seed=19)
+        single = GpuSampler("lv", prob.cfg, prob.obs)
+        single.initialize_uniform(**prob.prior)
+        shard = GpuShard("lv", prob.cfg, prob.obs, 0, 1)
+        f = ShardedFilter([shard], TorchComm())
+        f.initialize_uniform(**prob.prior)
+        tp = 0.0
+        for j in range(1, T + 1):
+            t1 = prob.times[j - 1]
+            r1 = single.pf_step(prob.ys[j - 1], j, tp, t1)
+            r2 = f.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
+            assert np.array_equal(single.step_diagnostics()[0], f.ancestors()), j
+            assert np.array_equal(r1.theta_mean, r2.theta_mean) and r1.ess == r2.ess, j
+            tp = t1
+        e1, e2 = single.get_ensemble(), f.get_ensemble()
+        for name in ("states", "params_u", "logw", "mean_u", "cov_u"):
+            assert np.array_equal(getattr(e1, name), getattr(e2, name)), name
+        single.close()
+        shard.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_free_running_full_size_lv():
     """BASELINE config 2 size (N = 2^20): 10 free-running steps, ancestors
     bit-exact against the oracle and the trace within 1e-8."""
