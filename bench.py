@@ -334,6 +334,8 @@ def run_sharded(args, world, rank, local):
     shard = GpuShard("lv", prob.cfg, prob.obs, rank, world, device=local)
     f = ShardedFilter([shard], TorchComm())
     f.initialize_uniform(**prob.prior)
+    if not args.python_sharded:
+        shard.attach_nccl()   # the native step: one C-ABI call per observation
     stream = shard.stream()
     j, tp = 0, 0.0
     for _ in range(args.warmup):
@@ -398,6 +400,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
+    ap.add_argument("--python-sharded", action="store_true",
+                    help="sharded path orchestrated phase by phase from Python (default: native NCCL step)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded path (NCCL collectives + migration) even at N = 1 (a check of that path)")
     ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")

@@ -227,6 +227,15 @@ pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out);
 /* ... the world x world matrix of the last serve (row r = rank r's sends). */
 pfsmc_gpu_status pfsmc_gpu_shard_count_matrix(pfsmc_gpu_sampler* s, uint32_t* out);
+
+/* Native sharded step: the whole filter::pf_step of the global filter in one
+ * call, the five exchanges as NCCL collectives on the handle's stream (NCCL is
+ * bound at run time to the process's libnccl.so.2). Rank 0 makes the 128-byte
+ * id, every rank attaches with it (one communicator per handle). */
+pfsmc_gpu_status pfsmc_gpu_nccl_unique_id(uint8_t* out128);
+pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t* id128);
+pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
+                                      double t_obs, double h, double* trace_out);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */

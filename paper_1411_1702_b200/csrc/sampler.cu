@@ -16,6 +16,8 @@
 // kernels read records with vector loads and the random ancestor gather
 // touches ceil(8R/32) sectors instead of d+p+1.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is bound at run time (dlopen), see NcclApi
 
 #include <algorithm>
 #include <cmath>
@@ -899,50 +901,51 @@ __device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
 }
 
 // Every rank walks all global slots (a warp = 32 consecutive slots, all of one
-// destination since N_local is a multiple of 16384) and serves those whose
-// uniform falls in its exact-CDF range. Send positions: one atomic per warp
-// (ballot + popc), slot order inside the warp.
-__global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendbuf, unsigned* send_cnt) {
+// destination since N_local is a multiple of 16384): the slot's serving rank
+// from the allgathered exact shard ranges feeds the migration count matrix
+// (identical on every rank: cnt[r * W + d] = slots of rank d served by r;
+// one atomic per group of lanes with the same server), and the slots this
+// rank serves are searched and their payloads written (one atomic per warp).
+__global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendbuf, unsigned* send_cnt,
+                                                            unsigned* cnt) {
   if (grid_error(c)) return;
   const int W = c.R + kShardPW;
-  const double lo = c.tile_info[0].x;
-  const double hi = c.tile_info[c.ntiles - 1].y;
   const long long cap = c.N;  // per destination: at most its N_local slots
   const int lane = threadIdx.x & 31;
   for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
        ng += static_cast<long long>(gridDim.x) * kThreads) {
     const double u = resample_uniform(c.seed, c.sp->j, ng);
-    const bool mine = u >= lo && u < hi;
+    const int r = serving_rank(c, u);
+    const int dest = static_cast<int>(ng / c.N);
+    const unsigned grp = __match_any_sync(0xffffffffu, r);
+    if (lane == __ffs(grp) - 1) atomicAdd(&cnt[r * c.world + dest], static_cast<unsigned>(__popc(grp)));
+    const bool mine = r == c.rank;
     const unsigned m = __ballot_sync(0xffffffffu, mine);
     if (!m) continue;
-    const int dest = static_cast<int>(ng / c.N);
     const int leader = __ffs(m) - 1;
     unsigned base = 0;
     if (lane == leader) base = atomicAdd(&send_cnt[dest], static_cast<unsigned>(__popc(m)));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (!mine) continue;
     const unsigned pos = base + static_cast<unsigned>(__popc(m & ((1u << lane) - 1u)));
-    const unsigned a = find_ancestor(c, u);
-    const double2* src = reinterpret_cast<const double2*>(c.rec[c.st->cur] + static_cast<long long>(a) * c.R);
-    double2* dst = reinterpret_cast<double2*>(sendbuf + (dest * cap + pos) * W);
-    for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldg(src + i);
-    dst[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(c.n0 + a));
-    dst[c.R / 2 + 1] = make_double2(static_cast<double>(ng - dest * c.N), 0.0);
-  }
-}
-
-// The whole migration count matrix, computed identically on every rank from
-// the keyed uniforms and the allgathered exact shard ranges: cnt[r * W + d] =
-// slots of rank d served by rank r. One atomic per group of lanes with the
-// same serving rank (match_any); a warp's 32 slots share the destination.
-__global__ void __launch_bounds__(kThreads) k_count_matrix(Ctx c, unsigned* cnt) {
-  if (grid_error(c)) return;
-  for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
-       ng += static_cast<long long>(gridDim.x) * kThreads) {
-    const int r = serving_rank(c, resample_uniform(c.seed, c.sp->j, ng));
-    const int dest = static_cast<int>(ng / c.N);
-    const unsigned grp = __match_any_sync(0xffffffffu, r);
-    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&cnt[r * c.world + dest], static_cast<unsigned>(__popc(grp)));
+    // warp-cooperative search (lanes not served here pass u = -1) and gather:
+    // consecutive lanes move consecutive 16-byte parts of the served payloads
+    const unsigned a = find_ancestor_warp(c, mine ? u : -1.0);
+    const int H = c.R / 2 + kShardPW / 2;  // 16-byte parts per payload
+    const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
+    for (int idx = lane; idx < 32 * H; idx += 32) {
+      const int src_lane = idx / H, part = idx - src_lane * H;
+      const unsigned as = __shfl_sync(0xffffffffu, a, src_lane);
+      const unsigned ps = __shfl_sync(0xffffffffu, pos, src_lane);
+      if (!((m >> src_lane) & 1u)) continue;
+      double2 v;
+      if (part < c.R / 2)
+        v = __ldg(rec + static_cast<long long>(as) * (c.R / 2) + part);
+      else if (part == c.R / 2)
+        v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(c.n0 + as));
+      else
+        v = make_double2(static_cast<double>(ng - lane + src_lane - dest * c.N), 0.0);
+      reinterpret_cast<double2*>(sendbuf + (dest * cap + ps) * W)[part] = v;
+    }
   }
 }
 
@@ -1232,6 +1235,47 @@ constexpr int kNumKernels = 5;
 
 using namespace pfsmc_gpu;
 
+// NCCL bound at run time: the process's already-loaded libnccl.so.2 (torch's)
+// when there is one, so one NCCL instance serves both; nothing links it.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name)); };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Send && a.Recv && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+void NCK(ncclResult_t r) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + nccl_api().GetErrorString(r));
+}
+
 struct pfsmc_gpu_sampler {
   pfsmc_gpu_config cfg{};
   std::vector<uint64_t> obs;
@@ -1265,6 +1309,7 @@ struct pfsmc_gpu_sampler {
   // sharding (pfsmc_gpu_create_shard)
   int rank = 0, world = 1;
   bool shard_api = false;  // created by pfsmc_gpu_create_shard
+  ncclComm_t nccl = nullptr;  // pfsmc_gpu_shard_attach_nccl (native sharded step)
   int ngroups_pred = 0, ngroups_upd = 0;
   double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
   double* gp_mom_all = nullptr;    // allgathered K3 group partials (world * ngroups * W)
@@ -1272,7 +1317,7 @@ struct pfsmc_gpu_sampler {
   double* sendbuf = nullptr;       // world * N_local payloads
   double* recvbuf = nullptr;       // N_local payloads
   unsigned* counts_dev = nullptr;  // [world] send + [world] recv
-  unsigned* counts_all = nullptr;  // the W x W migration count matrix (k_count_matrix)
+  unsigned* counts_all = nullptr;  // the W x W migration count matrix (k_serve_sharded)
   unsigned* counts_host = nullptr; // pinned mirror
 
   template <typename T>
@@ -1283,6 +1328,7 @@ struct pfsmc_gpu_sampler {
     return static_cast<T*>(p);
   }
   ~pfsmc_gpu_sampler() {
+    if (nccl) nccl_api().CommDestroy(nccl);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -1937,17 +1983,22 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
   });
 }
 
+static void shard_predict_impl(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
+                               double h) {
+  if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
+  CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
+  *s->sp_host = sp;
+  CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+  enqueue_prologue(s);
+  s->ks->predict(s->ctx, s->grid, s->stream);
+  CK(cudaGetLastError());
+}
+
 pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
                                          double t_prev, double t_obs, double h) {
   return guarded([&] {
-    if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
-    const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
-    CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
-    *s->sp_host = sp;
-    CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
-    enqueue_prologue(s);
-    s->ks->predict(s->ctx, s->grid, s->stream);
-    CK(cudaGetLastError());
+    shard_predict_impl(s, y, j, t_prev, t_obs, h);
     return PFSMC_GPU_OK;
   });
 }
@@ -1980,16 +2031,15 @@ pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
 
 // counts_out: [world] payloads this rank sends to each rank, then [world]
 // payloads it receives from each rank. Blocking (the exchange needs them).
-pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
-  return guarded([&] {
+static void shard_serve_impl(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  {
     const int W = s->world;
     // counts_dev: [W] actual sends of this rank; counts_all: the W x W matrix
     CK(cudaMemsetAsync(s->counts_dev, 0, 2 * W * sizeof(unsigned), s->stream));
     CK(cudaMemsetAsync(s->counts_all, 0, static_cast<size_t>(W) * W * sizeof(unsigned), s->stream));
     const long long nglob = s->ctx.n_glob;
     const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
-    k_serve_sharded<<<g, kThreads, 0, s->stream>>>(s->ctx, s->sendbuf, s->counts_dev);
-    k_count_matrix<<<g, kThreads, 0, s->stream>>>(s->ctx, s->counts_all);
+    k_serve_sharded<<<g, kThreads, 0, s->stream>>>(s->ctx, s->sendbuf, s->counts_dev, s->counts_all);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(s->counts_host, s->counts_dev, W * sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(s->counts_host + 2 * W, s->counts_all, static_cast<size_t>(W) * W * sizeof(unsigned),
@@ -2002,6 +2052,12 @@ pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_ou
       if (s->counts_host[d] != mat[s->rank * W + d]) throw std::runtime_error("shard_serve: count mismatch");
     for (int i = 0; i < W; ++i) counts_out[i] = mat[s->rank * W + i];      // sends
     for (int i = 0; i < W; ++i) counts_out[W + i] = mat[i * W + s->rank];  // receives
+  }
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  return guarded([&] {
+    shard_serve_impl(s, counts_out);
     return PFSMC_GPU_OK;
   });
 }
@@ -2036,21 +2092,109 @@ pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s) {
 
 // flags: 7 = a completed step (lse_w, cov, chol, flip); 2 = init refresh;
 // 0 = injection (shrink mean only). Blocking; trace_out optional.
+static void shard_finish_moments_impl(pfsmc_gpu_sampler* s, int flags, double* trace_out) {
+  s->ks->finish_moments(s->ctx, s->gp_mom_all, s->ngroups_upd * s->world, flags, s->stream);
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaGetLastError());
+  check_error(s);
+  if (trace_out) {
+    const int n = 2 * s->p + s->d + 1;
+    for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
+  }
+}
+
 pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out) {
   return guarded([&] {
-    s->ks->finish_moments(s->ctx, s->gp_mom_all, s->ngroups_upd * s->world, flags, s->stream);
-    CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
-    CK(cudaGetLastError());
-    check_error(s);
-    if (trace_out) {
-      const int n = 2 * s->p + s->d + 1;
-      for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
-    }
+    shard_finish_moments_impl(s, flags, trace_out);
     return PFSMC_GPU_OK;
   });
 }
 
+
+// ---- native sharded step over NCCL (one call per observation) ------------
+pfsmc_gpu_status pfsmc_gpu_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    if (!nccl_api().ok) throw std::runtime_error("nccl: libnccl.so.2 not available");
+    ncclUniqueId id;
+    NCK(nccl_api().GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t* id128) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (!nccl_api().ok) throw std::runtime_error("nccl: libnccl.so.2 not available");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    CK(cudaSetDevice(s->cfg.device));
+    if (s->nccl) NCK(nccl_api().CommDestroy(s->nccl));
+    NCK(nccl_api().CommInitRank(&s->nccl, s->world, id, s->rank));
+    return PFSMC_GPU_OK;
+  });
+}
+
+// One pf_step of the global filter: the five exchanges as NCCL
+// collectives on the sampler stream between the phase kernels, host syncs
+// only where the host needs data (the migration counts, the trace row).
+pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
+                                      double t_obs, double h, double* trace_out) {
+  return guarded([&] {
+    if (!s->nccl) throw ConfigError("shard_step: no NCCL communicator (pfsmc_gpu_shard_attach_nccl)");
+    const NcclApi& N = nccl_api();
+    const Ctx& c = s->ctx;
+    cudaStream_t st = s->stream;
+    const int W = s->world, me = s->rank;
+    shard_predict_impl(s, y, j, t_prev, t_obs, h);
+    // A: predict-kernel group partials -> global LSE
+    NCK(N.AllGather(c.gpart, s->gp_pred_all, 2 * static_cast<size_t>(s->ngroups_pred), ncclDouble, s->nccl, st));
+    k_finish_lse<<<1, kThreads, 0, st>>>(c, s->gp_pred_all, s->ngroups_pred * W);
+    // B: shard (approximate total, nonzero count) -> global prefix for the classification
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
+    k_shard_offset<<<1, 32, 0, st>>>(c, s->sums_all);
+    launch_scan(c, s->ntiles, st, 4);
+    // C: tile records, in place (this rank's slice of the global arrays)
+    NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));
+    NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8,
+                    s->nccl, st));
+    launch_scan(c, s->ntiles, st, 5);
+    launch_scan(c, s->ntiles, st, 2);
+    CK(cudaGetLastError());
+    // D: exact-mode migration; the counts are the locally derived matrix
+    std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
+    shard_serve_impl(s, cnt.data());
+    const unsigned* mat = s->counts_host + 2 * W;
+    const size_t item = sizeof(double) * static_cast<size_t>(c.R + kShardPW);
+    const size_t cap = static_cast<size_t>(s->N);
+    char* send = reinterpret_cast<char*>(s->sendbuf);
+    char* recv = reinterpret_cast<char*>(s->recvbuf);
+    size_t off = 0;
+    NCK(N.GroupStart());
+    for (int r = 0; r < W; ++r) {
+      const size_t k_in = mat[r * W + me], k_out = mat[me * W + r];
+      if (r == me) {
+        if (k_in)
+          CK(cudaMemcpyAsync(recv + off * item, send + r * cap * item, k_in * item, cudaMemcpyDeviceToDevice, st));
+      } else {
+        if (k_out) NCK(N.Send(send + r * cap * item, k_out * item, ncclUint8, r, s->nccl, st));
+        if (k_in) NCK(N.Recv(recv + off * item, k_in * item, ncclUint8, r, s->nccl, st));
+      }
+      off += k_in;
+    }
+    NCK(N.GroupEnd());
+    if (off != cap) throw std::runtime_error("shard_step: payload count mismatch");
+    k_place<<<s->grid, kThreads, 0, st>>>(c, s->recvbuf, static_cast<long long>(off));
+    s->ks->update(c, s->grid, st);
+    // E: update-kernel moment partials -> global lse_w, moments, trace row, chol
+    const size_t Wm = static_cast<size_t>(s->ks->moment_width());
+    NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
+    CK(cudaGetLastError());
+    shard_finish_moments_impl(s, 7, trace_out);
+    return PFSMC_GPU_OK;
+  });
+}
 
 // ---- BASELINE config 5 microbenchmark entry points (model PAYLOAD64) -----
 pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key) {

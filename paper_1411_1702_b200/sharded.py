@@ -118,6 +118,30 @@ class GpuShard(GpuSampler):
         self._check(self.lib.pfsmc_gpu_shard_count_matrix(self.h, out.ctypes.data_as(C.POINTER(C.c_uint32))))
         return out.reshape(self.world, self.world)
 
+    def attach_nccl(self, comm_group=None):
+        """Native step: one NCCL communicator for this handle (id from rank 0,
+        shared through torch.distributed)."""
+        import torch
+        import torch.distributed as dist
+        self.lib.pfsmc_gpu_nccl_unique_id.restype = C.c_int
+        self.lib.pfsmc_gpu_shard_attach_nccl.restype = C.c_int
+        self.lib.pfsmc_gpu_shard_step.restype = C.c_int
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            self._check(self.lib.pfsmc_gpu_nccl_unique_id(uid.ctypes.data_as(C.POINTER(C.c_uint8))))
+        t = torch.from_numpy(uid).to(f"cuda:{self.device}")
+        dist.broadcast(t, 0, group=comm_group)
+        uid = t.cpu().numpy()
+        self._check(self.lib.pfsmc_gpu_shard_attach_nccl(self.h, uid.ctypes.data_as(C.POINTER(C.c_uint8))))
+        self.native = True
+
+    def native_step(self, y, j, t_prev, t_obs, h) -> np.ndarray:
+        out = np.zeros(self.row_width)
+        y = _f64(y)
+        self._check(self.lib.pfsmc_gpu_shard_step(self.h, _ptr(y), C.c_uint64(j), C.c_double(t_prev),
+                                                   C.c_double(t_obs), C.c_double(h), _ptr(out)))
+        return out
+
     def update(self, n_recv: int):
         self._check(self.lib.pfsmc_gpu_shard_update(self.h, C.c_uint64(n_recv)))
 
@@ -298,6 +322,12 @@ class ShardedFilter:
 
     def pf_step(self, y, j: int, t_prev: float, t_obs: float, h: float) -> TraceRow:
         sh, comm = self.shards, self.comm
+        if len(sh) == 1 and getattr(sh[0], "native", False):
+            # one native call: the same phases and exchanges over NCCL (pfsmc_gpu_shard_step)
+            out = sh[0].native_step(y, j, t_prev, t_obs, h)
+            p, d = self.p, self.d
+            return TraceRow(j, t_obs, out[:p].copy(), out[p:2 * p].copy(), out[2 * p:2 * p + d].copy(),
+                            float(out[2 * p + d]))
         self._each(lambda s: s.predict(y, j, t_prev, t_obs, h))
         comm.allgather(sh, BUF_PRED, BUF_PRED_ALL)                       # A
         self._each(lambda s: s.finish_lse())                             # (+ local tile prefixes)

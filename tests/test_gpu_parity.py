@@ -545,19 +545,28 @@ def test_sharded_torchcomm_nccl_world1_bitwise():
         shard = GpuShard("lv", prob.cfg, prob.obs, 0, 1)
         f = ShardedFilter([shard], TorchComm())
         f.initialize_uniform(**prob.prior)
+        shard2 = GpuShard("lv", prob.cfg, prob.obs, 0, 1)   # the native NCCL step
+        f2 = ShardedFilter([shard2], TorchComm())
+        f2.initialize_uniform(**prob.prior)
+        shard2.attach_nccl()
         tp = 0.0
         for j in range(1, T + 1):
             t1 = prob.times[j - 1]
             r1 = single.pf_step(prob.ys[j - 1], j, tp, t1)
             r2 = f.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
+            r3 = f2.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
             assert np.array_equal(single.step_diagnostics()[0], f.ancestors()), j
+            assert np.array_equal(single.step_diagnostics()[0], f2.ancestors()), j
             assert np.array_equal(r1.theta_mean, r2.theta_mean) and r1.ess == r2.ess, j
+            assert np.array_equal(r1.theta_mean, r3.theta_mean) and r1.ess == r3.ess, j
             tp = t1
-        e1, e2 = single.get_ensemble(), f.get_ensemble()
+        e1, e2, e3 = single.get_ensemble(), f.get_ensemble(), f2.get_ensemble()
         for name in ("states", "params_u", "logw", "mean_u", "cov_u"):
             assert np.array_equal(getattr(e1, name), getattr(e2, name)), name
+            assert np.array_equal(getattr(e1, name), getattr(e3, name)), name
         single.close()
         shard.close()
+        shard2.close()
     finally:
         dist.destroy_process_group()
 
