@@ -519,6 +519,39 @@ def test_sharded_shards_reproduce_single_handle_bitwise(world):
         s.close()
 
 
+def test_sharded_metabolic_adaptive_bitwise():
+    """Sharding with the reference's own model and the adaptive integrator:
+    2 shards (LocalComm, one GPU) == the single handle, bit for bit."""
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    from paper_1411_1702_b200.sharded import GpuShard, LocalComm, ShardedFilter
+    n = 1 << 15
+    cfg = PfConfig(particles=n, shrink_a=0.98, seed=4, adaptive=True, rtol=1e-4)
+    obs = ObservationModel([0, 1, 2], 0.1)
+    prior = dict(th_mu=list(np.log([1.5, 0.7, 1.5, 0.5])), th_sigma=[0.5] * 4, x_mean=[1.0] * 3,
+                 x_std=[0.25] * 3, x_clamp=[1, 1, 1])
+    single = GpuSampler("metabolic", cfg, obs)
+    single.initialize_gaussian(**prior)
+    shards = [GpuShard("metabolic", cfg, obs, r, 2) for r in range(2)]
+    f = ShardedFilter(shards, LocalComm(2))
+    f.initialize_gaussian(**prior)
+    rng = np.random.default_rng(2)
+    tp = 1.6
+    for j in range(1, 5):
+        y = np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3)
+        r1 = single.pf_step(y, j, tp, tp + 0.2)
+        r2 = f.pf_step(y, j, tp, tp + 0.2, 0.05)
+        assert np.array_equal(single.step_diagnostics()[0], f.ancestors()), j
+        for a, b in ((r1.theta_mean, r2.theta_mean), (r1.theta_var, r2.theta_var), ([r1.ess], [r2.ess])):
+            assert np.array_equal(np.asarray(a), np.asarray(b)), j
+        tp += 0.2
+    e1, e2 = single.get_ensemble(), f.get_ensemble()
+    for name in ("states", "params_u", "logw", "mean_u", "cov_u"):
+        assert np.array_equal(getattr(e1, name), getattr(e2, name)), name
+    single.close()
+    for s in shards:
+        s.close()
+
+
 def test_sharded_torchcomm_nccl_world1_bitwise():
     """The multi-GPU orchestration path as bench.py --gpus N runs it (GpuShard +
     TorchComm over NCCL, collectives on the shard's stream), at world size 1 on
