@@ -199,6 +199,7 @@ LOCKSTEP = [
     ("lv_am2_n5003", dict(model="lv", family="am", order=2, h=0.1, seed=26), 5003, 5, 1),
     ("lv_bdf2_n257", dict(model="lv", family="bdf", order=2, h=0.05, seed=27), 257, 5, 2),
     ("lv_am1_n3", dict(model="lv", family="am", order=1, h=0.1, seed=28), 3, 4, 1),
+    ("lv_bdf1_n1", dict(model="lv", family="bdf", order=1, h=0.1, seed=30), 1, 3, 1),
     ("lv_ab2_n70001", dict(model="lv", family="ab", order=2, h=0.1, seed=29), 70001, 3, 1),
 ]
 
