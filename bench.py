@@ -506,13 +506,14 @@ def main():
     dom = max(names, key=lambda k: kt[k])
     avg_ms = kt[dom] / args.steps
     achieved = KERNEL_BYTES[dom] * n / (avg_ms / 1e3) / 1e9
-    traffic = None
+    traffic, prof = None, {}
     tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")
+            prof = json.load(open(tpath)).get(dom, {})
+            traffic = prof.get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic, prof = None, {}
     step_gbs = STEP_BYTES * n / (total_ms / args.steps / 1e3) / 1e9
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -525,7 +526,13 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind},
+                         "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind,
+                         # what actually limits the kernel (one ncu --set full capture of this
+                         # command, profiles/kernel_traffic.json): instruction issue, not HBM
+                         "ncu_issue_active_pct": prof.get("issue_active_pct"),
+                         "ncu_fp64_pipe_pct": prof.get("fp64_pipe_pct"),
+                         "ncu_achieved_occupancy_pct": prof.get("achieved_occupancy_pct"),
+                         "ncu_source": prof.get("source")},
             "step_roofline": {"bytes_per_particle": STEP_BYTES, "achieved": step_gbs, "peak": hbm,
                               "frac": step_gbs / hbm},
             "kernel_ms_per_step": {k: v / args.steps for k, v in kt.items()},

@@ -21,6 +21,10 @@ def main():
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
     acc = collections.defaultdict(list)
+    pct = collections.defaultdict(lambda: collections.defaultdict(list))
+    extra = {"issue_active_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
+             "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+             "achieved_occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active"}
     for r in rows[2:]:
         tot = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -28,7 +32,11 @@ def main():
             tot += float(r[i].replace(",", "")) * UNIT.get(units[i], 1)
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0].strip()
         acc[name].append(tot)
-    res = {k: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v), "source": rep.split("/")[-1]}
+        for key, metric in extra.items():
+            if metric in hdr:
+                pct[name][key].append(float(r[hdr.index(metric)].replace(",", "")))
+    res = {k: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v), "source": rep.split("/")[-1],
+               **{key: sum(x) / len(x) for key, x in pct[k].items()}}
            for k, v in acc.items()}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
