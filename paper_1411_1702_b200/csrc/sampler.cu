@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c) {
 // S3: exact per-element CDF (from the S2 per-thread handoff: no block
 // scans), per-tile local guide and the coarse guide.
 template <int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_scan_cdf(Ctx c) {
+__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx c) {
   using TC = TileCfg<ITEMS>;
   __shared__ double sg[TC::kSmem];
   if (grid_error(c)) return;
