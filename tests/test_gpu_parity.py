@@ -459,6 +459,34 @@ def test_run_matches_oracle_loop():
     gpu.close()
 
 
+def test_baseline_config1_full_run_vs_reference():
+    """BASELINE config 1 end to end: LV, N = 1024, all T = 200 observations,
+    the GPU's filter::run (one graph per step) against the unmodified
+    reference's pf_step loop (oracle/_ref), free running from the same
+    ensemble: every posterior mean / variance / ESS row within 1e-8."""
+    from oracle_ctypes import REF_SO, Reference
+    from paper_1411_1702_b200 import problems
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    R = Reference()
+    n, T = 1024, 200
+    prob = problems.lotka_volterra(particles=n, T=T, seed=1)
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=1, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 1, **prob.prior)
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    rows = gpu.run(prob.ys, prob.times)
+    tp, worst = 0.0, 0.0
+    for j in range(1, T + 1):
+        trace_r = R.pf_step(sc, ens, prob.ys[j - 1], j, tp, prob.times[j - 1])
+        r = rows[j]
+        tr = np.concatenate([r.theta_mean, r.theta_var, r.state_mean, [r.ess]])
+        worst = max(worst, _rel(tr, trace_r))
+        assert worst < REL_TRACE, (j, worst)
+        tp = prob.times[j - 1]
+    gpu.close()
+
+
 def test_cpp_drop_in_example_matches_oracle():
     """The C++ mirror (include/pfsmc_gpu.hpp) used as a pf_step call-site
     replacement: trace rows agree with the oracle run from the same prior."""
