@@ -334,8 +334,16 @@ def run_sharded(args, world, rank, local):
     shard = GpuShard("lv", prob.cfg, prob.obs, rank, world, device=local)
     f = ShardedFilter([shard], TorchComm())
     f.initialize_uniform(**prob.prior)
+    migration = "python-orchestrated, NCCL send/recv"
     if not args.python_sharded:
         shard.attach_nccl()   # the native step: one C-ABI call per observation
+        migration = "native step, NCCL send/recv"
+        if not args.nccl_exchange:
+            try:
+                if shard.attach_peers():
+                    migration = "native step, pull over NVLink peer memory"
+            except Exception:
+                pass
     stream = shard.stream()
     j, tp = 0, 0.0
     for _ in range(args.warmup):
@@ -374,7 +382,7 @@ def run_sharded(args, world, rank, local):
                        "global_particles": n_local * world, "h": 0.1, "shrink_a": 0.98,
                        "integrator": "am2 (m=1)", "l2": "flushed between timed steps",
                        "parallelism": f"sharded x{world}: one global filter, NCCL allgathers + exact-mode "
-                                      "ancestor migration"},
+                                      f"ancestor migration ({migration})"},
             "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": step_gbs / hbm, "traffic": None, "bytes_per_particle": STEP_BYTES,
                          "peak_source": peak_kind},
@@ -402,6 +410,8 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
     ap.add_argument("--python-sharded", action="store_true",
                     help="sharded path orchestrated phase by phase from Python (default: native NCCL step)")
+    ap.add_argument("--nccl-exchange", action="store_true",
+                    help="migrate with counted NCCL send/recv instead of the peer-memory pull")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded path (NCCL collectives + migration) even at N = 1 (a check of that path)")
     ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")

@@ -236,6 +236,13 @@ pfsmc_gpu_status pfsmc_gpu_nccl_unique_id(uint8_t* out128);
 pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t* id128);
 pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
                                       double t_obs, double h, double* trace_out);
+/* Migration over NVLink peer memory (replaces the counted send/recv and its
+ * host sync inside pfsmc_gpu_shard_step): each rank exports 6 CUDA IPC handles
+ * (6 x 64 bytes: its record buffers, ll_bar, exact CDF, segment ends, guide),
+ * the caller allgathers them (world x 384 bytes, rank order) and every rank
+ * attaches; then each slot pulls its ancestor from the serving rank's memory. */
+pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out384);
+pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */

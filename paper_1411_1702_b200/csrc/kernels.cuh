@@ -406,6 +406,43 @@ __device__ __forceinline__ long long find_segment(const Ctx& c, double u) {
   return lo;
 }
 
+// The search tables of one shard, possibly on a peer GPU (NVLink peer memory).
+struct SearchView {
+  const unsigned* coarse;
+  const double* seg_end;
+  const double* cdf;
+  double end;  // the shard's exact CDF end (its last tile's end)
+};
+
+// find_segment + the segment count over an explicit view (scalar form).
+__device__ __forceinline__ unsigned find_ancestor_view(const Ctx& c, const SearchView& v, double u) {
+  constexpr int seg_log2 = kSegLog2;
+  const long long nseg = (static_cast<long long>(c.N) + (1 << seg_log2) - 1) >> seg_log2;
+  const long long nb = 1LL << c.coarse_bits;
+  long long b = static_cast<long long>(scale2(u, c.coarse_bits));
+  b = min(max(b, 0LL), nb - 1);
+  long long lo = __ldcg(&v.coarse[b]);
+  long long hi = nseg - 1;
+  if (b + 1 < nb) {
+    const double edge = scale2(static_cast<double>(b + 1), -c.coarse_bits);
+    if (edge < v.end) hi = min(hi, static_cast<long long>(__ldcg(&v.coarse[b + 1])));
+  }
+  lo = min(lo, hi);
+  while (hi - lo > 4) {
+    const long long mid = (lo + hi) >> 1;
+    if (__ldcg(&v.seg_end[mid]) > u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  while (lo < hi && __ldcg(&v.seg_end[lo]) <= u) ++lo;
+  const long long k0 = lo << seg_log2;
+  const long long k1 = min(k0 + (1LL << seg_log2), static_cast<long long>(c.N));
+  int cnt = 0;
+  for (long long k = k0; k < k1; ++k) cnt += __ldcg(&v.cdf[k]) <= u;
+  return static_cast<unsigned>(min(k0 + cnt, static_cast<long long>(c.N) - 1));
+}
+
 // Scalar form (one thread, one slot).
 __device__ __forceinline__ unsigned find_ancestor(const Ctx& c, double u) {
   constexpr int seg_log2 = kSegLog2;

@@ -963,6 +963,41 @@ __global__ void __launch_bounds__(kThreads) k_place(Ctx c, const double* recvbuf
 
 // Global approximate offset of this shard (rank order) from the allgathered
 // (sum, count) pairs.
+// Every rank's search tables and records, as seen from this GPU: local
+// pointers for itself, CUDA IPC mappings (NVLink peer memory) for the others.
+constexpr int kMaxRanks = 8;
+struct PeerTable {
+  const double* rec0[kMaxRanks];
+  const double* rec1[kMaxRanks];
+  const double* llbar[kMaxRanks];
+  const double* cdf[kMaxRanks];
+  const double* seg_end[kMaxRanks];
+  const unsigned* coarse[kMaxRanks];
+};
+
+// The migration as one pull kernel over peer memory (no count exchange, no
+// host sync): slot n's uniform, its serving rank from the exact global shard
+// ranges, the exact search in that rank's CDF tables and the gather of that
+// rank's record and ll_bar straight into this rank's slot-ordered payload.
+__global__ void __launch_bounds__(kThreads) k_pull(Ctx c, PeerTable pt) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const double u = resample_uniform(c.seed, c.sp->j, c.n0 + n);
+  const int r = serving_rank(c, u);
+  const int ntl = c.ntiles;
+  SearchView v{pt.coarse[r], pt.seg_end[r], pt.cdf[r], c.gtile_info[(r + 1) * ntl - 1].y};
+  const unsigned a = find_ancestor_view(c, v, u);
+  const double* rec = (c.st->cur ? pt.rec1[r] : pt.rec0[r]) + static_cast<long long>(a) * c.R;
+  const int H = c.R / 2;
+  const double2* src = reinterpret_cast<const double2*>(rec);
+  double2* dst = reinterpret_cast<double2*>(c.payload + n * (c.R + 2));
+  for (int i = 0; i < H; ++i) dst[i] = __ldcg(src + i);
+  const long long ga = static_cast<long long>(r) * c.N + a;
+  dst[H] = make_double2(__ldcg(&pt.llbar[r][a]), static_cast<double>(ga));
+  c.anc[n] = static_cast<unsigned>(ga);
+}
+
 __global__ void k_shard_offset(Ctx c, const double* gathered) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0, n = 0.0;
@@ -1310,6 +1345,9 @@ struct pfsmc_gpu_sampler {
   int rank = 0, world = 1;
   bool shard_api = false;  // created by pfsmc_gpu_create_shard
   ncclComm_t nccl = nullptr;  // pfsmc_gpu_shard_attach_nccl (native sharded step)
+  PeerTable peers{};          // pfsmc_gpu_shard_attach_peers (migration over peer memory)
+  bool have_peers = false;
+  std::vector<void*> ipc_opened;
   int ngroups_pred = 0, ngroups_upd = 0;
   double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
   double* gp_mom_all = nullptr;    // allgathered K3 group partials (world * ngroups * W)
@@ -1329,6 +1367,7 @@ struct pfsmc_gpu_sampler {
   }
   ~pfsmc_gpu_sampler() {
     if (nccl) nccl_api().CommDestroy(nccl);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -2136,6 +2175,61 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t
   });
 }
 
+// ---- migration over NVLink peer memory --------------------------------------
+// The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
+// segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
+constexpr int kPeerBufs = 6;
+
+pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    const Ctx& c = s->ctx;
+    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse};
+    for (int i = 0; i < kPeerBufs; ++i) {
+      cudaIpcMemHandle_t h;
+      CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
+      std::memcpy(out + i * sizeof(h), &h, sizeof(h));
+    }
+    return PFSMC_GPU_OK;
+  });
+}
+
+// all_handles: world x kPeerBufs IPC handles in rank order (this rank's own
+// entry is ignored: local pointers).
+pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (s->world > kMaxRanks) throw ConfigError("attach_peers: at most 8 ranks");
+    CK(cudaSetDevice(s->cfg.device));
+    const Ctx& c = s->ctx;
+    PeerTable t{};
+    for (int r = 0; r < s->world; ++r) {
+      const void* p[kPeerBufs];
+      if (r == s->rank) {
+        p[0] = c.rec[0], p[1] = c.rec[1], p[2] = c.llbar, p[3] = c.cdf, p[4] = c.seg_end, p[5] = c.coarse;
+      } else {
+        for (int i = 0; i < kPeerBufs; ++i) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, all_handles + (static_cast<size_t>(r) * kPeerBufs + i) * sizeof(h), sizeof(h));
+          void* q = nullptr;
+          CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+          s->ipc_opened.push_back(q);
+          p[i] = q;
+        }
+      }
+      t.rec0[r] = static_cast<const double*>(p[0]);
+      t.rec1[r] = static_cast<const double*>(p[1]);
+      t.llbar[r] = static_cast<const double*>(p[2]);
+      t.cdf[r] = static_cast<const double*>(p[3]);
+      t.seg_end[r] = static_cast<const double*>(p[4]);
+      t.coarse[r] = static_cast<const unsigned*>(p[5]);
+    }
+    s->peers = t;
+    s->have_peers = true;
+    return PFSMC_GPU_OK;
+  });
+}
+
 // One pf_step of the global filter: the five exchanges as NCCL
 // collectives on the sampler stream between the phase kernels, host syncs
 // only where the host needs data (the migration counts, the trace row).
@@ -2162,6 +2256,19 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
     launch_scan(c, s->ntiles, st, 5);
     launch_scan(c, s->ntiles, st, 2);
     CK(cudaGetLastError());
+    if (s->have_peers) {
+      // D over peer memory: every rank's CDF tables are complete once every rank
+      // has reached this point (a 2-double allgather orders it on the streams);
+      // peers overwrite what was read only after the next collectives (E, A).
+      NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
+      k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
+      s->ks->update(c, s->grid, st);
+      const size_t Wm = static_cast<size_t>(s->ks->moment_width());
+      NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
+      CK(cudaGetLastError());
+      shard_finish_moments_impl(s, 7, trace_out);
+      return PFSMC_GPU_OK;
+    }
     // D: exact-mode migration; the counts are the locally derived matrix
     std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
     shard_serve_impl(s, cnt.data());

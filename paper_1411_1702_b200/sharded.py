@@ -135,6 +135,28 @@ class GpuShard(GpuSampler):
         self._check(self.lib.pfsmc_gpu_shard_attach_nccl(self.h, uid.ctypes.data_as(C.POINTER(C.c_uint8))))
         self.native = True
 
+    def attach_peers(self, comm_group=None) -> bool:
+        """Migration over NVLink peer memory: allgather every rank's CUDA IPC
+        handles (6 x 64 bytes) and map the peers' search tables and records.
+        Returns False (the counted send / receive stays in use) if the mapping
+        fails on any rank."""
+        import torch
+        import torch.distributed as dist
+        L = self.lib
+        L.pfsmc_gpu_shard_ipc_handles.restype = C.c_int
+        L.pfsmc_gpu_shard_attach_peers.restype = C.c_int
+        mine = np.zeros(384, dtype=np.uint8)
+        self._check(L.pfsmc_gpu_shard_ipc_handles(self.h, mine.ctypes.data_as(C.POINTER(C.c_uint8))))
+        dev = f"cuda:{self.device}"
+        allh = torch.zeros(384 * self.world, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(allh, torch.from_numpy(mine).to(dev), group=comm_group)
+        allh = allh.cpu().numpy()
+        rc = L.pfsmc_gpu_shard_attach_peers(self.h, allh.ctypes.data_as(C.POINTER(C.c_uint8)))
+        ok = torch.tensor([1 if rc == 0 else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=comm_group)
+        self.peers = bool(ok.item())
+        return self.peers
+
     def native_step(self, y, j, t_prev, t_obs, h) -> np.ndarray:
         out = np.zeros(self.row_width)
         y = _f64(y)

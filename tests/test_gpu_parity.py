@@ -611,24 +611,34 @@ def test_sharded_torchcomm_nccl_world1_bitwise():
         f2 = ShardedFilter([shard2], TorchComm())
         f2.initialize_uniform(**prob.prior)
         shard2.attach_nccl()
+        shard3 = GpuShard("lv", prob.cfg, prob.obs, 0, 1)   # native, migration pulled over peer memory
+        f3 = ShardedFilter([shard3], TorchComm())
+        f3.initialize_uniform(**prob.prior)
+        shard3.attach_nccl()
+        assert shard3.attach_peers()
         tp = 0.0
         for j in range(1, T + 1):
             t1 = prob.times[j - 1]
             r1 = single.pf_step(prob.ys[j - 1], j, tp, t1)
             r2 = f.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
             r3 = f2.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
+            r4 = f3.pf_step(prob.ys[j - 1], j, tp, t1, 0.1)
             assert np.array_equal(single.step_diagnostics()[0], f.ancestors()), j
             assert np.array_equal(single.step_diagnostics()[0], f2.ancestors()), j
+            assert np.array_equal(single.step_diagnostics()[0], f3.ancestors()), j
+            assert np.array_equal(r1.theta_mean, r4.theta_mean) and r1.ess == r4.ess, j
             assert np.array_equal(r1.theta_mean, r2.theta_mean) and r1.ess == r2.ess, j
             assert np.array_equal(r1.theta_mean, r3.theta_mean) and r1.ess == r3.ess, j
             tp = t1
-        e1, e2, e3 = single.get_ensemble(), f.get_ensemble(), f2.get_ensemble()
+        e1, e2, e3, e4 = single.get_ensemble(), f.get_ensemble(), f2.get_ensemble(), f3.get_ensemble()
         for name in ("states", "params_u", "logw", "mean_u", "cov_u"):
             assert np.array_equal(getattr(e1, name), getattr(e2, name)), name
             assert np.array_equal(getattr(e1, name), getattr(e3, name)), name
+            assert np.array_equal(getattr(e1, name), getattr(e4, name)), name
         single.close()
         shard.close()
         shard2.close()
+        shard3.close()
     finally:
         dist.destroy_process_group()
 
