@@ -1347,6 +1347,8 @@ struct pfsmc_gpu_sampler {
   ncclComm_t nccl = nullptr;  // pfsmc_gpu_shard_attach_nccl (native sharded step)
   PeerTable peers{};          // pfsmc_gpu_shard_attach_peers (migration over peer memory)
   bool have_peers = false;
+  cudaGraphExec_t shard_graph = nullptr;  // the peer-memory step (graph with NCCL nodes)
+  bool shard_graph_refused = false;
   std::vector<void*> ipc_opened;
   int ngroups_pred = 0, ngroups_upd = 0;
   double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
@@ -1366,6 +1368,7 @@ struct pfsmc_gpu_sampler {
     return static_cast<T*>(p);
   }
   ~pfsmc_gpu_sampler() {
+    if (shard_graph) cudaGraphExecDestroy(shard_graph);
     if (nccl) nccl_api().CommDestroy(nccl);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (graph) cudaGraphExecDestroy(graph);
@@ -2230,6 +2233,77 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
   });
 }
 
+// The device part of one peer-memory sharded step (everything between the
+// step-parameter upload and the DevState read-back), for eager launch or
+// capture into a CUDA graph (NCCL collectives capture).
+static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
+  const NcclApi& N = nccl_api();
+  const Ctx& c = s->ctx;
+  cudaStream_t st = s->stream;
+  const int W = s->world;
+  enqueue_prologue(s);
+  s->ks->predict(c, s->grid, st);
+  NCK(N.AllGather(c.gpart, s->gp_pred_all, 2 * static_cast<size_t>(s->ngroups_pred), ncclDouble, s->nccl, st));
+  k_finish_lse<<<1, kThreads, 0, st>>>(c, s->gp_pred_all, s->ngroups_pred * W);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
+  k_shard_offset<<<1, 32, 0, st>>>(c, s->sums_all);
+  launch_scan(c, s->ntiles, st, 4);
+  NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));
+  NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8,
+                  s->nccl, st));
+  launch_scan(c, s->ntiles, st, 5);
+  launch_scan(c, s->ntiles, st, 2);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete everywhere
+  k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
+  s->ks->update(c, s->grid, st);
+  const size_t Wm = static_cast<size_t>(s->ks->moment_width());
+  NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
+  s->ks->finish_moments(c, s->gp_mom_all, s->ngroups_upd * W, 7, st);
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+}
+
+// The peer-memory step: one CUDA graph per step (built on first use; eager
+// launches if capture is refused), one host sync for the trace row.
+static void shard_pull_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
+                            double h, double* trace_out) {
+  if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
+  CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
+  *s->sp_host = sp;
+  CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+  if (!s->shard_graph && !s->shard_graph_refused) {
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        enqueue_shard_pull_step(s);
+      } catch (const std::exception&) {
+        ok = false;
+      }
+      const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+      ok = ok && e == cudaSuccess && g != nullptr &&
+           cudaGraphInstantiate(&s->shard_graph, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    if (!ok) {
+      s->shard_graph = nullptr;
+      s->shard_graph_refused = true;
+      cudaGetLastError();  // clear
+    }
+  }
+  if (s->shard_graph)
+    CK(cudaGraphLaunch(s->shard_graph, s->stream));
+  else
+    enqueue_shard_pull_step(s);
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaGetLastError());
+  check_error(s);
+  if (trace_out) {
+    const int n = 2 * s->p + s->d + 1;
+    for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
+  }
+}
+
 // One pf_step of the global filter: the five exchanges as NCCL
 // collectives on the sampler stream between the phase kernels, host syncs
 // only where the host needs data (the migration counts, the trace row).
@@ -2237,6 +2311,10 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
                                       double t_obs, double h, double* trace_out) {
   return guarded([&] {
     if (!s->nccl) throw ConfigError("shard_step: no NCCL communicator (pfsmc_gpu_shard_attach_nccl)");
+    if (s->have_peers) {
+      shard_pull_step(s, y, j, t_prev, t_obs, h, trace_out);
+      return PFSMC_GPU_OK;
+    }
     const NcclApi& N = nccl_api();
     const Ctx& c = s->ctx;
     cudaStream_t st = s->stream;
@@ -2256,19 +2334,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
     launch_scan(c, s->ntiles, st, 5);
     launch_scan(c, s->ntiles, st, 2);
     CK(cudaGetLastError());
-    if (s->have_peers) {
-      // D over peer memory: every rank's CDF tables are complete once every rank
-      // has reached this point (a 2-double allgather orders it on the streams);
-      // peers overwrite what was read only after the next collectives (E, A).
-      NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
-      k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
-      s->ks->update(c, s->grid, st);
-      const size_t Wm = static_cast<size_t>(s->ks->moment_width());
-      NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
-      CK(cudaGetLastError());
-      shard_finish_moments_impl(s, 7, trace_out);
-      return PFSMC_GPU_OK;
-    }
+
     // D: exact-mode migration; the counts are the locally derived matrix
     std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
     shard_serve_impl(s, cnt.data());
