@@ -1,0 +1,328 @@
+// BASELINE config 5 (resample / reduction bandwidth microbenchmark on 64-byte
+// records) and the measured-peak helpers (FP64 DFMA, random gather), plus the
+// truth-trajectory entry point of the data generator.
+#include "sampler_internal.cuh"
+
+namespace pfsmc_gpu {
+
+// ---- BASELINE config 5: resample / reduction bandwidth microbenchmark ----
+// One iteration over the resident 64-byte records {x[4], h[2], theta[2]}:
+// log-sum-exp of lw (+ the exact scan's tile offsets), the weighted 2x2
+// parameter covariance, the exact multinomial resampling and the gather of
+// the ancestors' records into the next buffer.
+__global__ void __launch_bounds__(kThreads) k_c5_weights(Ctx c, double sigma, unsigned long long key) {
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  double z[1];
+  stream_normals<1>(c.seed, key, c.n0 + n, kInit, z);
+  c.lw[n] = sigma * z[0];
+}
+
+// One pass over the resident particles computes everything the iteration
+// reduces: the log-sum-exp of lw, the weighted 2x2 parameter covariance
+// (weighted_mean_cov, linalg.cpp:389-432, about the previous mean) and the
+// exact scan's tile offsets. A grid of a few blocks per SM loops over the
+// exact-CDF tiles; each thread's ITEMS (lw, theta) loads are all in flight
+// before the tile's partial: M_t = max lw, then sums of e = exp(lw - M_t)
+// times (1, d0, d1, d0 d0, d0 d1, d1 d1) and the finite count. The block
+// folds its tiles in order (combine_partials' rescaling rule); the last block
+// combines the block partials in a fixed order. Bitwise reproducible.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
+  constexpr int kTileT = ITEMS * kThreads;
+  constexpr int V = 7;  // S, A0, A1, B00, B01, B11, finite count
+  __shared__ double scratch[kWarps * V];
+  __shared__ double fin[V];
+  __shared__ int s_last;
+  if (grid_error(c)) return;
+  DevState& st = *c.st;
+  const double k0 = st.mu[0], k1 = st.mu[1];
+  const double* rec = c.rec[st.cur];
+  for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+    const long long base = static_cast<long long>(t) * kTileT;
+    double x[ITEMS];
+    double2 th[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const long long k = base + i * kThreads + threadIdx.x;
+      x[i] = k < c.N ? __ldcs(&c.lw[k]) : -INFINITY;
+      th[i] = k < c.N ? __ldcs(reinterpret_cast<const double2*>(rec + k * c.R + 6)) : make_double2(0.0, 0.0);
+    }
+    double m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (!isnan(x[i])) m = nan_free_max(m, x[i]);
+    const double M = block_max(m, scratch);
+    double v[V] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const double e = isnan(x[i]) ? NAN : (x[i] == -INFINITY ? 0.0 : exp(x[i] - M));
+      const double d0 = th[i].x - k0, d1 = th[i].y - k1;
+      v[0] += e;
+      v[1] += e * d0;
+      v[2] += e * d1;
+      v[3] += e * (d0 * d0);
+      v[4] += e * (d0 * d1);
+      v[5] += e * (d1 * d1);
+      v[6] += isfinite(x[i]) ? 1.0 : 0.0;
+    }
+    block_sums<V>(v, scratch);
+    if (threadIdx.x == 0) {
+      double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;  // per-tile partial (after the block slots)
+      tp[0] = M;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) tp[1 + k] = v[k];
+      c.trel[t] = v[0];
+      c.tile_m[t] = M;
+      c.tile_cnt_pre[t] = static_cast<long long>(v[6]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    // this block's partial over its tiles, in tile order
+    double M = -INFINITY;
+    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) M = nan_free_max(M, c.tile_m[t]);
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+      const double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;
+      const double w = tp[0] == -INFINITY ? 0.0 : exp(tp[0] - M);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) acc[k] += w * tp[1 + k];
+    }
+    double* bp = c.part + static_cast<size_t>(blockIdx.x) * V;
+    bp[0] = M;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) bp[1 + k] = acc[k];
+    __threadfence();
+    const unsigned old = atomicAdd(&c.cnt_scan[3], 1u);
+    s_last = (old == gridDim.x - 1);
+    if (s_last) c.cnt_scan[3] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  combine_partials<6, false>(c.part, gridDim.x, fin, scratch);
+  __syncthreads();
+  __shared__ double s_lse;
+  if (threadIdx.x == 0) {
+    const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
+    st.lse_g = lse;
+    if (!isfinite(lse)) atomicOr(&st.error, kErrPredict);
+    s_lse = lse;
+    const double S = fin[1];
+    const double m0 = fin[2] / S, m1 = fin[3] / S;
+    st.mu[0] = k0 + m0;
+    st.mu[1] = k1 + m1;
+    st.cov[0] = fin[4] / S - m0 * m0;
+    st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
+    st.cov[3] = fin[6] / S - m1 * m1;
+  }
+  __syncthreads();
+  if (isfinite(s_lse)) tile_prefixes(c, s_lse, c.tile_m);
+}
+
+// Survival of the fittest straight into the next record buffer (64-byte
+// records: four lanes per record, eight records per load instruction).
+__global__ void __launch_bounds__(kThreads) k_c5_serve(Ctx c, unsigned long long j) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const double u = n < c.N ? resample_uniform(c.seed, j, c.n0 + n) : -1.0;
+  const unsigned a = find_ancestor_warp(c, u);
+  if (n < c.N) c.anc[n] = a;
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const int cur = c.st->cur;
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur]);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+  const uint64_t pol = l2_policy_stream();
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const long long ns = wbase + slot;
+    if (ns < c.N) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
+}
+
+__global__ void k_flip(DevState* st) { st->cur ^= 1; }
+
+// FP64 roofline denominator: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(kThreads) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += x[i];
+  if (acc == 12345.678) out[0] = acc;  // keeps the chains live
+}
+
+// Random-gather roofline: dst[n] = src[h(n)] for 64-byte records, h a
+// bijective-free integer hash (splitmix64) — the same access shape as the
+// resampling gather, without the search. Same warp-cooperative layout.
+__global__ void __launch_bounds__(kThreads) k_gather_peak(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                          long long n_rec) {
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  uint64_t z = static_cast<uint64_t>(n) + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  const unsigned a = static_cast<unsigned>(z % static_cast<uint64_t>(n_rec));
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const uint64_t pol = l2_policy_stream();
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const long long ns = wbase + slot;
+    if (ns < n_rec) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
+}
+
+}  // namespace pfsmc_gpu
+
+extern "C" {
+
+// ---- BASELINE config 5 microbenchmark entry points (model PAYLOAD64) -----
+pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key) {
+  return guarded([&] {
+    if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    k_c5_weights<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, sigma, key);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// One resample/reduction iteration (enqueue only): LSE + tile offsets, the
+// weighted 2x2 covariance, the exact CDF, the ancestor search and gather.
+pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
+  return guarded([&] {
+    if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    Ctx c = s->ctx;
+    c.lg = c.lw;  // the fitness log-weights are the log-weights here
+    CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
+    // one wave: 126 (ITEMS 16) / 74 (ITEMS 8) registers => 2 / 3 blocks per SM
+    if (c.tile_log2 == 11)
+      k_c5_stats<8><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
+    else
+      k_c5_stats<16><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
+    launch_scan(c, s->ntiles, s->stream, 1);
+    launch_scan(c, s->ntiles, s->stream, 2);
+    k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
+    k_flip<<<1, 1, 0, s->stream>>>(s->st);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+
+// Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA).
+pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* out;
+    CK(cudaMalloc(&out, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8, iters = 4096;
+    k_dfma_peak<<<blocks, kThreads>>>(out, 256, 0.999999, 1e-7);  // warm-up
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, kThreads>>>(out, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *tflops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * kThreads / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return PFSMC_GPU_OK;
+  });
+}
+
+// One noise-free trajectory of a compiled-in model through the observation
+// times with the adaptive BDF(1,2) integrator (the data generator's truth
+// path, bench.cpp:296-317 with lmm::adaptive_bdf_interval). Blocking.
+pfsmc_gpu_status pfsmc_gpu_model_trajectory(int model, const double* model_consts, const double* theta_nat,
+                                            const double* x0, const double* times, uint64_t T, double t0,
+                                            double rtol, int device, double* states_out) {
+  return guarded([&] {
+    auto ks = make_kernels(model, PFSMC_GPU_BDF, 0);
+    if (!ks) throw ConfigError("unknown model id");
+    if (!(rtol > 0.0)) throw ConfigError("adaptive_bdf_interval: rtol must be positive");
+    if (T == 0) return PFSMC_GPU_OK;
+    double tp = t0;
+    for (uint64_t r = 0; r < T; ++r) {
+      if (!(times[r] > tp)) throw ConfigError("adaptive_bdf_interval: need t1 > t0");
+      tp = times[r];
+    }
+    if (model == MetabolicModel::ID && !(model_consts[5] > 0.0))
+      throw ConfigError("metabolic model: tau must be positive");
+    CK(cudaSetDevice(device));
+    const int d = ks->d, p = ks->p;
+    std::vector<double> prm(8 + p + d);
+    for (int k = 0; k < 8; ++k) prm[k] = model_consts ? model_consts[k] : 0.0;
+    for (int k = 0; k < p; ++k) prm[8 + k] = theta_nat[k];
+    for (int k = 0; k < d; ++k) prm[8 + p + k] = x0[k];
+    double *dprm, *dt, *dout;
+    int* dst;
+    CK(cudaMalloc(&dprm, sizeof(double) * prm.size()));
+    CK(cudaMalloc(&dt, sizeof(double) * T));
+    CK(cudaMalloc(&dout, sizeof(double) * T * d));
+    CK(cudaMalloc(&dst, sizeof(int)));
+    CK(cudaMemcpy(dprm, prm.data(), sizeof(double) * prm.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dt, times, sizeof(double) * T, cudaMemcpyHostToDevice));
+    ks->trajectory(dprm, dt, static_cast<int>(T), t0, rtol, 1e-9, 20, dout, dst, nullptr);  // NewtonOpts{}
+    CK(cudaGetLastError());
+    int st = 0;
+    CK(cudaMemcpy(&st, dst, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(states_out, dout, sizeof(double) * T * d, cudaMemcpyDeviceToHost));
+    cudaFree(dprm);
+    cudaFree(dt);
+    cudaFree(dout);
+    cudaFree(dst);
+    if (st != 0) throw NumericalError("reference trajectory integration failed (stiffness)");
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Measured random 64-byte-record gather throughput (GB/s of record bytes
+// read + written), over n_rec records (> L2), median-free: best of 5.
+pfsmc_gpu_status pfsmc_gpu_gather_peak(int device, long long n_rec, double* gbs) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    double2 *src, *dst;
+    CK(cudaMalloc(&src, static_cast<size_t>(n_rec) * 64));
+    CK(cudaMalloc(&dst, static_cast<size_t>(n_rec) * 64));
+    CK(cudaMemset(src, 0, static_cast<size_t>(n_rec) * 64));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = static_cast<int>((n_rec + kThreads - 1) / kThreads);
+    float best = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      CK(cudaEventRecord(e0));
+      k_gather_peak<<<blocks, kThreads>>>(src, dst, n_rec);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r > 0) best = std::min(best, ms);
+    }
+    *gbs = 128.0 * static_cast<double>(n_rec) / (best * 1e-3) / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(src);
+    cudaFree(dst);
+    return PFSMC_GPU_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// Host-side internals shared by the translation units of libpfsmc_gpu.so:
+// the sampler handle, the error / status plumbing, the cross-unit launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>  // types only: NCCL is bound at run time (dlopen), see NcclApi
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace pfsmc_gpu {
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " + \
+                               #x);                                                      \
+  } while (0)
+
+inline constexpr const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_serve,k_update";
+constexpr int kNumKernels = 5;
+
+
+constexpr int kShardPW = 4;  // extra doubles of a migration payload beyond the record
+
+// Every rank's search tables and records, as seen from this GPU: local
+// pointers for itself, CUDA IPC mappings (NVLink peer memory) for the others.
+constexpr int kMaxRanks = 8;
+struct PeerTable {
+  const double* rec0[kMaxRanks];
+  const double* rec1[kMaxRanks];
+  const double* llbar[kMaxRanks];
+  const double* cdf[kMaxRanks];
+  const double* seg_end[kMaxRanks];
+  const unsigned* coarse[kMaxRanks];
+};
+
+// launchers of kernels that live in another unit (scan.cu)
+void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which);
+void launch_serve(const Ctx& c, int grid, cudaStream_t st);
+void launch_gin(const Ctx& c, int ntiles, cudaStream_t st);
+void launch_search_only(const Ctx& c, int grid, cudaStream_t st);
+
+}  // namespace pfsmc_gpu
+
+using namespace pfsmc_gpu;
+
+// NCCL bound at run time: the process's already-loaded libnccl.so.2 (torch's)
+// when there is one, so one NCCL instance serves both; nothing links it.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api();
+void NCK(ncclResult_t r);
+
+struct pfsmc_gpu_sampler {
+  pfsmc_gpu_config cfg{};
+  std::vector<uint64_t> obs;
+  std::unique_ptr<KernelSet> ks;
+  int d = 0, p = 0;
+  long long N = 0;
+  int grid = 0, ntiles = 0;
+  int num_sms = 148;
+  Ctx ctx{};
+  cudaStream_t stream = nullptr;
+  // device buffers
+  std::vector<void*> allocs;
+  DevState* st = nullptr;
+  StepParams* sp_dev = nullptr;
+  StepParams* sp_host = nullptr;     // pinned
+  double* trace_host = nullptr;      // pinned
+  DevState* st_host = nullptr;       // pinned
+  double* flush_buf = nullptr;
+  long long flush_n = 0;
+  // resident observations
+  std::vector<StepParams> resident;
+  StepParams* resident_dev = nullptr;
+  double t0_resident = 0.0;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[kNumKernels + 1] = {};
+  double kernel_ms[kNumKernels] = {};
+  std::vector<cudaEvent_t> pending;  // (kNumKernels+1) per timed step
+  bool have_ensemble = false;
+  // sharding (pfsmc_gpu_create_shard)
+  int rank = 0, world = 1;
+  bool shard_api = false;  // created by pfsmc_gpu_create_shard
+  ncclComm_t nccl = nullptr;  // pfsmc_gpu_shard_attach_nccl (native sharded step)
+  PeerTable peers{};          // pfsmc_gpu_shard_attach_peers (migration over peer memory)
+  bool have_peers = false;
+  cudaGraphExec_t shard_graph = nullptr;  // the peer-memory step (graph with NCCL nodes)
+  bool shard_graph_refused = false;
+  std::vector<void*> ipc_opened;
+  int ngroups_pred = 0, ngroups_upd = 0;
+  double* gp_pred_all = nullptr;   // allgathered K1 group partials (world * ngroups * 2)
+  double* gp_mom_all = nullptr;    // allgathered K3 group partials (world * ngroups * W)
+  double* sums_all = nullptr;      // allgathered shard (sum, count) pairs
+  double* sendbuf = nullptr;       // world * N_local payloads
+  double* recvbuf = nullptr;       // N_local payloads
+  unsigned* counts_dev = nullptr;  // [world] send + [world] recv
+  unsigned* counts_all = nullptr;  // the W x W migration count matrix (k_serve_sharded)
+  unsigned* counts_host = nullptr; // pinned mirror
+
+  template <typename T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~pfsmc_gpu_sampler() {
+    if (shard_graph) cudaGraphExecDestroy(shard_graph);
+    if (nccl) nccl_api().CommDestroy(nccl);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : pending) cudaEventDestroy(e);
+    for (void* a : allocs) cudaFree(a);
+    if (sp_host) cudaFreeHost(sp_host);
+    if (trace_host) cudaFreeHost(trace_host);
+    if (st_host) cudaFreeHost(st_host);
+    if (counts_host) cudaFreeHost(counts_host);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+
+// ---- status plumbing (sampler.cu) ----
+extern thread_local std::string g_last_error;
+
+
+template <typename F>
+pfsmc_gpu_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const ConfigError& e) {
+    g_last_error = e.what();
+    return PFSMC_GPU_ERR_CONFIG;
+  } catch (const NumericalError& e) {
+    g_last_error = e.what();
+    return PFSMC_GPU_ERR_NUMERICAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PFSMC_GPU_ERR_INTERNAL;
+  }
+}
+
+int step_count(double t0, double t1, double h);
+StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs, double h);
+void check_error(pfsmc_gpu_sampler* s);
+void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed);
+void enqueue_prologue(pfsmc_gpu_sampler* s);
+void build_graph(pfsmc_gpu_sampler* s);
+void harvest_timing(pfsmc_gpu_sampler* s);
+void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp);

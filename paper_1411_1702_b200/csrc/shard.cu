@@ -1,0 +1,553 @@
+// One global filter sharded over GPUs: the sharded kernels,
+// NCCL bound at run time, the phase-by-phase C ABI, the native step with the
+// counted NCCL exchange or the pull over NVLink peer memory.
+#include <dlfcn.h>
+
+#include "sampler_internal.cuh"
+
+namespace pfsmc_gpu {
+
+__global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp, int ngroups) {
+  __shared__ double scratch[kWarps * 2];
+  __shared__ double fin[2];
+  if (grid_error(c)) return;
+  __shared__ double s_lse;
+  combine_partials<1, false>(gp, ngroups, fin, scratch);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double mx = fin[0];
+    const double lse = isfinite(mx) ? mx + log(fin[1]) : kNegInf;
+    c.st->lse_g = lse;
+    if (!isfinite(lse)) atomicOr(&c.st->error, kErrPredict);
+    s_lse = lse;
+  }
+  __syncthreads();
+  // local tile prefixes + this shard's total (allgathered next, phase B)
+  if (isfinite(s_lse)) tile_prefixes(c, s_lse);
+}
+
+// ---- sharded ancestor migration (pull model) ---------------------------
+// Rank r owns the exact-CDF range [start_r, end_r) of its tiles; the global
+// upper_bound(cdf, u) lands on rank r iff u is in that range. Every rank draws
+// the uniforms of ALL global slots (keyed streams: identical numbers on every
+// rank), serves those in its range from its own exact CDF, and ships
+// {record, ll_bar, ancestor, destination slot} to the slot's owner.
+
+__device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
+  const int ntl = c.ntiles;
+  for (int r = 0; r < c.world; ++r) {
+    const double lo = c.gtile_info[r * ntl].x;
+    const double hi = c.gtile_info[(r + 1) * ntl - 1].y;
+    if (u >= lo && u < hi) return r;
+  }
+  return c.world - 1;  // unreachable: the last range ends at the guarded cdf >= 1 > u
+}
+
+// Every rank walks all global slots (a warp = 32 consecutive slots, all of one
+// destination since N_local is a multiple of 16384): the slot's serving rank
+// from the allgathered exact shard ranges feeds the migration count matrix
+// (identical on every rank: cnt[r * W + d] = slots of rank d served by r;
+// one atomic per group of lanes with the same server), and the slots this
+// rank serves are searched and their payloads written (one atomic per warp).
+__global__ void __launch_bounds__(kThreads) k_serve_sharded(Ctx c, double* sendbuf, unsigned* send_cnt,
+                                                            unsigned* cnt) {
+  if (grid_error(c)) return;
+  const int W = c.R + kShardPW;
+  const long long cap = c.N;  // per destination: at most its N_local slots
+  const int lane = threadIdx.x & 31;
+  for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
+       ng += static_cast<long long>(gridDim.x) * kThreads) {
+    const double u = resample_uniform(c.seed, c.sp->j, ng);
+    const int r = serving_rank(c, u);
+    const int dest = static_cast<int>(ng / c.N);
+    const unsigned grp = __match_any_sync(0xffffffffu, r);
+    if (lane == __ffs(grp) - 1) atomicAdd(&cnt[r * c.world + dest], static_cast<unsigned>(__popc(grp)));
+    const bool mine = r == c.rank;
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    if (!m) continue;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(&send_cnt[dest], static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const unsigned pos = base + static_cast<unsigned>(__popc(m & ((1u << lane) - 1u)));
+    // warp-cooperative search (lanes not served here pass u = -1) and gather:
+    // consecutive lanes move consecutive 16-byte parts of the served payloads
+    const unsigned a = find_ancestor_warp(c, mine ? u : -1.0);
+    const int H = c.R / 2 + kShardPW / 2;  // 16-byte parts per payload
+    const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
+    for (int idx = lane; idx < 32 * H; idx += 32) {
+      const int src_lane = idx / H, part = idx - src_lane * H;
+      const unsigned as = __shfl_sync(0xffffffffu, a, src_lane);
+      const unsigned ps = __shfl_sync(0xffffffffu, pos, src_lane);
+      if (!((m >> src_lane) & 1u)) continue;
+      double2 v;
+      if (part < c.R / 2)
+        v = __ldg(rec + static_cast<long long>(as) * (c.R / 2) + part);
+      else if (part == c.R / 2)
+        v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(c.n0 + as));
+      else
+        v = make_double2(static_cast<double>(ng - lane + src_lane - dest * c.N), 0.0);
+      reinterpret_cast<double2*>(sendbuf + (dest * cap + ps) * W)[part] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_place(Ctx c, const double* recvbuf, long long count) {
+  if (grid_error(c)) return;
+  const long long i = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (i >= count) return;
+  const int W = c.R + kShardPW;
+  const double2* src = reinterpret_cast<const double2*>(recvbuf + i * W);
+  const long long slot = static_cast<long long>(recvbuf[i * W + c.R + 2]);
+  double2* dst = reinterpret_cast<double2*>(c.payload + slot * (c.R + 2));
+  for (int k = 0; k < c.R / 2 + 1; ++k) dst[k] = src[k];
+  c.anc[slot] = static_cast<unsigned>(recvbuf[i * W + c.R + 1]);
+}
+
+// Global approximate offset of this shard (rank order) from the allgathered
+// (sum, count) pairs.
+
+
+// The migration as one pull kernel over peer memory (no count exchange, no
+// host sync): slot n's uniform, its serving rank from the exact global shard
+// ranges, the exact search in that rank's CDF tables and the gather of that
+// rank's record and ll_bar straight into this rank's slot-ordered payload.
+__global__ void __launch_bounds__(kThreads) k_pull(Ctx c, PeerTable pt) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const double u = resample_uniform(c.seed, c.sp->j, c.n0 + n);
+  const int r = serving_rank(c, u);
+  const int ntl = c.ntiles;
+  SearchView v{pt.coarse[r], pt.seg_end[r], pt.cdf[r], c.gtile_info[(r + 1) * ntl - 1].y};
+  const unsigned a = find_ancestor_view(c, v, u);
+  const double* rec = (c.st->cur ? pt.rec1[r] : pt.rec0[r]) + static_cast<long long>(a) * c.R;
+  const int H = c.R / 2;
+  const double2* src = reinterpret_cast<const double2*>(rec);
+  double2* dst = reinterpret_cast<double2*>(c.payload + n * (c.R + 2));
+  for (int i = 0; i < H; ++i) dst[i] = __ldcg(src + i);
+  const long long ga = static_cast<long long>(r) * c.N + a;
+  dst[H] = make_double2(__ldcg(&pt.llbar[r][a]), static_cast<double>(ga));
+  c.anc[n] = static_cast<unsigned>(ga);
+}
+
+__global__ void k_shard_offset(Ctx c, const double* gathered) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0, n = 0.0;
+  for (int r = 0; r < c.rank; ++r) {
+    s += gathered[2 * r];
+    n += gathered[2 * r + 1];
+  }
+  c.shard_off[0] = s;
+  c.shard_off[1] = n;
+}
+
+// Injected-fitness parity path (pfsmc_gpu_resample_from_g): tile sums of
+// the given g (in place of the predict kernel's block partials), then the
+// same tile prefixes with lse = 0.
+}  // namespace pfsmc_gpu
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name)); };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Send && a.Recv && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+void NCK(ncclResult_t r) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string("nccl: ") + nccl_api().GetErrorString(r));
+}
+
+
+extern "C" {
+
+// ---------------------------------------------------------------- sharded phases
+// One handle per GPU, each owning global slots [rank*N/world, (rank+1)*N/world).
+// The host orchestrator (paper_1411_1702_b200/sharded.py) runs the phases in
+// order and performs the collectives on the exposed buffers between them.
+
+pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** ptr, uint64_t* bytes) {
+  return guarded([&] {
+    const Ctx& c = s->ctx;
+    const size_t W = static_cast<size_t>(s->ks->moment_width());
+    const size_t PW = static_cast<size_t>(c.R + kShardPW);
+    switch (which) {
+      case 0: *ptr = c.gpart; *bytes = sizeof(double) * 2 * s->ngroups_pred; break;
+      case 1: *ptr = s->gp_pred_all; *bytes = sizeof(double) * 2 * s->ngroups_pred * s->world; break;
+      case 2: *ptr = c.shard_sum; *bytes = sizeof(double) * 2; break;
+      case 3: *ptr = s->sums_all; *bytes = sizeof(double) * 2 * s->world; break;
+      case 4: *ptr = c.ghdr; *bytes = sizeof(TileHdr) * c.gntiles; break;
+      case 5: *ptr = c.gwin; *bytes = sizeof(TileWin) * static_cast<size_t>(c.gntiles) * kMaxWin; break;
+      case 6: *ptr = c.gpart; *bytes = sizeof(double) * W * s->ngroups_upd; break;
+      case 7: *ptr = s->gp_mom_all; *bytes = sizeof(double) * W * s->ngroups_upd * s->world; break;
+      case 8: *ptr = s->sendbuf; *bytes = sizeof(double) * PW * s->N * s->world; break;
+      case 9: *ptr = s->recvbuf; *bytes = sizeof(double) * PW * s->N; break;
+      case 10: *ptr = s->counts_dev; *bytes = sizeof(unsigned) * 2 * s->world; break;
+      case 11: *ptr = s->counts_all; *bytes = sizeof(unsigned) * s->world * s->world; break;
+      default: throw ConfigError("shard_buffer: unknown buffer id");
+    }
+    if (!s->shard_api && (which == 1 || which == 3 || which >= 7)) throw ConfigError("not a sharded handle");
+    return PFSMC_GPU_OK;
+  });
+}
+
+static void shard_predict_impl(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
+                               double h) {
+  if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
+  CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
+  *s->sp_host = sp;
+  CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+  enqueue_prologue(s);
+  s->ks->predict(s->ctx, s->grid, s->stream);
+  CK(cudaGetLastError());
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
+                                         double t_prev, double t_obs, double h) {
+  return guarded([&] {
+    shard_predict_impl(s, y, j, t_prev, t_obs, h);
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    k_finish_lse<<<1, kThreads, 0, s->stream>>>(s->ctx, s->gp_pred_all, s->ngroups_pred * s->world);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    k_shard_offset<<<1, 32, 0, s->stream>>>(s->ctx, s->sums_all);
+    launch_scan(s->ctx, s->ntiles, s->stream, 4);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    launch_scan(s->ctx, s->ntiles, s->stream, 5);
+    launch_scan(s->ctx, s->ntiles, s->stream, 2);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// counts_out: [world] payloads this rank sends to each rank, then [world]
+// payloads it receives from each rank. Blocking (the exchange needs them).
+static void shard_serve_impl(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  {
+    const int W = s->world;
+    // counts_dev: [W] actual sends of this rank; counts_all: the W x W matrix
+    CK(cudaMemsetAsync(s->counts_dev, 0, 2 * W * sizeof(unsigned), s->stream));
+    CK(cudaMemsetAsync(s->counts_all, 0, static_cast<size_t>(W) * W * sizeof(unsigned), s->stream));
+    const long long nglob = s->ctx.n_glob;
+    const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
+    k_serve_sharded<<<g, kThreads, 0, s->stream>>>(s->ctx, s->sendbuf, s->counts_dev, s->counts_all);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->counts_host, s->counts_dev, W * sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->counts_host + 2 * W, s->counts_all, static_cast<size_t>(W) * W * sizeof(unsigned),
+                       cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    check_error(s);
+    const unsigned* mat = s->counts_host + 2 * W;
+    for (int d = 0; d < W; ++d)  // the served counts must be the matrix row (self-check)
+      if (s->counts_host[d] != mat[s->rank * W + d]) throw std::runtime_error("shard_serve: count mismatch");
+    for (int i = 0; i < W; ++i) counts_out[i] = mat[s->rank * W + i];      // sends
+    for (int i = 0; i < W; ++i) counts_out[W + i] = mat[i * W + s->rank];  // receives
+  }
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_serve(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  return guarded([&] {
+    shard_serve_impl(s, counts_out);
+    return PFSMC_GPU_OK;
+  });
+}
+
+// The W x W migration count matrix of the last shard_serve (row r: rank r's sends).
+pfsmc_gpu_status pfsmc_gpu_shard_count_matrix(pfsmc_gpu_sampler* s, uint32_t* out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    const int W = s->world;
+    for (int i = 0; i < W * W; ++i) out[i] = s->counts_host[2 * W + i];
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv) {
+  return guarded([&] {
+    if (n_recv != static_cast<uint64_t>(s->N)) throw std::runtime_error("shard_update: payload count mismatch");
+    k_place<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->recvbuf, static_cast<long long>(n_recv));
+    s->ks->update(s->ctx, s->grid, s->stream);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    s->ks->moments(s->ctx, s->grid, s->stream, 1);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// flags: 7 = a completed step (lse_w, cov, chol, flip); 2 = init refresh;
+// 0 = injection (shrink mean only). Blocking; trace_out optional.
+static void shard_finish_moments_impl(pfsmc_gpu_sampler* s, int flags, double* trace_out) {
+  s->ks->finish_moments(s->ctx, s->gp_mom_all, s->ngroups_upd * s->world, flags, s->stream);
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaGetLastError());
+  check_error(s);
+  if (trace_out) {
+    const int n = 2 * s->p + s->d + 1;
+    for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
+  }
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out) {
+  return guarded([&] {
+    shard_finish_moments_impl(s, flags, trace_out);
+    return PFSMC_GPU_OK;
+  });
+}
+
+
+// ---- native sharded step over NCCL (one call per observation) ------------
+pfsmc_gpu_status pfsmc_gpu_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    if (!nccl_api().ok) throw std::runtime_error("nccl: libnccl.so.2 not available");
+    ncclUniqueId id;
+    NCK(nccl_api().GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t* id128) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (!nccl_api().ok) throw std::runtime_error("nccl: libnccl.so.2 not available");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    CK(cudaSetDevice(s->cfg.device));
+    if (s->nccl) NCK(nccl_api().CommDestroy(s->nccl));
+    NCK(nccl_api().CommInitRank(&s->nccl, s->world, id, s->rank));
+    return PFSMC_GPU_OK;
+  });
+}
+
+// ---- migration over NVLink peer memory --------------------------------------
+// The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
+// segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
+constexpr int kPeerBufs = 6;
+
+pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    const Ctx& c = s->ctx;
+    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse};
+    for (int i = 0; i < kPeerBufs; ++i) {
+      cudaIpcMemHandle_t h;
+      CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
+      std::memcpy(out + i * sizeof(h), &h, sizeof(h));
+    }
+    return PFSMC_GPU_OK;
+  });
+}
+
+// all_handles: world x kPeerBufs IPC handles in rank order (this rank's own
+// entry is ignored: local pointers).
+pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (s->world > kMaxRanks) throw ConfigError("attach_peers: at most 8 ranks");
+    CK(cudaSetDevice(s->cfg.device));
+    const Ctx& c = s->ctx;
+    PeerTable t{};
+    for (int r = 0; r < s->world; ++r) {
+      const void* p[kPeerBufs];
+      if (r == s->rank) {
+        p[0] = c.rec[0], p[1] = c.rec[1], p[2] = c.llbar, p[3] = c.cdf, p[4] = c.seg_end, p[5] = c.coarse;
+      } else {
+        for (int i = 0; i < kPeerBufs; ++i) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, all_handles + (static_cast<size_t>(r) * kPeerBufs + i) * sizeof(h), sizeof(h));
+          void* q = nullptr;
+          CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+          s->ipc_opened.push_back(q);
+          p[i] = q;
+        }
+      }
+      t.rec0[r] = static_cast<const double*>(p[0]);
+      t.rec1[r] = static_cast<const double*>(p[1]);
+      t.llbar[r] = static_cast<const double*>(p[2]);
+      t.cdf[r] = static_cast<const double*>(p[3]);
+      t.seg_end[r] = static_cast<const double*>(p[4]);
+      t.coarse[r] = static_cast<const unsigned*>(p[5]);
+    }
+    s->peers = t;
+    s->have_peers = true;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// The device part of one peer-memory sharded step (everything between the
+// step-parameter upload and the DevState read-back), for eager launch or
+// capture into a CUDA graph (NCCL collectives capture).
+static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
+  const NcclApi& N = nccl_api();
+  const Ctx& c = s->ctx;
+  cudaStream_t st = s->stream;
+  const int W = s->world;
+  enqueue_prologue(s);
+  s->ks->predict(c, s->grid, st);
+  NCK(N.AllGather(c.gpart, s->gp_pred_all, 2 * static_cast<size_t>(s->ngroups_pred), ncclDouble, s->nccl, st));
+  k_finish_lse<<<1, kThreads, 0, st>>>(c, s->gp_pred_all, s->ngroups_pred * W);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
+  k_shard_offset<<<1, 32, 0, st>>>(c, s->sums_all);
+  launch_scan(c, s->ntiles, st, 4);
+  NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));
+  NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8,
+                  s->nccl, st));
+  launch_scan(c, s->ntiles, st, 5);
+  launch_scan(c, s->ntiles, st, 2);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete everywhere
+  k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
+  s->ks->update(c, s->grid, st);
+  const size_t Wm = static_cast<size_t>(s->ks->moment_width());
+  NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
+  s->ks->finish_moments(c, s->gp_mom_all, s->ngroups_upd * W, 7, st);
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+}
+
+// The peer-memory step: one CUDA graph per step (built on first use; eager
+// launches if capture is refused), one host sync for the trace row.
+static void shard_pull_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
+                            double h, double* trace_out) {
+  if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
+  CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
+  *s->sp_host = sp;
+  CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+  if (!s->shard_graph && !s->shard_graph_refused) {
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        enqueue_shard_pull_step(s);
+      } catch (const std::exception&) {
+        ok = false;
+      }
+      const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+      ok = ok && e == cudaSuccess && g != nullptr &&
+           cudaGraphInstantiate(&s->shard_graph, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    if (!ok) {
+      s->shard_graph = nullptr;
+      s->shard_graph_refused = true;
+      cudaGetLastError();  // clear
+    }
+  }
+  if (s->shard_graph)
+    CK(cudaGraphLaunch(s->shard_graph, s->stream));
+  else
+    enqueue_shard_pull_step(s);
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaGetLastError());
+  check_error(s);
+  if (trace_out) {
+    const int n = 2 * s->p + s->d + 1;
+    for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
+  }
+}
+
+// One pf_step of the global filter: the five exchanges as NCCL
+// collectives on the sampler stream between the phase kernels, host syncs
+// only where the host needs data (the migration counts, the trace row).
+pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
+                                      double t_obs, double h, double* trace_out) {
+  return guarded([&] {
+    if (!s->nccl) throw ConfigError("shard_step: no NCCL communicator (pfsmc_gpu_shard_attach_nccl)");
+    if (s->have_peers) {
+      shard_pull_step(s, y, j, t_prev, t_obs, h, trace_out);
+      return PFSMC_GPU_OK;
+    }
+    const NcclApi& N = nccl_api();
+    const Ctx& c = s->ctx;
+    cudaStream_t st = s->stream;
+    const int W = s->world, me = s->rank;
+    shard_predict_impl(s, y, j, t_prev, t_obs, h);
+    // A: predict-kernel group partials -> global LSE
+    NCK(N.AllGather(c.gpart, s->gp_pred_all, 2 * static_cast<size_t>(s->ngroups_pred), ncclDouble, s->nccl, st));
+    k_finish_lse<<<1, kThreads, 0, st>>>(c, s->gp_pred_all, s->ngroups_pred * W);
+    // B: shard (approximate total, nonzero count) -> global prefix for the classification
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
+    k_shard_offset<<<1, 32, 0, st>>>(c, s->sums_all);
+    launch_scan(c, s->ntiles, st, 4);
+    // C: tile records, in place (this rank's slice of the global arrays)
+    NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));
+    NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8,
+                    s->nccl, st));
+    launch_scan(c, s->ntiles, st, 5);
+    launch_scan(c, s->ntiles, st, 2);
+    CK(cudaGetLastError());
+
+    // D: exact-mode migration; the counts are the locally derived matrix
+    std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
+    shard_serve_impl(s, cnt.data());
+    const unsigned* mat = s->counts_host + 2 * W;
+    const size_t item = sizeof(double) * static_cast<size_t>(c.R + kShardPW);
+    const size_t cap = static_cast<size_t>(s->N);
+    char* send = reinterpret_cast<char*>(s->sendbuf);
+    char* recv = reinterpret_cast<char*>(s->recvbuf);
+    size_t off = 0;
+    NCK(N.GroupStart());
+    for (int r = 0; r < W; ++r) {
+      const size_t k_in = mat[r * W + me], k_out = mat[me * W + r];
+      if (r == me) {
+        if (k_in)
+          CK(cudaMemcpyAsync(recv + off * item, send + r * cap * item, k_in * item, cudaMemcpyDeviceToDevice, st));
+      } else {
+        if (k_out) NCK(N.Send(send + r * cap * item, k_out * item, ncclUint8, r, s->nccl, st));
+        if (k_in) NCK(N.Recv(recv + off * item, k_in * item, ncclUint8, r, s->nccl, st));
+      }
+      off += k_in;
+    }
+    NCK(N.GroupEnd());
+    if (off != cap) throw std::runtime_error("shard_step: payload count mismatch");
+    k_place<<<s->grid, kThreads, 0, st>>>(c, s->recvbuf, static_cast<long long>(off));
+    s->ks->update(c, s->grid, st);
+    // E: update-kernel moment partials -> global lse_w, moments, trace row, chol
+    const size_t Wm = static_cast<size_t>(s->ks->moment_width());
+    NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
+    CK(cudaGetLastError());
+    shard_finish_moments_impl(s, 7, trace_out);
+    return PFSMC_GPU_OK;
+  });
+}
+
+}  // extern "C"
