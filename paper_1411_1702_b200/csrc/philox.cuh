@@ -7,7 +7,8 @@
 // 64x64->128 multiplies use the native IMAD.WIDE.U32-based __umul64hi plus a
 // plain 64-bit multiply; everything is integer, so device words are
 // bit-identical to the reference. Uniforms/normals follow rng.cpp:57-75; the
-// normals go through CUDA's log/sin/cos (<= 2 ulp from glibc) and are the one
+// normals go through CUDA's log and sincospi (a few ulp from glibc's log/sin/cos
+// of fl(2 pi u)) and are the one
 // place device streams are not bitwise equal to the host's.
 #pragma once
 #include <cstdint>
@@ -104,11 +105,11 @@ struct Stream {
     const double u1 = (static_cast<double>(next_u64() >> 11) + 1.0) * 0x1.0p-53;
     const double u2 = next_uniform();
     const double r = sqrt(-2.0 * log(u1));
-    const double angle = 2.0 * 3.14159265358979323846 * u2;
     double s, c;
 #ifdef __CUDA_ARCH__
-    sincos(angle, &s, &c);
+    sincospi(2.0 * u2, &s, &c);  // as stream_normals below
 #else
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
     s = sin(angle);
     c = cos(angle);
 #endif
@@ -139,11 +140,13 @@ PF_HD void stream_normals(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpos
     const double u1 = (static_cast<double>(w[2 * q] >> 11) + 1.0) * 0x1.0p-53;
     const double u2 = u64_to_uniform(w[2 * q + 1]);
     const double r = sqrt(-2.0 * log(u1));
-    const double angle = 2.0 * 3.14159265358979323846 * u2;
     double s, c;
 #ifdef __CUDA_ARCH__
-    sincos(angle, &s, &c);
+    // sin/cos(2 pi u2) without the range reduction (2 u2 is exact); differs
+    // from sin(fl(2 pi u2)) by the rounding of the product, <= 4.4e-16 absolute
+    sincospi(2.0 * u2, &s, &c);
 #else
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
     s = sin(angle);
     c = cos(angle);
 #endif

@@ -25,7 +25,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpfsmc_gpu.so")
+# PFSMC_GPU_LIB: an alternative build of the same library (A/B timing of two
+# builds on one box, profiles/ab.py); the default is the in-tree build.
+LIB_PATH = os.environ.get("PFSMC_GPU_LIB") or os.path.join(HERE, "libpfsmc_gpu.so")
 
 MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4, "metabolic": 5}
 MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 4: (6, 2), 5: (3, 4)}
