@@ -243,6 +243,15 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
  * attaches; then each slot pulls its ancestor from the serving rank's memory. */
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out384);
 pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles);
+/* Back to the counted send / receive (if any rank failed to map its peers). */
+pfsmc_gpu_status pfsmc_gpu_shard_detach_peers(pfsmc_gpu_sampler* s);
+/* Same-process shards (R handles of one filter in one process, e.g. on one
+ * GPU): the peer table from the handles themselves (rank order), no IPC. */
+pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_gpu_sampler* const* shards);
+/* Phase D over peer memory + the update kernel, phase by phase (replaces
+ * shard_serve + the payload exchange + shard_update): call after every
+ * rank's tables are complete (after the resolve phase). */
+pfsmc_gpu_status pfsmc_gpu_shard_pull(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */

@@ -414,6 +414,63 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
   });
 }
 
+// Same-process shards (one GPU or P2P-capable GPUs of one process): the peer
+// table from the other handles' own device pointers, no IPC. Used to run the
+// pull migration phase by phase (pfsmc_gpu_shard_pull) with R shards on one
+// GPU, the single-GPU check of the multi-rank pull path.
+pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_gpu_sampler* const* shards) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (s->world > kMaxRanks) throw ConfigError("attach_peers: at most 8 ranks");
+    PeerTable t{};
+    for (int r = 0; r < s->world; ++r) {
+      const pfsmc_gpu_sampler* o = shards[r];
+      if (!o || !o->shard_api || o->rank != r || o->world != s->world || o->N != s->N || o->ctx.R != s->ctx.R)
+        throw ConfigError("attach_peers_local: shards[] must be this filter's handles in rank order");
+      const Ctx& c = o->ctx;
+      t.rec0[r] = c.rec[0];
+      t.rec1[r] = c.rec[1];
+      t.llbar[r] = c.llbar;
+      t.cdf[r] = c.cdf;
+      t.seg_end[r] = c.seg_end;
+      t.coarse[r] = c.coarse;
+    }
+    s->peers = t;
+    s->have_peers = true;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Back to the counted send / receive (e.g. when another rank failed to map
+// its peers): unmaps the IPC mappings and drops the peer-memory step graph.
+pfsmc_gpu_status pfsmc_gpu_shard_detach_peers(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    CK(cudaSetDevice(s->cfg.device));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->shard_graph) cudaGraphExecDestroy(s->shard_graph);
+    s->shard_graph = nullptr;
+    s->shard_graph_refused = false;
+    for (void* q : s->ipc_opened) cudaIpcCloseMemHandle(q);
+    s->ipc_opened.clear();
+    s->peers = PeerTable{};
+    s->have_peers = false;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Phase D over peer memory plus the update kernel (replaces shard_serve, the
+// payload exchange and shard_update): every peer's tables must be complete
+// (the caller orders this after every rank's resolve / CDF phase).
+pfsmc_gpu_status pfsmc_gpu_shard_pull(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    if (!s->have_peers) throw ConfigError("shard_pull: no peer table (attach_peers / attach_peers_local)");
+    k_pull<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->peers);
+    s->ks->update(s->ctx, s->grid, s->stream);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
 // The device part of one peer-memory sharded step (everything between the
 // step-parameter upload and the DevState read-back), for eager launch or
 // capture into a CUDA graph (NCCL collectives capture).

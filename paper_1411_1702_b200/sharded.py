@@ -139,23 +139,40 @@ class GpuShard(GpuSampler):
         """Migration over NVLink peer memory: allgather every rank's CUDA IPC
         handles (6 x 64 bytes) and map the peers' search tables and records.
         Returns False (the counted send / receive stays in use) if the mapping
-        fails on any rank."""
+        fails on any rank; every rank takes part in both collectives whatever
+        happens locally, and a rank that mapped detaches again."""
         import torch
         import torch.distributed as dist
         L = self.lib
-        L.pfsmc_gpu_shard_ipc_handles.restype = C.c_int
-        L.pfsmc_gpu_shard_attach_peers.restype = C.c_int
+        for name in ("pfsmc_gpu_shard_ipc_handles", "pfsmc_gpu_shard_attach_peers", "pfsmc_gpu_shard_detach_peers"):
+            getattr(L, name).restype = C.c_int
         mine = np.zeros(384, dtype=np.uint8)
-        self._check(L.pfsmc_gpu_shard_ipc_handles(self.h, mine.ctypes.data_as(C.POINTER(C.c_uint8))))
+        ok_local = L.pfsmc_gpu_shard_ipc_handles(self.h, mine.ctypes.data_as(C.POINTER(C.c_uint8))) == 0
         dev = f"cuda:{self.device}"
         allh = torch.zeros(384 * self.world, dtype=torch.uint8, device=dev)
         dist.all_gather_into_tensor(allh, torch.from_numpy(mine).to(dev), group=comm_group)
         allh = allh.cpu().numpy()
-        rc = L.pfsmc_gpu_shard_attach_peers(self.h, allh.ctypes.data_as(C.POINTER(C.c_uint8)))
-        ok = torch.tensor([1 if rc == 0 else 0], dtype=torch.int32, device=dev)
+        if ok_local:
+            ok_local = L.pfsmc_gpu_shard_attach_peers(self.h, allh.ctypes.data_as(C.POINTER(C.c_uint8))) == 0
+        ok = torch.tensor([1 if ok_local else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=comm_group)
         self.peers = bool(ok.item())
+        if not self.peers:
+            self._check(L.pfsmc_gpu_shard_detach_peers(self.h))
         return self.peers
+
+    def attach_peers_local(self, shards) -> None:
+        """Peer table from same-process shards (rank order), no IPC."""
+        L = self.lib
+        L.pfsmc_gpu_shard_attach_peers_local.restype = C.c_int
+        hs = (C.c_void_p * self.world)(*[sh.h for sh in sorted(shards, key=lambda x: x.rank)])
+        self._check(L.pfsmc_gpu_shard_attach_peers_local(self.h, hs))
+        self.peers = True
+
+    def pull(self):
+        """Phase D over peer memory + the update kernel."""
+        self.lib.pfsmc_gpu_shard_pull.restype = C.c_int
+        self._check(self.lib.pfsmc_gpu_shard_pull(self.h))
 
     def native_step(self, y, j, t_prev, t_obs, h) -> np.ndarray:
         out = np.zeros(self.row_width)
@@ -310,9 +327,12 @@ class TorchComm:
 class ShardedFilter:
     """The global filter over `shards` (this process's shards) and `comm`."""
 
-    def __init__(self, shards: List, comm):
+    def __init__(self, shards: List, comm, pull: bool = False):
+        """pull: phase D as the peer-memory pull (shards attached with
+        attach_peers / attach_peers_local) instead of the counted exchange."""
         self.shards = sorted(shards, key=lambda s: s.rank)
         self.comm = comm
+        self.pull = pull
         s0 = self.shards[0]
         self.d, self.p, self.world = s0.d, s0.p, s0.world
 
@@ -346,10 +366,7 @@ class ShardedFilter:
         sh, comm = self.shards, self.comm
         if len(sh) == 1 and getattr(sh[0], "native", False):
             # one native call: the same phases and exchanges over NCCL (pfsmc_gpu_shard_step)
-            out = sh[0].native_step(y, j, t_prev, t_obs, h)
-            p, d = self.p, self.d
-            return TraceRow(j, t_obs, out[:p].copy(), out[p:2 * p].copy(), out[2 * p:2 * p + d].copy(),
-                            float(out[2 * p + d]))
+            return self._row(sh[0].native_step(y, j, t_prev, t_obs, h), j, t_obs)
         self._each(lambda s: s.predict(y, j, t_prev, t_obs, h))
         comm.allgather(sh, BUF_PRED, BUF_PRED_ALL)                       # A
         self._each(lambda s: s.finish_lse())                             # (+ local tile prefixes)
@@ -358,6 +375,16 @@ class ShardedFilter:
         comm.allgather_slices(sh, BUF_HDR)                               # C
         comm.allgather_slices(sh, BUF_WIN)
         self._each(lambda s: s.resolve())
+        if self.pull:
+            # D over peer memory. The 2-double allgather (as in the native
+            # step) orders every shard's pull after every shard's CDF tables;
+            # the peers' record buffers a pull reads are the ones no update of
+            # this step writes (double buffering), and E below orders the next
+            # step's overwrite of ll_bar / the tables after every pull.
+            comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)
+            self._each(lambda s: s.pull())
+            comm.allgather(sh, BUF_MOM, BUF_MOM_ALL)                     # E
+            return self._row(self._each(lambda s: s.finish_moments(STEP_FLAGS))[0], j, t_obs)
         served = {s.rank: s.serve() for s in sh}
         mat = sh[0].count_matrix()                                       # same on every rank: no exchange
         counts = {r: mat[r] for r in range(self.world)}                  # counts[r][d]: r sends to d
@@ -369,8 +396,9 @@ class ShardedFilter:
         for s in sh:
             s.update(int(sum(counts[r][s.rank] for r in range(self.world))))
         comm.allgather(sh, BUF_MOM, BUF_MOM_ALL)                         # E
-        rows = self._each(lambda s: s.finish_moments(STEP_FLAGS))
-        out = rows[0]
+        return self._row(self._each(lambda s: s.finish_moments(STEP_FLAGS))[0], j, t_obs)
+
+    def _row(self, out, j, t_obs) -> TraceRow:
         p, d = self.p, self.d
         return TraceRow(j, t_obs, out[:p].copy(), out[p:2 * p].copy(), out[2 * p:2 * p + d].copy(),
                         float(out[2 * p + d]))

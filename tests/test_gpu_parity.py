@@ -510,12 +510,15 @@ def test_cpp_drop_in_example_matches_oracle():
 
 
 # ---------------------------------------------------------------- sharding
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_shards_reproduce_single_handle_bitwise(world):
+@pytest.mark.parametrize("world,pull", [(2, False), (4, False), (2, True), (4, True)])
+def test_sharded_shards_reproduce_single_handle_bitwise(world, pull):
     """R shards (one GPU, LocalComm: phases strictly sequential, no kernel
     waits on another shard) reproduce the single-handle run bit for bit: the
     keyed streams use global slots, the LSE / moment partials are combined in
-    the single-handle order, and the CDF is exact."""
+    the single-handle order, and the CDF is exact. pull: the migration as the
+    peer-memory pull (k_pull reading the other shards' tables and records
+    through a peer table of their device pointers; the multi-rank path of the
+    native step's NVLink migration) instead of the counted exchange."""
     from paper_1411_1702_b200 import problems
     from paper_1411_1702_b200.sampler import GpuSampler
     from paper_1411_1702_b200.sharded import GpuShard, LocalComm, ShardedFilter
@@ -524,7 +527,10 @@ def test_sharded_shards_reproduce_single_handle_bitwise(world):
     single = GpuSampler("lv", prob.cfg, prob.obs)
     single.initialize_uniform(**prob.prior)
     shards = [GpuShard("lv", prob.cfg, prob.obs, r, world) for r in range(world)]
-    f = ShardedFilter(shards, LocalComm(world))
+    if pull:
+        for s in shards:
+            s.attach_peers_local(shards)
+    f = ShardedFilter(shards, LocalComm(world), pull=pull)
     f.initialize_uniform(**prob.prior)
     e1, e2 = single.get_ensemble(), f.get_ensemble()
     assert np.array_equal(e1.states, e2.states) and np.array_equal(e1.params_u, e2.params_u)
