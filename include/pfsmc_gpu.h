@@ -48,8 +48,12 @@ enum {
   PFSMC_GPU_MODEL_ROBERTSON = 2,
   PFSMC_GPU_MODEL_CHAIN8 = 3,
   PFSMC_GPU_MODEL_PAYLOAD64 = 4,  /* 64-byte record, resample microbenchmark only */
-  PFSMC_GPU_MODEL_METABOLIC = 5   /* the reference's problem 1, models::MetabolicModel
+  PFSMC_GPU_MODEL_METABOLIC = 5,  /* the reference's problem 1, models::MetabolicModel
                                      (models.cpp:37-119): d = 3, p = 4, time-dependent input */
+  PFSMC_GPU_MODEL_ADVDIFF = 6     /* the reference's problem 2, models::AdvDiffModel(n)
+                                     (models.cpp:158-266): periodic advection-diffusion on an
+                                     (n-1) x (n-1) grid, d = (n-1)^2, p = 5 (k1, k2 positive;
+                                     k3, c1, c2 not), n = model_consts[0], 4 <= n <= 33 */
 };
 /* lmm::Family (lmm.hpp:12) */
 enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
@@ -71,13 +75,14 @@ typedef struct pfsmc_gpu_config {
   int newton_max_iter;     /* NewtonOpts.max_iter (reference default 20) */
   uint64_t particles;      /* PfConfig.particles (global N) */
   const uint64_t* obs_indices; /* ObservationModel.indices */
-  uint64_t n_obs;          /* m_y <= 8 */
+  uint64_t n_obs;          /* m_y <= 8 (ADVDIFF: <= 32) */
   double sigma;            /* ObservationModel.sigma */
   int likelihood;          /* PFSMC_GPU_LIK_* */
   int device;              /* CUDA ordinal */
   double model_consts[8];  /* the bound model's constants; METABOLIC: (lambda, c0, A0, A,
                               t0_input, tau) = MetabolicConstants (models.hpp:67-74),
-                              reference defaults (1, 1, 1, 5, 2, 1); others: unused */
+                              reference defaults (1, 1, 1, 5, 2, 1); ADVDIFF: (n); others:
+                              unused */
   int adaptive;            /* IntegratorSpec.adaptive: variable-step BDF(1,2)
                               (lmm::adaptive_bdf_interval, lmm.cpp:894-1019); family,
                               order and the step h are then unused */

@@ -114,6 +114,7 @@ int or_stream_draws(uint64_t seed, uint64_t j, uint64_t n, int purpose, int kind
 /* ------------------------------------------------------------------------ */
 /* Models (oracle/ref/ref_models.hpp; plugin contract models.hpp:20-55)      */
 /* ------------------------------------------------------------------------ */
+static double g_mk_n(void);
 int or_model_dims(int model, int* d, int* p) {
   switch (model) {
     case OR_MODEL_DECAY: *d = 1; *p = 1; return OR_OK;
@@ -121,6 +122,15 @@ int or_model_dims(int model, int* d, int* p) {
     case OR_MODEL_ROBERTSON: *d = 3; *p = 3; return OR_OK;
     case OR_MODEL_CHAIN: *d = 8; *p = 4; return OR_OK;
     case OR_MODEL_METABOLIC: *d = 3; *p = 4; return OR_OK;
+    case OR_MODEL_ADVDIFF: {
+      /* AdvDiffModel(n): m = n - 1, dim m^2, 5 params (models.cpp:185-188, 242-249) */
+      const int n = (int)g_mk_n();
+      if (n < 3) return fail(OR_CONFIG, "advdiff model: grid parameter n must be >= 3");
+      if ((n - 1) * (n - 1) > OR_MAX_D) return fail(OR_CONFIG, "advdiff model: grid too large for the oracle");
+      *d = (n - 1) * (n - 1);
+      *p = 5;
+      return OR_OK;
+    }
   }
   return fail(OR_CONFIG, "unknown model id");
 }
@@ -138,6 +148,220 @@ static double g_mk[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
 void or_set_model_consts(const double* k) {
   for (int i = 0; i < 8; ++i) g_mk[i] = k[i];
 }
+
+static double g_mk_n(void) { return g_mk[0]; }
+
+/* ------------------------------------------------------------------------ */
+/* AdvDiffModel (models.cpp:158-266) over linalg's CSR (linalg.cpp:24-200)   */
+/* ------------------------------------------------------------------------ */
+typedef struct csr {
+  int nr, nc, nnz;
+  int* ro;
+  int* ci;
+  double* v;
+} csr;
+
+static csr csr_alloc(int nr, int nc, int cap) {
+  csr m;
+  m.nr = nr; m.nc = nc; m.nnz = 0;
+  m.ro = calloc((size_t)nr + 1, sizeof(int));
+  m.ci = malloc(sizeof(int) * (size_t)(cap ? cap : 1));
+  m.v = malloc(sizeof(double) * (size_t)(cap ? cap : 1));
+  return m;
+}
+static void csr_free(csr* m) { free(m->ro); free(m->ci); free(m->v); m->ro = NULL; m->ci = NULL; m->v = NULL; }
+static void csr_push(csr* m, int c, double v) { m->ci[m->nnz] = c; m->v[m->nnz] = v; ++m->nnz; }
+
+/* CsrMatrix::identity (linalg.cpp:50-59) */
+static csr csr_identity(int n) {
+  csr m = csr_alloc(n, n, n);
+  for (int i = 0; i < n; ++i) { csr_push(&m, i, 1.0); m.ro[i + 1] = m.nnz; }
+  return m;
+}
+/* periodic_diff_matrix (linalg.cpp:89-113), scale 1: row 0 (+1 @0, -1 @n-1),
+ * row i > 0 (-1 @i-1, +1 @i) */
+static csr periodic_diff(int n) {
+  csr m = csr_alloc(n, n, 2 * n);
+  csr_push(&m, 0, 1.0);
+  csr_push(&m, n - 1, -1.0);
+  m.ro[1] = 2;
+  for (int i = 1; i < n; ++i) {
+    csr_push(&m, i - 1, -1.0);
+    csr_push(&m, i, 1.0);
+    m.ro[i + 1] = m.nnz;
+  }
+  return m;
+}
+/* kron (linalg.cpp:115-140) */
+static csr csr_kron(const csr* a, const csr* b) {
+  csr m = csr_alloc(a->nr * b->nr, a->nc * b->nc, a->nnz * b->nnz);
+  for (int ia = 0; ia < a->nr; ++ia)
+    for (int ib = 0; ib < b->nr; ++ib) {
+      for (int ka = a->ro[ia]; ka < a->ro[ia + 1]; ++ka) {
+        const int col_base = a->ci[ka] * b->nc;
+        const double va = a->v[ka];
+        for (int kb = b->ro[ib]; kb < b->ro[ib + 1]; ++kb) csr_push(&m, col_base + b->ci[kb], va * b->v[kb]);
+      }
+      m.ro[ia * b->nr + ib + 1] = m.nnz;
+    }
+  return m;
+}
+/* csr_add (linalg.cpp:142-180): merge of sorted rows; shared entries
+ * v = 0 + alpha a, then v += beta b; a-only v = 0 + alpha a; b-only v = beta b. */
+static csr csr_add(double alpha, const csr* a, double beta, const csr* b) {
+  csr m = csr_alloc(a->nr, a->nc, a->nnz + b->nnz);
+  for (int i = 0; i < m.nr; ++i) {
+    int ka = a->ro[i], kb = b->ro[i];
+    const int ea = a->ro[i + 1], eb = b->ro[i + 1];
+    while (ka < ea || kb < eb) {
+      int col;
+      double v = 0.0;
+      if (ka < ea && (kb >= eb || a->ci[ka] <= b->ci[kb])) {
+        col = a->ci[ka];
+        v += alpha * a->v[ka];
+        ++ka;
+        if (kb < eb && b->ci[kb] == col) { v += beta * b->v[kb]; ++kb; }
+      } else {
+        col = b->ci[kb];
+        v = beta * b->v[kb];
+        ++kb;
+      }
+      csr_push(&m, col, v);
+    }
+    m.ro[i + 1] = m.nnz;
+  }
+  return m;
+}
+/* AdvDiffModel's transpose_mul (models.cpp:196-233): G = A^T B, entries
+ * summed per column after sorting. The operands are +-1 difference
+ * matrices, so every product and sum is an exact small integer and the sort
+ * order of equal columns cannot change a value. */
+static csr csr_tmul(const csr* a, const csr* b) {
+  const int nc = a->nc;
+  double* acc = calloc((size_t)b->nc, sizeof(double));
+  char* hit = calloc((size_t)b->nc, 1);
+  csr g = csr_alloc(nc, b->nc, a->nnz * 4 + nc);
+  /* rows[i] collects (col_b, va*vb) over k with A_ki != 0 */
+  for (int i = 0; i < nc; ++i) {
+    for (int k = 0; k < a->nr; ++k)
+      for (int ia = a->ro[k]; ia < a->ro[k + 1]; ++ia) {
+        if (a->ci[ia] != i) continue;
+        const double va = a->v[ia];
+        for (int ib = b->ro[k]; ib < b->ro[k + 1]; ++ib) {
+          const int c = b->ci[ib];
+          acc[c] = hit[c] ? acc[c] + va * b->v[ib] : va * b->v[ib];
+          hit[c] = 1;
+        }
+      }
+    for (int c = 0; c < b->nc; ++c)
+      if (hit[c]) { csr_push(&g, c, acc[c]); hit[c] = 0; }
+    g.ro[i + 1] = g.nnz;
+  }
+  free(acc); free(hit);
+  return g;
+}
+/* spmv (linalg.cpp:182-194) */
+static void csr_spmv(const csr* a, const double* x, double* y) {
+  for (int i = 0; i < a->nr; ++i) {
+    double sum = 0.0;
+    for (int k = a->ro[i]; k < a->ro[i + 1]; ++k) sum += a->v[k] * x[a->ci[k]];
+    y[i] = sum;
+  }
+}
+
+/* The model's fixed matrices for grid m = n - 1 (AdvDiffModel ctor,
+ * models.cpp:185-240): B1 = I (x) D, B2 = D (x) I, G11 = B1'B1, G22 = B2'B2,
+ * G12 = B1'B2 + B2'B1; cached per n. */
+static int g_adv_n = 0;
+static csr g_b1, g_b2, g_g11, g_g22, g_g12;
+static csr g_adv_L;     /* the bound operator (AdvDiffModel::bind) */
+static int g_adv_bound = 0;
+
+static void adv_build(int n) {
+  if (g_adv_n == n) return;
+  if (g_adv_n) {
+    csr_free(&g_b1); csr_free(&g_b2); csr_free(&g_g11); csr_free(&g_g22); csr_free(&g_g12);
+  }
+  const int m = n - 1;
+  csr ell = periodic_diff(m), eye = csr_identity(m);
+  g_b1 = csr_kron(&eye, &ell);
+  g_b2 = csr_kron(&ell, &eye);
+  g_g11 = csr_tmul(&g_b1, &g_b1);
+  g_g22 = csr_tmul(&g_b2, &g_b2);
+  csr t12 = csr_tmul(&g_b1, &g_b2), t21 = csr_tmul(&g_b2, &g_b1);
+  g_g12 = csr_add(1.0, &t12, 1.0, &t21);
+  csr_free(&t12); csr_free(&t21); csr_free(&ell); csr_free(&eye);
+  g_adv_n = n;
+}
+
+/* assemble_operator (models.cpp:251-261):
+ *   L = -(k1^2 G11 + k1 k3 G12 + (k2^2 + k3^2) G22) + c1 B1 + c2 B2 */
+static csr adv_assemble(const double* th) {
+  adv_build((int)g_mk[0]);
+  const double k1 = th[0], k2 = th[1], k3 = th[2], c1 = th[3], c2 = th[4];
+  csr diff = csr_add(-(k1 * k1), &g_g11, -(k1 * k3), &g_g12);
+  csr diff2 = csr_add(1.0, &diff, -(k2 * k2 + k3 * k3), &g_g22);
+  csr adv = csr_add(c1, &g_b1, c2, &g_b2);
+  csr L = csr_add(1.0, &diff2, 1.0, &adv);
+  csr_free(&diff); csr_free(&diff2); csr_free(&adv);
+  return L;
+}
+/* AdvDiffModel::bind for the particle being propagated (one at a time). */
+static void adv_bind(const double* th) {
+  if (g_adv_bound) csr_free(&g_adv_L);
+  g_adv_L = adv_assemble(th);
+  g_adv_bound = 1;
+}
+
+int or_advdiff_operator(int n, const double* theta_nat, double* dense_out) {
+  if (n < 3) return fail(OR_CONFIG, "advdiff model: grid parameter n must be >= 3");
+  const double keep = g_mk[0];
+  g_mk[0] = (double)n;
+  csr L = adv_assemble(theta_nat);
+  g_mk[0] = keep;
+  const int d = L.nr;
+  memset(dense_out, 0, sizeof(double) * (size_t)d * (size_t)d);
+  for (int i = 0; i < d; ++i)
+    for (int k = L.ro[i]; k < L.ro[i + 1]; ++k) dense_out[(size_t)i * d + L.ci[k]] = L.v[k];
+  csr_free(&L);
+  return OR_OK;
+}
+
+/* gaussian_plume_ic (models.cpp:130-156) */
+int or_gaussian_plume_ic(int n, double* u) {
+  static const double kGamma[6] = {0.04, 0.08, 0.07, 0.10, 0.05, 0.06};
+  static const double kXc[6] = {0.20, 0.30, 0.40, 0.50, 0.50, 0.70};
+  static const double kYc[6] = {0.80, 0.40, 0.40, 0.50, 0.60, 0.50};
+  const double kSqrt2Pi = 2.5066282746310002;
+  if (n < 3) return fail(OR_CONFIG, "gaussian_plume_ic: n must be >= 3");
+  const int m = n - 1;
+  for (int iy = 0; iy < m; ++iy) {
+    const double y = (double)iy / (double)m;
+    for (int ix = 0; ix < m; ++ix) {
+      const double x = (double)ix / (double)m;
+      double sum = 0.0;
+      for (int i = 0; i < 6; ++i) {
+        const double dx = x - kXc[i];
+        const double dy = y - kYc[i];
+        sum += exp(-(dx * dx + dy * dy) / (2.0 * kGamma[i] * kGamma[i])) / (kGamma[i] * kSqrt2Pi);
+      }
+      u[iy * m + ix] = sum;
+    }
+  }
+  return OR_OK;
+}
+
+/* The sparse Newton path's workspace (NewtonWorkspace, lmm.hpp:88-100): the
+ * factorisation of I - hb0 L is cached while hb0 is unchanged
+ * (lmm.cpp:233-243). The LU is the direct solver the oracle's Eigen stand-in
+ * runs (oracle/ref/eigen_stub/Eigen/SparseLU): DenseLu's pivot rule. */
+typedef struct sparse_ws {
+  int valid;
+  double hb0;
+  double* lu;
+  int* piv;
+} sparse_ws;
+static _Thread_local sparse_ws* g_sws = NULL;
 
 /* input_phi (models.cpp:37-42) */
 static double input_phi(double t, double A0, double A, double t0_input, double tau) {
@@ -163,6 +387,10 @@ static int model_rhs(int model, double t, const double* th, const double* x, dou
     case OR_MODEL_DECAY:
       o[0] = -th[0] * x[0];
       return 1;
+    case OR_MODEL_ADVDIFF: /* AdvDiffEval::rhs (models.cpp:164-170): spmv + finiteness */
+      (void)th;
+      csr_spmv(&g_adv_L, x, o);
+      return all_finite(o, g_adv_L.nr);
     case OR_MODEL_LV:
       o[0] = th[0] * x[0] - x[0] * x[1];
       o[1] = x[0] * x[1] - th[1] * x[1];
@@ -247,10 +475,12 @@ static int model_jac(int model, double t, const double* th, const double* x, dou
   return 0;
 }
 
-/* to_natural: exp for positive params (models.cpp:18-25). All parameters of
- * the four models are positive. */
-static void to_natural(int p, const double* u, double* nat) {
-  for (int i = 0; i < p; ++i) nat[i] = exp(u[i]);
+/* to_natural: exp for positive params (models.cpp:18-25). Every parameter of
+ * the other models is positive; AdvDiffModel's are {k1, k2} positive, {k3,
+ * c1, c2} not (models.cpp:242-249). */
+static int param_positive(int model, int i) { return model != OR_MODEL_ADVDIFF || i < 2; }
+static void to_natural_m(int model, int p, const double* u, double* nat) {
+  for (int i = 0; i < p; ++i) nat[i] = param_positive(model, i) ? exp(u[i]) : u[i];
 }
 
 /* ------------------------------------------------------------------------ */
@@ -389,18 +619,36 @@ static void lu_solve(int n, const double* lu, const int* piv, double* x) {
 static int newton_solve(int model, double t_next, const double* th, int d, double hb0,
                         const double* c, const double* guess, double tol,
                         int max_iter, double* out, int* iters) {
-  double f[OR_MAX_D], r[OR_MAX_D], J[OR_MAX_D * OR_MAX_D];
-  int piv[OR_MAX_D];
+  double f[OR_MAX_D], r[OR_MAX_D], J[64];
+  int piv[8];
   memcpy(out, guess, sizeof(double) * d);
   for (int iter = 1; iter <= max_iter; ++iter) {
     *iters = iter;
     if (!model_rhs(model, t_next, th, out, f)) return OR_ST_INVALID_RHS;
     for (int j = 0; j < d; ++j) r[j] = out[j] - hb0 * f[j] - c[j];
+    if (model == OR_MODEL_ADVDIFF) {
+      /* sparse path (lmm.cpp:233-243): M = csr_add(1, I, -hb0, L), factored
+       * once per hb0 and workspace */
+      sparse_ws* ws = g_sws;
+      if (!ws->valid || ws->hb0 != hb0) {
+        csr I = csr_identity(d);
+        csr M = csr_add(1.0, &I, -hb0, &g_adv_L);
+        memset(ws->lu, 0, sizeof(double) * (size_t)d * (size_t)d);
+        for (int i = 0; i < d; ++i)
+          for (int k = M.ro[i]; k < M.ro[i + 1]; ++k) ws->lu[(size_t)i * d + M.ci[k]] += M.v[k];
+        csr_free(&I); csr_free(&M);
+        if (!lu_factor(d, ws->lu, ws->piv)) return OR_ST_SINGULAR;
+        ws->hb0 = hb0;
+        ws->valid = 1;
+      }
+      lu_solve(d, ws->lu, ws->piv, r);
+    } else {
     if (!model_jac(model, t_next, th, out, J)) return OR_ST_INVALID_RHS;
     for (int i = 0; i < d * d; ++i) J[i] = -hb0 * J[i];
     for (int i = 0; i < d; ++i) J[i * d + i] += 1.0;
     if (!lu_factor(d, J, piv)) return OR_ST_SINGULAR;
     lu_solve(d, J, piv, r);
+    }
     /* newton_update_and_test (lmm.cpp:204-215) */
     double dn = 0.0, xn = 0.0;
     for (int j = 0; j < d; ++j) {
@@ -631,14 +879,40 @@ static int adaptive_bdf(int model, int d, const double* th, const double* x0, do
   return OR_OK;
 }
 
+/* Per-propagation model binding (OdeModel::bind, models.hpp:29-33) and, for
+ * the sparse model, a fresh NewtonWorkspace (ParticleRun::ws, lmm.cpp:365-369;
+ * adaptive_bdf_interval's ws, lmm.cpp:914-915). */
+static void model_begin(int model, const double* th, int d, sparse_ws* ws) {
+  ws->valid = 0;
+  ws->lu = NULL;
+  ws->piv = NULL;
+  if (model == OR_MODEL_ADVDIFF) {
+    adv_bind(th);
+    ws->lu = malloc(sizeof(double) * (size_t)d * (size_t)d);
+    ws->piv = malloc(sizeof(int) * (size_t)d);
+  }
+  g_sws = ws;
+}
+static void model_end(sparse_ws* ws) {
+  free(ws->lu);
+  free(ws->piv);
+  g_sws = NULL;
+}
+
 /* the integrator the config selects (filter.cpp:242-264) */
 static int propagate_cfg(const or_cfg* c, int d, const double* th, const double* x0, double t0,
                          double t1, double* state, double* gamma, int* status, int* iters) {
+  sparse_ws ws;
+  model_begin(c->model, th, d, &ws);
+  int rc;
   if (c->adaptive)
-    return adaptive_bdf(c->model, d, th, x0, t0, t1, c->rtol, c->newton_tol, c->newton_max_iter, state,
-                        gamma, status, iters);
-  return propagate(c->model, d, th, x0, t0, t1, c->h, c->family, c->order, c->newton_tol,
+    rc = adaptive_bdf(c->model, d, th, x0, t0, t1, c->rtol, c->newton_tol, c->newton_max_iter, state,
+                      gamma, status, iters);
+  else
+    rc = propagate(c->model, d, th, x0, t0, t1, c->h, c->family, c->order, c->newton_tol,
                    c->newton_max_iter, state, gamma, status, iters);
+  model_end(&ws);
+  return rc;
 }
 
 int or_propagate_interval(int model, const double* theta_nat, const double* x0,
@@ -649,8 +923,12 @@ int or_propagate_interval(int model, const double* theta_nat, const double* x0,
   int rc = or_model_dims(model, &d, &p);
   if (rc) return rc;
   if (order < 1 || order > 3) return fail(OR_CONFIG, "scheme_coefficients: order must be 1, 2 or 3");
-  return propagate(model, d, theta_nat, x0, t0, t1, h, family, order, tol,
-                   max_iter, state_out, gamma_out, status_out, iters_out);
+  sparse_ws ws;
+  model_begin(model, theta_nat, d, &ws);
+  rc = propagate(model, d, theta_nat, x0, t0, t1, h, family, order, tol,
+                 max_iter, state_out, gamma_out, status_out, iters_out);
+  model_end(&ws);
+  return rc;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -854,7 +1132,7 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
   for (uint64_t i = 0; i < n; ++i) {
     double nat[OR_MAX_P], xb[OR_MAX_D], gam[OR_MAX_D];
     int st, it;
-    to_natural((int)p, tb + i * p, nat);
+    to_natural_m(c->model, (int)p, tb + i * p, nat);
     if ((rc = propagate_cfg(c, (int)d, nat, e->states + i * d, t_prev, t_obs, xb, gam, &st, &it)))
       goto done;
     if (out && out->newton_iters) out->newton_iters[i] = it;
@@ -896,7 +1174,7 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
   for (uint64_t i = 0; i < n; ++i) {
     double nat[OR_MAX_P], xr[OR_MAX_D], gam[OR_MAX_D];
     int st, it;
-    to_natural((int)p, tnew + i * p, nat);
+    to_natural_m(c->model, (int)p, tnew + i * p, nat);
     if ((rc = propagate_cfg(c, (int)d, nat, xs + i * d, t_prev, t_obs, xr, gam, &st, &it)))
       goto done;
     if (out && out->newton_iters) out->newton_iters[i] += it;
@@ -928,7 +1206,8 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
   if ((rc = or_weighted_mean_cov(e->params_u, n, p, w, e->mean_u, e->cov_u))) goto done;
   if (out && out->trace) {
     double* t = out->trace;
-    for (uint64_t k = 0; k < p; ++k) t[k] = exp(e->mean_u[k]);
+    for (uint64_t k = 0; k < p; ++k)
+      t[k] = param_positive(c->model, (int)k) ? exp(e->mean_u[k]) : e->mean_u[k]; /* to_natural (filter.cpp:381-382) */
     for (uint64_t k = 0; k < p; ++k) t[p + k] = e->cov_u[k * p + k];
     for (uint64_t k = 0; k < d; ++k) t[2 * p + k] = 0.0;
     for (uint64_t i = 0; i < n; ++i)

@@ -25,13 +25,15 @@ enum { OR_PURPOSE_INIT = 0, OR_PURPOSE_PROLIFERATE = 1, OR_PURPOSE_INNOVATE = 2,
        OR_PURPOSE_RESAMPLE = 3 };
 enum { OR_AB = 0, OR_AM = 1, OR_BDF = 2 };
 enum { OR_MODEL_DECAY = 0, OR_MODEL_LV = 1, OR_MODEL_ROBERTSON = 2, OR_MODEL_CHAIN = 3,
-       OR_MODEL_METABOLIC = 5 /* the reference's models::MetabolicModel (models.cpp:37-119) */ };
+       OR_MODEL_METABOLIC = 5 /* the reference's models::MetabolicModel (models.cpp:37-119) */,
+       OR_MODEL_ADVDIFF = 6   /* the reference's models::AdvDiffModel (models.cpp:158-266):
+                                 d = (n-1)^2, p = 5, grid parameter n = model const 0 */ };
 enum { OR_LIK_GAUSSIAN = 0, OR_LIK_LOGNORMAL = 1 };
 enum { OR_ST_OK = 0, OR_ST_INVALID_RHS = 1, OR_ST_NEWTON_DIVERGENCE = 2,
        OR_ST_SINGULAR = 3, OR_ST_STIFFNESS = 4 };
 
-#define OR_MAX_D 8
-#define OR_MAX_P 4
+#define OR_MAX_D 1024 /* advdiff: n <= 33 */
+#define OR_MAX_P 8
 
 typedef struct or_cfg {
   int model;
@@ -76,8 +78,14 @@ int or_stream_draws(uint64_t seed, uint64_t j, uint64_t n, int purpose, int kind
                     uint64_t count, void* out);
 int or_model_dims(int model, int* d, int* p);
 int or_rhs(int model, const double* theta_nat, const double* x, double* f);
-/* Constants of the bound model (METABOLIC: lambda, c0, A0, A, t0_input, tau). */
+/* Constants of the bound model (METABOLIC: lambda, c0, A0, A, t0_input, tau;
+ * ADVDIFF: grid parameter n). */
 void or_set_model_consts(const double* k);
+/* models::gaussian_plume_ic (models.cpp:130-156): the advdiff truth x(0), (n-1)^2 values. */
+int or_gaussian_plume_ic(int n, double* out);
+/* AdvDiffModel::assemble_operator (models.cpp:251-261) as a dense d x d row-major
+ * matrix (test helper). */
+int or_advdiff_operator(int n, const double* theta_nat, double* dense_out);
 int or_propagate_interval(int model, const double* theta_nat, const double* x0,
                           double t0, double t1, double h, int family, int order,
                           double tol, int max_iter, double* state_out,

@@ -244,9 +244,12 @@ int ref_pf_step_ancestors(const ref_cfg* c, const ref_ens* e, const double* y,
     std::vector<double> nat(p);
     for (std::size_t i = 0; i < n; ++i) {
       models::to_natural(*model, {tb.data() + i * p, p}, nat);
-      const auto r = lmm::propagate_interval(*model, nat,
-                                             {e->states + i * d, d}, t_prev,
-                                             t_obs, c->h, scheme, opts);
+      // the integrator the config selects (filter.cpp:242-264)
+      const auto r = c->adaptive
+                         ? lmm::adaptive_bdf_interval(*model, nat, {e->states + i * d, d}, t_prev, t_obs,
+                                                      c->rtol, opts)
+                         : lmm::propagate_interval(*model, nat, {e->states + i * d, d}, t_prev, t_obs,
+                                                   c->h, scheme, opts);
       ll[i] = r.status == lmm::ParticleStatus::ok
                   ? filter::log_likelihood({y, c->m_y}, r.state, obs)
                   : -std::numeric_limits<double>::infinity();

@@ -196,7 +196,7 @@ class ChainModel : public OdeModel {
   }
 };
 
-enum ModelId { kDecay = 0, kLotkaVolterra = 1, kRobertson = 2, kChain = 3, kMetabolic = 5 };
+enum ModelId { kDecay = 0, kLotkaVolterra = 1, kRobertson = 2, kChain = 3, kMetabolic = 5, kAdvDiff = 6 };
 
 // Constants for the reference's own MetabolicModel (models.hpp:67-74), set
 // through the harness (ref_set_model_consts): lambda, c0, A0, A, t0_input, tau.
@@ -214,6 +214,8 @@ inline std::unique_ptr<OdeModel> make_model(int id) {
       k.tau = g_model_consts[5];
       return std::make_unique<pfsmc::models::MetabolicModel>(k);
     }
+    case kAdvDiff:  // the reference's problem 2, unmodified (models.cpp:185-266); n = grid parameter
+      return std::make_unique<pfsmc::models::AdvDiffModel>(static_cast<std::size_t>(g_model_consts[0]));
     case kDecay:
       return std::make_unique<DecayModel>();
     case kLotkaVolterra:

@@ -23,7 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-diag-suppress", "497", "-Xptxas", "-warn-spills"]
 SOURCES = ["sampler.cu", "scan.cu", "shard.cu", "c5.cu", "kernels_decay.cu", "kernels_lv.cu", "kernels_robertson.cu",
-           "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu",
+           "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu", "kernels_advdiff.cu", "kernels_advdiff_e1.cu",
+           "kernels_advdiff_e3.cu", "kernels_advdiff_e8.cu",
            "experiment.cpp"]  # host-only: the experiment-level drop-in (pfsmc_gpu_experiment.h)
 
 

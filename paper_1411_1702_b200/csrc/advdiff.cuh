@@ -1,0 +1,862 @@
+// AdvDiffModel — the reference's second problem (models.cpp:158-266): the
+// periodic advection-diffusion operator
+//   L(theta) = -(k1^2 G11 + k1 k3 G12 + (k2^2 + k3^2) G22) + c1 B1 + c2 B2
+// on an m x m grid (m = n - 1, x varies fastest, d = m^2 states), with
+// B1 = I (x) D, B2 = D (x) I, D the periodic backward difference
+// (linalg.cpp:89-113) and G the Gram products (models.cpp:196-240).
+//
+// B200 mapping: one CTA of kAT threads per particle. The state, its LMM
+// history and the Newton iterate are distributed over the threads (element
+// e = tid + s * kAT lives in slot s of thread tid's registers); the rhs is a
+// 7-point periodic stencil read from a shared-memory copy of the vector.
+// The reference factors I - h b0 L with a sparse LU per particle
+// (lmm.cpp:233-243, Eigen SparseLU). L is a sum of products of circulant
+// matrices, so it is block-circulant with circulant blocks: the 2-D DFT
+// diagonalises it, and the Newton correction is
+//   delta = F^-1 [ F r / (1 - h b0 lambda(k)) ],
+// lambda(k) = sum_o s_o exp(+2 pi i k.o / m) over the stencil offsets o.
+// The transforms are direct length-m DFT sums (m = 19 is prime in the
+// reference's default configuration) over shared-memory twiddles, half
+// spectrum (real input): O(d m) per solve instead of the LU's fill-in.
+// Everything else — stencil values, rhs summation order, the LMM ramp,
+// Newton's stopping rule, the LTE estimate, the adaptive BDF(1,2) step
+// control — is the reference's operation order (see lmm.cuh), so only the
+// solve differs from the reference, at rounding level (tests compare to the
+// oracle within 1e-10).
+#pragma once
+#include "kernels.cuh"
+
+namespace pfsmc_gpu {
+
+constexpr int kAT = 128;          // threads per particle CTA
+constexpr int kAWarps = kAT / 32;
+constexpr int kAdvP = 5;          // k1, k2, k3, c1, c2
+constexpr int kAdvMaxM = 32;      // grid side limit (d <= 1024)
+
+// Stencil offsets (dx, dy), in this order: (0,0) (-1,0) (1,0) (0,-1) (0,1) (1,-1) (-1,1).
+__host__ __device__ constexpr int adv_dx(int o) { return o == 1 ? -1 : o == 2 ? 1 : o == 5 ? 1 : o == 6 ? -1 : 0; }
+__host__ __device__ constexpr int adv_dy(int o) { return o == 3 ? -1 : o == 4 ? 1 : o == 5 ? -1 : o == 6 ? 1 : 0; }
+
+// The operator's entries, evaluated exactly as assemble_operator's csr_add
+// chain (models.cpp:251-261, linalg.cpp:142-180) produces them: shared
+// entries v = 0 + alpha a, then v += beta b; a-only v = 0 + alpha a; b-only
+// v = beta b. G11 = {(0,0): 2, (+-1,0): -1}, G22 = {(0,0): 2, (0,+-1): -1},
+// G12 = {(0,0): 2, (+-1,0), (0,+-1): -1, (1,-1), (-1,1): 1}, B1 = {(0,0): 1,
+// (-1,0): -1}, B2 = {(0,0): 1, (0,-1): -1}. (Bitwise equal to the
+// reference's CSR values for m >= 3: tests/test_advdiff.py.)
+__device__ __forceinline__ void adv_stencil(const double* th, double (&s)[7]) {
+  const double k1 = th[0], k2 = th[1], k3 = th[2], c1 = th[3], c2 = th[4];
+  const double A = -(k1 * k1), B = -(k1 * k3), Cc = -(k2 * k2 + k3 * k3);
+  // diff = csr_add(A, G11, B, G12)
+  const double d00 = (0.0 + A * 2.0) + B * 2.0;
+  const double dx1 = (0.0 + A * -1.0) + B * -1.0;  // (-1,0) and (1,0)
+  const double dy1 = B * -1.0;                     // (0,-1) and (0,1): G12 only
+  const double dxy = B * 1.0;                      // (1,-1) and (-1,1): G12 only
+  // diff2 = csr_add(1, diff, Cc, G22)
+  const double e00 = (0.0 + 1.0 * d00) + Cc * 2.0;
+  const double ex1 = 0.0 + 1.0 * dx1;
+  const double ey1 = (0.0 + 1.0 * dy1) + Cc * -1.0;
+  const double exy = 0.0 + 1.0 * dxy;
+  // adv = csr_add(c1, B1, c2, B2)
+  const double a00 = (0.0 + c1 * 1.0) + c2 * 1.0;
+  const double axm = 0.0 + c1 * -1.0;  // (-1,0): B1 only
+  const double aym = c2 * -1.0;        // (0,-1): B2 only
+  // L = csr_add(1, diff2, 1, adv)
+  s[0] = (0.0 + 1.0 * e00) + 1.0 * a00;
+  s[1] = (0.0 + 1.0 * ex1) + 1.0 * axm;
+  s[2] = 0.0 + 1.0 * ex1;
+  s[3] = (0.0 + 1.0 * ey1) + 1.0 * aym;
+  s[4] = 0.0 + 1.0 * ey1;
+  s[5] = 0.0 + 1.0 * exy;
+  s[6] = 0.0 + 1.0 * exy;
+}
+
+// Shared-memory carve of one particle CTA (dynamic smem; sizes from m).
+struct AdvSmem {
+  double* xs;     // d: the published vector (stencil / observation reads)
+  double* rs;     // d: the solve's right-hand side
+  double2* s1;    // m * H spectra
+  double2* s2;
+  double2* lam;   // m * H: lambda(k) of this particle's operator
+  double2* imu;   // m * H: 1 / (d (1 - h b0 lambda))
+  double2* tw;    // m: (cos, sin)(2 pi k / m)
+  double* red;    // 4 * kAWarps + 8 reduction scratch
+  double* pr;     // 16 per-particle scalars (theta, stencil broadcast)
+};
+
+__host__ __device__ inline int adv_half(int m) { return m / 2 + 1; }
+__host__ inline size_t adv_smem_bytes(int m) {
+  const size_t d = static_cast<size_t>(m) * m, mh = static_cast<size_t>(m) * adv_half(m);
+  return 2 * d * 8 + 4 * mh * 16 + static_cast<size_t>(m) * 16 + (4 * kAWarps + 8) * 8 + 16 * 8;
+}
+
+__device__ __forceinline__ AdvSmem adv_carve(char* base, int m) {
+  const int d = m * m, mh = m * adv_half(m);
+  AdvSmem a;
+  a.s1 = reinterpret_cast<double2*>(base);
+  a.s2 = a.s1 + mh;
+  a.lam = a.s2 + mh;
+  a.imu = a.lam + mh;
+  a.tw = a.imu + mh;
+  a.xs = reinterpret_cast<double*>(a.tw + m);
+  a.rs = a.xs + d;
+  a.red = a.rs + d;
+  a.pr = a.red + 4 * kAWarps + 8;
+  return a;
+}
+
+// The first K normals of a keyed stream, element k only (stream_normals'
+// order: pair q = k / 2 from words 2q, 2q+1; r cos then r sin).
+__device__ __forceinline__ double normal_at(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpose,
+                                            long long k) {
+  const long long q = k >> 1;
+  const U64x4 blk = philox4x64(static_cast<uint64_t>(q >> 1), j, n, purpose, seed, kKeyConstant);
+  const int l = static_cast<int>((q & 1) * 2);
+  const uint64_t w0 = l == 0 ? blk.v[0] : blk.v[2];
+  const uint64_t w1 = l == 0 ? blk.v[1] : blk.v[3];
+  const double u1 = (static_cast<double>(w0 >> 11) + 1.0) * 0x1.0p-53;
+  const double u2 = u64_to_uniform(w1);
+  const double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  return (k & 1) ? r * s : r * c;
+}
+// The k-th uniform of a keyed stream (word k).
+__device__ __forceinline__ double uniform_at(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpose,
+                                             long long k) {
+  const U64x4 blk = philox4x64(static_cast<uint64_t>(k >> 2), j, n, purpose, seed, kKeyConstant);
+  return u64_to_uniform(blk.v[k & 3]);
+}
+
+// Block reductions over the particle CTA (every thread gets the result).
+// max of two NaN-free values (ref_max semantics: NaN operands skipped by the
+// callers' per-thread folds) and an AND of a flag.
+__device__ __forceinline__ void adv_reduce2(double& a, double& b, int& flag, double* red) {
+  a = warp_max(a);
+  b = warp_max(b);
+  flag = __all_sync(0xffffffffu, flag);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    red[w] = a;
+    red[kAWarps + w] = b;
+    red[2 * kAWarps + w] = flag;
+  }
+  __syncthreads();
+  double ra = red[0], rb = red[kAWarps];
+  int rf = red[2 * kAWarps] != 0.0;
+#pragma unroll
+  for (int i = 1; i < kAWarps; ++i) {
+    ra = nan_free_max(ra, red[i]);
+    rb = nan_free_max(rb, red[kAWarps + i]);
+    rf &= red[2 * kAWarps + i] != 0.0;
+  }
+  a = ra;
+  b = rb;
+  flag = rf;
+}
+__device__ __forceinline__ int adv_all(int flag, double* red) {
+  double a = 0.0, b = 0.0;
+  adv_reduce2(a, b, flag, red);
+  return flag;
+}
+
+// The theta moments go through the fixed-size machinery of kernels.cuh with
+// this view: P = 5 and one (unused) state component; the trace row's state
+// mean comes from the k_adv_xmean passes.
+struct AdvThetaView {
+  static constexpr int D = 1, P = kAdvP;
+};
+
+// launchers of the particle-per-thread passes (kernels_advdiff.cu)
+void adv_launch_lg_reduce(const Ctx& c, int grid, cudaStream_t s);
+void adv_launch_moments(const Ctx& c, int grid, cudaStream_t s, int mode);
+void adv_launch_xmean(const Ctx& c, int d, cudaStream_t s);
+void adv_launch_init(const Ctx& c, cudaStream_t s, int kind, const double* prm, double lw0);
+
+// ---------------------------------------------------------------- propagator
+template <int FAM, int ORD, int E>
+struct AdvProp {
+  static constexpr int SD = FAM == kBDF ? (ORD == 0 ? 1 : ORD + 1) : 1;
+  static constexpr int FD = ORD == 0 ? 1 : FAM == kAB ? ORD + 1 : ORD;
+  double xs[SD][E];
+  double fs[FD][E];
+  AdvSmem sm;
+  int m, d, H;
+  double st[7];
+  double cached_hb0;
+  bool have_imu;
+
+  __device__ __forceinline__ bool own(int s) const { return threadIdx.x + s * kAT < d; }
+  __device__ __forceinline__ int eid(int s) const { return threadIdx.x + s * kAT; }
+
+  // f = L x over the owned elements; x published through sm.xs. Summation in
+  // ascending column order from 0.0, exactly spmv (linalg.cpp:182-194).
+  // Returns the block-wide "every f finite" (AdvDiffEval::rhs, models.cpp:164-170).
+  __device__ __forceinline__ int rhs(const double (&x)[E], double (&f)[E]) {
+    __syncthreads();  // previous readers of sm.xs are done
+#pragma unroll
+    for (int s = 0; s < E; ++s)
+      if (own(s)) sm.xs[eid(s)] = x[s];
+    __syncthreads();
+    int fin = 1;
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      f[s] = 0.0;
+      if (!own(s)) continue;
+      const int e = eid(s), iy = e / m, ix = e - iy * m;
+      const int xm = ix == 0 ? m - 1 : ix - 1, xp = ix == m - 1 ? 0 : ix + 1;
+      const int ym = iy == 0 ? m - 1 : iy - 1, yp = iy == m - 1 ? 0 : iy + 1;
+      const double* rm = sm.xs + ym * m;
+      const double* r0 = sm.xs + iy * m;
+      const double* rp = sm.xs + yp * m;
+      double sum = 0.0;
+      // row y-1: (0,-1) at ix, (1,-1) at xp; row y: (-1,0) (0,0) (1,0); row y+1: (-1,1) at xm, (0,1) at ix
+      auto row_m = [&](double& acc) {
+        if (ix == m - 1) {
+          acc += st[5] * rm[xp];
+          acc += st[3] * rm[ix];
+        } else {
+          acc += st[3] * rm[ix];
+          acc += st[5] * rm[xp];
+        }
+      };
+      auto row_0 = [&](double& acc) {
+        if (ix == 0) {
+          acc += st[0] * r0[ix];
+          acc += st[2] * r0[xp];
+          acc += st[1] * r0[xm];
+        } else if (ix == m - 1) {
+          acc += st[2] * r0[xp];
+          acc += st[1] * r0[xm];
+          acc += st[0] * r0[ix];
+        } else {
+          acc += st[1] * r0[xm];
+          acc += st[0] * r0[ix];
+          acc += st[2] * r0[xp];
+        }
+      };
+      auto row_p = [&](double& acc) {
+        if (ix == 0) {
+          acc += st[4] * rp[ix];
+          acc += st[6] * rp[xm];
+        } else {
+          acc += st[6] * rp[xm];
+          acc += st[4] * rp[ix];
+        }
+      };
+      if (iy == 0) {  // rows in ascending order: y, y+1, y-1 (= m-1)
+        row_0(sum);
+        row_p(sum);
+        row_m(sum);
+      } else if (iy == m - 1) {  // y+1 (= 0), y-1, y
+        row_p(sum);
+        row_m(sum);
+        row_0(sum);
+      } else {
+        row_m(sum);
+        row_0(sum);
+        row_p(sum);
+      }
+      f[s] = sum;
+      fin &= isfinite(sum) ? 1 : 0;
+    }
+    return adv_all(fin, sm.red);
+  }
+
+  // lambda(k) for this particle's stencil (once per propagation).
+  __device__ __forceinline__ void spectrum() {
+    const int mh = m * H;
+    for (int o = threadIdx.x; o < mh; o += kAT) {
+      const int ky = o / H, kx = o - ky * H;
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        int idx = (kx * adv_dx(q) + ky * adv_dy(q)) % m;
+        if (idx < 0) idx += m;
+        const double2 t = sm.tw[idx];
+        re += st[q] * t.x;
+        im += st[q] * t.y;
+      }
+      sm.lam[o] = make_double2(re, im);
+    }
+    have_imu = false;
+  }
+
+  // 1 / (d (1 - hb0 lambda)) for the current hb0; returns "nonsingular".
+  __device__ __forceinline__ int prepare(double hb0) {
+    if (have_imu && cached_hb0 == hb0) return 1;
+    __syncthreads();  // previous solves are done with imu
+    const int mh = m * H;
+    const double dd = static_cast<double>(d);
+    int ok = 1;
+    for (int o = threadIdx.x; o < mh; o += kAT) {
+      const double2 l = sm.lam[o];
+      const double mr = 1.0 - hb0 * l.x, mi = -(hb0 * l.y);
+      const double den = (mr * mr + mi * mi) * dd;
+      ok &= den != 0.0 && isfinite(den);
+      sm.imu[o] = make_double2(mr / den, -mi / den);
+    }
+    ok = adv_all(ok, sm.red);
+    have_imu = true;
+    cached_hb0 = hb0;
+    return ok;
+  }
+
+  // delta = (I - hb0 L)^-1 r, r taken from registers, delta returned in them.
+  __device__ __forceinline__ void solve(double (&r)[E]) {
+    const int mh = m * H;
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < E; ++s)
+      if (own(s)) sm.rs[eid(s)] = r[s];
+    __syncthreads();
+    // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r e^{-2 pi i kx ix / m}
+    for (int o = threadIdx.x; o < mh; o += kAT) {
+      const int iy = o / H, kx = o - iy * H;
+      const double* row = sm.rs + iy * m;
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int ix = 0; ix < m; ++ix) {
+        const double v = row[ix];
+        const double2 t = sm.tw[idx];
+        re += v * t.x;
+        im -= v * t.y;
+        idx += kx;
+        if (idx >= m) idx -= m;
+      }
+      sm.s1[o] = make_double2(re, im);
+    }
+    __syncthreads();
+    // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) e^{-2 pi i ky iy / m}, times imu
+    for (int o = threadIdx.x; o < mh; o += kAT) {
+      const int ky = o / H, kx = o - ky * H;
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int iy = 0; iy < m; ++iy) {
+        const double2 a = sm.s1[iy * H + kx];
+        const double2 t = sm.tw[idx];
+        re += a.x * t.x + a.y * t.y;
+        im += a.y * t.x - a.x * t.y;
+        idx += ky;
+        if (idx >= m) idx -= m;
+      }
+      const double2 q = sm.imu[o];
+      sm.s2[o] = make_double2(re * q.x - im * q.y, re * q.y + im * q.x);
+    }
+    __syncthreads();
+    // I2: B(iy, kx) = sum_ky D(ky, kx) e^{+2 pi i ky iy / m}
+    for (int o = threadIdx.x; o < mh; o += kAT) {
+      const int iy = o / H, kx = o - iy * H;
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int ky = 0; ky < m; ++ky) {
+        const double2 a = sm.s2[ky * H + kx];
+        const double2 t = sm.tw[idx];
+        re += a.x * t.x - a.y * t.y;
+        im += a.y * t.x + a.x * t.y;
+        idx += iy;
+        if (idx >= m) idx -= m;
+      }
+      sm.s1[o] = make_double2(re, im);
+    }
+    __syncthreads();
+    // I1: half spectrum -> real rows (Hermitian symmetry), owned elements
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      if (!own(s)) continue;
+      const int e = eid(s), iy = e / m, ix = e - iy * m;
+      const double2* b = sm.s1 + iy * H;
+      double sum = b[0].x;
+      int idx = ix;
+      for (int kx = 1; kx < H; ++kx) {
+        const double2 t = sm.tw[idx];
+        const double w = (2 * kx == m) ? 1.0 : 2.0;
+        sum += w * (b[kx].x * t.x - b[kx].y * t.y);
+        idx += ix;
+        if (idx >= m) idx -= m;
+      }
+      r[s] = sum;
+    }
+  }
+
+  // newton_solve, sparse path (lmm.cpp:219-266).
+  __device__ __forceinline__ int newton(double hb0, const double (&c)[E], double (&x)[E], double tol,
+                                        int max_iter, int& iters) {
+    for (int iter = 1; iter <= max_iter; ++iter) {
+      double f[E], r[E];
+      if (!rhs(x, f)) {
+        iters += iter;
+        return kInvalidRhs;
+      }
+#pragma unroll
+      for (int s = 0; s < E; ++s) r[s] = x[s] - hb0 * f[s] - c[s];
+      if (!prepare(hb0)) {
+        iters += iter;
+        return kSingular;
+      }
+      solve(r);
+      double dn = 0.0, xn = 0.0;
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        if (!own(s)) continue;
+        x[s] -= r[s];
+        dn = ref_max(dn, fabs(r[s]));
+        xn = ref_max(xn, fabs(x[s]));
+      }
+      int dummy = 1;
+      adv_reduce2(dn, xn, dummy, sm.red);
+      if (!isfinite(xn) || !isfinite(dn)) {
+        iters += iter;
+        return kInvalidRhs;
+      }
+      if (dn <= tol * (1.0 + xn)) {
+        iters += iter;
+        return kOk;
+      }
+    }
+    iters += max_iter;
+    return kNewtonDivergence;
+  }
+
+  // ---- the ramp (lmm.cpp:400-452), runtime order, as Propagator::step_rt
+  __device__ __forceinline__ void ab_step(int q, double h, double (&out)[E]) const {
+#pragma unroll
+    for (int s = 0; s < E; ++s) out[s] = 0.0 + 1.0 * xs[0][s];
+#pragma unroll
+    for (int i = 1; i <= FD; ++i) {
+      if (i <= q) {
+        const double hb = h * ab_beta(q, i);
+#pragma unroll
+        for (int s = 0; s < E; ++s) out[s] += hb * fs[i - 1][s];
+      }
+    }
+  }
+  __device__ __forceinline__ void implicit_terms(int pa, double h, double (&c)[E]) const {
+    if constexpr (FAM == kAM) {
+#pragma unroll
+      for (int s = 0; s < E; ++s) c[s] = 0.0 + 1.0 * xs[0][s];
+#pragma unroll
+      for (int i = 1; i < FD + 1; ++i) {
+        if (i < pa) {
+          const double hb = h * am_beta(pa, i);
+#pragma unroll
+          for (int s = 0; s < E; ++s) c[s] += hb * fs[i - 1][s];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < E; ++s) c[s] = 0.0;
+#pragma unroll
+      for (int i = 0; i < SD; ++i) {
+        if (i < pa) {
+          const double a = bdf_alpha(pa, i);
+#pragma unroll
+          for (int s = 0; s < E; ++s) c[s] += a * xs[i][s];
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void extrapolate(int q, double (&out)[E]) const {
+#pragma unroll
+    for (int s = 0; s < E; ++s) out[s] = 0.0;
+    double binom = static_cast<double>(q) + 1.0;
+    double sign = 1.0;
+#pragma unroll
+    for (int i = 0; i < SD; ++i) {
+      if (i <= q) {
+        const double coef = sign * binom;
+#pragma unroll
+        for (int s = 0; s < E; ++s) out[s] += coef * xs[i][s];
+        sign = -sign;
+        binom = binom * static_cast<double>(q + 1 - (i + 1)) / static_cast<double>(i + 2);
+      }
+    }
+  }
+  __device__ __forceinline__ void push(const double (&x)[E], const double (&f)[E]) {
+#pragma unroll
+    for (int i = SD - 1; i > 0; --i)
+#pragma unroll
+      for (int s = 0; s < E; ++s) xs[i][s] = xs[i - 1][s];
+#pragma unroll
+    for (int i = FD - 1; i > 0; --i)
+#pragma unroll
+      for (int s = 0; s < E; ++s) fs[i][s] = fs[i - 1][s];
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      xs[0][s] = x[s];
+      fs[0][s] = f[s];
+    }
+  }
+
+  __device__ __forceinline__ int step(int pa, int av, double h, double tol, int max_iter, double (&gamma)[E],
+                                      int& iters) {
+    double xnew[E], ref[E];
+    double factor;
+    if constexpr (FAM == kAB) {
+      ab_step(pa, h, xnew);
+      if (av >= pa + 1) {
+        ab_step(pa + 1, h, ref);
+      } else if (pa >= 2) {
+        ab_step(pa - 1, h, ref);
+      } else {
+#pragma unroll
+        for (int s = 0; s < E; ++s) ref[s] = xs[0][s];
+      }
+      factor = 1.0;
+    } else {
+      double c[E];
+      implicit_terms(pa, h, c);
+      ab_step(pa, h, xnew);
+      if constexpr (FAM == kAM) {
+#pragma unroll
+        for (int s = 0; s < E; ++s) ref[s] = xnew[s];
+        factor = fabs(am_C(pa)) / fabs(ab_C(pa) - am_C(pa));
+      } else {
+        if (av >= pa + 1) {
+          extrapolate(pa, ref);
+          factor = fabs(bdf_C(pa)) / fabs(1.0 - bdf_C(pa));
+        } else if (av < 2) {
+#pragma unroll
+          for (int s = 0; s < E; ++s) ref[s] = xnew[s];
+          factor = fabs(bdf_C(pa)) / fabs(ab_C(pa) - bdf_C(pa));
+        } else {
+          extrapolate(av - 1, ref);
+          factor = fabs(bdf_C(pa)) / fabs(1.0 - bdf_C(pa));
+        }
+      }
+      const double b0 = FAM == kAM ? am_beta(pa, 0) : bdf_beta0(pa);
+      const int st = newton(h * b0, c, xnew, tol, max_iter, iters);
+      if (st != kOk) return st;
+    }
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const double est = factor * fabs(xnew[s] - ref[s]);
+      gamma[s] += est * est;
+    }
+    double fnew[E];
+    if (!rhs(xnew, fnew)) return kInvalidRhs;
+    push(xnew, fnew);
+    return kOk;
+  }
+
+  // propagate_interval (lmm.cpp:468-503); x <- the last accepted state.
+  __device__ __forceinline__ int run(double (&x)[E], double t0, double h, int msteps, double tol, int max_iter,
+                                     double (&gamma)[E], int& iters) {
+    (void)t0;  // the operator is time-invariant
+#pragma unroll
+    for (int s = 0; s < E; ++s) gamma[s] = 0.0;
+    double f0[E];
+    if (!rhs(x, f0)) return kInvalidRhs;
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      xs[0][s] = x[s];
+      fs[0][s] = f0[s];
+    }
+    int st = kOk;
+    for (int k = 1; k <= msteps && st == kOk; ++k)
+      st = step(cmin(k, ORD), cmin(k, 4), h, tol, max_iter, gamma, iters);
+#pragma unroll
+    for (int s = 0; s < E; ++s) x[s] = xs[0][s];
+    return st;
+  }
+
+  // adaptive_bdf_interval (lmm.cpp:894-1019), block form of
+  // Propagator::run_adaptive: every control decision is made on block-reduced
+  // scalars, so all threads follow the same path.
+  __device__ __forceinline__ int run_adaptive(double (&x)[E], double t0, double t1, double rtol, double tol,
+                                              int max_iter, double (&gamma)[E], int& iters) {
+#pragma unroll
+    for (int s = 0; s < E; ++s) gamma[s] = 0.0;
+    const double total = t1 - t0;
+    const double h_min = total * 1e-10;
+    double fcur[E], xm1[E], xm2[E];
+#pragma unroll
+    for (int s = 0; s < E; ++s) xm1[s] = xm2[s] = 0.0;
+    double tm1 = 0.0, tm2 = 0.0;
+    int npoints = 1;
+    long long steps = 0;
+    if (!rhs(x, fcur)) return kInvalidRhs;
+    double t = t0;
+    double h = total * 1e-2;
+    while (t < t1 - total * 1e-12) {
+      h = ref_min(h, t1 - t);
+      if (h < h_min) return kStiffness;
+      const int p = npoints >= 2 ? 2 : 1;
+      const double t_next = t + h;
+      double hb0, factor, c[E], pred[E];
+      if (p == 1) {
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          c[s] = x[s];
+          pred[s] = x[s] + h * fcur[s];
+        }
+        hb0 = h;
+        factor = 0.5;
+      } else {
+        const double h_prev = t - tm1;
+        const double omega = h / h_prev;
+        const double a2 = -(omega * omega) / (1.0 + 2.0 * omega);
+        hb0 = h * (1.0 + omega) / (1.0 + 2.0 * omega);
+#pragma unroll
+        for (int s = 0; s < E; ++s) c[s] = x[s] + a2 * (xm1[s] - x[s]);
+        if (npoints >= 3) {
+          const double dt1 = t - tm1;
+          const double dt2 = tm1 - tm2;
+#pragma unroll
+          for (int s = 0; s < E; ++s) {
+            const double dd1 = (x[s] - xm1[s]) / dt1;
+            const double dd1p = (xm1[s] - xm2[s]) / dt2;
+            const double dd2 = (dd1 - dd1p) / (t - tm2);
+            pred[s] = x[s] + h * dd1 + h * (h + dt1) * dd2;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < E; ++s) pred[s] = x[s] + omega * (x[s] - xm1[s]);
+        }
+        factor = 2.0 / 11.0;
+      }
+      double xnew[E];
+#pragma unroll
+      for (int s = 0; s < E; ++s) xnew[s] = pred[s];
+      if (newton(hb0, c, xnew, tol, max_iter, iters) != kOk) {
+        h *= 0.25;
+        continue;
+      }
+      double err = 0.0, xn = 0.0;
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        if (!own(s)) continue;
+        err = ref_max(err, factor * fabs(xnew[s] - pred[s]));
+        xn = ref_max(xn, fabs(xnew[s]));
+      }
+      int dummy = 1;
+      adv_reduce2(err, xn, dummy, sm.red);
+      const double est_rel = err / (1.0 + xn);
+      double growth;
+      if (est_rel == 0.0) {
+        growth = 4.0;
+      } else {
+        growth = 0.9 * pow(rtol / est_rel, 1.0 / (static_cast<double>(p) + 1.0));
+        growth = ref_clamp(growth, 0.25, 4.0);
+      }
+      if (est_rel <= rtol) {
+        if (!rhs(xnew, fcur)) return kInvalidRhs;
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          xm2[s] = xm1[s];
+          xm1[s] = x[s];
+          x[s] = xnew[s];
+        }
+        tm2 = tm1;
+        tm1 = t;
+        t = t_next;
+        npoints = npoints + 1 < 3 ? npoints + 1 : 3;
+        ++steps;
+      }
+      h *= growth;
+    }
+    const double g = rtol * static_cast<double>(steps);
+#pragma unroll
+    for (int s = 0; s < E; ++s) gamma[s] = g;
+    return kOk;
+  }
+};
+
+// Binds the particle's operator: stencil from theta (natural), twiddles
+// into shared memory, lambda spectrum.
+template <class PR>
+__device__ __forceinline__ void adv_bind(PR& pr, const Ctx& c, char* smem, const double* th_nat) {
+  pr.m = c.adv_m;
+  pr.d = c.adv_d;
+  pr.H = adv_half(pr.m);
+  pr.sm = adv_carve(smem, pr.m);
+  for (int k = threadIdx.x; k < pr.m; k += kAT) pr.sm.tw[k] = c.adv_tw[k];
+  adv_stencil(th_nat, pr.st);
+  pr.have_imu = false;
+  pr.cached_hb0 = 0.0;
+  __syncthreads();
+  pr.spectrum();
+  __syncthreads();
+}
+
+// filter::log_likelihood (filter.cpp:124-141) on the published vector, thread 0.
+__device__ __forceinline__ double adv_loglik(const Ctx& c, const StepParams& sp, const double* xs) {
+  double ss = 0.0;
+  for (int k = 0; k < c.m_y; ++k) {
+    const double r = sp.y[k] - xs[c.obs_idx[k]];
+    ss += r * r;
+  }
+  return sp.ll_const - ss / c.two_s2;
+}
+
+template <int E>
+__device__ __forceinline__ void adv_publish(const AdvSmem& sm, int d, const double (&x)[E]) {
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = threadIdx.x + s * kAT;
+    if (e < d) sm.xs[e] = x[s];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- K1
+// One CTA per particle: shrink, Psi, log-likelihood, fitness log-weight.
+// The fitness log-sum-exp and the exact-CDF tile partials follow in
+// k_lg_reduce (the tail of k_predict over lg).
+template <int FAM, int ORD, int E>
+__global__ void __launch_bounds__(kAT) k_adv_predict(Ctx c) {
+  extern __shared__ __align__(16) char adv_smem[];
+  if (grid_error(c)) return;
+  const StepParams& sp = *c.sp;
+  const DevState& st = *c.st;
+  const long long n = blockIdx.x;
+  const double* rec = c.rec[st.cur] + n * c.R;
+  AdvProp<FAM, ORD, E> pr;
+  {
+    // shrink (filter.cpp:118) + to_natural (models.cpp:18-25: k1, k2 positive)
+    double th[kAdvP];
+#pragma unroll
+    for (int k = 0; k < kAdvP; ++k) {
+      const double tb = c.a * __ldg(rec + c.adv_d + k) + c.one_minus_a * st.mu[k];
+      th[k] = k < 2 ? exp(tb) : tb;
+    }
+    adv_bind(pr, c, adv_smem, th);
+  }
+  double x[E], gamma[E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = threadIdx.x + s * kAT;
+    x[s] = e < c.adv_d ? __ldg(rec + e) : 0.0;
+  }
+  int iters = 0, status;
+  if constexpr (ORD == 0)
+    status = pr.run_adaptive(x, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
+  else
+    status = pr.run(x, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+  adv_publish(pr.sm, c.adv_d, x);
+  if (threadIdx.x == 0) {
+    const double ll = status == kOk ? adv_loglik(c, sp, pr.sm.xs) : kNegInf;
+    c.llbar[n] = ll;
+    c.lg[n] = (c.lw[n] - st.lse_w) + ll;
+    if (FAM != kAB && iters) atomicAdd(&c.st->newton_iters, static_cast<unsigned long long>(iters));
+  }
+}
+
+// ---------------------------------------------------------------- K3
+// One CTA per slot n: gather of ancestor anc[n] (written by the search
+// pass), proliferation, repropagation, innovation, log-likelihood, reweight;
+// writes the next record buffer and lw. The moments follow in k_adv_moments.
+template <int FAM, int ORD, int E>
+__global__ void __launch_bounds__(kAT) k_adv_update(Ctx c) {
+  extern __shared__ __align__(16) char adv_smem[];
+  if (grid_error(c)) return;
+  const DevState& st = *c.st;
+  if (st.chol_failed) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(&c.st->error, kErrChol);
+    return;
+  }
+  const StepParams& sp = *c.sp;
+  const long long n = blockIdx.x;
+  const unsigned a = __ldg(&c.anc[n]);
+  const double* rec = c.rec[st.cur] + static_cast<long long>(a) * c.R;
+  double* out = c.rec[st.cur ^ 1] + n * c.R;
+  AdvProp<FAM, ORD, E> pr;
+  __shared__ double s_tb[kAdvP], s_th[kAdvP];
+  if (threadIdx.x == 0) {
+    // shrink of the ancestor + proliferation (filter.cpp:185-196)
+    double z[kAdvP];
+    stream_normals<kAdvP>(c.seed, sp.j, c.n0 + n, kProliferate, z);
+#pragma unroll
+    for (int r = 0; r < kAdvP; ++r) {
+      double tb = c.a * __ldg(rec + c.adv_d + r) + c.one_minus_a * st.mu[r];
+      double dot = 0.0;
+#pragma unroll
+      for (int q = 0; q <= r; ++q) dot += st.L[r * kAdvP + q] * z[q];
+      tb += c.s_prolif * dot;
+      s_tb[r] = tb;
+      s_th[r] = r < 2 ? exp(tb) : tb;
+    }
+  }
+  __syncthreads();
+  {
+    double th[kAdvP];
+#pragma unroll
+    for (int k = 0; k < kAdvP; ++k) th[k] = s_th[k];
+    adv_bind(pr, c, adv_smem, th);
+  }
+  double x[E], xr[E], gamma[E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = threadIdx.x + s * kAT;
+    x[s] = e < c.adv_d ? __ldg(rec + e) : 0.0;
+    xr[s] = x[s];
+  }
+  int iters = 0, status;
+  if constexpr (ORD == 0)
+    status = pr.run_adaptive(xr, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
+  else
+    status = pr.run(xr, sp.t_prev, sp.h, sp.m, c.tol, c.max_iter, gamma, iters);
+  if (status == kOk) {
+    // innovate (filter.cpp:201-208): x_k += sqrt(gamma_k) z_k, z from stream (seed, j, n, innovate)
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int e = threadIdx.x + s * kAT;
+      if (e < c.adv_d) xr[s] += sqrt(gamma[s]) * normal_at(c.seed, sp.j, c.n0 + n, kInnovate, e);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < E; ++s) xr[s] = x[s];
+  }
+  adv_publish(pr.sm, c.adv_d, xr);
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = threadIdx.x + s * kAT;
+    if (e < c.adv_d) out[e] = xr[s];
+  }
+  if (threadIdx.x < kAdvP) out[c.adv_d + threadIdx.x] = s_tb[threadIdx.x];
+  if (threadIdx.x >= kAdvP && c.adv_d + threadIdx.x < c.R) out[c.adv_d + threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) {
+    const double ll = status == kOk ? adv_loglik(c, sp, pr.sm.xs) : kNegInf;
+    c.lw[n] = ll - __ldg(&c.llbar[a]);  // update_weights (filter.cpp:214)
+    if (FAM != kAB && iters) atomicAdd(&c.st->newton_iters, static_cast<unsigned long long>(iters));
+  }
+}
+
+// One noise-free truth trajectory (bench.cpp:296-317 over
+// lmm::adaptive_bdf_interval), one particle CTA: prm = theta_nat[5], x0[d].
+template <int E>
+__global__ void __launch_bounds__(kAT) k_adv_trajectory(Ctx c, const double* prm, const double* times, int T,
+                                                        double t0, double rtol, double* out, int* status) {
+  extern __shared__ __align__(16) char adv_smem[];
+  AdvProp<kBDF, 0, E> pr;
+  double th[kAdvP];
+#pragma unroll
+  for (int k = 0; k < kAdvP; ++k) th[k] = prm[k];
+  adv_bind(pr, c, adv_smem, th);
+  double x[E], gamma[E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int e = threadIdx.x + s * kAT;
+    x[s] = e < c.adv_d ? prm[kAdvP + e] : 0.0;
+  }
+  double tp = t0;
+  int iters = 0;
+  if (threadIdx.x == 0) status[0] = 0;
+  for (int r = 0; r < T; ++r) {
+    const int st = pr.run_adaptive(x, tp, times[r], rtol, c.tol, c.max_iter, gamma, iters);
+    if (st != kOk) {
+      if (threadIdx.x == 0) status[0] = st;
+      return;
+    }
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int e = threadIdx.x + s * kAT;
+      if (e < c.adv_d) out[static_cast<long long>(r) * c.adv_d + e] = x[s];
+    }
+    tp = times[r];
+  }
+}
+
+}  // namespace pfsmc_gpu

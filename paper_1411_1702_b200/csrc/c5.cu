@@ -254,7 +254,15 @@ pfsmc_gpu_status pfsmc_gpu_model_trajectory(int model, const double* model_const
                                             const double* x0, const double* times, uint64_t T, double t0,
                                             double rtol, int device, double* states_out) {
   return guarded([&] {
-    auto ks = make_kernels(model, PFSMC_GPU_BDF, 0);
+    CK(cudaSetDevice(device));
+    int grid_n = 0;
+    if (model == PFSMC_GPU_MODEL_ADVDIFF) {
+      const double gn = model_consts ? model_consts[0] : 0.0;
+      if (!(gn == std::floor(gn)) || gn < 4.0 || gn > 33.0)
+        throw ConfigError("advdiff model: the GPU path supports 4 <= n <= 33");
+      grid_n = static_cast<int>(gn);
+    }
+    auto ks = make_kernels(model, PFSMC_GPU_BDF, 0, grid_n);
     if (!ks) throw ConfigError("unknown model id");
     if (!(rtol > 0.0)) throw ConfigError("adaptive_bdf_interval: rtol must be positive");
     if (T == 0) return PFSMC_GPU_OK;

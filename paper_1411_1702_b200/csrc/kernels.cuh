@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <memory>
+#include <vector>
 
 #include "../../include/pfsmc_gpu.h"
 #include "exact_cdf.cuh"
@@ -13,7 +14,8 @@
 
 namespace pfsmc_gpu {
 
-constexpr int kMaxObs = 8;
+constexpr int kMaxObs = 8;               // register models (loglik<M> unrolls to this)
+constexpr int kMaxObsAdv = 32;           // the advection-diffusion model (20 sites in the reference)
 constexpr int kMaxWin = 64;              // windows per tile before serial fallback
 constexpr double kNegInf = -INFINITY;
 
@@ -26,7 +28,7 @@ struct StepParams {
   int m;
   int pad;
   double t_obs;       // interval end (the adaptive integrator's t1)
-  double y[kMaxObs];  // observations (log y for the lognormal kind)
+  double y[kMaxObsAdv];  // observations (log y for the lognormal kind)
   double ll_const;    // -0.5 m (log 2pi + log s2)   (filter.cpp:140, host glibc log)
   double sly;         // sum log y (lognormal extension only)
 };
@@ -39,11 +41,11 @@ struct DevState {
   int pad;
   double lse_w;       // logw_n = lw_n - lse_w
   double lse_g;       // fitness log-normaliser of the current step
-  double mu[4];       // shrink mean = weighted mean of the current params
-  double cov[16];     // cov_u (p x p)
-  double L[16];       // chol_psd(cov_u), consumed by the next proliferation
+  double mu[8];       // shrink mean = weighted mean of the current params
+  double cov[64];     // cov_u (p x p), p <= 8
+  double L[64];       // chol_psd(cov_u), consumed by the next proliferation
   double jitter;
-  double trace[2 * 4 + 8 + 1];
+  double trace[2 * 8 + 8 + 1];  // theta mean/var, state mean (d <= 8; larger d: Ctx::xmean), ess
   unsigned long long newton_iters;
   double total_mass;  // exact CDF total (diagnostic)
   unsigned long long tstamp[8];  // %globaltimer probes (diagnostics)
@@ -81,7 +83,7 @@ struct ThreadRec {
 struct Ctx {
   int N, R, ntiles;
   int m_y, likelihood;
-  int obs_idx[kMaxObs];
+  int obs_idx[kMaxObsAdv];
   double a, one_minus_a, s_prolif;  // s = sqrt(1 - a^2)
   double tol;
   int max_iter;
@@ -91,6 +93,11 @@ struct Ctx {
   double rtol;       // adaptive BDF(1,2) tolerance (IntegratorSpec.rtol)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
+  // ---- advection-diffusion model (grid m x m, d = m^2; kernels_advdiff.cu) ----
+  int adv_m, adv_d;
+  const double2* adv_tw;  // (cos, sin)(2 pi k / m), k < m
+  double* xmean;          // state mean of the trace row (d doubles)
+  double* xmean_part;     // its per-chunk partials
   double* rec[2];
   double* payload;     // slot-ordered ancestor payloads {record, ll_bar, index} (R + 2 doubles)
   double* lw;
@@ -855,6 +862,10 @@ struct KernelSet {
   virtual void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) = 0;
   virtual void finish_moments(const Ctx& c, const double* gp, int ngroups, int flags, cudaStream_t s) = 0;
   virtual int moment_width() const = 0;
+  // block-per-particle models: ancestors only from the serve pass (the
+  // update kernel gathers the ancestor record itself) and the state mean of
+  // the trace row in Ctx::xmean
+  virtual bool block_model() const { return false; }
   int d = 0, p = 0;
 };
 
@@ -915,9 +926,13 @@ std::unique_ptr<KernelSet> make_kernels_robertson(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_chain(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_payload(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_metabolic(int fam, int order);
+// AdvDiffModel (models.cpp:158-266): one CTA per particle (kernels_advdiff.cu)
+std::unique_ptr<KernelSet> make_kernels_advdiff(int fam, int order, int grid_n);
+std::vector<double2> adv_twiddles(int m);  // (cos, sin)(2 pi k / m)
 
-inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order) {
+inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order, int grid_n = 0) {
   switch (model) {
+    case PFSMC_GPU_MODEL_ADVDIFF: return make_kernels_advdiff(fam, order, grid_n);
     case DecayModel::ID: return make_kernels_decay(fam, order);
     case LotkaVolterraModel::ID: return make_kernels_lv(fam, order);
     case RobertsonModel::ID: return make_kernels_robertson(fam, order);

@@ -1,0 +1,6 @@
+// AdvDiffModel kernel sets with E = 3 state element(s) per thread (d <= 3 x 128).
+#include "advdiff_set.cuh"
+
+namespace pfsmc_gpu {
+std::unique_ptr<KernelSet> adv_family_e3(int fam, int order, int n) { return adv_family<3>(fam, order, n); }
+}  // namespace pfsmc_gpu

@@ -117,7 +117,10 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   if (timed) CK(cudaEventRecord(ev[2], st));
   launch_scan(c, s->ntiles, st, 2);
   if (timed) CK(cudaEventRecord(ev[3], st));
-  launch_serve(c, s->grid, st);
+  if (s->ks->block_model())
+    launch_search_only(c, s->grid, st);  // the update CTAs gather their ancestor themselves
+  else
+    launch_serve(c, s->grid, st);
   if (timed) CK(cudaEventRecord(ev[4], st));
   s->ks->update(c, s->grid, st);
   if (timed) CK(cudaEventRecord(ev[5], st));
@@ -130,12 +133,32 @@ void enqueue_prologue(pfsmc_gpu_sampler* s) {
   CK(cudaMemsetAsync(&s->st->newton_iters, 0, sizeof(unsigned long long), s->stream));
 }
 
+// The step's host-visible state: DevState (+ the trace row's state mean for
+// the block-per-particle models, Ctx::xmean).
+void enqueue_readback(pfsmc_gpu_sampler* s) {
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  if (s->xmean_host)
+    CK(cudaMemcpyAsync(s->xmean_host, s->ctx.xmean, sizeof(double) * s->d, cudaMemcpyDeviceToHost, s->stream));
+}
+
+// TraceRow (filter.hpp:67-75): theta_mean[p], theta_var[p], state_mean[d], ess.
+void fill_trace(const pfsmc_gpu_sampler* s, const DevState& h, const double* xmean, double* out) {
+  const int p = s->p, d = s->d;
+  if (!s->ks->block_model()) {
+    for (int k = 0; k < 2 * p + d + 1; ++k) out[k] = h.trace[k];
+    return;
+  }
+  for (int k = 0; k < 2 * p; ++k) out[k] = h.trace[k];
+  for (int k = 0; k < d; ++k) out[2 * p + k] = xmean[k];
+  out[2 * p + d] = h.trace[2 * p + 1];  // AdvThetaView: one placeholder state slot, then ess
+}
+
 void build_graph(pfsmc_gpu_sampler* s) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
   enqueue_prologue(s);
   enqueue_kernels(s, false);
-  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  enqueue_readback(s);
   CK(cudaStreamEndCapture(s->stream, &g));
   CK(cudaGraphInstantiate(&s->graph, g, 0));
   CK(cudaGraphDestroy(g));
@@ -171,7 +194,7 @@ void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepPar
   if (s->timing) {
     enqueue_prologue(s);
     enqueue_kernels(s, true);
-    CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    enqueue_readback(s);
   } else {
     CK(cudaGraphLaunch(s->graph, s->stream));
   }
@@ -203,12 +226,25 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
         throw ConfigError("scheme_coefficients: order must be 1, 2 or 3");
       if (cfg->family < 0 || cfg->family > 2) throw ConfigError("scheme_coefficients: unknown family");
     }
-    if (cfg->n_obs > static_cast<uint64_t>(kMaxObs)) throw ConfigError("config: at most 8 observed components");
+    const bool adv = cfg->model == PFSMC_GPU_MODEL_ADVDIFF;
+    if (cfg->n_obs > static_cast<uint64_t>(adv ? kMaxObsAdv : kMaxObs))
+      throw ConfigError(adv ? "config: at most 32 observed components" : "config: at most 8 observed components");
+    int grid_n = 0;
+    if (adv) {
+      // AdvDiffModel(n) (models.cpp:185-188): n >= 3; the GPU path needs a
+      // grid side m = n - 1 >= 3 (distinct stencil columns) and <= 32
+      const double gn = cfg->model_consts[0];
+      if (!(gn == std::floor(gn)) || gn < 3.0) throw ConfigError("advdiff model: grid parameter n must be >= 3");
+      if (gn < 4.0 || gn > 33.0) throw ConfigError("advdiff model: the GPU path supports 4 <= n <= 33");
+      grid_n = static_cast<int>(gn);
+      if (shard_api) throw ConfigError("advdiff model: sharded handles are not supported");
+    }
     auto s = std::make_unique<pfsmc_gpu_sampler>();
     s->cfg = *cfg;
+    CK(cudaSetDevice(cfg->device));
     // adaptive: the variable-step BDF(1,2) kernels (order slot 0)
-    s->ks = cfg->adaptive ? make_kernels(cfg->model, PFSMC_GPU_BDF, 0)
-                          : make_kernels(cfg->model, cfg->family, cfg->order);
+    s->ks = cfg->adaptive ? make_kernels(cfg->model, PFSMC_GPU_BDF, 0, grid_n)
+                          : make_kernels(cfg->model, cfg->family, cfg->order, grid_n);
     if (!s->ks) throw ConfigError("unknown model id");
     if (cfg->model == MetabolicModel::ID && !(cfg->model_consts[5] > 0.0))
       throw ConfigError("metabolic model: tau must be positive");  // MetabolicModel ctor, models.cpp:104-108
@@ -238,7 +274,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.ntiles = s->ntiles;
     c.m_y = static_cast<int>(cfg->n_obs);
     c.likelihood = cfg->likelihood;
-    for (int k = 0; k < kMaxObs; ++k) c.obs_idx[k] = k < c.m_y ? static_cast<int>(s->obs[k]) : -1;
+    for (int k = 0; k < kMaxObsAdv; ++k) c.obs_idx[k] = k < c.m_y ? static_cast<int>(s->obs[k]) : -1;
     c.a = cfg->shrink_a;
     c.one_minus_a = 1.0 - cfg->shrink_a;
     c.s_prolif = std::sqrt(1.0 - cfg->shrink_a * cfg->shrink_a);
@@ -257,7 +293,22 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     const size_t NT = static_cast<size_t>(s->ntiles);
     c.rec[0] = s->dalloc<double>(N * c.R);
     c.rec[1] = s->dalloc<double>(N * c.R);
-    c.payload = s->dalloc<double>(N * (c.R + 2));
+    // slot-ordered ancestor payloads (k_serve); the block-per-particle
+    // models gather inside their update CTAs instead
+    c.payload = s->ks->block_model() ? nullptr : s->dalloc<double>(N * (c.R + 2));
+    if (adv) {
+      const int m = grid_n - 1;
+      std::vector<double2> tw = adv_twiddles(m);
+      double2* dtw = s->dalloc<double2>(m);
+      CK(cudaMemcpy(dtw, tw.data(), sizeof(double2) * m, cudaMemcpyHostToDevice));
+      c.adv_m = m;
+      c.adv_d = m * m;
+      c.adv_tw = dtw;
+      c.xmean = s->dalloc<double>(static_cast<size_t>(c.adv_d));
+      c.xmean_part = s->dalloc<double>(static_cast<size_t>(c.adv_d) * 64);
+      CK(cudaMemset(c.xmean, 0, sizeof(double) * c.adv_d));
+      CK(cudaMallocHost(&s->xmean_host, sizeof(double) * c.adv_d));
+    }
     c.lw = s->dalloc<double>(N);
     c.llbar = s->dalloc<double>(N);
     c.lg = s->dalloc<double>(N);
@@ -417,7 +468,7 @@ static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vecto
     h.lse_w = 0.0;
     h.error = 0;
     h.chol_failed = 0;
-    for (int k = 0; k < 4; ++k) h.mu[k] = 0.0;
+    for (int k = 0; k < 8; ++k) h.mu[k] = 0.0;
     CK(cudaMemcpyAsync(s->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, s->stream));
     const double lw0 = -std::log(static_cast<double>(s->cfg.particles));  // filter.cpp:86
     s->ks->init(s->ctx, s->grid, s->stream, kind, dprm, lw0);
@@ -466,10 +517,7 @@ pfsmc_gpu_status pfsmc_gpu_step(pfsmc_gpu_sampler* s, const double* y, uint64_t 
     CK(cudaStreamSynchronize(s->stream));
     harvest_timing(s);
     check_error(s);
-    if (trace_out) {
-      const int n = 2 * s->p + s->d + 1;
-      for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
-    }
+    if (trace_out) fill_trace(s, *s->st_host, s->xmean_host, trace_out);
     return PFSMC_GPU_OK;
   });
 }
@@ -508,10 +556,7 @@ pfsmc_gpu_status pfsmc_gpu_synchronize(pfsmc_gpu_sampler* s, double* trace_out) 
     CK(cudaStreamSynchronize(s->stream));
     harvest_timing(s);
     check_error(s);
-    if (trace_out) {
-      const int n = 2 * s->p + s->d + 1;
-      for (int k = 0; k < n; ++k) trace_out[k] = s->st_host->trace[k];
-    }
+    if (trace_out) fill_trace(s, *s->st_host, s->xmean_host, trace_out);
     return PFSMC_GPU_OK;
   });
 }
@@ -521,10 +566,9 @@ pfsmc_gpu_status pfsmc_gpu_run(pfsmc_gpu_sampler* s, double* rows, int* warn) {
     const int w = 2 * s->p + s->d + 1;
     // row 0 from the current ensemble (filter.cpp:409-426)
     s->ks->moments(s->ctx, s->grid, s->stream, 0);
-    DevState h{};
-    CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    enqueue_readback(s);
     CK(cudaStreamSynchronize(s->stream));
-    for (int k = 0; k < w; ++k) rows[k] = h.trace[k];
+    fill_trace(s, *s->st_host, s->xmean_host, rows);
     if (warn) warn[0] = 0;
     int streak = 0;
     for (size_t j = 1; j <= s->resident.size(); ++j) {
@@ -532,8 +576,8 @@ pfsmc_gpu_status pfsmc_gpu_run(pfsmc_gpu_sampler* s, double* rows, int* warn) {
       CK(cudaStreamSynchronize(s->stream));
       harvest_timing(s);
       check_error(s);
-      for (int k = 0; k < w; ++k) rows[j * w + k] = s->st_host->trace[k];
-      const double ess = s->st_host->trace[w - 1];
+      fill_trace(s, *s->st_host, s->xmean_host, rows + j * w);
+      const double ess = rows[j * w + w - 1];
       int flag = 0;
       if (ess < 1.0 + 1e-6) {
         if (++streak >= 3) flag = 1;

@@ -95,6 +95,7 @@ struct pfsmc_gpu_sampler {
   StepParams* sp_host = nullptr;     // pinned
   double* trace_host = nullptr;      // pinned
   DevState* st_host = nullptr;       // pinned
+  double* xmean_host = nullptr;      // pinned: the trace row's state mean (block models)
   double* flush_buf = nullptr;
   long long flush_n = 0;
   // resident observations
@@ -146,6 +147,7 @@ struct pfsmc_gpu_sampler {
     if (sp_host) cudaFreeHost(sp_host);
     if (trace_host) cudaFreeHost(trace_host);
     if (st_host) cudaFreeHost(st_host);
+    if (xmean_host) cudaFreeHost(xmean_host);
     if (counts_host) cudaFreeHost(counts_host);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -178,5 +180,7 @@ void check_error(pfsmc_gpu_sampler* s);
 void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed);
 void enqueue_prologue(pfsmc_gpu_sampler* s);
 void build_graph(pfsmc_gpu_sampler* s);
+void enqueue_readback(pfsmc_gpu_sampler* s);
+void fill_trace(const pfsmc_gpu_sampler* s, const DevState& h, const double* xmean, double* out);
 void harvest_timing(pfsmc_gpu_sampler* s);
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp);

@@ -29,8 +29,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # builds on one box, profiles/ab.py); the default is the in-tree build.
 LIB_PATH = os.environ.get("PFSMC_GPU_LIB") or os.path.join(HERE, "libpfsmc_gpu.so")
 
-MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4, "metabolic": 5}
+MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "payload64": 4, "metabolic": 5, "advdiff": 6}
 MODEL_DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 4: (6, 2), 5: (3, 4)}
+# AdvDiffModel(n) (models.cpp:185-249): grid (n-1)^2, params k1, k2 (positive), k3, c1, c2
+ADVDIFF_DEFAULT_N = 20  # bench::ExperimentConfig.n (bench.hpp:20)
+
+
+def model_dims(model: str, consts=None):
+    """(d, p) of a compiled-in model; advdiff's d comes from its grid parameter."""
+    if model == "advdiff":
+        n = int(consts[0]) if consts else ADVDIFF_DEFAULT_N
+        return (n - 1) * (n - 1), 5
+    return MODEL_DIMS[MODELS[model]]
 # models::MetabolicConstants defaults (models.hpp:67-74): lambda, c0, A0, A, t0_input, tau
 METABOLIC_DEFAULTS = (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
 FAMILIES = {"ab": 0, "am": 1, "bdf": 2}
@@ -68,7 +78,8 @@ class _Config(C.Structure):
 def model_consts_array(model: str, consts=None):
     """The C ABI's model_consts[8] (METABOLIC: MetabolicConstants order)."""
     if consts is None:
-        consts = METABOLIC_DEFAULTS if model == "metabolic" else ()
+        consts = (METABOLIC_DEFAULTS if model == "metabolic" else
+                  (ADVDIFF_DEFAULT_N,) if model == "advdiff" else ())
     v = list(map(float, consts)) + [0.0] * (8 - len(consts))
     return (C.c_double * 8)(*v[:8])
 
@@ -174,7 +185,7 @@ class GpuSampler:
         self.model = model
         self.cfg = cfg
         self.obs = obs
-        self.d, self.p = MODEL_DIMS[MODELS[model]]
+        self.d, self.p = model_dims(model, model_consts)
         self._idx = np.ascontiguousarray(list(obs.indices), dtype=np.uint64)
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed,
                     cfg.newton_tol, cfg.newton_max_iter, cfg.particles,

@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
-from oracle_ctypes import Oracle, Reference, StepConfig  # noqa: E402
+from oracle_ctypes import Oracle, Reference, StepConfig, set_advdiff_grid  # noqa: E402
 
 REF_KAT = "/root/reference/proj/tests/data/philox_vectors.csv"
 
@@ -60,7 +60,21 @@ CASES = {
     "metabolic_bdf2_m4": (dict(model="metabolic", family="bdf", order=2, h=0.05, a=0.98, seed=21,
                                obs_idx=(0, 1, 2), sigma=0.1), 80, "gauss_metabolic",
                           [(1.6 + 0.2 * k, 1.6 + 0.2 * (k + 1), 0.05) for k in range(5)]),
+    # the reference's own AdvDiffModel (problem 2), grid n = 6 (d = 25) / 5 (d = 16): bench.cpp:249-277
+    # priors, the plume x0 as a degenerate prior, sites drawn like generate_data (bench.cpp:327-341)
+    "advdiff_bdf2_n6": (dict(model="advdiff", family="bdf", order=2, h=0.05, a=0.98, seed=17,
+                             obs_idx=(3, 7, 11, 20, 24), sigma=0.05), 48, "gauss_advdiff_6",
+                        [(float(k), float(k + 1), 0.05) for k in range(3)]),
+    "advdiff_am3_n5": (dict(model="advdiff", family="am", order=3, h=0.1, a=0.98, seed=18,
+                            obs_idx=(0, 5, 9, 14), sigma=0.05), 40, "gauss_advdiff_5",
+                       [(float(k), float(k + 1), 0.1) for k in range(3)]),
+    "advdiff_adaptive_n5": (dict(model="advdiff", family="bdf", order=2, a=0.98, seed=19,
+                                 obs_idx=(1, 6, 12), sigma=0.05, adaptive=True, rtol=1e-3), 32,
+                            "gauss_advdiff_5", [(float(k), float(k + 1), 1.0) for k in range(2)]),
 }
+# grid parameter of the advdiff cases (AdvDiffModel(n), model_consts[0])
+CONSTS = {"advdiff_bdf2_n6": (6.0,), "advdiff_am3_n5": (5.0,), "advdiff_adaptive_n5": (5.0,)}
+ADV_TRUTH = np.array([9.0, 4.0, 6.0, 2.5, -1.5])  # bench.cpp:251-255
 
 
 def init_ens(kind, n, seed, O, R, sc):
@@ -73,9 +87,21 @@ def init_ens(kind, n, seed, O, R, sc):
         return R.init_gaussian(sc, n, np.log([0.04, 3e7, 1e4]) + 0.5, [1, 1, 1], [1, 0, 0], [0, 0, 0], [0, 0, 0])
     if kind == "gauss_metabolic":  # bench.cpp:214-237 defaults
         return R.init_gaussian(sc, n, np.log([1.5, 0.7, 1.5, 0.5]), [0.5] * 4, [1.0] * 3, [0.25] * 3, [1, 1, 1])
+    if kind.startswith("gauss_advdiff_"):  # bench.cpp:259-272
+        g = int(kind.rsplit("_", 1)[1])
+        x0 = plume(O, g)
+        return R.init_gaussian(sc, n, [np.log(7.0), np.log(5.0), 4.0, 0.0, 0.0], [0.35, 0.35, 2.0, 2.0, 2.0],
+                               x0, np.zeros_like(x0), np.zeros(len(x0), np.int32))
     if kind == "gauss_decay":
         return R.init_gaussian(sc, n, [np.log(0.8)], [0.4], [2.0], [0.1], [0])
     raise KeyError(kind)
+
+
+def plume(O, g):
+    import ctypes as C
+    x0 = np.zeros((g - 1) ** 2)
+    O.lib.or_gaussian_plume_ic(g, x0.ctypes.data_as(C.POINTER(C.c_double)))
+    return x0
 
 
 def pf_cases():
@@ -83,12 +109,18 @@ def pf_cases():
     rng = np.random.default_rng(2024)
     for name, (kw, n, init, steps) in CASES.items():
         sc = StepConfig(**kw)
+        consts = CONSTS.get(name)
+        if kw["model"] == "advdiff":
+            set_advdiff_grid(int(consts[0]), O, R)
         if steps is None:  # log-spaced Robertson intervals, m = 2
             ts = np.logspace(-4, 3, 400)[:4]
             tp = np.concatenate([[0.0], ts[:-1]])
             steps = [(a, b, (b - a) / 2) for a, b in zip(tp, ts)]
         ens = init_ens(init, n, kw["seed"], O, R, sc)
         d = {"config": json.dumps(kw), "n": n}
+        if consts:
+            d["model_consts"] = np.array(consts)
+        truth = plume(O, int(consts[0])) if kw["model"] == "advdiff" else None
         d["init_states"], d["init_params_u"], d["init_logw"] = ens.states.copy(), ens.params_u.copy(), ens.logw.copy()
         d["init_mean_u"], d["init_cov_u"] = ens.mean_u.copy(), ens.cov_u.copy()
         d["steps"] = np.array(steps)
@@ -101,6 +133,9 @@ def pf_cases():
                 y = np.array([0.09 * j, 0.001 * j, 0.0]) + 0.01 * rng.standard_normal(3)
             elif kw["model"] == "metabolic":
                 y = np.array([1.0, 1.2, 1.1]) + 0.1 * rng.standard_normal(3)
+            elif kw["model"] == "advdiff":  # truth path (fine BDF2) + N(0, sigma^2) at the sites
+                truth = O.propagate("advdiff", ADV_TRUTH, truth, t0, t1, 0.01, "bdf", 2)[0]
+                y = truth[list(kw["obs_idx"])] + kw["sigma"] * rng.standard_normal(len(kw["obs_idx"]))
             elif kw["model"] == "robertson":
                 y = np.array([1 - 0.04 * t1, 0.04 * t1 * 1e-3]) + 1e-3 * rng.standard_normal(2)
             else:
@@ -113,6 +148,8 @@ def pf_cases():
                 d[f"s{j}_{f}"] = getattr(ens, f).copy()
         d["ys"] = np.array(ys)
         np.savez_compressed(os.path.join(HERE, f"pf_{name}.npz"), **d)
+        O.set_model_consts()
+        R.set_model_consts()
         print("wrote", name)
 
 
@@ -131,7 +168,12 @@ def resample_cases():
 
 
 if __name__ == "__main__":
-    philox_kats()
-    streams()
-    pf_cases()
-    resample_cases()
+    only = sys.argv[1:]  # optional case-name filter (pf cases only)
+    if only:
+        CASES = {k: v for k, v in CASES.items() if any(o in k for o in only)}
+        pf_cases()
+    else:
+        philox_kats()
+        streams()
+        pf_cases()
+        resample_cases()

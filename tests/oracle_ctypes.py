@@ -20,8 +20,17 @@ ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libpfsmc_ref.so")
 
 FAMILIES = {"ab": 0, "am": 1, "bdf": 2}
-MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "metabolic": 5}
-DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 5: (3, 4)}
+MODELS = {"decay": 0, "lv": 1, "robertson": 2, "chain": 3, "metabolic": 5, "advdiff": 6}
+DIMS = {0: (1, 1), 1: (2, 2), 2: (3, 3), 3: (8, 4), 5: (3, 4), 6: (19 * 19, 5)}
+# AdvDiffModel parameters (models.cpp:242-249): k1, k2 positive (log space); k3, c1, c2 not
+ADVDIFF_POSITIVE = (True, True, False, False, False)
+
+
+def set_advdiff_grid(n, *checkers):
+    """Binds AdvDiffModel(n) (grid (n-1)^2) in every checker given and in DIMS."""
+    DIMS[6] = ((n - 1) * (n - 1), 5)
+    for c in checkers:
+        c.set_model_consts((float(n),))
 # models::MetabolicConstants defaults (models.hpp:67-74): lambda, c0, A0, A, t0_input, tau
 METABOLIC_DEFAULTS = (1.0, 1.0, 1.0, 5.0, 2.0, 1.0)
 LIKELIHOODS = {"gaussian": 0, "lognormal": 1}

@@ -235,7 +235,7 @@ def test_against_reference_fixtures(case):
     kw = json.loads(str(d["config"]))
     sc = StepConfig(**kw)
     n = int(d["n"])
-    gpu = _sampler(sc, n)
+    gpu = _sampler(sc, n, model_consts=tuple(d["model_consts"]) if "model_consts" in d.files else None)
     ens = OEns(d["init_states"], d["init_params_u"], d["init_logw"], d["init_mean_u"], d["init_cov_u"])
     for j, (t0, t1, h) in enumerate(d["steps"], 1):
         gpu.set_ensemble(_to_gpu_ens(ens))

@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle_ctypes import REF_SO, Oracle, OracleError, Reference, StepConfig
+from oracle_ctypes import METABOLIC_DEFAULTS, REF_SO, Oracle, OracleError, Reference, StepConfig, set_advdiff_grid
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 O = Oracle()
@@ -62,16 +62,21 @@ def test_oracle_replays_reference_bitwise(case):
     """Every field of every step equals the unmodified reference bit for bit."""
     d = np.load(os.path.join(GOLD, f"pf_{case}.npz"))
     sc = StepConfig(**json.loads(str(d["config"])))
-    ens = _ens_from(d, "init_")
-    for j, (t0, t1, h) in enumerate(d["steps"], 1):
-        sc.h = float(h)
-        trace, dg = O.pf_step(sc, ens, d["ys"][j - 1], j, float(t0), float(t1), diag=True)
-        assert np.array_equal(dg["ancestors"], d[f"s{j}_anc"])
-        assert np.array_equal(dg["g"], d[f"s{j}_g"])
-        assert np.array_equal(dg["loglik_bar"], d[f"s{j}_llbar"])
-        assert np.array_equal(trace, d[f"s{j}_trace"])
-        for f in ("states", "params_u", "logw", "mean_u", "cov_u"):
-            assert np.array_equal(getattr(ens, f), d[f"s{j}_{f}"]), (case, j, f)
+    if sc.model == "advdiff":
+        set_advdiff_grid(int(d["model_consts"][0]), O)
+    try:
+        ens = _ens_from(d, "init_")
+        for j, (t0, t1, h) in enumerate(d["steps"], 1):
+            sc.h = float(h)
+            trace, dg = O.pf_step(sc, ens, d["ys"][j - 1], j, float(t0), float(t1), diag=True)
+            assert np.array_equal(dg["ancestors"], d[f"s{j}_anc"])
+            assert np.array_equal(dg["g"], d[f"s{j}_g"])
+            assert np.array_equal(dg["loglik_bar"], d[f"s{j}_llbar"])
+            assert np.array_equal(trace, d[f"s{j}_trace"])
+            for f in ("states", "params_u", "logw", "mean_u", "cov_u"):
+                assert np.array_equal(getattr(ens, f), d[f"s{j}_{f}"]), (case, j, f)
+    finally:
+        O.set_model_consts(METABOLIC_DEFAULTS)
 
 
 def test_oracle_resample_matches_reference_fixture():
