@@ -8,14 +8,15 @@
 // ExperimentConfig::set (bench.cpp:110-153); same canonical JSON and FNV-1a
 // config hash (bench.cpp:155-178); same data CSV + .json sidecar input
 // (bench.cpp:398-445), equispaced-grid check (bench.cpp:449-476), problem
-// setup (bench.cpp:188-248, problem "metabolic"), filter::run semantics
+// setup (bench.cpp:188-277, problems "metabolic" and "advdiff"), filter::run semantics
 // (initial row, degeneracy streak; filter.cpp:396-443) and outputs: the trace
 // CSV (bench.cpp:484-499) and the report JSON (bench.cpp:501-527), tagged
 // "<problem>_<integrator>_gpu".
 //
-// Out of scope (ConfigError): problem "advdiff" (the sparse advection-
-// diffusion model). Integrator "adaptive-bdf2" runs the
-// device adaptive BDF(1,2) (lmm.cpp:894-1019) with the config's rtol.
+// Problem "advdiff" runs the reference's AdvDiffModel(n) on the
+// particle-per-CTA kernels (csrc/advdiff.cuh; the GPU path needs
+// 4 <= n <= 33). Integrator "adaptive-bdf2" runs the device adaptive
+// BDF(1,2) (lmm.cpp:894-1019) with the config's rtol.
 #include <charconv>
 #include <chrono>
 #include <cmath>
@@ -438,20 +439,79 @@ namespace {
 // ---- the problem (build_problem, bench.cpp:188-248) ----------------------
 struct Setup {
   Integrator integ;
+  int model = PFSMC_GPU_MODEL_METABOLIC;
+  std::size_t d = 3, p = 4;
   std::vector<double> th_mu, th_sigma, x_mean, x_std;
   std::vector<int> x_clamp;
   std::vector<std::string> param_names;
+  std::vector<int> param_positive;
+  std::vector<double> truth, x0_truth, obs_times;  // natural-space truth, x(0), observation times
+  bool fixed_obs_indices = true;                   // problem 1 observes everything
   double consts[8] = {};
 };
+
+// models::gaussian_plume_ic (models.cpp:130-156): six Gaussian bumps on the
+// unit square, x varies fastest.
+std::vector<double> gaussian_plume_ic(std::size_t n) {
+  static constexpr double kGamma[6] = {0.04, 0.08, 0.07, 0.10, 0.05, 0.06};
+  static constexpr double kXc[6] = {0.20, 0.30, 0.40, 0.50, 0.50, 0.70};
+  static constexpr double kYc[6] = {0.80, 0.40, 0.40, 0.50, 0.60, 0.50};
+  constexpr double kSqrt2Pi = 2.5066282746310002;
+  const std::size_t m = n - 1;
+  std::vector<double> u(m * m);
+  for (std::size_t iy = 0; iy < m; ++iy) {
+    const double y = static_cast<double>(iy) / static_cast<double>(m);
+    for (std::size_t ix = 0; ix < m; ++ix) {
+      const double x = static_cast<double>(ix) / static_cast<double>(m);
+      double sum = 0.0;
+      for (int i = 0; i < 6; ++i) {
+        const double dx = x - kXc[i];
+        const double dy = y - kYc[i];
+        sum += std::exp(-(dx * dx + dy * dy) / (2.0 * kGamma[i] * kGamma[i])) / (kGamma[i] * kSqrt2Pi);
+      }
+      u[iy * m + ix] = sum;
+    }
+  }
+  return u;
+}
+
+// build_problem, problem "advdiff" (bench.cpp:249-277).
+Setup build_advdiff(const pfsmc_gpu_experiment& cfg, Setup s) {
+  const auto& o = cfg.overrides;
+  if (cfg.n < 3) throw ConfigError("advdiff model: grid parameter n must be >= 3");  // AdvDiffModel ctor
+  s.model = PFSMC_GPU_MODEL_ADVDIFF;
+  s.consts[0] = static_cast<double>(cfg.n);
+  s.d = static_cast<std::size_t>((cfg.n - 1) * (cfg.n - 1));
+  s.p = 5;
+  s.param_names = {"k1", "k2", "k3", "c1", "c2"};
+  s.param_positive = {1, 1, 0, 0, 0};  // AdvDiffModel::params (models.cpp:242-249)
+  s.truth = {override_or(o, "truth.k1", 9.0), override_or(o, "truth.k2", 4.0), override_or(o, "truth.k3", 6.0),
+             override_or(o, "truth.c1", 2.5), override_or(o, "truth.c2", -1.5)};
+  s.x0_truth = gaussian_plume_ic(cfg.n);
+  const double prior_mu[5] = {std::log(7.0), std::log(5.0), 4.0, 0.0, 0.0};
+  const double prior_sd[5] = {0.35, 0.35, 2.0, 2.0, 2.0};
+  for (int k = 0; k < 5; ++k) {
+    s.th_mu.push_back(override_or(o, "prior." + s.param_names[k] + ".mu", prior_mu[k]));
+    s.th_sigma.push_back(override_or(o, "prior." + s.param_names[k] + ".sigma", prior_sd[k]));
+  }
+  // the initial plume is treated as known: a degenerate x0 prior
+  for (const double v : s.x0_truth) {
+    s.x_mean.push_back(v);
+    s.x_std.push_back(0.0);
+    s.x_clamp.push_back(0);
+  }
+  for (int t = 1; t <= 30; ++t) s.obs_times.push_back(static_cast<double>(t));
+  s.fixed_obs_indices = false;
+  return s;
+}
 
 Setup build_problem(const pfsmc_gpu_experiment& cfg) {
   Setup s;
   s.integ = parse_integrator(cfg.integrator);
   if (!(cfg.shrink_a > 0.0 && cfg.shrink_a < 1.0)) throw ConfigError("shrink-a must lie strictly between 0 and 1");
-  if (cfg.problem != "metabolic")
-    throw ConfigError("problem '" + cfg.problem +
-                      "' (sparse advection-diffusion) is not implemented by the GPU sampler");
+  if (cfg.problem == "advdiff") return build_advdiff(cfg, s);
   const auto& o = cfg.overrides;
+  s.param_positive = {1, 1, 1, 1};
   // MetabolicConstants (models.hpp:67-74) with const.* overrides
   s.consts[0] = override_or(o, "const.lambda", 1.0);
   s.consts[1] = override_or(o, "const.c0", 1.0);
@@ -474,6 +534,11 @@ Setup build_problem(const pfsmc_gpu_experiment& cfg) {
     s.x_clamp.push_back(1);
   }
   if (cfg.n_obs == 0 || !(cfg.t_end > 0.0)) throw ConfigError("metabolic problem needs n-obs >= 1 and t-end > 0");
+  s.truth = {override_or(o, "truth.V1", 2.0), override_or(o, "truth.k1", 0.5), override_or(o, "truth.V2", 1.0),
+             override_or(o, "truth.k2", 0.8)};
+  for (int k = 0; k < 3; ++k) s.x0_truth.push_back(override_or(o, "x0." + std::to_string(k) + ".truth", 1.0));
+  for (std::uint64_t i = 1; i <= cfg.n_obs; ++i)
+    s.obs_times.push_back(cfg.t_end * static_cast<double>(i) / static_cast<double>(cfg.n_obs));
   return s;
 }
 
@@ -563,7 +628,7 @@ struct SamplerHandle {
 
 void make_sampler(SamplerHandle& out, const pfsmc_gpu_experiment& cfg, const Setup& s, const Loaded& d) {
   pfsmc_gpu_config c{};
-  c.model = PFSMC_GPU_MODEL_METABOLIC;
+  c.model = s.model;
   c.family = s.integ.family;
   c.order = s.integ.order;
   c.shrink_a = cfg.shrink_a;
@@ -587,10 +652,11 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
   const Loaded data = load_data(data_csv);
   if (data.problem != cfg.problem)
     throw ConfigError("data file was generated for problem '" + data.problem + "', config says '" + cfg.problem + "'");
+  if (cfg.problem == "advdiff" && data.n != cfg.n) throw ConfigError("data grid size does not match config n");
   check_time_grid(data, setup.integ.adaptive, cfg.step);
   if (!setup.integ.adaptive && !(cfg.step > 0.0)) throw ConfigError("config: step size h must be positive");
   fs::create_directories(out_dir);
-  const std::size_t T = data.times.size(), p = 4, d = 3;
+  const std::size_t T = data.times.size(), p = setup.p, d = setup.d;
   if (cfg.warmup) {
     // one untimed assimilation step on a scratch ensemble (bench.cpp:559-565)
     SamplerHandle scratch;
@@ -657,8 +723,13 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
     out << "  \"efficiency\": 0.0,\n";
     out << "  \"final_estimate\": " << arr(est) << ",\n";
     out << "  \"final_std_u\": " << arr(sd) << ",\n";
-    out << "  \"param_names\": [\"V1\", \"k1\", \"V2\", \"k2\"],\n";
-    out << "  \"param_positive\": [1, 1, 1, 1],\n";
+    std::string names = "[", pos = "[";
+    for (std::size_t k = 0; k < p; ++k) {
+      names += (k ? ", " : "") + json_str(setup.param_names[k]);
+      pos += (k ? ", " : "") + std::to_string(setup.param_positive[k]);
+    }
+    out << "  \"param_names\": " << names << "],\n";
+    out << "  \"param_positive\": " << pos << "],\n";
     out << "  \"phases\": {\"proliferate\": 0.0, \"propagate\": 0.0, \"repropagate\": 0.0, \"resample\": 0.0, "
            "\"weights\": 0.0},\n";
     out << "  \"speedup\": 0.0,\n";
@@ -678,24 +749,38 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
 // (seed, r + 1, 0, init) of normals on the host, the CSV and the sidecar.
 void generate_impl(const pfsmc_gpu_experiment& cfg, const std::string& csv_path) {
   const Setup setup = build_problem(cfg);
-  const auto& o = cfg.overrides;
-  const std::vector<double> truth = {override_or(o, "truth.V1", 2.0), override_or(o, "truth.k1", 0.5),
-                                     override_or(o, "truth.V2", 1.0), override_or(o, "truth.k2", 0.8)};
-  std::vector<double> x0;
-  for (int k = 0; k < 3; ++k) x0.push_back(override_or(o, "x0." + std::to_string(k) + ".truth", 1.0));
-  std::vector<double> times;
-  for (std::uint64_t i = 1; i <= cfg.n_obs; ++i)
-    times.push_back(cfg.t_end * static_cast<double>(i) / static_cast<double>(cfg.n_obs));
-  const std::size_t d = 3, T = times.size();
+  const std::vector<double>& truth = setup.truth;
+  const std::vector<double>& times = setup.obs_times;
+  const std::size_t d = setup.d, T = times.size();
   std::vector<double> traj(T * d);
-  check_gpu(pfsmc_gpu_model_trajectory(PFSMC_GPU_MODEL_METABOLIC, setup.consts, truth.data(), x0.data(),
+  check_gpu(pfsmc_gpu_model_trajectory(setup.model, setup.consts, truth.data(), setup.x0_truth.data(),
                                        times.data(), T, 0.0, 1e-8, cfg.device, traj.data()));
-  const std::vector<std::uint64_t> indices = {0, 1, 2};  // problem 1 observes everything
+  // observation sites: fixed for problem 1; 20 distinct random grid nodes
+  // drawn once from stream (seed, 0, 0, init) for problem 2 (bench.cpp:327-341)
+  std::vector<std::uint64_t> indices;
+  if (setup.fixed_obs_indices) {
+    indices = {0, 1, 2};
+  } else {
+    pfsmc_gpu::Stream stream(cfg.seed, 0, 0, pfsmc_gpu::kInit);
+    std::vector<bool> used(d, false);
+    while (indices.size() < 20) {
+      const auto idx = static_cast<std::size_t>(stream.next_uniform() * static_cast<double>(d));
+      if (idx < d && !used[idx]) {
+        used[idx] = true;
+        indices.push_back(idx);
+      }
+    }
+  }
   double sigma = cfg.sigma;
   if (!(sigma > 0.0)) {
     double mx = 0.0;
-    for (const double v : traj) mx = std::max(mx, std::abs(v));
-    sigma = 0.05 * mx;
+    if (cfg.problem == "metabolic") {
+      for (const double v : traj) mx = std::max(mx, std::abs(v));
+      sigma = 0.05 * mx;
+    } else {
+      for (const double v : setup.x0_truth) mx = std::max(mx, std::abs(v));
+      sigma = mx / 50.0;
+    }
   }
   if (!(sigma >= 1e-12)) throw ConfigError("observation noise sigma must be >= 1e-12");
   std::ofstream out(csv_path);
@@ -719,10 +804,14 @@ void generate_impl(const pfsmc_gpu_experiment& cfg, const std::string& csv_path)
     for (std::size_t i = 0; i < v.size(); ++i) a += (i ? ", " : "") + json_num(v[i]);
     return a + "]";
   };
+  std::string idx = "[", names = "[";
+  for (std::size_t k = 0; k < indices.size(); ++k) idx += (k ? ", " : "") + std::to_string(indices[k]);
+  for (std::size_t k = 0; k < setup.param_names.size(); ++k)
+    names += (k ? ", " : "") + json_str(setup.param_names[k]);
   sout << "{\n";
   sout << "  \"n\": " << cfg.n << ",\n";
-  sout << "  \"obs_indices\": [0, 1, 2],\n";
-  sout << "  \"param_names\": [\"V1\", \"k1\", \"V2\", \"k2\"],\n";
+  sout << "  \"obs_indices\": " << idx << "],\n";
+  sout << "  \"param_names\": " << names << "],\n";
   sout << "  \"problem\": " << json_str(cfg.problem) << ",\n";
   sout << "  \"seed\": " << cfg.seed << ",\n";
   sout << "  \"sigma\": " << json_num(sigma) << ",\n";

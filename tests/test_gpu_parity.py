@@ -172,14 +172,22 @@ def test_cumsum_is_sequential():
     assert np.array_equal(np.cumsum(g), np.array(out))
 
 
+def _rel_rows(a, b):
+    """Normwise relative error per particle, max_k |a - b| / max_k |b| over a
+    state vector: the relative error of a field state (the advection-diffusion
+    model's d = (n-1)^2 grid values, many of them near zero)."""
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.max(np.max(np.abs(a - b), axis=1) / np.maximum(np.max(np.abs(b), axis=1), 1e-300)))
+
+
 # ---------------------------------------------------------------- lock-step
-def _compare_step(gpu, ens_o, trace_o, dg, row):
+def _compare_step(gpu, ens_o, trace_o, dg, row, field_state=False):
     anc_g, llb_g, _ = gpu.step_diagnostics()
     got = gpu.get_ensemble()
     mism = np.flatnonzero(anc_g.astype(np.int64) != dg["ancestors"])
     assert mism.size == 0, f"ancestor mismatch at slots {mism[:10]}"
     assert _rel(llb_g, dg["loglik_bar"]) < REL_STATE
-    assert _rel(got.states, ens_o.states) < REL_STATE
+    assert (_rel_rows if field_state else _rel)(got.states, ens_o.states) < REL_STATE
     assert _rel_scaled(got.params_u, ens_o.params_u) < REL_STATE
     w_g, w_o = np.exp(got.logw), np.exp(ens_o.logw)
     assert _rel_scaled(w_g, w_o) < REL_STATE
@@ -242,7 +250,7 @@ def test_against_reference_fixtures(case):
         row = gpu.pf_step(d["ys"][j - 1], j, float(t0), float(t1), h=float(h))
         nxt = OEns(d[f"s{j}_states"], d[f"s{j}_params_u"], d[f"s{j}_logw"], d[f"s{j}_mean_u"], d[f"s{j}_cov_u"])
         dg = {"ancestors": d[f"s{j}_anc"], "loglik_bar": d[f"s{j}_llbar"]}
-        _compare_step(gpu, nxt, d[f"s{j}_trace"], dg, row)
+        _compare_step(gpu, nxt, d[f"s{j}_trace"], dg, row, field_state=sc.model == "advdiff")
         ens = nxt
     gpu.close()
 
