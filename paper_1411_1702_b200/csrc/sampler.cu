@@ -148,7 +148,9 @@ void fill_trace(const pfsmc_gpu_sampler* s, const DevState& h, const double* xme
     for (int k = 0; k < 2 * p + d + 1; ++k) out[k] = h.trace[k];
     return;
   }
-  for (int k = 0; k < 2 * p; ++k) out[k] = h.trace[k];
+  // to_natural of the mean (filter.cpp:381-382): AdvDiffModel's k3, c1, c2 are not log-space
+  for (int k = 0; k < p; ++k) out[k] = k < 2 ? h.trace[k] : h.mu[k];
+  for (int k = p; k < 2 * p; ++k) out[k] = h.trace[k];
   for (int k = 0; k < d; ++k) out[2 * p + k] = xmean[k];
   out[2 * p + d] = h.trace[2 * p + 1];  // AdvThetaView: one placeholder state slot, then ess
 }

@@ -44,7 +44,7 @@ def _setup(n, N, seed, sites, **kw):
     set_advdiff_grid(n, O)
     d = (n - 1) ** 2
     x0 = plume(n)
-    idx = tuple(int(v) % d for v in sites)
+    idx = tuple(dict.fromkeys(int(v) % d for v in sites))  # distinct, in order
     sc = StepConfig(model="advdiff", a=0.98, seed=seed, obs_idx=idx, sigma=float(x0.max() / 10), **kw)
     ens = O.init_gaussian("advdiff", N, seed, PRIOR_MU, PRIOR_SD, x0, np.zeros(d), np.zeros(d, np.int32))
     return sc, ens, x0
@@ -96,8 +96,10 @@ def test_free_running_advdiff():
     d = (n - 1) ** 2
     gpu.initialize_gaussian(PRIOR_MU, PRIOR_SD, x0, np.zeros(d), np.zeros(d, np.int32))
     got = gpu.get_ensemble()
-    assert np.array_equal(got.params_u, ens.params_u) and np.array_equal(got.states, ens.states)
-    assert _rel(got.cov_u, ens.cov_u) < 1e-12
+    # device draws: CUDA log / sincospi vs glibc (<= 2 ulp); the degenerate x0 prior is exact
+    assert np.array_equal(got.states, ens.states)
+    assert np.max(np.abs(got.params_u - ens.params_u)) < 1e-14 * np.max(np.abs(ens.params_u))
+    assert np.max(np.abs(got.cov_u - ens.cov_u)) < 1e-12 * np.max(np.abs(ens.cov_u))
     for j in range(1, steps + 1):
         row = gpu.pf_step(ys[j - 1], j, j - 1.0, float(j))
         trace_o, dg = O.pf_step(sc, ens, ys[j - 1], j, j - 1.0, float(j), diag=True)

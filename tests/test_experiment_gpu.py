@@ -121,3 +121,42 @@ def test_generate_data_matches_reference(kv, tmp_path):
     o = C.c_char_p()
     assert R.pfsmc_run_experiment(r, dg.encode(), str(tmp_path / "o").encode(), C.byref(o)) == 0, \
         R.pfsmc_last_error()
+
+
+# ---- the reference's problem 2 (AdvDiffModel), bench.cpp:249-277 ----------
+@pytest.mark.parametrize("kv", [
+    [("problem", "advdiff"), ("n", "6"), ("particles", "300"), ("integrator", "bdf2"), ("step", "0.05"),
+     ("seed", "3")],
+    [("problem", "advdiff"), ("n", "5"), ("particles", "200"), ("integrator", "adaptive-bdf2"), ("rtol", "1e-3"),
+     ("seed", "1"), ("prior.k3.sigma", "1.5")],
+])
+def test_run_experiment_advdiff_matches_reference(kv, tmp_path):
+    """Same data file (the reference's generator), free-running 30
+    observations: trace rows within 1e-8, same report fields."""
+    test_run_experiment_matches_reference(kv, tmp_path)
+
+
+@pytest.mark.parametrize("kv", [[("problem", "advdiff"), ("n", "6"), ("seed", "5")],
+                                [("problem", "advdiff"), ("n", "20"), ("seed", "1"), ("truth.c1", "1.5")]])
+def test_generate_data_advdiff_matches_reference(kv, tmp_path):
+    """pfsmc_gpu_generate_data for problem 2: the 20 random sites from the
+    keyed stream and the noise are identical; the truth path is the adaptive
+    BDF(1,2) at rtol 1e-8 on both sides (GPU: DFT Newton solve; reference: LU),
+    so the values agree to the integrator's tolerance, not to rounding."""
+    G, R = _libs()
+    g, r = C.c_void_p(G.pfsmc_gpu_experiment_new()), C.c_void_p(R.pfsmc_config_new())
+    for k, v in kv:
+        assert R.pfsmc_config_set(r, k.encode(), v.encode()) == 0
+        assert G.pfsmc_gpu_experiment_set(g, k.encode(), v.encode()) == 0
+    dr, dg = str(tmp_path / "ref.csv"), str(tmp_path / "gpu.csv")
+    assert R.pfsmc_generate_data(r, dr.encode()) == 0
+    assert G.pfsmc_gpu_generate_data(g, dg.encode()) == 0, G.pfsmc_gpu_experiment_last_error()
+    hr, vr = _rows(dr)
+    hg, vg = _rows(dg)
+    assert hr == hg and vr.shape == vg.shape == (30, 21)
+    assert np.array_equal(vr[:, 0], vg[:, 0])
+    np.testing.assert_allclose(vg[:, 1:], vr[:, 1:], rtol=0, atol=1e-7 * np.max(np.abs(vr[:, 1:])))
+    sr, sg = json.load(open(dr[:-4] + ".json")), json.load(open(dg[:-4] + ".json"))
+    assert set(sr) == set(sg)
+    for key in sr:
+        assert sg[key] == sr[key], key
