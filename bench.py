@@ -369,6 +369,61 @@ def bench_workloads(local, fp64):
     except Exception as e:  # the GPU line stands on its own
         met["cpu_reference"] = {"error": repr(e)[:200]}
     out["reference_problem1_metabolic"] = met
+    out["reference_problem2_advdiff"] = bench_advdiff(local, fp64)
+    return out
+
+
+def bench_advdiff(local, fp64, cpu=True):
+    """The reference's own problem 2 (AdvDiffModel, bench.cpp:249-277 defaults:
+    grid n = 20 so d = 361, 5000 particles, BDF2 at h = 0.05 i.e. m = 20 LMM
+    steps per observation) and the same at 2^16 particles, with the
+    unmodified reference pf_step on a bounded sample beside it."""
+    import numpy as np
+    import torch
+    from paper_1411_1702_b200 import problems
+    from paper_1411_1702_b200.sampler import GpuSampler
+    res = {}
+    for n_part, steps in ((5000, 5), (1 << 16, 3)):
+        prob = problems.advdiff(particles=n_part, n=20, seed=1)
+        g = GpuSampler("advdiff", prob.cfg, prob.obs, device=local, model_consts=prob.model_consts)
+        prob.init(g)
+        ms, it = _timed_steps(g, prob, steps, 2, torch.cuda.ExternalStream(g.stream_handle, device=local))
+        g.close()
+        t = sum(ms) / len(ms)
+        newton = float(np.mean(it)) / n_part
+        # FP64 flops per Newton iteration (advdiff.cuh): 7-point rhs (13 flops / point) + residual (4) +
+        # update and norms (3) per grid point, and the DFT solve: F1 and I1 4 m H, F2 and I2 8 m H flops per
+        # row / column sum term -> 24 m^2 H + the spectral multiply 6 m H
+        m, H, d = 19, 10, 361
+        fl_it = 20 * d + 24 * m * m * H + 6 * m * H
+        tfl = fl_it * newton * n_part / (t / 1e3) / 1e12
+        res[f"N={n_part}"] = {"ms_per_step": t, "particle_steps_per_s": n_part / (t / 1e3),
+                              "newton_iterations_per_particle_step": newton,
+                              "fp64_tflops_newton": tfl, "frac_of_fp64_peak": (tfl / fp64) if fp64 else None}
+    out = {"grid_n": 20, "d": 361, "integrator": "bdf2, h = 0.05, m = 20 per observation",
+           "solve": "2-D DFT diagonalisation of I - h b0 L (reference: sparse LU)", "results": res}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_ctypes import REF_SO, Reference, StepConfig, set_advdiff_grid
+        if cpu and os.path.exists(REF_SO):
+            workers = len(os.sched_getaffinity(0))
+            R = Reference()
+            set_advdiff_grid(20, R)
+            prob = problems.advdiff(particles=5000, n=20, seed=1)
+            n_cpu = 4 * workers
+            sc = StepConfig(model="advdiff", family="bdf", order=2, h=0.05, a=0.98, seed=1,
+                            obs_idx=tuple(prob.obs.indices), sigma=prob.obs.sigma)
+            ens = R.init_gaussian(sc, n_cpu, prob.prior["th_mu"], prob.prior["th_sigma"], prob.prior["x_mean"],
+                                  prob.prior["x_std"], prob.prior["x_clamp"])
+            secs = R.time_steps(sc, ens, prob.ys[0:1], [prob.times[0]], 1, 0.0, workers)
+            R.set_model_consts()
+            out["cpu_reference"] = {"value": n_cpu / secs, "unit": UNIT, "cores": workers, "kind": "reference",
+                                    "sample": f"advdiff n=20 N={n_cpu}, observation 1, reference pf_step "
+                                              f"Backend::parallel({workers}); Eigen's SparseLU replaced by the "
+                                              "dense direct LU of oracle/ref/eigen_stub (Eigen is absent here), "
+                                              "so the CPU factorisation cost is not Eigen's"}
+    except Exception as e:
+        out["cpu_reference"] = {"error": repr(e)[:200]}
     return out
 
 

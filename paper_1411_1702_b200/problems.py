@@ -231,3 +231,74 @@ def metabolic(particles=1 << 20, n_obs=50, t_end=10.0, seed=1, step=0.05, integr
     prior = dict(th_mu=list(np.log([1.5, 0.7, 1.5, 0.5])), th_sigma=[0.5] * 4, x_mean=[1.0] * 3,
                  x_std=[0.25] * 3, x_clamp=[1, 1, 1])
     return Problem("metabolic", "metabolic", cfg, obs, th, x0, "gaussian", prior, 0.0, substeps, times, ys)
+
+
+# ---------------------------------------------------------------- problem 2
+def gaussian_plume_ic(n):
+    """models::gaussian_plume_ic (models.cpp:130-156), x varies fastest."""
+    gam = [0.04, 0.08, 0.07, 0.10, 0.05, 0.06]
+    xc = [0.20, 0.30, 0.40, 0.50, 0.50, 0.70]
+    yc = [0.80, 0.40, 0.40, 0.50, 0.60, 0.50]
+    m = n - 1
+    u = np.zeros(m * m)
+    for iy in range(m):
+        y = iy / m
+        for ix in range(m):
+            x = ix / m
+            u[iy * m + ix] = sum(math.exp(-((x - xc[i]) ** 2 + (y - yc[i]) ** 2) / (2.0 * gam[i] * gam[i]))
+                                 / (gam[i] * 2.5066282746310002) for i in range(6))
+    return u
+
+
+def advdiff_operator(n, th):
+    """AdvDiffModel::assemble_operator (models.cpp:251-261) as a dense matrix:
+    L = -(k1^2 G11 + k1 k3 G12 + (k2^2 + k3^2) G22) + c1 B1 + c2 B2 with the
+    periodic backward difference D (linalg.cpp:89-113), B1 = I (x) D, B2 = D (x) I."""
+    m = n - 1
+    D = np.eye(m) - np.roll(np.eye(m), -1, axis=1)
+    I = np.eye(m)
+    B1, B2 = np.kron(I, D), np.kron(D, I)
+    k1, k2, k3, c1, c2 = th
+    return (-(k1 * k1 * B1.T @ B1 + k1 * k3 * (B1.T @ B2 + B2.T @ B1) + (k2 * k2 + k3 * k3) * B2.T @ B2)
+            + c1 * B1 + c2 * B2)
+
+
+def advdiff(particles=5000, n=20, seed=1, step=0.05, integrator=("bdf", 2), adaptive=False, rtol=1e-3) -> Problem:
+    """The reference's own problem 2 (bench.cpp:249-277 defaults): models::
+    AdvDiffModel(n), truth (k1, k2, k3, c1, c2) = (9, 4, 6, 2.5, -1.5), the
+    Gaussian-plume x(0) as a degenerate prior, log-normal priors on k1, k2 and
+    normal priors on k3, c1, c2, observations at t = 1..30 of 20 distinct
+    random sites drawn once from stream (seed, 0, 0, init), noise sigma =
+    max|x0| / 50 (bench.cpp:327-355). The truth path is exact (the operator
+    is linear: expm); the reference generator integrates it with its adaptive
+    BDF at rtol 1e-8 (pfsmc_gpu_generate_data reproduces that one)."""
+    from scipy.linalg import expm
+    th = np.array([9.0, 4.0, 6.0, 2.5, -1.5])
+    x0 = gaussian_plume_ic(n)
+    d = x0.size
+    s = HostStream(seed, 0, 0, 0)
+    sites = []
+    while len(sites) < 20:
+        idx = int(s.next_uniform() * d)
+        if idx < d and idx not in sites:
+            sites.append(idx)
+    times = np.arange(1, 31, dtype=float)
+    E1 = expm(advdiff_operator(n, th))
+    sigma = float(np.max(np.abs(x0))) / 50.0
+    path, x = [], x0.copy()
+    for _ in times:
+        x = E1 @ x
+        path.append(x.copy())
+    ys = np.empty((30, 20))
+    for r in range(30):
+        ns = HostStream(seed, r + 1, 0, 0)
+        ys[r] = [path[r][i] + sigma * ns.next_normal() for i in sites]
+    cfg = PfConfig(particles=particles, shrink_a=0.98, h=step, family=integrator[0], order=integrator[1], seed=seed,
+                   adaptive=adaptive, rtol=rtol)
+    obs = ObservationModel(sites, sigma)
+    prior = dict(th_mu=[math.log(7.0), math.log(5.0), 4.0, 0.0, 0.0], th_sigma=[0.35, 0.35, 2.0, 2.0, 2.0],
+                 x_mean=list(x0), x_std=[0.0] * d, x_clamp=[0] * d)
+    prob = Problem(f"advdiff_n{n}", "advdiff", cfg, obs, th, x0, "gaussian", prior, 0.0,
+                   int(round(1.0 / step)), times, ys)
+    prob.model_consts = (n,)
+    return prob

@@ -106,7 +106,9 @@ def test_free_running_advdiff():
         anc_g, _, _ = gpu.step_diagnostics()
         assert np.array_equal(anc_g.astype(np.int64), dg["ancestors"]), f"step {j}"
         tr = np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]])
-        assert _rel(tr, trace_o) < REL_TRACE, j
+        assert _rel(tr[:10], trace_o[:10]) < REL_TRACE, j
+        assert _rel_rows(tr[None, 10:-1], trace_o[None, 10:-1]) < REL_TRACE, j
+        assert _rel(tr[-1:], trace_o[-1:]) < REL_TRACE, j
     got = gpu.get_ensemble()
     assert _rel_rows(got.states, ens.states) < 1e-8
     gpu.close()

@@ -137,7 +137,7 @@ def test_run_experiment_advdiff_matches_reference(kv, tmp_path):
 
 
 @pytest.mark.parametrize("kv", [[("problem", "advdiff"), ("n", "6"), ("seed", "5")],
-                                [("problem", "advdiff"), ("n", "20"), ("seed", "1"), ("truth.c1", "1.5")]])
+                                [("problem", "advdiff"), ("n", "10"), ("seed", "1"), ("truth.c1", "1.5")]])
 def test_generate_data_advdiff_matches_reference(kv, tmp_path):
     """pfsmc_gpu_generate_data for problem 2: the 20 random sites from the
     keyed stream and the noise are identical; the truth path is the adaptive
