@@ -62,7 +62,7 @@ def _obs(sc, x0, steps, h=0.01, seed=0):
 CASES = [
     # name, grid n, particles, steps, StepConfig kwargs
     ("n6_bdf2", 6, 512, 3, dict(family="bdf", order=2, h=0.05)),
-    ("n6_am3", 6, 300, 3, dict(family="am", order=3, h=0.1)),
+    ("n6_am3", 6, 300, 3, dict(family="am", order=3, h=0.02)),
     ("n5_ab1", 5, 200, 2, dict(family="ab", order=1, h=0.002)),
     ("n12_bdf3", 12, 256, 2, dict(family="bdf", order=3, h=0.05)),      # d = 121, E = 1
     ("n20_bdf2", 20, 96, 2, dict(family="bdf", order=2, h=0.05)),       # d = 361, E = 3 (the default grid)

@@ -91,15 +91,19 @@ def test_config_errors_match_reference():
     G.pfsmc_gpu_experiment_free(g)
 
 
-def test_out_of_scope_problem_and_missing_data_status(tmp_path):
+def test_problem_validation_and_missing_data_status(tmp_path):
     G = _gpu_lib()
     g = C.c_void_p(G.pfsmc_gpu_experiment_new())
     out = C.c_char_p()
     # missing data file: IO error before any GPU work
     assert G.pfsmc_gpu_run_experiment(g, str(tmp_path / "none.csv").encode(), str(tmp_path).encode(),
                                       C.byref(out)) == 4
+    # problem 2 (AdvDiffModel): the grid bound of the GPU path is a CONFIG error, like the
+    # reference's AdvDiffModel ctor for n < 3 (models.cpp:186-188); the data file is read first
     assert G.pfsmc_gpu_experiment_set(g, b"problem", b"advdiff") == 0
+    assert G.pfsmc_gpu_experiment_set(g, b"n", b"2") == 0
     assert G.pfsmc_gpu_run_experiment(g, str(tmp_path / "none.csv").encode(), str(tmp_path).encode(),
                                       C.byref(out)) == 2
-    assert b"not implemented" in G.pfsmc_gpu_experiment_last_error()
+    assert b"grid parameter n" in G.pfsmc_gpu_experiment_last_error()
+    assert G.pfsmc_gpu_experiment_set(g, b"problem", b"other") == 2
     G.pfsmc_gpu_experiment_free(g)
