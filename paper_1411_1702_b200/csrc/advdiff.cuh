@@ -275,8 +275,8 @@ struct AdvProp {
         int idx = (kx * adv_dx(q) + ky * adv_dy(q)) % m;
         if (idx < 0) idx += m;
         const double2 t = sm.tw[idx];
-        re += st[q] * t.x;
-        im += st[q] * t.y;
+        re = fma(st[q], t.x, re);
+        im = fma(st[q], t.y, im);
       }
       sm.lam[o] = make_double2(re, im);
     }
@@ -311,54 +311,79 @@ struct AdvProp {
     for (int s = 0; s < E; ++s)
       if (own(s)) sm.rs[eid(s)] = r[s];
     __syncthreads();
+    // The transforms are not the reference's arithmetic (it runs a sparse LU),
+    // so they use fused multiply-adds (fma) despite the build's --fmad=false.
+    // Two outputs per thread (o, o + kAT): two independent FMA chains.
     // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r e^{-2 pi i kx ix / m}
-    for (int o = threadIdx.x; o < mh; o += kAT) {
-      const int iy = o / H, kx = o - iy * H;
+    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
+      const int o2 = o + kAT < mh ? o + kAT : o;
+      const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
       const double* row = sm.rs + iy * m;
-      double re = 0.0, im = 0.0;
-      int idx = 0;
+      const double* row2 = sm.rs + iy2 * m;
+      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+      int idx = 0, idx2 = 0;
       for (int ix = 0; ix < m; ++ix) {
-        const double v = row[ix];
-        const double2 t = sm.tw[idx];
-        re += v * t.x;
-        im -= v * t.y;
+        const double v = row[ix], v2 = row2[ix];
+        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
+        re = fma(v, t.x, re);
+        im = fma(-v, t.y, im);
+        re2 = fma(v2, t2.x, re2);
+        im2 = fma(-v2, t2.y, im2);
         idx += kx;
         if (idx >= m) idx -= m;
+        idx2 += kx2;
+        if (idx2 >= m) idx2 -= m;
       }
       sm.s1[o] = make_double2(re, im);
+      if (o2 != o) sm.s1[o2] = make_double2(re2, im2);
     }
     __syncthreads();
     // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) e^{-2 pi i ky iy / m}, times imu
-    for (int o = threadIdx.x; o < mh; o += kAT) {
-      const int ky = o / H, kx = o - ky * H;
-      double re = 0.0, im = 0.0;
-      int idx = 0;
+    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
+      const int o2 = o + kAT < mh ? o + kAT : o;
+      const int ky = o / H, kx = o - ky * H, ky2 = o2 / H, kx2 = o2 - ky2 * H;
+      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+      int idx = 0, idx2 = 0;
       for (int iy = 0; iy < m; ++iy) {
-        const double2 a = sm.s1[iy * H + kx];
-        const double2 t = sm.tw[idx];
-        re += a.x * t.x + a.y * t.y;
-        im += a.y * t.x - a.x * t.y;
+        const double2 a = sm.s1[iy * H + kx], a2 = sm.s1[iy * H + kx2];
+        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
+        re = fma(a.x, t.x, fma(a.y, t.y, re));
+        im = fma(a.y, t.x, fma(-a.x, t.y, im));
+        re2 = fma(a2.x, t2.x, fma(a2.y, t2.y, re2));
+        im2 = fma(a2.y, t2.x, fma(-a2.x, t2.y, im2));
         idx += ky;
         if (idx >= m) idx -= m;
+        idx2 += ky2;
+        if (idx2 >= m) idx2 -= m;
       }
       const double2 q = sm.imu[o];
-      sm.s2[o] = make_double2(re * q.x - im * q.y, re * q.y + im * q.x);
+      sm.s2[o] = make_double2(fma(re, q.x, -im * q.y), fma(re, q.y, im * q.x));
+      if (o2 != o) {
+        const double2 q2 = sm.imu[o2];
+        sm.s2[o2] = make_double2(fma(re2, q2.x, -im2 * q2.y), fma(re2, q2.y, im2 * q2.x));
+      }
     }
     __syncthreads();
     // I2: B(iy, kx) = sum_ky D(ky, kx) e^{+2 pi i ky iy / m}
-    for (int o = threadIdx.x; o < mh; o += kAT) {
-      const int iy = o / H, kx = o - iy * H;
-      double re = 0.0, im = 0.0;
-      int idx = 0;
+    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
+      const int o2 = o + kAT < mh ? o + kAT : o;
+      const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
+      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+      int idx = 0, idx2 = 0;
       for (int ky = 0; ky < m; ++ky) {
-        const double2 a = sm.s2[ky * H + kx];
-        const double2 t = sm.tw[idx];
-        re += a.x * t.x - a.y * t.y;
-        im += a.y * t.x + a.x * t.y;
+        const double2 a = sm.s2[ky * H + kx], a2 = sm.s2[ky * H + kx2];
+        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
+        re = fma(a.x, t.x, fma(-a.y, t.y, re));
+        im = fma(a.y, t.x, fma(a.x, t.y, im));
+        re2 = fma(a2.x, t2.x, fma(-a2.y, t2.y, re2));
+        im2 = fma(a2.y, t2.x, fma(a2.x, t2.y, im2));
         idx += iy;
         if (idx >= m) idx -= m;
+        idx2 += iy2;
+        if (idx2 >= m) idx2 -= m;
       }
       sm.s1[o] = make_double2(re, im);
+      if (o2 != o) sm.s1[o2] = make_double2(re2, im2);
     }
     __syncthreads();
     // I1: half spectrum -> real rows (Hermitian symmetry), owned elements
@@ -372,7 +397,7 @@ struct AdvProp {
       for (int kx = 1; kx < H; ++kx) {
         const double2 t = sm.tw[idx];
         const double w = (2 * kx == m) ? 1.0 : 2.0;
-        sum += w * (b[kx].x * t.x - b[kx].y * t.y);
+        sum = fma(w, fma(b[kx].x, t.x, -b[kx].y * t.y), sum);
         idx += ix;
         if (idx >= m) idx -= m;
       }
@@ -579,9 +604,14 @@ struct AdvProp {
     if (!rhs(x, fcur)) return kInvalidRhs;
     double t = t0;
     double h = total * 1e-2;
+    long long attempts = 0;
     while (t < t1 - total * 1e-12) {
       h = ref_min(h, t1 - t);
       if (h < h_min) return kStiffness;
+      // The reference's loop has no attempt bound; cases exist where it never
+      // ends (its own generator at n = 4, 5). A GPU must not spin forever:
+      // kAdaptiveMaxAttempts step attempts end the interval as a stiffness failure.
+      if (++attempts > kAdaptiveMaxAttempts) return kStiffness;
       const int p = npoints >= 2 ? 2 : 1;
       const double t_next = t + h;
       double hb0, factor, c[E], pred[E];
@@ -706,7 +736,7 @@ __device__ __forceinline__ void adv_publish(const AdvSmem& sm, int d, const doub
 // The fitness log-sum-exp and the exact-CDF tile partials follow in
 // k_lg_reduce (the tail of k_predict over lg).
 template <int FAM, int ORD, int E>
-__global__ void __launch_bounds__(kAT) k_adv_predict(Ctx c) {
+__global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_predict(Ctx c) {
   extern __shared__ __align__(16) char adv_smem[];
   if (grid_error(c)) return;
   const StepParams& sp = *c.sp;
@@ -749,7 +779,7 @@ __global__ void __launch_bounds__(kAT) k_adv_predict(Ctx c) {
 // pass), proliferation, repropagation, innovation, log-likelihood, reweight;
 // writes the next record buffer and lw. The moments follow in k_adv_moments.
 template <int FAM, int ORD, int E>
-__global__ void __launch_bounds__(kAT) k_adv_update(Ctx c) {
+__global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_update(Ctx c) {
   extern __shared__ __align__(16) char adv_smem[];
   if (grid_error(c)) return;
   const DevState& st = *c.st;

@@ -23,6 +23,11 @@ namespace pfsmc_gpu {
 
 enum Family : int { kAB = 0, kAM = 1, kBDF = 2 };
 enum ParticleStatus : int { kOk = 0, kInvalidRhs = 1, kNewtonDivergence = 2, kSingular = 3, kStiffness = 4 };
+// Step attempts per interval of the adaptive BDF(1,2) before it reports
+// stiffness. The reference's loop (lmm.cpp:918-1016) has no such bound and
+// does not terminate in some cases (e.g. its own advdiff generator at n = 4,
+// 5); on the GPU an unbounded loop would hang the device.
+constexpr long long kAdaptiveMaxAttempts = 1LL << 24;
 
 // ---- coefficient tables (lmm.cpp:18-60) ----------------------------------
 __host__ __device__ constexpr double ab_beta(int order, int i) {
@@ -510,9 +515,12 @@ struct Propagator {
     if (!M::rhs(mk, t0, th, x, fcur)) return kInvalidRhs;
     double t = t0;
     double h = total * 1e-2;
+    long long attempts = 0;
     while (t < t1 - total * 1e-12) {
       h = ref_min(h, t1 - t);
       if (h < h_min) return kStiffness;
+      // no such bound in the reference (see kAdaptiveMaxAttempts)
+      if (++attempts > kAdaptiveMaxAttempts) return kStiffness;
       const int p = npoints >= 2 ? 2 : 1;
       const double t_next = t + h;
       double hb0, factor, c[D], pred[D];

@@ -127,7 +127,7 @@ def test_generate_data_matches_reference(kv, tmp_path):
 @pytest.mark.parametrize("kv", [
     [("problem", "advdiff"), ("n", "6"), ("particles", "300"), ("integrator", "bdf2"), ("step", "0.05"),
      ("seed", "3")],
-    [("problem", "advdiff"), ("n", "5"), ("particles", "48"), ("integrator", "adaptive-bdf2"), ("rtol", "1e-3"),
+    [("problem", "advdiff"), ("n", "6"), ("particles", "48"), ("integrator", "adaptive-bdf2"), ("rtol", "1e-3"),
      ("seed", "1"), ("prior.k3.sigma", "1.5")],
 ])
 def test_run_experiment_advdiff_matches_reference(kv, tmp_path):
