@@ -80,6 +80,7 @@ struct AdvSmem {
   double2* lam;   // m * H: lambda(k) of this particle's operator
   double2* imu;   // m * H: 1 / (d (1 - h b0 lambda))
   double2* tw;    // m: (cos, sin)(2 pi k / m)
+  double2* W;     // m x m: the DFT matrix e^{-2 pi i k j / m}, row k
   double* red;    // 4 * kAWarps + 8 reduction scratch
   double* pr;     // 16 per-particle scalars (theta, stencil broadcast)
 };
@@ -87,7 +88,7 @@ struct AdvSmem {
 __host__ __device__ inline int adv_half(int m) { return m / 2 + 1; }
 __host__ inline size_t adv_smem_bytes(int m) {
   const size_t d = static_cast<size_t>(m) * m, mh = static_cast<size_t>(m) * adv_half(m);
-  return 2 * d * 8 + 4 * mh * 16 + static_cast<size_t>(m) * 16 + (4 * kAWarps + 8) * 8 + 16 * 8;
+  return 2 * d * 8 + 4 * mh * 16 + static_cast<size_t>(m) * 16 + d * 16 + (4 * kAWarps + 8) * 8 + 16 * 8;
 }
 
 __device__ __forceinline__ AdvSmem adv_carve(char* base, int m) {
@@ -98,7 +99,8 @@ __device__ __forceinline__ AdvSmem adv_carve(char* base, int m) {
   a.lam = a.s2 + mh;
   a.imu = a.lam + mh;
   a.tw = a.imu + mh;
-  a.xs = reinterpret_cast<double*>(a.tw + m);
+  a.W = a.tw + m;
+  a.xs = reinterpret_cast<double*>(a.W + d);
   a.rs = a.xs + d;
   a.red = a.rs + d;
   a.pr = a.red + 4 * kAWarps + 8;
@@ -186,6 +188,7 @@ struct AdvProp {
   double st[7];
   double cached_hb0;
   bool have_imu;
+  int oy[E], ox[E];  // grid coordinates of the owned elements
 
   __device__ __forceinline__ bool own(int s) const { return threadIdx.x + s * kAT < d; }
   __device__ __forceinline__ int eid(int s) const { return threadIdx.x + s * kAT; }
@@ -204,7 +207,7 @@ struct AdvProp {
     for (int s = 0; s < E; ++s) {
       f[s] = 0.0;
       if (!own(s)) continue;
-      const int e = eid(s), iy = e / m, ix = e - iy * m;
+      const int iy = oy[s], ix = ox[s];
       const int xm = ix == 0 ? m - 1 : ix - 1, xp = ix == m - 1 ? 0 : ix + 1;
       const int ym = iy == 0 ? m - 1 : iy - 1, yp = iy == m - 1 ? 0 : iy + 1;
       const double* rm = sm.xs + ym * m;
@@ -313,48 +316,45 @@ struct AdvProp {
     __syncthreads();
     // The transforms are not the reference's arithmetic (it runs a sparse LU),
     // so they use fused multiply-adds (fma) despite the build's --fmad=false.
-    // Two outputs per thread (o, o + kAT): two independent FMA chains.
-    // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r e^{-2 pi i kx ix / m}
+    // Every sum walks a row of the shared DFT matrix W (no index arithmetic);
+    // two outputs per thread (o, o + kAT) give two independent FMA chains.
+    // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r(iy, ix) W(kx, ix)
     for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
       const int o2 = o + kAT < mh ? o + kAT : o;
       const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
       const double* row = sm.rs + iy * m;
       const double* row2 = sm.rs + iy2 * m;
+      const double2* w = sm.W + kx * m;
+      const double2* w2 = sm.W + kx2 * m;
       double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
-      int idx = 0, idx2 = 0;
+#pragma unroll 4
       for (int ix = 0; ix < m; ++ix) {
         const double v = row[ix], v2 = row2[ix];
-        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
+        const double2 t = w[ix], t2 = w2[ix];
         re = fma(v, t.x, re);
-        im = fma(-v, t.y, im);
+        im = fma(v, t.y, im);
         re2 = fma(v2, t2.x, re2);
-        im2 = fma(-v2, t2.y, im2);
-        idx += kx;
-        if (idx >= m) idx -= m;
-        idx2 += kx2;
-        if (idx2 >= m) idx2 -= m;
+        im2 = fma(v2, t2.y, im2);
       }
       sm.s1[o] = make_double2(re, im);
       if (o2 != o) sm.s1[o2] = make_double2(re2, im2);
     }
     __syncthreads();
-    // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) e^{-2 pi i ky iy / m}, times imu
+    // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) W(ky, iy), times imu
     for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
       const int o2 = o + kAT < mh ? o + kAT : o;
       const int ky = o / H, kx = o - ky * H, ky2 = o2 / H, kx2 = o2 - ky2 * H;
+      const double2* w = sm.W + ky * m;
+      const double2* w2 = sm.W + ky2 * m;
       double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
-      int idx = 0, idx2 = 0;
+#pragma unroll 4
       for (int iy = 0; iy < m; ++iy) {
         const double2 a = sm.s1[iy * H + kx], a2 = sm.s1[iy * H + kx2];
-        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
-        re = fma(a.x, t.x, fma(a.y, t.y, re));
-        im = fma(a.y, t.x, fma(-a.x, t.y, im));
-        re2 = fma(a2.x, t2.x, fma(a2.y, t2.y, re2));
-        im2 = fma(a2.y, t2.x, fma(-a2.x, t2.y, im2));
-        idx += ky;
-        if (idx >= m) idx -= m;
-        idx2 += ky2;
-        if (idx2 >= m) idx2 -= m;
+        const double2 t = w[iy], t2 = w2[iy];
+        re = fma(a.x, t.x, fma(-a.y, t.y, re));
+        im = fma(a.y, t.x, fma(a.x, t.y, im));
+        re2 = fma(a2.x, t2.x, fma(-a2.y, t2.y, re2));
+        im2 = fma(a2.y, t2.x, fma(a2.x, t2.y, im2));
       }
       const double2 q = sm.imu[o];
       sm.s2[o] = make_double2(fma(re, q.x, -im * q.y), fma(re, q.y, im * q.x));
@@ -364,42 +364,40 @@ struct AdvProp {
       }
     }
     __syncthreads();
-    // I2: B(iy, kx) = sum_ky D(ky, kx) e^{+2 pi i ky iy / m}
+    // I2: B(iy, kx) = c_kx sum_ky D(ky, kx) conj W(iy, ky), c = 2 except for
+    // kx = 0 and the Nyquist column (Hermitian half-spectrum weights)
     for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
       const int o2 = o + kAT < mh ? o + kAT : o;
       const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
+      const double2* w = sm.W + iy * m;
+      const double2* w2 = sm.W + iy2 * m;
       double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
-      int idx = 0, idx2 = 0;
+#pragma unroll 4
       for (int ky = 0; ky < m; ++ky) {
         const double2 a = sm.s2[ky * H + kx], a2 = sm.s2[ky * H + kx2];
-        const double2 t = sm.tw[idx], t2 = sm.tw[idx2];
-        re = fma(a.x, t.x, fma(-a.y, t.y, re));
-        im = fma(a.y, t.x, fma(a.x, t.y, im));
-        re2 = fma(a2.x, t2.x, fma(-a2.y, t2.y, re2));
-        im2 = fma(a2.y, t2.x, fma(a2.x, t2.y, im2));
-        idx += iy;
-        if (idx >= m) idx -= m;
-        idx2 += iy2;
-        if (idx2 >= m) idx2 -= m;
+        const double2 t = w[ky], t2 = w2[ky];
+        re = fma(a.x, t.x, fma(a.y, t.y, re));
+        im = fma(a.y, t.x, fma(-a.x, t.y, im));
+        re2 = fma(a2.x, t2.x, fma(a2.y, t2.y, re2));
+        im2 = fma(a2.y, t2.x, fma(-a2.x, t2.y, im2));
       }
-      sm.s1[o] = make_double2(re, im);
-      if (o2 != o) sm.s1[o2] = make_double2(re2, im2);
+      const double c1 = (kx == 0 || 2 * kx == m) ? 1.0 : 2.0;
+      const double c2 = (kx2 == 0 || 2 * kx2 == m) ? 1.0 : 2.0;
+      sm.s1[o] = make_double2(c1 * re, c1 * im);
+      if (o2 != o) sm.s1[o2] = make_double2(c2 * re2, c2 * im2);
     }
     __syncthreads();
-    // I1: half spectrum -> real rows (Hermitian symmetry), owned elements
+    // I1: half spectrum -> real rows: delta(iy, ix) = sum_kx Re(B(iy, kx) conj W(kx, ix))
 #pragma unroll
     for (int s = 0; s < E; ++s) {
       if (!own(s)) continue;
-      const int e = eid(s), iy = e / m, ix = e - iy * m;
-      const double2* b = sm.s1 + iy * H;
-      double sum = b[0].x;
-      int idx = ix;
-      for (int kx = 1; kx < H; ++kx) {
-        const double2 t = sm.tw[idx];
-        const double w = (2 * kx == m) ? 1.0 : 2.0;
-        sum = fma(w, fma(b[kx].x, t.x, -b[kx].y * t.y), sum);
-        idx += ix;
-        if (idx >= m) idx -= m;
+      const double2* b = sm.s1 + oy[s] * H;
+      const double2* w = sm.W + ox[s];  // column ix: W(kx, ix) = W[kx * m + ix]
+      double sum = 0.0;
+#pragma unroll 4
+      for (int kx = 0; kx < H; ++kx) {
+        const double2 t = w[kx * m];
+        sum = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sum));
       }
       r[s] = sum;
     }
@@ -702,6 +700,18 @@ __device__ __forceinline__ void adv_bind(PR& pr, const Ctx& c, char* smem, const
   pr.H = adv_half(pr.m);
   pr.sm = adv_carve(smem, pr.m);
   for (int k = threadIdx.x; k < pr.m; k += kAT) pr.sm.tw[k] = c.adv_tw[k];
+  __syncthreads();
+  for (int q = threadIdx.x; q < pr.d; q += kAT) {
+    const int k = q / pr.m, j = q - k * pr.m;
+    const double2 t = pr.sm.tw[(k * j) % pr.m];
+    pr.sm.W[q] = make_double2(t.x, -t.y);
+  }
+#pragma unroll
+  for (int s = 0; s < sizeof(pr.oy) / sizeof(pr.oy[0]); ++s) {
+    const int e = threadIdx.x + s * kAT;
+    pr.oy[s] = e / pr.m;
+    pr.ox[s] = e - pr.oy[s] * pr.m;
+  }
   adv_stencil(th_nat, pr.st);
   pr.have_imu = false;
   pr.cached_hb0 = 0.0;
