@@ -73,6 +73,7 @@ class ClockSampler:
         self.proc = None
         self.nvml = None
         self.stop = threading.Event()
+        self.err = None
 
     def _nvml_handle(self):
         import pynvml
@@ -92,18 +93,29 @@ class ClockSampler:
         nv, h = self.nvml
         bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        reasons_fns = [getattr(nv, n) for n in ("nvmlDeviceGetCurrentClocksEventReasons",
+                                                "nvmlDeviceGetCurrentClocksThrottleReasons") if hasattr(nv, n)]
         try:
             mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-        except Exception:
-            mx = None
-        while not self.stop.is_set():
+        except Exception as e:  # noqa: BLE001
+            mx, self.err = None, repr(e)[:120]
+        while True:
             try:
                 sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, mx, [n for n, b in zip(self.NAMES, bits) if r & b]))
-            except Exception:
-                pass
-            self.stop.wait(self.period)
+            except Exception as e:  # noqa: BLE001
+                sm, self.err = None, repr(e)[:120]
+            names = []
+            for fn in reasons_fns:
+                try:
+                    r = fn(h)
+                    names = [n for n, b in zip(self.NAMES, bits) if r & b]
+                    break
+                except Exception as e:  # noqa: BLE001
+                    self.err = repr(e)[:120]
+            if sm is not None:
+                self.rows.append((sm, mx, names))
+            if self.stop.wait(self.period):
+                break
 
     def _read_smi(self):
         for line in self.proc.stdout:
@@ -133,6 +145,14 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.stop.set()
+        if self.nvml and not self.rows:  # region shorter than the first poll: one closing sample
+            try:
+                nv, h = self.nvml
+                self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), []))
+                self.err = (self.err or "") + " (closing sample only)"
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)[:120]
         if self.proc:
             self.proc.terminate()
             try:
@@ -144,13 +164,15 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
         sm = [r[0] for r in self.rows]
         mx = [r[1] for r in self.rows if r[1] is not None]
         reasons = sorted({n for r in self.rows for n in r[2]})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows),
-                "source": "nvml" if self.nvml else "nvidia-smi"}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
+        if self.err:
+            out["note"] = self.err
+        return out
 
 
 def _dist():

@@ -197,6 +197,10 @@ struct AdvProp {
   // ascending column order from 0.0, exactly spmv (linalg.cpp:182-194).
   // Returns the block-wide "every f finite" (AdvDiffEval::rhs, models.cpp:164-170).
   __device__ __forceinline__ int rhs(const double (&x)[E], double (&f)[E]) {
+    return adv_all(rhs_local(x, f), sm.red);
+  }
+  // ... with the finiteness flag of this thread's elements only (the caller reduces it).
+  __device__ __forceinline__ int rhs_local(const double (&x)[E], double (&f)[E]) {
     __syncthreads();  // previous readers of sm.xs are done
 #pragma unroll
     for (int s = 0; s < E; ++s)
@@ -264,7 +268,7 @@ struct AdvProp {
       f[s] = sum;
       fin &= isfinite(sum) ? 1 : 0;
     }
-    return adv_all(fin, sm.red);
+    return fin;
   }
 
   // lambda(k) for this particle's stencil (once per propagation).
@@ -309,7 +313,8 @@ struct AdvProp {
   // delta = (I - hb0 L)^-1 r, r taken from registers, delta returned in them.
   __device__ __forceinline__ void solve(double (&r)[E]) {
     const int mh = m * H;
-    __syncthreads();
+    const int np = (mh + 1) >> 1;  // thread q < np computes outputs q and q + np
+    // (sm.rs was last read by the previous solve's F1, which a barrier since has closed)
 #pragma unroll
     for (int s = 0; s < E; ++s)
       if (own(s)) sm.rs[eid(s)] = r[s];
@@ -319,8 +324,8 @@ struct AdvProp {
     // Every sum walks a row of the shared DFT matrix W (no index arithmetic);
     // two outputs per thread (o, o + kAT) give two independent FMA chains.
     // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r(iy, ix) W(kx, ix)
-    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
-      const int o2 = o + kAT < mh ? o + kAT : o;
+    for (int o = threadIdx.x; o < np; o += kAT) {
+      const int o2 = o + np < mh ? o + np : o;
       const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
       const double* row = sm.rs + iy * m;
       const double* row2 = sm.rs + iy2 * m;
@@ -341,8 +346,8 @@ struct AdvProp {
     }
     __syncthreads();
     // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) W(ky, iy), times imu
-    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
-      const int o2 = o + kAT < mh ? o + kAT : o;
+    for (int o = threadIdx.x; o < np; o += kAT) {
+      const int o2 = o + np < mh ? o + np : o;
       const int ky = o / H, kx = o - ky * H, ky2 = o2 / H, kx2 = o2 - ky2 * H;
       const double2* w = sm.W + ky * m;
       const double2* w2 = sm.W + ky2 * m;
@@ -366,8 +371,8 @@ struct AdvProp {
     __syncthreads();
     // I2: B(iy, kx) = c_kx sum_ky D(ky, kx) conj W(iy, ky), c = 2 except for
     // kx = 0 and the Nyquist column (Hermitian half-spectrum weights)
-    for (int o = threadIdx.x; o < mh; o += 2 * kAT) {
-      const int o2 = o + kAT < mh ? o + kAT : o;
+    for (int o = threadIdx.x; o < np; o += kAT) {
+      const int o2 = o + np < mh ? o + np : o;
       const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
       const double2* w = sm.W + iy * m;
       const double2* w2 = sm.W + iy2 * m;
@@ -393,13 +398,18 @@ struct AdvProp {
       if (!own(s)) continue;
       const double2* b = sm.s1 + oy[s] * H;
       const double2* w = sm.W + ox[s];  // column ix: W(kx, ix) = W[kx * m + ix]
-      double sum = 0.0;
-#pragma unroll 4
-      for (int kx = 0; kx < H; ++kx) {
-        const double2 t = w[kx * m];
-        sum = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sum));
+      double sa = 0.0, sb = 0.0;  // even / odd kx: two chains
+      int kx = 0;
+      for (; kx + 1 < H; kx += 2) {
+        const double2 t = w[kx * m], u = w[(kx + 1) * m];
+        sa = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sa));
+        sb = fma(b[kx + 1].x, u.x, fma(b[kx + 1].y, u.y, sb));
       }
-      r[s] = sum;
+      if (kx < H) {
+        const double2 t = w[kx * m];
+        sa = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sa));
+      }
+      r[s] = sa + sb;
     }
   }
 
@@ -408,15 +418,15 @@ struct AdvProp {
                                         int max_iter, int& iters) {
     for (int iter = 1; iter <= max_iter; ++iter) {
       double f[E], r[E];
-      if (!rhs(x, f)) {
-        iters += iter;
-        return kInvalidRhs;
-      }
+      // the rhs finiteness verdict (checked first, as the reference does) rides
+      // on the norm reduction below: a non-finite f only poisons this
+      // iteration's iterate, which the failure discards
+      int fin = rhs_local(x, f);
 #pragma unroll
       for (int s = 0; s < E; ++s) r[s] = x[s] - hb0 * f[s] - c[s];
       if (!prepare(hb0)) {
         iters += iter;
-        return kSingular;
+        return adv_all(fin, sm.red) ? kSingular : kInvalidRhs;
       }
       solve(r);
       double dn = 0.0, xn = 0.0;
@@ -427,8 +437,11 @@ struct AdvProp {
         dn = ref_max(dn, fabs(r[s]));
         xn = ref_max(xn, fabs(x[s]));
       }
-      int dummy = 1;
-      adv_reduce2(dn, xn, dummy, sm.red);
+      adv_reduce2(dn, xn, fin, sm.red);
+      if (!fin) {
+        iters += iter;
+        return kInvalidRhs;
+      }
       if (!isfinite(xn) || !isfinite(dn)) {
         iters += iter;
         return kInvalidRhs;
