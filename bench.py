@@ -54,125 +54,108 @@ def _peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+_POLLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+bus = sys.argv[1]
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", flush=True)
+while True:
+    t = time.monotonic()
+    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+    try:
+        r = fn(h)
+    except Exception:
+        r = 0
+    print(f"{t:.6f},{sm},{mx}," + ",".join("1" if r & b else "0" for b in bits), flush=True)
+    time.sleep(float(sys.argv[3]))
+"""
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region.
 
-    Polls NVML (nvidia_ml_py) from a thread every ~2 ms, so even a timed region of a few
-    tens of milliseconds gets samples; falls back to `nvidia-smi -lms` when NVML is absent.
+    A separate process polls NVML (nvidia_ml_py) every ~1 ms and prints
+    CLOCK_MONOTONIC-stamped samples (no GIL contention with the timing loop);
+    the summary keeps the samples inside [enter, exit] of the timed region.
+    The poller is started and confirmed ready before the region begins.
     """
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int, period_s: float = 0.002):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index = index
         self.period = period_s
-        self.rows = []          # (sm_mhz, max_mhz, [reason names])
+        self.rows = []          # (t, sm_mhz, max_mhz, [reason names])
         self.proc = None
-        self.nvml = None
-        self.stop = threading.Event()
         self.err = None
+        self.t0 = self.t1 = None
 
-    def _nvml_handle(self):
-        import pynvml
-        pynvml.nvmlInit()
+    def _bus_id(self):
         try:
             import torch
-            bus = getattr(torch.cuda.get_device_properties(self.index), "pci_bus_id", None)
-            dom = getattr(torch.cuda.get_device_properties(self.index), "pci_domain_id", 0)
-            dev = getattr(torch.cuda.get_device_properties(self.index), "pci_device_id", 0)
-            if bus is not None:
-                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev:02x}.0")
-        except Exception:
-            pass
-        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            pr = torch.cuda.get_device_properties(self.index)
+            return f"{getattr(pr, 'pci_domain_id', 0):08x}:{pr.pci_bus_id:02x}:{getattr(pr, 'pci_device_id', 0):02x}.0"
+        except Exception:  # noqa: BLE001
+            return ""
 
-    def _poll_nvml(self):
-        nv, h = self.nvml
-        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-        reasons_fns = [getattr(nv, n) for n in ("nvmlDeviceGetCurrentClocksEventReasons",
-                                                "nvmlDeviceGetCurrentClocksThrottleReasons") if hasattr(nv, n)]
-        try:
-            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-        except Exception as e:  # noqa: BLE001
-            mx, self.err = None, repr(e)[:120]
-        while True:
-            try:
-                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-            except Exception as e:  # noqa: BLE001
-                sm, self.err = None, repr(e)[:120]
-            names = []
-            for fn in reasons_fns:
-                try:
-                    r = fn(h)
-                    names = [n for n, b in zip(self.NAMES, bits) if r & b]
-                    break
-                except Exception as e:  # noqa: BLE001
-                    self.err = repr(e)[:120]
-            if sm is not None:
-                self.rows.append((sm, mx, names))
-            if self.stop.wait(self.period):
-                break
-
-    def _read_smi(self):
+    def _read(self):
         for line in self.proc.stdout:
-            r = [x.strip() for x in line.split(",")]
-            try:
-                sm, mx = float(r[1]), float(r[2])
-            except (ValueError, IndexError):
+            f = line.strip().split(",")
+            if len(f) < 7:
                 continue
-            self.rows.append((sm, mx, [n for n, v in zip(self.NAMES, r[5:9]) if v.lower() == "active"]))
+            try:
+                self.rows.append((float(f[0]), float(f[1]), float(f[2]),
+                                  [n for n, v in zip(self.NAMES, f[3:7]) if v == "1"]))
+            except ValueError:
+                pass
 
     def __enter__(self):
         try:
-            self.nvml = self._nvml_handle()
-            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
-        except Exception:
-            self.nvml = None
-            try:
-                self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                              "--format=csv,noheader,nounits", "-lms", "100"],
-                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-                self.t = threading.Thread(target=self._read_smi, daemon=True)
-            except Exception:
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLLER, self._bus_id(), str(self.index),
+                                          str(self.period)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                         text=True)
+            first = self.proc.stdout.readline()  # blocks until the poller has NVML up
+            if not first.startswith("ready"):
+                self.err = (first + self.proc.stderr.read())[-200:]
                 self.proc = None
-                return self
-        self.t.start()
+            else:
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+                time.sleep(0.005)
+        except Exception as e:  # noqa: BLE001
+            self.err, self.proc = repr(e)[:200], None
+        self.t0 = time.monotonic()
         return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        if self.nvml and not self.rows:  # region shorter than the first poll: one closing sample
-            try:
-                nv, h = self.nvml
-                self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
-                                  float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), []))
-                self.err = (self.err or "") + " (closing sample only)"
-            except Exception as e:  # noqa: BLE001
-                self.err = repr(e)[:120]
+        self.t1 = time.monotonic()
         if self.proc:
+            time.sleep(0.003)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
-            except Exception:
+            except Exception:  # noqa: BLE001
                 self.proc.kill()
-        if self.nvml or self.proc:
             self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
-        sm = [r[0] for r in self.rows]
-        mx = [r[1] for r in self.rows if r[1] is not None]
-        reasons = sorted({n for r in self.rows for n in r[2]})
-        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
-               "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
-        if self.err:
-            out["note"] = self.err
-        return out
+        inside = [r for r in self.rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err,
+                    "samples_total": len(self.rows)}
+        sm = [r[1] for r in inside]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": sorted({n for r in inside for n in r[3]}), "samples": len(inside),
+                "region_ms": (self.t1 - self.t0) * 1e3, "source": "nvml poller process"}
 
 
 def _dist():
