@@ -70,6 +70,9 @@ CASES = [
     ("n6_adaptive", 6, 400, 3, dict(family="bdf", order=2, adaptive=True, rtol=1e-3)),
     ("n10_adaptive", 10, 200, 2, dict(family="bdf", order=2, adaptive=True, rtol=1e-3)),
     ("n26_bdf2", 26, 12, 1, dict(family="bdf", order=2, h=0.1)),        # d = 625, E = 8
+    ("n33_bdf1_max_grid", 33, 4, 1, dict(family="bdf", order=1, h=0.25)),  # d = 1024: the largest grid
+    ("n7_bdf2_one_particle", 7, 1, 2, dict(family="bdf", order=2, h=0.05)),
+    ("n7_am2_ragged3", 7, 3, 2, dict(family="am", order=2, h=0.05)),
 ]
 
 
@@ -111,6 +114,34 @@ def test_free_running_advdiff():
         assert _rel(tr[-1:], trace_o[-1:]) < REL_TRACE, j
     got = gpu.get_ensemble()
     assert _rel_rows(got.states, ens.states) < 1e-8
+    gpu.close()
+
+
+def test_advdiff_32_sites_and_total_degeneracy():
+    """The observation limit (32 sites) and the reference's NumericalError on
+    total degeneracy (filter.cpp:149-152) at the same step as the oracle."""
+    from paper_1411_1702_b200.sampler import NumericalError
+    n, N = 9, 64
+    sc, ens, x0 = _setup(n, N, 5, tuple(range(0, 64, 2)), family="bdf", order=2, h=0.05)
+    assert len(sc.obs_idx) == 32
+    ys = _obs(sc, x0, 1)
+    gpu = _sampler(sc, N, model_consts=(n,))
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    e0 = ens.copy()
+    row = gpu.pf_step(ys[0], 1, 0.0, 1.0)
+    trace_o, dg = O.pf_step(sc, ens, ys[0], 1, 0.0, 1.0, diag=True)
+    _compare_step(gpu, ens, trace_o, dg, row, field_state=True)
+    # a non-finite field in every particle: every rhs is invalid, every predictive
+    # likelihood -inf, and fitness_weights throws (NUMERICAL)
+    bad = e0.copy()
+    bad.states[:, 3] = np.inf
+    gpu.set_ensemble(_to_gpu_ens(bad))
+    with pytest.raises(NumericalError):
+        gpu.pf_step(ys[0], 1, 0.0, 1.0)
+    from oracle_ctypes import OracleError
+    with pytest.raises(OracleError) as ei:
+        O.pf_step(sc, bad.copy(), ys[0], 1, 0.0, 1.0)
+    assert ei.value.code == 3
     gpu.close()
 
 
