@@ -192,11 +192,23 @@ def _compare_step(gpu, ens_o, trace_o, dg, row, field_state=False):
     w_g, w_o = np.exp(got.logw), np.exp(ens_o.logw)
     assert _rel_scaled(w_g, w_o) < REL_STATE
     assert _rel(got.mean_u, ens_o.mean_u) < REL_TRACE
-    assert _rel_scaled(got.cov_u, ens_o.cov_u) < REL_TRACE
+    # a posterior collapsed onto one particle has a covariance of pure rounding
+    # noise (the reference's two-pass sum: ~1e-26 .. 1e-90; the device's shifted
+    # moments: exact 0); below 1e-20 of the parameter scale squared it is compared
+    # as such, otherwise normwise at the trace bar
+    floor = 1e-20 * max(1.0, float(np.max(np.abs(ens_o.params_u)))) ** 2
+    if np.max(np.abs(ens_o.cov_u)) < floor:
+        assert np.max(np.abs(got.cov_u)) < floor
+    else:
+        assert _rel_scaled(got.cov_u, ens_o.cov_u) < REL_TRACE
     tr = np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]])
     if field_state:  # the state mean of a field normwise (its entries cross zero), the rest per entry
         p, d = len(row.theta_mean), len(row.state_mean)
-        assert _rel(tr[:2 * p], trace_o[:2 * p]) < REL_TRACE
+        assert _rel(tr[:p], trace_o[:p]) < REL_TRACE
+        if np.max(np.abs(trace_o[p:2 * p])) < floor:  # collapsed posterior (see cov_u above)
+            assert np.max(np.abs(tr[p:2 * p])) < floor
+        else:
+            assert _rel(tr[p:2 * p], trace_o[p:2 * p]) < REL_TRACE
         assert _rel_rows(tr[None, 2 * p:2 * p + d], trace_o[None, 2 * p:2 * p + d]) < REL_TRACE
         assert _rel(tr[-1:], trace_o[-1:]) < REL_TRACE
     else:
