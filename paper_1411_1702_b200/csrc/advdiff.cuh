@@ -311,106 +311,146 @@ struct AdvProp {
   }
 
   // delta = (I - hb0 L)^-1 r, r taken from registers, delta returned in them.
+  // The transforms are not the reference's arithmetic (it runs a sparse LU),
+  // so they use fused multiply-adds (fma) despite the build's --fmad=false.
+  // Each pass is a small matrix product against the shared DFT matrix W,
+  // register-blocked 2 x 2 per thread: every shared load feeds two complex
+  // multiply-adds and each thread carries 4-8 independent FMA chains.
+  // Edge tiles clamp their second row / column (computed, not written).
   __device__ __forceinline__ void solve(double (&r)[E]) {
-    const int mh = m * H;
-    const int np = (mh + 1) >> 1;  // thread q < np computes outputs q and q + np
+    const int hy = (m + 1) >> 1, hx = (H + 1) >> 1;  // 2 x 2 tiles over (m rows, H columns)
+    const int nt = hy * hx;
     // (sm.rs was last read by the previous solve's F1, which a barrier since has closed)
 #pragma unroll
     for (int s = 0; s < E; ++s)
       if (own(s)) sm.rs[eid(s)] = r[s];
     __syncthreads();
-    // The transforms are not the reference's arithmetic (it runs a sparse LU),
-    // so they use fused multiply-adds (fma) despite the build's --fmad=false.
-    // Every sum walks a row of the shared DFT matrix W (no index arithmetic);
-    // two outputs per thread (o, o + kAT) give two independent FMA chains.
     // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r(iy, ix) W(kx, ix)
-    for (int o = threadIdx.x; o < np; o += kAT) {
-      const int o2 = o + np < mh ? o + np : o;
-      const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
-      const double* row = sm.rs + iy * m;
-      const double* row2 = sm.rs + iy2 * m;
-      const double2* w = sm.W + kx * m;
-      const double2* w2 = sm.W + kx2 * m;
-      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+    for (int q = threadIdx.x; q < nt; q += kAT) {
+      const int ty = q / hx, tx = q - ty * hx;
+      const int y0 = 2 * ty, x0 = 2 * tx;
+      const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
+      const double* r0 = sm.rs + y0 * m;
+      const double* r1 = sm.rs + y1 * m;
+      const double2* w0 = sm.W + x0 * m;
+      const double2* w1 = sm.W + x1 * m;
+      double a00r = 0.0, a00i = 0.0, a01r = 0.0, a01i = 0.0, a10r = 0.0, a10i = 0.0, a11r = 0.0, a11i = 0.0;
 #pragma unroll 4
-      for (int ix = 0; ix < m; ++ix) {
-        const double v = row[ix], v2 = row2[ix];
-        const double2 t = w[ix], t2 = w2[ix];
-        re = fma(v, t.x, re);
-        im = fma(v, t.y, im);
-        re2 = fma(v2, t2.x, re2);
-        im2 = fma(v2, t2.y, im2);
+      for (int j = 0; j < m; ++j) {
+        const double v0 = r0[j], v1 = r1[j];
+        const double2 t0 = w0[j], t1 = w1[j];
+        a00r = fma(v0, t0.x, a00r);
+        a00i = fma(v0, t0.y, a00i);
+        a01r = fma(v0, t1.x, a01r);
+        a01i = fma(v0, t1.y, a01i);
+        a10r = fma(v1, t0.x, a10r);
+        a10i = fma(v1, t0.y, a10i);
+        a11r = fma(v1, t1.x, a11r);
+        a11i = fma(v1, t1.y, a11i);
       }
-      sm.s1[o] = make_double2(re, im);
-      if (o2 != o) sm.s1[o2] = make_double2(re2, im2);
-    }
-    __syncthreads();
-    // F2 + diagonal solve: R(ky, kx) = sum_iy A(iy, kx) W(ky, iy), times imu
-    for (int o = threadIdx.x; o < np; o += kAT) {
-      const int o2 = o + np < mh ? o + np : o;
-      const int ky = o / H, kx = o - ky * H, ky2 = o2 / H, kx2 = o2 - ky2 * H;
-      const double2* w = sm.W + ky * m;
-      const double2* w2 = sm.W + ky2 * m;
-      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
-#pragma unroll 4
-      for (int iy = 0; iy < m; ++iy) {
-        const double2 a = sm.s1[iy * H + kx], a2 = sm.s1[iy * H + kx2];
-        const double2 t = w[iy], t2 = w2[iy];
-        re = fma(a.x, t.x, fma(-a.y, t.y, re));
-        im = fma(a.y, t.x, fma(a.x, t.y, im));
-        re2 = fma(a2.x, t2.x, fma(-a2.y, t2.y, re2));
-        im2 = fma(a2.y, t2.x, fma(a2.x, t2.y, im2));
-      }
-      const double2 q = sm.imu[o];
-      sm.s2[o] = make_double2(fma(re, q.x, -im * q.y), fma(re, q.y, im * q.x));
-      if (o2 != o) {
-        const double2 q2 = sm.imu[o2];
-        sm.s2[o2] = make_double2(fma(re2, q2.x, -im2 * q2.y), fma(re2, q2.y, im2 * q2.x));
+      sm.s1[y0 * H + x0] = make_double2(a00r, a00i);
+      if (x1 != x0) sm.s1[y0 * H + x1] = make_double2(a01r, a01i);
+      if (y1 != y0) {
+        sm.s1[y1 * H + x0] = make_double2(a10r, a10i);
+        if (x1 != x0) sm.s1[y1 * H + x1] = make_double2(a11r, a11i);
       }
     }
     __syncthreads();
-    // I2: B(iy, kx) = c_kx sum_ky D(ky, kx) conj W(iy, ky), c = 2 except for
+    // F2 + diagonal solve: R(ky, kx) = sum_iy W(ky, iy) A(iy, kx), times imu
+    for (int q = threadIdx.x; q < nt; q += kAT) {
+      const int ty = q / hx, tx = q - ty * hx;
+      const int y0 = 2 * ty, x0 = 2 * tx;
+      const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
+      const double2* w0 = sm.W + y0 * m;
+      const double2* w1 = sm.W + y1 * m;
+      double c00r = 0.0, c00i = 0.0, c01r = 0.0, c01i = 0.0, c10r = 0.0, c10i = 0.0, c11r = 0.0, c11i = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) {
+        const double2 a0 = sm.s1[j * H + x0], a1 = sm.s1[j * H + x1];
+        const double2 t0 = w0[j], t1 = w1[j];
+        c00r = fma(t0.x, a0.x, fma(-t0.y, a0.y, c00r));
+        c00i = fma(t0.x, a0.y, fma(t0.y, a0.x, c00i));
+        c01r = fma(t0.x, a1.x, fma(-t0.y, a1.y, c01r));
+        c01i = fma(t0.x, a1.y, fma(t0.y, a1.x, c01i));
+        c10r = fma(t1.x, a0.x, fma(-t1.y, a0.y, c10r));
+        c10i = fma(t1.x, a0.y, fma(t1.y, a0.x, c10i));
+        c11r = fma(t1.x, a1.x, fma(-t1.y, a1.y, c11r));
+        c11i = fma(t1.x, a1.y, fma(t1.y, a1.x, c11i));
+      }
+      auto put = [&](int y, int x, double re, double im) {
+        const double2 qv = sm.imu[y * H + x];
+        sm.s2[y * H + x] = make_double2(fma(re, qv.x, -im * qv.y), fma(re, qv.y, im * qv.x));
+      };
+      put(y0, x0, c00r, c00i);
+      if (x1 != x0) put(y0, x1, c01r, c01i);
+      if (y1 != y0) {
+        put(y1, x0, c10r, c10i);
+        if (x1 != x0) put(y1, x1, c11r, c11i);
+      }
+    }
+    __syncthreads();
+    // I2: B(iy, kx) = c_kx sum_ky conj W(iy, ky) D(ky, kx), c = 2 except for
     // kx = 0 and the Nyquist column (Hermitian half-spectrum weights)
-    for (int o = threadIdx.x; o < np; o += kAT) {
-      const int o2 = o + np < mh ? o + np : o;
-      const int iy = o / H, kx = o - iy * H, iy2 = o2 / H, kx2 = o2 - iy2 * H;
-      const double2* w = sm.W + iy * m;
-      const double2* w2 = sm.W + iy2 * m;
-      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+    for (int q = threadIdx.x; q < nt; q += kAT) {
+      const int ty = q / hx, tx = q - ty * hx;
+      const int y0 = 2 * ty, x0 = 2 * tx;
+      const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
+      const double2* w0 = sm.W + y0 * m;
+      const double2* w1 = sm.W + y1 * m;
+      double c00r = 0.0, c00i = 0.0, c01r = 0.0, c01i = 0.0, c10r = 0.0, c10i = 0.0, c11r = 0.0, c11i = 0.0;
 #pragma unroll 4
-      for (int ky = 0; ky < m; ++ky) {
-        const double2 a = sm.s2[ky * H + kx], a2 = sm.s2[ky * H + kx2];
-        const double2 t = w[ky], t2 = w2[ky];
-        re = fma(a.x, t.x, fma(a.y, t.y, re));
-        im = fma(a.y, t.x, fma(-a.x, t.y, im));
-        re2 = fma(a2.x, t2.x, fma(a2.y, t2.y, re2));
-        im2 = fma(a2.y, t2.x, fma(-a2.x, t2.y, im2));
+      for (int j = 0; j < m; ++j) {
+        const double2 a0 = sm.s2[j * H + x0], a1 = sm.s2[j * H + x1];
+        const double2 t0 = w0[j], t1 = w1[j];  // conj: (t.x, -t.y)
+        c00r = fma(t0.x, a0.x, fma(t0.y, a0.y, c00r));
+        c00i = fma(t0.x, a0.y, fma(-t0.y, a0.x, c00i));
+        c01r = fma(t0.x, a1.x, fma(t0.y, a1.y, c01r));
+        c01i = fma(t0.x, a1.y, fma(-t0.y, a1.x, c01i));
+        c10r = fma(t1.x, a0.x, fma(t1.y, a0.y, c10r));
+        c10i = fma(t1.x, a0.y, fma(-t1.y, a0.x, c10i));
+        c11r = fma(t1.x, a1.x, fma(t1.y, a1.y, c11r));
+        c11i = fma(t1.x, a1.y, fma(-t1.y, a1.x, c11i));
       }
-      const double c1 = (kx == 0 || 2 * kx == m) ? 1.0 : 2.0;
-      const double c2 = (kx2 == 0 || 2 * kx2 == m) ? 1.0 : 2.0;
-      sm.s1[o] = make_double2(c1 * re, c1 * im);
-      if (o2 != o) sm.s1[o2] = make_double2(c2 * re2, c2 * im2);
+      const double k0 = (x0 == 0 || 2 * x0 == m) ? 1.0 : 2.0;
+      const double k1 = (x1 == 0 || 2 * x1 == m) ? 1.0 : 2.0;
+      sm.s1[y0 * H + x0] = make_double2(k0 * c00r, k0 * c00i);
+      if (x1 != x0) sm.s1[y0 * H + x1] = make_double2(k1 * c01r, k1 * c01i);
+      if (y1 != y0) {
+        sm.s1[y1 * H + x0] = make_double2(k0 * c10r, k0 * c10i);
+        if (x1 != x0) sm.s1[y1 * H + x1] = make_double2(k1 * c11r, k1 * c11i);
+      }
     }
     __syncthreads();
-    // I1: half spectrum -> real rows: delta(iy, ix) = sum_kx Re(B(iy, kx) conj W(kx, ix))
-#pragma unroll
-    for (int s = 0; s < E; ++s) {
-      if (!own(s)) continue;
-      const double2* b = sm.s1 + oy[s] * H;
-      const double2* w = sm.W + ox[s];  // column ix: W(kx, ix) = W[kx * m + ix]
-      double sa = 0.0, sb = 0.0;  // even / odd kx: two chains
-      int kx = 0;
-      for (; kx + 1 < H; kx += 2) {
-        const double2 t = w[kx * m], u = w[(kx + 1) * m];
-        sa = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sa));
-        sb = fma(b[kx + 1].x, u.x, fma(b[kx + 1].y, u.y, sb));
+    // I1: half spectrum -> real rows, delta(iy, ix) = sum_kx Re(B(iy, kx) conj W(kx, ix)),
+    // 2 x 2 tiles over (iy, ix), through sm.rs (its F1 readers are past a barrier)
+    const int hm = (m + 1) >> 1, ntt = hm * hm;
+    for (int q = threadIdx.x; q < ntt; q += kAT) {
+      const int ty = q / hm, tx = q - ty * hm;
+      const int y0 = 2 * ty, x0 = 2 * tx;
+      const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, m - 1);
+      const double2* b0 = sm.s1 + y0 * H;
+      const double2* b1 = sm.s1 + y1 * H;
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < H; ++k) {
+        const double2 u0 = b0[k], u1 = b1[k];
+        const double2 t0 = sm.W[k * m + x0], t1 = sm.W[k * m + x1];
+        d00 = fma(u0.x, t0.x, fma(u0.y, t0.y, d00));
+        d01 = fma(u0.x, t1.x, fma(u0.y, t1.y, d01));
+        d10 = fma(u1.x, t0.x, fma(u1.y, t0.y, d10));
+        d11 = fma(u1.x, t1.x, fma(u1.y, t1.y, d11));
       }
-      if (kx < H) {
-        const double2 t = w[kx * m];
-        sa = fma(b[kx].x, t.x, fma(b[kx].y, t.y, sa));
+      sm.rs[y0 * m + x0] = d00;
+      if (x1 != x0) sm.rs[y0 * m + x1] = d01;
+      if (y1 != y0) {
+        sm.rs[y1 * m + x0] = d10;
+        if (x1 != x0) sm.rs[y1 * m + x1] = d11;
       }
-      r[s] = sa + sb;
     }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < E; ++s)
+      if (own(s)) r[s] = sm.rs[eid(s)];
   }
 
   // newton_solve, sparse path (lmm.cpp:219-266).
