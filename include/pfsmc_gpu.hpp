@@ -68,7 +68,8 @@ struct PfConfig {
   int newton_max_iter = 20;
   int device = 0;
   // the bound model's constants; METABOLIC: models::MetabolicConstants
-  // (lambda, c0, A0, A, t0_input, tau), reference defaults (models.hpp:67-74)
+  // (lambda, c0, A0, A, t0_input, tau), reference defaults (models.hpp:67-74);
+  // ADVDIFF: {n}, the AdvDiffModel grid parameter (set model_consts[0])
   double model_consts[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
   bool adaptive = false;  // IntegratorSpec.adaptive (variable-step BDF(1,2))
   double rtol = 1e-3;     // IntegratorSpec.rtol
