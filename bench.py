@@ -158,6 +158,21 @@ class ClockSampler:
                 "region_ms": (self.t1 - self.t0) * 1e3, "source": "nvml poller process"}
 
 
+def _issue_floor(prof, avg_ms, clocks):
+    wi = prof.get("warp_inst_per_launch")
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz")
+    if not wi or not mhz:
+        return {}
+    try:
+        import torch
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    except Exception:  # noqa: BLE001
+        sms = 148
+    floor_us = wi / (sms * 4 * mhz * 1e6) * 1e6
+    return {"ncu_warp_inst_per_launch": wi, "issue_floor_us": floor_us,
+            "frac_of_issue_floor": floor_us / (avg_ms * 1e3)}
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -671,7 +686,11 @@ def main():
                          "ncu_issue_active_pct": prof.get("issue_active_pct"),
                          "ncu_fp64_pipe_pct": prof.get("fp64_pipe_pct"),
                          "ncu_achieved_occupancy_pct": prof.get("achieved_occupancy_pct"),
-                         "ncu_source": prof.get("source")},
+                         "ncu_source": prof.get("source"),
+                         # the instruction-issue floor of the same kernel: its warp instructions
+                         # (ncu) at one issue per scheduler per cycle, 4 schedulers x the SMs, at
+                         # the sampled SM clock; frac_of_issue_floor = floor / measured duration
+                         **_issue_floor(prof, avg_ms, clk.summary())},
             "step_roofline": {"bytes_per_particle": STEP_BYTES, "achieved": step_gbs, "peak": hbm,
                               "frac": step_gbs / hbm},
             "kernel_ms_per_step": {k: v / args.steps for k, v in kt.items()},

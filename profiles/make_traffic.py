@@ -24,7 +24,8 @@ def main():
     pct = collections.defaultdict(lambda: collections.defaultdict(list))
     extra = {"issue_active_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
              "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-             "achieved_occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active"}
+             "achieved_occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+             "warp_inst_per_launch": "smsp__inst_executed.sum"}
     for r in rows[2:]:
         tot = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
