@@ -130,6 +130,13 @@ __device__ __forceinline__ double uniform_at(uint64_t seed, uint64_t j, uint64_t
   return u64_to_uniform(blk.v[k & 3]);
 }
 
+// a / b for 0 <= a < 2^14, 1 <= b <= 64 (grid indices): the float quotient of
+// a + 1/2 is at least 1/(2b) away from an integer and its relative error is
+// ~1e-7, so truncation is exact; no integer-division sequence.
+__device__ __forceinline__ int small_div(int a, int b) {
+  return __float2int_rz((static_cast<float>(a) + 0.5f) * __frcp_rn(static_cast<float>(b)));
+}
+
 // Block reductions over the particle CTA (every thread gets the result).
 // max of two NaN-free values (ref_max semantics: NaN operands skipped by the
 // callers' per-thread folds) and an AND of a flag.
@@ -275,12 +282,15 @@ struct AdvProp {
   __device__ __forceinline__ void spectrum() {
     const int mh = m * H;
     for (int o = threadIdx.x; o < mh; o += kAT) {
-      const int ky = o / H, kx = o - ky * H;
+      const int ky = small_div(o, H), kx = o - ky * H;
       double re = 0.0, im = 0.0;
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
-        int idx = (kx * adv_dx(q) + ky * adv_dy(q)) % m;
+        int idx = kx * adv_dx(q) + ky * adv_dy(q);  // in (-2m, 2m): fold without a division
         if (idx < 0) idx += m;
+        if (idx < 0) idx += m;
+        if (idx >= m) idx -= m;
+        if (idx >= m) idx -= m;
         const double2 t = sm.tw[idx];
         re = fma(st[q], t.x, re);
         im = fma(st[q], t.y, im);
@@ -327,7 +337,7 @@ struct AdvProp {
     __syncthreads();
     // F1: rows, real -> half spectrum: A(iy, kx) = sum_ix r(iy, ix) W(kx, ix)
     for (int q = threadIdx.x; q < nt; q += kAT) {
-      const int ty = q / hx, tx = q - ty * hx;
+      const int ty = small_div(q, hx), tx = q - ty * hx;
       const int y0 = 2 * ty, x0 = 2 * tx;
       const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
       const double* r0 = sm.rs + y0 * m;
@@ -358,7 +368,7 @@ struct AdvProp {
     __syncthreads();
     // F2 + diagonal solve: R(ky, kx) = sum_iy W(ky, iy) A(iy, kx), times imu
     for (int q = threadIdx.x; q < nt; q += kAT) {
-      const int ty = q / hx, tx = q - ty * hx;
+      const int ty = small_div(q, hx), tx = q - ty * hx;
       const int y0 = 2 * ty, x0 = 2 * tx;
       const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
       const double2* w0 = sm.W + y0 * m;
@@ -392,7 +402,7 @@ struct AdvProp {
     // I2: B(iy, kx) = c_kx sum_ky conj W(iy, ky) D(ky, kx), c = 2 except for
     // kx = 0 and the Nyquist column (Hermitian half-spectrum weights)
     for (int q = threadIdx.x; q < nt; q += kAT) {
-      const int ty = q / hx, tx = q - ty * hx;
+      const int ty = small_div(q, hx), tx = q - ty * hx;
       const int y0 = 2 * ty, x0 = 2 * tx;
       const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, H - 1);
       const double2* w0 = sm.W + y0 * m;
@@ -425,7 +435,7 @@ struct AdvProp {
     // 2 x 2 tiles over (iy, ix), through sm.rs (its F1 readers are past a barrier)
     const int hm = (m + 1) >> 1, ntt = hm * hm;
     for (int q = threadIdx.x; q < ntt; q += kAT) {
-      const int ty = q / hm, tx = q - ty * hm;
+      const int ty = small_div(q, hm), tx = q - ty * hm;
       const int y0 = 2 * ty, x0 = 2 * tx;
       const int y1 = min(y0 + 1, m - 1), x1 = min(x0 + 1, m - 1);
       const double2* b0 = sm.s1 + y0 * H;
@@ -753,16 +763,12 @@ __device__ __forceinline__ void adv_bind(PR& pr, const Ctx& c, char* smem, const
   pr.H = adv_half(pr.m);
   pr.sm = adv_carve(smem, pr.m);
   for (int k = threadIdx.x; k < pr.m; k += kAT) pr.sm.tw[k] = c.adv_tw[k];
-  __syncthreads();
-  for (int q = threadIdx.x; q < pr.d; q += kAT) {
-    const int k = q / pr.m, j = q - k * pr.m;
-    const double2 t = pr.sm.tw[(k * j) % pr.m];
-    pr.sm.W[q] = make_double2(t.x, -t.y);
-  }
+  // the DFT matrix, precomputed on the host (L2-resident, coalesced copy)
+  for (int q = threadIdx.x; q < pr.d; q += kAT) pr.sm.W[q] = __ldg(c.adv_W + q);
 #pragma unroll
   for (int s = 0; s < sizeof(pr.oy) / sizeof(pr.oy[0]); ++s) {
     const int e = threadIdx.x + s * kAT;
-    pr.oy[s] = e / pr.m;
+    pr.oy[s] = small_div(e, pr.m);
     pr.ox[s] = e - pr.oy[s] * pr.m;
   }
   adv_stencil(th_nat, pr.st);

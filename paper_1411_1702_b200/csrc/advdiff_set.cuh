@@ -30,13 +30,16 @@ struct AdvKernelSet final : KernelSet {
                   int max_iter, double* out, int* status, cudaStream_t s) override {
     // prm layout of the register models: consts[8], theta[P], x0[d]
     std::vector<double2> tw = adv_twiddles(m);
+    std::vector<double2> W = adv_dft_matrix(m);
     double2* dtw = nullptr;
-    if (cudaMalloc(&dtw, sizeof(double2) * m) != cudaSuccess) throw std::runtime_error("advdiff: cudaMalloc");
+    if (cudaMalloc(&dtw, sizeof(double2) * (m + d)) != cudaSuccess) throw std::runtime_error("advdiff: cudaMalloc");
     cudaMemcpyAsync(dtw, tw.data(), sizeof(double2) * m, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dtw + m, W.data(), sizeof(double2) * d, cudaMemcpyHostToDevice, s);
     Ctx c{};
     c.adv_m = m;
     c.adv_d = d;
     c.adv_tw = dtw;
+    c.adv_W = dtw + m;
     c.tol = tol;
     c.max_iter = max_iter;
     k_adv_trajectory<E><<<1, kAT, smem, s>>>(c, prm + 8, times, T, t0, rtol, out, status);

@@ -96,6 +96,7 @@ struct Ctx {
   // ---- advection-diffusion model (grid m x m, d = m^2; kernels_advdiff.cu) ----
   int adv_m, adv_d;
   const double2* adv_tw;  // (cos, sin)(2 pi k / m), k < m
+  const double2* adv_W;   // the DFT matrix e^{-2 pi i k j / m}, m x m
   double* xmean;          // state mean of the trace row (d doubles)
   double* xmean_part;     // its per-chunk partials
   double* rec[2];
@@ -928,7 +929,8 @@ std::unique_ptr<KernelSet> make_kernels_payload(int fam, int order);
 std::unique_ptr<KernelSet> make_kernels_metabolic(int fam, int order);
 // AdvDiffModel (models.cpp:158-266): one CTA per particle (kernels_advdiff.cu)
 std::unique_ptr<KernelSet> make_kernels_advdiff(int fam, int order, int grid_n);
-std::vector<double2> adv_twiddles(int m);  // (cos, sin)(2 pi k / m)
+std::vector<double2> adv_twiddles(int m);    // (cos, sin)(2 pi k / m)
+std::vector<double2> adv_dft_matrix(int m);  // e^{-2 pi i k j / m}, row-major m x m
 
 inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order, int grid_n = 0) {
   switch (model) {

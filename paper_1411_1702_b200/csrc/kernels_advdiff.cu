@@ -10,6 +10,17 @@
 
 namespace pfsmc_gpu {
 
+std::vector<double2> adv_dft_matrix(int m) {
+  const std::vector<double2> tw = adv_twiddles(m);
+  std::vector<double2> W(static_cast<size_t>(m) * m);
+  for (int k = 0; k < m; ++k)
+    for (int j = 0; j < m; ++j) {
+      const double2 t = tw[(k * j) % m];
+      W[static_cast<size_t>(k) * m + j] = make_double2(t.x, -t.y);
+    }
+  return W;
+}
+
 std::vector<double2> adv_twiddles(int m) {
   std::vector<double2> tw(m);
   const double two_pi = 6.283185307179586476925286766559;

@@ -301,11 +301,14 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     if (adv) {
       const int m = grid_n - 1;
       std::vector<double2> tw = adv_twiddles(m);
-      double2* dtw = s->dalloc<double2>(m);
+      std::vector<double2> W = adv_dft_matrix(m);
+      double2* dtw = s->dalloc<double2>(static_cast<size_t>(m) + m * m);
       CK(cudaMemcpy(dtw, tw.data(), sizeof(double2) * m, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dtw + m, W.data(), sizeof(double2) * m * m, cudaMemcpyHostToDevice));
       c.adv_m = m;
       c.adv_d = m * m;
       c.adv_tw = dtw;
+      c.adv_W = dtw + m;
       c.xmean = s->dalloc<double>(static_cast<size_t>(c.adv_d));
       c.xmean_part = s->dalloc<double>(static_cast<size_t>(c.adv_d) * 64);
       CK(cudaMemset(c.xmean, 0, sizeof(double) * c.adv_d));
