@@ -118,9 +118,9 @@ __device__ __forceinline__ double normal_at(uint64_t seed, uint64_t j, uint64_t 
   const uint64_t w1 = l == 0 ? blk.v[1] : blk.v[3];
   const double u1 = (static_cast<double>(w0 >> 11) + 1.0) * 0x1.0p-53;
   const double u2 = u64_to_uniform(w1);
-  const double r = sqrt_nonneg(-2.0 * log_unit(u1));
+  const double r = sqrt(-2.0 * log(u1));
   double s, c;
-  sincospi_unit(2.0 * u2, &s, &c);
+  sincospi(2.0 * u2, &s, &c);
   return (k & 1) ? r * s : r * c;
 }
 // The k-th uniform of a keyed stream (word k).
