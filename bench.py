@@ -288,6 +288,41 @@ def _timed_steps(gpu, prob, steps, warmup, stream):
     return ms, iters
 
 
+def _cpu_ref_rate(model, prob, kw, n_cpu=1 << 14, steps=2, note=None):
+    """The unmodified reference pf_step (oracle/_ref, all host threads) on a
+    bounded sample of a BASELINE workload: n_cpu particles, the first `steps`
+    observations (the CPU is far too slow for the full runs, and
+    its throughput is flat in N)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_ctypes import REF_SO, Oracle, Reference, StepConfig
+        if not os.path.exists(REF_SO):
+            return {"error": "oracle/_ref not built"}
+        workers = len(os.sched_getaffinity(0))
+        O, R = Oracle(), Reference()
+        seed = prob.cfg.seed
+        sc = StepConfig(model=model, h=prob.h_for(0.0, prob.times[0]), seed=seed, **kw)
+        if prob.prior_kind == "uniform":
+            ens = O.init_uniform(model, n_cpu, seed, **prob.prior)
+        else:
+            pr = prob.prior
+            ens = R.init_gaussian(sc, n_cpu, pr["th_mu"], pr["th_sigma"], pr["x_mean"], pr["x_std"],
+                                  pr.get("x_clamp", [0] * len(pr["x_mean"])))
+        secs, tp = 0.0, 0.0
+        for j in range(1, steps + 1):
+            t1 = prob.times[j - 1]
+            sc.h = prob.h_for(tp, t1)
+            secs += R.time_steps(sc, ens, prob.ys[j - 1:j], [t1], j, tp, workers)
+            tp = t1
+        out = {"value": n_cpu * steps / secs, "unit": UNIT, "cores": workers, "kind": "reference",
+               "sample": f"{model} N={n_cpu}, observations 1..{steps}, reference pf_step Backend::parallel({workers})"}
+        if note:
+            out["note"] = note
+        return out
+    except Exception as e:  # noqa: BLE001  (the GPU line stands on its own)
+        return {"error": repr(e)[:200]}
+
+
 def bench_workloads(local, fp64):
     """BASELINE configs 3-5 on one GPU (extra lines of the report; the
     headline metric is config 2)."""
@@ -354,6 +389,13 @@ def bench_workloads(local, fp64):
                            "ms_per_step": t, "particle_steps_per_s": n3 / (t / 1e3),
                            "newton_iterations_per_particle_step": float(np.mean(it)) / n3}
     g.close()
+    out["c3_robertson"]["cpu_reference"] = _cpu_ref_rate(
+        "robertson", prob, dict(family="bdf", order=2, a=0.99, obs_idx=(0, 2), sigma=0.02, newton_max_iter=4),
+        steps=1,
+        note="Gaussian likelihood in place of the lognormal extension (the reference has only the Gaussian "
+             "kind; the propagation dominates the cost); first observation only: at 2^14 particles every "
+             "particle's Newton (max_iter 4) fails in the second log-spaced interval, which the 2^22-particle "
+             "GPU run survives")
     # config 4: 8-compartment chain, 2^24, BDF3 m=3
     n4 = 1 << 24
     prob = problems.chain8(particles=n4, T=10, seed=1)
@@ -369,6 +411,8 @@ def bench_workloads(local, fp64):
                         "fp64_tflops_newton_only": tfl, "fp64_peak_tflops_measured": fp64,
                         "frac_of_fp64_peak": (tfl / fp64) if fp64 else None}
     g.close()
+    out["c4_chain8"]["cpu_reference"] = _cpu_ref_rate(
+        "chain", prob, dict(family="bdf", order=3, a=0.98, obs_idx=(0, 3, 7), sigma=0.01))
     # the reference's own problem 1 (models::MetabolicModel), BDF2 with m = 4 sub-steps,
     # N = 2^20, beside the unmodified reference pf_step on a bounded sample
     nm = 1 << 20
