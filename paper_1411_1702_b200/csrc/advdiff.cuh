@@ -82,13 +82,12 @@ struct AdvSmem {
   double2* tw;    // m: (cos, sin)(2 pi k / m)
   double2* W;     // m x m: the DFT matrix e^{-2 pi i k j / m}, row k
   double* red;    // 4 * kAWarps + 8 reduction scratch
-  double* pr;     // 16 per-particle scalars (theta, stencil broadcast)
 };
 
 __host__ __device__ inline int adv_half(int m) { return m / 2 + 1; }
 __host__ inline size_t adv_smem_bytes(int m) {
   const size_t d = static_cast<size_t>(m) * m, mh = static_cast<size_t>(m) * adv_half(m);
-  return 2 * d * 8 + 4 * mh * 16 + static_cast<size_t>(m) * 16 + d * 16 + (4 * kAWarps + 8) * 8 + 16 * 8;
+  return 2 * d * 8 + 4 * mh * 16 + static_cast<size_t>(m) * 16 + d * 16 + (4 * kAWarps + 8) * 8;
 }
 
 __device__ __forceinline__ AdvSmem adv_carve(char* base, int m) {
@@ -103,7 +102,6 @@ __device__ __forceinline__ AdvSmem adv_carve(char* base, int m) {
   a.xs = reinterpret_cast<double*>(a.W + d);
   a.rs = a.xs + d;
   a.red = a.rs + d;
-  a.pr = a.red + 4 * kAWarps + 8;
   return a;
 }
 
