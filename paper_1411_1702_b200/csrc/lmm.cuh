@@ -175,13 +175,24 @@ __device__ __forceinline__ bool band_solve(const typename M::K& mk, double tn, c
     fast &= !(fabs(sb[c]) > fabs(dg[c]));
   }
   if (!fast) return dense_newton_solve<M>(mk, tn, th, x, hb0, b);
+  // the D - 1 pivot reciprocals (inv = 1 / pivot, linalg.cpp:215) and the D
+  // back-substitution divisions are independent: batched IEEE divisions
+  double one[D - 1], inv[D - 1];
+#pragma unroll
+  for (int i = 0; i + 1 < D; ++i) one[i] = 1.0;
+  double dgl[D - 1];
+#pragma unroll
+  for (int i = 0; i + 1 < D; ++i) dgl[i] = dg[i];
+  ddiv_batch<D - 1>(one, dgl, inv);
 #pragma unroll
   for (int i = 1; i < D; ++i) {
-    const double l = sb[i - 1] * (1.0 / dg[i - 1]);
+    const double l = sb[i - 1] * inv[i - 1];
     b[i] -= l * b[i - 1];
   }
+  double bb[D];
 #pragma unroll
-  for (int ii = D - 1; ii >= 0; --ii) b[ii] /= dg[ii];
+  for (int i = 0; i < D; ++i) bb[i] = b[i];
+  ddiv_batch<D>(bb, dg, b);
   return true;
 }
 
