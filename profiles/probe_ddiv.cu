@@ -20,7 +20,7 @@ __global__ void k(unsigned long long n, unsigned long long* bad, unsigned long l
     double a = ldexp(ma, ea) * ((w.v[2] >> 40) & 1 ? -1.0 : 1.0);
     const double b = ldexp(mb, eb) * ((w.v[3] >> 40) & 1 ? -1.0 : 1.0);
     if ((i & 1023) == 0) a = 0.0;
-    if (!ddiv_safe(a, b)) { ++nu; continue; }
+    if (!ddiv_safe(a, b)) { ++nu; continue; }  // (|exponent| <= 60: never, zero dividends: safe)
     const double q0 = a / b, q1 = ddiv_seq(a, b);
     nb += __double_as_longlong(q0) != __double_as_longlong(q1);
   }
