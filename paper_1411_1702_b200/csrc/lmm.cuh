@@ -205,21 +205,27 @@ __device__ __forceinline__ int newton_solve(const typename M::K& mk, double tn, 
   constexpr int D = M::D;
   for (int iter = 1; iter <= max_iter; ++iter) {
     double f[D], r[D];
-    if (!M::rhs(mk, tn, th, x, f)) {
-      iters += iter;
-      return kInvalidRhs;
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) r[j] = x[j] - hb0 * f[j] - c[j];
     bool solved;
     if constexpr (M::kLowerBidiagonal) {
+      // rhs and the Jacobian band from one pass over x (their divisions in one
+      // batch); the verdicts are checked in the reference's order (rhs first)
       double jd[D], js[D - 1];
-      if (!M::jac_band(mk, tn, th, x, jd, js)) {
+      bool ok_f, ok_j;
+      M::rhs_jac_band(mk, tn, th, x, f, ok_f, jd, js, ok_j);
+      if (!ok_f || !ok_j) {
         iters += iter;
         return kInvalidRhs;
       }
+#pragma unroll
+      for (int j = 0; j < D; ++j) r[j] = x[j] - hb0 * f[j] - c[j];
       solved = band_solve<M>(mk, tn, th, x, hb0, jd, js, r);
     } else {
+      if (!M::rhs(mk, tn, th, x, f)) {
+        iters += iter;
+        return kInvalidRhs;
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) r[j] = x[j] - hb0 * f[j] - c[j];
       double A[D][D];
       if (!M::jac(mk, tn, th, x, A)) {
         iters += iter;
