@@ -754,9 +754,11 @@ struct AdvProp {
 
 // Binds the particle's operator: stencil from theta (natural), twiddles
 // into shared memory, lambda spectrum.
-template <class PR>
+// MT > 0: the grid side is a compile-time constant (the reference's default
+// n = 20, m = 19): every m-bound loop of the propagator gets a constant trip count.
+template <int MT, class PR>
 __device__ __forceinline__ void adv_bind(PR& pr, const Ctx& c, char* smem, const double* th_nat) {
-  pr.m = c.adv_m;
+  pr.m = MT > 0 ? MT : c.adv_m;
   pr.d = c.adv_d;
   pr.H = adv_half(pr.m);
   pr.sm = adv_carve(smem, pr.m);
@@ -802,7 +804,7 @@ __device__ __forceinline__ void adv_publish(const AdvSmem& sm, int d, const doub
 // One CTA per particle: shrink, Psi, log-likelihood, fitness log-weight.
 // The fitness log-sum-exp and the exact-CDF tile partials follow in
 // k_lg_reduce (the tail of k_predict over lg).
-template <int FAM, int ORD, int E>
+template <int FAM, int ORD, int E, int MT = 0>
 __global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_predict(Ctx c) {
   extern __shared__ __align__(16) char adv_smem[];
   if (grid_error(c)) return;
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_predict(Ctx c) {
       const double tb = c.a * __ldg(rec + c.adv_d + k) + c.one_minus_a * st.mu[k];
       th[k] = k < 2 ? exp(tb) : tb;
     }
-    adv_bind(pr, c, adv_smem, th);
+    adv_bind<MT>(pr, c, adv_smem, th);
   }
   double x[E], gamma[E];
 #pragma unroll
@@ -845,7 +847,7 @@ __global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_predict(Ctx c) {
 // One CTA per slot n: gather of ancestor anc[n] (written by the search
 // pass), proliferation, repropagation, innovation, log-likelihood, reweight;
 // writes the next record buffer and lw. The moments follow in k_adv_moments.
-template <int FAM, int ORD, int E>
+template <int FAM, int ORD, int E, int MT = 0>
 __global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_update(Ctx c) {
   extern __shared__ __align__(16) char adv_smem[];
   if (grid_error(c)) return;
@@ -881,7 +883,7 @@ __global__ void __launch_bounds__(kAT, E <= 3 ? 5 : 4) k_adv_update(Ctx c) {
     double th[kAdvP];
 #pragma unroll
     for (int k = 0; k < kAdvP; ++k) th[k] = s_th[k];
-    adv_bind(pr, c, adv_smem, th);
+    adv_bind<MT>(pr, c, adv_smem, th);
   }
   double x[E], xr[E], gamma[E];
 #pragma unroll
@@ -931,7 +933,7 @@ __global__ void __launch_bounds__(kAT) k_adv_trajectory(Ctx c, const double* prm
   double th[kAdvP];
 #pragma unroll
   for (int k = 0; k < kAdvP; ++k) th[k] = prm[k];
-  adv_bind(pr, c, adv_smem, th);
+  adv_bind<0>(pr, c, adv_smem, th);
   double x[E], gamma[E];
 #pragma unroll
   for (int s = 0; s < E; ++s) {

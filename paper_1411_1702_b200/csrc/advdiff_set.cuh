@@ -8,7 +8,7 @@
 
 namespace pfsmc_gpu {
 
-template <int FAM, int ORD, int E>
+template <int FAM, int ORD, int E, int MT = 0>
 struct AdvKernelSet final : KernelSet {
   int m;
   size_t smem;
@@ -17,9 +17,9 @@ struct AdvKernelSet final : KernelSet {
     d = m * m;
     p = kAdvP;
     smem = adv_smem_bytes(m);
-    cudaFuncSetAttribute(k_adv_predict<FAM, ORD, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_adv_predict<FAM, ORD, E, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    cudaFuncSetAttribute(k_adv_update<FAM, ORD, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_adv_update<FAM, ORD, E, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     cudaFuncSetAttribute(k_adv_trajectory<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
@@ -47,11 +47,11 @@ struct AdvKernelSet final : KernelSet {
     cudaFree(dtw);
   }
   void predict(const Ctx& c, int grid, cudaStream_t s) override {
-    k_adv_predict<FAM, ORD, E><<<c.N, kAT, smem, s>>>(c);
+    k_adv_predict<FAM, ORD, E, MT><<<c.N, kAT, smem, s>>>(c);
     adv_launch_lg_reduce(c, grid, s);
   }
   void update(const Ctx& c, int grid, cudaStream_t s) override {
-    k_adv_update<FAM, ORD, E><<<c.N, kAT, smem, s>>>(c);
+    k_adv_update<FAM, ORD, E, MT><<<c.N, kAT, smem, s>>>(c);
     adv_launch_moments(c, grid, s, 2);
     xmean(c, s);
   }
@@ -70,23 +70,23 @@ struct AdvKernelSet final : KernelSet {
   int moment_width() const override { return MomentLayout<AdvThetaView>::V + 1; }
 };
 
-template <int FAM, int E>
+template <int FAM, int E, int MT>
 std::unique_ptr<KernelSet> adv_order(int order, int n) {
   if constexpr (FAM == kBDF)
-    if (order == 0) return std::make_unique<AdvKernelSet<FAM, 0, E>>(n);
+    if (order == 0) return std::make_unique<AdvKernelSet<FAM, 0, E, MT>>(n);
   switch (order) {
-    case 1: return std::make_unique<AdvKernelSet<FAM, 1, E>>(n);
-    case 2: return std::make_unique<AdvKernelSet<FAM, 2, E>>(n);
-    case 3: return std::make_unique<AdvKernelSet<FAM, 3, E>>(n);
+    case 1: return std::make_unique<AdvKernelSet<FAM, 1, E, MT>>(n);
+    case 2: return std::make_unique<AdvKernelSet<FAM, 2, E, MT>>(n);
+    case 3: return std::make_unique<AdvKernelSet<FAM, 3, E, MT>>(n);
   }
   return nullptr;
 }
-template <int E>
+template <int E, int MT = 0>
 std::unique_ptr<KernelSet> adv_family(int fam, int order, int n) {
   switch (fam) {
-    case kAB: return adv_order<kAB, E>(order, n);
-    case kAM: return adv_order<kAM, E>(order, n);
-    case kBDF: return adv_order<kBDF, E>(order, n);
+    case kAB: return adv_order<kAB, E, MT>(order, n);
+    case kAM: return adv_order<kAM, E, MT>(order, n);
+    case kBDF: return adv_order<kBDF, E, MT>(order, n);
   }
   return nullptr;
 }
