@@ -326,7 +326,7 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const do
 
 // ---------------------------------------------------------------- K1
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1)) k_predict(Ctx c) {
+__global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1)) k_predict(Ctx c) {
   constexpr int D = M::D, P = M::P;
   __shared__ double scratch[kWarps * 2];
   __shared__ double fin[2];
@@ -607,7 +607,7 @@ __device__ void chol_psd_device(DevState& st) {
 }
 
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads, (M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1)) k_update(Ctx c) {
+__global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1)) k_update(Ctx c) {
   constexpr int D = M::D, P = M::P;
   using ML = MomentLayout<M>;
   constexpr int V = ML::V;
