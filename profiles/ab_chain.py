@@ -1,6 +1,6 @@
 """A/B timing of two library builds on BASELINE config 4 (chain, BDF3 m = 3)
 or the reference's problem 1 (metabolic, BDF2 m = 4):
-    python profiles/ab_chain.py A.so B.so [rounds] [n] [chain|metabolic]
+    python profiles/ab_chain.py A.so B.so [rounds] [n] [chain|metabolic|robertson]
 Each run: a fresh process, 2 warm-up + 3 timed drop-in steps at n particles
 (device events), alternating builds; prints ms/step and the medians."""
 import json
@@ -19,7 +19,9 @@ from paper_1411_1702_b200.sampler import GpuSampler
 import bench
 n = int(sys.argv[1])
 model = sys.argv[2]
-prob = problems.chain8(particles=n, T=8, seed=1) if model == "chain" else problems.metabolic(particles=n, n_obs=50, seed=1)
+prob = (problems.chain8(particles=n, T=8, seed=1) if model == "chain" else
+        problems.robertson(particles=n, T=400, seed=1) if model == "robertson" else
+        problems.metabolic(particles=n, n_obs=50, seed=1))
 g = GpuSampler(model, prob.cfg, prob.obs)
 prob.init(g)
 ms, it = bench._timed_steps(g, prob, 3, 2, torch.cuda.ExternalStream(g.stream_handle))
