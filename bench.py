@@ -47,6 +47,15 @@ KERNEL_BYTES = {                              # per particle per launch
 }
 
 
+# FP64 flops the device executes per chain Newton iteration (banded path,
+# lmm.cuh band_solve + ChainModel::rhs_jac_band, counting FMA as 2 and a
+# division as 1): rhs + band 13 div + 7 add + 7 mul (flux), 6x(2 mul + sub + sub)
+# + 2 mul + sub (o), 6 mul (den^2), 7x(mul + mul + sub) (jd) ~ 80; residual 3x8;
+# band: 2 mul + add per diagonal and sub-diagonal entry ~ 45, 7 reciprocals,
+# 7x(mul + mul + sub) forward, 8 divisions back; update + norms 8x(sub + 2 abs)
+EXEC_FLOPS_PER_NEWTON_CHAIN = 80 + 24 + 45 + 7 + 21 + 8 + 24
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -265,10 +274,14 @@ def gather_peak(device, n_rec=1 << 25):
     return v.value if rc == 0 else None
 
 
-def _timed_steps(gpu, prob, steps, warmup, stream):
-    """Blocking drop-in steps with per-step events (L2 flushed between)."""
+C3_WINDOWS = (50, 200, 320)
+
+
+def _timed_steps(gpu, prob, steps, warmup, stream, j0=0, t0=0.0):
+    """Blocking drop-in steps with per-step events (L2 flushed between),
+    observations j0 + 1 .. j0 + warmup + steps."""
     import torch
-    ms, j, tp = [], 0, 0.0
+    ms, j, tp = [], j0, t0
     iters = []
     for k in range(warmup + steps):
         j += 1
@@ -319,6 +332,40 @@ def _cpu_ref_rate(model, prob, kw, n_cpu=1 << 14, steps=2, note=None):
         if note:
             out["note"] = note
         return out
+    except Exception as e:  # noqa: BLE001  (the GPU line stands on its own)
+        return {"error": repr(e)[:200]}
+
+
+def _cpu_ref_windows(prob, kw, n_cpu=1 << 14):
+    """C3 on the CPU: the unmodified reference pf_step (all host threads) over
+    the same log-spaced grid from j = 1, timed in the same windows as the GPU.
+    The reference has only the Gaussian likelihood, so it stands in for the
+    lognormal extension (same propagation, which dominates the cost)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_ctypes import REF_SO, Reference, StepConfig
+        if not os.path.exists(REF_SO):
+            return {"error": "oracle/_ref not built"}
+        workers = len(os.sched_getaffinity(0))
+        R = Reference()
+        seed = prob.cfg.seed
+        sc = StepConfig(model="robertson", h=prob.h_for(0.0, prob.times[0]), seed=seed, **kw)
+        pr = prob.prior
+        ens = R.init_gaussian(sc, n_cpu, pr["th_mu"], pr["th_sigma"], pr["x_mean"], pr["x_std"], [0, 0, 0])
+        timed = {j for w in C3_WINDOWS for j in range(w, w + 5)}
+        secs, done, tp = 0.0, 0, 0.0
+        for j in range(1, max(timed) + 1):
+            t1 = prob.times[j - 1]
+            sc.h = prob.h_for(tp, t1)
+            dt = R.time_steps(sc, ens, prob.ys[j - 1:j], [t1], j, tp, workers)
+            if j in timed:
+                secs += dt
+                done += 1
+            tp = t1
+        return {"value": n_cpu * done / secs, "unit": UNIT, "cores": workers, "kind": "reference",
+                "sample": f"robertson N={n_cpu}, Gaussian likelihood, run from j=1, timed at observations "
+                          + ", ".join(f"{w}..{w + 4}" for w in C3_WINDOWS)
+                          + f", reference pf_step Backend::parallel({workers})"}
     except Exception as e:  # noqa: BLE001  (the GPU line stands on its own)
         return {"error": repr(e)[:200]}
 
@@ -378,24 +425,42 @@ def bench_workloads(local, fp64):
                                     "random_gather_peak_gbs": gpk,
                                     "random_read_rate_gbs": rnd_rate / 1e9 if rnd_rate else None,
                                     "results": c5}
-    # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal (first log-spaced intervals)
+    # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal: the filter runs the
+    # log-spaced grid from j = 1 and is timed in windows spread along it (early,
+    # mid, stiff), since the cost per step grows with the Newton iterations
     n3 = 1 << 22
     prob = problems.robertson(particles=n3, T=400, seed=1)
     g = GpuSampler("robertson", prob.cfg, prob.obs, device=local)
     prob.init(g)
-    ms, it = _timed_steps(g, prob, 5, 2, torch.cuda.ExternalStream(g.stream_handle, device=local))
-    t = sum(ms) / len(ms)
-    out["c3_robertson"] = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4", "steps": len(ms),
-                           "ms_per_step": t, "particle_steps_per_s": n3 / (t / 1e3),
-                           "newton_iterations_per_particle_step": float(np.mean(it)) / n3}
+    out["c3_robertson"] = c3 = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4",
+                                "likelihood": "lognormal (BASELINE extension)", "windows": {}}
+    st3 = torch.cuda.ExternalStream(g.stream_handle, device=local)
+    j3, tp3 = 0, 0.0
+    tot_ms, tot_steps, tot_it = 0.0, 0, 0.0
+    for w0 in C3_WINDOWS:
+        while j3 < w0 - 1:  # advance untimed to the window
+            j3 += 1
+            t1 = prob.times[j3 - 1]
+            g.pf_step(prob.ys[j3 - 1], j3, tp3, t1, h=prob.h_for(tp3, t1))
+            tp3 = t1
+        ms, it = _timed_steps(g, prob, 5, 0, st3, j0=j3, t0=tp3)
+        j3 += 5
+        tp3 = prob.times[j3 - 1]
+        t = sum(ms) / len(ms)
+        ipp = float(np.mean(it)) / n3
+        c3["windows"][f"j={w0}..{w0 + 4}"] = {
+            "t_obs": [float(prob.times[w0 - 1]), float(prob.times[w0 + 3])], "ms_per_step": t,
+            "particle_steps_per_s": n3 / (t / 1e3), "newton_iterations_per_particle_step": ipp,
+            "newton_iterations_per_solve": ipp / 4.0}
+        tot_ms += sum(ms)
+        tot_steps += len(ms)
+        tot_it += float(np.sum(it))
     g.close()
-    out["c3_robertson"]["cpu_reference"] = _cpu_ref_rate(
-        "robertson", prob, dict(family="bdf", order=2, a=0.99, obs_idx=(0, 2), sigma=0.02, newton_max_iter=4),
-        steps=1,
-        note="Gaussian likelihood in place of the lognormal extension (the reference has only the Gaussian "
-             "kind; the propagation dominates the cost); first observation only: at 2^14 particles every "
-             "particle's Newton (max_iter 4) fails in the second log-spaced interval, which the 2^22-particle "
-             "GPU run survives")
+    c3["ms_per_step"] = tot_ms / tot_steps
+    c3["particle_steps_per_s"] = n3 / (c3["ms_per_step"] / 1e3)
+    c3["newton_iterations_per_particle_step"] = tot_it / tot_steps / n3
+    c3["cpu_reference"] = _cpu_ref_windows(
+        prob, dict(family="bdf", order=2, a=0.99, obs_idx=(0, 2), sigma=0.02, newton_max_iter=4))
     # config 4: 8-compartment chain, 2^24, BDF3 m=3
     n4 = 1 << 24
     prob = problems.chain8(particles=n4, T=10, seed=1)
@@ -403,13 +468,21 @@ def bench_workloads(local, fp64):
     prob.init(g)
     ms, it = _timed_steps(g, prob, 2, 1, torch.cuda.ExternalStream(g.stream_handle, device=local))
     t = sum(ms) / len(ms)
+    # Newton iterations per particle-step, BOTH propagations (k_predict and
+    # k_update add to one per-step counter, lmm.cpp:488 convention)
     newton = float(np.mean(it)) / n4
-    flops = 2 * 643 * newton  # survey §8(d): N_it(8) = 643 flops per Newton iteration (dominant term)
+    # N_it(8) = 643 FP64 flops per Newton iteration (dense-LU
+    # count, the reference algorithm's); the device's banded solve executes
+    # fewer (EXEC_FLOPS_PER_NEWTON_CHAIN), so both are reported
+    flops = 643 * newton
     tfl = flops * n4 / (t / 1e3) / 1e12
+    tfl_exec = EXEC_FLOPS_PER_NEWTON_CHAIN * newton * n4 / (t / 1e3) / 1e12
     out["c4_chain8"] = {"particles": n4, "integrator": "bdf3, m=3", "steps": len(ms), "ms_per_step": t,
                         "particle_steps_per_s": n4 / (t / 1e3), "newton_iterations_per_particle_step": newton,
-                        "fp64_tflops_newton_only": tfl, "fp64_peak_tflops_measured": fp64,
-                        "frac_of_fp64_peak": (tfl / fp64) if fp64 else None}
+                        "fp64_tflops_newton_algorithmic": tfl, "fp64_tflops_newton_executed": tfl_exec,
+                        "fp64_peak_tflops_measured": fp64,
+                        "frac_of_fp64_peak": (tfl / fp64) if fp64 else None,
+                        "frac_of_fp64_peak_executed": (tfl_exec / fp64) if fp64 else None}
     g.close()
     out["c4_chain8"]["cpu_reference"] = _cpu_ref_rate(
         "chain", prob, dict(family="bdf", order=3, a=0.98, obs_idx=(0, 3, 7), sigma=0.01))

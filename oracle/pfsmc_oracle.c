@@ -12,9 +12,12 @@
 #include "pfsmc_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 static _Thread_local char g_err[256];
 static int fail(int code, const char* msg) {
@@ -24,6 +27,54 @@ static int fail(int code, const char* msg) {
 const char* or_last_error(void) { return g_err; }
 
 static inline double dmax(double a, double b) { return (a < b) ? b : a; }
+
+/* Per-particle loops over host threads (the reference maps particles over its
+ * thread pool, filter.cpp:234-265; exec.cpp:183-212): chunks of 256 indices
+ * handed out by an atomic counter. The arithmetic per particle is unchanged,
+ * so results do not depend on the thread count. ORACLE_THREADS=1 runs it
+ * inline. */
+typedef void (*par_body)(void* ctx, uint64_t i);
+typedef struct {
+  par_body f;
+  void* ctx;
+  uint64_t n;
+  atomic_ullong next;
+} par_job;
+static void* par_worker(void* arg) {
+  par_job* jb = (par_job*)arg;
+  for (;;) {
+    const uint64_t i0 = atomic_fetch_add(&jb->next, 256);
+    if (i0 >= jb->n) break;
+    const uint64_t i1 = i0 + 256 < jb->n ? i0 + 256 : jb->n;
+    for (uint64_t i = i0; i < i1; ++i) jb->f(jb->ctx, i);
+  }
+  return NULL;
+}
+static int par_threads(void) {
+  const char* e = getenv("ORACLE_THREADS");
+  long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+  if (t < 1) t = 1;
+  if (t > 64) t = 64;
+  return (int)t;
+}
+static void par_for(uint64_t n, par_body f, void* ctx, int allow_threads) {
+  const int T = allow_threads ? par_threads() : 1;
+  if (T == 1 || n < 2048) {
+    for (uint64_t i = 0; i < n; ++i) f(ctx, i);
+    return;
+  }
+  par_job jb;
+  jb.f = f;
+  jb.ctx = ctx;
+  jb.n = n;
+  atomic_init(&jb.next, 0);
+  pthread_t th[64];
+  int started = 0;
+  for (int t = 1; t < T; ++t)
+    if (pthread_create(&th[started], NULL, par_worker, &jb) == 0) ++started;
+  par_worker(&jb);
+  for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+}
 
 /* ------------------------------------------------------------------------ */
 /* RNG: Philox4x64-10 and keyed streams (rng.cpp:9-75)                       */
@@ -1102,6 +1153,63 @@ int or_chol_psd(const double* cov, uint64_t p, double* lower, double* jitter) {
 /* ------------------------------------------------------------------------ */
 /* pf_step (filter.cpp:292-394)                                              */
 /* ------------------------------------------------------------------------ */
+/* The two per-particle propagation passes of or_pf_step as loop bodies. */
+typedef struct {
+  const or_cfg* c;
+  const or_ens* e;
+  const double* y;
+  double t_prev, t_obs;
+  const double* th_u;  /* shrunk (predict) or proliferated (repropagate) params */
+  double* ll;          /* ll_bar (predict) or ll_new (repropagate) */
+  double* xs;          /* repropagate: the reshuffled states, updated in place */
+  void* unused0;
+  void* unused1;
+  or_step_out* out;
+  int d, p;
+  _Atomic int rc;
+  uint64_t j;
+} prop_ctx;
+
+static void predict_body(void* vctx, uint64_t i) {
+  prop_ctx* pc = (prop_ctx*)vctx;
+  const or_cfg* c = pc->c;
+  double nat[OR_MAX_P], xb[OR_MAX_D], gam[OR_MAX_D];
+  int st, it;
+  to_natural_m(c->model, pc->p, pc->th_u + i * pc->p, nat);
+  const int r2 = propagate_cfg(c, pc->d, nat, pc->e->states + i * pc->d, pc->t_prev, pc->t_obs, xb, gam, &st, &it);
+  if (r2) {
+    atomic_store(&pc->rc, r2);
+    return;
+  }
+  if (pc->out && pc->out->newton_iters) pc->out->newton_iters[i] = it;
+  pc->ll[i] = st == OR_ST_OK ? or_log_likelihood(c, pc->y, xb) : kNegInf;
+}
+
+static void repropagate_body(void* vctx, uint64_t i) {
+  prop_ctx* pc = (prop_ctx*)vctx;
+  const or_cfg* c = pc->c;
+  const int d = pc->d;
+  or_step_out* out = pc->out;
+  double nat[OR_MAX_P], xr[OR_MAX_D], gam[OR_MAX_D];
+  int st, it;
+  to_natural_m(c->model, pc->p, pc->th_u + i * pc->p, nat);
+  const int r2 = propagate_cfg(c, d, nat, pc->xs + i * d, pc->t_prev, pc->t_obs, xr, gam, &st, &it);
+  if (r2) {
+    atomic_store(&pc->rc, r2);
+    return;
+  }
+  if (out && out->newton_iters) out->newton_iters[i] += it;
+  if (out && out->status_new) out->status_new[i] = st;
+  if (out && out->gamma) memcpy(out->gamma + i * d, gam, sizeof(double) * d);
+  pc->ll[i] = kNegInf;
+  if (st != OR_ST_OK) return;
+  memcpy(pc->xs + i * d, xr, sizeof(double) * d);
+  stream sn;
+  stream_init(&sn, c->seed, pc->j, i, OR_PURPOSE_INNOVATE);
+  for (int k = 0; k < d; ++k) pc->xs[i * d + k] += sqrt(gam[k]) * next_normal(&sn);
+  pc->ll[i] = or_log_likelihood(c, pc->y, pc->xs + i * d);
+}
+
 int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
                double t_prev, double t_obs, or_step_out* out) {
   const uint64_t n = e->n, d = e->d, p = e->p;
@@ -1128,15 +1236,13 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
   for (uint64_t i = 0; i < n; ++i)
     for (uint64_t k = 0; k < p; ++k) tb[i * p + k] = c->a * e->params_u[i * p + k] + (1.0 - c->a) * mean[k];
 
-  /* predict + log-likelihood (filter.cpp:304-324) */
-  for (uint64_t i = 0; i < n; ++i) {
-    double nat[OR_MAX_P], xb[OR_MAX_D], gam[OR_MAX_D];
-    int st, it;
-    to_natural_m(c->model, (int)p, tb + i * p, nat);
-    if ((rc = propagate_cfg(c, (int)d, nat, e->states + i * d, t_prev, t_obs, xb, gam, &st, &it)))
-      goto done;
-    if (out && out->newton_iters) out->newton_iters[i] = it;
-    ll_bar[i] = st == OR_ST_OK ? or_log_likelihood(c, y, xb) : kNegInf;
+  /* predict + log-likelihood (filter.cpp:304-324), per particle over host
+     threads (par_for; the sparse model's bound operator is process-global,
+     so it stays on one thread) */
+  {
+    prop_ctx pc = {c, e, y, t_prev, t_obs, tb, ll_bar, NULL, NULL, NULL, out, (int)d, (int)p, OR_OK};
+    par_for(n, predict_body, &pc, c->model != OR_MODEL_ADVDIFF);
+    if ((rc = pc.rc)) goto done;
   }
   if (out && out->loglik_bar) memcpy(out->loglik_bar, ll_bar, sizeof(double) * n);
 
@@ -1170,23 +1276,12 @@ int or_pf_step(const or_cfg* c, or_ens* e, const double* y, uint64_t j,
     }
   }
 
-  /* repropagate + innovate + log-lik (filter.cpp:346-366) */
-  for (uint64_t i = 0; i < n; ++i) {
-    double nat[OR_MAX_P], xr[OR_MAX_D], gam[OR_MAX_D];
-    int st, it;
-    to_natural_m(c->model, (int)p, tnew + i * p, nat);
-    if ((rc = propagate_cfg(c, (int)d, nat, xs + i * d, t_prev, t_obs, xr, gam, &st, &it)))
-      goto done;
-    if (out && out->newton_iters) out->newton_iters[i] += it;
-    if (out && out->status_new) out->status_new[i] = st;
-    if (out && out->gamma) memcpy(out->gamma + i * d, gam, sizeof(double) * d);
-    ll_new[i] = kNegInf;
-    if (st != OR_ST_OK) continue;
-    memcpy(xs + i * d, xr, sizeof(double) * d);
-    stream sn;
-    stream_init(&sn, c->seed, j, i, OR_PURPOSE_INNOVATE);
-    for (uint64_t k = 0; k < d; ++k) xs[i * d + k] += sqrt(gam[k]) * next_normal(&sn);
-    ll_new[i] = or_log_likelihood(c, y, xs + i * d);
+  /* repropagate + innovate + log-lik (filter.cpp:346-366), per particle */
+  {
+    prop_ctx pc = {c, e, y, t_prev, t_obs, tnew, ll_new, xs, NULL, NULL, out, (int)d, (int)p, OR_OK};
+    pc.j = j;
+    par_for(n, repropagate_body, &pc, c->model != OR_MODEL_ADVDIFF);
+    if ((rc = pc.rc)) goto done;
   }
 
   /* update_weights (filter.cpp:210-222) + moments (filter.cpp:368-392) */

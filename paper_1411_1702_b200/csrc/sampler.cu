@@ -88,14 +88,26 @@ StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double
   return sp;
 }
 
+// The device error word is sticky: once a step fails, every later step's
+// kernels early-exit (grid_error) until the host has reported it, so a queued
+// run of non-blocking steps surfaces the FIRST failure at the next
+// synchronize (the reference throws out of filter::run at that step). The
+// host clears it after reading it.
+void clear_error(pfsmc_gpu_sampler* s) {
+  CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->st_host->error = 0;
+}
+
 void check_error(pfsmc_gpu_sampler* s) {
-  const DevState& st = *s->st_host;
-  if (st.error & kErrPredict)
+  const int err = s->st_host->error;
+  if (err) clear_error(s);
+  if (err & kErrPredict)
     throw NumericalError("total degeneracy: every particle has zero predictive likelihood");
-  if (st.error & kErrChol) throw NumericalError("chol_psd: degenerate covariance");
-  if (st.error & kErrUpdate)
+  if (err & kErrChol) throw NumericalError("chol_psd: degenerate covariance");
+  if (err & kErrUpdate)
     throw NumericalError("total degeneracy: every repropagated particle has zero likelihood");
-  if (st.error & kErrInternal) throw std::runtime_error("exact CDF: internal inconsistency");
+  if (err & kErrInternal) throw std::runtime_error("exact CDF: internal inconsistency");
 }
 
 void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
@@ -127,9 +139,9 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   CK(cudaGetLastError());
 }
 
-// Step prologue: clear per-step error/iteration counters (device memsets).
+// Step prologue: clear the per-step Newton-iteration counter. (The error
+// word is NOT cleared here: it is sticky, see check_error.)
 void enqueue_prologue(pfsmc_gpu_sampler* s) {
-  CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
   CK(cudaMemsetAsync(&s->st->newton_iters, 0, sizeof(unsigned long long), s->stream));
 }
 
@@ -186,6 +198,8 @@ void harvest_timing(pfsmc_gpu_sampler* s) {
 // previous step has completed, so the slot is free) or from the resident
 // device array (no host involvement).
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp) {
+  if (s->shard_api)
+    throw ConfigError("step: a shard handle runs only the sharded phases (pfsmc_gpu_shard_step / shard_*)");
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
   if (dev_sp) {
     CK(cudaMemcpyAsync(s->sp_dev, dev_sp, sizeof(StepParams), cudaMemcpyDeviceToDevice, s->stream));
@@ -217,7 +231,9 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     if (!cfg) throw ConfigError("null config");
     // PfConfig::validate (filter.cpp:45-74)
     if (cfg->particles == 0) throw ConfigError("config: particles must be >= 1");
-    if (cfg->particles > (1ULL << 31)) throw ConfigError("config: particles must be < 2^31 per handle");
+    if (cfg->particles / static_cast<uint64_t>(world) >= (1ULL << 31))
+      throw ConfigError("config: particles must be < 2^31 per handle");
+    if (cfg->particles >= (1ULL << 32)) throw ConfigError("config: particles must be < 2^32 in total");
     if (!(cfg->shrink_a > 0.0 && cfg->shrink_a < 1.0))
       throw ConfigError("config: shrink factor a must lie in (0, 1)");
     if (!(cfg->sigma > 0.0)) throw ConfigError("config: observation noise sigma must be positive");
@@ -377,13 +393,12 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
       s->gp_pred_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_pred * 2);
       s->gp_mom_all = s->dalloc<double>(static_cast<size_t>(world) * s->ngroups_upd * W);
       s->sums_all = s->dalloc<double>(2 * world);
-      s->sendbuf = s->dalloc<double>(static_cast<size_t>(world) * N * (c.R + kShardPW));
-      s->recvbuf = s->dalloc<double>(N * (c.R + kShardPW));
+      // sendbuf / recvbuf (counted NCCL exchange only): allocated on first use
       s->counts_dev = s->dalloc<unsigned>(2 * world);
       s->counts_all = s->dalloc<unsigned>(static_cast<size_t>(world) * world);
       CK(cudaMallocHost(&s->counts_host, (2 * world + world * world) * sizeof(unsigned)));
     }
-    build_graph(s.get());
+    if (!shard_api) build_graph(s.get());  // shard handles step through the sharded phases only
     *out = s.release();
     return PFSMC_GPU_OK;
   });
@@ -568,6 +583,7 @@ pfsmc_gpu_status pfsmc_gpu_synchronize(pfsmc_gpu_sampler* s, double* trace_out) 
 
 pfsmc_gpu_status pfsmc_gpu_run(pfsmc_gpu_sampler* s, double* rows, int* warn) {
   return guarded([&] {
+    if (s->shard_api) throw ConfigError("run: a shard handle runs only the sharded phases");
     const int w = 2 * s->p + s->d + 1;
     // row 0 from the current ensemble (filter.cpp:409-426)
     s->ks->moments(s->ctx, s->grid, s->stream, 0);

@@ -177,6 +177,8 @@ pfsmc_gpu_status guarded(F&& f) {
 int step_count(double t0, double t1, double h);
 StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs, double h);
 void check_error(pfsmc_gpu_sampler* s);
+void clear_error(pfsmc_gpu_sampler* s);
+void ensure_exchange_buffers(pfsmc_gpu_sampler* s);
 void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed);
 void enqueue_prologue(pfsmc_gpu_sampler* s);
 void build_graph(pfsmc_gpu_sampler* s);

@@ -174,6 +174,19 @@ void NCK(ncclResult_t r) {
 }
 
 
+// The counted exchange's payload buffers (world x N_local send slots, N_local
+// receive slots), allocated on first use: the peer-memory pull and the
+// offspring-allocation mode never touch them, so weak scaling does not pay
+// world x N_local payloads per GPU for a path it does not run.
+void ensure_exchange_buffers(pfsmc_gpu_sampler* s) {
+  if (s->sendbuf) return;
+  if (!s->shard_api) throw ConfigError("not a sharded handle");
+  const size_t PW = static_cast<size_t>(s->ctx.R + kShardPW);
+  const size_t N = static_cast<size_t>(s->N);
+  s->sendbuf = s->dalloc<double>(static_cast<size_t>(s->world) * N * PW);
+  s->recvbuf = s->dalloc<double>(N * PW);
+}
+
 extern "C" {
 
 // ---------------------------------------------------------------- sharded phases
@@ -186,6 +199,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
     const Ctx& c = s->ctx;
     const size_t W = static_cast<size_t>(s->ks->moment_width());
     const size_t PW = static_cast<size_t>(c.R + kShardPW);
+    if (which == 8 || which == 9) ensure_exchange_buffers(s);
     switch (which) {
       case 0: *ptr = c.gpart; *bytes = sizeof(double) * 2 * s->ngroups_pred; break;
       case 1: *ptr = s->gp_pred_all; *bytes = sizeof(double) * 2 * s->ngroups_pred * s->world; break;
@@ -255,6 +269,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
 // counts_out: [world] payloads this rank sends to each rank, then [world]
 // payloads it receives from each rank. Blocking (the exchange needs them).
 static void shard_serve_impl(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  ensure_exchange_buffers(s);
   {
     const int W = s->world;
     // counts_dev: [W] actual sends of this rank; counts_all: the W x W matrix
@@ -298,6 +313,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_count_matrix(pfsmc_gpu_sampler* s, uint32_t* ou
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv) {
   return guarded([&] {
     if (n_recv != static_cast<uint64_t>(s->N)) throw std::runtime_error("shard_update: payload count mismatch");
+    ensure_exchange_buffers(s);
     k_place<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->recvbuf, static_cast<long long>(n_recv));
     s->ks->update(s->ctx, s->grid, s->stream);
     CK(cudaGetLastError());
@@ -359,6 +375,19 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t
   });
 }
 
+// Drops a previous peer table: the peer-memory step graph captured it by
+// value (k_pull's arguments), and its IPC mappings are closed.
+static void drop_peers(pfsmc_gpu_sampler* s) {
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->shard_graph) cudaGraphExecDestroy(s->shard_graph);
+  s->shard_graph = nullptr;
+  s->shard_graph_refused = false;
+  for (void* q : s->ipc_opened) cudaIpcCloseMemHandle(q);
+  s->ipc_opened.clear();
+  s->peers = PeerTable{};
+  s->have_peers = false;
+}
+
 // ---- migration over NVLink peer memory --------------------------------------
 // The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
 // segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
@@ -385,6 +414,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
     if (!s->shard_api) throw ConfigError("not a sharded handle");
     if (s->world > kMaxRanks) throw ConfigError("attach_peers: at most 8 ranks");
     CK(cudaSetDevice(s->cfg.device));
+    drop_peers(s);
     const Ctx& c = s->ctx;
     PeerTable t{};
     for (int r = 0; r < s->world; ++r) {
@@ -422,6 +452,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
   return guarded([&] {
     if (!s->shard_api) throw ConfigError("not a sharded handle");
     if (s->world > kMaxRanks) throw ConfigError("attach_peers: at most 8 ranks");
+    drop_peers(s);
     PeerTable t{};
     for (int r = 0; r < s->world; ++r) {
       const pfsmc_gpu_sampler* o = shards[r];
@@ -446,14 +477,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
 pfsmc_gpu_status pfsmc_gpu_shard_detach_peers(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     CK(cudaSetDevice(s->cfg.device));
-    CK(cudaStreamSynchronize(s->stream));
-    if (s->shard_graph) cudaGraphExecDestroy(s->shard_graph);
-    s->shard_graph = nullptr;
-    s->shard_graph_refused = false;
-    for (void* q : s->ipc_opened) cudaIpcCloseMemHandle(q);
-    s->ipc_opened.clear();
-    s->peers = PeerTable{};
-    s->have_peers = false;
+    drop_peers(s);
     return PFSMC_GPU_OK;
   });
 }
@@ -579,6 +603,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
     const unsigned* mat = s->counts_host + 2 * W;
     const size_t item = sizeof(double) * static_cast<size_t>(c.R + kShardPW);
     const size_t cap = static_cast<size_t>(s->N);
+    ensure_exchange_buffers(s);
     char* send = reinterpret_cast<char*>(s->sendbuf);
     char* recv = reinterpret_cast<char*>(s->recvbuf);
     size_t off = 0;

@@ -33,7 +33,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .sampler import MODEL_DIMS, MODELS, GpuSampler, ObservationModel, PfConfig, TraceRow, _f64, _ptr
+from .sampler import MODEL_DIMS, MODELS, ConfigError, GpuSampler, ObservationModel, PfConfig, TraceRow, _f64, _ptr
 
 (BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
  BUF_CNT, BUF_CNT_ALL) = range(12)
@@ -77,6 +77,17 @@ class GpuShard(GpuSampler):
         self.n0 = rank * self.n
         self.row_width = 2 * self.p + self.d + 1
         self._bufs = {}
+
+    # -- a shard is one part of a global filter: the single-handle step ---
+    # paths would run on its local partials only (no global LSE / moments)
+    def pf_step(self, *a, **k):
+        raise ConfigError("a shard handle steps through ShardedFilter / native_step, not pf_step")
+
+    def run(self, *a, **k):
+        raise ConfigError("a shard handle steps through ShardedFilter / native_step, not run")
+
+    def step_resident(self, *a, **k):
+        raise ConfigError("a shard handle steps through ShardedFilter / native_step, not step_resident")
 
     # -- exchange buffers ------------------------------------------------
     def buffer(self, which: int):

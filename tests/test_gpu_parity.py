@@ -451,6 +451,51 @@ def test_total_degeneracy_raises_numerical_at_same_step():
     gpu.close()
 
 
+def test_queued_step_error_is_sticky():
+    """A failure inside a run of non-blocking resident steps (step 3 of 5: an
+    observation no particle can explain) surfaces at the next synchronize and
+    is not wiped by the steps queued after it; the ensemble stays at step 2's
+    (later steps early-exit), like filter::run throwing at that step."""
+    from paper_1411_1702_b200.sampler import NumericalError
+    n = 4096
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=2, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, 2, [0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+    ys = np.array([[1.1, 0.9], [1.0, 0.95], [1e200, 1e200], [1.0, 1.0], [1.0, 1.0]])
+    ts = 0.1 * np.arange(1, 6)
+    gpu = _sampler(sc, n)
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    gpu.upload_observations(ys, ts, 0.0)
+    gpu.step_resident(1)
+    gpu.step_resident(2)
+    gpu.synchronize()
+    after2 = gpu.get_ensemble()
+    for j in (3, 4, 5):
+        gpu.step_resident(j)
+    with pytest.raises(NumericalError, match="total degeneracy"):
+        gpu.synchronize()
+    got = gpu.get_ensemble()
+    assert np.array_equal(got.states, after2.states) and np.array_equal(got.params_u, after2.params_u)
+    gpu.synchronize()  # reported once: the word is clear again
+    gpu.pf_step(ys[3], 4, 0.2, 0.3)  # and the filter continues from step 2
+    gpu.close()
+
+
+def test_shard_handle_rejects_single_handle_step():
+    from paper_1411_1702_b200.sampler import ConfigError, PfConfig, ObservationModel
+    from paper_1411_1702_b200.sharded import GpuShard
+    sh = GpuShard("lv", PfConfig(particles=1 << 15, seed=1), ObservationModel([0, 1], 0.05), 0, 2)
+    with pytest.raises(ConfigError):
+        sh.pf_step([1.0, 1.0], 1, 0.0, 0.1)
+    # the C ABI refuses it too (not just the Python override)
+    import ctypes as C
+    y = np.array([1.0, 1.0])
+    out = np.zeros(8)
+    rc = sh.lib.pfsmc_gpu_step(sh.h, y.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(1), C.c_double(0.0),
+                               C.c_double(0.1), C.c_double(0.1), out.ctypes.data_as(C.POINTER(C.c_double)))
+    assert rc == 2
+    sh.close()
+
+
 def test_config_errors():
     from paper_1411_1702_b200.sampler import ConfigError
     with pytest.raises(ConfigError):
