@@ -275,6 +275,12 @@ def gather_peak(device, n_rec=1 << 25):
 
 
 C3_WINDOWS = (50, 200, 320)
+ARITH = "exact"  # --arithmetic: the device arithmetic variant (pfsmc_gpu_config.arithmetic)
+
+
+def _cfg(prob):
+    import dataclasses
+    return dataclasses.replace(prob.cfg, arithmetic=ARITH)
 
 
 def _timed_steps(gpu, prob, steps, warmup, stream, j0=0, t0=0.0):
@@ -430,7 +436,7 @@ def bench_workloads(local, fp64):
     # mid, stiff), since the cost per step grows with the Newton iterations
     n3 = 1 << 22
     prob = problems.robertson(particles=n3, T=400, seed=1)
-    g = GpuSampler("robertson", prob.cfg, prob.obs, device=local)
+    g = GpuSampler("robertson", _cfg(prob), prob.obs, device=local)
     prob.init(g)
     out["c3_robertson"] = c3 = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4",
                                 "likelihood": "lognormal (BASELINE extension)", "windows": {}}
@@ -464,7 +470,7 @@ def bench_workloads(local, fp64):
     # config 4: 8-compartment chain, 2^24, BDF3 m=3
     n4 = 1 << 24
     prob = problems.chain8(particles=n4, T=10, seed=1)
-    g = GpuSampler("chain", prob.cfg, prob.obs, device=local)
+    g = GpuSampler("chain", _cfg(prob), prob.obs, device=local)
     prob.init(g)
     ms, it = _timed_steps(g, prob, 2, 1, torch.cuda.ExternalStream(g.stream_handle, device=local))
     t = sum(ms) / len(ms)
@@ -490,7 +496,7 @@ def bench_workloads(local, fp64):
     # N = 2^20, beside the unmodified reference pf_step on a bounded sample
     nm = 1 << 20
     prob = problems.metabolic(particles=nm, n_obs=50, seed=1)
-    g = GpuSampler("metabolic", prob.cfg, prob.obs, device=local)
+    g = GpuSampler("metabolic", _cfg(prob), prob.obs, device=local)
     prob.init(g)
     ms, it = _timed_steps(g, prob, 5, 3, torch.cuda.ExternalStream(g.stream_handle, device=local))
     g.close()
@@ -592,7 +598,7 @@ def run_sharded(args, world, rank, local):
 
     n_local = args.particles
     prob = problems.lotka_volterra(particles=n_local * world, T=T_OBS, seed=1)
-    shard = GpuShard("lv", prob.cfg, prob.obs, rank, world, device=local)
+    shard = GpuShard("lv", _cfg(prob), prob.obs, rank, world, device=local)
     f = ShardedFilter([shard], TorchComm())
     f.initialize_uniform(**prob.prior)
     migration = "python-orchestrated, NCCL send/recv"
@@ -676,7 +682,11 @@ def main():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded path (NCCL collectives + migration) even at N = 1 (a check of that path)")
     ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")
+    ap.add_argument("--arithmetic", default="exact", choices=["exact", "fast"],
+                    help="device arithmetic: exact (reference op order, bitwise Psi) or fast (FMA; tolerance parity)")
     args = ap.parse_args()
+    global ARITH
+    ARITH = args.arithmetic
     world, rank, local = _dist()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
@@ -706,7 +716,7 @@ def main():
     T = min(T_OBS, 2 * args.steps + args.warmup + args.e2e_steps + 1)
     prob = problems.lotka_volterra(particles=n, T=T_OBS, seed=1)
     # replicas: every rank filters its own N-particle ensemble
-    cfg = prob.cfg
+    cfg = _cfg(prob)
     gpu = GpuSampler("lv", cfg, prob.obs, device=local)
     gpu.initialize_uniform(**prob.prior)
     gpu.upload_observations(prob.ys[:T], prob.times[:T], 0.0)
@@ -793,6 +803,7 @@ def main():
             "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles_per_gpu": n,
                        "global_particles": n * world, "d": D, "p": P, "h": 0.1, "shrink_a": 0.98,
                        "integrator": "am2 (reference semantics: m=1 => AM1 corrector, AB1 predictor)",
+                       "arithmetic": ARITH,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",

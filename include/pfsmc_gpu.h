@@ -60,6 +60,14 @@ enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
 /* Observation noise. GAUSSIAN is filter::log_likelihood (filter.cpp:124-141);
  * LOGNORMAL is an extension for BASELINE config 3 (no reference counterpart). */
 enum { PFSMC_GPU_LIK_GAUSSIAN = 0, PFSMC_GPU_LIK_LOGNORMAL = 1 };
+/* Device arithmetic. EXACT: the reference's operation order without FMA
+ * contraction and IEEE divisions where the reference divides (the reference
+ * build has no FMA, CMakeLists.txt:7-9), so Psi is bitwise the CPU's.
+ * FAST: FMA contraction and one reciprocal per shared denominator; results
+ * within the north_star tolerances (states 1e-10 relative, trace 1e-8,
+ * ancestors exact except classified near-ties), not bitwise. Same RNG
+ * streams, same exact resampling CDF. */
+enum { PFSMC_GPU_ARITH_EXACT = 0, PFSMC_GPU_ARITH_FAST = 1 };
 
 typedef struct pfsmc_gpu_sampler pfsmc_gpu_sampler;
 
@@ -87,6 +95,7 @@ typedef struct pfsmc_gpu_config {
                               (lmm::adaptive_bdf_interval, lmm.cpp:894-1019); family,
                               order and the step h are then unused */
   double rtol;             /* IntegratorSpec.rtol (adaptive only; reference default 1e-3) */
+  int arithmetic;          /* PFSMC_GPU_ARITH_EXACT (default, 0) or PFSMC_GPU_ARITH_FAST */
 } pfsmc_gpu_config;
 
 const char* pfsmc_gpu_version(void);
@@ -242,11 +251,13 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_nccl(pfsmc_gpu_sampler* s, const uint8_t
 pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
                                       double t_obs, double h, double* trace_out);
 /* Migration over NVLink peer memory (replaces the counted send/recv and its
- * host sync inside pfsmc_gpu_shard_step): each rank exports 6 CUDA IPC handles
- * (6 x 64 bytes: its record buffers, ll_bar, exact CDF, segment ends, guide),
- * the caller allgathers them (world x 384 bytes, rank order) and every rank
- * attaches; then each slot pulls its ancestor from the serving rank's memory. */
-pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out384);
+ * host sync inside pfsmc_gpu_shard_step): each rank exports PFSMC_GPU_IPC_BYTES
+ * of CUDA IPC handles (7 x 64 bytes: its record buffers, ll_bar, exact CDF,
+ * segment ends, guide, offspring prefix), the caller allgathers them (world x
+ * PFSMC_GPU_IPC_BYTES, rank order) and every rank attaches; then each slot
+ * pulls its ancestor from the serving rank's memory. */
+#define PFSMC_GPU_IPC_BYTES 448
+pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out448);
 pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles);
 /* Back to the counted send / receive (if any rank failed to map its peers). */
 pfsmc_gpu_status pfsmc_gpu_shard_detach_peers(pfsmc_gpu_sampler* s);
@@ -258,6 +269,36 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
  * rank's tables are complete (after the resolve phase). */
 pfsmc_gpu_status pfsmc_gpu_shard_pull(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
+
+/* Migration mode of the sharded step (north_star).
+ * EXACT (default): every slot's ancestor from the global multinomial, bitwise
+ * the single handle (ancestors, states, trace); (G-1)/G of the slots fetch a
+ * remote ancestor whatever the weights.
+ * OFFSPRING: the same keyed uniforms and exact CDF give each particle its
+ * offspring count o_i (bitwise the single handle's counts, i.e.
+ * bincount(ancestors)); the children are laid out in ancestor order, rank by
+ * rank, so each GPU builds its children from its own ancestors and only the
+ * load imbalance (children beyond its N_local slots) migrates; children are
+ * keyed by their new global slot (a relabelling: distributionally equivalent
+ * to the single handle, not bitwise, after the first step). */
+enum { PFSMC_GPU_SHARD_EXACT = 0, PFSMC_GPU_SHARD_OFFSPRING = 1 };
+pfsmc_gpu_status pfsmc_gpu_shard_set_mode(pfsmc_gpu_sampler* s, int mode);
+/* Offspring mode, phase by phase (after shard_resolve): the walk of every
+ * global slot's uniform (no exchange) -> this rank's per-particle counts and
+ * the children of every rank (totals_out: world counts, identical on all
+ * ranks); blocking. */
+pfsmc_gpu_status pfsmc_gpu_shard_offspring(pfsmc_gpu_sampler* s, uint64_t* totals_out);
+/* ... the per-particle offspring counts of this rank's particles (N_local). */
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_counts(pfsmc_gpu_sampler* s, uint32_t* counts_out);
+/* ... counted path: packs this rank's children per destination into buffer 8
+ * (the shard_serve layout: destination d's items at d * N_local) and returns
+ * the world x world item matrix (row q = rank q's sends); exchange as for
+ * shard_serve, then shard_update(N_local). */
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_pack(pfsmc_gpu_sampler* s, uint32_t* matrix_out);
+/* ... peer-memory path: every slot pulls its child's ancestor from the rank
+ * whose children cover it, then the update kernel (replaces pack + exchange
+ * + shard_update). */
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_pull(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */
 pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out);

@@ -73,6 +73,7 @@ struct PfConfig {
   double model_consts[8] = {1.0, 1.0, 1.0, 5.0, 2.0, 1.0, 0.0, 0.0};
   bool adaptive = false;  // IntegratorSpec.adaptive (variable-step BDF(1,2))
   double rtol = 1e-3;     // IntegratorSpec.rtol
+  bool fast_arithmetic = false;  // PFSMC_GPU_ARITH_FAST: FMA + shared reciprocals (within tolerance)
 };
 
 // filter::TraceRow (filter.hpp:67-75).
@@ -104,6 +105,7 @@ class Sampler {
     for (int k = 0; k < 8; ++k) c.model_consts[k] = cfg.model_consts[k];
     c.adaptive = cfg.adaptive ? 1 : 0;
     c.rtol = cfg.rtol;
+    c.arithmetic = cfg.fast_arithmetic ? PFSMC_GPU_ARITH_FAST : PFSMC_GPU_ARITH_EXACT;
     check(pfsmc_gpu_create(&c, &h_));
   }
   ~Sampler() { pfsmc_gpu_destroy(h_); }

@@ -5,7 +5,9 @@ Every translation unit is compiled for sm_100a only
 the static CUDA runtime. ``--fmad=false`` keeps the device arithmetic in the
 reference's evaluation order without FMA contraction (the reference's own
 build has none: /root/reference/proj/CMakeLists.txt:7-9), which is what makes
-Psi bitwise comparable to the CPU oracle.
+Psi bitwise comparable to the CPU oracle. The propagating kernel units are
+compiled a second time as the FAST variant (``-DPFSMC_FAST=1 --fmad=true``,
+csrc/variant.cuh) for handles created with PFSMC_GPU_ARITH_FAST.
 """
 from __future__ import annotations
 
@@ -26,6 +28,12 @@ SOURCES = ["sampler.cu", "scan.cu", "shard.cu", "c5.cu", "kernels_decay.cu", "ke
            "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu", "kernels_advdiff.cu", "kernels_advdiff_e1.cu",
            "kernels_advdiff_e3.cu", "kernels_advdiff_e8.cu",
            "experiment.cpp"]  # host-only: the experiment-level drop-in (pfsmc_gpu_experiment.h)
+# The performance variant of the propagating kernels (csrc/variant.cuh): the
+# same units with FMA contraction and shared reciprocals, selected per handle
+# by pfsmc_gpu_config.arithmetic = PFSMC_GPU_ARITH_FAST.
+FAST_SOURCES = ["kernels_decay.cu", "kernels_lv.cu", "kernels_robertson.cu", "kernels_chain.cu",
+                "kernels_metabolic.cu"]
+FAST_FLAGS = [f if f != "--fmad=false" else "--fmad=true" for f in FLAGS] + ["-DPFSMC_FAST=1"]
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -39,10 +47,13 @@ def _stale(obj: str, src: str) -> bool:
 
 
 def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+    fast = src.startswith("fast:")
+    src = src[5:] if fast else src
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ("_fast.o" if fast else ".o"))
     path = os.path.join(CSRC, src)
     if _stale(obj, path):
-        flags = FLAGS if src.endswith(".cu") else ["-O2", "-std=c++17", "-Xcompiler", "-fPIC"]
+        flags = (FAST_FLAGS if fast else FLAGS) if src.endswith(".cu") else ["-O2", "-std=c++17", "-Xcompiler",
+                                                                             "-fPIC"]
         cmd = [NVCC, *flags, "-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -55,8 +66,9 @@ def _compile(src: str) -> str:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
+    units = SOURCES + ["fast:" + f for f in FAST_SOURCES]
+    with ThreadPoolExecutor(max_workers=len(units)) as ex:
+        objs = list(ex.map(_compile, units))
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -22,9 +22,10 @@
 // order. Windows are ~log2(N) per scan (one per binade crossing), so the
 // serial part is tiny. Elements with g == 0 are the identity.
 #pragma once
+#include "variant.cuh"
 #include <cstdint>
 
-namespace pfsmc_gpu {
+PFSMC_BEGIN
 
 // Binade index with the subnormal range folded into e = -1022
 // (ulp 2^-1074 on [0, 2^-1021)).
@@ -132,4 +133,4 @@ __device__ __forceinline__ bool piece_apply(const Piece& a, double& s) {
   return true;
 }
 
-}  // namespace pfsmc_gpu
+PFSMC_END  // namespace pfsmc_gpu::PFSMC_VNS

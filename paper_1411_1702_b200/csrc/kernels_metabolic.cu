@@ -1,10 +1,12 @@
 // Kernel instantiations for MetabolicModel (the reference's problem 1,
 // models.cpp:37-119): every (family, order) of the fixed-step integrator set
 // (lmm.cpp:64-77: AB/AM/BDF x orders 1-3).
+// Built twice: exact (reference operation order) and fast (-DPFSMC_FAST=1
+// --fmad=true), see variant.cuh.
 #include "kernels.cuh"
 
 namespace pfsmc_gpu {
-std::unique_ptr<KernelSet> make_kernels_metabolic(int fam, int order) {
+std::unique_ptr<KernelSet> PFSMC_ENTRY(metabolic)(int fam, int order) {
   return make_family<MetabolicModel>(fam, order);
 }
 }  // namespace pfsmc_gpu

@@ -17,9 +17,10 @@
 // every history index is static and nothing touches local memory; for large d
 // (the 8-species chain) one runtime-order body keeps the code in the I-cache.
 #pragma once
+#include "variant.cuh"
 #include "models.cuh"
 
-namespace pfsmc_gpu {
+PFSMC_BEGIN
 
 enum Family : int { kAB = 0, kAM = 1, kBDF = 2 };
 enum ParticleStatus : int { kOk = 0, kInvalidRhs = 1, kNewtonDivergence = 2, kSingular = 3, kStiffness = 4 };
@@ -72,6 +73,9 @@ __device__ __forceinline__ double ref_clamp(double v, double lo, double hi) {
 template <int D>
 __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[D]) {
   int piv[D];
+#if PFSMC_FAST
+  double invd[D];  // fast variant: back substitution multiplies by the pivot reciprocals
+#endif
 #pragma unroll
   for (int col = 0; col < D; ++col) {
     int pivot = col;
@@ -98,6 +102,9 @@ __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[
       }
     }
     const double inv = 1.0 / A[col][col];
+#if PFSMC_FAST
+    invd[col] = inv;
+#endif
 #pragma unroll
     for (int r = col + 1; r < D; ++r) {
       const double f = A[r][col] * inv;
@@ -125,7 +132,11 @@ __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[
   for (int ii = D - 1; ii >= 0; --ii) {
 #pragma unroll
     for (int j = ii + 1; j < D; ++j) b[ii] -= A[ii][j] * b[j];
+#if PFSMC_FAST
+    b[ii] *= invd[ii];
+#else
     b[ii] /= A[ii][ii];
+#endif
   }
   return true;
 }
@@ -175,6 +186,21 @@ __device__ __forceinline__ bool band_solve(const typename M::K& mk, double tn, c
     fast &= !(fabs(sb[c]) > fabs(dg[c]));
   }
   if (!fast) return dense_newton_solve<M>(mk, tn, th, x, hb0, b);
+#if PFSMC_FAST
+  // fast variant: the D pivot reciprocals in one batch; forward elimination
+  // and back substitution multiply by them (no division)
+  {
+    double one[D], inv[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) one[i] = 1.0;
+    ddiv_batch<D>(one, dg, inv);
+#pragma unroll
+    for (int i = 1; i < D; ++i) b[i] -= (sb[i - 1] * inv[i - 1]) * b[i - 1];
+#pragma unroll
+    for (int i = 0; i < D; ++i) b[i] *= inv[i];
+    return true;
+  }
+#endif
   // the D - 1 pivot reciprocals (inv = 1 / pivot, linalg.cpp:215) and the D
   // back-substitution divisions are independent: batched IEEE divisions
   double one[D - 1], inv[D - 1];
@@ -654,4 +680,4 @@ struct Propagator {
   }
 };
 
-}  // namespace pfsmc_gpu
+PFSMC_END  // namespace pfsmc_gpu::PFSMC_VNS

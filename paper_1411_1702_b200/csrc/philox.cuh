@@ -11,6 +11,7 @@
 // of fl(2 pi u)) and are the one
 // place device streams are not bitwise equal to the host's.
 #pragma once
+#include "variant.cuh"
 #include <cstdint>
 
 #ifdef __CUDACC__
@@ -19,7 +20,7 @@
 #define PF_HD inline
 #endif
 
-namespace pfsmc_gpu {
+PFSMC_BEGIN
 
 enum Purpose : uint64_t { kInit = 0, kProliferate = 1, kInnovate = 2, kResample = 3 };
 
@@ -160,4 +161,4 @@ PF_HD double resample_uniform(uint64_t seed, uint64_t j, uint64_t n) {
   return u64_to_uniform(philox4x64(0, j, n, kResample, seed, kKeyConstant).v[0]);
 }
 
-}  // namespace pfsmc_gpu
+PFSMC_END  // namespace pfsmc_gpu::PFSMC_VNS

@@ -10,9 +10,10 @@
 // Cross-block combination uses the "last block done" pattern in two levels
 // (groups of kGroup blocks, then the groups), so no launch is spent on it.
 #pragma once
+#include "variant.cuh"
 #include <cstdint>
 
-namespace pfsmc_gpu {
+PFSMC_BEGIN
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -259,4 +260,4 @@ __device__ __forceinline__ SumCnt block_excl_scan_sc(SumCnt v, SumCnt& total, Su
   return ex;
 }
 
-}  // namespace pfsmc_gpu
+PFSMC_END  // namespace pfsmc_gpu::PFSMC_VNS

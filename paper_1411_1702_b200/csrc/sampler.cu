@@ -261,8 +261,11 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     s->cfg = *cfg;
     CK(cudaSetDevice(cfg->device));
     // adaptive: the variable-step BDF(1,2) kernels (order slot 0)
-    s->ks = cfg->adaptive ? make_kernels(cfg->model, PFSMC_GPU_BDF, 0, grid_n)
-                          : make_kernels(cfg->model, cfg->family, cfg->order, grid_n);
+    if (cfg->arithmetic != PFSMC_GPU_ARITH_EXACT && cfg->arithmetic != PFSMC_GPU_ARITH_FAST)
+      throw ConfigError("config: arithmetic must be PFSMC_GPU_ARITH_EXACT or PFSMC_GPU_ARITH_FAST");
+    const bool fast = cfg->arithmetic == PFSMC_GPU_ARITH_FAST;
+    s->ks = cfg->adaptive ? make_kernels(cfg->model, PFSMC_GPU_BDF, 0, grid_n, fast)
+                          : make_kernels(cfg->model, cfg->family, cfg->order, grid_n, fast);
     if (!s->ks) throw ConfigError("unknown model id");
     if (cfg->model == MetabolicModel::ID && !(cfg->model_consts[5] > 0.0))
       throw ConfigError("metabolic model: tau must be positive");  // MetabolicModel ctor, models.cpp:104-108
@@ -397,6 +400,12 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
       s->counts_dev = s->dalloc<unsigned>(2 * world);
       s->counts_all = s->dalloc<unsigned>(static_cast<size_t>(world) * world);
       CK(cudaMallocHost(&s->counts_host, (2 * world + world * world) * sizeof(unsigned)));
+      // offspring-allocation mode (shard.cu)
+      s->ocnt = s->dalloc<unsigned>(N + 1);
+      s->ooff = s->dalloc<unsigned>(N + 1);
+      s->oblk = s->dalloc<unsigned>(N / 2048 + 2);
+      s->otot = s->dalloc<unsigned long long>(world);
+      CK(cudaMallocHost(&s->otot_host, world * sizeof(unsigned long long)));
     }
     if (!shard_api) build_graph(s.get());  // shard handles step through the sharded phases only
     *out = s.release();

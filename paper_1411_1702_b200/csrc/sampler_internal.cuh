@@ -48,7 +48,19 @@ struct PeerTable {
   const double* cdf[kMaxRanks];
   const double* seg_end[kMaxRanks];
   const unsigned* coarse[kMaxRanks];
+  const unsigned* ooff[kMaxRanks];  // offspring mode: exclusive prefix of per-particle offspring counts
 };
+
+// Migration modes of a sharded step (pfsmc_gpu_shard_set_mode):
+//  EXACT      every slot fetches the ancestor the global multinomial gives it
+//             (bitwise the single handle; (G-1)/G of all slots cross GPUs);
+//  OFFSPRING  the same uniforms and exact CDF give each particle its offspring
+//             count (bitwise the single handle's counts); the children are laid
+//             out in ancestor order, shard by shard, so each GPU builds its
+//             children from its own ancestors and only the load imbalance
+//             (children beyond a GPU's N_local) migrates. Slots are relabelled:
+//             the children are a permutation of the single handle's, keyed by
+//             their new global slot (distributionally equivalent after step 1).
 
 // launchers of kernels that live in another unit (scan.cu)
 void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which);
@@ -127,6 +139,12 @@ struct pfsmc_gpu_sampler {
   unsigned* counts_dev = nullptr;  // [world] send + [world] recv
   unsigned* counts_all = nullptr;  // the W x W migration count matrix (k_serve_sharded)
   unsigned* counts_host = nullptr; // pinned mirror
+  int shard_mode = 0;              // 0 exact, 1 offspring (PFSMC_GPU_SHARD_*)
+  unsigned* ocnt = nullptr;        // offspring counts per local particle (N_local + 1)
+  unsigned* ooff = nullptr;        // their exclusive prefix (N_local + 1; [N_local] = this rank's children)
+  unsigned* oblk = nullptr;        // scan block sums
+  unsigned long long* otot = nullptr;       // children per rank (world), from the global walk
+  unsigned long long* otot_host = nullptr;  // pinned mirror
 
   template <typename T>
   T* dalloc(size_t count) {
@@ -149,6 +167,7 @@ struct pfsmc_gpu_sampler {
     if (st_host) cudaFreeHost(st_host);
     if (xmean_host) cudaFreeHost(xmean_host);
     if (counts_host) cudaFreeHost(counts_host);
+    if (otot_host) cudaFreeHost(otot_host);
     if (stream) cudaStreamDestroy(stream);
   }
 };

@@ -142,9 +142,191 @@ __global__ void k_shard_offset(Ctx c, const double* gathered) {
   c.shard_off[1] = n;
 }
 
-// Injected-fitness parity path (pfsmc_gpu_resample_from_g): tile sums of
-// the given g (in place of the predict kernel's block partials), then the
-// same tile prefixes with lse = 0.
+// ---- offspring-allocation mode (north_star) ----------------
+// The single handle's multinomial gives slot n the ancestor
+// l_n = upper_bound(CDF, u_n) (filter.cpp:169-176); particle i's offspring
+// count is o_i = #{n : l_n = i}. Every rank walks the keyed uniforms of ALL
+// global slots (identical numbers everywhere, no exchange): the serving rank
+// of each u (allgathered exact shard ranges) gives every rank's child total,
+// and the uniforms this rank serves are searched in its exact CDF tables, so
+// o_i is bitwise the single handle's count. The children are then laid out
+// in ancestor order, rank by rank: rank r's children occupy global positions
+// [P_r, P_r + O_r), P the exclusive prefix of the totals. Position p belongs
+// to rank p / N_local, so a rank builds its own children from its own
+// ancestors and only the imbalance (children outside its slot range) crosses
+// GPUs.
+__global__ void __launch_bounds__(kThreads) k_offspring_walk(Ctx c, unsigned* ocnt, unsigned long long* otot) {
+  if (grid_error(c)) return;
+  const int lane = threadIdx.x & 31;
+  for (long long ng = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; ng < c.n_glob;
+       ng += static_cast<long long>(gridDim.x) * kThreads) {
+    const double u = resample_uniform(c.seed, c.sp->j, ng);
+    const int r = serving_rank(c, u);
+    const unsigned grp = __match_any_sync(0xffffffffu, r);
+    if (lane == __ffs(grp) - 1) atomicAdd(&otot[r], static_cast<unsigned long long>(__popc(grp)));
+    const bool mine = r == c.rank;
+    if (!__any_sync(0xffffffffu, mine)) continue;
+    const unsigned a = find_ancestor_warp(c, mine ? u : -1.0);
+    if (mine) atomicAdd(&ocnt[a], 1u);
+  }
+}
+
+// Exclusive prefix of the per-particle counts (N_local + 1 entries), three
+// passes over 2048-element blocks (counts and totals are exact integers).
+constexpr int kOffItems = 8;
+constexpr int kOffBlock = kOffItems * kThreads;
+__global__ void __launch_bounds__(kThreads) k_off_blocksum(const unsigned* cnt, long long n, unsigned* bsum) {
+  __shared__ int sw[2 * kWarps];
+  const long long base = static_cast<long long>(blockIdx.x) * kOffBlock + threadIdx.x * kOffItems;
+  unsigned v = 0;
+#pragma unroll
+  for (int i = 0; i < kOffItems; ++i) v += base + i < n ? cnt[base + i] : 0u;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = static_cast<int>(v);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < kWarps; ++w) t += static_cast<unsigned>(sw[w]);
+    bsum[blockIdx.x] = t;
+  }
+}
+__global__ void __launch_bounds__(1024) k_off_scan_blocks(unsigned* bsum, int nb) {
+  // one block: exclusive scan of nb block sums (serial per thread chunk + warp scans)
+  __shared__ unsigned sw[32];
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per, b1 = min(b0 + per, nb);
+  unsigned s = 0;
+  for (int b = b0; b < b1; ++b) s += bsum[b];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = sw[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    sw[lane] = t;
+  }
+  __syncthreads();
+  unsigned ex = x - s + (w ? sw[w - 1] : 0u);
+  for (int b = b0; b < b1; ++b) {
+    const unsigned v = bsum[b];
+    bsum[b] = ex;
+    ex += v;
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_off_apply(const unsigned* cnt, long long n, const unsigned* bsum,
+                                                        unsigned* off) {
+  __shared__ int sw[2 * kWarps];
+  const long long base = static_cast<long long>(blockIdx.x) * kOffBlock + threadIdx.x * kOffItems;
+  unsigned v[kOffItems], s = 0;
+#pragma unroll
+  for (int i = 0; i < kOffItems; ++i) {
+    v[i] = base + i < n ? cnt[base + i] : 0u;
+    s += v[i];
+  }
+  int total;
+  // block-exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sw[w] = static_cast<int>(x);
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = lane < kWarps ? static_cast<unsigned>(sw[lane]) : 0u;
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kWarps) sw[kWarps + lane] = static_cast<int>(t);
+  }
+  __syncthreads();
+  total = sw[2 * kWarps - 1];
+  (void)total;
+  unsigned ex = bsum[blockIdx.x] + x - s + (w ? static_cast<unsigned>(sw[kWarps + w - 1]) : 0u);
+#pragma unroll
+  for (int i = 0; i < kOffItems; ++i) {
+    if (base + i <= n) off[base + i] = ex;  // off[n] = the total
+    ex += v[i];
+  }
+}
+
+// Children of this rank and their global positions from the walk totals.
+__device__ __forceinline__ long long offspring_prefix(const Ctx& c, const unsigned long long* otot, int r) {
+  long long p = 0;
+  for (int q = 0; q < r; ++q) p += static_cast<long long>(otot[q]);
+  return p;
+}
+
+// The ancestor of local child k: the last i with off[i] <= k (off is the
+// exclusive prefix of the counts, so children of i are off[i] .. off[i+1]-1).
+__device__ __forceinline__ unsigned child_ancestor(const unsigned* off, long long n, unsigned k) {
+  long long lo = 0, hi = n - 1;  // off[lo] <= k < off[hi + 1]
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (__ldcg(&off[mid]) <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return static_cast<unsigned>(lo);
+}
+
+// Counted path: this rank's children, packed per destination rank into the
+// send regions (dest d at d * cap) as {record, ll_bar, global ancestor,
+// local slot on d} — the k_place payload layout.
+__global__ void __launch_bounds__(kThreads) k_offspring_pack(Ctx c, const unsigned* off,
+                                                             const unsigned long long* otot, double* sendbuf,
+                                                             long long cap) {
+  if (grid_error(c)) return;
+  const long long P = offspring_prefix(c, otot, c.rank);
+  const long long O = static_cast<long long>(otot[c.rank]);
+  const int W = c.R + kShardPW;
+  const double* rec = c.rec[c.st->cur];
+  for (long long k = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; k < O;
+       k += static_cast<long long>(gridDim.x) * kThreads) {
+    const long long p = P + k;             // global position of the child
+    const int d = static_cast<int>(p / c.N);
+    const long long first = max(P, static_cast<long long>(d) * c.N);  // this rank's first child on d
+    const unsigned a = child_ancestor(off, c.N, static_cast<unsigned>(k));
+    double* dst = sendbuf + (static_cast<long long>(d) * cap + (p - first)) * W;
+    const double2* src = reinterpret_cast<const double2*>(rec + static_cast<long long>(a) * c.R);
+    for (int i = 0; i < c.R / 2; ++i) reinterpret_cast<double2*>(dst)[i] = __ldg(src + i);
+    reinterpret_cast<double2*>(dst)[c.R / 2] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(c.n0 + a));
+    reinterpret_cast<double2*>(dst)[c.R / 2 + 1] = make_double2(static_cast<double>(p - static_cast<long long>(d) * c.N), 0.0);
+  }
+}
+
+// Peer-memory path: each slot of this rank pulls its child's ancestor from
+// the rank whose children cover that position (mostly itself).
+__global__ void __launch_bounds__(kThreads) k_offspring_pull(Ctx c, PeerTable pt, const unsigned long long* otot) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  if (n >= c.N) return;
+  const long long p = c.n0 + n;
+  int q = 0;
+  long long P = 0;
+  while (q + 1 < c.world && P + static_cast<long long>(otot[q]) <= p) {
+    P += static_cast<long long>(otot[q]);
+    ++q;
+  }
+  const unsigned a = child_ancestor(pt.ooff[q], c.N, static_cast<unsigned>(p - P));
+  const double* rec = (c.st->cur ? pt.rec1[q] : pt.rec0[q]) + static_cast<long long>(a) * c.R;
+  const double2* src = reinterpret_cast<const double2*>(rec);
+  double2* dst = reinterpret_cast<double2*>(c.payload + n * (c.R + 2));
+  for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldcg(src + i);
+  const long long ga = static_cast<long long>(q) * c.N + a;
+  dst[c.R / 2] = make_double2(__ldcg(&pt.llbar[q][a]), static_cast<double>(ga));
+  c.anc[n] = static_cast<unsigned>(ga);
+}
+
 }  // namespace pfsmc_gpu
 
 const NcclApi& nccl_api() {
@@ -187,7 +369,115 @@ void ensure_exchange_buffers(pfsmc_gpu_sampler* s) {
   s->recvbuf = s->dalloc<double>(N * PW);
 }
 
+// Offspring mode, device part: the global walk (per-particle counts of this
+// rank, children per rank) and the prefix of the counts. Enqueued only.
+static void enqueue_offspring(pfsmc_gpu_sampler* s) {
+  const long long N = s->N;
+  CK(cudaMemsetAsync(s->ocnt, 0, sizeof(unsigned) * (N + 1), s->stream));
+  CK(cudaMemsetAsync(s->otot, 0, sizeof(unsigned long long) * s->world, s->stream));
+  const long long nglob = s->ctx.n_glob;
+  const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
+  k_offspring_walk<<<g, kThreads, 0, s->stream>>>(s->ctx, s->ocnt, s->otot);
+  const int nb = static_cast<int>(N / kOffBlock + 1);
+  k_off_blocksum<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk);
+  k_off_scan_blocks<<<1, 1024, 0, s->stream>>>(s->oblk, nb);
+  k_off_apply<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk, s->ooff);
+  CK(cudaGetLastError());
+}
+
+// The offspring-mode migration matrix from the children per rank (identical
+// on every rank): S[q][d] = |[P_q, P_q + O_q) n [d N, (d + 1) N)|.
+static std::vector<uint64_t> offspring_matrix(const unsigned long long* tot, int W, long long N) {
+  std::vector<uint64_t> S(static_cast<size_t>(W) * W, 0);
+  long long P = 0;
+  for (int q = 0; q < W; ++q) {
+    const long long a = P, b = P + static_cast<long long>(tot[q]);
+    for (int d = 0; d < W; ++d) {
+      const long long lo = std::max(a, d * N), hi = std::min(b, (d + 1) * N);
+      if (hi > lo) S[static_cast<size_t>(q) * W + d] = static_cast<uint64_t>(hi - lo);
+    }
+    P = b;
+  }
+  return S;
+}
+
+static void offspring_totals_impl(pfsmc_gpu_sampler* s) {
+  enqueue_offspring(s);
+  CK(cudaMemcpyAsync(s->otot_host, s->otot, sizeof(unsigned long long) * s->world, cudaMemcpyDeviceToHost,
+                     s->stream));
+  CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  check_error(s);
+  unsigned long long tot = 0;
+  for (int q = 0; q < s->world; ++q) tot += s->otot_host[q];
+  if (tot != static_cast<unsigned long long>(s->ctx.n_glob)) throw std::runtime_error("offspring: child total mismatch");
+}
+
+static void offspring_pack_impl(pfsmc_gpu_sampler* s) {
+  ensure_exchange_buffers(s);
+  const long long O = static_cast<long long>(s->otot_host[s->rank]);
+  const int g = static_cast<int>(std::max<long long>(1, std::min<long long>((O + kThreads - 1) / kThreads, 148LL * 16)));
+  k_offspring_pack<<<g, kThreads, 0, s->stream>>>(s->ctx, s->ooff, s->otot, s->sendbuf, s->N);
+  CK(cudaGetLastError());
+}
+
 extern "C" {
+
+// ---------------------------------------------------------------- offspring mode
+pfsmc_gpu_status pfsmc_gpu_shard_set_mode(pfsmc_gpu_sampler* s, int mode) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (mode != PFSMC_GPU_SHARD_EXACT && mode != PFSMC_GPU_SHARD_OFFSPRING)
+      throw ConfigError("shard_set_mode: unknown migration mode");
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->shard_graph) cudaGraphExecDestroy(s->shard_graph);  // captured for the other mode
+    s->shard_graph = nullptr;
+    s->shard_graph_refused = false;
+    s->shard_mode = mode;
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_offspring(pfsmc_gpu_sampler* s, uint64_t* totals_out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    offspring_totals_impl(s);
+    if (totals_out)
+      for (int q = 0; q < s->world; ++q) totals_out[q] = s->otot_host[q];
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_counts(pfsmc_gpu_sampler* s, uint32_t* counts_out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    CK(cudaMemcpyAsync(counts_out, s->ocnt, sizeof(unsigned) * s->N, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_pack(pfsmc_gpu_sampler* s, uint32_t* matrix_out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    offspring_pack_impl(s);
+    if (matrix_out) {
+      const auto S = offspring_matrix(s->otot_host, s->world, s->N);
+      for (size_t i = 0; i < S.size(); ++i) matrix_out[i] = static_cast<uint32_t>(S[i]);
+    }
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_pull(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    if (!s->have_peers) throw ConfigError("shard_offspring_pull: no peer table (attach_peers / attach_peers_local)");
+    k_offspring_pull<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->peers, s->otot);
+    s->ks->update(s->ctx, s->grid, s->stream);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
 
 // ---------------------------------------------------------------- sharded phases
 // One handle per GPU, each owning global slots [rank*N/world, (rank+1)*N/world).
@@ -391,13 +681,13 @@ static void drop_peers(pfsmc_gpu_sampler* s) {
 // ---- migration over NVLink peer memory --------------------------------------
 // The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
 // segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
-constexpr int kPeerBufs = 6;
+constexpr int kPeerBufs = 7;  // + the offspring prefix (offspring mode)
 
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out) {
   return guarded([&] {
     if (!s->shard_api) throw ConfigError("not a sharded handle");
     const Ctx& c = s->ctx;
-    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse};
+    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse, s->ooff};
     for (int i = 0; i < kPeerBufs; ++i) {
       cudaIpcMemHandle_t h;
       CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
@@ -421,6 +711,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
       const void* p[kPeerBufs];
       if (r == s->rank) {
         p[0] = c.rec[0], p[1] = c.rec[1], p[2] = c.llbar, p[3] = c.cdf, p[4] = c.seg_end, p[5] = c.coarse;
+        p[6] = s->ooff;
       } else {
         for (int i = 0; i < kPeerBufs; ++i) {
           cudaIpcMemHandle_t h;
@@ -437,6 +728,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
       t.cdf[r] = static_cast<const double*>(p[3]);
       t.seg_end[r] = static_cast<const double*>(p[4]);
       t.coarse[r] = static_cast<const unsigned*>(p[5]);
+      t.ooff[r] = static_cast<const unsigned*>(p[6]);
     }
     s->peers = t;
     s->have_peers = true;
@@ -465,6 +757,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
       t.cdf[r] = c.cdf;
       t.seg_end[r] = c.seg_end;
       t.coarse[r] = c.coarse;
+      t.ooff[r] = o->ooff;
     }
     s->peers = t;
     s->have_peers = true;
@@ -515,8 +808,14 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
                   s->nccl, st));
   launch_scan(c, s->ntiles, st, 5);
   launch_scan(c, s->ntiles, st, 2);
-  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete everywhere
-  k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
+  if (s->shard_mode == PFSMC_GPU_SHARD_OFFSPRING) {
+    enqueue_offspring(s);  // counts + prefix from the global walk (no exchange)
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every rank's prefix complete
+    k_offspring_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers, s->otot);
+  } else {
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete everywhere
+    k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
+  }
   s->ks->update(c, s->grid, st);
   const size_t Wm = static_cast<size_t>(s->ks->moment_width());
   NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
@@ -597,10 +896,22 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
     launch_scan(c, s->ntiles, st, 2);
     CK(cudaGetLastError());
 
-    // D: exact-mode migration; the counts are the locally derived matrix
-    std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
-    shard_serve_impl(s, cnt.data());
-    const unsigned* mat = s->counts_host + 2 * W;
+    // D: migration. Exact mode: every slot's ancestor payload from its
+    // serving rank (the locally derived count matrix). Offspring mode: this
+    // rank's children in ancestor order, only the imbalance to other ranks.
+    std::vector<unsigned> omat;
+    const unsigned* mat;
+    if (s->shard_mode == PFSMC_GPU_SHARD_OFFSPRING) {
+      offspring_totals_impl(s);
+      offspring_pack_impl(s);
+      const auto S = offspring_matrix(s->otot_host, W, s->N);
+      omat.assign(S.begin(), S.end());
+      mat = omat.data();
+    } else {
+      std::vector<uint32_t> cnt(2 * static_cast<size_t>(W));
+      shard_serve_impl(s, cnt.data());
+      mat = s->counts_host + 2 * W;
+    }
     const size_t item = sizeof(double) * static_cast<size_t>(c.R + kShardPW);
     const size_t cap = static_cast<size_t>(s->N);
     ensure_exchange_buffers(s);

@@ -59,6 +59,8 @@ class NumericalError(PfsmcError):
     code = 3
 
 
+ARITHMETIC = {"exact": 0, "fast": 1}
+
 _ERRORS = {1: PfsmcError, 2: ConfigError, 3: NumericalError}
 
 _dp = C.POINTER(C.c_double)
@@ -72,7 +74,7 @@ class _Config(C.Structure):
                 ("newton_max_iter", C.c_int), ("particles", C.c_uint64),
                 ("obs_indices", _u64p), ("n_obs", C.c_uint64), ("sigma", C.c_double),
                 ("likelihood", C.c_int), ("device", C.c_int), ("model_consts", C.c_double * 8),
-                ("adaptive", C.c_int), ("rtol", C.c_double)]
+                ("adaptive", C.c_int), ("rtol", C.c_double), ("arithmetic", C.c_int)]
 
 
 def model_consts_array(model: str, consts=None):
@@ -144,6 +146,7 @@ class PfConfig:
     newton_max_iter: int = 20
     adaptive: bool = False  # IntegratorSpec.adaptive: variable-step BDF(1,2) (lmm.cpp:894-1019)
     rtol: float = 1e-3      # IntegratorSpec.rtol (adaptive only)
+    arithmetic: str = "exact"  # "exact" (reference op order, bitwise Psi) or "fast" (FMA; within tolerance)
 
 
 @dataclass
@@ -191,7 +194,7 @@ class GpuSampler:
                     cfg.newton_tol, cfg.newton_max_iter, cfg.particles,
                     _ptr(self._idx, _u64p), len(self._idx), obs.sigma,
                     LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts),
-                    int(cfg.adaptive), cfg.rtol)
+                    int(cfg.adaptive), cfg.rtol, ARITHMETIC[cfg.arithmetic])
         h = C.c_void_p()
         self._check(self.lib.pfsmc_gpu_create(C.byref(c), C.byref(h)))
         self.h = h

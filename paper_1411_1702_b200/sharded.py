@@ -38,6 +38,25 @@ from .sampler import MODEL_DIMS, MODELS, ConfigError, GpuSampler, ObservationMod
 (BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
  BUF_CNT, BUF_CNT_ALL) = range(12)
 STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
+IPC_BYTES = 448  # PFSMC_GPU_IPC_BYTES
+SHARD_MODES = {"exact": 0, "offspring": 1}  # PFSMC_GPU_SHARD_EXACT / _OFFSPRING
+
+
+def offspring_matrix(totals, world: int, n_local: int) -> np.ndarray:
+    """Offspring mode: rank q's children occupy global positions
+    [P_q, P_q + O_q) (P the exclusive prefix of the totals); position p lives
+    on rank p // n_local. S[q, d] = children of q placed on d (only the
+    off-diagonal imbalance crosses GPUs)."""
+    S = np.zeros((world, world), dtype=np.int64)
+    P = 0
+    for q in range(world):
+        a, b = P, P + int(totals[q])
+        for d in range(world):
+            lo, hi = max(a, d * n_local), min(b, (d + 1) * n_local)
+            if hi > lo:
+                S[q, d] = hi - lo
+        P = b
+    return S
 
 
 class _CudaArray:
@@ -53,7 +72,7 @@ class GpuShard(GpuSampler):
 
     def __init__(self, model: str, cfg: PfConfig, obs: ObservationModel, rank: int, world: int,
                  device: int = 0, model_consts=None):
-        from .sampler import FAMILIES, LIKELIHOODS, _Config, load_library, model_consts_array
+        from .sampler import ARITHMETIC, FAMILIES, LIKELIHOODS, _Config, load_library, model_consts_array
         self.lib = load_library()
         self.model, self.cfg, self.obs = model, cfg, obs
         self.d, self.p = MODEL_DIMS[MODELS[model]]
@@ -62,7 +81,7 @@ class GpuShard(GpuSampler):
         c = _Config(MODELS[model], FAMILIES[cfg.family], cfg.order, cfg.shrink_a, cfg.seed, cfg.newton_tol,
                     cfg.newton_max_iter, cfg.particles, _ptr(self._idx, C.POINTER(C.c_uint64)), len(self._idx),
                     obs.sigma, LIKELIHOODS[obs.likelihood], device, model_consts_array(model, model_consts),
-                    int(cfg.adaptive), cfg.rtol)
+                    int(cfg.adaptive), cfg.rtol, ARITHMETIC[cfg.arithmetic])
         L = self.lib
         for name in ("pfsmc_gpu_create_shard", "pfsmc_gpu_shard_buffer", "pfsmc_gpu_shard_predict",
                      "pfsmc_gpu_shard_finish_lse", "pfsmc_gpu_shard_scan_records",
@@ -148,7 +167,7 @@ class GpuShard(GpuSampler):
 
     def attach_peers(self, comm_group=None) -> bool:
         """Migration over NVLink peer memory: allgather every rank's CUDA IPC
-        handles (6 x 64 bytes) and map the peers' search tables and records.
+        handles (7 x 64 bytes) and map the peers' search tables and records.
         Returns False (the counted send / receive stays in use) if the mapping
         fails on any rank; every rank takes part in both collectives whatever
         happens locally, and a rank that mapped detaches again."""
@@ -157,10 +176,10 @@ class GpuShard(GpuSampler):
         L = self.lib
         for name in ("pfsmc_gpu_shard_ipc_handles", "pfsmc_gpu_shard_attach_peers", "pfsmc_gpu_shard_detach_peers"):
             getattr(L, name).restype = C.c_int
-        mine = np.zeros(384, dtype=np.uint8)
+        mine = np.zeros(IPC_BYTES, dtype=np.uint8)
         ok_local = L.pfsmc_gpu_shard_ipc_handles(self.h, mine.ctypes.data_as(C.POINTER(C.c_uint8))) == 0
         dev = f"cuda:{self.device}"
-        allh = torch.zeros(384 * self.world, dtype=torch.uint8, device=dev)
+        allh = torch.zeros(IPC_BYTES * self.world, dtype=torch.uint8, device=dev)
         dist.all_gather_into_tensor(allh, torch.from_numpy(mine).to(dev), group=comm_group)
         allh = allh.cpu().numpy()
         if ok_local:
@@ -179,6 +198,36 @@ class GpuShard(GpuSampler):
         hs = (C.c_void_p * self.world)(*[sh.h for sh in sorted(shards, key=lambda x: x.rank)])
         self._check(L.pfsmc_gpu_shard_attach_peers_local(self.h, hs))
         self.peers = True
+
+    # -- offspring-allocation mode ----------------------------------------
+    def set_mode(self, mode: str):
+        self.lib.pfsmc_gpu_shard_set_mode.restype = C.c_int
+        self._check(self.lib.pfsmc_gpu_shard_set_mode(self.h, SHARD_MODES[mode]))
+        self.mode = mode
+
+    def offspring(self) -> np.ndarray:
+        """Walk of every global slot's uniform: this rank's per-particle
+        offspring counts (device) and the children of every rank (returned)."""
+        self.lib.pfsmc_gpu_shard_offspring.restype = C.c_int
+        tot = np.zeros(self.world, dtype=np.uint64)
+        self._check(self.lib.pfsmc_gpu_shard_offspring(self.h, tot.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return tot
+
+    def offspring_counts(self) -> np.ndarray:
+        self.lib.pfsmc_gpu_shard_offspring_counts.restype = C.c_int
+        out = np.zeros(self.n, dtype=np.uint32)
+        self._check(self.lib.pfsmc_gpu_shard_offspring_counts(self.h, out.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return out
+
+    def offspring_pack(self) -> np.ndarray:
+        self.lib.pfsmc_gpu_shard_offspring_pack.restype = C.c_int
+        m = np.zeros(self.world * self.world, dtype=np.uint32)
+        self._check(self.lib.pfsmc_gpu_shard_offspring_pack(self.h, m.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return m.reshape(self.world, self.world)
+
+    def offspring_pull(self):
+        self.lib.pfsmc_gpu_shard_offspring_pull.restype = C.c_int
+        self._check(self.lib.pfsmc_gpu_shard_offspring_pull(self.h))
 
     def pull(self):
         """Phase D over peer memory + the update kernel."""
@@ -338,12 +387,23 @@ class TorchComm:
 class ShardedFilter:
     """The global filter over `shards` (this process's shards) and `comm`."""
 
-    def __init__(self, shards: List, comm, pull: bool = False):
+    def __init__(self, shards: List, comm, pull: bool = False, mode: str = "exact"):
         """pull: phase D as the peer-memory pull (shards attached with
-        attach_peers / attach_peers_local) instead of the counted exchange."""
+        attach_peers / attach_peers_local) instead of the counted exchange.
+        mode: "exact" (every slot's ancestor from the global multinomial,
+        bitwise the single handle) or "offspring" (per-particle offspring
+        counts from the same uniforms and exact CDF, children built on the
+        ancestor's shard, only the load imbalance migrates; see
+        pfsmc_gpu_shard_set_mode)."""
+        if mode not in SHARD_MODES:
+            raise ValueError(f"unknown migration mode {mode!r}")
         self.shards = sorted(shards, key=lambda s: s.rank)
         self.comm = comm
         self.pull = pull
+        self.mode = mode
+        for s in self.shards:
+            if hasattr(s, "set_mode"):
+                s.set_mode(mode)
         s0 = self.shards[0]
         self.d, self.p, self.world = s0.d, s0.p, s0.world
 
@@ -386,6 +446,24 @@ class ShardedFilter:
         comm.allgather_slices(sh, BUF_HDR)                               # C
         comm.allgather_slices(sh, BUF_WIN)
         self._each(lambda s: s.resolve())
+        if self.mode == "offspring":
+            tot = [s.offspring() for s in sh][0]                         # identical on every rank
+            self.last_totals = np.asarray(tot, dtype=np.int64)
+            if self.pull:
+                comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                 # every rank's prefix complete
+                self._each(lambda s: s.offspring_pull())
+            else:
+                mats = [s.offspring_pack() for s in sh]
+                S = offspring_matrix(tot, self.world, sh[0].n)
+                for m in mats:
+                    if not np.array_equal(np.asarray(m, dtype=np.int64), S):
+                        raise RuntimeError("offspring exchange: matrix mismatch")
+                counts = {r: S[r] for r in range(self.world)}
+                comm.exchange(sh, counts, 8 * sh[0].payload_doubles())   # D: only the imbalance
+                for s in sh:
+                    s.update(int(S[:, s.rank].sum()))
+            comm.allgather(sh, BUF_MOM, BUF_MOM_ALL)                     # E
+            return self._row(self._each(lambda s: s.finish_moments(STEP_FLAGS))[0], j, t_obs)
         if self.pull:
             # D over peer memory. The 2-double allgather (as in the native
             # step) orders every shard's pull after every shard's CDF tables;

@@ -193,6 +193,43 @@ class CpuShard:
         self.bufs[10][:] = cnt
         return cnt
 
+    # ---------------------------------------------------------- offspring mode
+    def set_mode(self, mode):
+        self.mode = mode
+
+    def offspring(self):
+        """Per-particle offspring counts of this shard's particles from every
+        global slot's keyed uniform and the exact sequential CDF; children per
+        rank (identical on every rank)."""
+        u_all = np.array([O.draws(self.sc.seed, self.j, ng, 3, 1, 1)[0] for ng in range(self.n_glob)])
+        k = np.minimum(np.searchsorted(self.cdf, u_all, side="right"), self.n_glob - 1)
+        owner = k // self.n
+        self.otot = np.bincount(owner, minlength=self.world).astype(np.int64)
+        mine = k[owner == self.rank] - self.n0
+        self.ocnt = np.bincount(mine, minlength=self.n).astype(np.int64)
+        return self.otot.copy()
+
+    def offspring_counts(self):
+        return self.ocnt.astype(np.uint32)
+
+    def offspring_pack(self):
+        from paper_1411_1702_b200.sharded import offspring_matrix
+        P = int(self.otot[:self.rank].sum())
+        anc_local = np.repeat(np.arange(self.n), self.ocnt)  # children in ancestor order
+        send = self.bufs[8].reshape(self.world, self.n, self.W)
+        for kk, a in enumerate(anc_local):
+            p = P + kk
+            dest = p // self.n
+            first = max(P, dest * self.n)
+            row = send[dest, p - first]
+            row[:] = 0.0
+            row[:self.d] = self.states[a]
+            row[self.d:self.d + self.p] = self.params_u[a]
+            row[self.R] = self.llbar[a]
+            row[self.R + 1] = float(self.n0 + a)
+            row[self.R + 2] = float(p - dest * self.n)
+        return offspring_matrix(self.otot, self.world, self.n).astype(np.uint32)
+
     def update(self, n_recv):
         recv = self.bufs[9].reshape(self.n, self.W)[:n_recv]
         slots = recv[:, self.R + 2].astype(np.int64)

@@ -27,11 +27,11 @@ REL_STATE = 1e-10
 REL_TRACE = 1e-8
 
 
-def _sampler(sc: StepConfig, n, likelihood="gaussian", model_consts=None):
+def _sampler(sc: StepConfig, n, likelihood="gaussian", model_consts=None, arithmetic="exact"):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     cfg = PfConfig(particles=n, shrink_a=sc.a, h=sc.h, family=sc.family, order=sc.order, seed=sc.seed,
                    newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter, adaptive=sc.adaptive,
-                   rtol=sc.rtol)
+                   rtol=sc.rtol, arithmetic=arithmetic)
     return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood),
                       model_consts=model_consts)
 
@@ -230,14 +230,18 @@ LOCKSTEP = [
 ]
 
 
-@pytest.mark.parametrize("name,kw,n,steps,m", LOCKSTEP, ids=[c[0] for c in LOCKSTEP])
+LOCKSTEP_FAST = [("fast_" + c[0], *c[1:]) for c in LOCKSTEP if c[0] in ("lv_am2_m1", "lv_bdf3_m4", "lv_am2_n5003")]
+
+
+@pytest.mark.parametrize("name,kw,n,steps,m", LOCKSTEP + LOCKSTEP_FAST, ids=[c[0] for c in LOCKSTEP + LOCKSTEP_FAST])
 def test_lockstep_lotka_volterra(name, kw, n, steps, m):
-    """Both sides start every step from the same (oracle) ensemble."""
+    """Both sides start every step from the same (oracle) ensemble. The
+    fast_* cases run the FMA variant (PFSMC_GPU_ARITH_FAST) at the same bars."""
     from paper_1411_1702_b200 import problems
     sc = StepConfig(**kw, obs_idx=(0, 1), sigma=0.05)
     prob = problems.lotka_volterra(particles=n, T=steps, seed=kw["seed"])
     ens = O.init_uniform("lv", n, kw["seed"], **prob.prior)
-    gpu = _sampler(sc, n)
+    gpu = _sampler(sc, n, arithmetic="fast" if name.startswith("fast_") else "exact")
     tp = 0.0
     for j in range(1, steps + 1):
         gpu.set_ensemble(_to_gpu_ens(ens))

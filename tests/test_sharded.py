@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from cpu_shard import CpuShard
+from oracle_ctypes import Ensemble as OEns
 from oracle_ctypes import Oracle, StepConfig
 
 O = Oracle()
@@ -42,9 +43,9 @@ def _oracle_run():
     return traces, ancs, ens
 
 
-def _sharded_run(shards, comm):
+def _sharded_run(shards, comm, mode="exact"):
     from paper_1411_1702_b200.sharded import ShardedFilter
-    f = ShardedFilter(shards, comm)
+    f = ShardedFilter(shards, comm, mode=mode)
     f.initialize_uniform(**PRIOR)
     traces, ancs = [], []
     tp = 0.0
@@ -109,3 +110,95 @@ def test_gloo_world2_matches_oracle():
     # rank r holds slots [r*N/2, (r+1)*N/2)
     states = np.concatenate([p["states"] for p in parts])
     np.testing.assert_allclose(states, re.states, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- offspring mode
+def _offspring_run(shards, comm, check_single=True):
+    """Offspring-allocation mode: before every step the global ensemble is
+    also stepped by the single-handle oracle, whose ancestors give the
+    multinomial offspring counts the sharded filter must reproduce bitwise."""
+    from paper_1411_1702_b200.sharded import ShardedFilter
+    f = ShardedFilter(shards, comm, mode="offspring")
+    f.initialize_uniform(**PRIOR)
+    sc = _sc()
+    out = []
+    tp = 0.0
+    for j, y in enumerate(_ys(), 1):
+        want, anc_single = None, None
+        if check_single:  # needs the whole ensemble in this process
+            g = f.get_ensemble()
+            ens = OEns(g.states.copy(), g.params_u.copy(), g.logw.copy(), g.mean_u.copy(), g.cov_u.copy())
+            _tr, dg = O.pf_step(sc, ens, y, j, tp, tp + 0.1, diag=True)
+            want, anc_single = np.bincount(dg["ancestors"], minlength=N_GLOB), dg["ancestors"]
+        row = f.pf_step(y, j, tp, tp + 0.1, 0.1)
+        got = np.concatenate([s.offspring_counts() for s in f.shards]).astype(np.int64)
+        anc = f.ancestors()
+        out.append((want, got, anc, anc_single, np.concatenate([row.theta_mean, row.theta_var,
+                                                                 row.state_mean, [row.ess]])))
+        tp += 0.1
+    return out, f.get_ensemble()
+
+
+def test_local_comm_offspring_counts_match_single_handle():
+    """Offspring counts bitwise the single handle's multinomial counts (same
+    keyed uniforms, same exact CDF); the children are laid out in ancestor
+    order (rank by rank), so the slot ancestors are the sorted single-handle
+    ancestors of the shards that hold them."""
+    from paper_1411_1702_b200.sharded import LocalComm
+    shards = [CpuShard(_sc(), N_GLOB, r, 2) for r in range(2)]
+    out, ens = _offspring_run(shards, LocalComm(2))
+    for j, (want, got, anc, anc_single, tr) in enumerate(out, 1):
+        assert np.array_equal(got, want), f"step {j}: offspring counts differ"
+        # the children in ancestor order: the slot ancestors are the sorted
+        # single-handle ancestors
+        assert np.array_equal(anc, np.sort(anc_single)), j
+        assert np.isfinite(tr).all()
+    assert np.isfinite(ens.states).all()
+
+
+def test_offspring_matrix_moves_only_the_imbalance():
+    from paper_1411_1702_b200.sharded import offspring_matrix
+    n = 10
+    # balanced: nothing crosses
+    assert np.array_equal(offspring_matrix([10, 10, 10], 3, n), np.diag([10, 10, 10]))
+    # rank 0 has 17 children: 7 spill onto rank 1, whose 5 children spill 2 onto rank 2
+    S = offspring_matrix([17, 5, 8], 3, n)
+    assert np.array_equal(S, np.array([[10, 7, 0], [0, 3, 2], [0, 0, 8]]))
+    assert S.sum() == 30 and np.array_equal(S.sum(0), [10, 10, 10])
+    # degenerate weights: one rank makes every child
+    S = offspring_matrix([0, 30, 0], 3, n)
+    assert np.array_equal(S, np.array([[0, 0, 0], [10, 10, 10], [0, 0, 0]]))
+
+
+def _offspring_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1411_1702_b200.sharded import TorchComm
+        shard = CpuShard(_sc(), N_GLOB, rank, world)
+        out, ens = _offspring_run([shard], TorchComm(), check_single=False)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), got=np.array([o[1] for o in out]),
+                 anc=np.array([o[2] for o in out]),
+                 tr=np.array([o[4] for o in out]), states=ens.states)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_offspring_mode():
+    """Offspring mode across two gloo processes: each rank's counts are the
+    single handle's for its particles; the trace and the states equal the
+    one-process (LocalComm) offspring run."""
+    import torch.multiprocessing as mp
+    from paper_1411_1702_b200.sharded import LocalComm
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_offspring_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        parts = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(2)]
+    local, lens = _offspring_run([CpuShard(_sc(), N_GLOB, r, 2) for r in range(2)], LocalComm(2))
+    half = N_GLOB // 2
+    for r, p in enumerate(parts):
+        for j in range(STEPS):
+            assert np.array_equal(p["got"][j], local[j][0][r * half:(r + 1) * half]), (r, j)
+            assert np.array_equal(p["anc"][j], local[j][2][r * half:(r + 1) * half]), (r, j)
+            np.testing.assert_allclose(p["tr"][j], local[j][4], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(np.concatenate([p["states"] for p in parts]), lens.states, rtol=1e-13)

@@ -37,10 +37,10 @@ REL_TRACE = 1e-8
 EPS = 2.0 ** -53
 
 
-def _sampler(sc: StepConfig, n, likelihood="gaussian"):
+def _sampler(sc: StepConfig, n, likelihood="gaussian", arithmetic="exact"):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     cfg = PfConfig(particles=n, shrink_a=sc.a, h=sc.h, family=sc.family, order=sc.order, seed=sc.seed,
-                   newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter)
+                   newton_tol=sc.newton_tol, newton_max_iter=sc.newton_max_iter, arithmetic=arithmetic)
     return GpuSampler(sc.model, cfg, ObservationModel(list(sc.obs_idx), sc.sigma, likelihood))
 
 
@@ -83,7 +83,21 @@ class Tally:
         self.steps = 0
 
 
-def compare_step(gpu, nxt, trace_ref, anc_ref, g_ref, llbar_ref, row, seed, j, tally: Tally):
+def _relrows(a, b):
+    """Normwise relative error per particle: max_k |a - b| / max_k |b| over the
+    state vector (the relative error of the particle's state)."""
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.max(np.abs(a - b), axis=1) / np.maximum(np.max(np.abs(b), axis=1), 1e-300)))
+
+
+def compare_step(gpu, nxt, trace_ref, anc_ref, g_ref, llbar_ref, row, seed, j, tally: Tally, state_rows=False):
+    """state_rows: states compared as vectors per particle (the FAST
+    arithmetic: in Robertson's stiff end x2 ~ 1e-6 next to x1, x3 ~ 0.5, and
+    a 1-ulp change in the FMA-contracted Newton update is ~1e-10 of the x2
+    column alone, 1e-16 of the state); the exact build is held to the
+    per-component bar."""
     anc_g, llb_g, _ = gpu.step_diagnostics()
     got = gpu.get_ensemble()
     anc_g = anc_g.astype(np.int64)
@@ -99,7 +113,7 @@ def compare_step(gpu, nxt, trace_ref, anc_ref, g_ref, llbar_ref, row, seed, j, t
             keep[mism] = False
     if llbar_ref is not None:
         assert _relmax(llb_g, llbar_ref) < REL_STATE, j
-    assert _relmax(got.states[keep], nxt.states[keep]) < REL_STATE, j
+    assert (_relrows if state_rows else _relmax)(got.states[keep], nxt.states[keep]) < REL_STATE, j
     assert _relmax(got.params_u[keep], nxt.params_u[keep]) < REL_STATE, j
     if keep.all():
         assert _relmax(np.exp(got.logw), np.exp(nxt.logw)) < REL_STATE, j
@@ -117,7 +131,7 @@ def compare_step(gpu, nxt, trace_ref, anc_ref, g_ref, llbar_ref, row, seed, j, t
         assert _relmax(tr[None, 2 * p:], trace_ref[None, 2 * p:]) < REL_TRACE, j
 
 
-def _run_lockstep(gpu, ref_step, ens, ys, times, seed, steps, substeps, tally, t0=0.0):
+def _run_lockstep(gpu, ref_step, ens, ys, times, seed, steps, substeps, tally, t0=0.0, state_rows=False):
     """Lock-step driver: both sides start every step from the reference-side
     ensemble. Returns the step at which both raised (same message), or None."""
     from paper_1411_1702_b200.sampler import NumericalError
@@ -135,19 +149,20 @@ def _run_lockstep(gpu, ref_step, ens, ys, times, seed, steps, substeps, tally, t
         try:
             trace_r, anc_r, g_r, llb_r = ref_step(nxt, ys[j - 1], j, tp, t1, h)
         except OracleError as e:
-            assert e.args[0] == 3, e  # NUMERICAL
-            ref_err = e.args[1]
+            assert e.code == 3, e  # NUMERICAL
+            ref_err = str(e).split("] ", 1)[1]
         assert (gpu_err is None) == (ref_err is None), (j, gpu_err, ref_err)
         if gpu_err is not None:
             assert gpu_err == ref_err, (j, gpu_err, ref_err)
             return j
-        compare_step(gpu, nxt, trace_r, anc_r, g_r, llb_r, row, seed, j, tally)
+        compare_step(gpu, nxt, trace_r, anc_r, g_r, llb_r, row, seed, j, tally, state_rows)
         ens = nxt
         tp = t1
     return None
 
 
-def test_robertson_lognormal_full_grid_lockstep():
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_robertson_lognormal_full_grid_lockstep(arith):
     """BASELINE config 3 with its lognormal likelihood, all 400 log-spaced
     intervals, N = 2^16, against the C oracle. The stiff regime (t >~ 1,
     where Newton <= 4 binds: ~3 iterations per solve, most predictions die)
@@ -160,7 +175,7 @@ def test_robertson_lognormal_full_grid_lockstep():
                     newton_max_iter=4, likelihood="lognormal")
     pr = prob.prior
     ens = O.init_gaussian("robertson", n, seed, pr["th_mu"], pr["th_sigma"], pr["x_mean"], pr["x_std"], [0, 0, 0])
-    gpu = _sampler(sc, n, likelihood="lognormal")
+    gpu = _sampler(sc, n, likelihood="lognormal", arithmetic=arith)
     iters = []
 
     def ref_step(e, y, j, tp, t1, h):
@@ -170,7 +185,8 @@ def test_robertson_lognormal_full_grid_lockstep():
         return tr, dg["ancestors"], dg["g"], dg["loglik_bar"]
 
     tally = Tally()
-    died = _run_lockstep(gpu, ref_step, ens, prob.ys, prob.times, seed, 400, 2, tally)
+    died = _run_lockstep(gpu, ref_step, ens, prob.ys, prob.times, seed, 400, 2, tally,
+                         state_rows=arith == "fast")
     gpu.close()
     # the run reaches the stiff end of the grid (t ~ 1e2 .. 1e3) before dying
     assert died is None or died > 380, died
@@ -214,7 +230,8 @@ def test_robertson_gaussian_full_grid_vs_live_reference():
     assert tally.flips <= 8, vars(tally)
 
 
-def test_chain_lockstep_2e20_twenty_steps():
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_chain_lockstep_2e20_twenty_steps(arith):
     """BASELINE config 4's chain (BDF3, m = 3, uniform prior [0.5, 2] x truth,
     x(0) = 0) at N = 2^20 for 20 lock-step observations against the C oracle
     (threaded over the host cores; the same per-particle arithmetic)."""
@@ -224,7 +241,7 @@ def test_chain_lockstep_2e20_twenty_steps():
     sc = StepConfig(model="chain", family="bdf", order=3, h=0.1 / 3, a=0.98, seed=seed, obs_idx=(0, 3, 7),
                     sigma=0.01)
     ens = O.init_uniform("chain", n, seed, **prob.prior)
-    gpu = _sampler(sc, n)
+    gpu = _sampler(sc, n, arithmetic=arith)
 
     def ref_step(e, y, j, tp, t1, h):
         sc.h = h
