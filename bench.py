@@ -226,6 +226,43 @@ def cpu_reference(n, steps, seconds_cap, workers, prob, use_ref=True, warmup=0):
                          else "C restatement, 1 thread")}
 
 
+def _lv_config(world, n):
+    """The headline workload's config dict, identical in both arms."""
+    return {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles_per_gpu": n,
+            "global_particles": n * world, "d": D, "p": P, "h": 0.1, "shrink_a": 0.98,
+            "integrator": "am2 (reference semantics: m=1 => AM1 corrector, AB1 predictor)",
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_sequential(prob, n=1 << 16):
+    """The reference pf_step with Backend::sequential() (exec.hpp:47-62) on one
+    observation at n particles (its throughput is flat in N)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_ctypes import REF_SO, Oracle, Reference, StepConfig
+        if not os.path.exists(REF_SO):
+            return None
+        sc = StepConfig(model="lv", family=prob.cfg.family, order=prob.cfg.order, h=0.1, a=0.98,
+                        seed=prob.cfg.seed, obs_idx=(0, 1), sigma=0.05)
+        ens = Oracle().init_uniform("lv", n, prob.cfg.seed, **prob.prior)
+        secs = Reference().time_steps(sc, ens, prob.ys[0:2], list(prob.times[0:2]), 1, 0.0, 0)
+        return {"value": 2 * n / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"LV N={n}, observations 1..2, reference pf_step Backend::sequential()"}
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)[:200]}
+
+
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return 0
@@ -237,7 +274,7 @@ def run_reference_arm(args, world, rank):
     # Exactly K timed steps; beyond 32 of them each step is a smaller sample of the
     # ensemble (the reference's throughput is flat in N), so the run
     # stays within a few minutes.
-    w = min(args.warmup, 3)
+    w = max(args.warmup, 3)  # the same W as the GPU arm (bench.py forces W >= 3 there too)
     n_ref = N_PER_GPU
     while args.steps * n_ref > 32 * N_PER_GPU and n_ref > (1 << 14):
         n_ref //= 2
@@ -246,9 +283,9 @@ def run_reference_arm(args, world, rank):
             "warmup": w, "ms_per_step": 1e3 * cb["seconds"] / cb["steps"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded RK4 LV)",
             "impl": "reference",
-            "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles": N_PER_GPU,
-                       "particles_per_timed_step": n_ref, "h": 0.1, "shrink_a": 0.98, "integrator": "am2 (m=1)"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": _lv_config(args.gpus, N_PER_GPU), "particles_per_timed_step": n_ref,
+            "cpu_baseline": {**{k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -596,11 +633,24 @@ def run_sharded(args, world, rank, local):
     from paper_1411_1702_b200 import problems
     from paper_1411_1702_b200.sharded import GpuShard, ShardedFilter, TorchComm
 
-    n_local = args.particles
-    prob = problems.lotka_volterra(particles=n_local * world, T=T_OBS, seed=1)
-    shard = GpuShard("lv", _cfg(prob), prob.obs, rank, world, device=local)
-    f = ShardedFilter([shard], TorchComm())
-    f.initialize_uniform(**prob.prior)
+    cfgno = args.config
+    if cfgno == 2:    # LV, N = 2^20 per GPU (weak scaling)
+        n_local = args.particles
+        prob = problems.lotka_volterra(particles=n_local * world, T=T_OBS, seed=1)
+        model, scaling, j_start = "lv", "weak", 0
+    elif cfgno == 3:  # Robertson, N = 2^22 in total (strong), timed in the stiff part of the grid
+        n_local = (1 << 22) // world
+        prob = problems.robertson(particles=n_local * world, T=400, seed=1)
+        model, scaling, j_start = "robertson", "strong", C3_WINDOWS[1] - 1 - args.warmup
+    elif cfgno == 4:  # chain, N = 2^24 in total (strong)
+        n_local = (1 << 24) // world
+        prob = problems.chain8(particles=n_local * world, T=args.warmup + args.steps + 1, seed=1)
+        model, scaling, j_start = "chain", "strong", 0
+    else:
+        raise SystemExit("--config must be 2, 3 or 4 for the sharded filter (config 5: --config 5 single GPU)")
+    shard = GpuShard(model, _cfg(prob), prob.obs, rank, world, device=local)
+    f = ShardedFilter([shard], TorchComm(), mode=args.shard_mode)
+    prob.init(f)
     migration = "python-orchestrated, NCCL send/recv"
     if not args.python_sharded:
         shard.attach_nccl()   # the native step: one C-ABI call per observation
@@ -611,11 +661,15 @@ def run_sharded(args, world, rank, local):
                     migration = "native step, pull over NVLink peer memory"
             except Exception:
                 pass
-    stream = shard.stream()
     j, tp = 0, 0.0
+    while j < j_start:  # untimed advance along the observation grid
+        j += 1
+        f.pf_step(prob.ys[j - 1], j, tp, prob.times[j - 1], prob.h_for(tp, prob.times[j - 1]))
+        tp = prob.times[j - 1]
+    stream = shard.stream()
     for _ in range(args.warmup):
         j += 1
-        f.pf_step(prob.ys[j - 1], j, tp, prob.times[j - 1], 0.1)
+        f.pf_step(prob.ys[j - 1], j, tp, prob.times[j - 1], prob.h_for(tp, prob.times[j - 1]))
         tp = prob.times[j - 1]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     dist.barrier()
@@ -627,7 +681,7 @@ def run_sharded(args, world, rank, local):
             j += 1
             with torch.cuda.stream(stream):
                 ev[k][0].record(stream)
-            row = f.pf_step(prob.ys[j - 1], j, tp, prob.times[j - 1], 0.1)
+            row = f.pf_step(prob.ys[j - 1], j, tp, prob.times[j - 1], prob.h_for(tp, prob.times[j - 1]))
             with torch.cuda.stream(stream):
                 ev[k][1].record(stream)
             tp = prob.times[j - 1]
@@ -640,22 +694,33 @@ def run_sharded(args, world, rank, local):
     value = n_local * world * args.steps / (total_ms / 1e3)
     peaks, peak_kind = _peaks()
     hbm = float(peaks["hbm_gbs"])
-    step_gbs = STEP_BYTES * n_local / (total_ms / args.steps / 1e3) / 1e9
+    d_, p_ = shard.d, shard.p
+    step_bytes = 24 * (d_ + p_ + 1) + 56  # B = 24F + 56
+    step_gbs = step_bytes * n_local / (total_ms / args.steps / 1e3) / 1e9
+    names = {2: "BASELINE config 2: Lotka-Volterra PF-SMC", 3: "BASELINE config 3: Robertson PF-SMC (lognormal)",
+             4: "BASELINE config 4: 8-compartment chain PF-SMC"}
+    mode_txt = ("exact-mode ancestor migration (bitwise the single filter; (G-1)/G of the slots fetch a remote "
+                "ancestor)" if args.shard_mode == "exact" else
+                "offspring-allocation migration (per-particle offspring counts bitwise the single filter's; "
+                "children built on the ancestor's GPU; only the load imbalance crosses GPUs)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded RK4 Lotka-Volterra observations, uniform priors)",
-            "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles_per_gpu": n_local,
-                       "global_particles": n_local * world, "h": 0.1, "shrink_a": 0.98,
-                       "integrator": "am2 (m=1)", "l2": "flushed between timed steps",
-                       "parallelism": f"sharded x{world}: one global filter, NCCL allgathers + exact-mode "
-                                      f"ancestor migration ({migration})"},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded {prob.name} observations)",
+            "config": {"workload": names[cfgno], "particles_per_gpu": n_local,
+                       "global_particles": n_local * world, "first_timed_observation": j - args.steps + 1,
+                       "shrink_a": prob.cfg.shrink_a, "arithmetic": ARITH,
+                       "integrator": f"{prob.cfg.family}{prob.cfg.order} (m={prob.substeps})",
+                       "l2": "flushed between timed steps", "shard_mode": args.shard_mode,
+                       "parallelism": f"sharded x{world}: one global filter, NCCL allgathers + {mode_txt} "
+                                      f"({migration})"},
             "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": step_gbs, "peak": hbm, "unit": "GB/s",
-                         "frac": step_gbs / hbm, "traffic": None, "bytes_per_particle": STEP_BYTES,
+                         "frac": step_gbs / hbm, "traffic": None, "bytes_per_particle": step_bytes,
                          "peak_source": peak_kind},
             "gpu_launches": 12 * args.steps,
-            "e2e": {"value": n_local * world * args.steps / t_wall, "unit": UNIT, "h2d_bytes_per_step": 16,
-                    "d2h_bytes_per_step": 8 * (2 * P + D + 1), "path": "ShardedFilter.pf_step (host y in, trace out)"},
+            "e2e": {"value": n_local * world * args.steps / t_wall, "unit": UNIT,
+                    "h2d_bytes_per_step": shard.transfer_bytes()[0], "d2h_bytes_per_step": shard.transfer_bytes()[1],
+                    "path": "ShardedFilter.pf_step (host y in, trace out)"},
             "clocks": clk.summary(),
             "final_trace": {"theta_mean": list(map(float, row.theta_mean)), "ess": float(row.ess)}}
     if rank == 0:
@@ -682,6 +747,11 @@ def main():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sharded path (NCCL collectives + migration) even at N = 1 (a check of that path)")
     ap.add_argument("--no-workloads", action="store_true", help="skip the configs 3-5 extra lines")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE config for N > 1 (sharded) runs; the single-GPU line is config 2 with 3-5 as "
+                         "workload extras")
+    ap.add_argument("--shard-mode", default="offspring", choices=["exact", "offspring"],
+                    help="sharded migration mode (pfsmc_gpu_shard_set_mode)")
     ap.add_argument("--arithmetic", default="exact", choices=["exact", "fast"],
                     help="device arithmetic: exact (reference op order, bitwise Psi) or fast (FMA; tolerance parity)")
     args = ap.parse_args()
@@ -777,8 +847,10 @@ def main():
         t = torch.tensor([e2e_s], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": n * world * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * 2,
-           "d2h_bytes_per_step": 8 * (2 * P + D + 1), "steps": e2e_steps,
+    h2d, d2h = gpu.transfer_bytes()
+    e2e = {"value": n * world * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+           "bytes_note": "StepParams up (y, times, constants), DevState down (trace row, error word, moments)",
            "path": "pfsmc_gpu_step (C ABI drop-in for filter::pf_step), blocking"}
 
     peaks, peak_kind = _peaks()
@@ -800,12 +872,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RK4 Lotka-Volterra observations, uniform priors)",
-            "config": {"workload": "BASELINE config 2: Lotka-Volterra PF-SMC", "particles_per_gpu": n,
-                       "global_particles": n * world, "d": D, "p": P, "h": 0.1, "shrink_a": 0.98,
-                       "integrator": "am2 (reference semantics: m=1 => AM1 corrector, AB1 predictor)",
-                       "arithmetic": ARITH,
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": _lv_config(world, n), "arithmetic": ARITH,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind,
@@ -834,7 +901,8 @@ def main():
             line["workloads"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(N_PER_GPU, 20, 15.0, len(os.sched_getaffinity(0)), prob)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {**{k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                                "cpu_model": _cpu_model(), "sequential": cpu_sequential(prob)}
     if rank == 0:
         print(json.dumps(line))
     gpu.close()

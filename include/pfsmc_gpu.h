@@ -146,6 +146,9 @@ pfsmc_gpu_status pfsmc_gpu_upload_observations(pfsmc_gpu_sampler* s, const doubl
                                                double h);
 pfsmc_gpu_status pfsmc_gpu_step_resident(pfsmc_gpu_sampler* s, uint64_t j);
 pfsmc_gpu_status pfsmc_gpu_synchronize(pfsmc_gpu_sampler* s, double* trace_out);
+/* Host<->device bytes of one blocking pfsmc_gpu_step (step parameters up,
+ * device state incl. the trace row down): the e2e accounting. */
+pfsmc_gpu_status pfsmc_gpu_step_transfer_bytes(pfsmc_gpu_sampler* s, uint64_t* h2d, uint64_t* d2h);
 
 /* filter::run (filter.cpp:396-443) on resident observations: rows (T+1) x
  * (2p + d + 1) of the PosteriorTrace, row 0 from the current ensemble;

@@ -696,6 +696,17 @@ pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, in
   });
 }
 
+// Bytes one blocking pfsmc_gpu_step moves between host and device: the step
+// parameters up (observations, times, constants), the device state down
+// (trace row, error word, moments) and, for block models, the state mean.
+pfsmc_gpu_status pfsmc_gpu_step_transfer_bytes(pfsmc_gpu_sampler* s, uint64_t* h2d, uint64_t* d2h) {
+  return guarded([&] {
+    if (h2d) *h2d = sizeof(StepParams);
+    if (d2h) *d2h = sizeof(DevState) + (s && s->xmean_host ? sizeof(double) * s->d : 0);
+    return PFSMC_GPU_OK;
+  });
+}
+
 pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     if (!s->flush_buf) {

@@ -322,5 +322,12 @@ class GpuSampler:
     def c5_iteration(self, j: int):
         self._check(self.lib.pfsmc_gpu_c5_iteration(self.h, C.c_uint64(j)))
 
+    def transfer_bytes(self):
+        """(H2D, D2H) bytes of one blocking pf_step (pfsmc_gpu_step_transfer_bytes)."""
+        self.lib.pfsmc_gpu_step_transfer_bytes.restype = C.c_int
+        a, b = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.pfsmc_gpu_step_transfer_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def flush_l2(self):
         self._check(self.lib.pfsmc_gpu_flush_l2(self.h))
