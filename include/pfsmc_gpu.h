@@ -55,6 +55,19 @@ enum {
                                      (n-1) x (n-1) grid, d = (n-1)^2, p = 5 (k1, k2 positive;
                                      k3, c1, c2 not), n = model_consts[0], 4 <= n <= 33 */
 };
+/* Caller-defined models: ids >= PFSMC_GPU_MODEL_USER_BASE are served by
+ * plugin libraries built against include/pfsmc_gpu_model.cuh (the device
+ * form of the OdeModel::bind -> ModelEval::{rhs, jacobian} contract,
+ * models.hpp:20-55); loading such a library registers its models. */
+#define PFSMC_GPU_MODEL_USER_BASE 64
+/* Called by a plugin's static initialiser (PFSMC_GPU_REGISTER_MODEL): make_kernels
+ * is the plugin's `std::unique_ptr<KernelSet> (*)(int family, int order)`;
+ * fast = 1 registers the FMA variant (the unit compiled with -DPFSMC_FAST=1). */
+pfsmc_gpu_status pfsmc_gpu_register_model(int id, const char* name, int d, int p, int fast,
+                                          void* make_kernels);
+/* The i-th registered plugin model (i = 0, 1, ...); CONFIG past the end. */
+pfsmc_gpu_status pfsmc_gpu_registered_model(int index, int* id, const char** name, int* d, int* p);
+
 /* lmm::Family (lmm.hpp:12) */
 enum { PFSMC_GPU_AB = 0, PFSMC_GPU_AM = 1, PFSMC_GPU_BDF = 2 };
 /* Observation noise. GAUSSIAN is filter::log_likelihood (filter.cpp:124-141);

@@ -74,6 +74,7 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_plugin(verbose)
     # the C++ drop-in example over include/pfsmc_gpu.hpp (exercised by a GPU test)
     root = os.path.dirname(HERE)
     ex_src = os.path.join(root, "examples", "drop_in_lv.cpp")
@@ -89,6 +90,38 @@ def build(verbose: bool = False) -> str:
     if verbose:
         print(f"[build] {LIB}")
     return LIB
+
+
+PLUGIN_DIR = os.path.join(os.path.dirname(HERE), "examples", "user_model")
+PLUGIN_LIB = os.path.join(PLUGIN_DIR, "libuser_models.so")
+
+
+def build_plugin(verbose: bool = False) -> str:
+    """The example model plugin (include/pfsmc_gpu_model.cuh), exact + fast
+    units, linked against libpfsmc_gpu.so (its static initialisers register
+    the models there)."""
+    src = os.path.join(PLUGIN_DIR, "user_models.cu")
+    if not os.path.exists(src):
+        return ""
+    inc = ["-I", os.path.join(os.path.dirname(HERE), "include")]
+    objs = []
+    for fast in (False, True):
+        obj = os.path.join(BUILD, "user_models" + ("_fast.o" if fast else ".o"))
+        if _stale(obj, src):
+            cmd = [NVCC, *(FAST_FLAGS if fast else FLAGS), *inc, "-c", src, "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"plugin build failed:\n{r.stderr}")
+        objs.append(obj)
+    if not os.path.exists(PLUGIN_LIB) or any(os.path.getmtime(o) > os.path.getmtime(PLUGIN_LIB) for o in objs + [LIB]):
+        cmd = [NVCC, *ARCH, "-shared", "-o", PLUGIN_LIB, *objs, "-L", HERE, "-lpfsmc_gpu",
+               "-Xlinker", "-rpath,$ORIGIN/../../paper_1411_1702_b200"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"plugin link failed:\n{r.stderr}")
+    if verbose:
+        print(f"[build] {PLUGIN_LIB}")
+    return PLUGIN_LIB
 
 
 if __name__ == "__main__":

@@ -46,6 +46,25 @@ __global__ void k_flush(double* buf, long long n) {
 
 thread_local std::string g_last_error;
 
+// ---- caller-defined model registry (include/pfsmc_gpu_model.cuh) ----
+namespace {
+struct UserModel {
+  int id, d, p;
+  std::string name;
+  pfsmc_gpu::KernelFactory exact = nullptr, fast = nullptr;
+};
+std::vector<UserModel>& user_models() {
+  static std::vector<UserModel> v;
+  return v;
+}
+}  // namespace
+
+pfsmc_gpu::KernelFactory pfsmc_gpu::registered_factory(int model, bool fast) {
+  for (const UserModel& m : user_models())
+    if (m.id == model) return fast && m.fast ? m.fast : m.exact;
+  return nullptr;
+}
+
 // interval_step_count (lmm.cpp:350-362)
 int step_count(double t0, double t1, double h) {
   if (!(t1 > t0) || !(h > 0.0)) throw ConfigError("propagate_interval: need t1 > t0 and h > 0");
@@ -197,10 +216,64 @@ void harvest_timing(pfsmc_gpu_sampler* s) {
 // Params come either from the pinned host slot (blocking drop-in step; the
 // previous step has completed, so the slot is free) or from the resident
 // device array (no host involvement).
+// The reference's checks on the Ensemble handed to pf_step that the device
+// path would not repeat (it normalises weights itself and keeps cov_u
+// symmetric by construction): weighted_mean_cov's weight gate in shrink
+// (linalg.cpp:395-409, filter.cpp:107-122) and chol_psd's symmetry check in
+// proliferate (linalg.cpp:474-480, filter.cpp:185-187). Run on the host at
+// injection; the failure is raised by the next step, where the reference
+// raises it.
+void check_injected(pfsmc_gpu_sampler* s, const double* logw, const double* cov_u) {
+  s->pending_code = 0;
+  s->pending_msg.clear();
+  const size_t N = static_cast<size_t>(s->N);
+  double wsum = 0.0, comp = 0.0;  // Kahan sum, as the reference
+  for (size_t i = 0; i < N; ++i) {
+    const double w = std::exp(logw[i]);
+    if (w < 0.0 || !std::isfinite(w)) {
+      s->pending_code = PFSMC_GPU_ERR_CONFIG;
+      s->pending_msg = "weighted_mean_cov: weights must be nonnegative";
+      return;
+    }
+    const double yk = w - comp;
+    const double tk = wsum + yk;
+    comp = (tk - wsum) - yk;
+    wsum = tk;
+  }
+  // a shard holds part of the weights: the gate is the global filter's (the
+  // caller's, ShardedFilter.set_ensemble)
+  if (!s->shard_api && std::abs(wsum - 1.0) > 1e-12) {
+    s->pending_code = PFSMC_GPU_ERR_CONFIG;
+    s->pending_msg = "weighted_mean_cov: weights must sum to 1";
+    return;
+  }
+  const int p = s->p;
+  for (int i = 0; i < p; ++i)
+    for (int j = i + 1; j < p; ++j)
+      if (std::abs(cov_u[i * p + j] - cov_u[j * p + i]) > 1e-12) {
+        s->pending_code = PFSMC_GPU_ERR_INTERNAL;  // std::invalid_argument in the reference
+        s->pending_msg = "chol_psd: matrix must be symmetric";
+        return;
+      }
+}
+
+struct InternalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void raise_pending(pfsmc_gpu_sampler* s) {
+  if (!s->pending_code) return;
+  const int code = s->pending_code;
+  const std::string msg = s->pending_msg;
+  if (code == PFSMC_GPU_ERR_CONFIG) throw ConfigError(msg);
+  throw InternalError(msg);
+}
+
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp) {
   if (s->shard_api)
     throw ConfigError("step: a shard handle runs only the sharded phases (pfsmc_gpu_shard_step / shard_*)");
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  raise_pending(s);
   if (dev_sp) {
     CK(cudaMemcpyAsync(s->sp_dev, dev_sp, sizeof(StepParams), cudaMemcpyDeviceToDevice, s->stream));
   } else {
@@ -218,7 +291,37 @@ void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepPar
 
 extern "C" {
 
-const char* pfsmc_gpu_version(void) { return "pfsmc_gpu 0.1 (sm_100a)"; }
+const char* pfsmc_gpu_version(void) { return "pfsmc_gpu 0.2 (sm_100a)"; }
+
+pfsmc_gpu_status pfsmc_gpu_register_model(int id, const char* name, int d, int p, int fast, void* make) {
+  return guarded([&] {
+    if (id < PFSMC_GPU_MODEL_USER_BASE) throw ConfigError("register_model: ids below PFSMC_GPU_MODEL_USER_BASE are built in");
+    if (!make || d < 1 || p < 1 || d > 8 || p > 8) throw ConfigError("register_model: need a factory, 1 <= d, p <= 8");
+    auto f = reinterpret_cast<pfsmc_gpu::KernelFactory>(make);
+    for (UserModel& m : user_models()) {
+      if (m.id != id) continue;
+      if (m.d != d || m.p != p) throw ConfigError("register_model: id already registered with other dimensions");
+      (fast ? m.fast : m.exact) = f;
+      return PFSMC_GPU_OK;
+    }
+    UserModel m{id, d, p, name ? name : "", nullptr, nullptr};
+    (fast ? m.fast : m.exact) = f;
+    user_models().push_back(m);
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_registered_model(int index, int* id, const char** name, int* d, int* p) {
+  return guarded([&] {
+    if (index < 0 || index >= static_cast<int>(user_models().size())) throw ConfigError("registered_model: no such index");
+    const UserModel& m = user_models()[static_cast<size_t>(index)];
+    if (id) *id = m.id;
+    if (name) *name = m.name.c_str();
+    if (d) *d = m.d;
+    if (p) *p = m.p;
+    return PFSMC_GPU_OK;
+  });
+}
 const char* pfsmc_gpu_last_error(void) { return g_last_error.c_str(); }
 
 static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int world,
@@ -437,6 +540,7 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     CK(cudaMemcpyAsync(tmp_x, states, sizeof(double) * N * d, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(tmp_t, params_u, sizeof(double) * N * p, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->ctx.lw, logw, sizeof(double) * N, cudaMemcpyHostToDevice, s->stream));
+    check_injected(s, logw, cov_u);
     DevState h{};
     CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
@@ -489,6 +593,8 @@ pfsmc_gpu_status pfsmc_gpu_get_ensemble(pfsmc_gpu_sampler* s, double* states, do
 
 static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vector<double>& prm) {
   return guarded([&] {
+    s->pending_code = 0;
+    s->pending_msg.clear();
     double* dprm = s->dalloc<double>(prm.size());
     CK(cudaMemcpyAsync(dprm, prm.data(), sizeof(double) * prm.size(), cudaMemcpyHostToDevice, s->stream));
     DevState h{};

@@ -121,6 +121,11 @@ struct pfsmc_gpu_sampler {
   double kernel_ms[kNumKernels] = {};
   std::vector<cudaEvent_t> pending;  // (kNumKernels+1) per timed step
   bool have_ensemble = false;
+  // An injected ensemble the reference's pf_step would reject (raised by the
+  // next step, as the reference raises inside pf_step): 0 none, else the
+  // pfsmc_gpu_status code, with its message.
+  int pending_code = 0;
+  std::string pending_msg;
   // sharding (pfsmc_gpu_create_shard)
   int rank = 0, world = 1;
   bool shard_api = false;  // created by pfsmc_gpu_create_shard
@@ -196,6 +201,7 @@ pfsmc_gpu_status guarded(F&& f) {
 int step_count(double t0, double t1, double h);
 StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs, double h);
 void check_error(pfsmc_gpu_sampler* s);
+void raise_pending(pfsmc_gpu_sampler* s);
 void clear_error(pfsmc_gpu_sampler* s);
 void ensure_exchange_buffers(pfsmc_gpu_sampler* s);
 void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed);

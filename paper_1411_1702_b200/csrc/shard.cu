@@ -513,6 +513,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
 static void shard_predict_impl(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
                                double h) {
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  raise_pending(s);
   const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
   CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
   *s->sp_host = sp;
@@ -828,6 +829,7 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
 static void shard_pull_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs,
                             double h, double* trace_out) {
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
+  raise_pending(s);
   const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
   CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
   *s->sp_host = sp;

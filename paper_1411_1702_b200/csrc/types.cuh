@@ -174,7 +174,17 @@ std::unique_ptr<KernelSet> make_kernels_advdiff(int fam, int order, int grid_n);
 std::vector<double2> adv_twiddles(int m);    // (cos, sin)(2 pi k / m)
 std::vector<double2> adv_dft_matrix(int m);  // e^{-2 pi i k j / m}, row-major m x m
 
+// Caller-defined models (include/pfsmc_gpu_model.cuh): a plugin library
+// registers, per model id, the factory of its (family, order) kernel sets
+// (exact and optionally fast variant) when it is loaded.
+using KernelFactory = std::unique_ptr<KernelSet> (*)(int fam, int order);
+KernelFactory registered_factory(int model, bool fast);
+
 inline std::unique_ptr<KernelSet> make_kernels(int model, int fam, int order, int grid_n = 0, bool fast = false) {
+  if (model >= PFSMC_GPU_MODEL_USER_BASE) {
+    KernelFactory f = registered_factory(model, fast);
+    return f ? f(fam, order) : nullptr;
+  }
   if (fast) {
     switch (model) {
       case PFSMC_GPU_MODEL_DECAY: return make_kernels_decay_fast(fam, order);

@@ -114,6 +114,26 @@ def load_library(path: str = LIB_PATH):
     return _lib
 
 
+def load_model_plugin(path: str) -> dict:
+    """Loads a caller-defined model plugin (include/pfsmc_gpu_model.cuh;
+    examples/user_model/) and makes its models usable by name. Returns
+    {name: (id, d, p)} of every registered plugin model."""
+    lib = load_library()
+    C.CDLL(path, mode=getattr(os, "RTLD_GLOBAL", 0x100))  # static initialisers register the models
+    lib.pfsmc_gpu_registered_model.restype = C.c_int
+    out, i = {}, 0
+    while True:
+        mid, d, p, name = C.c_int(), C.c_int(), C.c_int(), C.c_char_p()
+        if lib.pfsmc_gpu_registered_model(i, C.byref(mid), C.byref(name), C.byref(d), C.byref(p)) != 0:
+            break
+        nm = name.value.decode()
+        MODELS[nm] = mid.value
+        MODEL_DIMS[mid.value] = (d.value, p.value)
+        out[nm] = (mid.value, d.value, p.value)
+        i += 1
+    return out
+
+
 def _ptr(a, t=_dp):
     return None if a is None else a.ctypes.data_as(t)
 

@@ -1,7 +1,9 @@
 """Key per-kernel metrics from an ncu report: duration, DRAM bytes,
 achieved occupancy, issue activity, instruction count, FP64 pipe.
 
-  python profiles/ncu_summary.py <report.ncu-rep>
+  python profiles/ncu_summary.py <report.ncu-rep | raw page .csv>
+(a .csv is the output of `ncu -i report --page raw --csv`, exported on the
+GPU box so the large report need not travel)
 """
 import csv
 import io
@@ -21,9 +23,14 @@ KEYS = [("gpu__time_duration.sum", "dur_us", 1e-3),
 
 
 def main():
-    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if sys.argv[1].endswith(".csv"):
+        out = open(sys.argv[1]).read()
+    else:
+        out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    while rows and "Kernel Name" not in rows[0]:
+        rows = rows[1:]
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
     print(f"{'kernel':44s} " + " ".join(f"{k[1]:>11s}" for k in KEYS))
@@ -37,8 +44,8 @@ def main():
                     x = float(v)
                     if name.startswith("dram__bytes"):
                         x *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-                    if name == "gpu__time_duration.sum":
-                        x *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(u, 1)
+                    if name == "gpu__time_duration.sum":  # -> ns, then dur_us = ns * 1e-3
+                        x *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(u, 1)
                     vals.append(f"{x * scale:11.2f}")
                 except ValueError:
                     vals.append(f"{v:>11s}")

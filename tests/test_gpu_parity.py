@@ -795,3 +795,63 @@ def test_c5_resample_iteration_matches_oracle(n, sigmas):
         np.testing.assert_allclose(e.mean_u, mean, rtol=1e-10, atol=1e-13)
         np.testing.assert_allclose(e.cov_u, cov, rtol=1e-8, atol=1e-13)
         s.close()
+
+
+# ---------------------------------------------------------------- error paths of chol_psd / weights
+def _err_sampler_and_ens(n=4096, seed=3):
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, a=0.98, seed=seed, obs_idx=(0, 1), sigma=0.05)
+    ens = O.init_uniform("lv", n, seed, [0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
+    return sc, ens, _sampler(sc, n)
+
+
+def test_chol_jitter_rung_above_zero_matches_oracle():
+    """cov_u slightly indefinite: chol_psd's ladder (linalg.cpp:486-498)
+    fails the first rungs and succeeds with a positive jitter (1e-6 tr/p
+    here); the proliferation uses that jittered factor on both sides."""
+    sc, ens, gpu = _err_sampler_and_ens()
+    c = 1e-2
+    ens.cov_u = np.array([[c, c * (1 + 1e-7)], [c * (1 + 1e-7), c]])
+    L, jit = O.chol_psd(ens.cov_u)
+    assert any(jit == r * c for r in (1e-12, 1e-10, 1e-8, 1e-6, 1e-4)) and jit > 0  # a rung above 0
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    row = gpu.pf_step([1.1, 0.9], 1, 0.0, 0.1)
+    trace_o, dg = O.pf_step(sc, ens, [1.1, 0.9], 1, 0.0, 0.1, diag=True)
+    _compare_step(gpu, ens, trace_o, dg, row)
+    gpu.close()
+
+
+@pytest.mark.parametrize("case", ["chol_failure", "weights_sum", "asymmetric_cov"])
+def test_injected_ensemble_errors_match_reference(case):
+    """An ensemble the reference's pf_step rejects: a covariance no rung of
+    the jitter ladder can factor (NUMERICAL "chol_psd: degenerate covariance",
+    linalg.cpp:499), weights that do not sum to 1 (CONFIG, the Kahan gate of
+    weighted_mean_cov, linalg.cpp:395-409) and an asymmetric covariance
+    (chol_psd's symmetry check, std::invalid_argument -> INTERNAL,
+    linalg.cpp:474-480). Same status family and message on the GPU as in the
+    C oracle and (when built) the live reference, at the same step."""
+    from oracle_ctypes import REF_SO, OracleError, Reference
+    from paper_1411_1702_b200.sampler import ConfigError, NumericalError, PfsmcError
+    sc, ens, gpu = _err_sampler_and_ens()
+    if case == "chol_failure":
+        ens.cov_u = np.array([[1.0, 2.0], [2.0, 1.0]])
+        want_cls, code, msg = NumericalError, 3, "chol_psd: degenerate covariance"
+    elif case == "weights_sum":
+        ens.logw = ens.logw + 1e-9
+        want_cls, code, msg = ConfigError, 2, "weighted_mean_cov: weights must sum to 1"
+    else:
+        ens.cov_u = ens.cov_u.copy()
+        ens.cov_u[0, 1] += 1e-9
+        want_cls, code, msg = PfsmcError, 1, "chol_psd: matrix must be symmetric"
+    gpu.set_ensemble(_to_gpu_ens(ens))
+    with pytest.raises(want_cls) as e:
+        gpu.pf_step([1.1, 0.9], 1, 0.0, 0.1)
+    assert msg in str(e.value)
+    assert type(e.value) is want_cls or want_cls is PfsmcError
+    checkers = [O] + ([Reference()] if os.path.exists(REF_SO) else [])
+    for chk in checkers:
+        with pytest.raises(OracleError) as eo:
+            chk.pf_step(sc, ens.copy(), [1.1, 0.9], 1, 0.0, 0.1)
+        assert msg in str(eo.value), (chk, eo.value)
+        if chk is not O:
+            assert eo.value.code == code, eo.value
+    gpu.close()
