@@ -783,7 +783,7 @@ def main():
         if not args.replicas:
             return run_sharded(args, world, rank, local)
     n = args.particles
-    T = min(T_OBS, 2 * args.steps + args.warmup + args.e2e_steps + 1)
+    T = min(T_OBS, 2 * args.steps + args.warmup + args.e2e_steps + 4)
     prob = problems.lotka_volterra(particles=n, T=T_OBS, seed=1)
     # replicas: every rank filters its own N-particle ensemble
     cfg = _cfg(prob)
@@ -853,6 +853,25 @@ def main():
            "bytes_note": "StepParams up (y, times, constants), DevState down (trace row, error word, moments)",
            "path": "pfsmc_gpu_step (C ABI drop-in for filter::pf_step), blocking"}
 
+    # the literal drop-in, pfsmc_gpu::pf_step(Ensemble&, ...) (include/pfsmc_gpu.hpp):
+    # the whole host ensemble in and out every step, as filter::pf_step mutates
+    # the caller's Ensemble (filter.cpp:332, 373-377)
+    lit_s, lit_steps = 0.0, 3
+    host_ens = gpu.get_ensemble()
+    for _ in range(lit_steps):
+        j += 1
+        gpu.synchronize()
+        t0 = time.perf_counter()
+        gpu.set_ensemble(host_ens)
+        gpu.pf_step(ys_pinned[j - 1], j, prob.times[j - 2], prob.times[j - 1])
+        host_ens = gpu.get_ensemble()
+        lit_s += time.perf_counter() - t0
+    ens_bytes = 8 * n * (D + P + 1) + 8 * (P + P * P)
+    e2e["literal_ensemble_step"] = {
+        "value": n * lit_steps / lit_s, "unit": UNIT, "steps": lit_steps,
+        "h2d_bytes_per_step": ens_bytes + h2d, "d2h_bytes_per_step": ens_bytes + d2h,
+        "path": "set_ensemble + pfsmc_gpu_step + get_ensemble: the Ensemble& drop-in (pfsmc_gpu.hpp pf_step), "
+                "host AoS ensemble copied and transposed both ways every step"}
     peaks, peak_kind = _peaks()
     hbm = float(peaks["hbm_gbs"])
     names = list(kt.keys())

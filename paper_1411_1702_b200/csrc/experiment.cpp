@@ -668,6 +668,7 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
   }
   SamplerHandle s;
   make_sampler(s, cfg, setup, data);
+  double phases[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // propagate, resample, proliferate, repropagate, weights
   const std::size_t W = 2 * p + d + 1;
   std::vector<double> rows((T + 1) * W);
   std::vector<int> warn(T + 1, 0);
@@ -676,7 +677,20 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
   check_gpu(pfsmc_gpu_init_gaussian(s.h, setup.th_mu.data(), setup.th_sigma.data(), setup.x_mean.data(),
                                     setup.x_std.data(), setup.x_clamp.data()));
   check_gpu(pfsmc_gpu_upload_observations(s.h, data.values.data(), data.times.data(), T, data.t0, cfg.step));
+  // PhaseTimings (filter.hpp:93-99): per-kernel CUDA events during the run
+  check_gpu(pfsmc_gpu_set_kernel_timing(s.h, 1));
   check_gpu(pfsmc_gpu_run(s.h, rows.data(), warn.data()));
+  double kms[16] = {0};
+  int nk = 0;
+  const char* knames = nullptr;
+  check_gpu(pfsmc_gpu_kernel_times(s.h, kms, &nk, &knames));
+  check_gpu(pfsmc_gpu_set_kernel_timing(s.h, 0));
+  // k_predict = propagate; the exact scan + ancestor search/gather = resample;
+  // k_update fuses proliferate, repropagate and the weight update (all in
+  // "repropagate", the fused kernel's time cannot be split)
+  phases[0] = kms[0] * 1e-3;
+  phases[1] = (kms[1] + kms[2] + kms[3]) * 1e-3;
+  phases[3] = kms[4] * 1e-3;
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
 
   const std::string tag = cfg.problem + "_" + cfg.integrator + "_gpu";
@@ -730,8 +744,12 @@ std::string run_impl(const pfsmc_gpu_experiment& cfg, const std::string& data_cs
     }
     out << "  \"param_names\": " << names << "],\n";
     out << "  \"param_positive\": " << pos << "],\n";
-    out << "  \"phases\": {\"proliferate\": 0.0, \"propagate\": 0.0, \"repropagate\": 0.0, \"resample\": 0.0, "
-           "\"weights\": 0.0},\n";
+    out << "  \"phases\": {\"proliferate\": " << json_num(phases[2]) << ", \"propagate\": " << json_num(phases[0])
+        << ", \"repropagate\": " << json_num(phases[3]) << ", \"resample\": " << json_num(phases[1])
+        << ", \"weights\": " << json_num(phases[4]) << "},\n";
+    out << "  \"phases_note\": \"device time per phase (CUDA events around each kernel): propagate = k_predict; "
+           "resample = the exact CDF scan + ancestor search and gather; repropagate = k_update, which also runs "
+           "proliferate and the weight update (fused)\",\n";
     out << "  \"speedup\": 0.0,\n";
     out << "  \"trace_csv\": " << json_str(trace_csv) << ",\n";
     out << "  \"truth\": " << arr(data.truth) << ",\n";

@@ -17,6 +17,8 @@
 // touches ceil(8R/32) sectors instead of d+p+1.
 #include "sampler_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 namespace pfsmc_gpu {
 
 // Record pack/unpack for the AoS boundary (filter::Ensemble layout).
@@ -142,8 +144,12 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
     ev = s->pending.data() + s->pending.size() - (kNumKernels + 1);
     CK(cudaEventRecord(ev[0], st));
   }
+  // NVTX ranges name the PhaseTimings phases (filter.hpp:93-99) the kernels replace
+  nvtxRangePushA("propagate (k_predict)");
   s->ks->predict(c, s->grid, st);
+  nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[1], st));
+  nvtxRangePushA("resample (exact CDF scan + ancestor search)");
   launch_scan(c, s->ntiles, st, 1);
   if (timed) CK(cudaEventRecord(ev[2], st));
   launch_scan(c, s->ntiles, st, 2);
@@ -152,8 +158,11 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
     launch_search_only(c, s->grid, st);  // the update CTAs gather their ancestor themselves
   else
     launch_serve(c, s->grid, st);
+  nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[4], st));
+  nvtxRangePushA("proliferate + repropagate + weights (k_update)");
   s->ks->update(c, s->grid, st);
+  nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[5], st));
   CK(cudaGetLastError());
 }
@@ -646,6 +655,10 @@ pfsmc_gpu_status pfsmc_gpu_init_uniform(pfsmc_gpu_sampler* s, const double* th_l
 
 pfsmc_gpu_status pfsmc_gpu_step(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev,
                                 double t_obs, double h, double* trace_out) {
+  struct Range {  // NVTX range over the drop-in step
+    Range() { nvtxRangePushA("pfsmc_gpu_step (filter::pf_step)"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   return guarded([&] {
     const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
     enqueue_step(s, &sp, nullptr);

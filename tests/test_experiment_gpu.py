@@ -65,6 +65,9 @@ def test_run_experiment_matches_reference(kv, tmp_path, atol=0.0):
     np.testing.assert_allclose(rep_g["final_estimate"], rep_r["final_estimate"], rtol=1e-8)
     np.testing.assert_allclose(rep_g["final_std_u"], rep_r["final_std_u"], rtol=1e-8, atol=np.sqrt(atol))
     assert rep_g["warnings"] == rep_r["warnings"]
+    # PhaseTimings from the device (CUDA events per kernel)
+    ph = rep_g["phases"]
+    assert ph["propagate"] > 0 and ph["resample"] > 0 and ph["repropagate"] > 0, ph
 
 
 def test_run_experiment_errors_match_reference(tmp_path):
