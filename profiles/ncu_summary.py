@@ -43,9 +43,9 @@ def main():
                 try:
                     x = float(v)
                     if name.startswith("dram__bytes"):
-                        x *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                        x *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
                     if name == "gpu__time_duration.sum":  # -> ns, then dur_us = ns * 1e-3
-                        x *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(u, 1)
+                        x *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}.get(u, 1)
                     vals.append(f"{x * scale:11.2f}")
                 except ValueError:
                     vals.append(f"{v:>11s}")
