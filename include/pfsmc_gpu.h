@@ -203,6 +203,19 @@ pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, in
  * theta, exact multinomial resampling, gather of the 64-byte records. */
 pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key);
 pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
+/* Ancestor search of the config-5 iteration (filter.cpp:169-176: every slot's
+ * ancestor is upper_bound(cdf, u_n), bit-exact either way):
+ *   GUIDE    slot-order search (guide table -> segment ends -> one CDF segment)
+ *            and gather, one pass;
+ *   BUCKETED the uniforms are first bucketed by value (a one-pass counting
+ *            partition into 2^k ranges of [0, 1)), then searched and gathered
+ *            in bucket order, so the CDF, the search tables and the ancestor
+ *            records are read once, in narrow L2-resident windows; the
+ *            records are written to their slots (64-byte stores);
+ *   SPLIT    the GUIDE search writing only the ancestors, then a separate
+ *            slot-order gather. */
+enum { PFSMC_GPU_C5_SEARCH_GUIDE = 0, PFSMC_GPU_C5_SEARCH_BUCKETED = 1, PFSMC_GPU_C5_SEARCH_SPLIT = 2 };
+pfsmc_gpu_status pfsmc_gpu_c5_set_search(pfsmc_gpu_sampler* s, int mode);
 
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop; the FP64
  * roofline denominator the benchmarks report against). */

@@ -143,6 +143,168 @@ __global__ void __launch_bounds__(kThreads) k_c5_serve(Ctx c, unsigned long long
   }
 }
 
+// PFSMC_GPU_C5_SEARCH_SPLIT: the same search as k_c5_serve writing only the
+// ancestors (k_search_only), then this gather: while the search runs, the
+// only large random stream is the CDF segments, so the search tables stay in
+// L2; the gather is then the bare random-record gather.
+__global__ void __launch_bounds__(kThreads) k_c5_gather(Ctx c) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const unsigned a = n < c.N ? __ldcs(&c.anc[n]) : 0u;
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const int cur = c.st->cur;
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur]);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+  const uint64_t pol = l2_policy_stream();
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const long long ns = wbase + slot;
+    if (ns < c.N) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
+}
+
+// ---- bucketed ancestor search (PFSMC_GPU_C5_SEARCH_BUCKETED) ----
+// The slot-order search above reads, per slot, a guide entry, a few segment
+// ends and one 64-byte CDF segment at random, then the ancestor's record at
+// random: at 2^25 the tables fall out of L2 under the streaming traffic
+// (285 B of DRAM reads per slot for 128 B of compulsory random reads,
+// profiles/r01_notes.md). Here the uniforms are first partitioned by value
+// into 2^k equal ranges of [0, 1) (a counting partition: per-block shared
+// histogram, one global reservation per (block, bucket), the items written at
+// their reserved positions), then searched and gathered bucket by bucket:
+// neighbouring threads search neighbouring uniforms, so the guide, the segment
+// ends, the CDF segments and the ancestor records are each read from DRAM
+// about once, in a narrow window that stays in L2 (and L1) while the bucket
+// is served; the records are written to their slots as 64-byte stores. The
+// search itself is unchanged (find_ancestor_warp: upper_bound over the exact
+// CDF), so every ancestor is the slot-order one bit for bit; only the order
+// in which slots are served changes. Items beyond a bucket's capacity (cap is
+// mean + 8 sigma of the binomial count, so essentially never) go to a spill
+// list served after the buckets; a spill-list overflow raises kErrInternal.
+constexpr int kBucketItems = 16;              // uniforms per thread in the partition pass
+constexpr int kSpillCap = 1 << 16;            // spill-list entries
+constexpr int kMaxBucketBits = 12;            // <= 4096 buckets (shared histogram)
+
+struct C5Buckets {
+  int nb_bits;
+  long long cap;
+  unsigned* count;  // [NB] fill, [NB] spill count, [NB + 1] spill overflow flag
+  double* u;        // NB * cap + kSpillCap
+  unsigned* n;
+  unsigned* anc;
+};
+
+__global__ void __launch_bounds__(kThreads) k_c5_bucket(Ctx c, unsigned long long j, C5Buckets b) {
+  __shared__ unsigned hist[1 << kMaxBucketBits];
+  __shared__ unsigned base[1 << kMaxBucketBits];
+  if (grid_error(c)) return;
+  const int nb = 1 << b.nb_bits;
+  for (int i = threadIdx.x; i < nb; i += kThreads) hist[i] = 0;
+  __syncthreads();
+  const long long n0 = static_cast<long long>(blockIdx.x) * (kThreads * kBucketItems);
+  double u[kBucketItems];
+  unsigned key[kBucketItems];  // bucket << 16 | rank inside this block's bucket run
+#pragma unroll
+  for (int i = 0; i < kBucketItems; ++i) {
+    const long long n = n0 + i * kThreads + threadIdx.x;
+    u[i] = -1.0;
+    key[i] = 0xffffffffu;
+    if (n < c.N) {
+      u[i] = resample_uniform(c.seed, j, c.n0 + n);
+      const int k = min(static_cast<int>(scale2(u[i], b.nb_bits)), nb - 1);
+      key[i] = (static_cast<unsigned>(k) << 16) | atomicAdd(&hist[k], 1u);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nb; k += kThreads)
+    base[k] = hist[k] ? atomicAdd(&b.count[k], hist[k]) : 0u;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kBucketItems; ++i) {
+    if (key[i] == 0xffffffffu) continue;
+    const long long n = n0 + i * kThreads + threadIdx.x;
+    const int k = static_cast<int>(key[i] >> 16);
+    const long long pos = static_cast<long long>(base[k]) + (key[i] & 0xffffu);
+    long long at;
+    if (pos < b.cap) {
+      at = static_cast<long long>(k) * b.cap + pos;
+    } else {
+      const unsigned s = atomicAdd(&b.count[nb], 1u);
+      if (s >= static_cast<unsigned>(kSpillCap)) {
+        atomicOr(&c.st->error, kErrInternal);
+        continue;
+      }
+      at = static_cast<long long>(nb) * b.cap + s;
+    }
+    b.u[at] = u[i];
+    b.n[at] = static_cast<unsigned>(n);
+  }
+}
+
+// Block -> its run of bucket positions: blocks_per_bucket blocks per bucket
+// (consecutive, so the grid walks [0, 1) in increasing u), then the spill
+// list. Returns false when the whole block lies past the fill (block-uniform);
+// else `at` = the block's first position and `rem` = valid positions from it.
+__device__ __forceinline__ bool bucket_run(const C5Buckets& b, int blocks_per_bucket, long long& at,
+                                           unsigned& rem) {
+  const int nb = 1 << b.nb_bits;
+  const int k = blockIdx.x / blocks_per_bucket;
+  long long i0;
+  unsigned filled;
+  if (k < nb) {
+    i0 = static_cast<long long>(blockIdx.x % blocks_per_bucket) * kThreads;
+    filled = min(static_cast<unsigned>(b.cap), __ldcg(&b.count[k]));
+    at = static_cast<long long>(k) * b.cap + i0;
+  } else {
+    i0 = static_cast<long long>(blockIdx.x - nb * blocks_per_bucket) * kThreads;
+    filled = min(static_cast<unsigned>(kSpillCap), __ldcg(&b.count[nb]));
+    at = static_cast<long long>(nb) * b.cap + i0;
+  }
+  if (i0 >= filled) return false;
+  rem = filled - static_cast<unsigned>(i0);
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads) k_c5_bucket_serve(Ctx c, C5Buckets b, int blocks_per_bucket) {
+  if (grid_error(c)) return;
+  long long at;
+  unsigned rem;
+  if (!bucket_run(b, blocks_per_bucket, at, rem)) return;
+  const bool mine = threadIdx.x < rem;  // valid threads are a prefix of the block
+  const double u = mine ? __ldcs(&b.u[at + threadIdx.x]) : -1.0;
+  const unsigned n = mine ? __ldcs(&b.n[at + threadIdx.x]) : 0u;
+  const unsigned a = find_ancestor_warp<true>(c, u);
+  if (mine) b.anc[at + threadIdx.x] = a;
+  const int lane = threadIdx.x & 31;
+  const int cur = c.st->cur;
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur]);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+  const uint64_t wpol = l2_policy_stream();
+  const int nvalid = __popc(__ballot_sync(0xffffffffu, mine));
+  // four lanes per 64-byte record: the ancestor's record (read through L2,
+  // where its bucket neighbours find it) to the slot (one-shot stores)
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const unsigned ns = __shfl_sync(0xffffffffu, n, slot);
+    if (slot < nvalid)
+      st_hint(dst + static_cast<long long>(ns) * 4 + part, __ldg(src + static_cast<long long>(as) * 4 + part), wpol);
+  }
+}
+
+// ctx.anc[n] from the bucket-major (slot, ancestor) pairs: only when the
+// step diagnostics are read (pfsmc_gpu_get_step_diagnostics).
+__global__ void __launch_bounds__(kThreads) k_c5_bucket_anc(Ctx c, C5Buckets b, int blocks_per_bucket) {
+  long long at;
+  unsigned rem;
+  if (!bucket_run(b, blocks_per_bucket, at, rem) || threadIdx.x >= rem) return;
+  c.anc[b.n[at + threadIdx.x]] = b.anc[at + threadIdx.x];
+}
+
 __global__ void k_flip(DevState* st) { st->cur ^= 1; }
 
 // FP64 roofline denominator: 8 independent DFMA chains per thread.
@@ -183,6 +345,40 @@ __global__ void __launch_bounds__(kThreads) k_gather_peak(const double2* __restr
   }
 }
 
+int c5_bpb(const C5Buckets& b) { return static_cast<int>((b.cap + kThreads - 1) / kThreads); }
+
+// Bucket buffers, allocated on the first bucketed iteration: 2^k buckets of
+// about 2^16 uniforms each (at most 2^12 buckets), capacity mean + 8 sigma.
+C5Buckets c5_buckets(pfsmc_gpu_sampler* s) {
+  if (!s->c5_u) {
+    int bits = 0;
+    while (bits < kMaxBucketBits && (s->N >> (bits + 1)) >= (1LL << 16)) ++bits;
+    const double lam = std::ceil(static_cast<double>(s->N) / static_cast<double>(1LL << bits));
+    long long cap = static_cast<long long>(lam + 8.0 * std::sqrt(lam)) + kThreads;
+    cap = (cap + kThreads - 1) / kThreads * kThreads;
+    if (s->c5_cap_override > 0) cap = s->c5_cap_override;
+    const size_t slots = (static_cast<size_t>(cap) << bits) + kSpillCap;
+    s->c5_nb_bits = bits;
+    s->c5_cap = cap;
+    s->c5_count = s->dalloc<unsigned>((size_t(1) << bits) + 2);
+    s->c5_u = s->dalloc<double>(slots);
+    s->c5_n = s->dalloc<unsigned>(slots);
+    s->c5_anc = s->dalloc<unsigned>(slots);
+  }
+  return C5Buckets{s->c5_nb_bits, s->c5_cap, s->c5_count, s->c5_u, s->c5_n, s->c5_anc};
+}
+
+// The bucketed iteration leaves its ancestors in bucket order; slot order on
+// demand (step diagnostics).
+void c5_flush_ancestors(pfsmc_gpu_sampler* s) {
+  if (!s->c5_anc_pending) return;
+  const C5Buckets b = c5_buckets(s);
+  k_c5_bucket_anc<<<(1 << b.nb_bits) * c5_bpb(b) + kSpillCap / kThreads, kThreads, 0, s->stream>>>(s->ctx, b,
+                                                                                                      c5_bpb(b));
+  CK(cudaGetLastError());
+  s->c5_anc_pending = false;
+}
+
 }  // namespace pfsmc_gpu
 
 extern "C" {
@@ -212,9 +408,52 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
       k_c5_stats<16><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
     launch_scan(c, s->ntiles, s->stream, 1);
     launch_scan(c, s->ntiles, s->stream, 2);
-    k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
+    if (s->c5_search == PFSMC_GPU_C5_SEARCH_BUCKETED) {
+      const C5Buckets b = c5_buckets(s);
+      const int nb = 1 << b.nb_bits;
+      // the partition pass draws the uniforms; it only needs lse-free data, but
+      // runs after the scan so the CDF tables are complete when serving starts
+      CK(cudaMemsetAsync(b.count, 0, sizeof(unsigned) * (nb + 1), s->stream));
+      const int pgrid = static_cast<int>((s->N + kThreads * kBucketItems - 1) / (kThreads * kBucketItems));
+      k_c5_bucket<<<pgrid, kThreads, 0, s->stream>>>(c, j, b);
+      k_c5_bucket_serve<<<nb * c5_bpb(b) + kSpillCap / kThreads, kThreads, 0, s->stream>>>(c, b, c5_bpb(b));
+      s->c5_anc_pending = true;
+    } else if (s->c5_search == PFSMC_GPU_C5_SEARCH_SPLIT) {
+      StepParams sp{};
+      sp.j = j;
+      *s->sp_host = sp;
+      CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
+      launch_search_only(c, s->grid, s->stream);
+      k_c5_gather<<<s->grid, kThreads, 0, s->stream>>>(c);
+      s->c5_anc_pending = false;
+    } else {
+      k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
+      s->c5_anc_pending = false;
+    }
     k_flip<<<1, 1, 0, s->stream>>>(s->st);
+    // the error word reaches the host with the next pfsmc_gpu_synchronize
+    CK(cudaMemcpyAsync(&s->st_host->error, &s->st->error, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_c5_set_search(pfsmc_gpu_sampler* s, int mode) {
+  return guarded([&] {
+    if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    if (mode < PFSMC_GPU_C5_SEARCH_GUIDE || mode > PFSMC_GPU_C5_SEARCH_SPLIT)
+      throw ConfigError("c5_set_search: mode must be PFSMC_GPU_C5_SEARCH_GUIDE, _BUCKETED or _SPLIT");
+    s->c5_search = mode;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Test knob (not in the public header): bucket capacity override, to drive
+// items into the spill list; 0 restores the default.
+pfsmc_gpu_status pfsmc_gpu_c5_debug_bucket_cap(pfsmc_gpu_sampler* s, long long cap) {
+  return guarded([&] {
+    if (s->c5_u) throw ConfigError("c5_debug_bucket_cap: set before the first bucketed iteration");
+    s->c5_cap_override = cap;
     return PFSMC_GPU_OK;
   });
 }

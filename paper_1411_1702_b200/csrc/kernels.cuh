@@ -92,6 +92,11 @@ __device__ __forceinline__ uint64_t l2_policy_stream() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
@@ -337,7 +342,11 @@ __device__ __forceinline__ unsigned find_ancestor(const Ctx& c, double u) {
 // Warp-cooperative form: every lane of the warp must call it (lanes without
 // a slot pass u = -1). The segment reads are spread so that each load
 // instruction covers whole 64-byte segments (four lanes each), i.e. one L1
-// wavefront per segment instead of one per lane and per 16 bytes.
+// wavefront per segment instead of one per lane and per 16 bytes. The CDF
+// segments are read evict-first (slot order: one-shot random reads) unless
+// the caller searches value-bucketed uniforms (LOCAL: neighbouring lanes and
+// warps read the same segments, so they stay cached).
+template <bool LOCAL = false>
 __device__ __forceinline__ unsigned find_ancestor_warp(const Ctx& c, double u) {
   constexpr int SEGL2 = kSegLog2;
   constexpr int P = 1 << (SEGL2 - 1);  // lanes per segment (16-byte parts)
@@ -354,7 +363,8 @@ __device__ __forceinline__ unsigned find_ancestor_warp(const Ctx& c, double u) {
     const long long kk = ks + 2 * (lane % P);
     int cnt = 0;
     if (kk + 1 < N) {
-      const double2 v = ld_hint(reinterpret_cast<const double2*>(c.cdf + kk), l2_policy_stream());
+      const double2 v = LOCAL ? __ldg(reinterpret_cast<const double2*>(c.cdf + kk))
+                              : ld_hint(reinterpret_cast<const double2*>(c.cdf + kk), l2_policy_stream());
       cnt = (v.x <= us) + (v.y <= us);
     } else if (kk < N) {
       cnt = __ldg(&c.cdf[kk]) <= us;

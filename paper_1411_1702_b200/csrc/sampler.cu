@@ -283,6 +283,7 @@ void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepPar
     throw ConfigError("step: a shard handle runs only the sharded phases (pfsmc_gpu_shard_step / shard_*)");
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
   raise_pending(s);
+  s->c5_anc_pending = false;  // this step writes ctx.anc in slot order
   if (dev_sp) {
     CK(cudaMemcpyAsync(s->sp_dev, dev_sp, sizeof(StepParams), cudaMemcpyDeviceToDevice, s->stream));
   } else {
@@ -743,6 +744,7 @@ pfsmc_gpu_status pfsmc_gpu_get_step_diagnostics(pfsmc_gpu_sampler* s, uint32_t* 
                                                 double* loglik_bar, uint64_t* newton_iters) {
   return guarded([&] {
     const size_t N = static_cast<size_t>(s->N);
+    if (ancestors) c5_flush_ancestors(s);
     if (ancestors) CK(cudaMemcpyAsync(ancestors, s->ctx.anc, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, s->stream));
     if (loglik_bar) CK(cudaMemcpyAsync(loglik_bar, s->ctx.llbar, sizeof(double) * N, cudaMemcpyDeviceToHost, s->stream));
     DevState h{};
@@ -778,6 +780,7 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
     Ctx c = s->ctx;
     c.gin = dg;
+    s->c5_anc_pending = false;
     launch_gin(c, s->ntiles, s->stream);
     launch_scan(c, s->ntiles, s->stream, 1);
     launch_scan(c, s->ntiles, s->stream, 2);

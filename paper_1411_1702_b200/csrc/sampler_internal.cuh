@@ -150,6 +150,16 @@ struct pfsmc_gpu_sampler {
   unsigned* oblk = nullptr;        // scan block sums
   unsigned long long* otot = nullptr;       // children per rank (world), from the global walk
   unsigned long long* otot_host = nullptr;  // pinned mirror
+  // config 5, bucketed ancestor search (c5.cu; allocated on first use)
+  int c5_search = 0;               // PFSMC_GPU_C5_SEARCH_GUIDE / _BUCKETED
+  int c5_nb_bits = 0;              // 2^bits uniform buckets
+  long long c5_cap = 0;            // slots per bucket
+  long long c5_cap_override = 0;   // test knob: force a small capacity (spill path)
+  unsigned* c5_count = nullptr;    // [NB] bucket fill + [NB] spill counter / overflow flag
+  double* c5_u = nullptr;          // bucket-major uniforms (NB * cap), then the spill list
+  unsigned* c5_n = nullptr;        // their slots
+  unsigned* c5_anc = nullptr;      // their ancestors (bucket-major; scattered to ctx.anc on demand)
+  bool c5_anc_pending = false;     // ctx.anc not yet written for the last bucketed iteration
 
   template <typename T>
   T* dalloc(size_t count) {
@@ -211,3 +221,6 @@ void enqueue_readback(pfsmc_gpu_sampler* s);
 void fill_trace(const pfsmc_gpu_sampler* s, const DevState& h, const double* xmean, double* out);
 void harvest_timing(pfsmc_gpu_sampler* s);
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp);
+namespace pfsmc_gpu {
+void c5_flush_ancestors(pfsmc_gpu_sampler* s);  // c5.cu
+}

@@ -108,7 +108,8 @@ def load_library(path: str = LIB_PATH):
                      "pfsmc_gpu_step_resident", "pfsmc_gpu_synchronize", "pfsmc_gpu_run",
                      "pfsmc_gpu_get_step_diagnostics", "pfsmc_gpu_resample_from_g",
                      "pfsmc_gpu_set_kernel_timing", "pfsmc_gpu_kernel_times", "pfsmc_gpu_flush_l2",
-                     "pfsmc_gpu_c5_set_logweights", "pfsmc_gpu_c5_iteration"):
+                     "pfsmc_gpu_c5_set_logweights", "pfsmc_gpu_c5_iteration", "pfsmc_gpu_c5_set_search",
+                     "pfsmc_gpu_c5_debug_bucket_cap"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
     return _lib
@@ -341,6 +342,14 @@ class GpuSampler:
 
     def c5_iteration(self, j: int):
         self._check(self.lib.pfsmc_gpu_c5_iteration(self.h, C.c_uint64(j)))
+
+    def c5_set_search(self, mode: str, debug_bucket_cap: int = 0):
+        """'guide' (slot-order search + gather) or 'bucketed' (uniforms
+        partitioned by value first; include/pfsmc_gpu.h). debug_bucket_cap
+        forces a small bucket capacity (spill-list test)."""
+        if debug_bucket_cap:
+            self._check(self.lib.pfsmc_gpu_c5_debug_bucket_cap(self.h, C.c_longlong(debug_bucket_cap)))
+        self._check(self.lib.pfsmc_gpu_c5_set_search(self.h, {"guide": 0, "bucketed": 1, "split": 2}[mode]))
 
     def transfer_bytes(self):
         """(H2D, D2H) bytes of one blocking pf_step (pfsmc_gpu_step_transfer_bytes)."""

@@ -797,6 +797,53 @@ def test_c5_resample_iteration_matches_oracle(n, sigmas):
         s.close()
 
 
+@pytest.mark.parametrize("n,cap", [(1 << 16, 0), ((1 << 22) + 4097 * 3 + 5, 0), ((1 << 20) + 77, 0),
+                                   (1 << 16, 256), (3 * 4096 + 11, 512)])
+def test_c5_bucketed_search_is_the_slot_order_search(n, cap):
+    """The bucketed ancestor search (uniforms partitioned by value, served in
+    bucket order) gives every slot the slot-order search's ancestor and record,
+    bit for bit; cap > 0 forces a tiny bucket capacity so most items take the
+    spill list."""
+    from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
+    rng = np.random.default_rng(11)
+    states = rng.standard_normal((n, 6))
+    params = rng.standard_normal((n, 2))
+    out = {}
+    for mode in ("guide", "bucketed", "split"):
+        s = GpuSampler("payload64", PfConfig(particles=n, seed=78), ObservationModel([0], 1.0))
+        s.c5_set_search(mode, debug_bucket_cap=cap if mode == "bucketed" else 0)
+        s.set_ensemble(Ensemble(states, params, np.zeros(n), np.zeros(2), np.eye(2)))
+        s.c5_set_logweights(2.0, 9)
+        res = []
+        for it in range(1, 4):  # chained iterations: the second and third resample the first's output
+            s.c5_iteration(it)
+            s.synchronize()
+            anc, _, _ = s.step_diagnostics()
+            e = s.get_ensemble()
+            res.append((anc.copy(), e.states.copy(), e.params_u.copy(), e.mean_u.copy(), e.cov_u.copy()))
+        out[mode] = res
+        s.close()
+    for other in ("bucketed", "split"):
+        for a, b in zip(out["guide"], out[other]):
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y), other
+
+
+def test_c5_bucket_spill_overflow_raises():
+    """More items than bucket capacity + spill list: an internal error at the
+    next synchronize, not a silent partial gather."""
+    from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
+    n = 1 << 17
+    s = GpuSampler("payload64", PfConfig(particles=n, seed=78), ObservationModel([0], 1.0))
+    s.c5_set_search("bucketed", debug_bucket_cap=256)
+    s.set_ensemble(Ensemble(np.zeros((n, 6)), np.zeros((n, 2)), np.zeros(n), np.zeros(2), np.eye(2)))
+    s.c5_set_logweights(1.0, 9)
+    s.c5_iteration(1)
+    with pytest.raises(Exception, match="internal"):
+        s.synchronize()
+    s.close()
+
+
 # ---------------------------------------------------------------- error paths of chol_psd / weights
 def _err_sampler_and_ens(n=4096, seed=3):
     sc = StepConfig(model="lv", family="am", order=2, h=0.1, a=0.98, seed=seed, obs_idx=(0, 1), sigma=0.05)
