@@ -131,10 +131,12 @@ __device__ __forceinline__ bool grid_error(const Ctx& c) {
 // Only the exact scan's classification reads these, through the rigorous
 // bound of exact_cdf.cuh (sum_bound); no pass over the fitness vector and no
 // look-back is needed.
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
 struct TileGroupHook {
   const Ctx* c;
   __device__ void operator()(int g, int gsize) const {
-    const int bpt_log2 = c->tile_log2 - 8;  // K1 blocks per tile
+    const int bpt_log2 = c->tile_log2 - c->k1_block_log2;  // K1 blocks per tile (<= 32)
     const double mg = __ldcg(&c->gpart[2 * g]);
     const int b0 = g * kGroup;
     double w = 0.0;
@@ -158,11 +160,14 @@ struct TileGroupHook {
   }
 };
 
-// tile_m (C5 path): per-tile maxima instead of the group maxima.
+// tile_m (C5 path): per-tile maxima instead of the group maxima. NT: the
+// calling kernel's block size; the groups are kGroup K1 blocks of
+// 2^k1_block_log2 particles.
+template <int NT = kThreads>
 __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const double* tile_m = nullptr) {
-  __shared__ SumCnt sw[2 * kWarps];
-  const int tpg_log2 = 6 - (c.tile_log2 - 8);  // tiles per group
-  const int per = (c.ntiles + kThreads - 1) / kThreads;
+  __shared__ SumCnt sw[2 * (NT / 32)];
+  const int tpg_log2 = 6 - (c.tile_log2 - c.k1_block_log2);  // tiles per group
+  const int per = (c.ntiles + NT - 1) / NT;
   const int t0 = threadIdx.x * per, t1 = min(t0 + per, c.ntiles);
   double s[8];
   long long n[8];
@@ -179,7 +184,7 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const do
     acc.c += k;
   }
   SumCnt tot;
-  SumCnt ex = block_excl_scan_sc(acc, tot, sw);
+  SumCnt ex = block_excl_scan_sc<NT>(acc, tot, sw);
   for (int t = t0; t < t1; ++t) {
     double v;
     long long k;
@@ -196,22 +201,40 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const do
     ex.s += v;
     ex.c += k;
   }
-  if (threadIdx.x == kThreads - 1) {
+  if (threadIdx.x == NT - 1) {
     c.shard_sum[0] = tot.s;
     c.shard_sum[1] = static_cast<double>(tot.c);
   }
 }
 
 // ---------------------------------------------------------------- K1
+// CTAs per SM the model's K1 / K3 are built for (launch bounds)
+template <class M>
+constexpr int k1_min_blocks() {
+  return BlockOf<M>::value == 128 ? 3 : M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1;
+}
+template <class M>
+constexpr int k3_min_blocks() {
+  return BlockOf<M>::value == 128 ? 3 : M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1;
+}
+// Dynamic shared memory of a K1 / K3 CTA: the LMM history columns.
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1)) k_predict(Ctx c) {
+constexpr int hist_smem_bytes() {
+  using Pr = Propagator<M, FAM, ORD>;
+  return Pr::kSmemHist ? Pr::kHistDoubles * BlockOf<M>::value * static_cast<int>(sizeof(double)) : 0;
+}
+
+template <class M, int FAM, int ORD>
+__global__ void __launch_bounds__(BlockOf<M>::value, k1_min_blocks<M>()) k_predict(Ctx c) {
   constexpr int D = M::D, P = M::P;
-  __shared__ double scratch[kWarps * 2];
+  constexpr int KT = BlockOf<M>::value;
+  __shared__ double scratch[KT / 32 * 2];
   __shared__ double fin[2];
+  extern __shared__ double hist_smem[];
   if (grid_error(c)) return;
   const StepParams& sp = *c.sp;  // read fields in place (no local copy)
   const DevState& st = *c.st;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const long long n = static_cast<long long>(blockIdx.x) * KT + threadIdx.x;
   double lgv = kNegInf;
   int iters = 0;
   if (n < c.N) {
@@ -223,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M:
     for (int k = 0; k < P; ++k) th[k] = exp(c.a * tu[k] + c.one_minus_a * st.mu[k]);
     Propagator<M, FAM, ORD> prop;
     prop.mk = M::load_k(c.mconst);
+    prop.bind_history(hist_smem + threadIdx.x);
     int status;
     if constexpr (ORD == 0)
       status = prop.run_adaptive(th, x, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
@@ -242,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M:
   const double one[1] = {1.0};
   const int nfin = __syncthreads_count(isfinite(lgv) != 0);
   if (threadIdx.x == 0) c.blk_cnt[blockIdx.x] = nfin;
-  block_partial<1, false>(lgv, one, c.part + blockIdx.x * 2, scratch);
-  if (tree_reduce_last<1, false>(c.part, c.gpart, c.cnt_pred, fin, scratch, !c.sharded,
-                                 TileGroupHook{&c})) {
+  block_partial<1, false, KT>(lgv, one, c.part + blockIdx.x * 2, scratch);
+  if (tree_reduce_last<1, false, TileGroupHook, KT>(c.part, c.gpart, c.cnt_pred, fin, scratch, !c.sharded,
+                                                     TileGroupHook{&c})) {
     __shared__ double s_lse;
     if (threadIdx.x == 0) {
       // logsumexp (filter.cpp:16-23) + the degeneracy check (filter.cpp:149-152)
@@ -255,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M:
       s_lse = lse;
     }
     __syncthreads();
-    if (isfinite(s_lse)) tile_prefixes(c, s_lse);
+    if (isfinite(s_lse)) tile_prefixes<KT>(c, s_lse);
   }
 }
 
@@ -490,15 +514,17 @@ __device__ void chol_psd_device(DevState& st) {
 }
 
 template <class M, int FAM, int ORD>
-__global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1)) k_update(Ctx c) {
+__global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_update(Ctx c) {
   constexpr int D = M::D, P = M::P;
+  constexpr int KT = BlockOf<M>::value;
   using ML = MomentLayout<M>;
   constexpr int V = ML::V;
-  __shared__ double scratch[kWarps * V];
+  __shared__ double scratch[KT / 32 * V];
   __shared__ double fin[V + 1];  // M + V values
   __shared__ double sL[P * P], sK[P];
-  constexpr int kTsc = V <= 12 ? V * kThreads : 1;
+  constexpr int kTsc = V <= 12 ? V * KT : 1;
   __shared__ double tsc[kTsc];
+  extern __shared__ double hist_smem[];
   if (grid_error(c)) return;
   DevState& st = *c.st;
   if (st.chol_failed) {
@@ -511,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M:
   __syncthreads();
   const StepParams& sp = *c.sp;  // read fields in place (no local copy)
   const int cur = st.cur;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const long long n = static_cast<long long>(blockIdx.x) * KT + threadIdx.x;
   double lwv = kNegInf;
   double vals[V];  // moment leaf
 #pragma unroll
@@ -541,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M:
     for (int k = 0; k < D; ++k) xr[k] = x[k];
     Propagator<M, FAM, ORD> prop;
     prop.mk = M::load_k(c.mconst);
+    prop.bind_history(hist_smem + threadIdx.x);
     int status;
     if constexpr (ORD == 0)
       status = prop.run_adaptive(th, xr, sp.t_prev, sp.t_obs, c.rtol, c.tol, c.max_iter, gamma, iters);
@@ -582,9 +609,9 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M:
     for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(0xffffffffu, it, o);
     if ((threadIdx.x & 31) == 0 && it) atomicAdd(&st.newton_iters, static_cast<unsigned long long>(it));
   }
-  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch,
-                         V <= 12 ? tsc : nullptr);
-  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
+  block_partial<V, true, KT>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch,
+                             V <= 12 ? tsc : nullptr);
+  if (tree_reduce_last<V, true, NoGroupHook, KT>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
     if (threadIdx.x == 0) {
       double K[P];
 #pragma unroll
@@ -601,14 +628,15 @@ __global__ void __launch_bounds__(kThreads, (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M:
 // Moments of the resident ensemble (after injection / initialisation):
 // refreshes the shrink mean (and, for init, cov + chol); lse_w untouched.
 template <class M>
-__global__ void __launch_bounds__(kThreads) k_moments(Ctx c, int set_cov) {
+__global__ void __launch_bounds__(BlockOf<M>::value) k_moments(Ctx c, int set_cov) {
   constexpr int D = M::D, P = M::P;
+  constexpr int KT = BlockOf<M>::value;  // the partial layout of k_update
   using ML = MomentLayout<M>;
   constexpr int V = ML::V;
-  __shared__ double scratch[kWarps * V];
+  __shared__ double scratch[KT / 32 * V];
   __shared__ double fin[V + 1];  // M + V values
   DevState& st = *c.st;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const long long n = static_cast<long long>(blockIdx.x) * KT + threadIdx.x;
   double lwv = kNegInf;
   double vals[V];
 #pragma unroll
@@ -632,8 +660,8 @@ __global__ void __launch_bounds__(kThreads) k_moments(Ctx c, int set_cov) {
     for (int k = 0; k < D; ++k) vals[1 + ML::NA + ML::NB + k] = x[k];
     vals[V - 1] = 1.0;
   }
-  block_partial<V, true>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
-  if (tree_reduce_last<V, true>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
+  block_partial<V, true, KT>(lwv, vals, c.part + static_cast<size_t>(blockIdx.x) * (V + 1), scratch);
+  if (tree_reduce_last<V, true, NoGroupHook, KT>(c.part, c.gpart, c.cnt_upd, fin, scratch, !c.sharded)) {
     if (threadIdx.x == 0) {
       finalize_moments<M>(c, fin, K, false, set_cov != 0);
       chol_psd_device<P>(st);
@@ -737,22 +765,38 @@ __global__ void k_trajectory(const double* prm, const double* times, int T, doub
 
 template <class M, int FAM, int ORD>
 struct KernelSetT final : KernelSet {
+  static constexpr int KT = BlockOf<M>::value;
+  static constexpr int kHist = hist_smem_bytes<M, FAM, ORD>();
+  int attr_device = -1;  // the device whose kernels got the dynamic-smem attribute
   KernelSetT() {
     d = M::D;
     p = M::P;
+    kt = KT;
+  }
+  void set_attributes() {
+    if constexpr (kHist > 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev == attr_device) return;
+      cudaFuncSetAttribute(k_predict<M, FAM, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHist);
+      cudaFuncSetAttribute(k_update<M, FAM, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHist);
+      attr_device = dev;
+    }
   }
   void trajectory(const double* prm, const double* times, int T, double t0, double rtol, double tol,
                   int max_iter, double* out, int* status, cudaStream_t s) override {
     k_trajectory<M><<<1, 32, 0, s>>>(prm, times, T, t0, rtol, tol, max_iter, out, status);
   }
   void predict(const Ctx& c, int grid, cudaStream_t s) override {
-    k_predict<M, FAM, ORD><<<grid, kThreads, 0, s>>>(c);
+    set_attributes();
+    k_predict<M, FAM, ORD><<<grid, KT, kHist, s>>>(c);
   }
   void update(const Ctx& c, int grid, cudaStream_t s) override {
-    k_update<M, FAM, ORD><<<grid, kThreads, 0, s>>>(c);
+    set_attributes();
+    k_update<M, FAM, ORD><<<grid, KT, kHist, s>>>(c);
   }
   void moments(const Ctx& c, int grid, cudaStream_t s, int set_cov) override {
-    k_moments<M><<<grid, kThreads, 0, s>>>(c, set_cov);
+    k_moments<M><<<grid, KT, 0, s>>>(c, set_cov);
   }
   void chol(const Ctx& c, cudaStream_t s) override { k_chol<M::P><<<1, 32, 0, s>>>(c.st); }
   void init(const Ctx& c, int grid, cudaStream_t s, int kind, const double* prm, double lw0) override {

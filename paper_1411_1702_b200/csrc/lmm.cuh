@@ -69,6 +69,19 @@ __device__ __forceinline__ double ref_clamp(double v, double lo, double hi) {
   return (v < lo) ? lo : (hi < v) ? hi : v;
 }
 
+// max(0, |v_0|, ..., |v_{N-1}|) with NaN entries skipped, as a fmax tree.
+template <int N>
+__device__ __forceinline__ double max_abs_tree(const double (&v)[N]) {
+  double t[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) t[j] = fabs(v[j]);
+#pragma unroll
+  for (int w = 1; w < N; w <<= 1)
+#pragma unroll
+    for (int j = 0; j + w < N; j += 2 * w) t[j] = fmax(t[j], t[j + w]);
+  return fmax(0.0, t[0]);
+}
+
 // ---- LU with partial pivoting, in registers (linalg.cpp:201-258) --------
 template <int D>
 __device__ __forceinline__ bool lu_solve_inplace(double (&A)[D][D], double (&b)[D]) {
@@ -178,7 +191,9 @@ __device__ __forceinline__ bool band_solve(const typename M::K& mk, double tn, c
   for (int i = 0; i < D; ++i) {
     dg[i] = -hb0 * jd[i];
     dg[i] += 1.0;
-    fast &= fabs(dg[i]) >= 2.2250738585072014e-308 && fabs(dg[i]) <= 1.7976931348623157e308;
+    // DBL_MIN <= |dg| <= DBL_MAX (not NaN), decided by the high word alone
+    const unsigned ha = static_cast<unsigned>(__double2hiint(dg[i])) & 0x7fffffffu;
+    fast &= ha - 0x00100000u < 0x7ff00000u - 0x00100000u;
   }
 #pragma unroll
   for (int c = 0; c + 1 < D; ++c) {
@@ -190,10 +205,8 @@ __device__ __forceinline__ bool band_solve(const typename M::K& mk, double tn, c
   // fast variant: the D pivot reciprocals in one batch; forward elimination
   // and back substitution multiply by them (no division)
   {
-    double one[D], inv[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) one[i] = 1.0;
-    ddiv_batch<D>(one, dg, inv);
+    double inv[D];
+    drcp_batch<D>(dg, inv);
 #pragma unroll
     for (int i = 1; i < D; ++i) b[i] -= (sb[i - 1] * inv[i - 1]) * b[i - 1];
 #pragma unroll
@@ -269,13 +282,12 @@ __device__ __forceinline__ int newton_solve(const typename M::K& mk, double tn, 
       iters += iter;
       return kSingular;
     }
-    double dn = 0.0, xn = 0.0;
+    // the max-norms (lmm.cpp:250-256: a std::max pass from 0 over |.|, which
+    // skips NaN entries) as fmax trees: fmax also skips NaN and max is exact,
+    // so the values are the reference's, with a log-depth dependency chain
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      x[j] -= r[j];
-      dn = ref_max(dn, fabs(r[j]));
-      xn = ref_max(xn, fabs(x[j]));
-    }
+    for (int j = 0; j < D; ++j) x[j] -= r[j];
+    const double dn = max_abs_tree<D>(r), xn = max_abs_tree<D>(x);
     if (!isfinite(xn) || !isfinite(dn)) {
       iters += iter;
       return kInvalidRhs;
@@ -298,20 +310,49 @@ struct Propagator {
   static constexpr int SD = FAM == kBDF ? ORD + 1 : 1;              // states kept
   static constexpr int FD = ORD == 0 ? 1 : FAM == kAB ? ORD + 1 : ORD;  // f values kept
 
-  double xs[SD][D];
-  double fs[FD][D];
+  // History storage: registers, or (models with kSmemHistory: the 8-species
+  // chain) a per-thread column of dynamic shared memory bound by the kernel
+  // (bind_history), entry (slot, j) at hist_[(slot * D + j) * kHistStride], as
+  // ring buffers. Same values, same arithmetic; the registers it frees let
+  // three CTAs share an SM instead of one.
+  static constexpr bool kSmemHist = SmemHistOf<M>::value;
+  static constexpr int kHistStride = BlockOf<M>::value;
+  static constexpr int kHistDoubles = (SD + FD) * D;  // per thread
+  double xs[kSmemHist ? 1 : SD][D];
+  double fs[kSmemHist ? 1 : FD][D];
+  double* hist_ = nullptr;
+  int hx = 0, hf = 0;
+  __device__ __forceinline__ void bind_history(double* column) { hist_ = column; }
+  __device__ __forceinline__ double& X(int i, int j) {
+    if constexpr (kSmemHist) {
+      const int sl = hx + i < SD ? hx + i : hx + i - SD;
+      return hist_[(sl * D + j) * kHistStride];
+    } else {
+      return xs[i][j];
+    }
+  }
+  __device__ __forceinline__ double X(int i, int j) const { return const_cast<Propagator*>(this)->X(i, j); }
+  __device__ __forceinline__ double& F(int i, int j) {
+    if constexpr (kSmemHist) {
+      const int sl = hf + i < FD ? hf + i : hf + i - FD;
+      return hist_[((SD + sl) * D + j) * kHistStride];
+    } else {
+      return fs[i][j];
+    }
+  }
+  __device__ __forceinline__ double F(int i, int j) const { return const_cast<Propagator*>(this)->F(i, j); }
   typename M::K mk;  // model constants (the bound OdeModel's state, models.hpp:20-55)
 
   // AB(q) explicit combination: 0 + 1.0*x_n, then (h*beta_i) f_{n+1-i}.
   template <int Q>
   __device__ __forceinline__ void ab_step(double h, double (&out)[D]) const {
 #pragma unroll
-    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * xs[0][j];
+    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * X(0, j);
 #pragma unroll
     for (int i = 1; i <= Q; ++i) {
       const double hb = h * ab_beta(Q, i);
 #pragma unroll
-      for (int j = 0; j < D; ++j) out[j] += hb * fs[i - 1][j];
+      for (int j = 0; j < D; ++j) out[j] += hb * F(i - 1, j);
     }
   }
 
@@ -320,12 +361,12 @@ struct Propagator {
   __device__ __forceinline__ void implicit_terms(double h, double (&c)[D]) const {
     if constexpr (FAM == kAM) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * xs[0][j];
+      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * X(0, j);
 #pragma unroll
       for (int i = 1; i < PA; ++i) {
         const double hb = h * am_beta(PA, i);
 #pragma unroll
-        for (int j = 0; j < D; ++j) c[j] += hb * fs[i - 1][j];
+        for (int j = 0; j < D; ++j) c[j] += hb * F(i - 1, j);
       }
     } else {
 #pragma unroll
@@ -334,7 +375,7 @@ struct Propagator {
       for (int i = 0; i < PA; ++i) {
         const double a = bdf_alpha(PA, i);
 #pragma unroll
-        for (int j = 0; j < D; ++j) c[j] += a * xs[i][j];
+        for (int j = 0; j < D; ++j) c[j] += a * X(i, j);
       }
     }
   }
@@ -350,25 +391,31 @@ struct Propagator {
     for (int i = 0; i <= Q; ++i) {
       const double coef = sign * binom;
 #pragma unroll
-      for (int j = 0; j < D; ++j) out[j] += coef * xs[i][j];
+      for (int j = 0; j < D; ++j) out[j] += coef * X(i, j);
       sign = -sign;
       binom = binom * static_cast<double>(Q + 1 - (i + 1)) / static_cast<double>(i + 2);
     }
   }
 
   __device__ __forceinline__ void push(const double (&x)[D], const double (&f)[D]) {
+    if constexpr (kSmemHist) {
+      // ring buffers: the newest entry moves one slot down, nothing is copied
+      hx = hx == 0 ? SD - 1 : hx - 1;
+      hf = hf == 0 ? FD - 1 : hf - 1;
+    } else {
 #pragma unroll
-    for (int i = SD - 1; i > 0; --i)
+      for (int i = SD - 1; i > 0; --i)
 #pragma unroll
-      for (int j = 0; j < D; ++j) xs[i][j] = xs[i - 1][j];
+        for (int j = 0; j < D; ++j) xs[i][j] = xs[i - 1][j];
 #pragma unroll
-    for (int i = FD - 1; i > 0; --i)
+      for (int i = FD - 1; i > 0; --i)
 #pragma unroll
-      for (int j = 0; j < D; ++j) fs[i][j] = fs[i - 1][j];
+        for (int j = 0; j < D; ++j) fs[i][j] = fs[i - 1][j];
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      xs[0][j] = x[j];
-      fs[0][j] = f[j];
+      X(0, j) = x[j];
+      F(0, j) = f[j];
     }
   }
 
@@ -387,7 +434,7 @@ struct Propagator {
         ab_step<PA - 1>(h, ref);
       } else {
 #pragma unroll
-        for (int j = 0; j < D; ++j) ref[j] = xs[0][j];
+        for (int j = 0; j < D; ++j) ref[j] = X(0, j);
       }
       factor = 1.0;
     } else {
@@ -434,26 +481,26 @@ struct Propagator {
   // sequence is exactly that of the templates above.
   __device__ __forceinline__ void ab_step_rt(int q, double h, double (&out)[D]) const {
 #pragma unroll
-    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * xs[0][j];
+    for (int j = 0; j < D; ++j) out[j] = 0.0 + 1.0 * X(0, j);
 #pragma unroll
     for (int i = 1; i <= FD; ++i) {
       if (i <= q) {
         const double hb = h * ab_beta(q, i);
 #pragma unroll
-        for (int j = 0; j < D; ++j) out[j] += hb * fs[i - 1][j];
+        for (int j = 0; j < D; ++j) out[j] += hb * F(i - 1, j);
       }
     }
   }
   __device__ __forceinline__ void implicit_terms_rt(int pa, double h, double (&c)[D]) const {
     if constexpr (FAM == kAM) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * xs[0][j];
+      for (int j = 0; j < D; ++j) c[j] = 0.0 + 1.0 * X(0, j);
 #pragma unroll
       for (int i = 1; i < FD + 1; ++i) {
         if (i < pa) {
           const double hb = h * am_beta(pa, i);
 #pragma unroll
-          for (int j = 0; j < D; ++j) c[j] += hb * fs[i - 1][j];
+          for (int j = 0; j < D; ++j) c[j] += hb * F(i - 1, j);
         }
       }
     } else {
@@ -464,7 +511,7 @@ struct Propagator {
         if (i < pa) {
           const double a = bdf_alpha(pa, i);
 #pragma unroll
-          for (int j = 0; j < D; ++j) c[j] += a * xs[i][j];
+          for (int j = 0; j < D; ++j) c[j] += a * X(i, j);
         }
       }
     }
@@ -479,7 +526,7 @@ struct Propagator {
       if (i <= q) {
         const double coef = sign * binom;
 #pragma unroll
-        for (int j = 0; j < D; ++j) out[j] += coef * xs[i][j];
+        for (int j = 0; j < D; ++j) out[j] += coef * X(i, j);
         sign = -sign;
         binom = binom * static_cast<double>(q + 1 - (i + 1)) / static_cast<double>(i + 2);
       }
@@ -497,7 +544,7 @@ struct Propagator {
         ab_step_rt(pa - 1, h, ref);
       } else {
 #pragma unroll
-        for (int j = 0; j < D; ++j) ref[j] = xs[0][j];
+        for (int j = 0; j < D; ++j) ref[j] = X(0, j);
       }
       factor = 1.0;
     } else {
@@ -648,10 +695,11 @@ struct Propagator {
     for (int j = 0; j < D; ++j) gamma[j] = 0.0;
     double f0[D];
     if (!M::rhs(mk, t0, th, x, f0)) return kInvalidRhs;
+    hx = hf = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      xs[0][j] = x[j];
-      fs[0][j] = f0[j];
+      X(0, j) = x[j];
+      F(0, j) = f0[j];
     }
     int st = kOk;
     if constexpr (D >= 6) {
@@ -660,7 +708,7 @@ struct Propagator {
                      iters);
       if (true) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) x[j] = xs[0][j];
+        for (int j = 0; j < D; ++j) x[j] = X(0, j);
         return st;
       }
     }
@@ -675,7 +723,7 @@ struct Propagator {
         st = step<ORD, 4>(th, t0 + static_cast<double>(k) * h, h, tol, max_iter, gamma, iters);
     }
 #pragma unroll
-    for (int j = 0; j < D; ++j) x[j] = xs[0][j];
+    for (int j = 0; j < D; ++j) x[j] = X(0, j);
     return st;
   }
 };

@@ -35,7 +35,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-wide max (all threads get the result). scratch >= kWarps doubles.
+// Block-wide max (all threads get the result). scratch >= NT / 32 doubles.
+// NT: threads per block (kThreads unless a model's kernels use another size).
+template <int NT = kThreads>
 __device__ __forceinline__ double block_max(double v, double* scratch) {
   v = warp_max(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -44,12 +46,12 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   __syncthreads();
   double r = scratch[0];
 #pragma unroll
-  for (int i = 1; i < kWarps; ++i) r = nan_free_max(r, scratch[i]);
+  for (int i = 1; i < NT / 32; ++i) r = nan_free_max(r, scratch[i]);
   return r;
 }
 
-// Block-wide sums of V values; result valid in thread 0. scratch >= kWarps*V.
-template <int V>
+// Block-wide sums of V values; result valid in thread 0. scratch >= NT/32*V.
+template <int V, int NT = kThreads>
 __device__ __forceinline__ void block_sums(double (&v)[V], double* scratch) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
@@ -63,38 +65,39 @@ __device__ __forceinline__ void block_sums(double (&v)[V], double* scratch) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       double s = scratch[k];
-      for (int i = 1; i < kWarps; ++i) s += scratch[i * V + k];
+      for (int i = 1; i < NT / 32; ++i) s += scratch[i * V + k];
       v[k] = s;
     }
   }
 }
 
 // Block-wide sums through a shared-memory transpose (fewer instructions
-// than V shuffle trees): each thread stores its V values, then V*8 threads
-// each fold 32 entries of one value in order, then V threads fold the 8
+// than V shuffle trees): each thread stores its V values, then V*NW threads
+// each fold 32 entries of one value in order, then V threads fold the NW
 // chunk sums in order. Fixed shape => bitwise reproducible. Result in
-// thread 0's v[]. tsc >= V * kThreads doubles.
-template <int V>
+// thread 0's v[]. tsc >= V * NT doubles (V * NW <= NT).
+template <int V, int NT = kThreads>
 __device__ __forceinline__ void block_sums_smem(double (&v)[V], double* tsc) {
+  constexpr int NW = NT / 32;
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < V; ++k) tsc[k * kThreads + threadIdx.x] = v[k];
+  for (int k = 0; k < V; ++k) tsc[k * NT + threadIdx.x] = v[k];
   __syncthreads();
   double part = 0.0;
-  if (threadIdx.x < V * kWarps) {
-    const int k = threadIdx.x / kWarps, ch = threadIdx.x % kWarps;
-    const double* src = tsc + k * kThreads + ch * 32;
+  if (threadIdx.x < V * NW) {
+    const int k = threadIdx.x / NW, ch = threadIdx.x % NW;
+    const double* src = tsc + k * NT + ch * 32;
 #pragma unroll 8
     for (int i = 0; i < 32; ++i) part += src[i];
   }
   __syncthreads();
-  if (threadIdx.x < V * kWarps) tsc[threadIdx.x] = part;
+  if (threadIdx.x < V * NW) tsc[threadIdx.x] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-      double s = tsc[k * kWarps];
-      for (int i = 1; i < kWarps; ++i) s += tsc[k * kWarps + i];
+      double s = tsc[k * NW];
+      for (int i = 1; i < NW; ++i) s += tsc[k * NW + i];
       v[k] = s;
     }
   }
@@ -104,12 +107,12 @@ __device__ __forceinline__ void block_sums_smem(double (&v)[V], double* tsc) {
 // by e = exp(x - M) inside, the last one by e^2 when SQ). Thread 0 writes
 // (M, sums[V]) to out[0..V]. tsc: V * kThreads doubles of shared scratch
 // (null: shuffle trees, scratch >= kWarps * V).
-template <int V, bool SQ>
+template <int V, bool SQ, int NT = kThreads>
 __device__ __forceinline__ void block_partial(double x, const double (&vals)[V], double* out,
                                               double* scratch, double* tsc = nullptr) {
   const bool is_nan = isnan(x);
   const double leaf_max = is_nan ? -INFINITY : x;
-  const double M = block_max(leaf_max, scratch);
+  const double M = block_max<NT>(leaf_max, scratch);
   double e;
   if (is_nan)
     e = NAN;
@@ -121,9 +124,9 @@ __device__ __forceinline__ void block_partial(double x, const double (&vals)[V],
 #pragma unroll
   for (int k = 0; k < V; ++k) v[k] = ((SQ && k == V - 1) ? e * e : e) * vals[k];
   if (tsc)
-    block_sums_smem<V>(v, tsc);
+    block_sums_smem<V, NT>(v, tsc);
   else
-    block_sums<V>(v, scratch);
+    block_sums<V, NT>(v, scratch);
   if (threadIdx.x == 0) {
     out[0] = M;
 #pragma unroll
@@ -134,16 +137,16 @@ __device__ __forceinline__ void block_partial(double x, const double (&vals)[V],
 // Combine `count` partials (stride V+1) into one, by one block, fixed order:
 // thread t folds partials t, t+256, ... sequentially (rescaled), then a fixed
 // warp/block tree. Result in out[0..V] (thread 0 writes).
-template <int V, bool SQ>
+template <int V, bool SQ, int NT = kThreads>
 __device__ __forceinline__ void combine_partials(const double* in, int count, double* out,
                                                  double* scratch) {
   double m = -INFINITY;
-  for (int i = threadIdx.x; i < count; i += kThreads) m = nan_free_max(m, __ldcg(in + i * (V + 1)));
-  const double M = block_max(m, scratch);
+  for (int i = threadIdx.x; i < count; i += NT) m = nan_free_max(m, __ldcg(in + i * (V + 1)));
+  const double M = block_max<NT>(m, scratch);
   double v[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) v[k] = 0.0;
-  for (int i = threadIdx.x; i < count; i += kThreads) {
+  for (int i = threadIdx.x; i < count; i += NT) {
     const double mi = __ldcg(in + i * (V + 1));
     const double c = (mi == -INFINITY) ? 0.0 : exp(mi - M);
 #pragma unroll
@@ -152,7 +155,7 @@ __device__ __forceinline__ void combine_partials(const double* in, int count, do
       v[k] += w * __ldcg(in + i * (V + 1) + 1 + k);
     }
   }
-  block_sums<V>(v, scratch);
+  block_sums<V, NT>(v, scratch);
   if (threadIdx.x == 0) {
     out[0] = M;
 #pragma unroll
@@ -171,7 +174,7 @@ struct NoGroupHook {
 
 // hook(g, gsize) runs in the last block of group g after its group partial
 // is written (all of the group's block partials are visible).
-template <int V, bool SQ, class Hook = NoGroupHook>
+template <int V, bool SQ, class Hook = NoGroupHook, int NT = kThreads>
 __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_part,
                                                  unsigned* counters, double* final_out,
                                                  double* scratch, bool final_level = true,
@@ -192,8 +195,8 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials<V, SQ>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
-                          group_part + g * (V + 1), scratch);
+  combine_partials<V, SQ, NT>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
+                              group_part + g * (V + 1), scratch);
   __syncthreads();
   hook(g, gsize);
   if (!final_level) return false;  // sharded: the group partials are exported
@@ -207,7 +210,7 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials<V, SQ>(group_part, ngroups, final_out, scratch);
+  combine_partials<V, SQ, NT>(group_part, ngroups, final_out, scratch);
   __syncthreads();
   return true;
 }
@@ -221,7 +224,9 @@ struct SumCnt {
 // Block-wide exclusive scan of (sum, count) in a fixed shape: warp shuffle
 // scan, warp totals through smem, scanned by warp 0. Approximate sums only
 // (the bound in exact_cdf.cuh covers any tree); counts exact.
+template <int NT = kThreads>
 __device__ __forceinline__ SumCnt block_excl_scan_sc(SumCnt v, SumCnt& total, SumCnt* sw) {
+  constexpr int kWarps = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   SumCnt x = v;
 #pragma unroll

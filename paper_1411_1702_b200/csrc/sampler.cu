@@ -146,7 +146,7 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   }
   // NVTX ranges name the PhaseTimings phases (filter.hpp:93-99) the kernels replace
   nvtxRangePushA("propagate (k_predict)");
-  s->ks->predict(c, s->grid, st);
+  s->ks->predict(c, s->grid_m, st);
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[1], st));
   nvtxRangePushA("resample (exact CDF scan + ancestor search)");
@@ -161,7 +161,7 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[4], st));
   nvtxRangePushA("proliferate + repropagate + weights (k_update)");
-  s->ks->update(c, s->grid, st);
+  s->ks->update(c, s->grid_m, st);
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[5], st));
   CK(cudaGetLastError());
@@ -400,6 +400,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     s->world = world;
     s->N = static_cast<long long>(cfg->particles / world);
     s->grid = static_cast<int>((s->N + kThreads - 1) / kThreads);
+    s->grid_m = static_cast<int>((s->N + s->ks->kt - 1) / s->ks->kt);
     const int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
     s->ntiles = static_cast<int>((s->N + (1LL << tile_log2) - 1) >> tile_log2);
     Ctx& c = s->ctx;
@@ -452,6 +453,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
     c.tile_log2 = tile_log2;
+    c.k1_block_log2 = ilog2(s->ks->kt);
     // the ancestor search's tables (segment ends, guide): small, read with
     // an L2 evict-last policy so the one-shot gathers stream past them. (A
     // persisting access-policy window was measured: it cost the streaming
@@ -468,7 +470,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.tile0 = static_cast<int>(NT) * rank;
     c.gtile_info = s->dalloc<double2>(GNT);
     c.tile_info = c.gtile_info + c.tile0;
-    c.blk_cnt = s->dalloc<int>(static_cast<size_t>(s->grid));
+    c.blk_cnt = s->dalloc<int>(static_cast<size_t>(s->grid_m));
     c.trel = s->dalloc<double>(NT);
     c.tile_m = s->dalloc<double>(NT);
     c.trec = s->dalloc<ThreadRec>(NT * kThreads);
@@ -484,9 +486,9 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.shard_off = s->dalloc<double>(2);
     CK(cudaMemset(c.shard_off, 0, 2 * sizeof(double)));
     const int vmax = 1 + 4 + 10 + 8 + 1 + 1;
-    c.part = s->dalloc<double>(static_cast<size_t>(s->grid) * vmax + 64);
-    c.gpart = s->dalloc<double>(static_cast<size_t>(s->grid / kGroup + 2) * vmax + 64);
-    const int ngroups = (s->grid + kGroup - 1) / kGroup;
+    c.part = s->dalloc<double>(static_cast<size_t>(s->grid_m) * vmax + 64);
+    c.gpart = s->dalloc<double>(static_cast<size_t>(s->grid_m / kGroup + 2) * vmax + 64);
+    const int ngroups = (s->grid_m + kGroup - 1) / kGroup;
     unsigned* cnts = s->dalloc<unsigned>(2 * (ngroups + 1) + 8);
     CK(cudaMemset(cnts, 0, (2 * (ngroups + 1) + 8) * sizeof(unsigned)));
     c.cnt_pred = cnts;
@@ -501,7 +503,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     CK(cudaMallocHost(&s->sp_host, sizeof(StepParams)));
     CK(cudaMallocHost(&s->st_host, sizeof(DevState)));
     CK(cudaMallocHost(&s->trace_host, 64 * sizeof(double)));
-    s->ngroups_pred = (s->grid + kGroup - 1) / kGroup;
+    s->ngroups_pred = (s->grid_m + kGroup - 1) / kGroup;
     s->ngroups_upd = s->ngroups_pred;
     s->shard_api = shard_api;
     if (shard_api) {
@@ -563,7 +565,7 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     k_pack<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, d, p, tmp_x, tmp_t, 0);
     // shrink mean + chol(cov_u); sharded: the caller finishes it globally
     // (pfsmc_gpu_shard_moments + allgather + pfsmc_gpu_shard_finish_moments(0))
-    if (!s->shard_api) s->ks->moments(s->ctx, s->grid, s->stream, 0);
+    if (!s->shard_api) s->ks->moments(s->ctx, s->grid_m, s->stream, 0);
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     cudaFree(tmp_x);
@@ -620,8 +622,8 @@ static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vecto
     // first pass: mean about 0; second pass: cov about that mean (sharded:
     // the caller runs both passes globally)
     if (!s->shard_api) {
-      s->ks->moments(s->ctx, s->grid, s->stream, 1);
-      s->ks->moments(s->ctx, s->grid, s->stream, 1);
+      s->ks->moments(s->ctx, s->grid_m, s->stream, 1);
+      s->ks->moments(s->ctx, s->grid_m, s->stream, 1);
     }
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
@@ -715,7 +717,7 @@ pfsmc_gpu_status pfsmc_gpu_run(pfsmc_gpu_sampler* s, double* rows, int* warn) {
     if (s->shard_api) throw ConfigError("run: a shard handle runs only the sharded phases");
     const int w = 2 * s->p + s->d + 1;
     // row 0 from the current ensemble (filter.cpp:409-426)
-    s->ks->moments(s->ctx, s->grid, s->stream, 0);
+    s->ks->moments(s->ctx, s->grid_m, s->stream, 0);
     enqueue_readback(s);
     CK(cudaStreamSynchronize(s->stream));
     fill_trace(s, *s->st_host, s->xmean_host, rows);

@@ -97,6 +97,7 @@ struct pfsmc_gpu_sampler {
   int d = 0, p = 0;
   long long N = 0;
   int grid = 0, ntiles = 0;
+  int grid_m = 0;  // CTAs of the model kernels (predict / update / moments): N / ks->kt
   int num_sms = 148;
   Ctx ctx{};
   cudaStream_t stream = nullptr;

@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(kThreads) k_gin_tiles(Ctx c) {
     c.trel[blockIdx.x] = v[0];
     c.tile_cnt_pre[blockIdx.x] = static_cast<long long>(v[1]);
   }
-  const int ngroups = (c.ntiles * (tile / kThreads) + kGroup - 1) / kGroup;
+  const int ngroups = (c.ntiles * (tile >> c.k1_block_log2) + kGroup - 1) / kGroup;
   for (int g = blockIdx.x * kThreads + threadIdx.x; g < ngroups; g += gridDim.x * kThreads) c.gpart[2 * g] = 0.0;
 }
 

@@ -473,7 +473,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_offspring_pull(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     if (!s->have_peers) throw ConfigError("shard_offspring_pull: no peer table (attach_peers / attach_peers_local)");
     k_offspring_pull<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->peers, s->otot);
-    s->ks->update(s->ctx, s->grid, s->stream);
+    s->ks->update(s->ctx, s->grid_m, s->stream);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
@@ -519,7 +519,7 @@ static void shard_predict_impl(pfsmc_gpu_sampler* s, const double* y, uint64_t j
   *s->sp_host = sp;
   CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
   enqueue_prologue(s);
-  s->ks->predict(s->ctx, s->grid, s->stream);
+  s->ks->predict(s->ctx, s->grid_m, s->stream);
   CK(cudaGetLastError());
 }
 
@@ -606,7 +606,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv) {
     if (n_recv != static_cast<uint64_t>(s->N)) throw std::runtime_error("shard_update: payload count mismatch");
     ensure_exchange_buffers(s);
     k_place<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->recvbuf, static_cast<long long>(n_recv));
-    s->ks->update(s->ctx, s->grid, s->stream);
+    s->ks->update(s->ctx, s->grid_m, s->stream);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
@@ -614,7 +614,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv) {
 
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s) {
   return guarded([&] {
-    s->ks->moments(s->ctx, s->grid, s->stream, 1);
+    s->ks->moments(s->ctx, s->grid_m, s->stream, 1);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
@@ -783,7 +783,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_pull(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     if (!s->have_peers) throw ConfigError("shard_pull: no peer table (attach_peers / attach_peers_local)");
     k_pull<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->peers);
-    s->ks->update(s->ctx, s->grid, s->stream);
+    s->ks->update(s->ctx, s->grid_m, s->stream);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
@@ -798,7 +798,7 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
   cudaStream_t st = s->stream;
   const int W = s->world;
   enqueue_prologue(s);
-  s->ks->predict(c, s->grid, st);
+  s->ks->predict(c, s->grid_m, st);
   NCK(N.AllGather(c.gpart, s->gp_pred_all, 2 * static_cast<size_t>(s->ngroups_pred), ncclDouble, s->nccl, st));
   k_finish_lse<<<1, kThreads, 0, st>>>(c, s->gp_pred_all, s->ngroups_pred * W);
   NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
@@ -817,7 +817,7 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
     NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete everywhere
     k_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers);
   }
-  s->ks->update(c, s->grid, st);
+  s->ks->update(c, s->grid_m, st);
   const size_t Wm = static_cast<size_t>(s->ks->moment_width());
   NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));
   s->ks->finish_moments(c, s->gp_mom_all, s->ngroups_upd * W, 7, st);
@@ -935,7 +935,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
     NCK(N.GroupEnd());
     if (off != cap) throw std::runtime_error("shard_step: payload count mismatch");
     k_place<<<s->grid, kThreads, 0, st>>>(c, s->recvbuf, static_cast<long long>(off));
-    s->ks->update(c, s->grid, st);
+    s->ks->update(c, s->grid_m, st);
     // E: update-kernel moment partials -> global lse_w, moments, trace row, chol
     const size_t Wm = static_cast<size_t>(s->ks->moment_width());
     NCK(N.AllGather(c.gpart, s->gp_mom_all, Wm * s->ngroups_upd, ncclDouble, s->nccl, st));

@@ -86,6 +86,7 @@ struct Ctx {
   double rtol;       // adaptive BDF(1,2) tolerance (IntegratorSpec.rtol)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
+  int k1_block_log2;  // particles per predict CTA (KernelSet::kt), log2
   // ---- advection-diffusion model (grid m x m, d = m^2; kernels_advdiff.cu) ----
   int adv_m, adv_d;
   const double2* adv_tw;  // (cos, sin)(2 pi k / m), k < m
@@ -153,6 +154,7 @@ struct KernelSet {
   // the trace row in Ctx::xmean
   virtual bool block_model() const { return false; }
   int d = 0, p = 0;
+  int kt = 256;  // threads per CTA (= particles per CTA) of predict / update / moments
 };
 
 // One translation unit per model instantiates its 9 (family, order) kernel
