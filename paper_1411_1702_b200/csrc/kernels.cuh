@@ -412,7 +412,7 @@ struct MomentLayout {
 // Finalise (M, S, A, B, X, Q) into lse_w, mean, cov, trace, chol for the
 // next step; K is the shift the partials were taken about.
 template <class M>
-__device__ void finalize_moments(const Ctx& c, const double* fin, const double (&K)[M::P],
+__device__ __noinline__ void finalize_moments(const Ctx& c, const double* fin, const double (&K)[M::P],
                                  bool set_lse, bool set_cov) {
   using ML = MomentLayout<M>;
   constexpr int P = M::P, D = M::D;
@@ -461,7 +461,7 @@ __device__ void finalize_moments(const Ctx& c, const double* fin, const double (
 // operation order as the reference; sqrt and division are IEEE-exact, so L
 // is bitwise the reference's for the same C.
 template <int P>
-__device__ void chol_psd_device(DevState& st) {
+__device__ __noinline__ void chol_psd_device(DevState& st) {
   const double* C = st.cov;
   double trace = 0.0;
   for (int i = 0; i < P; ++i) trace += C[i * P + i];
@@ -546,12 +546,16 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
   if (n < c.N) {
     // survival of the fittest (filter.cpp:169-176): the ancestor's record and
     // ll_bar were gathered into slot order by k_serve (coalesced read here)
-    double x[D], tu[P], tb[P], th[P], gamma[D];
-    load_record<M>(c.payload, c.R + 2, n, x, tu);
+    // xr: the ancestor's state, propagated in place (on failure it is read
+    // again rather than kept live through the propagation)
+    double xr[D], tu[P], tb[P], th[P], gamma[D];
+    load_record<M>(c.payload, c.R + 2, n, xr, tu);
     const double llb = __ldg(&c.payload[n * (c.R + 2) + c.R]);
     // shrink of the ancestor (filter.cpp:118), proliferation (filter.cpp:185-196)
     double z[P];
-    stream_normals<P>(c.seed, sp.j, c.n0 + n, kProliferate, z);
+    // large models (d >= 6): Philox rounds as a loop (code size, not speed)
+    constexpr bool kRoll = D >= 6;
+    stream_normals<P, kRoll>(c.seed, sp.j, c.n0 + n, kProliferate, z);
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       tb[r] = c.a * tu[r] + c.one_minus_a * sK[r];
@@ -562,9 +566,6 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
       th[r] = exp(tb[r]);
     }
     // repropagate + innovate + log-lik (filter.cpp:351-365)
-    double xr[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) xr[k] = x[k];
     Propagator<M, FAM, ORD> prop;
     prop.mk = M::load_k(c.mconst);
     prop.bind_history(hist_smem + threadIdx.x);
@@ -576,13 +577,12 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
     double ll = kNegInf;
     if (status == kOk) {
       double zi[D];
-      stream_normals<D>(c.seed, sp.j, c.n0 + n, kInnovate, zi);
+      stream_normals<D, kRoll>(c.seed, sp.j, c.n0 + n, kInnovate, zi);
 #pragma unroll
       for (int k = 0; k < D; ++k) xr[k] += sqrt(gamma[k]) * zi[k];
       ll = loglik<M>(c, sp, xr);
     } else {
-#pragma unroll
-      for (int k = 0; k < D; ++k) xr[k] = x[k];
+      load_record<M>(c.payload, c.R + 2, n, xr, tu);  // the particle keeps its state
     }
     lwv = ll - llb;  // update_weights (filter.cpp:214)
     store_record<M>(c.rec[cur ^ 1], c.R, n, xr, tb);

@@ -47,24 +47,39 @@ struct U64x4 {
   uint64_t v[4];
 };
 
-// rng.cpp:28-41
+// rng.cpp:28-41. ROLL: the ten rounds as a loop (kernels whose code size
+// matters more than the loop overhead); same words.
+PF_HD void philox_round(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3, uint64_t k0, uint64_t k1) {
+  uint64_t hi0, lo0, hi1, lo1;
+  mulhilo64(kMult0, c0, hi0, lo0);
+  mulhilo64(kMult1, c2, hi1, lo1);
+  const uint64_t n0 = hi1 ^ c1 ^ k0;
+  const uint64_t n2 = hi0 ^ c3 ^ k1;
+  c0 = n0;
+  c1 = lo1;
+  c2 = n2;
+  c3 = lo0;
+}
+template <bool ROLL = false>
 PF_HD U64x4 philox4x64(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
                        uint64_t k0, uint64_t k1) {
-#pragma unroll
-  for (int round = 0; round < 10; ++round) {
-    if (round > 0) {
+  if constexpr (ROLL) {
+    philox_round(c0, c1, c2, c3, k0, k1);
+#pragma unroll 1
+    for (int round = 1; round < 10; ++round) {
       k0 += kWeyl0;
       k1 += kWeyl1;
+      philox_round(c0, c1, c2, c3, k0, k1);
     }
-    uint64_t hi0, lo0, hi1, lo1;
-    mulhilo64(kMult0, c0, hi0, lo0);
-    mulhilo64(kMult1, c2, hi1, lo1);
-    const uint64_t n0 = hi1 ^ c1 ^ k0;
-    const uint64_t n2 = hi0 ^ c3 ^ k1;
-    c0 = n0;
-    c1 = lo1;
-    c2 = n2;
-    c3 = lo0;
+  } else {
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+      if (round > 0) {
+        k0 += kWeyl0;
+        k1 += kWeyl1;
+      }
+      philox_round(c0, c1, c2, c3, k0, k1);
+    }
   }
   return {{c0, c1, c2, c3}};
 }
@@ -124,7 +139,7 @@ struct Stream {
 // RngStream::next_normal returns them (rng.cpp:61-75): pair q uses words 2q
 // (u1) and 2q+1 (u2) and yields r cos, then the cached r sin. All indices are
 // compile-time, so nothing spills to local memory.
-template <int K>
+template <int K, bool ROLL = false>
 PF_HD void stream_normals(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpose,
                           double (&out)[K]) {
   constexpr int kPairs = (K + 1) / 2;
@@ -132,7 +147,7 @@ PF_HD void stream_normals(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpos
   uint64_t w[kBlocks * 4];
 #pragma unroll
   for (int b = 0; b < kBlocks; ++b) {
-    const U64x4 blk = philox4x64(static_cast<uint64_t>(b), j, n, purpose, seed, kKeyConstant);
+    const U64x4 blk = philox4x64<ROLL>(static_cast<uint64_t>(b), j, n, purpose, seed, kKeyConstant);
 #pragma unroll
     for (int l = 0; l < 4; ++l) w[4 * b + l] = blk.v[l];
   }

@@ -163,6 +163,21 @@ __device__ __forceinline__ void combine_partials(const double* in, int count, do
   }
 }
 
+// combine_partials out of line: the last-block paths of kernels with many
+// moment values (their unrolled shuffle trees would otherwise sit in the
+// middle of the hot kernel's code).
+template <int V, bool SQ, int NT>
+__device__ __noinline__ void combine_partials_cold(const double* in, int count, double* out, double* scratch) {
+  combine_partials<V, SQ, NT>(in, count, out, scratch);
+}
+template <int V, bool SQ, int NT>
+__device__ __forceinline__ void combine_partials_sel(const double* in, int count, double* out, double* scratch) {
+  if constexpr (V >= 16)
+    combine_partials_cold<V, SQ, NT>(in, count, out, scratch);
+  else
+    combine_partials<V, SQ, NT>(in, count, out, scratch);
+}
+
 // Two-level last-block-done tree. Every block calls this after writing its
 // partial at part[blockIdx.x*(V+1)]; returns true in exactly one block (the
 // last), where `final_out` holds the grand partial (thread 0 wrote it, and a
@@ -195,8 +210,8 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials<V, SQ, NT>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
-                              group_part + g * (V + 1), scratch);
+  combine_partials_sel<V, SQ, NT>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
+                                  group_part + g * (V + 1), scratch);
   __syncthreads();
   hook(g, gsize);
   if (!final_level) return false;  // sharded: the group partials are exported
@@ -210,7 +225,7 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials<V, SQ, NT>(group_part, ngroups, final_out, scratch);
+  combine_partials_sel<V, SQ, NT>(group_part, ngroups, final_out, scratch);
   __syncthreads();
   return true;
 }
