@@ -209,13 +209,15 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const do
 
 // ---------------------------------------------------------------- K1
 // CTAs per SM the model's K1 / K3 are built for (launch bounds)
+// (measured per model at 256 threads, scaled to the model's CTA size; the
+// shared-memory-history chain: 3 CTAs of 128)
 template <class M>
 constexpr int k1_min_blocks() {
-  return BlockOf<M>::value == 128 ? 3 : M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1;
+  return SmemHistOf<M>::value ? 3 : (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1) * (kThreads / BlockOf<M>::value);
 }
 template <class M>
 constexpr int k3_min_blocks() {
-  return BlockOf<M>::value == 128 ? 3 : M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1;
+  return SmemHistOf<M>::value ? 3 : (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1) * (kThreads / BlockOf<M>::value);
 }
 // Dynamic shared memory of a K1 / K3 CTA: the LMM history columns.
 template <class M, int FAM, int ORD>
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
   constexpr int V = ML::V;
   __shared__ double scratch[KT / 32 * V];
   __shared__ double fin[V + 1];  // M + V values
-  __shared__ double sL[P * P], sK[P];
+
   constexpr int kTsc = V <= 12 ? V * KT : 1;
   __shared__ double tsc[kTsc];
   extern __shared__ double hist_smem[];
@@ -532,9 +534,11 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
     if (threadIdx.x == 0) atomicOr(&st.error, kErrChol);
     return;
   }
-  if (threadIdx.x < P * P) sL[threadIdx.x] = st.L[threadIdx.x];
-  if (threadIdx.x < P) sK[threadIdx.x] = st.mu[threadIdx.x];
-  __syncthreads();
+  // the shrink mean and chol(C) of the previous step: every thread reads the
+  // same few words (L1 broadcast), no block barrier before the work starts;
+  // only the last block rewrites them, after every block's reads
+  const double* sL = st.L;
+  const double* sK = st.mu;
   const StepParams& sp = *c.sp;  // read fields in place (no local copy)
   const int cur = st.cur;
   const long long n = static_cast<long long>(blockIdx.x) * KT + threadIdx.x;
