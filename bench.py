@@ -640,6 +640,8 @@ def run_sharded(args, world, rank, local):
     from paper_1411_1702_b200.sharded import GpuShard, ShardedFilter, TorchComm
 
     cfgno = args.config
+    if cfgno == 5:
+        return run_sharded_c5(args, world, rank, local)
     if cfgno == 2:    # LV, N = 2^20 per GPU (weak scaling)
         n_local = args.particles
         prob = problems.lotka_volterra(particles=n_local * world, T=T_OBS, seed=1)
@@ -653,7 +655,7 @@ def run_sharded(args, world, rank, local):
         prob = problems.chain8(particles=n_local * world, T=args.warmup + args.steps + 1, seed=1)
         model, scaling, j_start = "chain", "strong", 0
     else:
-        raise SystemExit("--config must be 2, 3 or 4 for the sharded filter (config 5: --config 5 single GPU)")
+        raise SystemExit("--config must be 2, 3, 4 or 5")
     shard = GpuShard(model, _cfg(prob), prob.obs, rank, world, device=local)
     f = ShardedFilter([shard], TorchComm(), mode=args.shard_mode)
     prob.init(f)
@@ -729,6 +731,98 @@ def run_sharded(args, world, rank, local):
                     "path": "ShardedFilter.pf_step (host y in, trace out)"},
             "clocks": clk.summary(),
             "final_trace": {"theta_mean": list(map(float, row.theta_mean)), "ess": float(row.ess)}}
+    if rank == 0:
+        print(json.dumps(line))
+    shard.close()
+    dist.destroy_process_group()
+    return 0
+
+
+def run_sharded_c5(args, world, rank, local):
+    """BASELINE config 5 over N GPUs: 2^25 64-byte records per GPU (weak
+    scaling, 2^28 at N = 8), one global resample / reduction iteration per
+    step: LSE + weighted 2x2 covariance (group partials allgathered), the
+    exact scan over all shards, the exact multinomial and the gather with the
+    records of other GPUs pulled over NVLink peer memory (exact migration).
+    Device time per iteration (CUDA events, max over ranks); NVLink bytes from
+    the device count of records pulled from other GPUs."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1411_1702_b200.sampler import Ensemble, ObservationModel, PfConfig
+    from paper_1411_1702_b200.sharded import GpuShard, ShardedFilter, TorchComm
+
+    n_local = 1 << 25 if args.particles == N_PER_GPU else args.particles
+    shard = GpuShard("payload64", PfConfig(particles=n_local * world, seed=5), ObservationModel([0], 1.0), rank, world,
+                     device=local)
+    f = ShardedFilter([shard], TorchComm(), pull=True)
+    rng = np.random.default_rng(1000 + rank)
+    shard.set_ensemble(Ensemble(rng.standard_normal((n_local, 6)), rng.standard_normal((n_local, 2)),
+                                np.zeros(n_local), np.zeros(2), np.eye(2)))
+    f._refresh(0)  # the global shrink mean of the injected records
+    shard.attach_nccl()
+    peers = shard.attach_peers()
+    if not peers:
+        raise SystemExit("config 5 sharded: the peer-memory mapping failed")
+    stream = shard.stream()
+    res = {}
+    total_all, remote_all, its_all = 0.0, 0, 0
+    with ClockSampler(local) as clk:
+        for sigma in (0.1, 1.0, 4.0):
+            shard.c5_set_logweights(sigma, 1)
+            for it in range(args.warmup):
+                f.c5_iteration(it + 1)
+            shard.synchronize()
+            r0 = shard.c5_remote_pulls()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            dist.barrier()
+            torch.cuda.synchronize()
+            for k in range(args.steps):
+                shard.flush_l2()
+                with torch.cuda.stream(stream):
+                    ev[k][0].record(stream)
+                f.c5_iteration(args.warmup + k + 1)
+                with torch.cuda.stream(stream):
+                    ev[k][1].record(stream)
+            shard.synchronize()
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in ev)
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            remote = shard.c5_remote_pulls() - r0
+            rt = torch.tensor([remote], dtype=torch.int64, device=f"cuda:{local}")
+            dist.all_reduce(rt)
+            remote = int(rt.item())
+            per_it = ms / args.steps
+            res[f"sigma={sigma}"] = {
+                "ms_per_iteration": per_it,
+                "particle_iterations_per_s": n_local * world / (per_it / 1e3),
+                "hbm_gbs_per_gpu_algorithmic": 184.0 * n_local / (per_it / 1e3) / 1e9,
+                "remote_records_per_iteration": remote / args.steps,
+                "nvlink_record_gbs_per_gpu": 64.0 * remote / args.steps / world / (per_it / 1e3) / 1e9}
+            total_all += ms
+            remote_all += remote
+            its_all += args.steps
+    per_it = total_all / its_all
+    peaks, peak_kind = _peaks()
+    hbm = float(peaks["hbm_gbs"])
+    value = n_local * world / (per_it / 1e3)
+    gbs = 184.0 * n_local / (per_it / 1e3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "particle-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_it, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (N(0,1) records, lw ~ N(0, sigma^2))",
+            "config": {"workload": "BASELINE config 5: resample/reduction bandwidth microbenchmark",
+                       "particles_per_gpu": n_local, "global_particles": n_local * world, "record_bytes": 64,
+                       "sigmas": [0.1, 1.0, 4.0], "l2": "flushed between timed iterations",
+                       "parallelism": f"sharded x{world}: group-partial allgathers, exact scan over all shards, "
+                                      "exact-mode migration pulled over NVLink peer memory"},
+            "roofline": {"bound": "hbm", "kernel": "whole iteration", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": gbs / hbm, "traffic": None, "bytes_per_particle": 184, "peak_source": peak_kind},
+            "nvlink_record_gbs_per_gpu": 64.0 * remote_all / its_all / world / (per_it / 1e3) / 1e9,
+            "results": res, "gpu_launches": 8 * its_all, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line))
     shard.close()

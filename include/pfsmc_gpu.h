@@ -255,7 +255,8 @@ pfsmc_gpu_status pfsmc_gpu_flush_l2(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_create_shard(const pfsmc_gpu_config* cfg, int rank, int world,
                                         pfsmc_gpu_sampler** out);
 /* Device pointer + size of exchange buffer `which` (see the sequence above;
- * 4/5 are global arrays whose own slice starts at rank * bytes / world). */
+ * 4/5 are global arrays whose own slice starts at rank * bytes / world;
+ * 12/13: the config-5 stats group partials, own / all ranks). */
 pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** ptr,
                                         uint64_t* bytes);
 pfsmc_gpu_status pfsmc_gpu_shard_predict(pfsmc_gpu_sampler* s, const double* y, uint64_t j,
@@ -331,6 +332,27 @@ pfsmc_gpu_status pfsmc_gpu_shard_offspring_pull(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */
 pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out);
+
+/* BASELINE config 5 over several GPUs (PAYLOAD64 shard handles, particles per
+ * shard a multiple of 64 exact-CDF tiles): one resample / reduction iteration
+ * of the global ensemble, exact migration (every slot's ancestor is the
+ * single handle's, bitwise; its 64-byte record is pulled over NVLink peer
+ * memory when another GPU holds it). Phase by phase:
+ *   shard_c5_stats -> allgather buf 12 into 13 -> shard_c5_finish
+ *     (global log-sum-exp, weighted mean / covariance: the single handle's
+ *      group partials combined in the same order)
+ *   allgather buf 2 into 3 -> shard_scan_records
+ *   allgather the own slices of bufs 4, 5 -> shard_resolve
+ *   allgather buf 2 into 3 (every rank's CDF tables complete) -> shard_c5_pull(j)
+ *   (every rank's pull done) -> shard_c5_flip
+ * or natively (NCCL attached, peers attached): shard_c5_iteration(j). */
+pfsmc_gpu_status pfsmc_gpu_shard_c5_stats(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_c5_finish(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_c5_pull(pfsmc_gpu_sampler* s, uint64_t j);
+pfsmc_gpu_status pfsmc_gpu_shard_c5_flip(pfsmc_gpu_sampler* s);
+pfsmc_gpu_status pfsmc_gpu_shard_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
+/* Records this rank pulled from other GPUs so far (64 bytes each over NVLink). */
+pfsmc_gpu_status pfsmc_gpu_shard_c5_remote_pulls(pfsmc_gpu_sampler* s, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -24,20 +24,47 @@ __global__ void __launch_bounds__(kThreads) k_c5_weights(Ctx c, double sigma, un
 // exact scan's tile offsets. A grid of a few blocks per SM loops over the
 // exact-CDF tiles; each thread's ITEMS (lw, theta) loads are all in flight
 // before the tile's partial: M_t = max lw, then sums of e = exp(lw - M_t)
-// times (1, d0, d1, d0 d0, d0 d1, d1 d1) and the finite count. The block
-// folds its tiles in order (combine_partials' rescaling rule); the last block
-// combines the block partials in a fixed order. Bitwise reproducible.
-template <int ITEMS>
+// times (1, d0, d1, d0 d0, d0 d1, d1 d1) and the finite count. The partials
+// combine in a fixed two-level tree that does not depend on the grid: groups
+// of kC5Group consecutive tiles (combined by the block that finishes a
+// group's last tile), then the groups in order (by the block that finishes
+// the last group). Bitwise reproducible, and a shard whose range is whole
+// groups exports exactly the single handle's group partials (SHARDED: the
+// final level runs in k_c5_finish over every rank's groups).
+constexpr int kC5Group = 64;  // tiles per group partial
+constexpr int kC5V = 6;       // S, A0, A1, B00, B01, B11 (partial = M + 6)
+
+__device__ __forceinline__ void c5_finalize(const Ctx& c, const double* fin, double k0, double k1,
+                                            double* s_lse) {
+  DevState& st = *c.st;
+  const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
+  st.lse_g = lse;
+  if (!isfinite(lse)) atomicOr(&st.error, kErrPredict);
+  *s_lse = lse;
+  const double S = fin[1];
+  const double m0 = fin[2] / S, m1 = fin[3] / S;
+  st.mu[0] = k0 + m0;
+  st.mu[1] = k1 + m1;
+  st.cov[0] = fin[4] / S - m0 * m0;
+  st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
+  st.cov[3] = fin[6] / S - m1 * m1;
+}
+
+template <int ITEMS, int SHARDED>
 __global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
   constexpr int kTileT = ITEMS * kThreads;
   constexpr int V = 7;  // S, A0, A1, B00, B01, B11, finite count
   __shared__ double scratch[kWarps * V];
-  __shared__ double fin[V];
-  __shared__ int s_last;
+  __shared__ double fin[kC5V + 1];
+  __shared__ int s_flag;
+  __shared__ double s_lse;
   if (grid_error(c)) return;
   DevState& st = *c.st;
   const double k0 = st.mu[0], k1 = st.mu[1];
   const double* rec = c.rec[st.cur];
+  const int ngroups = (c.ntiles + kC5Group - 1) / kC5Group;
+  double* tpart = c.part + static_cast<size_t>(c.ntiles) * (kC5V + 1);  // per-tile partials
+  unsigned* gcnt = c.cnt_upd;                                            // [ngroups] + [final]
   for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
     const long long base = static_cast<long long>(t) * kTileT;
     double x[ITEMS];
@@ -67,55 +94,62 @@ __global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
       v[6] += isfinite(x[i]) ? 1.0 : 0.0;
     }
     block_sums<V>(v, scratch);
+    const int g = t / kC5Group;
+    const int gsize = min(kC5Group, c.ntiles - g * kC5Group);
     if (threadIdx.x == 0) {
-      double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;  // per-tile partial (after the block slots)
+      double* tp = tpart + static_cast<size_t>(t) * (kC5V + 1);
       tp[0] = M;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) tp[1 + k] = v[k];
+      for (int k = 0; k < kC5V; ++k) tp[1 + k] = v[k];
       c.trel[t] = v[0];
       c.tile_m[t] = M;
       c.tile_cnt_pre[t] = static_cast<long long>(v[6]);
+      __threadfence();
+      const unsigned old = atomicAdd(&gcnt[g], 1u);
+      s_flag = old == static_cast<unsigned>(gsize - 1);
+      if (s_flag) gcnt[g] = 0;
     }
-  }
-  if (threadIdx.x == 0) {
-    // this block's partial over its tiles, in tile order
-    double M = -INFINITY;
-    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) M = nan_free_max(M, c.tile_m[t]);
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-      const double* tp = c.part + static_cast<size_t>(c.ntiles + t) * V;
-      const double w = tp[0] == -INFINITY ? 0.0 : exp(tp[0] - M);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) acc[k] += w * tp[1 + k];
+    __syncthreads();
+    if (s_flag) {  // block-uniform: this block completed group g
+      __threadfence();
+      combine_partials<kC5V, false>(tpart + static_cast<size_t>(g) * kC5Group * (kC5V + 1), gsize,
+                                    c.gpart + static_cast<size_t>(g) * (kC5V + 1), scratch);
+      __syncthreads();
+      if (!SHARDED) {
+        if (threadIdx.x == 0) {
+          __threadfence();
+          const unsigned old = atomicAdd(&gcnt[ngroups], 1u);
+          s_flag = old == static_cast<unsigned>(ngroups - 1);
+          if (s_flag) gcnt[ngroups] = 0;
+        }
+        __syncthreads();
+        if (s_flag) {  // the last group: the final level, then the tile offsets
+          __threadfence();
+          combine_partials<kC5V, false>(c.gpart, ngroups, fin, scratch);
+          __syncthreads();
+          if (threadIdx.x == 0) c5_finalize(c, fin, k0, k1, &s_lse);
+          __syncthreads();
+          if (isfinite(s_lse)) tile_prefixes(c, s_lse, c.tile_m);
+        }
+      }
     }
-    double* bp = c.part + static_cast<size_t>(blockIdx.x) * V;
-    bp[0] = M;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) bp[1 + k] = acc[k];
-    __threadfence();
-    const unsigned old = atomicAdd(&c.cnt_scan[3], 1u);
-    s_last = (old == gridDim.x - 1);
-    if (s_last) c.cnt_scan[3] = 0;
+    __syncthreads();
   }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  combine_partials<6, false>(c.part, gridDim.x, fin, scratch);
-  __syncthreads();
+}
+
+// Sharded: every rank combines every rank's group partials (global group
+// order = rank order) exactly as the single handle's final level, then its
+// own tiles' offsets and its approximate total (phase B).
+__global__ void __launch_bounds__(kThreads) k_c5_finish(Ctx c, const double* gall, int ngroups_all) {
+  __shared__ double scratch[kWarps * 7];
+  __shared__ double fin[kC5V + 1];
   __shared__ double s_lse;
-  if (threadIdx.x == 0) {
-    const double lse = isfinite(fin[0]) ? fin[0] + log(fin[1]) : kNegInf;
-    st.lse_g = lse;
-    if (!isfinite(lse)) atomicOr(&st.error, kErrPredict);
-    s_lse = lse;
-    const double S = fin[1];
-    const double m0 = fin[2] / S, m1 = fin[3] / S;
-    st.mu[0] = k0 + m0;
-    st.mu[1] = k1 + m1;
-    st.cov[0] = fin[4] / S - m0 * m0;
-    st.cov[1] = st.cov[2] = fin[5] / S - m0 * m1;
-    st.cov[3] = fin[6] / S - m1 * m1;
-  }
+  if (grid_error(c)) return;
+  const double k0 = c.st->mu[0], k1 = c.st->mu[1];
+  __syncthreads();
+  combine_partials<kC5V, false>(gall, ngroups_all, fin, scratch);
+  __syncthreads();
+  if (threadIdx.x == 0) c5_finalize(c, fin, k0, k1, &s_lse);
   __syncthreads();
   if (isfinite(s_lse)) tile_prefixes(c, s_lse, c.tile_m);
 }
@@ -305,6 +339,41 @@ __global__ void __launch_bounds__(kThreads) k_c5_bucket_anc(Ctx c, C5Buckets b, 
   c.anc[b.n[at + threadIdx.x]] = b.anc[at + threadIdx.x];
 }
 
+// Sharded config 5, exact migration over NVLink peer memory: slot n (global
+// n0 + n) draws its uniform, finds its serving rank from the exact global
+// shard ranges, searches that rank's CDF tables and copies that rank's
+// 64-byte record straight into this rank's next record buffer (four lanes per
+// record). remote counts the records that crossed GPUs (NVLink bytes).
+__global__ void __launch_bounds__(kThreads) k_c5_pull(Ctx c, PeerTable pt, unsigned long long j,
+                                                      unsigned long long* remote) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const bool mine = n < c.N;
+  const double u = mine ? resample_uniform(c.seed, j, c.n0 + n) : -1.0;
+  const int r = mine ? serving_rank(c, u) : 0;
+  const int ntl = c.ntiles;
+  const SearchView v{pt.coarse[r], pt.seg_end[r], pt.cdf[r], c.gtile_info[(r + 1) * ntl - 1].y};
+  const unsigned a = find_ancestor_warp_view(c, v, u);
+  if (mine) c.anc[n] = static_cast<unsigned>(static_cast<long long>(r) * c.N + a);
+  const unsigned far = __ballot_sync(0xffffffffu, mine && r != c.rank);
+  if ((threadIdx.x & 31) == 0 && far) atomicAdd(remote, static_cast<unsigned long long>(__popc(far)));
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const int cur = c.st->cur;
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+#pragma unroll
+  for (int q = 0; q < 32; q += 8) {
+    const int slot = q + lane / 4, part = lane & 3;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const int rs = __shfl_sync(0xffffffffu, r, slot);
+    const long long ns = wbase + slot;
+    if (ns < c.N) {
+      const double2* src = reinterpret_cast<const double2*>(cur ? pt.rec1[rs] : pt.rec0[rs]);
+      dst[ns * 4 + part] = __ldcg(src + static_cast<long long>(as) * 4 + part);
+    }
+  }
+}
+
 __global__ void k_flip(DevState* st) { st->cur ^= 1; }
 
 // FP64 roofline denominator: 8 independent DFMA chains per thread.
@@ -343,6 +412,70 @@ __global__ void __launch_bounds__(kThreads) k_gather_peak(const double2* __restr
     const long long ns = wbase + slot;
     if (ns < n_rec) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
   }
+}
+
+// ---- sharded config 5 (one global iteration over every GPU's records) ----
+int c5_shard_groups(const pfsmc_gpu_sampler* s) { return (s->ntiles + kC5Group - 1) / kC5Group; }
+double* c5_group_all(pfsmc_gpu_sampler* s) {
+  if (!s->c5_gall) {
+    s->c5_gall = s->dalloc<double>(static_cast<size_t>(7) * c5_shard_groups(s) * s->world);
+    s->c5_remote = s->dalloc<unsigned long long>(1);
+    CK(cudaMemset(s->c5_remote, 0, sizeof(unsigned long long)));
+  }
+  return s->c5_gall;
+}
+
+static void c5_shard_check(pfsmc_gpu_sampler* s) {
+  if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+  if (!s->shard_api) throw ConfigError("c5 shard phases: not a sharded handle");
+  if (s->ntiles % kC5Group != 0)
+    throw ConfigError("c5 sharded: particles per shard must be a multiple of 64 exact-CDF tiles");
+  c5_group_all(s);
+}
+
+static void c5_launch_stats(pfsmc_gpu_sampler* s, const Ctx& c, bool sharded) {
+  // one wave: 126 (ITEMS 16) / 74 (ITEMS 8) registers => 2 / 3 blocks per SM
+  if (c.tile_log2 == 11) {
+    const int g = std::min(s->ntiles, s->num_sms * 3);
+    if (sharded) k_c5_stats<8, 1><<<g, kThreads, 0, s->stream>>>(c);
+    else k_c5_stats<8, 0><<<g, kThreads, 0, s->stream>>>(c);
+  } else {
+    const int g = std::min(s->ntiles, s->num_sms * 2);
+    if (sharded) k_c5_stats<16, 1><<<g, kThreads, 0, s->stream>>>(c);
+    else k_c5_stats<16, 0><<<g, kThreads, 0, s->stream>>>(c);
+  }
+}
+
+static Ctx c5_ctx(pfsmc_gpu_sampler* s) {
+  Ctx c = s->ctx;
+  c.lg = c.lw;  // the fitness log-weights are the log-weights here
+  return c;
+}
+
+// The device part of one sharded iteration with NCCL collectives and the
+// peer pull.
+static void enqueue_c5_shard_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
+  const NcclApi& N = nccl_api();
+  const Ctx c = c5_ctx(s);
+  cudaStream_t st = s->stream;
+  const size_t G = static_cast<size_t>(c5_shard_groups(s));
+  CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), st));
+  c5_launch_stats(s, c, true);
+  NCK(N.AllGather(c.gpart, s->c5_gall, 7 * G, ncclDouble, s->nccl, st));                      // A
+  k_c5_finish<<<1, kThreads, 0, st>>>(c, s->c5_gall, static_cast<int>(G) * s->world);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));                      // B
+  launch_shard_offset(c, s->sums_all, st);
+  launch_scan(c, s->ntiles, st, 4);
+  NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));  // C
+  NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8, s->nccl,
+                  st));
+  launch_scan(c, s->ntiles, st, 5);
+  launch_scan(c, s->ntiles, st, 2);
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every rank's tables complete
+  k_c5_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers, j, s->c5_remote);                      // D
+  NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every pull done before the flip
+  k_flip<<<1, 1, 0, st>>>(s->st);
+  CK(cudaMemcpyAsync(&s->st_host->error, &s->st->error, sizeof(int), cudaMemcpyDeviceToHost, st));
 }
 
 int c5_bpb(const C5Buckets& b) { return static_cast<int>((b.cap + kThreads - 1) / kThreads); }
@@ -403,9 +536,9 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
     // one wave: 126 (ITEMS 16) / 74 (ITEMS 8) registers => 2 / 3 blocks per SM
     if (c.tile_log2 == 11)
-      k_c5_stats<8><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
+      k_c5_stats<8, 0><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
     else
-      k_c5_stats<16><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
+      k_c5_stats<16, 0><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
     launch_scan(c, s->ntiles, s->stream, 1);
     launch_scan(c, s->ntiles, s->stream, 2);
     if (s->c5_search == PFSMC_GPU_C5_SEARCH_BUCKETED) {
@@ -433,6 +566,77 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
     k_flip<<<1, 1, 0, s->stream>>>(s->st);
     // the error word reaches the host with the next pfsmc_gpu_synchronize
     CK(cudaMemcpyAsync(&s->st_host->error, &s->st->error, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// ---- sharded config 5: phases (any orchestration) and the native iteration
+pfsmc_gpu_status pfsmc_gpu_shard_c5_stats(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    c5_shard_check(s);
+    s->c5_fitness_is_lw = true;
+    CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
+    c5_launch_stats(s, c5_ctx(s), true);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_c5_finish(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    c5_shard_check(s);
+    k_c5_finish<<<1, kThreads, 0, s->stream>>>(c5_ctx(s), s->c5_gall, c5_shard_groups(s) * s->world);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Phase D of the sharded iteration over peer memory (every rank's CDF tables
+// complete, peers attached), then the buffer flip. The caller orders the flip
+// after every rank's pull before the next iteration overwrites a record buffer.
+pfsmc_gpu_status pfsmc_gpu_shard_c5_pull(pfsmc_gpu_sampler* s, uint64_t j) {
+  return guarded([&] {
+    c5_shard_check(s);
+    if (!s->have_peers) throw ConfigError("shard_c5_pull: no peer table (attach_peers / attach_peers_local)");
+    k_c5_pull<<<s->grid, kThreads, 0, s->stream>>>(c5_ctx(s), s->peers, j, s->c5_remote);
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_shard_c5_flip(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    c5_shard_check(s);
+    k_flip<<<1, 1, 0, s->stream>>>(s->st);
+    CK(cudaMemcpyAsync(&s->st_host->error, &s->st->error, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaGetLastError());
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Records this rank pulled from other GPUs since the handle was created
+// (NVLink traffic of the migration = 64 bytes each, plus the searches).
+pfsmc_gpu_status pfsmc_gpu_shard_c5_remote_pulls(pfsmc_gpu_sampler* s, uint64_t* out) {
+  return guarded([&] {
+    c5_shard_check(s);
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, s->c5_remote, sizeof(v), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *out = v;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// One config-5 iteration of the global ensemble (enqueue only; errors at the
+// next pfsmc_gpu_synchronize): the five phases with NCCL collectives in
+// between and the migration pulled over NVLink peer memory.
+pfsmc_gpu_status pfsmc_gpu_shard_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
+  return guarded([&] {
+    c5_shard_check(s);
+    if (!s->nccl) throw ConfigError("shard_c5_iteration: attach_nccl first");
+    if (!s->have_peers) throw ConfigError("shard_c5_iteration: attach_peers first");
+    enqueue_c5_shard_iteration(s, j);  // eager: 9 launches + 7 collectives per ~ms iteration
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });

@@ -326,6 +326,18 @@ struct SearchView {
   double end;  // the shard's exact CDF end (its last tile's end)
 };
 
+// The rank whose exact-CDF range [start_r, end_r) holds u (sharded filter;
+// gtile_info holds every rank's tiles' exact (start, end)).
+__device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
+  const int ntl = c.ntiles;
+  for (int r = 0; r < c.world; ++r) {
+    const double lo = c.gtile_info[r * ntl].x;
+    const double hi = c.gtile_info[(r + 1) * ntl - 1].y;
+    if (u >= lo && u < hi) return r;
+  }
+  return c.world - 1;  // unreachable: the last range ends at the guarded cdf >= 1 > u
+}
+
 // find_segment + the segment count over an explicit view (scalar form).
 __device__ __forceinline__ unsigned find_ancestor_view(const Ctx& c, const SearchView& v, double u) {
   constexpr int seg_log2 = kSegLog2;
@@ -353,6 +365,65 @@ __device__ __forceinline__ unsigned find_ancestor_view(const Ctx& c, const Searc
   int cnt = 0;
   for (long long k = k0; k < k1; ++k) cnt += __ldcg(&v.cdf[k]) <= u;
   return static_cast<unsigned>(min(k0 + cnt, static_cast<long long>(c.N) - 1));
+}
+
+// Warp-cooperative search over per-lane views (each lane's serving shard,
+// possibly a peer GPU): the segment bracket per lane as find_ancestor_view,
+// then the 64-byte segment counts spread over four lanes per segment as in
+// find_ancestor_warp. Every lane must call it (lanes without a slot: u < 0).
+__device__ __forceinline__ unsigned find_ancestor_warp_view(const Ctx& c, const SearchView& v, double u) {
+  constexpr int SEGL2 = kSegLog2;
+  constexpr int P = 1 << (SEGL2 - 1);
+  constexpr int S = 32 / P;
+  const int lane = threadIdx.x & 31;
+  const long long N = c.N;
+  long long k0 = 0;
+  if (u >= 0.0) {
+    const long long nseg = (N + (1 << SEGL2) - 1) >> SEGL2;
+    const long long nb = 1LL << c.coarse_bits;
+    long long b = static_cast<long long>(scale2(u, c.coarse_bits));
+    b = min(max(b, 0LL), nb - 1);
+    long long lo = __ldcg(&v.coarse[b]);
+    long long hi = nseg - 1;
+    if (b + 1 < nb) {
+      const double edge = scale2(static_cast<double>(b + 1), -c.coarse_bits);
+      if (edge < v.end) hi = min(hi, static_cast<long long>(__ldcg(&v.coarse[b + 1])));
+    }
+    lo = min(lo, hi);
+    while (hi - lo > 4) {
+      const long long mid = (lo + hi) >> 1;
+      if (__ldcg(&v.seg_end[mid]) > u)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    while (lo < hi && __ldcg(&v.seg_end[lo]) <= u) ++lo;
+    k0 = lo << SEGL2;
+  }
+  const unsigned long long cdf_bits = reinterpret_cast<unsigned long long>(v.cdf);
+  int mine = 0;
+#pragma unroll
+  for (int q = 0; q < 32; q += S) {
+    const int src = q + lane / P;
+    const long long ks = __shfl_sync(0xffffffffu, k0, src);
+    const double us = __shfl_sync(0xffffffffu, u, src);
+    const double* cdf = reinterpret_cast<const double*>(__shfl_sync(0xffffffffu, cdf_bits, src));
+    const long long kk = ks + 2 * (lane % P);
+    int cnt = 0;
+    if (us >= 0.0) {
+      if (kk + 1 < N) {
+        const double2 w = __ldcg(reinterpret_cast<const double2*>(cdf + kk));
+        cnt = (w.x <= us) + (w.y <= us);
+      } else if (kk < N) {
+        cnt = __ldcg(&cdf[kk]) <= us;
+      }
+    }
+#pragma unroll
+    for (int o = P / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const int got = __shfl_sync(0xffffffffu, cnt, ((lane - q) & (S - 1)) * P);
+    if (lane >= q && lane < q + S) mine = got;
+  }
+  return static_cast<unsigned>(min(k0 + mine, N - 1));
 }
 
 // Scalar form (one thread, one slot).

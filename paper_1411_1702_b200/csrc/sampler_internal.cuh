@@ -67,6 +67,7 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which);
 void launch_serve(const Ctx& c, int grid, cudaStream_t st);
 void launch_gin(const Ctx& c, int ntiles, cudaStream_t st);
 void launch_search_only(const Ctx& c, int grid, cudaStream_t st);
+void launch_shard_offset(const Ctx& c, const double* gathered, cudaStream_t st);  // shard.cu
 
 }  // namespace pfsmc_gpu
 
@@ -161,6 +162,9 @@ struct pfsmc_gpu_sampler {
   unsigned* c5_n = nullptr;        // their slots
   unsigned* c5_anc = nullptr;      // their ancestors (bucket-major; scattered to ctx.anc on demand)
   bool c5_anc_pending = false;     // ctx.anc not yet written for the last bucketed iteration
+  double* c5_gall = nullptr;       // sharded: every rank's stats group partials (world * groups * 7)
+  bool c5_fitness_is_lw = false;   // sharded scan phases of a config-5 iteration read lw as the fitness
+  unsigned long long* c5_remote = nullptr;  // sharded: records pulled from other GPUs (device counter)
 
   template <typename T>
   T* dalloc(size_t count) {
@@ -224,4 +228,6 @@ void harvest_timing(pfsmc_gpu_sampler* s);
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp);
 namespace pfsmc_gpu {
 void c5_flush_ancestors(pfsmc_gpu_sampler* s);  // c5.cu
+int c5_shard_groups(const pfsmc_gpu_sampler* s);
+double* c5_group_all(pfsmc_gpu_sampler* s);
 }

@@ -31,17 +31,8 @@ __global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp
 // upper_bound(cdf, u) lands on rank r iff u is in that range. Every rank draws
 // the uniforms of ALL global slots (keyed streams: identical numbers on every
 // rank), serves those in its range from its own exact CDF, and ships
-// {record, ll_bar, ancestor, destination slot} to the slot's owner.
-
-__device__ __forceinline__ int serving_rank(const Ctx& c, double u) {
-  const int ntl = c.ntiles;
-  for (int r = 0; r < c.world; ++r) {
-    const double lo = c.gtile_info[r * ntl].x;
-    const double hi = c.gtile_info[(r + 1) * ntl - 1].y;
-    if (u >= lo && u < hi) return r;
-  }
-  return c.world - 1;  // unreachable: the last range ends at the guarded cdf >= 1 > u
-}
+// {record, ll_bar, ancestor, destination slot} to the slot's owner
+// (serving_rank: kernels.cuh).
 
 // Every rank walks all global slots (a warp = 32 consecutive slots, all of one
 // destination since N_local is a multiple of 16384): the slot's serving rank
@@ -140,6 +131,10 @@ __global__ void k_shard_offset(Ctx c, const double* gathered) {
   }
   c.shard_off[0] = s;
   c.shard_off[1] = n;
+}
+
+void launch_shard_offset(const Ctx& c, const double* gathered, cudaStream_t st) {
+  k_shard_offset<<<1, 32, 0, st>>>(c, gathered);
 }
 
 // ---- offspring-allocation mode (north_star) ----------------
@@ -503,6 +498,8 @@ pfsmc_gpu_status pfsmc_gpu_shard_buffer(pfsmc_gpu_sampler* s, int which, void** 
       case 9: *ptr = s->recvbuf; *bytes = sizeof(double) * PW * s->N; break;
       case 10: *ptr = s->counts_dev; *bytes = sizeof(unsigned) * 2 * s->world; break;
       case 11: *ptr = s->counts_all; *bytes = sizeof(unsigned) * s->world * s->world; break;
+      case 12: *ptr = c.gpart; *bytes = sizeof(double) * 7 * c5_shard_groups(s); break;  // config 5
+      case 13: *ptr = c5_group_all(s); *bytes = sizeof(double) * 7 * c5_shard_groups(s) * s->world; break;
       default: throw ConfigError("shard_buffer: unknown buffer id");
     }
     if (!s->shard_api && (which == 1 || which == 3 || which >= 7)) throw ConfigError("not a sharded handle");
@@ -514,6 +511,7 @@ static void shard_predict_impl(pfsmc_gpu_sampler* s, const double* y, uint64_t j
                                double h) {
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
   raise_pending(s);
+  s->c5_fitness_is_lw = false;
   const StepParams sp = make_params(s, y, j, t_prev, t_obs, h);
   CK(cudaStreamSynchronize(s->stream));  // the pinned params slot is free
   *s->sp_host = sp;
@@ -539,10 +537,19 @@ pfsmc_gpu_status pfsmc_gpu_shard_finish_lse(pfsmc_gpu_sampler* s) {
   });
 }
 
+// The scan phases' context: the fitness log-weights are lg after a predict
+// phase, the log-weights themselves in a config-5 iteration (shard_c5_stats).
+static Ctx scan_ctx(const pfsmc_gpu_sampler* s) {
+  Ctx c = s->ctx;
+  if (s->c5_fitness_is_lw) c.lg = c.lw;
+  return c;
+}
+
 pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s) {
   return guarded([&] {
-    k_shard_offset<<<1, 32, 0, s->stream>>>(s->ctx, s->sums_all);
-    launch_scan(s->ctx, s->ntiles, s->stream, 4);
+    const Ctx c = scan_ctx(s);
+    k_shard_offset<<<1, 32, 0, s->stream>>>(c, s->sums_all);
+    launch_scan(c, s->ntiles, s->stream, 4);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
@@ -550,8 +557,9 @@ pfsmc_gpu_status pfsmc_gpu_shard_scan_records(pfsmc_gpu_sampler* s) {
 
 pfsmc_gpu_status pfsmc_gpu_shard_resolve(pfsmc_gpu_sampler* s) {
   return guarded([&] {
-    launch_scan(s->ctx, s->ntiles, s->stream, 5);
-    launch_scan(s->ctx, s->ntiles, s->stream, 2);
+    const Ctx c = scan_ctx(s);
+    launch_scan(c, s->ntiles, s->stream, 5);
+    launch_scan(c, s->ntiles, s->stream, 2);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });

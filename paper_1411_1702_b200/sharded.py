@@ -36,7 +36,7 @@ import numpy as np
 from .sampler import MODEL_DIMS, MODELS, ConfigError, GpuSampler, ObservationModel, PfConfig, TraceRow, _f64, _ptr
 
 (BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
- BUF_CNT, BUF_CNT_ALL) = range(12)
+ BUF_CNT, BUF_CNT_ALL, BUF_C5, BUF_C5_ALL) = range(14)
 STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
 IPC_BYTES = 448  # PFSMC_GPU_IPC_BYTES
 SHARD_MODES = {"exact": 0, "offspring": 1}  # PFSMC_GPU_SHARD_EXACT / _OFFSPRING
@@ -251,6 +251,32 @@ class GpuShard(GpuSampler):
         out = np.zeros(self.row_width)
         self._check(self.lib.pfsmc_gpu_shard_finish_moments(self.h, flags, _ptr(out)))
         return out
+
+    # -- BASELINE config 5 (payload64 shards) --------------------------------
+    def _c5(self, name, *args):
+        fn = getattr(self.lib, name)
+        fn.restype = C.c_int
+        self._check(fn(self.h, *args))
+
+    def c5_stats(self):
+        self._c5("pfsmc_gpu_shard_c5_stats")
+
+    def c5_finish(self):
+        self._c5("pfsmc_gpu_shard_c5_finish")
+
+    def c5_pull(self, j: int):
+        self._c5("pfsmc_gpu_shard_c5_pull", C.c_uint64(j))
+
+    def c5_flip(self):
+        self._c5("pfsmc_gpu_shard_c5_flip")
+
+    def c5_native_iteration(self, j: int):
+        self._c5("pfsmc_gpu_shard_c5_iteration", C.c_uint64(j))
+
+    def c5_remote_pulls(self) -> int:
+        v = C.c_uint64()
+        self._c5("pfsmc_gpu_shard_c5_remote_pulls", C.byref(v))
+        return int(v.value)
 
     def payload_doubles(self) -> int:
         return (self.d + self.p + 1) // 2 * 2 + 4
@@ -486,6 +512,29 @@ class ShardedFilter:
             s.update(int(sum(counts[r][s.rank] for r in range(self.world))))
         comm.allgather(sh, BUF_MOM, BUF_MOM_ALL)                         # E
         return self._row(self._each(lambda s: s.finish_moments(STEP_FLAGS))[0], j, t_obs)
+
+    def c5_iteration(self, j: int):
+        """One BASELINE config-5 iteration of the global 64-byte-record
+        ensemble (payload64 shards, peers attached): global log-sum-exp and
+        weighted 2x2 covariance, the exact multinomial resampling and the
+        gather with migration over peer memory; bitwise the single handle's
+        pfsmc_gpu_c5_iteration."""
+        sh, comm = self.shards, self.comm
+        if len(sh) == 1 and getattr(sh[0], "native", False):
+            sh[0].c5_native_iteration(j)
+            return
+        self._each(lambda s: s.c5_stats())
+        comm.allgather(sh, BUF_C5, BUF_C5_ALL)                           # A
+        self._each(lambda s: s.c5_finish())
+        comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # B
+        self._each(lambda s: s.scan_records())
+        comm.allgather_slices(sh, BUF_HDR)                               # C
+        comm.allgather_slices(sh, BUF_WIN)
+        self._each(lambda s: s.resolve())
+        comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # every rank's tables complete
+        self._each(lambda s: s.c5_pull(j))                               # D
+        comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # every pull done
+        self._each(lambda s: s.c5_flip())
 
     def _row(self, out, j, t_obs) -> TraceRow:
         p, d = self.p, self.d
