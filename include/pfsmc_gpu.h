@@ -286,7 +286,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
  * segment ends, guide, offspring prefix), the caller allgathers them (world x
  * PFSMC_GPU_IPC_BYTES, rank order) and every rank attaches; then each slot
  * pulls its ancestor from the serving rank's memory. */
-#define PFSMC_GPU_IPC_BYTES 448
+#define PFSMC_GPU_IPC_BYTES 512
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out448);
 pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles);
 /* Back to the counted send / receive (if any rank failed to map its peers). */
@@ -298,6 +298,10 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
  * shard_serve + the payload exchange + shard_update): call after every
  * rank's tables are complete (after the resolve phase). */
 pfsmc_gpu_status pfsmc_gpu_shard_pull(pfsmc_gpu_sampler* s);
+/* shard_resolve reading every shard's tile windows over peer memory (peers
+ * attached): with it, phase C exchanges only the tile headers (buffer 4), not
+ * the window lists (buffer 5). */
+pfsmc_gpu_status pfsmc_gpu_shard_resolve_peers(pfsmc_gpu_sampler* s);
 pfsmc_gpu_status pfsmc_gpu_shard_update(pfsmc_gpu_sampler* s, uint64_t n_recv);
 
 /* Migration mode of the sharded step (north_star).

@@ -467,9 +467,7 @@ static void enqueue_c5_shard_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
   launch_shard_offset(c, s->sums_all, st);
   launch_scan(c, s->ntiles, st, 4);
   NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));  // C
-  NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8, s->nccl,
-                  st));
-  launch_scan(c, s->ntiles, st, 5);
+  launch_resolve_global(c, s->ntiles, st, peer_winsrc(s));  // windows read over peer memory
   launch_scan(c, s->ntiles, st, 2);
   NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every rank's tables complete
   k_c5_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers, j, s->c5_remote);                      // D

@@ -40,7 +40,6 @@ constexpr int kShardPW = 4;  // extra doubles of a migration payload beyond the 
 
 // Every rank's search tables and records, as seen from this GPU: local
 // pointers for itself, CUDA IPC mappings (NVLink peer memory) for the others.
-constexpr int kMaxRanks = 8;
 struct PeerTable {
   const double* rec0[kMaxRanks];
   const double* rec1[kMaxRanks];
@@ -49,6 +48,7 @@ struct PeerTable {
   const double* seg_end[kMaxRanks];
   const unsigned* coarse[kMaxRanks];
   const unsigned* ooff[kMaxRanks];  // offspring mode: exclusive prefix of per-particle offspring counts
+  const TileWin* win[kMaxRanks];    // the exact scan's tile windows (read by every rank's resolver)
 };
 
 // Migration modes of a sharded step (pfsmc_gpu_shard_set_mode):
@@ -64,6 +64,8 @@ struct PeerTable {
 
 // launchers of kernels that live in another unit (scan.cu)
 void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which);
+// the global resolver over every shard's tiles, windows from `ws`
+void launch_resolve_global(const Ctx& c, int ntiles, cudaStream_t st, const WinSrc& ws);
 void launch_serve(const Ctx& c, int grid, cudaStream_t st);
 void launch_gin(const Ctx& c, int ntiles, cudaStream_t st);
 void launch_search_only(const Ctx& c, int grid, cudaStream_t st);
@@ -229,5 +231,6 @@ void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepPar
 namespace pfsmc_gpu {
 void c5_flush_ancestors(pfsmc_gpu_sampler* s);  // c5.cu
 int c5_shard_groups(const pfsmc_gpu_sampler* s);
+WinSrc peer_winsrc(const pfsmc_gpu_sampler* s);  // shard.cu
 double* c5_group_all(pfsmc_gpu_sampler* s);
 }

@@ -277,7 +277,7 @@ struct WinSmem {
 // false, having written nothing, when a tile overflowed its window list or
 // the windows exceed the staging area: the caller then runs resolve_chain.
 template <int ITEMS>
-__device__ bool resolve_windows(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
+__device__ bool resolve_windows(const Ctx& c, const TileHdr* hdr, const WinSrc& win, double* win_after,
                                 double2* tile_info, int ntiles, WinSmem& ws) {
   const int K = (ntiles + kThreads - 1) / kThreads;
   const int tb = min(static_cast<int>(threadIdx.x) * K, ntiles), te = min(tb + K, ntiles);
@@ -311,7 +311,7 @@ __device__ bool resolve_windows(const Ctx& c, const TileHdr* hdr, const TileWin*
     for (int t = tb; t < te; ++t) {
       const TileHdr h = load_hdr(hdr, t);
       for (int k = 0; k < h.nwin; ++k) {
-        const TileWin* gw = win + static_cast<size_t>(t) * kMaxWin + k;
+        const TileWin* gw = win.at(t, k);
         Piece pc{__ldcg(&gw->d0), __ldcg(&gw->d1), __ldcg(&gw->e), 0};
         if (k == 0) pc = piece_combine(E, pc);
         ws.wp[wo] = pc;
@@ -373,7 +373,7 @@ __device__ bool resolve_windows(const Ctx& c, const TileHdr* hdr, const TileWin*
 // is staged in shared memory. Used for the single handle (own tiles) and,
 // sharded, for all shards' tiles on every rank.
 template <int ITEMS>
-__device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* win, double* win_after,
+__device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const WinSrc& win, double* win_after,
                               double2* tile_info, int ntiles, bool own_g, ResolverSmem& rs) {
   using TC = TileCfg<ITEMS>;
   const int K = min(kMaxSuper, (ntiles + kThreads - 1) / kThreads);
@@ -415,7 +415,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
       int w = ex.wofs;  // record where the windows live; loaded cooperatively below
       for (int ti = tb; ti < te; ++ti) {
         const int n = __ldcg(&hdr[ti].nwin);
-        for (int k = 0; k < n && w < kResolveWin; ++k, ++w) rs.wsrc[w] = win + static_cast<size_t>(ti) * kMaxWin + k;
+        for (int k = 0; k < n && w < kResolveWin; ++k, ++w) rs.wsrc[w] = win.at(ti, k);
       }
     }
     __syncthreads();
@@ -451,7 +451,7 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const TileWin* w
               if (wo < kResolveWin) {
                 tw = rs.win[wo];
               } else {
-                const TileWin* gw = win + static_cast<size_t>(ti) * kMaxWin + k;
+                const TileWin* gw = win.at(ti, k);
                 tw.g = __ldcg(&gw->g);
                 tw.e = __ldcg(&gw->e);
                 tw.d0 = __ldcg(&gw->d0);
@@ -606,21 +606,24 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) c.st->tstamp[1] = global_ns();
-  if (!resolve_windows<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, sm.ws))
-    resolve_chain<ITEMS>(c, c.hdr, c.win, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
+  WinSrc own{};
+  own.base[0] = c.win;
+  own.tiles_per_rank = c.ntiles;
+  if (!resolve_windows<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, sm.ws))
+    resolve_chain<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
   if (threadIdx.x == 0) c.st->tstamp[2] = global_ns();
 }
 
 // Sharded: every rank resolves the exact chain over ALL shards' tiles.
 template <int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c) {
+__global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c, WinSrc ws) {
   __shared__ union {
     ResolverSmem rs;
     WinSmem ws;
   } sm;
   if (grid_error(c)) return;
-  if (!resolve_windows<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, sm.ws))
-    resolve_chain<ITEMS>(c, c.ghdr, c.gwin, c.gwin_after, c.gtile_info, c.gntiles, false, sm.rs);
+  if (!resolve_windows<ITEMS>(c, c.ghdr, ws, c.gwin_after, c.gtile_info, c.gntiles, sm.ws))
+    resolve_chain<ITEMS>(c, c.ghdr, ws, c.gwin_after, c.gtile_info, c.gntiles, false, sm.rs);
 }
 
 // S3: exact per-element CDF (from the S2 per-thread handoff: no block
@@ -768,6 +771,11 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
   }
 }
 
+void launch_resolve_global(const Ctx& c, int ntiles, cudaStream_t st, const WinSrc& ws) {
+  if (c.tile_log2 == 11) k_resolve_global<8><<<1, kThreads, 0, st>>>(c, ws);
+  else k_resolve_global<16><<<1, kThreads, 0, st>>>(c, ws);
+}
+
 void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
   const bool small = c.tile_log2 == 11;
   switch (which) {
@@ -783,10 +791,13 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
       if (small) k_scan_pieces<8, 1><<<ntiles, kThreads, 0, st>>>(c);
       else k_scan_pieces<16, 1><<<ntiles, kThreads, 0, st>>>(c);
       break;
-    case 5:
-      if (small) k_resolve_global<8><<<1, kThreads, 0, st>>>(c);
-      else k_resolve_global<16><<<1, kThreads, 0, st>>>(c);
+    case 5: {  // windows from the allgathered copy of every shard's lists
+      WinSrc ws{};
+      for (int r = 0; r < c.world && r < kMaxRanks; ++r) ws.base[r] = c.gwin + static_cast<size_t>(r) * ntiles * kMaxWin;
+      ws.tiles_per_rank = ntiles;
+      launch_resolve_global(c, ntiles, st, ws);
       break;
+    }
   }
 }
 

@@ -322,6 +322,16 @@ __global__ void __launch_bounds__(kThreads) k_offspring_pull(Ctx c, PeerTable pt
   c.anc[n] = static_cast<unsigned>(ga);
 }
 
+// The resolver's windows read straight from every shard's own list over
+// peer memory (phase C without the window allgather: only the tile headers
+// are exchanged, and only the windows that exist cross NVLink).
+WinSrc peer_winsrc(const pfsmc_gpu_sampler* s) {
+  WinSrc ws{};
+  for (int r = 0; r < s->world && r < kMaxRanks; ++r) ws.base[r] = s->peers.win[r];
+  ws.tiles_per_rank = s->ntiles;
+  return ws;
+}
+
 }  // namespace pfsmc_gpu
 
 const NcclApi& nccl_api() {
@@ -690,13 +700,13 @@ static void drop_peers(pfsmc_gpu_sampler* s) {
 // ---- migration over NVLink peer memory --------------------------------------
 // The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
 // segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
-constexpr int kPeerBufs = 7;  // + the offspring prefix (offspring mode)
+constexpr int kPeerBufs = 8;  // + the offspring prefix (offspring mode), the tile windows
 
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out) {
   return guarded([&] {
     if (!s->shard_api) throw ConfigError("not a sharded handle");
     const Ctx& c = s->ctx;
-    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse, s->ooff};
+    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse, s->ooff, c.win};
     for (int i = 0; i < kPeerBufs; ++i) {
       cudaIpcMemHandle_t h;
       CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
@@ -721,6 +731,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
       if (r == s->rank) {
         p[0] = c.rec[0], p[1] = c.rec[1], p[2] = c.llbar, p[3] = c.cdf, p[4] = c.seg_end, p[5] = c.coarse;
         p[6] = s->ooff;
+        p[7] = c.win;
       } else {
         for (int i = 0; i < kPeerBufs; ++i) {
           cudaIpcMemHandle_t h;
@@ -738,6 +749,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
       t.seg_end[r] = static_cast<const double*>(p[4]);
       t.coarse[r] = static_cast<const unsigned*>(p[5]);
       t.ooff[r] = static_cast<const unsigned*>(p[6]);
+      t.win[r] = static_cast<const TileWin*>(p[7]);
     }
     s->peers = t;
     s->have_peers = true;
@@ -767,6 +779,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
       t.seg_end[r] = c.seg_end;
       t.coarse[r] = c.coarse;
       t.ooff[r] = o->ooff;
+      t.win[r] = c.win;
     }
     s->peers = t;
     s->have_peers = true;
@@ -780,6 +793,19 @@ pfsmc_gpu_status pfsmc_gpu_shard_detach_peers(pfsmc_gpu_sampler* s) {
   return guarded([&] {
     CK(cudaSetDevice(s->cfg.device));
     drop_peers(s);
+    return PFSMC_GPU_OK;
+  });
+}
+
+// shard_resolve with the windows read over peer memory (peers attached; every
+// shard's scan_records done and the headers allgathered).
+pfsmc_gpu_status pfsmc_gpu_shard_resolve_peers(pfsmc_gpu_sampler* s) {
+  return guarded([&] {
+    if (!s->have_peers) throw ConfigError("shard_resolve_peers: no peer table (attach_peers / attach_peers_local)");
+    const Ctx c = scan_ctx(s);
+    launch_resolve_global(c, s->ntiles, s->stream, peer_winsrc(s));
+    launch_scan(c, s->ntiles, s->stream, 2);
+    CK(cudaGetLastError());
     return PFSMC_GPU_OK;
   });
 }
@@ -812,10 +838,9 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
   NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));
   k_shard_offset<<<1, 32, 0, st>>>(c, s->sums_all);
   launch_scan(c, s->ntiles, st, 4);
+  // phase C: the headers only; the windows are read over peer memory
   NCK(N.AllGather(c.hdr, c.ghdr, sizeof(TileHdr) * static_cast<size_t>(s->ntiles), ncclUint8, s->nccl, st));
-  NCK(N.AllGather(c.win, c.gwin, sizeof(TileWin) * static_cast<size_t>(s->ntiles) * kMaxWin, ncclUint8,
-                  s->nccl, st));
-  launch_scan(c, s->ntiles, st, 5);
+  launch_resolve_global(c, s->ntiles, st, peer_winsrc(s));
   launch_scan(c, s->ntiles, st, 2);
   if (s->shard_mode == PFSMC_GPU_SHARD_OFFSPRING) {
     enqueue_offspring(s);  // counts + prefix from the global walk (no exchange)

@@ -62,6 +62,22 @@ struct TileWin {
   long long d0, d1;
 };
 
+// Where the resolver finds tile t's windows: rank r = t / tiles_per_rank
+// holds them at base[r] + (t - r * tiles_per_rank) * kMaxWin (the handle's own
+// list, the allgathered copy of every shard's, or the shards' own lists read
+// over peer memory).
+constexpr int kMaxRanks = 8;
+struct WinSrc {
+  const TileWin* base[kMaxRanks];
+  int tiles_per_rank;
+#ifdef __CUDACC__
+  __device__ __forceinline__ const TileWin* at(int t, int k) const {
+    const int r = t / tiles_per_rank;
+    return base[r] + static_cast<size_t>(t - r * tiles_per_rank) * kMaxWin + k;
+  }
+#endif
+};
+
 // Per-thread handoff from the records phase to the CDF phase of the exact
 // scan: the thread's approximate prefix and the exact segment carry.
 struct ThreadRec {

@@ -38,7 +38,7 @@ from .sampler import MODEL_DIMS, MODELS, ConfigError, GpuSampler, ObservationMod
 (BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
  BUF_CNT, BUF_CNT_ALL, BUF_C5, BUF_C5_ALL) = range(14)
 STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
-IPC_BYTES = 448  # PFSMC_GPU_IPC_BYTES
+IPC_BYTES = 512  # PFSMC_GPU_IPC_BYTES
 SHARD_MODES = {"exact": 0, "offspring": 1}  # PFSMC_GPU_SHARD_EXACT / _OFFSPRING
 
 
@@ -135,6 +135,11 @@ class GpuShard(GpuSampler):
 
     def resolve(self):
         self._check(self.lib.pfsmc_gpu_shard_resolve(self.h))
+
+    def resolve_peers(self):
+        """resolve with the windows read from the other shards over peer memory."""
+        self.lib.pfsmc_gpu_shard_resolve_peers.restype = C.c_int
+        self._check(self.lib.pfsmc_gpu_shard_resolve_peers(self.h))
 
     def serve(self) -> np.ndarray:
         counts = np.zeros(2 * self.world, dtype=np.uint32)
@@ -469,9 +474,7 @@ class ShardedFilter:
         self._each(lambda s: s.finish_lse())                             # (+ local tile prefixes)
         comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # B
         self._each(lambda s: s.scan_records())
-        comm.allgather_slices(sh, BUF_HDR)                               # C
-        comm.allgather_slices(sh, BUF_WIN)
-        self._each(lambda s: s.resolve())
+        self._phase_c()
         if self.mode == "offspring":
             tot = [s.offspring() for s in sh][0]                         # identical on every rank
             self.last_totals = np.asarray(tot, dtype=np.int64)
@@ -528,13 +531,22 @@ class ShardedFilter:
         self._each(lambda s: s.c5_finish())
         comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # B
         self._each(lambda s: s.scan_records())
-        comm.allgather_slices(sh, BUF_HDR)                               # C
-        comm.allgather_slices(sh, BUF_WIN)
-        self._each(lambda s: s.resolve())
+        self._phase_c()
         comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # every rank's tables complete
         self._each(lambda s: s.c5_pull(j))                               # D
         comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                         # every pull done
         self._each(lambda s: s.c5_flip())
+
+    def _phase_c(self):
+        """C: tile headers to every rank; the windows too, unless the shards
+        read each other's window lists over peer memory (pull mode)."""
+        sh, comm = self.shards, self.comm
+        comm.allgather_slices(sh, BUF_HDR)
+        if self.pull and all(getattr(s, "peers", False) for s in sh):
+            self._each(lambda s: s.resolve_peers())
+        else:
+            comm.allgather_slices(sh, BUF_WIN)
+            self._each(lambda s: s.resolve())
 
     def _row(self, out, j, t_obs) -> TraceRow:
         p, d = self.p, self.d
