@@ -431,7 +431,7 @@ def bench_workloads(local, fp64):
                             np.zeros(2), np.eye(2)))
     stream = torch.cuda.ExternalStream(s.stream_handle, device=local)
     by_search = {}
-    for search in ("guide", "bucketed"):
+    for search in ("guide", "split", "bucketed"):
         s.c5_set_search(search)
         c5 = by_search[search] = {}
         for sigma in (0.1, 1.0, 4.0):
@@ -510,29 +510,36 @@ def bench_workloads(local, fp64):
     c3["newton_iterations_per_particle_step"] = tot_it / tot_steps / n3
     c3["cpu_reference"] = _cpu_ref_windows(
         prob, dict(family="bdf", order=2, a=0.99, obs_idx=(0, 2), sigma=0.02, newton_max_iter=4))
-    # config 4: 8-compartment chain, 2^24, BDF3 m=3
+    # config 4: 8-compartment chain, 2^24, BDF3 m=3, both arithmetic variants
+    # (exact: the reference's operation order, bitwise Psi; fast: FMA and
+    # reciprocals, parity at the north_star tolerances)
+    import dataclasses
     n4 = 1 << 24
     prob = problems.chain8(particles=n4, T=10, seed=1)
-    g = GpuSampler("chain", _cfg(prob), prob.obs, device=local)
-    prob.init(g)
-    ms, it = _timed_steps(g, prob, 2, 1, torch.cuda.ExternalStream(g.stream_handle, device=local))
-    t = sum(ms) / len(ms)
-    # Newton iterations per particle-step, BOTH propagations (k_predict and
-    # k_update add to one per-step counter, lmm.cpp:488 convention)
-    newton = float(np.mean(it)) / n4
-    # N_it(8) = 643 FP64 flops per Newton iteration (dense-LU
-    # count, the reference algorithm's); the device's banded solve executes
-    # fewer (EXEC_FLOPS_PER_NEWTON_CHAIN), so both are reported
-    flops = 643 * newton
-    tfl = flops * n4 / (t / 1e3) / 1e12
-    tfl_exec = EXEC_FLOPS_PER_NEWTON_CHAIN * newton * n4 / (t / 1e3) / 1e12
-    out["c4_chain8"] = {"particles": n4, "integrator": "bdf3, m=3", "steps": len(ms), "ms_per_step": t,
-                        "particle_steps_per_s": n4 / (t / 1e3), "newton_iterations_per_particle_step": newton,
-                        "fp64_tflops_newton_algorithmic": tfl, "fp64_tflops_newton_executed": tfl_exec,
-                        "fp64_peak_tflops_measured": fp64,
-                        "frac_of_fp64_peak": (tfl / fp64) if fp64 else None,
-                        "frac_of_fp64_peak_executed": (tfl_exec / fp64) if fp64 else None}
-    g.close()
+    c4 = {}
+    for arith in ("exact", "fast"):
+        g = GpuSampler("chain", dataclasses.replace(prob.cfg, arithmetic=arith), prob.obs, device=local)
+        prob.init(g)
+        ms, it = _timed_steps(g, prob, 2, 1, torch.cuda.ExternalStream(g.stream_handle, device=local))
+        g.close()
+        t = sum(ms) / len(ms)
+        # Newton iterations per particle-step, BOTH propagations (k_predict and
+        # k_update add to one per-step counter, lmm.cpp:488 convention)
+        newton = float(np.mean(it)) / n4
+        # N_it(8) = 643 FP64 flops per Newton iteration (dense-LU
+        # count, the reference algorithm's); the device's banded solve executes
+        # fewer (EXEC_FLOPS_PER_NEWTON_CHAIN), so both are reported
+        flops = 643 * newton
+        tfl = flops * n4 / (t / 1e3) / 1e12
+        tfl_exec = EXEC_FLOPS_PER_NEWTON_CHAIN * newton * n4 / (t / 1e3) / 1e12
+        c4[arith] = {"particles": n4, "integrator": "bdf3, m=3", "arithmetic": arith, "steps": len(ms),
+                     "ms_per_step": t, "particle_steps_per_s": n4 / (t / 1e3),
+                     "newton_iterations_per_particle_step": newton,
+                     "fp64_tflops_newton_algorithmic": tfl, "fp64_tflops_newton_executed": tfl_exec,
+                     "fp64_peak_tflops_measured": fp64,
+                     "frac_of_fp64_peak": (tfl / fp64) if fp64 else None,
+                     "frac_of_fp64_peak_executed": (tfl_exec / fp64) if fp64 else None}
+    out["c4_chain8"] = {**c4["exact"], "fast_arithmetic": c4["fast"]}
     out["c4_chain8"]["cpu_reference"] = _cpu_ref_rate(
         "chain", prob, dict(family="bdf", order=3, a=0.98, obs_idx=(0, 3, 7), sigma=0.01))
     # the reference's own problem 1 (models::MetabolicModel), BDF2 with m = 4 sub-steps,
@@ -1011,6 +1018,37 @@ def main():
             "gpu_launches": len(kt) * args.steps,
             "e2e": e2e, "clocks": clk.summary(),
             "final_trace": {"theta_mean": list(map(float, last[:P])), "ess": float(last[-1])}}
+    # the same resident graph step with the FAST arithmetic variant (FMA,
+    # reciprocals; parity at the north_star tolerances, tests/test_gpu_parity.py
+    # fast_* cases) on its own handle, same seed / observations
+    if world == 1 and ARITH == "exact":
+        import dataclasses
+        gf = GpuSampler("lv", dataclasses.replace(cfg, arithmetic="fast"), prob.obs, device=local)
+        gf.initialize_uniform(**prob.prior)
+        gf.upload_observations(prob.ys[:T], prob.times[:T], 0.0)
+        sf = torch.cuda.ExternalStream(gf.stream_handle, device=local)
+        jf = 0
+        for _ in range(args.warmup):
+            jf += 1
+            gf.step_resident(jf)
+        gf.synchronize()
+        evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            gf.flush_l2()
+            jf += 1
+            with torch.cuda.stream(sf):
+                evf[k][0].record(sf)
+            gf.step_resident(jf)
+            with torch.cuda.stream(sf):
+                evf[k][1].record(sf)
+        gf.synchronize()
+        torch.cuda.synchronize()
+        fms = sum(a.elapsed_time(b) for a, b in evf) / args.steps
+        gf.close()
+        line["fast_arithmetic"] = {"value": n / (fms / 1e3), "unit": UNIT, "ms_per_step": fms,
+                                   "note": "same workload, PFSMC_GPU_ARITH_FAST handle (FMA contraction, reciprocal "
+                                           "multiplies); the headline value is the exact (reference operation "
+                                           "order) build"}
     fp64 = fp64_peak(local)
     line["fp64_peak_tflops_measured"] = fp64
     if world == 1 and not args.no_workloads:
