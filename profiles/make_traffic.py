@@ -1,7 +1,7 @@
 """profiles/kernel_traffic.json from an ncu --set full report: DRAM bytes
 (read + write) per launch for each kernel (mean over the captured launches).
 
-  python profiles/make_traffic.py <report.ncu-rep> [out.json]
+  python profiles/make_traffic.py <report.ncu-rep | raw page .csv> [out.json]
 """
 import collections
 import csv
@@ -16,8 +16,13 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def main():
     rep = sys.argv[1]
     out = sys.argv[2] if len(sys.argv) > 2 else "profiles/kernel_traffic.json"
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i report --page raw --csv` exported on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    while rows and "Kernel Name" not in rows[0]:
+        rows = rows[1:]
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
     acc = collections.defaultdict(list)
@@ -31,7 +36,7 @@ def main():
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(m)
             tot += float(r[i].replace(",", "")) * UNIT.get(units[i], 1)
-        name = r[ki].split("(")[0].replace("void ", "").split("<")[0].strip()
+        name = r[ki].split("(")[0].replace("void ", "").split("<")[0].strip().split("::")[-1]
         acc[name].append(tot)
         for key, metric in extra.items():
             if metric in hdr:
