@@ -10,6 +10,10 @@
  *     static constexpr bool kLowerBidiagonal = false;  // true: J is lower
  *                                              // bidiagonal and the model
  *                                              // provides rhs_jac_band (banded Newton)
+ *     // optional, for large states: threads per CTA of the model's kernels
+ *     // and the LMM history in shared memory (as the 8-species chain)
+ *     //   static constexpr int kBlock = 128;
+ *     //   static constexpr bool kSmemHistory = true;
  *     using K = pfsmc_gpu::NoConsts;           // or a struct of bound constants
  *     __device__ static K load_k(const double* consts);  // pfsmc_gpu_config.model_consts
  *     __device__ static bool rhs(const K&, double t, const double (&th)[P],
