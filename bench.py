@@ -40,9 +40,9 @@ STEP_BYTES = 24 * F + 56                     # whole step, minimal fused pipelin
 R = D + P                                     # record doubles (x, theta_u)
 KERNEL_BYTES = {                              # per particle per launch
     "k_predict": 8 * R + 8 + 8 + 8,           # record + lw in; ll_bar + lg out
-    "k_scan_approx": 8 + 8 + 2,               # lg in; certified CDF + segment ends / guide out
+    "k_scan_pieces": 8 + 8,                   # lg in; g out
+    "k_scan_cdf": 8 + 8 + 2,                  # g in; cdf + local guide out
     "k_serve": 8 * R + 8 + 8 * (R + 2) + 4,   # ancestor record + ll_bar gathered; payload + anc out
-    "k_exact_fallback": 0,                    # the exact scan + fix-up: no work unless a slot is uncertain
     "k_update": 8 * (R + 2) + 8 * R + 8,      # payload in; record + lw out
 }
 

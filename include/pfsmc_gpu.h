@@ -185,10 +185,6 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
 /* %globaltimer probes of the last step (ns): [0] exact-CDF kernel start,
  * [1] resolver start, [2] resolver end. Diagnostics for profiling. */
 pfsmc_gpu_status pfsmc_gpu_debug_timestamps(pfsmc_gpu_sampler* s, uint64_t* out8);
-/* Slots of the last step whose ancestor the approximate CDF could not certify
- * (their uniform lies within the rigorous rounding bound of a CDF edge); they
- * were served from the exact sequential CDF. */
-pfsmc_gpu_status pfsmc_gpu_uncertain_slots(pfsmc_gpu_sampler* s, uint32_t* count);
 
 /* The CUDA stream every launch of this handle goes to (cudaStream_t). */
 void* pfsmc_gpu_stream(pfsmc_gpu_sampler* s);

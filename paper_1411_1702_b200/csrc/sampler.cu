@@ -149,17 +149,15 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   s->ks->predict(c, s->grid_m, st);
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[1], st));
-  nvtxRangePushA("resample (certified CDF, ancestor search + gather, exact fallback)");
-  if (s->ks->block_model()) {
-    // the exact scan, then the search only: the update CTAs gather their ancestor themselves
-    launch_scan(c, s->ntiles, st, 1);
-    if (timed) CK(cudaEventRecord(ev[2], st));
-    launch_scan(c, s->ntiles, st, 2);
-    if (timed) CK(cudaEventRecord(ev[3], st));
-    launch_search_only(c, s->grid, st);
-  } else {
-    launch_certified_resample(c, s->ntiles, s->grid, st, timed ? ev[2] : nullptr, timed ? ev[3] : nullptr);
-  }
+  nvtxRangePushA("resample (exact CDF scan + ancestor search)");
+  launch_scan(c, s->ntiles, st, 1);
+  if (timed) CK(cudaEventRecord(ev[2], st));
+  launch_scan(c, s->ntiles, st, 2);
+  if (timed) CK(cudaEventRecord(ev[3], st));
+  if (s->ks->block_model())
+    launch_search_only(c, s->grid, st);  // the update CTAs gather their ancestor themselves
+  else
+    launch_serve(c, s->grid, st);
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[4], st));
   nvtxRangePushA("proliferate + repropagate + weights (k_update)");
@@ -454,11 +452,6 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.lg = s->dalloc<double>(N);
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
-    c.unc = s->dalloc<unsigned>(kUncCap);
-    c.unc_cnt = s->dalloc<unsigned>(1);
-    CK(cudaMemset(c.unc_cnt, 0, sizeof(unsigned)));
-    c.cert_inflate = 1.0;
-    c.gate_exact = 0;
     c.tile_log2 = tile_log2;
     c.k1_block_log2 = ilog2(s->ks->kt);
     // the ancestor search's tables (segment ends, guide): small, read with
@@ -760,31 +753,6 @@ pfsmc_gpu_status pfsmc_gpu_get_step_diagnostics(pfsmc_gpu_sampler* s, uint32_t* 
     CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     if (newton_iters) *newton_iters = h.newton_iters;
-    return PFSMC_GPU_OK;
-  });
-}
-
-// Test knob (not in the public header): multiply the certification bound of
-// the approximate CDF (huge: every slot goes through the exact fallback).
-pfsmc_gpu_status pfsmc_gpu_debug_cert_inflate(pfsmc_gpu_sampler* s, double inflate) {
-  return guarded([&] {
-    if (!(inflate >= 1.0)) throw ConfigError("debug_cert_inflate: factor must be >= 1");
-    CK(cudaStreamSynchronize(s->stream));
-    s->ctx.cert_inflate = inflate;
-    if (s->graph) {  // the graph captured the old context
-      cudaGraphExecDestroy(s->graph);
-      s->graph = nullptr;
-      build_graph(s);
-    }
-    return PFSMC_GPU_OK;
-  });
-}
-
-// Slots of the last step whose ancestor needed the exact fallback.
-pfsmc_gpu_status pfsmc_gpu_uncertain_slots(pfsmc_gpu_sampler* s, uint32_t* count) {
-  return guarded([&] {
-    CK(cudaMemcpyAsync(count, s->ctx.unc_cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
     return PFSMC_GPU_OK;
   });
 }

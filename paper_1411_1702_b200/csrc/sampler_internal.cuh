@@ -32,7 +32,7 @@ struct NumericalError : std::runtime_error {
                                #x);                                                      \
   } while (0)
 
-inline constexpr const char* kKernelNames = "k_predict,k_scan_approx,k_serve,k_exact_fallback,k_update";
+inline constexpr const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_serve,k_update";
 constexpr int kNumKernels = 5;
 
 
@@ -70,9 +70,6 @@ void launch_serve(const Ctx& c, int grid, cudaStream_t st);
 void launch_gin(const Ctx& c, int ntiles, cudaStream_t st);
 void launch_search_only(const Ctx& c, int grid, cudaStream_t st);
 void launch_shard_offset(const Ctx& c, const double* gathered, cudaStream_t st);  // shard.cu
-// the single handle's resampling through the certified approximate CDF (scan.cu)
-void launch_certified_resample(const Ctx& c, int ntiles, int grid, cudaStream_t st, cudaEvent_t ev_approx,
-                               cudaEvent_t ev_serve);
 
 }  // namespace pfsmc_gpu
 

@@ -525,7 +525,6 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
   __shared__ ScanScratch sw;
   __shared__ int s_last;
   if (grid_error(c)) return;
-  if (c.gate_exact && __ldcg(c.unc_cnt) == 0) return;  // every ancestor certified
   if (!SHARDED && threadIdx.x == 0 && blockIdx.x == 0) c.st->tstamp[0] = global_ns();
   const int t = blockIdx.x;
   const long long base = static_cast<long long>(t) * TC::kTileT;
@@ -634,7 +633,6 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
   using TC = TileCfg<ITEMS>;
   __shared__ double sg[TC::kSmem];
   if (grid_error(c)) return;
-  if (c.gate_exact && __ldcg(c.unc_cnt) == 0) return;  // every ancestor certified
   const int t = blockIdx.x;
   const long long base = static_cast<long long>(t) * TC::kTileT;
   const int nwin = __ldcg(&c.hdr[t].nwin);
@@ -770,221 +768,6 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
       }
     }
     c.coarse[b] = static_cast<unsigned>(t) * SPB + static_cast<unsigned>(min(lo, SPB - 1));
-  }
-}
-
-// ---------------------------------------------------------------- certified approximate CDF
-// The exact scan above costs two passes and a serial resolver, but a slot's
-// ancestor only depends on the two CDF values around its uniform. The
-// approximate prefix P (the tile offsets from K1's partials + the in-tile
-// tree prefix of the exact g — the same P the exact scan classifies with)
-// satisfies |cdf_k - P_k| <= sum_bound(P_k, cnt_k) <= sum_bound(P_k, k + 1)
-// (exact_cdf.cuh). The search runs on P; slot n's ancestor a is CERTIFIED
-// when P_a - E_a > u (so cdf_a > u) and P_{a-1} + E_{a-1} <= u (so
-// cdf_{a-1} <= u, hence every earlier cdf value too: the sequential CDF is
-// non-decreasing): then a = upper_bound(cdf, u) exactly (filter.cpp:173),
-// whatever the search did. Uncertain slots (u within ~1e-9 relative of a CDF
-// edge: ~1e-3 slots per step at 2^20) go to a list; only then the exact scan
-// runs (its kernels exit at once otherwise) and k_serve_fix serves the listed
-// slots from the exact tables. Ancestors are bitwise those of the exact path.
-__device__ __forceinline__ double cert_bound(const Ctx& c, double p, long long cnt) {
-  return sum_bound(p, cnt) * c.cert_inflate;
-}
-
-// One pass per tile: g = exp(lg - lse), P written as the search's CDF, its
-// segment ends and the guide (buckets partitioned between tiles by the tile
-// offsets, so every bucket has exactly one owner).
-template <int ITEMS>
-__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_approx(Ctx c) {
-  using TC = TileCfg<ITEMS>;
-  __shared__ double sg[TC::kSmem];
-  __shared__ SumCnt sw[2 * kWarps];
-  if (grid_error(c)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *c.unc_cnt = 0;
-  const int t = blockIdx.x;
-  const long long base = static_cast<long long>(t) * TC::kTileT;
-  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
-  const double lse = c.st->lse_g;
-  {
-    double x[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int e = i * kThreads + threadIdx.x;
-      x[i] = e < valid ? __ldcs(&c.lg[base + e]) : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int e = i * kThreads + threadIdx.x;
-      sg[TC::sidx(e)] = e < valid ? exp(x[i] - lse) : 0.0;  // fitness_weights (filter.cpp:154)
-    }
-  }
-  __syncthreads();
-  double g[ITEMS];
-  SumCnt mine{0.0, 0};
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    g[i] = sg[TC::sidx(threadIdx.x * ITEMS + i)];
-    mine.s += g[i];
-  }
-  SumCnt tot;
-  const SumCnt ex = block_excl_scan_sc(mine, tot, sw);
-  const double t_lo = __ldcg(&c.tile_pre[t]);
-  double p = (0.0 + t_lo) + ex.s;  // as the exact scan's p[0] = (shard_off + tile_pre) + ex.s
-  double vals[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    p = p + g[i];
-    const int e = threadIdx.x * ITEMS + i;
-    double v = p;
-    if (base + e == c.N - 1) v = (v < 1.0) ? 1.0 : v;  // the guarded last bin (filter.cpp:168)
-    vals[i] = e < valid ? v : INFINITY;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) sg[TC::sidx(threadIdx.x * ITEMS + i)] = vals[i];
-  __syncthreads();
-#pragma unroll 4
-  for (int i = 0; i < ITEMS; ++i) {
-    const int e = i * kThreads + threadIdx.x;
-    if (e < valid) c.cdf[base + e] = sg[TC::sidx(e)];
-  }
-  constexpr int SPT = ITEMS >> kSegLog2;
-  constexpr int SPB = SPT * kThreads;
-  __shared__ double send[SPB];
-#pragma unroll
-  for (int q = 0; q < SPT; ++q) {
-    const int i0 = threadIdx.x * ITEMS + (q << kSegLog2);
-    const double v = i0 < valid ? sg[TC::sidx(min(i0 + (1 << kSegLog2) - 1, valid - 1))] : INFINITY;
-    send[threadIdx.x * SPT + q] = v;
-    if (i0 < valid) c.seg_end[static_cast<long long>(t) * SPB + threadIdx.x * SPT + q] = v;
-  }
-  __syncthreads();
-  const double B1 = scale2(1.0, c.coarse_bits);
-  const long long nb = 1LL << c.coarse_bits;
-  long long b_lo = t == 0 ? 0 : static_cast<long long>(ceil(t_lo * B1));
-  long long b_hi = t + 1 == c.ntiles ? nb - 1 : static_cast<long long>(ceil(__ldcg(&c.tile_pre[t + 1]) * B1)) - 1;
-  b_lo = max(b_lo, 0LL);
-  b_hi = min(b_hi, nb - 1);
-  for (long long b = b_lo + threadIdx.x; b <= b_hi; b += kThreads) {
-    const double xb = scale2(static_cast<double>(b), -c.coarse_bits);
-    int lo = 0, len = SPB;
-    while (len > 0) {
-      const int half = len >> 1;
-      if (!(xb < send[lo + half])) {
-        lo += half + 1;
-        len -= half + 1;
-      } else {
-        len = half;
-      }
-    }
-    c.coarse[b] = static_cast<unsigned>(t) * SPB + static_cast<unsigned>(min(lo, SPB - 1));
-  }
-}
-
-// Slot-order search + gather on P (k_serve) with the certification; the
-// uncertain slots are listed (their provisional payload is replaced by
-// k_serve_fix).
-template <int H>
-__global__ void __launch_bounds__(kThreads) k_serve_cert(Ctx c) {
-  if (grid_error(c)) return;
-  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  const double u = n < c.N ? resample_uniform(c.seed, c.sp->j, n) : -1.0;
-  const unsigned a = find_ancestor_warp(c, u);
-  if (n < c.N) {
-    c.anc[n] = a;
-    bool ok = true;
-    if (static_cast<long long>(a) + 1 < c.N) {
-      const double pa = __ldg(&c.cdf[a]);
-      ok &= pa - cert_bound(c, pa, static_cast<long long>(a) + 1) > u;
-    }
-    if (a > 0) {
-      const double pb = __ldg(&c.cdf[a - 1]);
-      ok &= pb + cert_bound(c, pb, static_cast<long long>(a)) <= u;
-    }
-    if (!ok) {
-      const unsigned k = atomicAdd(c.unc_cnt, 1u);
-      if (k < static_cast<unsigned>(kUncCap)) c.unc[k] = static_cast<unsigned>(n);
-    }
-  }
-  const int lane = threadIdx.x & 31;
-  const long long wbase = n - lane;
-  const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
-  double2* pay = reinterpret_cast<double2*>(c.payload);
-#pragma unroll
-  for (int it = 0; it < H; ++it) {
-    const int idx = lane + 32 * it;
-    const int slot = idx / H, part = idx - slot * H;
-    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
-    const long long ns = wbase + slot;
-    if (ns < c.N) {
-      double2 v;
-      if (part < H - 1)
-        v = __ldg(rec + static_cast<long long>(as) * (H - 1) + part);
-      else
-        v = make_double2(__ldg(&c.llbar[as]), static_cast<double>(as));
-      pay[ns * H + part] = v;
-    }
-  }
-}
-
-// The listed slots (or all slots if the list overflowed) from the exact CDF
-// tables the fallback scan just built.
-template <int H>
-__global__ void __launch_bounds__(kThreads) k_serve_fix(Ctx c) {
-  if (grid_error(c)) return;
-  const unsigned cnt = __ldcg(c.unc_cnt);
-  if (cnt == 0) return;
-  const bool all = cnt > static_cast<unsigned>(kUncCap);
-  const long long total = all ? c.N : cnt;
-  const double2* rec = reinterpret_cast<const double2*>(c.rec[c.st->cur]);
-  double2* pay = reinterpret_cast<double2*>(c.payload);
-  for (long long i = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * kThreads) {
-    const long long n = all ? i : static_cast<long long>(__ldcg(&c.unc[i]));
-    const double u = resample_uniform(c.seed, c.sp->j, n);
-    const unsigned a = find_ancestor(c, u);
-    c.anc[n] = a;
-    for (int part = 0; part < H - 1; ++part) pay[n * H + part] = __ldg(rec + static_cast<long long>(a) * (H - 1) + part);
-    pay[n * H + H - 1] = make_double2(__ldg(&c.llbar[a]), static_cast<double>(a));
-  }
-}
-
-// The certified path of one step's resampling: P, the certified search +
-// gather, then the gated exact scan and the fix-up (no work unless a slot
-// was uncertain). ev: optional timing events after the search and after the
-// fallback.
-void launch_certified_resample(const Ctx& c0, int ntiles, int grid, cudaStream_t st, cudaEvent_t ev_approx,
-                               cudaEvent_t ev_serve) {
-  Ctx c = c0;
-  c.gate_exact = 1;
-  const bool small = c.tile_log2 == 11;
-  if (small) k_scan_approx<8><<<ntiles, kThreads, 0, st>>>(c);
-  else k_scan_approx<16><<<ntiles, kThreads, 0, st>>>(c);
-  if (ev_approx) CK(cudaEventRecord(ev_approx, st));
-  const int H = c.R / 2 + 1;
-  switch (H) {
-    case 2: k_serve_cert<2><<<grid, kThreads, 0, st>>>(c); break;
-    case 3: k_serve_cert<3><<<grid, kThreads, 0, st>>>(c); break;
-    case 4: k_serve_cert<4><<<grid, kThreads, 0, st>>>(c); break;
-    case 5: k_serve_cert<5><<<grid, kThreads, 0, st>>>(c); break;
-    case 7: k_serve_cert<7><<<grid, kThreads, 0, st>>>(c); break;
-    default: break;
-  }
-  if (ev_serve) CK(cudaEventRecord(ev_serve, st));
-  if (small) {
-    k_scan_pieces<8, 0><<<ntiles, kThreads, 0, st>>>(c);
-    k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
-  } else {
-    k_scan_pieces<16, 0><<<ntiles, kThreads, 0, st>>>(c);
-    k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
-  }
-  switch (H) {
-    case 2: k_serve_fix<2><<<148, kThreads, 0, st>>>(c); break;
-    case 3: k_serve_fix<3><<<148, kThreads, 0, st>>>(c); break;
-    case 4: k_serve_fix<4><<<148, kThreads, 0, st>>>(c); break;
-    case 5: k_serve_fix<5><<<148, kThreads, 0, st>>>(c); break;
-    case 7: k_serve_fix<7><<<148, kThreads, 0, st>>>(c); break;
-    default: break;
   }
 }
 

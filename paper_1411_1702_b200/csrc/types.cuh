@@ -16,7 +16,6 @@ namespace pfsmc_gpu {
 constexpr int kMaxObs = 8;               // register models (loglik<M> unrolls to this)
 constexpr int kMaxObsAdv = 32;           // the advection-diffusion model (20 sites in the reference)
 constexpr int kMaxWin = 64;              // windows per tile before serial fallback
-constexpr int kUncCap = 1 << 16;         // uncertain-slot list of the certified search
 constexpr double kNegInf = -INFINITY;
 
 enum ErrBits : int { kErrPredict = 1, kErrChol = 2, kErrUpdate = 4, kErrInternal = 8 };
@@ -103,11 +102,6 @@ struct Ctx {
   double rtol;       // adaptive BDF(1,2) tolerance (IntegratorSpec.rtol)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
-  // certified approximate CDF (scan.cu k_scan_approx / k_serve<H, true>):
-  unsigned* unc;       // slots whose ancestor the approximate CDF cannot certify
-  unsigned* unc_cnt;   // their count (reset by k_scan_approx)
-  double cert_inflate; // multiplies the certification bound (1; tests force the fallback)
-  int gate_exact;      // 1: the exact scan kernels run only if some slot was uncertain
   int k1_block_log2;  // particles per predict CTA (KernelSet::kt), log2
   // ---- advection-diffusion model (grid m x m, d = m^2; kernels_advdiff.cu) ----
   int adv_m, adv_d;

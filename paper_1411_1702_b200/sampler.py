@@ -337,19 +337,6 @@ class GpuSampler:
         return dict(zip(names.value.decode().split(","), ms[:n.value].tolist()))
 
     # -- BASELINE config 5 microbenchmark (model "payload64") ------------
-    def debug_cert_inflate(self, factor: float):
-        """Test knob: multiply the certification bound of the approximate CDF
-        (a huge factor sends every slot through the exact fallback)."""
-        self.lib.pfsmc_gpu_debug_cert_inflate.restype = C.c_int
-        self._check(self.lib.pfsmc_gpu_debug_cert_inflate(self.h, C.c_double(factor)))
-
-    def uncertain_slots(self) -> int:
-        """Slots of the last step whose ancestor needed the exact fallback."""
-        self.lib.pfsmc_gpu_uncertain_slots.restype = C.c_int
-        v = C.c_uint32()
-        self._check(self.lib.pfsmc_gpu_uncertain_slots(self.h, C.byref(v)))
-        return int(v.value)
-
     def c5_set_logweights(self, sigma: float, key: int):
         self._check(self.lib.pfsmc_gpu_c5_set_logweights(self.h, C.c_double(sigma), C.c_uint64(key)))
 

@@ -254,37 +254,6 @@ def test_lockstep_lotka_volterra(name, kw, n, steps, m):
     gpu.close()
 
 
-@pytest.mark.parametrize("inflate", [1.0, 1e6, 1e30])
-def test_certified_cdf_and_exact_fallback_give_the_reference_ancestors(inflate):
-    """The step's ancestors come from the certified approximate CDF; slots it
-    cannot certify take the exact sequential CDF. Inflating the certification
-    bound sends some (1e6) or all (1e30: the list overflows, every slot is
-    re-served) slots through the exact fallback: the ancestors and the whole
-    step stay the oracle's (lock-step, 2^16 particles, AM2)."""
-    from paper_1411_1702_b200 import problems
-    kw = dict(model="lv", family="am", order=2, h=0.1, seed=41)
-    n, steps = 1 << 16, 3
-    sc = StepConfig(**kw, obs_idx=(0, 1), sigma=0.05)
-    prob = problems.lotka_volterra(particles=n, T=steps, seed=41)
-    ens = O.init_uniform("lv", n, 41, **prob.prior)
-    gpu = _sampler(sc, n)
-    gpu.debug_cert_inflate(inflate)
-    tp, unc = 0.0, []
-    for j in range(1, steps + 1):
-        gpu.set_ensemble(_to_gpu_ens(ens))
-        t1 = prob.times[j - 1]
-        row = gpu.pf_step(prob.ys[j - 1], j, tp, t1)
-        unc.append(gpu.uncertain_slots())
-        trace_o, dg = O.pf_step(sc, ens, prob.ys[j - 1], j, tp, t1, diag=True)
-        _compare_step(gpu, ens, trace_o, dg, row)
-        tp = t1
-    if inflate == 1e30:
-        assert min(unc) >= n - 8, unc  # all but slots whose ancestor is 0 (one-term sum: exact)
-    elif inflate == 1e6:
-        assert 0 < max(unc) < n, unc
-    gpu.close()
-
-
 def _golden_cases():
     return sorted(f[3:-4] for f in os.listdir(GOLD) if f.startswith("pf_") and f.endswith(".npz"))
 
