@@ -220,10 +220,12 @@ constexpr int k3_min_blocks() {
   return SmemHistOf<M>::value ? 3 : (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1) * (kThreads / BlockOf<M>::value);
 }
 // Dynamic shared memory of a K1 / K3 CTA: the LMM history columns.
+// (+ P + D doubles per thread: the K3 proliferation / innovation normals)
 template <class M, int FAM, int ORD>
 constexpr int hist_smem_bytes() {
   using Pr = Propagator<M, FAM, ORD>;
-  return Pr::kSmemHist ? Pr::kHistDoubles * BlockOf<M>::value * static_cast<int>(sizeof(double)) : 0;
+  return Pr::kSmemHist ? (Pr::kHistDoubles + M::P + M::D) * BlockOf<M>::value * static_cast<int>(sizeof(double))
+                       : 0;
 }
 
 template <class M, int FAM, int ORD>
@@ -630,7 +632,19 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
     double z[P];
     // large models (d >= 6): Philox rounds as a loop (code size, not speed)
     constexpr bool kRoll = D >= 6;
-    stream_normals<P, kRoll>(c.seed, sp.j, c.n0 + n, kProliferate, z);
+    using Pr = Propagator<M, FAM, ORD>;
+    // shared-memory-history models: both normal sets drawn up front into a
+    // shared-memory column (one instance of the Box-Muller code, nothing live
+    // in registers through the propagation)
+    double* zcol = hist_smem + (Pr::kSmemHist ? Pr::kHistDoubles * KT : 0) + threadIdx.x;
+    if constexpr (Pr::kSmemHist) {
+      stream_normals_strided<P>(c.seed, sp.j, c.n0 + n, kProliferate, zcol, KT);
+      stream_normals_strided<D>(c.seed, sp.j, c.n0 + n, kInnovate, zcol + P * KT, KT);
+#pragma unroll
+      for (int q = 0; q < P; ++q) z[q] = zcol[q * KT];
+    } else {
+      stream_normals<P, kRoll>(c.seed, sp.j, c.n0 + n, kProliferate, z);
+    }
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       tb[r] = c.a * tu[r] + c.one_minus_a * sK[r];
@@ -652,7 +666,12 @@ __global__ void __launch_bounds__(BlockOf<M>::value, k3_min_blocks<M>()) k_updat
     double ll = kNegInf;
     if (status == kOk) {
       double zi[D];
-      stream_normals<D, kRoll>(c.seed, sp.j, c.n0 + n, kInnovate, zi);
+      if constexpr (Pr::kSmemHist) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) zi[k] = zcol[(P + k) * KT];
+      } else {
+        stream_normals<D, kRoll>(c.seed, sp.j, c.n0 + n, kInnovate, zi);
+      }
 #pragma unroll
       for (int k = 0; k < D; ++k) xr[k] += sqrt(gamma[k]) * zi[k];
       ll = loglik<M>(c, sp, xr);

@@ -171,6 +171,36 @@ PF_HD void stream_normals(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpos
   }
 }
 
+// stream_normals written to a strided buffer (out[k * stride]), the Philox
+// blocks and the Box-Muller pairs as a loop: one instance of the
+// transcendental code instead of one per pair (kernels whose instruction
+// footprint matters; the buffer is a shared-memory column). Same values.
+#ifdef __CUDACC__
+template <int K>
+__device__ __forceinline__ void stream_normals_strided(uint64_t seed, uint64_t j, uint64_t n, uint64_t purpose,
+                                                       double* out, int stride) {
+  constexpr int kPairs = (K + 1) / 2;
+  constexpr int kBlocks = (2 * kPairs + 3) / 4;
+#pragma unroll 1
+  for (int b = 0; b < kBlocks; ++b) {
+    const U64x4 blk = philox4x64<true>(static_cast<uint64_t>(b), j, n, purpose, seed, kKeyConstant);
+#pragma unroll 1
+    for (int l = 0; l < 2; ++l) {
+      const int q = 2 * b + l;
+      if (q >= kPairs) break;
+      const uint64_t w1 = l ? blk.v[2] : blk.v[0], w2 = l ? blk.v[3] : blk.v[1];
+      const double u1 = (static_cast<double>(w1 >> 11) + 1.0) * 0x1.0p-53;
+      const double u2 = u64_to_uniform(w2);
+      const double r = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincospi(2.0 * u2, &sn, &cs);
+      out[(2 * q) * stride] = r * cs;
+      if (2 * q + 1 < K) out[(2 * q + 1) * stride] = r * sn;
+    }
+  }
+}
+#endif
+
 // The resampling uniform of slot n at time j (filter.cpp:171-172).
 PF_HD double resample_uniform(uint64_t seed, uint64_t j, uint64_t n) {
   return u64_to_uniform(philox4x64(0, j, n, kResample, seed, kKeyConstant).v[0]);
