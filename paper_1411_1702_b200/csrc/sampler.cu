@@ -15,6 +15,8 @@
 // aligned, double-buffered) plus SoA lw / ll_bar / lg / cdf arrays: streamed
 // kernels read records with vector loads and the random ancestor gather
 // touches ceil(8R/32) sectors instead of d+p+1.
+#include <cstdlib>
+
 #include "sampler_internal.cuh"
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
@@ -150,9 +152,17 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
   nvtxRangePop();
   if (timed) CK(cudaEventRecord(ev[1], st));
   nvtxRangePushA("resample (exact CDF scan + ancestor search)");
-  launch_scan(c, s->ntiles, st, 1);
-  if (timed) CK(cudaEventRecord(ev[2], st));
-  launch_scan(c, s->ntiles, st, 2);
+  {
+    // up to 2^22 particles the fitness vector fits L2: the records pass stores
+    // g into the CDF buffer and the CDF pass reads it back instead of
+    // recomputing the exps (each tile only reads and then rewrites its own range)
+    Ctx cp = c, cc = c;
+    cp.store_g = s->N <= (1LL << 22) && !c.gin;
+    if (cp.store_g) cc.gin = c.cdf;
+    launch_scan(cp, s->ntiles, st, 1);
+    if (timed) CK(cudaEventRecord(ev[2], st));
+    launch_scan(cc, s->ntiles, st, 2);
+  }
   if (timed) CK(cudaEventRecord(ev[3], st));
   if (s->ks->block_model())
     launch_search_only(c, s->grid, st);  // the update CTAs gather their ancestor themselves
@@ -401,7 +411,11 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     s->N = static_cast<long long>(cfg->particles / world);
     s->grid = static_cast<int>((s->N + kThreads - 1) / kThreads);
     s->grid_m = static_cast<int>((s->N + s->ks->kt - 1) / s->ks->kt);
-    const int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
+    int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
+    if (const char* e = std::getenv("PFSMC_GPU_TILE_LOG2")) {  // experiments only (11 or 12)
+      const int v = std::atoi(e);
+      if (v == 11 || v == 12) tile_log2 = v;
+    }
     s->ntiles = static_cast<int>((s->N + (1LL << tile_log2) - 1) >> tile_log2);
     Ctx& c = s->ctx;
     c.N = static_cast<int>(s->N);
@@ -453,6 +467,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.cdf = s->dalloc<double>(N);
     c.anc = s->dalloc<unsigned>(N);
     c.tile_log2 = tile_log2;
+    c.store_g = 0;
     c.k1_block_log2 = ilog2(s->ks->kt);
     // the ancestor search's tables (segment ends, guide): small, read with
     // an L2 evict-last policy so the one-shot gathers stream past them. (A

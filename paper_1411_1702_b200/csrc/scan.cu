@@ -546,8 +546,9 @@ __global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
       const int e = i * kThreads + threadIdx.x;
       const long long k = base + e;
       double g = 0.0;
-      if (k < c.N) g = c.gin ? x[i] : exp(x[i] - lse);  // S3 recomputes it (bitwise)
+      if (k < c.N) g = c.gin ? x[i] : exp(x[i] - lse);  // S3 recomputes it (bitwise) or reads it back
       sm.g[TC::sidx(e)] = g;
+      if (c.store_g && k < c.N) __stcg(&c.cdf[k], g);  // L2-resident sizes: S3 reads g instead of exp
     }
   }
   __syncthreads();

@@ -102,6 +102,7 @@ struct Ctx {
   double rtol;       // adaptive BDF(1,2) tolerance (IntegratorSpec.rtol)
   int coarse_bits;  // coarse guide has 2^coarse_bits buckets
   int tile_log2;    // exact-CDF tile = 2^tile_log2 elements (10 or 12)
+  int store_g;      // k_scan_pieces also stores g = exp(lg - lse) into cdf (read back by k_scan_cdf as gin)
   int k1_block_log2;  // particles per predict CTA (KernelSet::kt), log2
   // ---- advection-diffusion model (grid m x m, d = m^2; kernels_advdiff.cu) ----
   int adv_m, adv_d;
