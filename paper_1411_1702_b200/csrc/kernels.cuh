@@ -781,7 +781,8 @@ __global__ void __launch_bounds__(kThreads) k_finish_moments(Ctx c, const double
 #pragma unroll
   for (int k = 0; k < P; ++k) K[k] = st.mu[k];
   __syncthreads();
-  combine_partials<V, true>(gp, ngroups, fin, scratch);
+  // the single handle's final level (tree_reduce_last): one warp, same order
+  if (threadIdx.x < 32) combine_partials_warp<V, true>(gp, ngroups, fin);
   __syncthreads();
   if (threadIdx.x == 0) {
     finalize_moments<M>(c, fin, K, (flags & 1) != 0, (flags & 2) != 0);

@@ -163,19 +163,36 @@ __device__ __forceinline__ void combine_partials(const double* in, int count, do
   }
 }
 
-// combine_partials out of line: the last-block paths of kernels with many
-// moment values (their unrolled shuffle trees would otherwise sit in the
-// middle of the hot kernel's code).
-template <int V, bool SQ, int NT>
-__device__ __noinline__ void combine_partials_cold(const double* in, int count, double* out, double* scratch) {
-  combine_partials<V, SQ, NT>(in, count, out, scratch);
-}
-template <int V, bool SQ, int NT>
-__device__ __forceinline__ void combine_partials_sel(const double* in, int count, double* out, double* scratch) {
-  if constexpr (V >= 16)
-    combine_partials_cold<V, SQ, NT>(in, count, out, scratch);
-  else
-    combine_partials<V, SQ, NT>(in, count, out, scratch);
+// combine_partials by ONE warp (the tree levels below run on the critical
+// tail of their kernel: the last block's combine is the only work left on the
+// GPU, so fewer barriers and no idle warps shorten the step): lane l folds
+// partials l, l + 32, ... in order (rescaled to the common max), then a fixed
+// butterfly. Lane 0 writes out[]. Fixed shape => bitwise reproducible.
+template <int V, bool SQ>
+__device__ __noinline__ void combine_partials_warp(const double* in, int count, double* out) {
+  const int lane = threadIdx.x & 31;
+  double m = -INFINITY;
+  for (int i = lane; i < count; i += 32) m = nan_free_max(m, __ldcg(in + i * (V + 1)));
+  const double M = warp_max(m);
+  double v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = 0.0;
+  for (int i = lane; i < count; i += 32) {
+    const double mi = __ldcg(in + i * (V + 1));
+    const double c = (mi == -INFINITY) ? 0.0 : exp(mi - M);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const double w = (SQ && k == V - 1) ? c * c : c;
+      v[k] += w * __ldcg(in + i * (V + 1) + 1 + k);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+    out[0] = M;
+#pragma unroll
+    for (int k = 0; k < V; ++k) out[1 + k] = v[k];
+  }
 }
 
 // Two-level last-block-done tree. Every block calls this after writing its
@@ -199,19 +216,21 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   const int ngroups = (nblocks + kGroup - 1) / kGroup;
   const int g = blockIdx.x / kGroup;
   const int gsize = min(kGroup, nblocks - g * kGroup);
-  // the block partial was written by thread 0 only: it alone fences
+  // the block partial was written by thread 0 only: its arrival is one
+  // acquire-release atomic (publishes the partial, and the last arriver
+  // acquires everyone's), cheaper than a full fence before a relaxed atomic
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(&counters[g], 1u);
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&counters[g]) : "memory");
     s_flag = (old == static_cast<unsigned>(gsize - 1));
     if (s_flag) counters[g] = 0;
   }
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials_sel<V, SQ, NT>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize,
-                                  group_part + g * (V + 1), scratch);
+  if (threadIdx.x < 32)
+    combine_partials_warp<V, SQ>(part + static_cast<size_t>(g) * kGroup * (V + 1), gsize, group_part + g * (V + 1));
   __syncthreads();
   hook(g, gsize);
   if (!final_level) return false;  // sharded: the group partials are exported
@@ -225,7 +244,7 @@ __device__ __forceinline__ bool tree_reduce_last(double* part, double* group_par
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  combine_partials_sel<V, SQ, NT>(group_part, ngroups, final_out, scratch);
+  if (threadIdx.x < 32) combine_partials_warp<V, SQ>(group_part, ngroups, final_out);
   __syncthreads();
   return true;
 }

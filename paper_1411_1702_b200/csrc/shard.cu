@@ -12,7 +12,7 @@ __global__ void __launch_bounds__(kThreads) k_finish_lse(Ctx c, const double* gp
   __shared__ double fin[2];
   if (grid_error(c)) return;
   __shared__ double s_lse;
-  combine_partials<1, false>(gp, ngroups, fin, scratch);
+  if (threadIdx.x < 32) combine_partials_warp<1, false>(gp, ngroups, fin);  // as tree_reduce_last
   __syncthreads();
   if (threadIdx.x == 0) {
     const double mx = fin[0];

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python profiles/ab_lv.py ab/base.so ab/wcomb.so 3 > gpurun_out/ab_wcomb.txt 2>&1
+timeout 600 python profiles/ab_chain.py ab/base.so ab/wcomb.so 2 4194304 chain exact > gpurun_out/ab_wcomb_chain.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_r3c.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_r3c.log
