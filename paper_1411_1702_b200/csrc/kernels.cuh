@@ -213,11 +213,13 @@ __device__ __forceinline__ void tile_prefixes(const Ctx& c, double lse, const do
 // shared-memory-history chain: 3 CTAs of 128)
 template <class M>
 constexpr int k1_min_blocks() {
-  return SmemHistOf<M>::value ? 3 : (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1) * (kThreads / BlockOf<M>::value);
+  return MinBlocksOf<M>::k1 ? MinBlocksOf<M>::k1
+                            : (M::ID == 5 ? 2 : M::D <= 2 ? 6 : M::D <= 3 ? 4 : 1) * (kThreads / BlockOf<M>::value);
 }
 template <class M>
 constexpr int k3_min_blocks() {
-  return SmemHistOf<M>::value ? 3 : (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1) * (kThreads / BlockOf<M>::value);
+  return MinBlocksOf<M>::k3 ? MinBlocksOf<M>::k3
+                            : (M::ID == 5 ? 2 : M::D <= 2 ? 4 : M::D <= 3 ? 3 : 1) * (kThreads / BlockOf<M>::value);
 }
 // Dynamic shared memory of a K1 / K3 CTA: the LMM history columns.
 // (+ P + D doubles per thread: the K3 proliferation / innovation normals)
