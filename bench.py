@@ -477,37 +477,44 @@ def bench_workloads(local, fp64):
     # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal: the filter runs the
     # log-spaced grid from j = 1 and is timed in windows spread along it (early,
     # mid, stiff), since the cost per step grows with the Newton iterations
+    import dataclasses
     n3 = 1 << 22
     prob = problems.robertson(particles=n3, T=400, seed=1)
-    g = GpuSampler("robertson", _cfg(prob), prob.obs, device=local)
-    prob.init(g)
-    out["c3_robertson"] = c3 = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4",
-                                "likelihood": "lognormal (BASELINE extension)", "windows": {}}
-    st3 = torch.cuda.ExternalStream(g.stream_handle, device=local)
-    j3, tp3 = 0, 0.0
-    tot_ms, tot_steps, tot_it = 0.0, 0, 0.0
-    for w0 in C3_WINDOWS:
-        while j3 < w0 - 1:  # advance untimed to the window
-            j3 += 1
-            t1 = prob.times[j3 - 1]
-            g.pf_step(prob.ys[j3 - 1], j3, tp3, t1, h=prob.h_for(tp3, t1))
-            tp3 = t1
-        ms, it = _timed_steps(g, prob, 5, 0, st3, j0=j3, t0=tp3)
-        j3 += 5
-        tp3 = prob.times[j3 - 1]
-        t = sum(ms) / len(ms)
-        ipp = float(np.mean(it)) / n3
-        c3["windows"][f"j={w0}..{w0 + 4}"] = {
-            "t_obs": [float(prob.times[w0 - 1]), float(prob.times[w0 + 3])], "ms_per_step": t,
-            "particle_steps_per_s": n3 / (t / 1e3), "newton_iterations_per_particle_step": ipp,
-            "newton_iterations_per_solve": ipp / 4.0}
-        tot_ms += sum(ms)
-        tot_steps += len(ms)
-        tot_it += float(np.sum(it))
-    g.close()
-    c3["ms_per_step"] = tot_ms / tot_steps
-    c3["particle_steps_per_s"] = n3 / (c3["ms_per_step"] / 1e3)
-    c3["newton_iterations_per_particle_step"] = tot_it / tot_steps / n3
+
+    def c3_run(arith):
+        g = GpuSampler("robertson", dataclasses.replace(prob.cfg, arithmetic=arith), prob.obs, device=local)
+        prob.init(g)
+        r = {"particles": n3, "integrator": "bdf2, m=2, newton_max_iter=4", "arithmetic": arith,
+             "likelihood": "lognormal (BASELINE extension)", "windows": {}}
+        st3 = torch.cuda.ExternalStream(g.stream_handle, device=local)
+        j3, tp3 = 0, 0.0
+        tot_ms, tot_steps, tot_it = 0.0, 0, 0.0
+        for w0 in C3_WINDOWS:
+            while j3 < w0 - 1:  # advance untimed to the window
+                j3 += 1
+                t1 = prob.times[j3 - 1]
+                g.pf_step(prob.ys[j3 - 1], j3, tp3, t1, h=prob.h_for(tp3, t1))
+                tp3 = t1
+            ms, it = _timed_steps(g, prob, 5, 0, st3, j0=j3, t0=tp3)
+            j3 += 5
+            tp3 = prob.times[j3 - 1]
+            t = sum(ms) / len(ms)
+            ipp = float(np.mean(it)) / n3
+            r["windows"][f"j={w0}..{w0 + 4}"] = {
+                "t_obs": [float(prob.times[w0 - 1]), float(prob.times[w0 + 3])], "ms_per_step": t,
+                "particle_steps_per_s": n3 / (t / 1e3), "newton_iterations_per_particle_step": ipp,
+                "newton_iterations_per_solve": ipp / 4.0}
+            tot_ms += sum(ms)
+            tot_steps += len(ms)
+            tot_it += float(np.sum(it))
+        g.close()
+        r["ms_per_step"] = tot_ms / tot_steps
+        r["particle_steps_per_s"] = n3 / (r["ms_per_step"] / 1e3)
+        r["newton_iterations_per_particle_step"] = tot_it / tot_steps / n3
+        return r
+
+    out["c3_robertson"] = c3 = c3_run("exact")
+    c3["fast_arithmetic"] = c3_run("fast")
     c3["cpu_reference"] = _cpu_ref_windows(
         prob, dict(family="bdf", order=2, a=0.99, obs_idx=(0, 2), sigma=0.02, newton_max_iter=4))
     # config 4: 8-compartment chain, 2^24, BDF3 m=3, both arithmetic variants
