@@ -313,6 +313,7 @@ def gather_peak(device, n_rec=1 << 25):
 
 C3_WINDOWS = (50, 200, 320)
 ARITH = "exact"  # --arithmetic: the device arithmetic variant (pfsmc_gpu_config.arithmetic)
+SHARD_FAILURE = []  # N > 1: why the sharded path fell back to replicas (if it did)
 
 
 def _cfg(prob):
@@ -653,6 +654,8 @@ def run_sharded(args, world, rank, local):
     from paper_1411_1702_b200 import problems
     from paper_1411_1702_b200.sharded import GpuShard, ShardedFilter, TorchComm
 
+    if os.environ.get("PFSMC_BENCH_FORCE_SHARD_FAIL"):  # exercises the replicas fallback
+        raise RuntimeError("forced sharded-path failure (PFSMC_BENCH_FORCE_SHARD_FAIL)")
     cfgno = args.config
     if cfgno == 5:
         return run_sharded_c5(args, world, rank, local)
@@ -895,7 +898,16 @@ def main():
             sk.close()
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         if not args.replicas:
-            return run_sharded(args, world, rank, local)
+            try:
+                return run_sharded(args, world, rank, local)
+            except Exception as e:  # noqa: BLE001
+                # the scaling line must still be produced: independent replicas
+                # (no collectives in the data path), with the failure recorded
+                print(f"[bench] sharded path failed on rank {rank}: {e!r}; falling back to replicas",
+                      file=sys.stderr, flush=True)
+                SHARD_FAILURE.append(repr(e)[:300])
+                if not dist.is_initialized():
+                    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     n = args.particles
     T = min(T_OBS, 2 * args.steps + args.warmup + args.e2e_steps + 4)
     prob = problems.lotka_volterra(particles=n, T=T_OBS, seed=1)
@@ -1005,7 +1017,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RK4 Lotka-Volterra observations, uniform priors)",
-            "config": _lv_config(world, n), "arithmetic": ARITH,
+            "config": {**_lv_config(world, n),
+                       **({"sharded_path_failed": SHARD_FAILURE[0]} if SHARD_FAILURE else {})},
+            "arithmetic": ARITH,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind,
