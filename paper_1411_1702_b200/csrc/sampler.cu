@@ -15,8 +15,6 @@
 // aligned, double-buffered) plus SoA lw / ll_bar / lg / cdf arrays: streamed
 // kernels read records with vector loads and the random ancestor gather
 // touches ceil(8R/32) sectors instead of d+p+1.
-#include <cstdlib>
-
 #include "sampler_internal.cuh"
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
@@ -411,11 +409,9 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     s->N = static_cast<long long>(cfg->particles / world);
     s->grid = static_cast<int>((s->N + kThreads - 1) / kThreads);
     s->grid_m = static_cast<int>((s->N + s->ks->kt - 1) / s->ks->kt);
-    int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
-    if (const char* e = std::getenv("PFSMC_GPU_TILE_LOG2")) {  // experiments only (11 or 12)
-      const int v = std::atoi(e);
-      if (v == 11 || v == 12) tile_log2 = v;
-    }
+    // 2048-element tiles up to 2^22 (4096 at 2^20 measured 10% slower: the
+    // per-thread serial chains double, profiles/r02_notes.md)
+    const int tile_log2 = s->N <= (1LL << 22) ? 11 : 12;
     s->ntiles = static_cast<int>((s->N + (1LL << tile_log2) - 1) >> tile_log2);
     Ctx& c = s->ctx;
     c.N = static_cast<int>(s->N);
