@@ -990,7 +990,7 @@ def main():
         t0 = time.perf_counter()
         gpu.set_ensemble(host_ens)
         gpu.pf_step(ys_pinned[j - 1], j, prob.times[j - 2], prob.times[j - 1])
-        host_ens = gpu.get_ensemble()
+        gpu.get_ensemble(out=host_ens)  # in place, as filter::pf_step mutates the caller's Ensemble
         lit_s += time.perf_counter() - t0
     ens_bytes = 8 * n * (D + P + 1) + 8 * (P + P * P)
     e2e["literal_ensemble_step"] = {

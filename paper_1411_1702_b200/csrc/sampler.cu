@@ -38,6 +38,63 @@ __global__ void k_pack(Ctx c, int d, int p, const double* states, const double* 
   }
 }
 
+// The injected weights' gate (weighted_mean_cov, linalg.cpp:395-409): every
+// w = exp(logw) finite and >= 0, and their sum; per-thread compensated sums
+// over a grid-stride range, then a fixed-order combine by the last block
+// (deterministic; within ~1e-15 of the reference's sequential Kahan sum, far
+// inside the 1e-12 gate). out[0] = sum, out[1] = 1 if any weight is invalid.
+__global__ void __launch_bounds__(kThreads) k_weight_gate(const double* logw, long long n, double* part,
+                                                          unsigned* cnt, double* out) {
+  __shared__ double ss[kThreads];
+  __shared__ int s_last;
+  double sum = 0.0, comp = 0.0;
+  int bad = 0;
+  for (long long i = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * kThreads) {
+    const double w = exp(logw[i]);
+    bad |= !(w >= 0.0) || !isfinite(w);
+    const double y = w - comp, t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+  bad = __syncthreads_or(bad);
+  ss[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0, cb = 0.0;
+    for (int k = 0; k < kThreads; ++k) {
+      const double y = ss[k] - cb, t = b + y;
+      cb = (t - b) - y;
+      b = t;
+    }
+    part[2 * blockIdx.x] = b;
+    part[2 * blockIdx.x + 1] = bad;
+    __threadfence();
+    const unsigned old = atomicAdd(cnt, 1u);
+    s_last = old == gridDim.x - 1;
+    if (s_last) *cnt = 0;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  double b = 0.0, cb = 0.0, anybad = 0.0;
+  for (unsigned k = 0; k < gridDim.x; ++k) {
+    const double y = __ldcg(&part[2 * k]) - cb, t = b + y;
+    cb = (t - b) - y;
+    b = t;
+    anybad += __ldcg(&part[2 * k + 1]);
+  }
+  out[0] = b;
+  out[1] = anybad;
+}
+
+// logw_n = lw_n - lse_w (update_weights' normalisation, filter.cpp:220) into
+// a staging buffer for the read-back.
+__global__ void k_normalized_logw(const double* lw, const DevState* st, long long n, double* out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = lw[i] - st->lse_w;
+}
+
 __global__ void k_flush(double* buf, long long n) {
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -240,22 +297,34 @@ void harvest_timing(pfsmc_gpu_sampler* s) {
 // proliferate (linalg.cpp:474-480, filter.cpp:185-187). Run on the host at
 // injection; the failure is raised by the next step, where the reference
 // raises it.
-void check_injected(pfsmc_gpu_sampler* s, const double* logw, const double* cov_u) {
+void ensure_staging(pfsmc_gpu_sampler* s) {
+  if (s->stage_x) return;
+  const size_t N = static_cast<size_t>(s->N);
+  s->stage_x = s->dalloc<double>(N * s->d);
+  s->stage_t = s->dalloc<double>(N * s->p);
+  s->stage_w = s->dalloc<double>(N);
+  s->gate_part = s->dalloc<double>(2 * static_cast<size_t>(s->num_sms) * 4 + 2);
+  s->gate_cnt = s->dalloc<unsigned>(1);
+  CK(cudaMemset(s->gate_cnt, 0, sizeof(unsigned)));
+  s->gate_out = s->dalloc<double>(2);
+}
+
+// dev_logw: the injected log-weights already on the device (ctx.lw).
+void check_injected(pfsmc_gpu_sampler* s, const double* dev_logw, const double* cov_u) {
   s->pending_code = 0;
   s->pending_msg.clear();
-  const size_t N = static_cast<size_t>(s->N);
-  double wsum = 0.0, comp = 0.0;  // Kahan sum, as the reference
-  for (size_t i = 0; i < N; ++i) {
-    const double w = std::exp(logw[i]);
-    if (w < 0.0 || !std::isfinite(w)) {
-      s->pending_code = PFSMC_GPU_ERR_CONFIG;
-      s->pending_msg = "weighted_mean_cov: weights must be nonnegative";
-      return;
-    }
-    const double yk = w - comp;
-    const double tk = wsum + yk;
-    comp = (tk - wsum) - yk;
-    wsum = tk;
+  ensure_staging(s);
+  const int g = static_cast<int>(std::min<long long>((s->N + kThreads - 1) / kThreads, s->num_sms * 4LL));
+  k_weight_gate<<<g, kThreads, 0, s->stream>>>(dev_logw, s->N, s->gate_part, s->gate_cnt, s->gate_out);
+  CK(cudaGetLastError());
+  double res[2];
+  CK(cudaMemcpyAsync(res, s->gate_out, sizeof(res), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  const double wsum = res[0];
+  if (res[1] != 0.0) {
+    s->pending_code = PFSMC_GPU_ERR_CONFIG;
+    s->pending_msg = "weighted_mean_cov: weights must be nonnegative";
+    return;
   }
   // a shard holds part of the weights: the gate is the global filter's (the
   // caller's, ShardedFilter.set_ensemble)
@@ -558,12 +627,13 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
   return guarded([&] {
     const size_t N = static_cast<size_t>(s->N);
     const int d = s->d, p = s->p;
-    double* tmp_x = s->dalloc<double>(N * d);
-    double* tmp_t = s->dalloc<double>(N * p);
+    ensure_staging(s);  // persistent device staging (no allocation per call)
+    double* tmp_x = s->stage_x;
+    double* tmp_t = s->stage_t;
     CK(cudaMemcpyAsync(tmp_x, states, sizeof(double) * N * d, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(tmp_t, params_u, sizeof(double) * N * p, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->ctx.lw, logw, sizeof(double) * N, cudaMemcpyHostToDevice, s->stream));
-    check_injected(s, logw, cov_u);
+    check_injected(s, s->ctx.lw, cov_u);
     DevState h{};
     CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
@@ -579,9 +649,6 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     if (!s->shard_api) s->ks->moments(s->ctx, s->grid_m, s->stream, 0);
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
-    cudaFree(tmp_x);
-    cudaFree(tmp_t);
-    s->allocs.resize(s->allocs.size() - 2);
     s->have_ensemble = true;
     return PFSMC_GPU_OK;
   });
@@ -592,24 +659,24 @@ pfsmc_gpu_status pfsmc_gpu_get_ensemble(pfsmc_gpu_sampler* s, double* states, do
   return guarded([&] {
     const size_t N = static_cast<size_t>(s->N);
     const int d = s->d, p = s->p;
-    double* tmp_x = s->dalloc<double>(N * d);
-    double* tmp_t = s->dalloc<double>(N * p);
+    ensure_staging(s);
+    double* tmp_x = s->stage_x;
+    double* tmp_t = s->stage_t;
     k_pack<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, d, p, tmp_x, tmp_t, 1);
     if (states) CK(cudaMemcpyAsync(states, tmp_x, sizeof(double) * N * d, cudaMemcpyDeviceToHost, s->stream));
     if (params_u) CK(cudaMemcpyAsync(params_u, tmp_t, sizeof(double) * N * p, cudaMemcpyDeviceToHost, s->stream));
     DevState h{};
     CK(cudaMemcpyAsync(&h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
-    if (logw) CK(cudaMemcpyAsync(logw, s->ctx.lw, sizeof(double) * N, cudaMemcpyDeviceToHost, s->stream));
+    if (logw) {  // update_weights' lw -= lse (filter.cpp:220) on the device
+      k_normalized_logw<<<s->grid, kThreads, 0, s->stream>>>(s->ctx.lw, s->st, s->N, s->stage_w);
+      CK(cudaMemcpyAsync(logw, s->stage_w, sizeof(double) * N, cudaMemcpyDeviceToHost, s->stream));
+    }
     CK(cudaStreamSynchronize(s->stream));
-    if (logw)
-      for (size_t i = 0; i < N; ++i) logw[i] = logw[i] - h.lse_w;  // update_weights: lw -= lse
+    CK(cudaGetLastError());
     if (mean_u)
       for (int k = 0; k < p; ++k) mean_u[k] = h.mu[k];
     if (cov_u)
       for (int k = 0; k < p * p; ++k) cov_u[k] = h.cov[k];
-    cudaFree(tmp_x);
-    cudaFree(tmp_t);
-    s->allocs.resize(s->allocs.size() - 2);
     return PFSMC_GPU_OK;
   });
 }

@@ -168,6 +168,14 @@ struct pfsmc_gpu_sampler {
   bool c5_fitness_is_lw = false;   // sharded scan phases of a config-5 iteration read lw as the fitness
   unsigned long long* c5_remote = nullptr;  // sharded: records pulled from other GPUs (device counter)
 
+  // the Ensemble& boundary's device staging (set / get_ensemble), allocated once
+  double* stage_x = nullptr;   // N x d states (AoS, the caller's layout)
+  double* stage_t = nullptr;   // N x p params_u
+  double* stage_w = nullptr;   // N normalised logw
+  double* gate_part = nullptr; // k_weight_gate block partials
+  unsigned* gate_cnt = nullptr;
+  double* gate_out = nullptr;
+
   template <typename T>
   T* dalloc(size_t count) {
     void* p = nullptr;
@@ -218,6 +226,7 @@ pfsmc_gpu_status guarded(F&& f) {
 int step_count(double t0, double t1, double h);
 StepParams make_params(pfsmc_gpu_sampler* s, const double* y, uint64_t j, double t_prev, double t_obs, double h);
 void check_error(pfsmc_gpu_sampler* s);
+void ensure_staging(pfsmc_gpu_sampler* s);
 void raise_pending(pfsmc_gpu_sampler* s);
 void clear_error(pfsmc_gpu_sampler* s);
 void ensure_exchange_buffers(pfsmc_gpu_sampler* s);

@@ -250,9 +250,16 @@ class GpuSampler:
              _f64(ens.mean_u, (p,)), _f64(ens.cov_u, (p, p))]
         self._check(self.lib.pfsmc_gpu_set_ensemble(self.h, *[_ptr(x) for x in a]))
 
-    def get_ensemble(self) -> Ensemble:
+    def get_ensemble(self, out: Optional[Ensemble] = None) -> Ensemble:
+        """The resident ensemble in the reference layout; `out` (C-contiguous
+        float64 arrays of the right shapes) is filled in place, as the
+        reference's pf_step mutates the caller's Ensemble (filter.cpp:332)."""
         n, d, p = self.n, self.d, self.p
-        e = Ensemble(np.zeros((n, d)), np.zeros((n, p)), np.zeros(n), np.zeros(p), np.zeros((p, p)))
+        ok = out is not None and all(
+            isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.shape == sh
+            for a, sh in ((out.states, (n, d)), (out.params_u, (n, p)), (out.logw, (n,)), (out.mean_u, (p,)),
+                          (out.cov_u, (p, p))))
+        e = out if ok else Ensemble(np.zeros((n, d)), np.zeros((n, p)), np.zeros(n), np.zeros(p), np.zeros((p, p)))
         self._check(self.lib.pfsmc_gpu_get_ensemble(self.h, _ptr(e.states), _ptr(e.params_u),
                                                      _ptr(e.logw), _ptr(e.mean_u), _ptr(e.cov_u)))
         return e
