@@ -286,7 +286,7 @@ pfsmc_gpu_status pfsmc_gpu_shard_step(pfsmc_gpu_sampler* s, const double* y, uin
  * segment ends, guide, offspring prefix), the caller allgathers them (world x
  * PFSMC_GPU_IPC_BYTES, rank order) and every rank attaches; then each slot
  * pulls its ancestor from the serving rank's memory. */
-#define PFSMC_GPU_IPC_BYTES 512
+#define PFSMC_GPU_IPC_BYTES 640
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out448);
 pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_t* all_handles);
 /* Back to the counted send / receive (if any rank failed to map its peers). */
@@ -333,6 +333,13 @@ pfsmc_gpu_status pfsmc_gpu_shard_offspring_pack(pfsmc_gpu_sampler* s, uint32_t* 
  * whose children cover it, then the update kernel (replaces pack + exchange
  * + shard_update). */
 pfsmc_gpu_status pfsmc_gpu_shard_offspring_pull(pfsmc_gpu_sampler* s);
+/* Offspring counts over peer memory (peers attached) instead of the walk of
+ * every global slot: O(N_local) work per rank. Phases with a barrier across
+ * ranks between them: 0 zero the counts, 1 count this rank's slots into the
+ * ancestors' owners (every rank's CDF tables complete), 2 totals + this
+ * rank's prefix (returns every rank's children, blocking). Then
+ * shard_offspring_pull after a barrier. The native step uses this sequence. */
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_peer(pfsmc_gpu_sampler* s, int phase, uint64_t* totals_out);
 pfsmc_gpu_status pfsmc_gpu_shard_moments(pfsmc_gpu_sampler* s);
 /* flags: 7 completed step, 2 initialisation refresh, 0 injected ensemble. */
 pfsmc_gpu_status pfsmc_gpu_shard_finish_moments(pfsmc_gpu_sampler* s, int flags, double* trace_out);

@@ -600,6 +600,7 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
       s->ooff = s->dalloc<unsigned>(N + 1);
       s->oblk = s->dalloc<unsigned>(N / 2048 + 2);
       s->otot = s->dalloc<unsigned long long>(world);
+      s->ocount = s->dalloc<unsigned long long>(world);
       CK(cudaMallocHost(&s->otot_host, world * sizeof(unsigned long long)));
     }
     if (!shard_api) build_graph(s.get());  // shard handles step through the sharded phases only

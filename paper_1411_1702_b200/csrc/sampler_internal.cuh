@@ -49,6 +49,8 @@ struct PeerTable {
   const unsigned* coarse[kMaxRanks];
   const unsigned* ooff[kMaxRanks];  // offspring mode: exclusive prefix of per-particle offspring counts
   const TileWin* win[kMaxRanks];    // the exact scan's tile windows (read by every rank's resolver)
+  unsigned* ocnt[kMaxRanks];        // offspring mode: per-particle offspring counts (peer atomics)
+  unsigned long long* ocount[kMaxRanks];  // ... each rank's children per serving rank (world entries)
 };
 
 // Migration modes of a sharded step (pfsmc_gpu_shard_set_mode):
@@ -153,6 +155,7 @@ struct pfsmc_gpu_sampler {
   unsigned* ooff = nullptr;        // their exclusive prefix (N_local + 1; [N_local] = this rank's children)
   unsigned* oblk = nullptr;        // scan block sums
   unsigned long long* otot = nullptr;       // children per rank (world), from the global walk
+  unsigned long long* ocount = nullptr;     // peer counting: this rank's slots per serving rank (world)
   unsigned long long* otot_host = nullptr;  // pinned mirror
   // config 5, bucketed ancestor search (c5.cu; allocated on first use)
   int c5_search = 0;               // PFSMC_GPU_C5_SEARCH_GUIDE / _BUCKETED

@@ -299,6 +299,36 @@ __global__ void __launch_bounds__(kThreads) k_offspring_pack(Ctx c, const unsign
   }
 }
 
+// Offspring counts without the global walk (peer memory): each rank draws
+// only ITS slots' uniforms, finds the serving rank and the ancestor in that
+// rank's tables (warp-cooperative search over peer memory) and increments the
+// ancestor's count on its owner with a peer atomic; its slots per serving rank
+// go to its own `ocount`. O(N_local) per rank instead of O(N_global); the
+// counts are the same integers as the walk's (every slot counted once).
+__global__ void __launch_bounds__(kThreads) k_offspring_count_peer(Ctx c, PeerTable pt, unsigned long long* ocount) {
+  if (grid_error(c)) return;
+  const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
+  const bool mine = n < c.N;
+  const double u = mine ? resample_uniform(c.seed, c.sp->j, c.n0 + n) : -1.0;
+  const int r = mine ? serving_rank(c, u) : 0;
+  const int ntl = c.ntiles;
+  const SearchView v{pt.coarse[r], pt.seg_end[r], pt.cdf[r], c.gtile_info[(r + 1) * ntl - 1].y};
+  const unsigned a = find_ancestor_warp_view(c, v, u);
+  if (mine) atomicAdd(pt.ocnt[r] + a, 1u);
+  const unsigned grp = __match_any_sync(0xffffffffu, mine ? r : -1);
+  if (mine && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&ocount[r], static_cast<unsigned long long>(__popc(grp)));
+}
+
+// Children per rank, identical on every rank: otot[q] = sum over ranks of
+// their slots served by q (every rank's ocount, read over peer memory).
+__global__ void k_offspring_totals_peer(Ctx c, PeerTable pt, unsigned long long* otot) {
+  const int q = threadIdx.x;
+  if (q >= c.world) return;
+  unsigned long long t = 0;
+  for (int r = 0; r < c.world; ++r) t += __ldcg(&pt.ocount[r][q]);
+  otot[q] = t;
+}
+
 // Peer-memory path: each slot of this rank pulls its child's ancestor from
 // the rank whose children cover that position (mostly itself).
 __global__ void __launch_bounds__(kThreads) k_offspring_pull(Ctx c, PeerTable pt, const unsigned long long* otot) {
@@ -376,6 +406,16 @@ void ensure_exchange_buffers(pfsmc_gpu_sampler* s) {
 
 // Offspring mode, device part: the global walk (per-particle counts of this
 // rank, children per rank) and the prefix of the counts. Enqueued only.
+// Exclusive prefix of this rank's per-particle offspring counts (ooff).
+static void enqueue_offspring_prefix(pfsmc_gpu_sampler* s) {
+  const long long N = s->N;
+  const int nb = static_cast<int>(N / kOffBlock + 1);
+  k_off_blocksum<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk);
+  k_off_scan_blocks<<<1, 1024, 0, s->stream>>>(s->oblk, nb);
+  k_off_apply<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk, s->ooff);
+}
+
+// Counts by the walk of every global slot (no peer memory needed).
 static void enqueue_offspring(pfsmc_gpu_sampler* s) {
   const long long N = s->N;
   CK(cudaMemsetAsync(s->ocnt, 0, sizeof(unsigned) * (N + 1), s->stream));
@@ -383,10 +423,25 @@ static void enqueue_offspring(pfsmc_gpu_sampler* s) {
   const long long nglob = s->ctx.n_glob;
   const int g = static_cast<int>(std::min<long long>((nglob + kThreads - 1) / kThreads, 148LL * 16));
   k_offspring_walk<<<g, kThreads, 0, s->stream>>>(s->ctx, s->ocnt, s->otot);
-  const int nb = static_cast<int>(N / kOffBlock + 1);
-  k_off_blocksum<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk);
-  k_off_scan_blocks<<<1, 1024, 0, s->stream>>>(s->oblk, nb);
-  k_off_apply<<<nb, kThreads, 0, s->stream>>>(s->ocnt, N, s->oblk, s->ooff);
+  enqueue_offspring_prefix(s);
+  CK(cudaGetLastError());
+}
+
+// Counts over peer memory, three phases separated by barriers across ranks:
+// 0 zero this rank's counts (before the barrier that precedes any rank's
+// counting), 1 count this rank's slots into the ancestors' owners (every
+// rank's CDF tables complete), 2 (every increment done) the totals and the
+// prefix of this rank's counts.
+static void enqueue_offspring_peer(pfsmc_gpu_sampler* s, int phase) {
+  if (phase == 0) {
+    CK(cudaMemsetAsync(s->ocnt, 0, sizeof(unsigned) * (s->N + 1), s->stream));
+    CK(cudaMemsetAsync(s->ocount, 0, sizeof(unsigned long long) * s->world, s->stream));
+  } else if (phase == 1) {
+    k_offspring_count_peer<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, s->peers, s->ocount);
+  } else {
+    k_offspring_totals_peer<<<1, 32, 0, s->stream>>>(s->ctx, s->peers, s->otot);
+    enqueue_offspring_prefix(s);
+  }
   CK(cudaGetLastError());
 }
 
@@ -449,6 +504,31 @@ pfsmc_gpu_status pfsmc_gpu_shard_offspring(pfsmc_gpu_sampler* s, uint64_t* total
     offspring_totals_impl(s);
     if (totals_out)
       for (int q = 0; q < s->world; ++q) totals_out[q] = s->otot_host[q];
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Offspring counts over peer memory, phase by phase (see enqueue_offspring_peer;
+// the caller puts a barrier across ranks between the phases). Phase 2 also
+// returns the children of every rank (world entries, blocking).
+pfsmc_gpu_status pfsmc_gpu_shard_offspring_peer(pfsmc_gpu_sampler* s, int phase, uint64_t* totals_out) {
+  return guarded([&] {
+    if (!s->shard_api) throw ConfigError("not a sharded handle");
+    if (!s->have_peers) throw ConfigError("shard_offspring_peer: no peer table (attach_peers / attach_peers_local)");
+    if (phase < 0 || phase > 2) throw ConfigError("shard_offspring_peer: phase must be 0, 1 or 2");
+    enqueue_offspring_peer(s, phase);
+    if (phase == 2) {
+      CK(cudaMemcpyAsync(s->otot_host, s->otot, sizeof(unsigned long long) * s->world, cudaMemcpyDeviceToHost,
+                         s->stream));
+      CK(cudaMemcpyAsync(s->st_host, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+      CK(cudaStreamSynchronize(s->stream));
+      check_error(s);
+      unsigned long long tot = 0;
+      for (int q = 0; q < s->world; ++q) tot += s->otot_host[q];
+      if (tot != static_cast<unsigned long long>(s->ctx.n_glob)) throw std::runtime_error("offspring: child total mismatch");
+      if (totals_out)
+        for (int q = 0; q < s->world; ++q) totals_out[q] = s->otot_host[q];
+    }
     return PFSMC_GPU_OK;
   });
 }
@@ -700,13 +780,14 @@ static void drop_peers(pfsmc_gpu_sampler* s) {
 // ---- migration over NVLink peer memory --------------------------------------
 // The six buffers a peer reads (record buffers, ll_bar, the exact CDF, the
 // segment ends, the guide), as CUDA IPC handles: 6 x 64 bytes.
-constexpr int kPeerBufs = 8;  // + the offspring prefix (offspring mode), the tile windows
+constexpr int kPeerBufs = 10;  // + the offspring prefix and counts (offspring mode), the tile windows
 
 pfsmc_gpu_status pfsmc_gpu_shard_ipc_handles(pfsmc_gpu_sampler* s, uint8_t* out) {
   return guarded([&] {
     if (!s->shard_api) throw ConfigError("not a sharded handle");
     const Ctx& c = s->ctx;
-    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse, s->ooff, c.win};
+    const void* bufs[kPeerBufs] = {c.rec[0], c.rec[1], c.llbar, c.cdf, c.seg_end, c.coarse, s->ooff, c.win,
+                                   s->ocnt, s->ocount};
     for (int i = 0; i < kPeerBufs; ++i) {
       cudaIpcMemHandle_t h;
       CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
@@ -732,6 +813,8 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
         p[0] = c.rec[0], p[1] = c.rec[1], p[2] = c.llbar, p[3] = c.cdf, p[4] = c.seg_end, p[5] = c.coarse;
         p[6] = s->ooff;
         p[7] = c.win;
+        p[8] = s->ocnt;
+        p[9] = s->ocount;
       } else {
         for (int i = 0; i < kPeerBufs; ++i) {
           cudaIpcMemHandle_t h;
@@ -750,6 +833,8 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers(pfsmc_gpu_sampler* s, const uint8_
       t.coarse[r] = static_cast<const unsigned*>(p[5]);
       t.ooff[r] = static_cast<const unsigned*>(p[6]);
       t.win[r] = static_cast<const TileWin*>(p[7]);
+      t.ocnt[r] = static_cast<unsigned*>(const_cast<void*>(p[8]));
+      t.ocount[r] = static_cast<unsigned long long*>(const_cast<void*>(p[9]));
     }
     s->peers = t;
     s->have_peers = true;
@@ -780,6 +865,8 @@ pfsmc_gpu_status pfsmc_gpu_shard_attach_peers_local(pfsmc_gpu_sampler* s, pfsmc_
       t.coarse[r] = c.coarse;
       t.ooff[r] = o->ooff;
       t.win[r] = c.win;
+      t.ocnt[r] = o->ocnt;
+      t.ocount[r] = o->ocount;
     }
     s->peers = t;
     s->have_peers = true;
@@ -843,7 +930,12 @@ static void enqueue_shard_pull_step(pfsmc_gpu_sampler* s) {
   launch_resolve_global(c, s->ntiles, st, peer_winsrc(s));
   launch_scan(c, s->ntiles, st, 2);
   if (s->shard_mode == PFSMC_GPU_SHARD_OFFSPRING) {
-    enqueue_offspring(s);  // counts + prefix from the global walk (no exchange)
+    // counts over peer memory: O(N_local) per rank (k_offspring_count_peer)
+    enqueue_offspring_peer(s, 0);
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // tables complete, counts zeroed
+    enqueue_offspring_peer(s, 1);
+    NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every increment done
+    enqueue_offspring_peer(s, 2);
     NCK(N.AllGather(c.shard_sum, s->sums_all, 2, ncclDouble, s->nccl, st));  // every rank's prefix complete
     k_offspring_pull<<<s->grid, kThreads, 0, st>>>(c, s->peers, s->otot);
   } else {

@@ -38,7 +38,7 @@ from .sampler import MODEL_DIMS, MODELS, ConfigError, GpuSampler, ObservationMod
 (BUF_PRED, BUF_PRED_ALL, BUF_SUM, BUF_SUM_ALL, BUF_HDR, BUF_WIN, BUF_MOM, BUF_MOM_ALL, BUF_SEND, BUF_RECV,
  BUF_CNT, BUF_CNT_ALL, BUF_C5, BUF_C5_ALL) = range(14)
 STEP_FLAGS, INIT_FLAGS, INJECT_FLAGS = 7, 2, 0
-IPC_BYTES = 512  # PFSMC_GPU_IPC_BYTES
+IPC_BYTES = 640  # PFSMC_GPU_IPC_BYTES
 SHARD_MODES = {"exact": 0, "offspring": 1}  # PFSMC_GPU_SHARD_EXACT / _OFFSPRING
 
 
@@ -217,6 +217,15 @@ class GpuShard(GpuSampler):
         tot = np.zeros(self.world, dtype=np.uint64)
         self._check(self.lib.pfsmc_gpu_shard_offspring(self.h, tot.ctypes.data_as(C.POINTER(C.c_uint64))))
         return tot
+
+    def offspring_peer(self, phase: int) -> Optional[np.ndarray]:
+        """Offspring counts over peer memory, phase 0 / 1 / 2 (a barrier
+        across ranks between phases); phase 2 returns every rank's children."""
+        self.lib.pfsmc_gpu_shard_offspring_peer.restype = C.c_int
+        tot = np.zeros(self.world, dtype=np.uint64)
+        self._check(self.lib.pfsmc_gpu_shard_offspring_peer(self.h, phase,
+                                                            tot.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return tot if phase == 2 else None
 
     def offspring_counts(self) -> np.ndarray:
         self.lib.pfsmc_gpu_shard_offspring_counts.restype = C.c_int
@@ -476,12 +485,19 @@ class ShardedFilter:
         self._each(lambda s: s.scan_records())
         self._phase_c()
         if self.mode == "offspring":
-            tot = [s.offspring() for s in sh][0]                         # identical on every rank
-            self.last_totals = np.asarray(tot, dtype=np.int64)
             if self.pull:
+                # counts over peer memory: each rank draws only its own slots
+                self._each(lambda s: s.offspring_peer(0))
+                comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                 # counts zeroed everywhere
+                self._each(lambda s: s.offspring_peer(1))
+                comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                 # every increment done
+                tot = [s.offspring_peer(2) for s in sh][0]               # identical on every rank
+                self.last_totals = np.asarray(tot, dtype=np.int64)
                 comm.allgather(sh, BUF_SUM, BUF_SUM_ALL)                 # every rank's prefix complete
                 self._each(lambda s: s.offspring_pull())
             else:
+                tot = [s.offspring() for s in sh][0]                     # identical on every rank
+                self.last_totals = np.asarray(tot, dtype=np.int64)
                 mats = [s.offspring_pack() for s in sh]
                 S = offspring_matrix(tot, self.world, sh[0].n)
                 for m in mats:
