@@ -217,6 +217,16 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
 enum { PFSMC_GPU_C5_SEARCH_GUIDE = 0, PFSMC_GPU_C5_SEARCH_BUCKETED = 1, PFSMC_GPU_C5_SEARCH_SPLIT = 2 };
 pfsmc_gpu_status pfsmc_gpu_c5_set_search(pfsmc_gpu_sampler* s, int mode);
 
+/* The exact sequential-CDF scan of a single (unsharded) handle:
+ *   FUSED    one kernel: tile classification, decoupled look-back for the exact
+ *            sum before each tile, CDF values and search tables (the default);
+ *   TWO_PASS the records pass with its one-block window resolver, then the CDF
+ *            pass (the form the sharded step uses, where the tile records cross
+ *            GPUs). Bitwise identical results. Takes effect at the next step
+ *            (the blocking step's CUDA graph is rebuilt). */
+enum { PFSMC_GPU_SCAN_FUSED = 0, PFSMC_GPU_SCAN_TWO_PASS = 1 };
+pfsmc_gpu_status pfsmc_gpu_set_scan_mode(pfsmc_gpu_sampler* s, int mode);
+
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop; the FP64
  * roofline denominator the benchmarks report against). */
 pfsmc_gpu_status pfsmc_gpu_fp64_peak(int device, double* tflops);

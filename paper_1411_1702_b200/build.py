@@ -22,7 +22,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpfsmc_gpu.so")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+FLAGS = ARCH + (["-DPFSMC_SCAN_TRACE"] if os.environ.get("PFSMC_SCAN_TRACE") else []) + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-diag-suppress", "497", "-Xptxas", "-warn-spills"]
 SOURCES = ["sampler.cu", "scan.cu", "shard.cu", "c5.cu", "kernels_decay.cu", "kernels_lv.cu", "kernels_robertson.cu",
            "kernels_chain.cu", "kernels_payload.cu", "kernels_metabolic.cu", "kernels_advdiff.cu", "kernels_advdiff_e1.cu",

@@ -537,8 +537,7 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
       k_c5_stats<8, 0><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
     else
       k_c5_stats<16, 0><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
-    launch_scan(c, s->ntiles, s->stream, 1);
-    launch_scan(c, s->ntiles, s->stream, 2);
+    launch_scan_single(s, c, s->stream);
     if (s->c5_search == PFSMC_GPU_C5_SEARCH_BUCKETED) {
       const C5Buckets b = c5_buckets(s);
       const int nb = 1 << b.nb_bits;

@@ -211,12 +211,17 @@ void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed) {
     // up to 2^22 particles the fitness vector fits L2: the records pass stores
     // g into the CDF buffer and the CDF pass reads it back instead of
     // recomputing the exps (each tile only reads and then rewrites its own range)
-    Ctx cp = c, cc = c;
-    cp.store_g = s->N <= (1LL << 22) && !c.gin;
-    if (cp.store_g) cc.gin = c.cdf;
-    launch_scan(cp, s->ntiles, st, 1);
-    if (timed) CK(cudaEventRecord(ev[2], st));
-    launch_scan(cc, s->ntiles, st, 2);
+    if (s->scan_mode == PFSMC_GPU_SCAN_FUSED) {
+      launch_scan(c, s->ntiles, st, 3);  // single pass; the k_scan_cdf slot of the kernel times stays ~0
+      if (timed) CK(cudaEventRecord(ev[2], st));
+    } else {
+      Ctx cp = c, cc = c;
+      cp.store_g = s->N <= (1LL << 22) && !c.gin;
+      if (cp.store_g) cc.gin = c.cdf;
+      launch_scan(cp, s->ntiles, st, 1);
+      if (timed) CK(cudaEventRecord(ev[2], st));
+      launch_scan(cc, s->ntiles, st, 2);
+    }
   }
   if (timed) CK(cudaEventRecord(ev[3], st));
   if (s->ks->block_model())
@@ -556,6 +561,10 @@ static pfsmc_gpu_status create_impl(const pfsmc_gpu_config* cfg, int rank, int w
     c.trec = s->dalloc<ThreadRec>(NT * kThreads);
     c.tile_pre = s->dalloc<double>(NT);
     c.tile_cnt_pre = s->dalloc<long long>(NT);
+    c.look_agg = s->dalloc<LookAgg>(NT);
+    c.look_pre = s->dalloc<LookPre>(NT);
+    CK(cudaMemset(c.look_agg, 0, sizeof(LookAgg) * NT));
+    CK(cudaMemset(c.look_pre, 0, sizeof(LookPre) * NT));
     c.ghdr = s->dalloc<TileHdr>(GNT);
     c.gwin = s->dalloc<TileWin>(GNT * kMaxWin);
     c.gwin_after = s->dalloc<double>(GNT * kMaxWin);
@@ -846,6 +855,18 @@ pfsmc_gpu_status pfsmc_gpu_debug_timestamps(pfsmc_gpu_sampler* s, uint64_t* out8
   });
 }
 
+// Diagnostics (not in the public header): per-tile timeline of the last
+// k_scan_fused launch (start, classification done, look-back done, end; ns,
+// plus the SM id), written into the two-pass scan's idle handoff buffer.
+pfsmc_gpu_status pfsmc_gpu_debug_tile_times(pfsmc_gpu_sampler* s, uint64_t* out, int ntiles) {
+  return guarded([&] {
+    CK(cudaMemcpyAsync(out, s->ctx.trec, sizeof(uint64_t) * 6 * std::min(ntiles, s->ntiles), cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return PFSMC_GPU_OK;
+  });
+}
+
 pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g, uint64_t j,
                                            uint32_t* ancestors_out, double* cdf_out) {
   return guarded([&] {
@@ -863,8 +884,7 @@ pfsmc_gpu_status pfsmc_gpu_resample_from_g(pfsmc_gpu_sampler* s, const double* g
     c.gin = dg;
     s->c5_anc_pending = false;
     launch_gin(c, s->ntiles, s->stream);
-    launch_scan(c, s->ntiles, s->stream, 1);
-    launch_scan(c, s->ntiles, s->stream, 2);
+    launch_scan_single(s, c, s->stream);
     launch_search_only(c, s->grid, s->stream);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ancestors_out, c.anc, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, s->stream));
@@ -895,6 +915,22 @@ pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, in
       for (int k = 0; k < kNumKernels; ++k) ms_out[k] = s->kernel_ms[k];
     if (n_kernels) *n_kernels = kNumKernels;
     if (names_out) *names_out = kKernelNames;
+    return PFSMC_GPU_OK;
+  });
+}
+
+pfsmc_gpu_status pfsmc_gpu_set_scan_mode(pfsmc_gpu_sampler* s, int mode) {
+  return guarded([&] {
+    if (mode != PFSMC_GPU_SCAN_FUSED && mode != PFSMC_GPU_SCAN_TWO_PASS)
+      throw ConfigError("set_scan_mode: mode must be PFSMC_GPU_SCAN_FUSED or PFSMC_GPU_SCAN_TWO_PASS");
+    if (mode == s->scan_mode) return PFSMC_GPU_OK;
+    CK(cudaStreamSynchronize(s->stream));
+    s->scan_mode = mode;
+    if (s->graph) {  // the blocking step's graph holds the scan launches
+      CK(cudaGraphExecDestroy(s->graph));
+      s->graph = nullptr;
+      build_graph(s);
+    }
     return PFSMC_GPU_OK;
   });
 }

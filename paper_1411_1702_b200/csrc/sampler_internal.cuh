@@ -158,6 +158,7 @@ struct pfsmc_gpu_sampler {
   unsigned long long* ocount = nullptr;     // peer counting: this rank's slots per serving rank (world)
   unsigned long long* otot_host = nullptr;  // pinned mirror
   // config 5, bucketed ancestor search (c5.cu; allocated on first use)
+  int scan_mode = PFSMC_GPU_SCAN_FUSED;  // exact-CDF scan of the single handle (pfsmc_gpu_set_scan_mode)
   int c5_search = 0;               // PFSMC_GPU_C5_SEARCH_GUIDE / _BUCKETED
   int c5_nb_bits = 0;              // 2^bits uniform buckets
   long long c5_cap = 0;            // slots per bucket
@@ -234,6 +235,15 @@ void raise_pending(pfsmc_gpu_sampler* s);
 void clear_error(pfsmc_gpu_sampler* s);
 void ensure_exchange_buffers(pfsmc_gpu_sampler* s);
 void enqueue_kernels(pfsmc_gpu_sampler* s, bool timed);
+// the single handle's exact scan in the handle's scan mode (one fused pass, or records + CDF passes)
+inline void launch_scan_single(pfsmc_gpu_sampler* s, const Ctx& c, cudaStream_t st) {
+  if (s->scan_mode == PFSMC_GPU_SCAN_FUSED) {
+    launch_scan(c, s->ntiles, st, 3);
+  } else {
+    launch_scan(c, s->ntiles, st, 1);
+    launch_scan(c, s->ntiles, st, 2);
+  }
+}
 void enqueue_prologue(pfsmc_gpu_sampler* s);
 void build_graph(pfsmc_gpu_sampler* s);
 void enqueue_readback(pfsmc_gpu_sampler* s);

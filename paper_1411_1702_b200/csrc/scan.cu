@@ -627,95 +627,67 @@ __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c, WinSrc ws) {
     resolve_chain<ITEMS>(c, c.ghdr, ws, c.gwin_after, c.gtile_info, c.gntiles, false, sm.rs);
 }
 
-// S3: exact per-element CDF (from the S2 per-thread handoff: no block
-// scans), per-tile local guide and the coarse guide.
+// Exact CDF values of one thread chunk: from the chunk's analysis, the
+// segmented carry (the piece since the last window before the chunk, or since
+// the tile start), the exact value before the tile and the exact sums after
+// the tile's windows (`wafter`, the tile's list; global or shared memory).
 template <int ITEMS>
-__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx c) {
-  using TC = TileCfg<ITEMS>;
-  __shared__ double sg[TC::kSmem];
-  if (grid_error(c)) return;
-  const int t = blockIdx.x;
-  const long long base = static_cast<long long>(t) * TC::kTileT;
-  const int nwin = __ldcg(&c.hdr[t].nwin);
-  const double2 ti = __ldcg(&c.tile_info[t]);
-  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
-  double vals[ITEMS];
-  if (nwin >= 0) {
-    ThreadTile<ITEMS> tt;
-    // g = exp(lg - lse) recomputed exactly as S2 did (same inputs, same op)
-    const double lse = c.st->lse_g;
-    const double2* gsrc = reinterpret_cast<const double2*>((c.gin ? c.gin : c.lg) + base + threadIdx.x * ITEMS);
+__device__ __forceinline__ bool chunk_values(const ThreadTile<ITEMS>& tt, const Piece& carry, int win_excl,
+                                             double tile_in, const double* wafter, double (&vals)[ITEMS]) {
+  int w = win_excl;
+  double seg = w > 0 ? wafter[w - 1] : tile_in;
+  bool ok = true;
+  if (tt.uniform_e != kNoBinade || tt.lc[ITEMS] == 0) {
+    // no window in this chunk: one exact base value, then integer steps
+    double s0 = seg;
+    ok &= piece_apply(carry, s0);
+    if (tt.lc[ITEMS] == 0) {
 #pragma unroll
-    for (int i = 0; i < ITEMS / 2; ++i) {
-      const double2 v = __ldcs(gsrc + i);
-      const int e = threadIdx.x * ITEMS + 2 * i;
-      tt.g[2 * i] = e < valid ? v.x : 0.0;
-      tt.g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
-    }
-    if (!c.gin) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int e = threadIdx.x * ITEMS + i;
-        tt.g[i] = e < valid ? exp(tt.g[i] - lse) : 0.0;
-      }
-    }
-    const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
-    tt.p[0] = tr.p0;
-    tt.cnt0 = tr.cnt0;
-    chunk_analyse<ITEMS>(tt);
-    const Piece carry{tr.d0, tr.d1, tr.e, tr.flag};
-    int w = tr.win_excl;
-    double seg = w > 0 ? __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w - 1]) : ti.x;
-    bool ok = true;
-    if (tt.uniform_e != kNoBinade || tt.lc[ITEMS] == 0) {
-      // no window in this chunk: one exact base value, then integer steps
-      double s0 = seg;
-      ok &= piece_apply(carry, s0);
-      if (tt.lc[ITEMS] == 0) {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
-      } else {
-        const int e = tt.uniform_e;
-        const UlpScale scale = ulp_scale(e);
-        long long m = static_cast<long long>(scale2(s0, 52 - e));
-        const long long m_hi = 1LL << 53;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          if (tt.g[i] != 0.0) {
-            long long d0, d1;
-            run_delta(tt.g[i], scale, d0, d1);
-            m += (m & 1) ? d1 : d0;
-          }
-          vals[i] = scale2(static_cast<double>(m), e - 52);
-        }
-        ok &= m < m_hi && binade_of(s0) == e;  // self-check of the bound
-      }
+      for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
     } else {
-      Piece acc = carry;
+      const int e = tt.uniform_e;
+      const UlpScale scale = ulp_scale(e);
+      long long m = static_cast<long long>(scale2(s0, 52 - e));
+      const long long m_hi = 1LL << 53;
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        Piece pc;
-        const int kind = classify_at(tt, i, pc);
-        acc = piece_combine(acc, pc);
-        double sk = seg;
-        if (kind == 2) {
-          seg = __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + w]);
-          ++w;
-          sk = seg;
-        } else {
-          ok &= piece_apply(acc, sk);
+        if (tt.g[i] != 0.0) {
+          long long d0, d1;
+          run_delta(tt.g[i], scale, d0, d1);
+          m += (m & 1) ? d1 : d0;
         }
-        vals[i] = sk;
+        vals[i] = scale2(static_cast<double>(m), e - 52);
       }
+      ok &= m < m_hi && binade_of(s0) == e;  // self-check of the bound
     }
-    if (!ok) atomicOr(&c.st->error, kErrInternal);
   } else {
+    Piece acc = carry;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      const int e = threadIdx.x * ITEMS + i;
-      vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
+      Piece pc;
+      const int kind = classify_at(tt, i, pc);
+      acc = piece_combine(acc, pc);
+      double sk = seg;
+      if (kind == 2) {
+        seg = wafter[w];
+        ++w;
+        sk = seg;
+      } else {
+        ok &= piece_apply(acc, sk);
+      }
+      vals[i] = sk;
     }
   }
+  return ok;
+}
+
+// One tile's outputs from its per-thread exact values: the CDF (coalesced
+// through shared memory), the segment ends and the tile's guide buckets.
+// ti = the exact CDF (before the tile, at its last element incl. the guard).
+template <int ITEMS>
+__device__ __forceinline__ void tile_emit(const Ctx& c, int t, long long base, int valid, const double (&vals)[ITEMS],
+                                          double2 ti, double* sg, double* send) {
+  using TC = TileCfg<ITEMS>;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x * ITEMS + i;
@@ -736,7 +708,6 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
   // (the one 64/128-byte CDF segment) before the record gather.
   constexpr int SPT = ITEMS >> kSegLog2;  // segments per thread
   constexpr int SPB = SPT * kThreads;     // segments per tile
-  __shared__ double send[SPB];
 #pragma unroll
   for (int q = 0; q < SPT; ++q) {
     const int i0 = threadIdx.x * ITEMS + (q << kSegLog2);
@@ -772,6 +743,479 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
   }
 }
 
+// S3: exact per-element CDF (from the S2 per-thread handoff: no block
+// scans), per-tile local guide and the coarse guide.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx c) {
+  using TC = TileCfg<ITEMS>;
+  __shared__ double sg[TC::kSmem];
+  __shared__ double send[(ITEMS >> kSegLog2) * kThreads];
+  if (grid_error(c)) return;
+  const int t = blockIdx.x;
+  const long long base = static_cast<long long>(t) * TC::kTileT;
+  const int nwin = __ldcg(&c.hdr[t].nwin);
+  const double2 ti = __ldcg(&c.tile_info[t]);
+  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
+  double vals[ITEMS];
+  if (nwin >= 0) {
+    ThreadTile<ITEMS> tt;
+    // g = exp(lg - lse) recomputed exactly as S2 did (same inputs, same op)
+    const double lse = c.st->lse_g;
+    const double2* gsrc = reinterpret_cast<const double2*>((c.gin ? c.gin : c.lg) + base + threadIdx.x * ITEMS);
+#pragma unroll
+    for (int i = 0; i < ITEMS / 2; ++i) {
+      const double2 v = __ldcs(gsrc + i);
+      const int e = threadIdx.x * ITEMS + 2 * i;
+      tt.g[2 * i] = e < valid ? v.x : 0.0;
+      tt.g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
+    }
+    if (!c.gin) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int e = threadIdx.x * ITEMS + i;
+        tt.g[i] = e < valid ? exp(tt.g[i] - lse) : 0.0;
+      }
+    }
+    const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
+    tt.p[0] = tr.p0;
+    tt.cnt0 = tr.cnt0;
+    chunk_analyse<ITEMS>(tt);
+    const Piece carry{tr.d0, tr.d1, tr.e, tr.flag};
+    if (!chunk_values<ITEMS>(tt, carry, tr.win_excl, ti.x, c.win_after + static_cast<size_t>(t) * kMaxWin, vals))
+      atomicOr(&c.st->error, kErrInternal);
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = threadIdx.x * ITEMS + i;
+      vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
+    }
+  }
+  tile_emit<ITEMS>(c, t, base, valid, vals, ti, sg, send);
+}
+
+// ------------------------------------------------- single-pass exact scan
+// The same exact CDF in ONE kernel (single handle): a tile classifies its
+// elements as k_scan_pieces does, then learns the exact sum before it by a
+// decoupled look-back instead of a resolver pass:
+//  * a window-free tile publishes its aggregate piece at once (LookAgg);
+//  * every tile publishes the exact CDF at its last element (LookPre) as soon
+//    as it knows the exact value before it; a tile with windows applies them
+//    in order with real IEEE adds (one thread, ~log2 N windows in the whole
+//    scan) before publishing;
+//  * the look-back (warp 0) composes the aggregate pieces of the predecessors
+//    back to the nearest published exact value, oldest first (the monoid is
+//    not commutative).
+// Tiles are handed out by ticket, so every predecessor of a running tile is
+// running or done (forward progress); the flags carry a launch epoch, so no
+// reset pass is needed. The values, tables and the guard are then produced by
+// the code k_scan_cdf uses (chunk_values / tile_emit): bitwise the two-pass
+// result, which stays the sharded path (its records cross GPUs).
+// 16-byte words of the look-back records. An aligned 16-byte access is one
+// transaction, so LookPre's value and flag are seen together; LookAgg's flag
+// word is stored with release / loaded with acquire, which orders its payload
+// word.
+__device__ __forceinline__ void ld_relaxed_v2(const void* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_acquire_v2(const void* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.acquire.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2(void* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void st_release_v2(void* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void publish_agg(LookAgg* r, const Piece& pc, unsigned tag) {
+  st_relaxed_v2(&r->d0, static_cast<unsigned long long>(pc.d0), static_cast<unsigned long long>(pc.d1));
+  st_release_v2(&r->e, (static_cast<unsigned long long>(tag) << 32) | static_cast<unsigned>(pc.e), 0ull);
+}
+__device__ __forceinline__ void publish_pre(LookPre* r, double v, unsigned tag) {
+  st_relaxed_v2(r, static_cast<unsigned long long>(__double_as_longlong(v)), static_cast<unsigned long long>(tag));
+}
+
+constexpr unsigned kLookSpinLimit = 1u << 21;  // polls (~1 s) before a tile gives up (INTERNAL)
+
+// Warp-wide: the exact CDF value before tile t. `bail`: gave up (error word
+// set elsewhere, or the spin limit): the caller skips its outputs.
+__device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, bool& ok, bool& bail) {
+  const int lane = threadIdx.x & 31;
+  Piece acc = piece_identity();  // tiles [hi, t) composed, oldest first
+  double base = 0.0;
+  bail = false;
+  int hi = t;
+  while (hi > 0) {
+    const int q = hi - 1 - lane;  // lane 0 looks at the nearest predecessor
+    int state = 0;                // 1: aggregate piece seen (and loaded), 2: exact value seen
+    Piece x = piece_identity();
+    double pv = 0.0;
+    unsigned spins = 0;
+    int fp;
+    for (;;) {
+      if (q >= 0 && state != 2) {
+        // both records polled at once (independent loads); the aggregate's
+        // payload is fetched when its flag first shows, off the critical hop
+        unsigned long long v0, v1, a0 = 0, a1 = 0;
+        ld_relaxed_v2(&c.look_pre[q], v0, v1);
+        if (state == 0) ld_relaxed_v2(&c.look_agg[q].e, a0, a1);
+        if (static_cast<unsigned>(v1) == tag) {
+          state = 2;
+          pv = __longlong_as_double(static_cast<long long>(v0));
+        } else if (state == 0 && static_cast<unsigned>(a0 >> 32) == tag) {
+          state = 1;
+          unsigned long long d0, d1;
+          __threadfence();  // acquire: the payload word was stored before the flag word was released
+          ld_relaxed_v2(&c.look_agg[q].d0, d0, d1);
+          x = Piece{static_cast<long long>(d0), static_cast<long long>(d1), static_cast<int>(static_cast<unsigned>(a0)), 0};
+        }
+      }
+      const unsigned valid = __ballot_sync(0xffffffffu, q >= 0);
+      const unsigned pm = __ballot_sync(0xffffffffu, state == 2);
+      const unsigned am = __ballot_sync(0xffffffffu, state != 0);
+      fp = pm ? __ffs(pm) - 1 : 32;
+      const unsigned need = (fp >= 32 ? 0xffffffffu : ((1u << fp) - 1u)) & valid;  // tiles after the exact value
+      if ((am & need) == need) break;
+      ++spins;
+      const bool stop = spins > kLookSpinLimit || ((spins & 63u) == 0 && grid_error(c));
+      if (__any_sync(0xffffffffu, stop)) {
+        if (spins > kLookSpinLimit && lane == 0) atomicOr(&c.st->error, kErrInternal);
+        bail = true;
+        return 0.0;
+      }
+    }
+    if (lane >= fp) x = piece_identity();  // only the tiles after the exact value compose
+    // ordered tree: lane l ends with tiles (q_l - o + 1 .. q_l), older first
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Piece y;
+      y.d0 = __shfl_down_sync(0xffffffffu, x.d0, o);
+      y.d1 = __shfl_down_sync(0xffffffffu, x.d1, o);
+      y.e = __shfl_down_sync(0xffffffffu, x.e, o);
+      y.flag = 0;
+      if (lane + o < 32) x = piece_combine(y, x);
+    }
+    Piece chunk;
+    chunk.d0 = __shfl_sync(0xffffffffu, x.d0, 0);
+    chunk.d1 = __shfl_sync(0xffffffffu, x.d1, 0);
+    chunk.e = __shfl_sync(0xffffffffu, x.e, 0);
+    chunk.flag = 0;
+    acc = piece_combine(chunk, acc);
+    if (fp < 32) {
+      base = __shfl_sync(0xffffffffu, pv, fp);
+      break;
+    }
+    hi -= 32;
+  }
+  double s = base;  // hi <= 0 without an exact value: the chain starts at 0
+  ok &= piece_apply(acc, s);
+  return s;
+}
+
+// Composite element of the fused kernel's second block scan: the segmented
+// piece and the window count.
+struct PieceWin {
+  Piece pc;
+  int nwin;
+};
+__device__ __forceinline__ PieceWin pw_combine(const PieceWin& a, const PieceWin& b) {
+  return PieceWin{piece_combine(a.pc, b.pc), a.nwin + b.nwin};
+}
+
+template <int ITEMS>
+struct FusedSmem {
+  double g[TileCfg<ITEMS>::kSmem];
+  double send[(ITEMS >> kSegLog2) * kThreads];
+  SumCnt wsc[kWarps];   // warp totals of the (sum, count) scan
+  PieceWin wpw[kWarps];  // warp totals of the (piece, windows) scan
+  Piece wp[kMaxWin];    // piece from the previous window (or the tile start) to each window
+  double wg[kMaxWin];   // the window elements
+  double wa[kMaxWin];   // exact sums after the windows
+  Piece tail;           // piece after the tile's last window (the whole tile if it has none)
+  double s_in, s_end;
+  int tile, bail;
+};
+
+// The general per-chunk path of the fused kernel (chunks that hold a window
+// or an exact rounding tie: ~log2 N chunks per scan, but they sit on the
+// critical path - the first tile's successors wait for it): element by
+// element with running scalars, no arrays. STAGE = false: the chunk's
+// aggregate piece and window count; STAGE = true (after the block scan): the
+// chunk's windows laid out in the tile's list, each with the piece since the
+// previous window. The per-element rule is classify() of exact_cdf.cuh: the
+// bound at the element's start is the bound at the previous element's end.
+template <int ITEMS, bool STAGE>
+__device__ __forceinline__ void chunk_general(const double* my, double p0, long long cnt0, Piece carry, int win_excl,
+                                              Piece* wp, double* wg, Piece& agg, int& nwin) {
+  Piece acc = STAGE ? carry : piece_identity();
+  int nw = 0;
+  double p = p0;
+  long long cnt = cnt0;
+  double lo = p - sum_bound(p, cnt);
+#pragma unroll 1
+  for (int i = 0; i < ITEMS; ++i) {
+    const double g = my[i];
+    if (g == 0.0) continue;  // identity
+    const double pn = p + g;
+    ++cnt;
+    const double En = sum_bound(pn, cnt);
+    const int e_lo = binade_of(lo), e_hi = binade_of(pn + En);
+    if (e_lo != e_hi) {  // window: applied with a real IEEE add by the tile's resolver
+      if (STAGE) {
+        wp[win_excl + nw] = Piece{acc.d0, acc.d1, acc.e, 0};
+        wg[win_excl + nw] = g;
+      }
+      ++nw;
+      acc = Piece{0, 0, kNoBinade, 1};
+    } else {
+      const UlpScale scale = ulp_scale(e_lo);
+      const double v = (g * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
+      const double q = rint(v);                    // ties to the even neighbour
+      const double diff = v - q;                   // exact
+      Piece pc{static_cast<long long>(q), 0, e_lo, 0};
+      pc.d1 = pc.d0 + (fabs(diff) == 0.5 ? static_cast<long long>(diff + diff) : 0);  // odd running sum: the odd neighbour
+      acc = piece_combine(acc, pc);
+    }
+    p = pn;
+    lo = pn - En;
+  }
+  agg = acc;
+  nwin = nw;
+}
+
+template <int ITEMS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
+  using TC = TileCfg<ITEMS>;
+  __shared__ FusedSmem<ITEMS> sm;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool err = grid_error(c);
+  if (threadIdx.x == 0) {
+    sm.tile = static_cast<int>(atomicAdd(&c.cnt_scan[2], 1u));
+    sm.bail = 0;
+  }
+  const unsigned tag = __ldcg(&c.cnt_scan[3]) + 1u;  // launch epoch (bumped by the block that finishes last)
+  __syncthreads();
+  const int t = sm.tile;
+  if (!err) {
+    const bool last_tile = t == static_cast<int>(gridDim.x) - 1;
+    if (threadIdx.x == 0 && t == 0) c.st->tstamp[0] = global_ns();
+    if (threadIdx.x == 0 && last_tile) c.st->tstamp[1] = global_ns();
+#ifdef PFSMC_SCAN_TRACE
+    unsigned long long* ttr = reinterpret_cast<unsigned long long*>(c.trec) + 6 * static_cast<size_t>(t);
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      ttr[0] = global_ns();
+      ttr[5] = smid;
+    }
+#endif
+    const long long base = static_cast<long long>(t) * TC::kTileT;
+    const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
+    {
+      // stage g = exp(lg - lse) (fitness_weights, filter.cpp:154): all loads in flight, then the exps
+      const double lse = c.st->lse_g;
+      const double* src = c.gin ? c.gin : c.lg;
+      double x[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int e = i * kThreads + threadIdx.x;
+        x[i] = e < valid ? __ldcs(&src[base + e]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int e = i * kThreads + threadIdx.x;
+        double g = 0.0;
+        if (e < valid) g = c.gin ? x[i] : exp(x[i] - lse);
+        sm.g[TC::sidx(e)] = g;
+      }
+    }
+    __syncthreads();
+    // ---- approximate prefix of the thread's chunk (block scan of (sum, nonzero count), one barrier)
+    const double* my = &sm.g[TC::sidx(threadIdx.x * ITEMS)];  // the chunk is contiguous (one pad per chunk)
+    SumCnt mine{0.0, 0};
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const double g = my[i];
+      mine.s += g;
+      mine.c += (g != 0.0);
+    }
+    SumCnt inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ys = __shfl_up_sync(0xffffffffu, inc.s, o);
+      const long long yc = __shfl_up_sync(0xffffffffu, inc.c, o);
+      if (lane >= o) {
+        inc.s = ys + inc.s;
+        inc.c += yc;
+      }
+    }
+    if (lane == 31) sm.wsc[wid] = inc;
+    __syncthreads();
+    double p0 = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
+    long long cnt0 = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
+    {
+      SumCnt pre{0.0, 0};
+      for (int w = 0; w < wid; ++w) {
+        pre.s = pre.s + sm.wsc[w].s;
+        pre.c += sm.wsc[w].c;
+      }
+      p0 += pre.s + (inc.s - mine.s);
+      cnt0 += pre.c + (inc.c - mine.c);
+    }
+    // ---- chunk analysis. Common path: the whole chunk certainly inside one
+    // binade and no exact tie => element i is the integer step rint(g / ulp);
+    // anything else goes through the general element-by-element code.
+    const int lcn = static_cast<int>(mine.c);
+    Piece agg = piece_identity();
+    int nwin = 0;
+    if (lcn != 0) {
+      double pend = p0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) pend = pend + my[i];
+      const double E = sum_bound(pend, cnt0 + lcn);
+      const int e_lo = binade_of(p0 - E), e_hi = binade_of(pend + E);
+      bool general = e_lo != e_hi;
+      if (!general) {
+        const UlpScale scale = ulp_scale(e_lo);
+        long long acc = 0;
+        bool tie = false;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const double v = (my[i] * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
+          const double q = rint(v);
+          tie |= fabs(v - q) == 0.5;  // v - q is exact
+          acc += static_cast<long long>(q);
+        }
+        general = tie;
+        agg = Piece{acc, acc, e_lo, 0};
+      }
+      if (general) chunk_general<ITEMS, false>(my, p0, cnt0, piece_identity(), 0, nullptr, nullptr, agg, nwin);
+    }
+    // ---- segmented scan of the chunk pieces + window counts (one barrier)
+    PieceWin pinc{agg, nwin};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      PieceWin y;
+      y.pc = shfl_up_piece(pinc.pc, o);
+      y.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, o);
+      if (lane >= o) pinc = pw_combine(y, pinc);
+    }
+    if (lane == 31) sm.wpw[wid] = pinc;
+    PieceWin pex;
+    pex.pc = shfl_up_piece(pinc.pc, 1);
+    pex.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, 1);
+    if (lane == 0) pex = PieceWin{piece_identity(), 0};
+    __syncthreads();
+    int win_total = 0;
+    {
+      PieceWin pre{piece_identity(), 0};
+      for (int w = 0; w < kWarps; ++w) {
+        const PieceWin x = sm.wpw[w];
+        if (w < wid) pre = pw_combine(pre, x);
+        win_total += x.nwin;
+      }
+      pex = pw_combine(pre, pex);
+    }
+    const Piece carry = pex.pc;
+    const int win_excl = pex.nwin;
+    const bool overflow = win_total > kMaxWin;
+    if (threadIdx.x == kThreads - 1) {
+      const Piece tail = piece_combine(carry, agg);
+      sm.tail = tail;
+      if (win_total == 0) publish_agg(&c.look_agg[t], tail, tag);  // window-free: successors compose through it at once
+    }
+    if (nwin > 0 && !overflow) {
+      Piece a2;
+      int n2;
+      chunk_general<ITEMS, true>(my, p0, cnt0, carry, win_excl, sm.wp, sm.wg, a2, n2);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      bool ok = true, bail = false;
+      if (threadIdx.x == 0 && last_tile) c.st->tstamp[3] = global_ns();
+#ifdef PFSMC_SCAN_TRACE
+      if (threadIdx.x == 0) ttr[1] = global_ns();
+#endif
+      double s = look_back(c, t, tag, ok, bail);
+      if (threadIdx.x == 0 && last_tile) c.st->tstamp[4] = global_ns();
+#ifdef PFSMC_SCAN_TRACE
+      if (threadIdx.x == 0) ttr[2] = global_ns();
+#endif
+      if (threadIdx.x == 0) {
+        const double s_in = s;
+        if (!bail) {
+          if (overflow) {
+            // serial tile (window overflow): the plain sequential sum, in place
+            for (int e = 0; e < valid; ++e) {
+              s = s + sm.g[TC::sidx(e)];
+              sm.g[TC::sidx(e)] = s;
+            }
+          } else {
+            for (int w = 0; w < win_total; ++w) {
+              ok &= piece_apply(sm.wp[w], s);
+              s = s + sm.wg[w];  // the window element: a real IEEE add, as acc += g[i]
+              sm.wa[w] = s;
+            }
+            ok &= piece_apply(sm.tail, s);
+          }
+          if (!last_tile) {
+            publish_pre(&c.look_pre[t], s, tag);
+          } else {
+            c.st->total_mass = s;
+            s = (s < 1.0) ? 1.0 : s;  // guard the last bin (filter.cpp:168)
+          }
+          if (!ok) atomicOr(&c.st->error, kErrInternal);
+        }
+        sm.s_in = s_in;
+        sm.s_end = s;
+        sm.bail = bail;
+      }
+    }
+    __syncthreads();
+    if (!sm.bail) {
+      const double2 ti = make_double2(sm.s_in, sm.s_end);
+      double vals[ITEMS];
+      bool ok = true;
+      if (overflow) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) vals[i] = threadIdx.x * ITEMS + i < valid ? my[i] : 0.0;
+      } else {
+        // the exact sum before the chunk (the carry piece applied to the exact
+        // value after the last window before it), then the chunk's elements
+        // with real IEEE adds: the sequential CDF itself (filter.cpp:162-167)
+        double sk = win_excl > 0 ? sm.wa[win_excl - 1] : ti.x;
+        ok = piece_apply(carry, sk);
+        double chk = sk;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          sk = sk + my[i];
+          vals[i] = sk;
+        }
+        // self-check of the piece algebra against the real adds (window-free chunks)
+        if (nwin == 0) ok &= piece_apply(agg, chk) && chk == sk;
+      }
+      if (!ok) atomicOr(&c.st->error, kErrInternal);
+      // (each thread rewrites only the staged positions it read: no barrier needed here)
+      tile_emit<ITEMS>(c, t, base, valid, vals, ti, sm.g, sm.send);
+      if (threadIdx.x == 0 && last_tile) c.st->tstamp[2] = global_ns();
+      if (threadIdx.x == 0 && t == 0) c.st->tstamp[5] = global_ns();
+#ifdef PFSMC_SCAN_TRACE
+      if (threadIdx.x == 0) ttr[3] = global_ns();
+#endif
+    }
+  }
+  // launch epilogue: the block that finishes last re-arms the ticket and bumps
+  // the epoch (every block read the epoch before its own count, so none of
+  // this launch can see the bump)
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
+    if (old == gridDim.x - 1) {
+      c.cnt_scan[1] = 0;
+      c.cnt_scan[2] = 0;
+      c.cnt_scan[3] = tag;
+    }
+  }
+}
+
 void launch_resolve_global(const Ctx& c, int ntiles, cudaStream_t st, const WinSrc& ws) {
   if (c.tile_log2 == 11) k_resolve_global<8><<<1, kThreads, 0, st>>>(c, ws);
   else k_resolve_global<16><<<1, kThreads, 0, st>>>(c, ws);
@@ -787,6 +1231,11 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
     case 2:
       if (small) k_scan_cdf<8><<<ntiles, kThreads, 0, st>>>(c);
       else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
+      break;
+    case 3:  // single pass (single handle)
+      // 4 / 3 CTAs per SM (64 / 78 registers): measured faster than 3 / 2 (profiles/r02_notes.md)
+      if (small) k_scan_fused<8, 4><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_fused<16, 3><<<ntiles, kThreads, 0, st>>>(c);
       break;
     case 4:
       if (small) k_scan_pieces<8, 1><<<ntiles, kThreads, 0, st>>>(c);

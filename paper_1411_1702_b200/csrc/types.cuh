@@ -78,6 +78,19 @@ struct WinSrc {
 #endif
 };
 
+// Single-pass exact scan (k_scan_fused): what a tile publishes for the
+// look-back of its successors. flag = launch epoch + 1 when valid.
+struct alignas(16) LookAgg {  // aggregate piece of a window-free tile: two 16-byte words,
+  long long d0, d1;           // the payload word first, then the flag word (released)
+  int e;
+  unsigned flag;
+  unsigned long long pad;
+};
+struct alignas(16) LookPre {  // exact CDF at the tile's last element: one 16-byte word
+  double v;                   // (value and flag travel together)
+  unsigned flag, pad;
+};
+
 // Per-thread handoff from the records phase to the CDF phase of the exact
 // scan: the thread's approximate prefix and the exact segment carry.
 struct ThreadRec {
@@ -134,7 +147,9 @@ struct Ctx {
   double* gpart;       // group partials
   unsigned* cnt_pred;  // last-block counters of k_predict (ngroups + 1)
   unsigned* cnt_upd;   // ... of k_update / k_moments (ngroups + 1)
-  unsigned* cnt_scan;  // [1] k_scan_pieces done counter, [2] its dynamic tile id
+  unsigned* cnt_scan;  // [1] scan blocks done, [2] k_scan_fused tile ticket, [3] its launch epoch
+  LookAgg* look_agg;   // k_scan_fused look-back records (ntiles each)
+  LookPre* look_pre;
   const double* gin;   // injected fitness (parity mode) or null
   DevState* st;
   const StepParams* sp;

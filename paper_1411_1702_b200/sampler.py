@@ -109,7 +109,7 @@ def load_library(path: str = LIB_PATH):
                      "pfsmc_gpu_get_step_diagnostics", "pfsmc_gpu_resample_from_g",
                      "pfsmc_gpu_set_kernel_timing", "pfsmc_gpu_kernel_times", "pfsmc_gpu_flush_l2",
                      "pfsmc_gpu_c5_set_logweights", "pfsmc_gpu_c5_iteration", "pfsmc_gpu_c5_set_search",
-                     "pfsmc_gpu_c5_debug_bucket_cap"):
+                     "pfsmc_gpu_c5_debug_bucket_cap", "pfsmc_gpu_set_scan_mode"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
     return _lib
@@ -357,6 +357,12 @@ class GpuSampler:
         if debug_bucket_cap:
             self._check(self.lib.pfsmc_gpu_c5_debug_bucket_cap(self.h, C.c_longlong(debug_bucket_cap)))
         self._check(self.lib.pfsmc_gpu_c5_set_search(self.h, {"guide": 0, "bucketed": 1, "split": 2}[mode]))
+
+    def set_scan_mode(self, mode: str):
+        """'fused' (one-kernel exact scan with decoupled look-back, the default)
+        or 'two_pass' (records pass + resolver, CDF pass; include/pfsmc_gpu.h).
+        Bitwise identical results."""
+        self._check(self.lib.pfsmc_gpu_set_scan_mode(self.h, {"fused": 0, "two_pass": 1}[mode]))
 
     def transfer_bytes(self):
         """(H2D, D2H) bytes of one blocking pf_step (pfsmc_gpu_step_transfer_bytes)."""

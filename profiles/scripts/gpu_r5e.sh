@@ -1,0 +1,16 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "resample or scan_modes or c5 or free_running" > gpurun_out/pytest_r5e.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_r5e.log
+tail -5 gpurun_out/pytest_r5e.log
+for hi in 0 1; do
+echo "HI=$hi"
+PFSMC_SCAN_HI=$hi timeout 300 python profiles/probe_tiles.py 2>&1 | grep -v "   tile"
+PFSMC_SCAN_HI=$hi timeout 600 python profiles/probe_scanmode.py lv c5 > gpurun_out/scanmode_r5e_$hi.json 2> gpurun_out/scanmode_r5e_$hi.err
+python - <<PY
+import json
+d=json.load(open("gpurun_out/scanmode_r5e_$hi.json"))
+for k,v in d.items():
+    print(k, v["ms_per_step"] if isinstance(v,dict) else v, v.get("kernel_us") if isinstance(v,dict) else "")
+PY
+done

@@ -105,7 +105,11 @@ def _g_cases(rng):
     return out
 
 
-def test_resample_from_injected_g_is_bit_exact():
+SCAN_MODES = ["fused", "two_pass"]  # pfsmc_gpu_set_scan_mode: bitwise the same CDF either way
+
+
+@pytest.mark.parametrize("scan", SCAN_MODES)
+def test_resample_from_injected_g_is_bit_exact(scan):
     """Kernel-level parity of resample_multinomial (filter.cpp:158-178): the
     device CDF equals the reference's sequential sum bit for bit, so the
     ancestors are identical for every fitness vector."""
@@ -114,6 +118,7 @@ def test_resample_from_injected_g_is_bit_exact():
     for name, g in _g_cases(rng).items():
         n = len(g)
         s = GpuSampler("lv", PfConfig(particles=n, seed=99), ObservationModel([0, 1], 0.05))
+        s.set_scan_mode(scan)
         anc, cdf = s.resample_from_g(g, 4, with_cdf=True)
         ref_cdf = np.cumsum(g)
         ref_cdf[-1] = max(ref_cdf[-1], 1.0)
@@ -123,7 +128,8 @@ def test_resample_from_injected_g_is_bit_exact():
         s.close()
 
 
-def test_resample_randomized_structures_bit_exact():
+@pytest.mark.parametrize("scan", SCAN_MODES)
+def test_resample_randomized_structures_bit_exact(scan):
     """Property check over 40 seeded random fitness structures (sizes from 1
     to ~3e5, zero runs, σ up to 8 log-normal mass, subnormal and huge
     values): the device CDF is the sequential sum bit for bit and the
@@ -143,6 +149,7 @@ def test_resample_randomized_structures_bit_exact():
         if rng.random() < 0.5 and g.sum() > 0:
             g = g / g.sum()
         s = GpuSampler("lv", PfConfig(particles=n, seed=7 + case), ObservationModel([0, 1], 0.05))
+        s.set_scan_mode(scan)
         anc, cdf = s.resample_from_g(g, 3, with_cdf=True)
         ref = np.cumsum(g)
         ref[-1] = max(ref[-1], 1.0)
@@ -152,12 +159,14 @@ def test_resample_randomized_structures_bit_exact():
         s.close()
 
 
-def test_resample_golden_fixture():
+@pytest.mark.parametrize("scan", SCAN_MODES)
+def test_resample_golden_fixture(scan):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     d = np.load(os.path.join(GOLD, "resample.npz"))
     for k in [x[:-2] for x in d.files if x.endswith("_g")]:
         g = d[f"{k}_g"]
         s = GpuSampler("lv", PfConfig(particles=len(g), seed=99), ObservationModel([0, 1], 0.05))
+        s.set_scan_mode(scan)
         assert np.array_equal(s.resample_from_g(g, 4).astype(np.int64), d[f"{k}_anc"]), k
         s.close()
 
@@ -722,6 +731,33 @@ def test_sharded_torchcomm_nccl_world1_bitwise():
         shard3.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_scan_modes_give_the_same_filter_bitwise():
+    """The single-pass exact scan (decoupled look-back) and the two-pass form
+    (records + resolver, CDF pass) give the same ancestors, ensemble and trace,
+    bit for bit, over free-running steps (2^18 + a ragged tail: 129 tiles)."""
+    from paper_1411_1702_b200 import problems
+    n, steps = (1 << 18) + 333, 8
+    prob = problems.lotka_volterra(particles=n, T=steps, seed=9)
+    sc = StepConfig(model="lv", family="am", order=2, h=0.1, seed=9, obs_idx=(0, 1), sigma=0.05)
+    out = {}
+    for mode in SCAN_MODES:
+        gpu = _sampler(sc, n)
+        gpu.set_scan_mode(mode)
+        gpu.initialize_uniform(**prob.prior)
+        tp, rows, ancs = 0.0, [], []
+        for j in range(1, steps + 1):
+            t1 = prob.times[j - 1]
+            row = gpu.pf_step(prob.ys[j - 1], j, tp, t1)
+            rows.append(np.concatenate([row.theta_mean, row.theta_var, row.state_mean, [row.ess]]))
+            ancs.append(gpu.step_diagnostics()[0].copy())
+            tp = t1
+        e = gpu.get_ensemble()
+        out[mode] = (np.array(rows), np.array(ancs), e.states.copy(), e.params_u.copy(), e.logw.copy())
+        gpu.close()
+    for a, b in zip(out["fused"], out["two_pass"]):
+        assert np.array_equal(a, b)
 
 
 def test_free_running_full_size_lv():
