@@ -42,6 +42,7 @@ KERNEL_BYTES = {                              # per particle per launch
     "k_predict": 8 * R + 8 + 8 + 8,           # record + lw in; ll_bar + lg out
     "k_scan_pieces": 8 + 8,                   # lg in; g out
     "k_scan_cdf": 8 + 8 + 2,                  # g in; cdf + local guide out
+    "k_scan_fused": 8 + 8 + 2,                # lg in; cdf + search tables out (single-pass scan)
     "k_serve": 8 * R + 8 + 8 * (R + 2) + 4,   # ancestor record + ll_bar gathered; payload + anc out
     "k_update": 8 * (R + 2) + 8 * R + 8,      # payload in; record + lw out
 }
@@ -1020,6 +1021,7 @@ def main():
             "config": {**_lv_config(world, n),
                        **({"sharded_path_failed": SHARD_FAILURE[0]} if SHARD_FAILURE else {})},
             "arithmetic": ARITH,
+            "exact_scan": "single pass (k_scan_fused: decoupled look-back); the two-pass form serves the sharded step",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "bytes_per_particle": KERNEL_BYTES[dom], "peak_source": peak_kind,

@@ -192,7 +192,8 @@ void* pfsmc_gpu_stream(pfsmc_gpu_sampler* s);
 /* Per-kernel device time accounting (CUDA events around each launch of the
  * step's kernels, on the sampler's stream). While enabled, steps launch
  * kernels directly instead of replaying the CUDA graph. names_out receives a
- * static, comma-separated kernel list. */
+ * static, comma-separated kernel list of n_kernels entries ("-" marks an
+ * event slot without a kernel: the fused scan mode has one scan launch). */
 pfsmc_gpu_status pfsmc_gpu_set_kernel_timing(pfsmc_gpu_sampler* s, int enable);
 pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, int* n_kernels,
                                         const char** names_out);

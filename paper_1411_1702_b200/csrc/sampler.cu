@@ -860,7 +860,7 @@ pfsmc_gpu_status pfsmc_gpu_debug_timestamps(pfsmc_gpu_sampler* s, uint64_t* out8
 // plus the SM id), written into the two-pass scan's idle handoff buffer.
 pfsmc_gpu_status pfsmc_gpu_debug_tile_times(pfsmc_gpu_sampler* s, uint64_t* out, int ntiles) {
   return guarded([&] {
-    CK(cudaMemcpyAsync(out, s->ctx.trec, sizeof(uint64_t) * 6 * std::min(ntiles, s->ntiles), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(out, s->ctx.trec, sizeof(uint64_t) * 8 * std::min(ntiles, s->ntiles), cudaMemcpyDeviceToHost,
                        s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return PFSMC_GPU_OK;
@@ -914,7 +914,8 @@ pfsmc_gpu_status pfsmc_gpu_kernel_times(pfsmc_gpu_sampler* s, double* ms_out, in
     if (ms_out)
       for (int k = 0; k < kNumKernels; ++k) ms_out[k] = s->kernel_ms[k];
     if (n_kernels) *n_kernels = kNumKernels;
-    if (names_out) *names_out = kKernelNames;
+    // five event slots in both scan modes; the fused scan leaves the second scan slot empty ("-")
+    if (names_out) *names_out = s->scan_mode == PFSMC_GPU_SCAN_FUSED ? kKernelNamesFused : kKernelNames;
     return PFSMC_GPU_OK;
   });
 }
@@ -926,6 +927,7 @@ pfsmc_gpu_status pfsmc_gpu_set_scan_mode(pfsmc_gpu_sampler* s, int mode) {
     if (mode == s->scan_mode) return PFSMC_GPU_OK;
     CK(cudaStreamSynchronize(s->stream));
     s->scan_mode = mode;
+
     if (s->graph) {  // the blocking step's graph holds the scan launches
       CK(cudaGraphExecDestroy(s->graph));
       s->graph = nullptr;

@@ -33,6 +33,7 @@ struct NumericalError : std::runtime_error {
   } while (0)
 
 inline constexpr const char* kKernelNames = "k_predict,k_scan_pieces,k_scan_cdf,k_serve,k_update";
+inline constexpr const char* kKernelNamesFused = "k_predict,k_scan_fused,-,k_serve,k_update";
 constexpr int kNumKernels = 5;
 
 

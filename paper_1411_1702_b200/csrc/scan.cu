@@ -811,33 +811,51 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
 // the code k_scan_cdf uses (chunk_values / tile_emit): bitwise the two-pass
 // result, which stays the sharded path (its records cross GPUs).
 // 16-byte words of the look-back records. An aligned 16-byte access is one
-// transaction, so LookPre's value and flag are seen together; LookAgg's flag
-// word is stored with release / loaded with acquire, which orders its payload
-// word.
+// transaction, so a record's value and its tag are seen together: relaxed
+// gpu-scope loads and stores suffice, no fence on either side.
 __device__ __forceinline__ void ld_relaxed_v2(const void* p, unsigned long long& a, unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-__device__ __forceinline__ void ld_acquire_v2(const void* p, unsigned long long& a, unsigned long long& b) {
-  asm volatile("ld.acquire.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_v2(void* p, unsigned long long a, unsigned long long b) {
   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
-__device__ __forceinline__ void st_release_v2(void* p, unsigned long long a, unsigned long long b) {
-  asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-}
-__device__ __forceinline__ void publish_agg(LookAgg* r, const Piece& pc, unsigned tag) {
-  st_relaxed_v2(&r->d0, static_cast<unsigned long long>(pc.d0), static_cast<unsigned long long>(pc.d1));
-  st_release_v2(&r->e, (static_cast<unsigned long long>(tag) << 32) | static_cast<unsigned>(pc.e), 0ull);
-}
 __device__ __forceinline__ void publish_pre(LookPre* r, double v, unsigned tag) {
   st_relaxed_v2(r, static_cast<unsigned long long>(__double_as_longlong(v)), static_cast<unsigned long long>(tag));
+}
+// The aggregate piece of a window-free tile in one 16-byte word. A composed
+// piece has d1 - d0 in {-1, 0, 1} (two running sums that start one apart end
+// 0, 1 or 2 apart: a tie moves them apart or together by one, and
+// equal-parity sums move together), so the piece and the tag fit.
+__device__ __forceinline__ void publish_agg(LookAgg* r, const Piece& pc, unsigned tag, int* err) {
+  if (static_cast<unsigned long long>(pc.d1 - pc.d0 + 1) > 2ull) atomicOr(err, kErrInternal);  // never expected
+  const unsigned ecode = pc.e == kNoBinade ? 0u : static_cast<unsigned>(pc.e + 2048);
+  const unsigned long long meta =
+      (static_cast<unsigned long long>(tag) << 32) | (ecode << 16) | static_cast<unsigned>(pc.d1 - pc.d0 + 1);
+  st_relaxed_v2(r, static_cast<unsigned long long>(pc.d0), meta);
+}
+__device__ __forceinline__ Piece unpack_agg(unsigned long long d0, unsigned long long meta) {
+  const unsigned lo = static_cast<unsigned>(meta);
+  const unsigned ecode = lo >> 16;
+  Piece pc;
+  pc.d0 = static_cast<long long>(d0);
+  pc.d1 = pc.d0 + static_cast<long long>(lo & 0xffu) - 1;
+  pc.e = ecode ? static_cast<int>(ecode) - 2048 : kNoBinade;
+  pc.flag = 0;
+  return pc;
 }
 
 constexpr unsigned kLookSpinLimit = 1u << 21;  // polls (~1 s) before a tile gives up (INTERNAL)
 
 // Warp-wide: the exact CDF value before tile t. `bail`: gave up (error word
 // set elsewhere, or the spin limit): the caller skips its outputs.
+// The walk goes back 32 tiles a round, composing the aggregate pieces of the
+// window-free tiles (oldest first: the monoid is not commutative), until it
+// meets a published exact value (or the start of the chain). A tile with
+// windows publishes only its exact end value, so the ~log2 N such tiles form
+// the one serial chain of the scan (one L2 round trip per link).
+// (Measured and not kept, profiles/r02_notes.md: replaying through window
+// tiles from their published window lists instead of waiting for their exact
+// values, and loading the records several rounds ahead.)
 __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, bool& ok, bool& bail) {
   const int lane = threadIdx.x & 31;
   Piece acc = piece_identity();  // tiles [hi, t) composed, oldest first
@@ -846,27 +864,23 @@ __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, b
   int hi = t;
   while (hi > 0) {
     const int q = hi - 1 - lane;  // lane 0 looks at the nearest predecessor
-    int state = 0;                // 1: aggregate piece seen (and loaded), 2: exact value seen
+    int state = 0;                // 1: aggregate piece seen, 2: exact value seen
     Piece x = piece_identity();
     double pv = 0.0;
     unsigned spins = 0;
     int fp;
     for (;;) {
       if (q >= 0 && state != 2) {
-        // both records polled at once (independent loads); the aggregate's
-        // payload is fetched when its flag first shows, off the critical hop
+        // both records polled at once (independent loads, one 16-byte word each)
         unsigned long long v0, v1, a0 = 0, a1 = 0;
         ld_relaxed_v2(&c.look_pre[q], v0, v1);
-        if (state == 0) ld_relaxed_v2(&c.look_agg[q].e, a0, a1);
+        if (state == 0) ld_relaxed_v2(&c.look_agg[q], a0, a1);
         if (static_cast<unsigned>(v1) == tag) {
           state = 2;
           pv = __longlong_as_double(static_cast<long long>(v0));
-        } else if (state == 0 && static_cast<unsigned>(a0 >> 32) == tag) {
+        } else if (state == 0 && static_cast<unsigned>(a1 >> 32) == tag) {
+          x = unpack_agg(a0, a1);
           state = 1;
-          unsigned long long d0, d1;
-          __threadfence();  // acquire: the payload word was stored before the flag word was released
-          ld_relaxed_v2(&c.look_agg[q].d0, d0, d1);
-          x = Piece{static_cast<long long>(d0), static_cast<long long>(d1), static_cast<int>(static_cast<unsigned>(a0)), 0};
         }
       }
       const unsigned valid = __ballot_sync(0xffffffffu, q >= 0);
@@ -884,21 +898,33 @@ __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, b
       }
     }
     if (lane >= fp) x = piece_identity();  // only the tiles after the exact value compose
-    // ordered tree: lane l ends with tiles (q_l - o + 1 .. q_l), older first
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Piece y;
-      y.d0 = __shfl_down_sync(0xffffffffu, x.d0, o);
-      y.d1 = __shfl_down_sync(0xffffffffu, x.d1, o);
-      y.e = __shfl_down_sync(0xffffffffu, x.e, o);
-      y.flag = 0;
-      if (lane + o < 32) x = piece_combine(y, x);
-    }
+    // common round: no rounding tie, one binade => the pieces are plain integer steps and
+    // compose by a sum (any order); otherwise the ordered tree below
+    const int emax = __reduce_max_sync(0xffffffffu, x.e);  // kNoBinade (all-zero tiles) is below every binade
+    const bool plain = emax != kNoBinade &&
+                       !__any_sync(0xffffffffu, x.d0 != x.d1 || (x.e != emax && x.e != kNoBinade));
     Piece chunk;
-    chunk.d0 = __shfl_sync(0xffffffffu, x.d0, 0);
-    chunk.d1 = __shfl_sync(0xffffffffu, x.d1, 0);
-    chunk.e = __shfl_sync(0xffffffffu, x.e, 0);
-    chunk.flag = 0;
+    if (plain) {
+      long long sum = x.d0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      chunk = Piece{sum, sum, emax, 0};
+    } else {
+      // ordered tree: lane l ends with tiles (q_l - o + 1 .. q_l), older first
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        Piece y;
+        y.d0 = __shfl_down_sync(0xffffffffu, x.d0, o);
+        y.d1 = __shfl_down_sync(0xffffffffu, x.d1, o);
+        y.e = __shfl_down_sync(0xffffffffu, x.e, o);
+        y.flag = 0;
+        if (lane + o < 32) x = piece_combine(y, x);
+      }
+      chunk.d0 = __shfl_sync(0xffffffffu, x.d0, 0);
+      chunk.d1 = __shfl_sync(0xffffffffu, x.d1, 0);
+      chunk.e = __shfl_sync(0xffffffffu, x.e, 0);
+      chunk.flag = 0;
+    }
     acc = piece_combine(chunk, acc);
     if (fp < 32) {
       base = __shfl_sync(0xffffffffu, pv, fp);
@@ -922,7 +948,7 @@ __device__ __forceinline__ PieceWin pw_combine(const PieceWin& a, const PieceWin
 }
 
 template <int ITEMS>
-struct FusedSmem {
+struct alignas(16) FusedSmem {
   double g[TileCfg<ITEMS>::kSmem];
   double send[(ITEMS >> kSegLog2) * kThreads];
   SumCnt wsc[kWarps];   // warp totals of the (sum, count) scan
@@ -1000,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
     if (threadIdx.x == 0 && t == 0) c.st->tstamp[0] = global_ns();
     if (threadIdx.x == 0 && last_tile) c.st->tstamp[1] = global_ns();
 #ifdef PFSMC_SCAN_TRACE
-    unsigned long long* ttr = reinterpret_cast<unsigned long long*>(c.trec) + 6 * static_cast<size_t>(t);
+    unsigned long long* ttr = reinterpret_cast<unsigned long long*>(c.trec) + 8 * static_cast<size_t>(t);
     if (threadIdx.x == 0) {
       unsigned smid;
       asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1121,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
     if (threadIdx.x == kThreads - 1) {
       const Piece tail = piece_combine(carry, agg);
       sm.tail = tail;
-      if (win_total == 0) publish_agg(&c.look_agg[t], tail, tag);  // window-free: successors compose through it at once
+      if (win_total == 0) publish_agg(&c.look_agg[t], tail, tag, &c.st->error);  // window-free: successors compose through it at once
     }
     if (nwin > 0 && !overflow) {
       Piece a2;
@@ -1129,18 +1155,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
       chunk_general<ITEMS, true>(my, p0, cnt0, carry, win_excl, sm.wp, sm.wg, a2, n2);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
+    // the look-back warp differs from tile to tile (tiles sharing an SM arrive 148 apart; warp w issues on
+    // scheduler w % 4), so co-resident tiles' look-backs do not share an issue port
+    const int lbw = (t / 37) & 3;  // 148 = 4 * 37
+    if (wid == lbw) {
       bool ok = true, bail = false;
-      if (threadIdx.x == 0 && last_tile) c.st->tstamp[3] = global_ns();
+      if (lane == 0 && last_tile) c.st->tstamp[3] = global_ns();
 #ifdef PFSMC_SCAN_TRACE
-      if (threadIdx.x == 0) ttr[1] = global_ns();
+      if (lane == 0) ttr[1] = global_ns();
 #endif
       double s = look_back(c, t, tag, ok, bail);
-      if (threadIdx.x == 0 && last_tile) c.st->tstamp[4] = global_ns();
+      if (lane == 0 && last_tile) c.st->tstamp[4] = global_ns();
 #ifdef PFSMC_SCAN_TRACE
-      if (threadIdx.x == 0) ttr[2] = global_ns();
+      if (lane == 0) ttr[2] = global_ns();
 #endif
-      if (threadIdx.x == 0) {
+      if (lane == 0) {
         const double s_in = s;
         if (!bail) {
           if (overflow) {
@@ -1164,6 +1193,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
             s = (s < 1.0) ? 1.0 : s;  // guard the last bin (filter.cpp:168)
           }
           if (!ok) atomicOr(&c.st->error, kErrInternal);
+          c.tile_info[t] = make_double2(s_in, s);  // the search reads the last tile's end (find_segment)
         }
         sm.s_in = s_in;
         sm.s_end = s;

@@ -80,11 +80,9 @@ struct WinSrc {
 
 // Single-pass exact scan (k_scan_fused): what a tile publishes for the
 // look-back of its successors. flag = launch epoch + 1 when valid.
-struct alignas(16) LookAgg {  // aggregate piece of a window-free tile: two 16-byte words,
-  long long d0, d1;           // the payload word first, then the flag word (released)
-  int e;
-  unsigned flag;
-  unsigned long long pad;
+struct alignas(16) LookAgg {  // a tile's piece in ONE 16-byte word (value and flag travel together):
+  long long d0;               // delta for an even running sum
+  unsigned long long meta;    // epoch tag << 32 | binade code << 16 | (d1 - d0 + 1)
 };
 struct alignas(16) LookPre {  // exact CDF at the tile's last element: one 16-byte word
   double v;                   // (value and flag travel together)

@@ -341,7 +341,15 @@ class GpuSampler:
         n = C.c_int()
         names = C.c_char_p()
         self._check(self.lib.pfsmc_gpu_kernel_times(self.h, _ptr(ms), C.byref(n), C.byref(names)))
-        return dict(zip(names.value.decode().split(","), ms[:n.value].tolist()))
+        out = {}
+        last = None
+        for name, v in zip(names.value.decode().split(","), ms[:n.value].tolist()):
+            if name == "-":  # an event slot without a kernel (fused scan): its gap belongs to the previous launch
+                out[last] += v
+            else:
+                out[name] = v
+                last = name
+        return out
 
     # -- BASELINE config 5 microbenchmark (model "payload64") ------------
     def c5_set_logweights(self, sigma: float, key: int):

@@ -66,6 +66,7 @@ def lv(out):
         g.set_kernel_timing(False)
         out[f"lv_{mode}"] = {"ms_per_step": statistics.median(res[mode]), "rounds": res[mode],
                              "kernel_us": {k: (k1[k] - k0.get(k, 0.0)) / 10 * 1000 for k in k1}}
+        # (kernel-time counters accumulate across modes: names change with the mode, so subtract by name)
     g.close()
 
 

@@ -5,9 +5,9 @@ from paper_1411_1702_b200 import problems
 from paper_1411_1702_b200.sampler import GpuSampler, Ensemble, ObservationModel, PfConfig
 
 def show(tag, h, nt):
-    buf = np.zeros(6 * nt, dtype=np.uint64)
+    buf = np.zeros(8 * nt, dtype=np.uint64)
     h.lib.pfsmc_gpu_debug_tile_times(h.h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), C.c_int(nt))
-    t = buf.reshape(nt, 6).astype(np.int64)
+    t = buf.reshape(nt, 8).astype(np.int64)
     t0 = t[:, 0].min()
     st, p1, lb, en = [(t[:, k] - t0) / 1e3 for k in range(4)]
     print(tag, "tiles", nt, "kernel span %.1f us" % en.max())
@@ -16,7 +16,7 @@ def show(tag, h, nt):
     print("  values+emit:                median %.1f  p90 %.1f  max %.1f" % (np.median(en - lb), np.percentile(en - lb, 90), (en - lb).max()))
     idx = sorted(set([0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, nt - 1]))
     for i in idx:
-        print("   tile %5d sm %3d start %7.1f p1 %7.1f lb %7.1f end %7.1f" % (i, t[i, 5], st[i], p1[i], lb[i], en[i]))
+        print("   tile %5d sm %3d start %6.1f p1 %6.1f lb %6.1f end %6.1f" % (i, t[i, 5], st[i], p1[i], lb[i], en[i]))
     sms = len(set(t[:, 5].tolist()))
     print("  distinct SMs", sms, " tiles started in first 5us:", int((st < 5).sum()))
 
