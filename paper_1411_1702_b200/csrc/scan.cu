@@ -846,6 +846,37 @@ __device__ __forceinline__ Piece unpack_agg(unsigned long long d0, unsigned long
 
 constexpr unsigned kLookSpinLimit = 1u << 21;  // polls (~1 s) before a tile gives up (INTERNAL)
 
+// Composition of the warp's pieces, lane 31 (oldest) first, lane 0 last; every lane gets the result.
+// Common case: no rounding tie, one binade => the pieces are plain integer steps and compose by a sum
+// (any order); otherwise the ordered tree (the monoid is not commutative).
+__device__ __forceinline__ Piece warp_compose(Piece x) {
+  const int lane = threadIdx.x & 31;
+  const int emax = __reduce_max_sync(0xffffffffu, x.e);  // kNoBinade (all-zero tiles) is below every binade
+  const bool plain = emax != kNoBinade && !__any_sync(0xffffffffu, x.d0 != x.d1 || (x.e != emax && x.e != kNoBinade));
+  if (plain) {
+    long long sum = x.d0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    return Piece{sum, sum, emax, 0};
+  }
+  // ordered tree: lane l ends with lanes (l + o - 1 .. l), older first
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Piece y;
+    y.d0 = __shfl_down_sync(0xffffffffu, x.d0, o);
+    y.d1 = __shfl_down_sync(0xffffffffu, x.d1, o);
+    y.e = __shfl_down_sync(0xffffffffu, x.e, o);
+    y.flag = 0;
+    if (lane + o < 32) x = piece_combine(y, x);
+  }
+  Piece r;
+  r.d0 = __shfl_sync(0xffffffffu, x.d0, 0);
+  r.d1 = __shfl_sync(0xffffffffu, x.d1, 0);
+  r.e = __shfl_sync(0xffffffffu, x.e, 0);
+  r.flag = 0;
+  return r;
+}
+
 // Warp-wide: the exact CDF value before tile t. `bail`: gave up (error word
 // set elsewhere, or the spin limit): the caller skips its outputs.
 // The walk goes back 32 tiles a round, composing the aggregate pieces of the
@@ -869,6 +900,8 @@ __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, b
     double pv = 0.0;
     unsigned spins = 0;
     int fp;
+    int pre_lane = -1;  // the one tile the round waited for (its later tiles pre-composed), or -1
+    Piece pre_chunk = piece_identity();
     for (;;) {
       if (q >= 0 && state != 2) {
         // both records polled at once (independent loads, one 16-byte word each)
@@ -888,7 +921,14 @@ __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, b
       const unsigned am = __ballot_sync(0xffffffffu, state != 0);
       fp = pm ? __ffs(pm) - 1 : 32;
       const unsigned need = (fp >= 32 ? 0xffffffffu : ((1u << fp) - 1u)) & valid;  // tiles after the exact value
-      if ((am & need) == need) break;
+      const unsigned miss = need & ~am;
+      if (miss == 0) break;
+      if (pre_lane < 0 && (miss & (miss - 1)) == 0) {
+        // waiting for one tile only (a tile with windows: it publishes nothing but its exact value):
+        // compose the tiles after it now, so its value is the only thing left on the chain
+        pre_lane = __ffs(miss) - 1;
+        pre_chunk = warp_compose(lane < pre_lane ? x : piece_identity());
+      }
       ++spins;
       const bool stop = spins > kLookSpinLimit || ((spins & 63u) == 0 && grid_error(c));
       if (__any_sync(0xffffffffu, stop)) {
@@ -897,34 +937,9 @@ __device__ __forceinline__ double look_back(const Ctx& c, int t, unsigned tag, b
         return 0.0;
       }
     }
-    if (lane >= fp) x = piece_identity();  // only the tiles after the exact value compose
-    // common round: no rounding tie, one binade => the pieces are plain integer steps and
-    // compose by a sum (any order); otherwise the ordered tree below
-    const int emax = __reduce_max_sync(0xffffffffu, x.e);  // kNoBinade (all-zero tiles) is below every binade
-    const bool plain = emax != kNoBinade &&
-                       !__any_sync(0xffffffffu, x.d0 != x.d1 || (x.e != emax && x.e != kNoBinade));
-    Piece chunk;
-    if (plain) {
-      long long sum = x.d0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      chunk = Piece{sum, sum, emax, 0};
-    } else {
-      // ordered tree: lane l ends with tiles (q_l - o + 1 .. q_l), older first
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        Piece y;
-        y.d0 = __shfl_down_sync(0xffffffffu, x.d0, o);
-        y.d1 = __shfl_down_sync(0xffffffffu, x.d1, o);
-        y.e = __shfl_down_sync(0xffffffffu, x.e, o);
-        y.flag = 0;
-        if (lane + o < 32) x = piece_combine(y, x);
-      }
-      chunk.d0 = __shfl_sync(0xffffffffu, x.d0, 0);
-      chunk.d1 = __shfl_sync(0xffffffffu, x.d1, 0);
-      chunk.e = __shfl_sync(0xffffffffu, x.e, 0);
-      chunk.flag = 0;
-    }
+    // only the tiles after the exact value compose; when the round waited for exactly one tile, the
+    // composition of the tiles after it was made while waiting
+    const Piece chunk = (pre_lane >= 0 && fp == pre_lane) ? pre_chunk : warp_compose(lane < fp ? x : piece_identity());
     acc = piece_combine(chunk, acc);
     if (fp < 32) {
       base = __shfl_sync(0xffffffffu, pv, fp);
