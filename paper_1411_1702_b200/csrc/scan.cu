@@ -7,9 +7,9 @@ namespace pfsmc_gpu {
 
 // ---------------------------------------------------------------- exact CDF
 // Tiles of ITEMS * 256 elements (thread t owns elements ITEMS*t .. +ITEMS-1).
-// ITEMS = 4 (1024-element tiles) keeps the per-thread serial chains short
-// and the grid wide for N <= 2^22; ITEMS = 16 bounds the tile count (and the
-// resolver's work) at larger N. One pad double per thread chunk keeps the
+// ITEMS = 8 (2048-element tiles) keeps the per-thread chunks short and the
+// grid wide for N <= 2^22; ITEMS = 16 bounds the tile count (and the chain of
+// tiles) at larger N. One pad double per thread chunk keeps the
 // per-thread contiguous shared-memory reads conflict-free.
 template <int ITEMS>
 struct TileCfg {
@@ -18,172 +18,15 @@ struct TileCfg {
   __device__ static __forceinline__ int sidx(int e) { return e + e / ITEMS; }
 };
 
-// Block-wide exclusive segmented scan of Piece, fixed shape.
-__device__ __forceinline__ Piece block_excl_scan_piece(Piece v, Piece* sw) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Piece x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const Piece y = shfl_up_piece(x, o);
-    if (lane >= o) x = piece_combine(y, x);
-  }
-  if (lane == 31) sw[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    Piece t = lane < kWarps ? sw[lane] : piece_identity();
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const Piece y = shfl_up_piece(t, o);
-      if (lane >= o) t = piece_combine(y, t);
-    }
-    if (lane < kWarps) sw[kWarps + lane] = t;
-  }
-  __syncthreads();
-  Piece ex = shfl_up_piece(x, 1);
-  if (lane == 0) ex = piece_identity();
-  if (w) ex = piece_combine(sw[kWarps + w - 1], ex);
-  __syncthreads();
-  return ex;
-}
-
-// Block-wide exclusive scan of ints.
-__device__ __forceinline__ int block_excl_scan_int(int v, int& total, int* sw) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sw[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < kWarps ? sw[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < kWarps) sw[kWarps + lane] = t;
-  }
-  __syncthreads();
-  total = sw[2 * kWarps - 1];
-  const int ex = x - v + (w ? sw[kWarps + w - 1] : 0);
-  __syncthreads();
-  return ex;
-}
-
-// Per-thread view of one tile, shared by S2 and S3 (identical code =>
-// identical classification in both).
-template <int ITEMS>
-struct ThreadTile {
-  double g[ITEMS];
-  double p[ITEMS + 1];  // approximate prefix before each element (p[ITEMS]: after the last)
-  int lc[ITEMS + 1];    // nonzero count before each element, relative to cnt0
-  long long cnt0;       // nonzero count before the first element
-  int uniform_e;        // binade of the whole chunk (fast path) or kNoBinade
-  Piece agg;            // the chunk's aggregate piece
-  int nwin;             // windows in the chunk
-};
-
-struct ScanScratch {
-  SumCnt sc[2 * kWarps];
-  Piece pc[2 * kWarps];
-  int si[2 * kWarps];
-};
-
-// Fast-path rounding of one element in a known binade: delta for even /
-// odd m (identical unless g/u ends in exactly one half).
-// The scale 2^(52-e) is passed as two exact factors: for the subnormal
-// binade (e = -1022) 2^1074 itself overflows, 2^537 * 2^537 does not.
+// The scale 2^(52-e) that turns an element into units of binade e's ulp,
+// as two exact factors: for the subnormal binade (e = -1022) 2^1074 itself
+// overflows, 2^537 * 2^537 does not.
 struct UlpScale {
   double s1, s2;
 };
 __device__ __forceinline__ UlpScale ulp_scale(int e) {
   const int k = 52 - e;
   return k <= 1000 ? UlpScale{scale2(1.0, k), 1.0} : UlpScale{scale2(1.0, k - k / 2), scale2(1.0, k / 2)};
-}
-
-__device__ __forceinline__ void run_delta(double g, UlpScale scale, long long& d0, long long& d1) {
-  const double v = (g * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
-  const double q = floor(v);
-  const double f = v - q;
-  const long long qi = static_cast<long long>(q);
-  if (f < 0.5) {
-    d0 = d1 = qi;
-  } else if (f > 0.5) {
-    d0 = d1 = qi + 1;
-  } else {
-    d0 = qi + (qi & 1);
-    d1 = qi + ((1 + qi) & 1);
-  }
-}
-
-// Classification of element i against the approximate prefix (general path).
-template <int ITEMS>
-__device__ __forceinline__ int classify_at(const ThreadTile<ITEMS>& tt, int i, Piece& pc) {
-  return classify(tt.g[i], tt.p[i], tt.cnt0 + tt.lc[i], tt.p[i + 1], tt.cnt0 + tt.lc[i + 1], pc);
-}
-
-// Chunk analysis given p[0] and cnt0: prefix, fast-path test, aggregate.
-// Fast path: when [p0 - E, p_end + E] lies in one binade, every nonzero
-// element is a run element of that binade (the per-element bounds are
-// nested inside), so the per-element classification would agree.
-template <int ITEMS>
-__device__ __forceinline__ void chunk_analyse(ThreadTile<ITEMS>& tt) {
-  tt.lc[0] = 0;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    tt.p[i + 1] = tt.p[i] + tt.g[i];
-    tt.lc[i + 1] = tt.lc[i] + (tt.g[i] != 0.0);
-  }
-  tt.uniform_e = kNoBinade;
-  tt.agg = piece_identity();
-  tt.nwin = 0;
-  if (tt.lc[ITEMS] == 0) return;  // all zero: identity
-  const double E = sum_bound(tt.p[ITEMS], tt.cnt0 + tt.lc[ITEMS]);
-  const int e_lo = binade_of(tt.p[0] - E);
-  const int e_hi = binade_of(tt.p[ITEMS] + E);
-  if (e_lo == e_hi) {
-    tt.uniform_e = e_lo;
-    const UlpScale scale = ulp_scale(e_lo);
-    long long s0 = 0, s1 = 0;
-    bool tie = false;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      long long d0, d1;
-      run_delta(tt.g[i], scale, d0, d1);
-      tie |= (d0 != d1);
-      s0 += d0;
-      s1 += d1;
-    }
-    if (!tie) {
-      tt.agg = Piece{s0, s1, e_lo, 0};
-      return;
-    }
-    Piece a = piece_identity();
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      Piece pc = piece_identity();
-      if (tt.g[i] != 0.0) {
-        run_delta(tt.g[i], scale, pc.d0, pc.d1);
-        pc.e = e_lo;
-      }
-      a = piece_combine(a, pc);
-    }
-    tt.agg = a;
-    return;
-  }
-  Piece a = piece_identity();
-  int nw = 0;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    Piece pc;
-    nw += (classify_at(tt, i, pc) == 2);
-    a = piece_combine(a, pc);
-  }
-  tt.agg = a;
-  tt.nwin = nw;
 }
 
 // Composite resolver scan element: the segmented piece over window-free
@@ -505,116 +348,6 @@ __device__ void resolve_chain(const Ctx& c, const TileHdr* hdr, const WinSrc& wi
   if (threadIdx.x == 0 && rs.bad) atomicOr(&c.st->error, kErrInternal);
 }
 
-template <int ITEMS>
-union PiecesSmem {
-  double g[TileCfg<ITEMS>::kSmem];
-  ResolverSmem rs;
-  WinSmem ws;
-};
-
-// S2: fitness g = exp(lg - lse) (fitness_weights, filter.cpp:154), written
-// once; the approximate prefix from the tile offsets computed in the predict
-// kernel's tail (no look-back); classification, windows and tile records;
-// the per-thread handoff for S3. SHARDED = 0: the last block resolves the
-// exact chain (single handle); 1: records only (every rank resolves all
-// shards' records after the allgather, k_resolve_global).
-template <int ITEMS, int SHARDED>
-__global__ void __launch_bounds__(kThreads) k_scan_pieces(Ctx c) {
-  using TC = TileCfg<ITEMS>;
-  __shared__ PiecesSmem<ITEMS> sm;
-  __shared__ ScanScratch sw;
-  __shared__ int s_last;
-  if (grid_error(c)) return;
-  if (!SHARDED && threadIdx.x == 0 && blockIdx.x == 0) c.st->tstamp[0] = global_ns();
-  const int t = blockIdx.x;
-  const long long base = static_cast<long long>(t) * TC::kTileT;
-  const double lse = c.st->lse_g;
-  const double pre = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
-  const long long cpre = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
-  ThreadTile<ITEMS> tt;
-  {
-    // all ITEMS loads in flight first, then the exps
-    const double* src = c.gin ? c.gin : c.lg;
-    double x[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const long long k = base + i * kThreads + threadIdx.x;
-      x[i] = k < c.N ? __ldcs(&src[k]) : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int e = i * kThreads + threadIdx.x;
-      const long long k = base + e;
-      double g = 0.0;
-      if (k < c.N) g = c.gin ? x[i] : exp(x[i] - lse);  // S3 recomputes it (bitwise) or reads it back
-      sm.g[TC::sidx(e)] = g;
-      if (c.store_g && k < c.N) __stcg(&c.cdf[k], g);  // L2-resident sizes: S3 reads g instead of exp
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) tt.g[i] = sm.g[TC::sidx(threadIdx.x * ITEMS + i)];
-  SumCnt mine{0.0, 0};
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    mine.s += tt.g[i];
-    mine.c += (tt.g[i] != 0.0);
-  }
-  SumCnt tot;
-  const SumCnt ex = block_excl_scan_sc(mine, tot, sw.sc);
-  tt.p[0] = pre + ex.s;
-  tt.cnt0 = cpre + ex.c;
-  chunk_analyse<ITEMS>(tt);
-  const Piece carry = block_excl_scan_piece(tt.agg, sw.pc);
-  int win_total;
-  const int win_excl = block_excl_scan_int(tt.nwin, win_total, sw.si);
-  const bool overflow = win_total > kMaxWin;
-  c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x] =
-      ThreadRec{tt.p[0], tt.cnt0, carry.d0, carry.d1, carry.e, carry.flag, win_excl, 0};
-  if (tt.nwin > 0 && !overflow) {
-    Piece acc = carry;
-    int w = win_excl;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      Piece pc;
-      const int kind = classify_at(tt, i, pc);
-      if (kind == 2) {
-        TileWin tw;
-        tw.g = tt.g[i];
-        tw.e = acc.e;
-        tw.local = threadIdx.x * ITEMS + i;
-        tw.d0 = acc.d0;
-        tw.d1 = acc.d1;
-        c.win[static_cast<size_t>(t) * kMaxWin + w] = tw;
-        ++w;
-      }
-      acc = piece_combine(acc, pc);
-    }
-  }
-  if (threadIdx.x == kThreads - 1) {
-    const Piece acc = piece_combine(carry, tt.agg);
-    c.hdr[t] = TileHdr{overflow ? -1 : win_total, acc.e, acc.d0, acc.d1};
-  }
-  if (SHARDED) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
-    s_last = (old == gridDim.x - 1);
-    if (s_last) c.cnt_scan[1] = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (threadIdx.x == 0) c.st->tstamp[1] = global_ns();
-  WinSrc own{};
-  own.base[0] = c.win;
-  own.tiles_per_rank = c.ntiles;
-  if (!resolve_windows<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, sm.ws))
-    resolve_chain<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
-  if (threadIdx.x == 0) c.st->tstamp[2] = global_ns();
-}
-
 // Sharded: every rank resolves the exact chain over ALL shards' tiles.
 template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c, WinSrc ws) {
@@ -625,60 +358,6 @@ __global__ void __launch_bounds__(kThreads) k_resolve_global(Ctx c, WinSrc ws) {
   if (grid_error(c)) return;
   if (!resolve_windows<ITEMS>(c, c.ghdr, ws, c.gwin_after, c.gtile_info, c.gntiles, sm.ws))
     resolve_chain<ITEMS>(c, c.ghdr, ws, c.gwin_after, c.gtile_info, c.gntiles, false, sm.rs);
-}
-
-// Exact CDF values of one thread chunk: from the chunk's analysis, the
-// segmented carry (the piece since the last window before the chunk, or since
-// the tile start), the exact value before the tile and the exact sums after
-// the tile's windows (`wafter`, the tile's list; global or shared memory).
-template <int ITEMS>
-__device__ __forceinline__ bool chunk_values(const ThreadTile<ITEMS>& tt, const Piece& carry, int win_excl,
-                                             double tile_in, const double* wafter, double (&vals)[ITEMS]) {
-  int w = win_excl;
-  double seg = w > 0 ? wafter[w - 1] : tile_in;
-  bool ok = true;
-  if (tt.uniform_e != kNoBinade || tt.lc[ITEMS] == 0) {
-    // no window in this chunk: one exact base value, then integer steps
-    double s0 = seg;
-    ok &= piece_apply(carry, s0);
-    if (tt.lc[ITEMS] == 0) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) vals[i] = s0;
-    } else {
-      const int e = tt.uniform_e;
-      const UlpScale scale = ulp_scale(e);
-      long long m = static_cast<long long>(scale2(s0, 52 - e));
-      const long long m_hi = 1LL << 53;
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        if (tt.g[i] != 0.0) {
-          long long d0, d1;
-          run_delta(tt.g[i], scale, d0, d1);
-          m += (m & 1) ? d1 : d0;
-        }
-        vals[i] = scale2(static_cast<double>(m), e - 52);
-      }
-      ok &= m < m_hi && binade_of(s0) == e;  // self-check of the bound
-    }
-  } else {
-    Piece acc = carry;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      Piece pc;
-      const int kind = classify_at(tt, i, pc);
-      acc = piece_combine(acc, pc);
-      double sk = seg;
-      if (kind == 2) {
-        seg = wafter[w];
-        ++w;
-        sk = seg;
-      } else {
-        ok &= piece_apply(acc, sk);
-      }
-      vals[i] = sk;
-    }
-  }
-  return ok;
 }
 
 // One tile's outputs from its per-thread exact values: the CDF (coalesced
@@ -743,56 +422,6 @@ __device__ __forceinline__ void tile_emit(const Ctx& c, int t, long long base, i
   }
 }
 
-// S3: exact per-element CDF (from the S2 per-thread handoff: no block
-// scans), per-tile local guide and the coarse guide.
-template <int ITEMS>
-__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx c) {
-  using TC = TileCfg<ITEMS>;
-  __shared__ double sg[TC::kSmem];
-  __shared__ double send[(ITEMS >> kSegLog2) * kThreads];
-  if (grid_error(c)) return;
-  const int t = blockIdx.x;
-  const long long base = static_cast<long long>(t) * TC::kTileT;
-  const int nwin = __ldcg(&c.hdr[t].nwin);
-  const double2 ti = __ldcg(&c.tile_info[t]);
-  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
-  double vals[ITEMS];
-  if (nwin >= 0) {
-    ThreadTile<ITEMS> tt;
-    // g = exp(lg - lse) recomputed exactly as S2 did (same inputs, same op)
-    const double lse = c.st->lse_g;
-    const double2* gsrc = reinterpret_cast<const double2*>((c.gin ? c.gin : c.lg) + base + threadIdx.x * ITEMS);
-#pragma unroll
-    for (int i = 0; i < ITEMS / 2; ++i) {
-      const double2 v = __ldcs(gsrc + i);
-      const int e = threadIdx.x * ITEMS + 2 * i;
-      tt.g[2 * i] = e < valid ? v.x : 0.0;
-      tt.g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
-    }
-    if (!c.gin) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int e = threadIdx.x * ITEMS + i;
-        tt.g[i] = e < valid ? exp(tt.g[i] - lse) : 0.0;
-      }
-    }
-    const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
-    tt.p[0] = tr.p0;
-    tt.cnt0 = tr.cnt0;
-    chunk_analyse<ITEMS>(tt);
-    const Piece carry{tr.d0, tr.d1, tr.e, tr.flag};
-    if (!chunk_values<ITEMS>(tt, carry, tr.win_excl, ti.x, c.win_after + static_cast<size_t>(t) * kMaxWin, vals))
-      atomicOr(&c.st->error, kErrInternal);
-  } else {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int e = threadIdx.x * ITEMS + i;
-      vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
-    }
-  }
-  tile_emit<ITEMS>(c, t, base, valid, vals, ti, sg, send);
-}
-
 // ------------------------------------------------- single-pass exact scan
 // The same exact CDF in ONE kernel (single handle): a tile classifies its
 // elements as k_scan_pieces does, then learns the exact sum before it by a
@@ -808,8 +437,9 @@ __global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx
 // Tiles are handed out by ticket, so every predecessor of a running tile is
 // running or done (forward progress); the flags carry a launch epoch, so no
 // reset pass is needed. The values, tables and the guard are then produced by
-// the code k_scan_cdf uses (chunk_values / tile_emit): bitwise the two-pass
-// result, which stays the sharded path (its records cross GPUs).
+// the code k_scan_cdf uses (real IEEE adds from the chunk's exact start,
+// tile_emit): bitwise the two-pass result, which stays the sharded path (its
+// records cross GPUs).
 // 16-byte words of the look-back records. An aligned 16-byte access is one
 // transaction, so a record's value and its tag are seen together: relaxed
 // gpu-scope loads and stores suffice, no fence on either side.
@@ -984,9 +614,29 @@ struct alignas(16) FusedSmem {
 // chunk's windows laid out in the tile's list, each with the piece since the
 // previous window. The per-element rule is classify() of exact_cdf.cuh: the
 // bound at the element's start is the bound at the previous element's end.
-template <int ITEMS, bool STAGE>
+// Where a staging pass puts window w of the tile: the fused kernel's shared
+// lists, or the two-pass scan's global tile records.
+struct SmemWinSink {
+  Piece* wp;
+  double* wg;
+  __device__ __forceinline__ void put(int w, const Piece& pc, double g) const {
+    wp[w] = Piece{pc.d0, pc.d1, pc.e, 0};
+    wg[w] = g;
+  }
+};
+struct GlobalWinSink {
+  TileWin* tw;
+  __device__ __forceinline__ void put(int w, const Piece& pc, double g) const {
+    tw[w] = TileWin{g, pc.e, 0, pc.d0, pc.d1};
+  }
+};
+struct NoWinSink {
+  __device__ __forceinline__ void put(int, const Piece&, double) const {}
+};
+
+template <int ITEMS, bool STAGE, class Sink>
 __device__ __forceinline__ void chunk_general(const double* my, double p0, long long cnt0, Piece carry, int win_excl,
-                                              Piece* wp, double* wg, Piece& agg, int& nwin) {
+                                              const Sink& sink, Piece& agg, int& nwin) {
   Piece acc = STAGE ? carry : piece_identity();
   int nw = 0;
   double p = p0;
@@ -1001,10 +651,7 @@ __device__ __forceinline__ void chunk_general(const double* my, double p0, long 
     const double En = sum_bound(pn, cnt);
     const int e_lo = binade_of(lo), e_hi = binade_of(pn + En);
     if (e_lo != e_hi) {  // window: applied with a real IEEE add by the tile's resolver
-      if (STAGE) {
-        wp[win_excl + nw] = Piece{acc.d0, acc.d1, acc.e, 0};
-        wg[win_excl + nw] = g;
-      }
+      if (STAGE) sink.put(win_excl + nw, acc, g);
       ++nw;
       acc = Piece{0, 0, kNoBinade, 1};
     } else {
@@ -1021,6 +668,139 @@ __device__ __forceinline__ void chunk_general(const double* my, double p0, long 
   }
   agg = acc;
   nwin = nw;
+}
+
+// What a thread knows about its chunk after the tile's two block scans.
+struct TileChunk {
+  double p0;        // approximate prefix before the chunk
+  long long cnt0;   // nonzero elements before the chunk
+  Piece agg;        // the chunk's aggregate piece (cut at its windows)
+  Piece carry;      // the piece since the last window before the chunk (since the tile start if none)
+  int nwin;         // windows in the chunk
+  int win_excl;     // windows in the tile before the chunk
+};
+
+// The tile analysis shared by the single-pass scan and the two-pass records
+// kernel: stage g = exp(lg - lse) in shared memory, scan (sum, nonzero count)
+// for the chunks' approximate prefixes, classify each chunk (common path:
+// integer steps; else chunk_general), scan (piece, windows). Two barriers
+// after the staging one.
+template <int ITEMS>
+__device__ __forceinline__ void tile_analyse(const Ctx& c, int t, long long base, int valid, double* sg, SumCnt* wsc,
+                                             PieceWin* wpw, TileChunk& out, int& win_total) {
+  using TC = TileCfg<ITEMS>;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {
+    // stage g = exp(lg - lse) (fitness_weights, filter.cpp:154): all loads in flight, then the exps
+    const double lse = c.st->lse_g;
+    const double* src = c.gin ? c.gin : c.lg;
+    double x[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = i * kThreads + threadIdx.x;
+      x[i] = e < valid ? __ldcs(&src[base + e]) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = i * kThreads + threadIdx.x;
+      double g = 0.0;
+      if (e < valid) g = c.gin ? x[i] : exp(x[i] - lse);
+      sg[TC::sidx(e)] = g;
+    }
+  }
+  __syncthreads();
+  // ---- approximate prefix of the thread's chunk (block scan of (sum, nonzero count), one barrier)
+  const double* my = &sg[TC::sidx(threadIdx.x * ITEMS)];  // the chunk is contiguous (one pad per chunk)
+  SumCnt mine{0.0, 0};
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const double g = my[i];
+    mine.s += g;
+    mine.c += (g != 0.0);
+  }
+  SumCnt inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ys = __shfl_up_sync(0xffffffffu, inc.s, o);
+    const long long yc = __shfl_up_sync(0xffffffffu, inc.c, o);
+    if (lane >= o) {
+      inc.s = ys + inc.s;
+      inc.c += yc;
+    }
+  }
+  if (lane == 31) wsc[wid] = inc;
+  __syncthreads();
+  double p0 = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
+  long long cnt0 = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
+  {
+    SumCnt pre{0.0, 0};
+    for (int w = 0; w < wid; ++w) {
+      pre.s = pre.s + wsc[w].s;
+      pre.c += wsc[w].c;
+    }
+    p0 += pre.s + (inc.s - mine.s);
+    cnt0 += pre.c + (inc.c - mine.c);
+  }
+  // ---- chunk analysis. Common path: the whole chunk certainly inside one
+  // binade and no exact tie => element i is the integer step rint(g / ulp);
+  // anything else goes through the general element-by-element code.
+  const int lcn = static_cast<int>(mine.c);
+  Piece agg = piece_identity();
+  int nwin = 0;
+  if (lcn != 0) {
+    double pend = p0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) pend = pend + my[i];
+    const double E = sum_bound(pend, cnt0 + lcn);
+    const int e_lo = binade_of(p0 - E), e_hi = binade_of(pend + E);
+    bool general = e_lo != e_hi;
+    if (!general) {
+      const UlpScale scale = ulp_scale(e_lo);
+      long long acc = 0;
+      bool tie = false;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const double v = (my[i] * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
+        const double q = rint(v);
+        tie |= fabs(v - q) == 0.5;  // v - q is exact
+        acc += static_cast<long long>(q);
+      }
+      general = tie;
+      agg = Piece{acc, acc, e_lo, 0};
+    }
+    if (general) chunk_general<ITEMS, false>(my, p0, cnt0, piece_identity(), 0, NoWinSink{}, agg, nwin);
+  }
+  // ---- segmented scan of the chunk pieces + window counts (one barrier)
+  PieceWin pinc{agg, nwin};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    PieceWin y;
+    y.pc = shfl_up_piece(pinc.pc, o);
+    y.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, o);
+    if (lane >= o) pinc = pw_combine(y, pinc);
+  }
+  if (lane == 31) wpw[wid] = pinc;
+  PieceWin pex;
+  pex.pc = shfl_up_piece(pinc.pc, 1);
+  pex.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, 1);
+  if (lane == 0) pex = PieceWin{piece_identity(), 0};
+  __syncthreads();
+  win_total = 0;
+  {
+    PieceWin pre{piece_identity(), 0};
+    for (int w = 0; w < kWarps; ++w) {
+      const PieceWin x = wpw[w];
+      if (w < wid) pre = pw_combine(pre, x);
+      win_total += x.nwin;
+    }
+    pex = pw_combine(pre, pex);
+  }
+  out.p0 = p0;
+  out.cnt0 = cnt0;
+  out.agg = agg;
+  out.carry = pex.pc;
+  out.nwin = nwin;
+  out.win_excl = pex.nwin;
 }
 
 template <int ITEMS, int MINB>
@@ -1051,113 +831,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
 #endif
     const long long base = static_cast<long long>(t) * TC::kTileT;
     const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
-    {
-      // stage g = exp(lg - lse) (fitness_weights, filter.cpp:154): all loads in flight, then the exps
-      const double lse = c.st->lse_g;
-      const double* src = c.gin ? c.gin : c.lg;
-      double x[ITEMS];
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int e = i * kThreads + threadIdx.x;
-        x[i] = e < valid ? __ldcs(&src[base + e]) : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const int e = i * kThreads + threadIdx.x;
-        double g = 0.0;
-        if (e < valid) g = c.gin ? x[i] : exp(x[i] - lse);
-        sm.g[TC::sidx(e)] = g;
-      }
-    }
-    __syncthreads();
-    // ---- approximate prefix of the thread's chunk (block scan of (sum, nonzero count), one barrier)
-    const double* my = &sm.g[TC::sidx(threadIdx.x * ITEMS)];  // the chunk is contiguous (one pad per chunk)
-    SumCnt mine{0.0, 0};
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const double g = my[i];
-      mine.s += g;
-      mine.c += (g != 0.0);
-    }
-    SumCnt inc = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double ys = __shfl_up_sync(0xffffffffu, inc.s, o);
-      const long long yc = __shfl_up_sync(0xffffffffu, inc.c, o);
-      if (lane >= o) {
-        inc.s = ys + inc.s;
-        inc.c += yc;
-      }
-    }
-    if (lane == 31) sm.wsc[wid] = inc;
-    __syncthreads();
-    double p0 = c.shard_off[0] + __ldcg(&c.tile_pre[t]);
-    long long cnt0 = static_cast<long long>(c.shard_off[1]) + __ldcg(&c.tile_cnt_pre[t]);
-    {
-      SumCnt pre{0.0, 0};
-      for (int w = 0; w < wid; ++w) {
-        pre.s = pre.s + sm.wsc[w].s;
-        pre.c += sm.wsc[w].c;
-      }
-      p0 += pre.s + (inc.s - mine.s);
-      cnt0 += pre.c + (inc.c - mine.c);
-    }
-    // ---- chunk analysis. Common path: the whole chunk certainly inside one
-    // binade and no exact tie => element i is the integer step rint(g / ulp);
-    // anything else goes through the general element-by-element code.
-    const int lcn = static_cast<int>(mine.c);
-    Piece agg = piece_identity();
-    int nwin = 0;
-    if (lcn != 0) {
-      double pend = p0;
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) pend = pend + my[i];
-      const double E = sum_bound(pend, cnt0 + lcn);
-      const int e_lo = binade_of(p0 - E), e_hi = binade_of(pend + E);
-      bool general = e_lo != e_hi;
-      if (!general) {
-        const UlpScale scale = ulp_scale(e_lo);
-        long long acc = 0;
-        bool tie = false;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          const double v = (my[i] * scale.s1) * scale.s2;  // exact: g < 2^(e+1)
-          const double q = rint(v);
-          tie |= fabs(v - q) == 0.5;  // v - q is exact
-          acc += static_cast<long long>(q);
-        }
-        general = tie;
-        agg = Piece{acc, acc, e_lo, 0};
-      }
-      if (general) chunk_general<ITEMS, false>(my, p0, cnt0, piece_identity(), 0, nullptr, nullptr, agg, nwin);
-    }
-    // ---- segmented scan of the chunk pieces + window counts (one barrier)
-    PieceWin pinc{agg, nwin};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      PieceWin y;
-      y.pc = shfl_up_piece(pinc.pc, o);
-      y.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, o);
-      if (lane >= o) pinc = pw_combine(y, pinc);
-    }
-    if (lane == 31) sm.wpw[wid] = pinc;
-    PieceWin pex;
-    pex.pc = shfl_up_piece(pinc.pc, 1);
-    pex.nwin = __shfl_up_sync(0xffffffffu, pinc.nwin, 1);
-    if (lane == 0) pex = PieceWin{piece_identity(), 0};
-    __syncthreads();
-    int win_total = 0;
-    {
-      PieceWin pre{piece_identity(), 0};
-      for (int w = 0; w < kWarps; ++w) {
-        const PieceWin x = sm.wpw[w];
-        if (w < wid) pre = pw_combine(pre, x);
-        win_total += x.nwin;
-      }
-      pex = pw_combine(pre, pex);
-    }
-    const Piece carry = pex.pc;
-    const int win_excl = pex.nwin;
+    const double* my = &sm.g[TC::sidx(threadIdx.x * ITEMS)];  // the thread's chunk is contiguous (one pad per chunk)
+    TileChunk ch;
+    int win_total;
+    tile_analyse<ITEMS>(c, t, base, valid, sm.g, sm.wsc, sm.wpw, ch, win_total);
+    const double p0 = ch.p0;
+    const long long cnt0 = ch.cnt0;
+    const Piece agg = ch.agg, carry = ch.carry;
+    const int nwin = ch.nwin, win_excl = ch.win_excl;
     const bool overflow = win_total > kMaxWin;
     if (threadIdx.x == kThreads - 1) {
       const Piece tail = piece_combine(carry, agg);
@@ -1167,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
     if (nwin > 0 && !overflow) {
       Piece a2;
       int n2;
-      chunk_general<ITEMS, true>(my, p0, cnt0, carry, win_excl, sm.wp, sm.wg, a2, n2);
+      chunk_general<ITEMS, true>(my, p0, cnt0, carry, win_excl, SmemWinSink{sm.wp, sm.wg}, a2, n2);
     }
     __syncthreads();
     // the look-back warp differs from tile to tile (tiles sharing an SM arrive 148 apart; warp w issues on
@@ -1259,6 +940,140 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan_fused(Ctx c) {
       c.cnt_scan[3] = tag;
     }
   }
+}
+
+// ------------------------------------------------- two-pass exact scan
+// The form the sharded step uses (the tile records cross GPUs between the
+// passes) and PFSMC_GPU_SCAN_TWO_PASS: the same tile analysis as the fused
+// kernel, then the tile's records instead of a look-back.
+template <int ITEMS>
+struct PiecesSmem {
+  union {
+    struct {
+      double g[TileCfg<ITEMS>::kSmem];
+      SumCnt wsc[kWarps];
+      PieceWin wpw[kWarps];
+    } a;
+    ResolverSmem rs;
+    WinSmem ws;
+  };
+};
+
+// S2: the tile analysis; the tile's windows (each with the piece since the
+// previous window), its header (window count, tail piece) and the per-thread
+// handoff for S3 (carry piece, window rank, the chunk's aggregate piece).
+// SHARDED = 0: the last block resolves the exact chain (single handle); 1:
+// records only (every rank resolves all shards' records after the allgather,
+// k_resolve_global).
+template <int ITEMS, int SHARDED>
+__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 3 : 2)) k_scan_pieces(Ctx c) {
+  using TC = TileCfg<ITEMS>;
+  __shared__ PiecesSmem<ITEMS> sm;
+  __shared__ int s_last;
+  if (grid_error(c)) return;
+  if (!SHARDED && threadIdx.x == 0 && blockIdx.x == 0) c.st->tstamp[0] = global_ns();
+  const int t = blockIdx.x;
+  const long long base = static_cast<long long>(t) * TC::kTileT;
+  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
+  const double* my = &sm.a.g[TC::sidx(threadIdx.x * ITEMS)];
+  TileChunk ch;
+  int win_total;
+  tile_analyse<ITEMS>(c, t, base, valid, sm.a.g, sm.a.wsc, sm.a.wpw, ch, win_total);
+  if (c.store_g) {  // L2-resident sizes: S3 reads g back instead of the exps
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = i * kThreads + threadIdx.x;
+      if (e < valid) __stcg(&c.cdf[base + e], sm.a.g[TC::sidx(e)]);
+    }
+  }
+  const bool overflow = win_total > kMaxWin;
+  c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x] =
+      ThreadRec{ch.carry.d0, ch.carry.d1, ch.agg.d0, ch.agg.d1, ch.carry.e, ch.agg.e, ch.win_excl, ch.nwin};
+  if (ch.nwin > 0 && !overflow) {
+    Piece a2;
+    int n2;
+    chunk_general<ITEMS, true>(my, ch.p0, ch.cnt0, ch.carry, ch.win_excl,
+                               GlobalWinSink{c.win + static_cast<size_t>(t) * kMaxWin}, a2, n2);
+  }
+  if (threadIdx.x == kThreads - 1) {
+    const Piece acc = piece_combine(ch.carry, ch.agg);
+    c.hdr[t] = TileHdr{overflow ? -1 : win_total, acc.e, acc.d0, acc.d1};
+  }
+  if (SHARDED) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd(&c.cnt_scan[1], 1u);
+    s_last = (old == gridDim.x - 1);
+    if (s_last) c.cnt_scan[1] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) c.st->tstamp[1] = global_ns();
+  WinSrc own{};
+  own.base[0] = c.win;
+  own.tiles_per_rank = c.ntiles;
+  if (!resolve_windows<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, sm.ws))
+    resolve_chain<ITEMS>(c, c.hdr, own, c.win_after, c.tile_info, c.ntiles, true, sm.rs);
+  if (threadIdx.x == 0) c.st->tstamp[2] = global_ns();
+}
+
+// S3: the exact per-element CDF from the S2 handoff: the exact value before
+// the chunk (the carry piece applied to the exact value after the last window
+// before it, or to the tile's exact start), then the chunk's elements by real
+// IEEE adds - the sequential CDF itself (filter.cpp:162-167); the chunk's
+// aggregate piece is checked against those adds. Then the search tables.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads, (ITEMS == 8 ? 4 : 2)) k_scan_cdf(Ctx c) {
+  using TC = TileCfg<ITEMS>;
+  __shared__ double sg[TC::kSmem];
+  __shared__ double send[(ITEMS >> kSegLog2) * kThreads];
+  if (grid_error(c)) return;
+  const int t = blockIdx.x;
+  const long long base = static_cast<long long>(t) * TC::kTileT;
+  const int nwin = __ldcg(&c.hdr[t].nwin);
+  const double2 ti = __ldcg(&c.tile_info[t]);
+  const int valid = static_cast<int>(min(static_cast<long long>(TC::kTileT), c.N - base));
+  double vals[ITEMS];
+  if (nwin >= 0) {
+    // g = exp(lg - lse) recomputed exactly as S2 did (same inputs, same op), or read back
+    const double lse = c.st->lse_g;
+    const double2* gsrc = reinterpret_cast<const double2*>((c.gin ? c.gin : c.lg) + base + threadIdx.x * ITEMS);
+    double g[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS / 2; ++i) {
+      const double2 v = __ldcs(gsrc + i);
+      const int e = threadIdx.x * ITEMS + 2 * i;
+      g[2 * i] = e < valid ? v.x : 0.0;
+      g[2 * i + 1] = e + 1 < valid ? v.y : 0.0;
+    }
+    if (!c.gin) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int e = threadIdx.x * ITEMS + i;
+        g[i] = e < valid ? exp(g[i] - lse) : 0.0;
+      }
+    }
+    const ThreadRec tr = c.trec[static_cast<size_t>(t) * kThreads + threadIdx.x];
+    double sk = tr.win_excl > 0 ? __ldcg(&c.win_after[static_cast<size_t>(t) * kMaxWin + tr.win_excl - 1]) : ti.x;
+    bool ok = piece_apply(Piece{tr.d0, tr.d1, tr.e, 0}, sk);
+    double chk = sk;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      sk = sk + g[i];
+      vals[i] = sk;
+    }
+    if (tr.nwin == 0) ok &= piece_apply(Piece{tr.a0, tr.a1, tr.ae, 0}, chk) && chk == sk;
+    if (!ok) atomicOr(&c.st->error, kErrInternal);
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = threadIdx.x * ITEMS + i;
+      vals[i] = e < valid ? __ldcg(&c.cdf[base + e]) : 0.0;
+    }
+  }
+  tile_emit<ITEMS>(c, t, base, valid, vals, ti, sg, send);
 }
 
 void launch_resolve_global(const Ctx& c, int ntiles, cudaStream_t st, const WinSrc& ws) {

@@ -89,14 +89,15 @@ struct alignas(16) LookPre {  // exact CDF at the tile's last element: one 16-by
   unsigned flag, pad;
 };
 
-// Per-thread handoff from the records phase to the CDF phase of the exact
-// scan: the thread's approximate prefix and the exact segment carry.
+// Per-thread handoff from the records phase to the CDF phase of the two-pass
+// exact scan: the piece since the last window before the thread's chunk (the
+// tile start if none), the chunk's own aggregate piece (checked against the
+// real adds), the windows before the chunk and inside it.
 struct ThreadRec {
-  double p0;
-  long long cnt0;
-  long long d0, d1;
-  int e, flag;
-  int win_excl, pad;
+  long long d0, d1;  // carry piece
+  long long a0, a1;  // the chunk's aggregate piece
+  int e, ae;         // their binades
+  int win_excl, nwin;
 };
 
 // Immutable launch context (pointers + constants), passed by value.
