@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(kThreads) k_offspring_pack(Ctx c, const unsign
 // go to its own `ocount`. O(N_local) per rank instead of O(N_global); the
 // counts are the same integers as the walk's (every slot counted once).
 __global__ void __launch_bounds__(kThreads) k_offspring_count_peer(Ctx c, PeerTable pt, unsigned long long* ocount) {
+  __shared__ unsigned s_cnt[kMaxRanks];
   if (grid_error(c)) return;
+  if (threadIdx.x < kMaxRanks) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
   const bool mine = n < c.N;
   const double u = mine ? resample_uniform(c.seed, c.sp->j, c.n0 + n) : -1.0;
@@ -315,8 +318,13 @@ __global__ void __launch_bounds__(kThreads) k_offspring_count_peer(Ctx c, PeerTa
   const SearchView v{pt.coarse[r], pt.seg_end[r], pt.cdf[r], c.gtile_info[(r + 1) * ntl - 1].y};
   const unsigned a = find_ancestor_warp_view(c, v, u);
   if (mine) atomicAdd(pt.ocnt[r] + a, 1u);
+  // slots per serving rank: per warp, then per block in shared memory, one global atomic per
+  // (block, rank) - a global atomic per warp on the same word serialises in L2
   const unsigned grp = __match_any_sync(0xffffffffu, mine ? r : -1);
-  if (mine && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&ocount[r], static_cast<unsigned long long>(__popc(grp)));
+  if (mine && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&s_cnt[r], static_cast<unsigned>(__popc(grp)));
+  __syncthreads();
+  if (threadIdx.x < kMaxRanks && s_cnt[threadIdx.x])
+    atomicAdd(&ocount[threadIdx.x], static_cast<unsigned long long>(s_cnt[threadIdx.x]));
 }
 
 // Children per rank, identical on every rank: otot[q] = sum over ranks of
@@ -334,8 +342,8 @@ __global__ void k_offspring_totals_peer(Ctx c, PeerTable pt, unsigned long long*
 __global__ void __launch_bounds__(kThreads) k_offspring_pull(Ctx c, PeerTable pt, const unsigned long long* otot) {
   if (grid_error(c)) return;
   const long long n = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x;
-  if (n >= c.N) return;
-  const long long p = c.n0 + n;
+  const bool live = n < c.N;
+  const long long p = c.n0 + min(n, static_cast<long long>(c.N) - 1);
   int q = 0;
   long long P = 0;
   while (q + 1 < c.world && P + static_cast<long long>(otot[q]) <= p) {
@@ -343,13 +351,30 @@ __global__ void __launch_bounds__(kThreads) k_offspring_pull(Ctx c, PeerTable pt
     ++q;
   }
   const unsigned a = child_ancestor(pt.ooff[q], c.N, static_cast<unsigned>(p - P));
-  const double* rec = (c.st->cur ? pt.rec1[q] : pt.rec0[q]) + static_cast<long long>(a) * c.R;
-  const double2* src = reinterpret_cast<const double2*>(rec);
-  double2* dst = reinterpret_cast<double2*>(c.payload + n * (c.R + 2));
-  for (int i = 0; i < c.R / 2; ++i) dst[i] = __ldcg(src + i);
   const long long ga = static_cast<long long>(q) * c.N + a;
-  dst[c.R / 2] = make_double2(__ldcg(&pt.llbar[q][a]), static_cast<double>(ga));
-  c.anc[n] = static_cast<unsigned>(ga);
+  if (live) c.anc[n] = static_cast<unsigned>(ga);
+  // warp-cooperative copy (as k_serve): consecutive lanes move consecutive 16-byte parts of the warp's 32
+  // payloads, so the stores are coalesced and a record's parts are read together
+  const int lane = threadIdx.x & 31;
+  const long long wbase = n - lane;
+  const int H = c.R / 2 + 1;  // 16-byte parts per payload {record, (ll_bar, global ancestor)}
+  const int cur = c.st->cur;
+  double2* pay = reinterpret_cast<double2*>(c.payload);
+  for (int it = 0; it < H; ++it) {
+    const int idx = lane + 32 * it;
+    const int slot = idx / H, part = idx - slot * H;
+    const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+    const int qs = __shfl_sync(0xffffffffu, q, slot);
+    const long long ns = wbase + slot;
+    if (ns < c.N) {
+      double2 v;
+      if (part < H - 1)
+        v = __ldcg(reinterpret_cast<const double2*>(cur ? pt.rec1[qs] : pt.rec0[qs]) + static_cast<long long>(as) * (H - 1) + part);
+      else
+        v = make_double2(__ldcg(&pt.llbar[qs][as]), static_cast<double>(static_cast<long long>(qs) * c.N + as));
+      pay[ns * H + part] = v;
+    }
+  }
 }
 
 // The resolver's windows read straight from every shard's own list over
