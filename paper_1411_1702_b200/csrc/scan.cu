@@ -1,6 +1,7 @@
 // The exact sequential CDF (filter.cpp:158-168) and the ancestor search +
-// gather (filter.cpp:169-176, 330-335): tile decomposition, window resolver,
-// S3 CDF values and search tables, k_serve. See DESIGN.md §4.
+// gather (filter.cpp:169-176, 330-335): the tile analysis, the single-pass
+// look-back scan, the two-pass form with its window resolver, the search
+// tables, k_serve. See DESIGN.md §4.
 #include "sampler_internal.cuh"
 
 namespace pfsmc_gpu {
@@ -431,7 +432,7 @@ __device__ __forceinline__ void tile_emit(const Ctx& c, int t, long long base, i
 //    as it knows the exact value before it; a tile with windows applies them
 //    in order with real IEEE adds (one thread, ~log2 N windows in the whole
 //    scan) before publishing;
-//  * the look-back (warp 0) composes the aggregate pieces of the predecessors
+//  * the look-back (one warp) composes the aggregate pieces of the predecessors
 //    back to the nearest published exact value, oldest first (the monoid is
 //    not commutative).
 // Tiles are handed out by ticket, so every predecessor of a running tile is
@@ -606,14 +607,6 @@ struct alignas(16) FusedSmem {
   int tile, bail;
 };
 
-// The general per-chunk path of the fused kernel (chunks that hold a window
-// or an exact rounding tie: ~log2 N chunks per scan, but they sit on the
-// critical path - the first tile's successors wait for it): element by
-// element with running scalars, no arrays. STAGE = false: the chunk's
-// aggregate piece and window count; STAGE = true (after the block scan): the
-// chunk's windows laid out in the tile's list, each with the piece since the
-// previous window. The per-element rule is classify() of exact_cdf.cuh: the
-// bound at the element's start is the bound at the previous element's end.
 // Where a staging pass puts window w of the tile: the fused kernel's shared
 // lists, or the two-pass scan's global tile records.
 struct SmemWinSink {
@@ -634,6 +627,14 @@ struct NoWinSink {
   __device__ __forceinline__ void put(int, const Piece&, double) const {}
 };
 
+// The general per-chunk path of the tile analysis (chunks that hold a window
+// or an exact rounding tie: ~log2 N chunks per scan, but they sit on the
+// critical path - the first tile's successors wait for it): element by
+// element with running scalars, no arrays. STAGE = false: the chunk's
+// aggregate piece and window count; STAGE = true (after the block scan): the
+// chunk's windows handed to the sink in tile order, each with the piece since
+// the previous window. The per-element rule is classify() of exact_cdf.cuh: the
+// bound at the element's start is the bound at the previous element's end.
 template <int ITEMS, bool STAGE, class Sink>
 __device__ __forceinline__ void chunk_general(const double* my, double p0, long long cnt0, Piece carry, int win_excl,
                                               const Sink& sink, Piece& agg, int& nwin) {
