@@ -519,6 +519,11 @@ def test_config_errors():
     gpu.initialize_uniform([0.5, 0.5], [1.5, 1.5], [0.5, 0.5], [1.5, 1.5])
     with pytest.raises(ConfigError, match="integer step count"):
         gpu.pf_step([1.0, 1.0], 1, 0.0, 0.1, h=0.03)
+    # the scan-mode knob: unknown modes are CONFIG; the kernel-time slots are named per mode
+    assert gpu.lib.pfsmc_gpu_set_scan_mode(gpu.h, 7) == ConfigError.code
+    assert "k_scan_fused" in gpu.kernel_times() and "k_scan_cdf" not in gpu.kernel_times()
+    gpu.set_scan_mode("two_pass")
+    assert {"k_scan_pieces", "k_scan_cdf"} <= set(gpu.kernel_times())
     gpu.close()
 
 
