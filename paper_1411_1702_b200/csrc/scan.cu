@@ -1094,9 +1094,9 @@ void launch_scan(const Ctx& c, int ntiles, cudaStream_t st, int which) {
       else k_scan_cdf<16><<<ntiles, kThreads, 0, st>>>(c);
       break;
     case 3:  // single pass (single handle)
-      // 4 / 3 CTAs per SM (64 / 78 registers): measured faster than 3 / 2 (profiles/r02_notes.md)
+      // 4 CTAs per SM (64 registers) for both tile sizes: measured faster than 3 / 2 (profiles/r02_notes.md)
       if (small) k_scan_fused<8, 4><<<ntiles, kThreads, 0, st>>>(c);
-      else k_scan_fused<16, 3><<<ntiles, kThreads, 0, st>>>(c);
+      else k_scan_fused<16, 4><<<ntiles, kThreads, 0, st>>>(c);
       break;
     case 4:
       if (small) k_scan_pieces<8, 1><<<ntiles, kThreads, 0, st>>>(c);
