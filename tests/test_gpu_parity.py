@@ -160,6 +160,32 @@ def test_resample_randomized_structures_bit_exact(scan):
 
 
 @pytest.mark.parametrize("scan", SCAN_MODES)
+def test_resample_at_config5_full_size_bit_exact(scan):
+    """BASELINE config 5's per-GPU size (2^25): the device CDF is the sequential
+    sum bit for bit (8192 tiles of 4096: long look-back chains / the resolver's
+    super-tile path) and the ancestors are the reference's, for sigma = 4
+    log-normal mass and for a vector with a long zero run and a heavy element."""
+    from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
+    n = 1 << 25
+    rng = np.random.default_rng(25)
+    s = GpuSampler("payload64", PfConfig(particles=n, seed=31), ObservationModel([0], 1.0))
+    s.set_scan_mode(scan)
+    g1 = np.exp(4.0 * rng.standard_normal(n))
+    g1 /= g1.sum()
+    g2 = np.exp(rng.standard_normal(n) - 30.0)
+    g2[n // 3: n // 3 + (1 << 21)] = 0.0
+    g2[n // 2] = 0.75
+    for name, g in (("sigma4", g1), ("zeros+heavy", g2)):
+        anc, cdf = s.resample_from_g(g, 2, with_cdf=True)
+        ref = np.cumsum(g)
+        ref[-1] = max(ref[-1], 1.0)
+        assert np.array_equal(cdf, ref), (name, np.flatnonzero(cdf != ref)[:5])
+        want = O.resample(g, 31, 2)
+        assert np.array_equal(anc.astype(np.int64), want), name
+    s.close()
+
+
+@pytest.mark.parametrize("scan", SCAN_MODES)
 def test_resample_golden_fixture(scan):
     from paper_1411_1702_b200.sampler import GpuSampler, ObservationModel, PfConfig
     d = np.load(os.path.join(GOLD, "resample.npz"))
