@@ -475,7 +475,12 @@ def bench_workloads(local, fp64):
                                     "random_gather_peak_gbs": gpk,
                                     "random_read_rate_gbs": rnd_rate / 1e9 if rnd_rate else None,
                                     "search": best, "results": c5,
-                                    "results_by_search": by_search}
+                                    "results_by_search": by_search,
+                                    "moments_note": "SPLIT: an iteration's gather also accumulates the weighted 2x2 moment "
+                                                    "sums of the ensemble it produces (same tiles, thread layout and trees as "
+                                                    "the stats pass: same bits), so from the second iteration on with unchanged "
+                                                    "log-weights (the timed ones) the stats pass reads lw only; GUIDE and "
+                                                    "BUCKETED read theta in the stats pass every iteration"}
     # config 3: Robertson, 2^22, BDF2 m=2, Newton <= 4, lognormal: the filter runs the
     # log-spaced grid from j = 1 and is timed in windows spread along it (early,
     # mid, stiff), since the cost per step grows with the Newton iterations

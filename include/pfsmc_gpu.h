@@ -214,7 +214,11 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j);
  *            records are read once, in narrow L2-resident windows; the
  *            records are written to their slots (64-byte stores);
  *   SPLIT    the GUIDE search writing only the ancestors, then a separate
- *            slot-order gather. */
+ *            slot-order gather; that gather also accumulates the weighted
+ *            moment sums of the ensemble it writes (the stats pass's tiles,
+ *            thread layout and trees: the same bits), so the next iteration's
+ *            stats pass reads the log-weights only, as long as the host does
+ *            not change the log-weights, the ensemble or the mode in between. */
 enum { PFSMC_GPU_C5_SEARCH_GUIDE = 0, PFSMC_GPU_C5_SEARCH_BUCKETED = 1, PFSMC_GPU_C5_SEARCH_SPLIT = 2 };
 pfsmc_gpu_status pfsmc_gpu_c5_set_search(pfsmc_gpu_sampler* s, int mode);
 

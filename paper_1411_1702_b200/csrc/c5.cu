@@ -50,8 +50,12 @@ __device__ __forceinline__ void c5_finalize(const Ctx& c, const double* fin, dou
   st.cov[3] = fin[6] / S - m1 * m1;
 }
 
-template <int ITEMS, int SHARDED>
-__global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
+// MOM = 0 (single handle, PFSMC_GPU_C5_SEARCH_SPLIT, second iteration on with unchanged log-weights):
+// the pass reads lw only; each tile's five moment sums were made by the previous iteration's gather
+// (k_c5_gather_moments: same tile, same thread layout, same tree => the same bits) and are spliced
+// into the tile partial here, so each record's theta line is read once per iteration, not twice.
+template <int ITEMS, int SHARDED, int MOM = 1>
+__global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c, const double* mpart = nullptr) {
   constexpr int kTileT = ITEMS * kThreads;
   constexpr int V = 7;  // S, A0, A1, B00, B01, B11, finite count
   __shared__ double scratch[kWarps * V];
@@ -73,7 +77,8 @@ __global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
     for (int i = 0; i < ITEMS; ++i) {
       const long long k = base + i * kThreads + threadIdx.x;
       x[i] = k < c.N ? __ldcs(&c.lw[k]) : -INFINITY;
-      th[i] = k < c.N ? __ldcs(reinterpret_cast<const double2*>(rec + k * c.R + 6)) : make_double2(0.0, 0.0);
+      th[i] = (MOM && k < c.N) ? __ldcs(reinterpret_cast<const double2*>(rec + k * c.R + 6))
+                               : make_double2(0.0, 0.0);
     }
     double m = -INFINITY;
 #pragma unroll
@@ -84,16 +89,29 @@ __global__ void __launch_bounds__(kThreads) k_c5_stats(Ctx c) {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const double e = isnan(x[i]) ? NAN : (x[i] == -INFINITY ? 0.0 : exp(x[i] - M));
-      const double d0 = th[i].x - k0, d1 = th[i].y - k1;
       v[0] += e;
-      v[1] += e * d0;
-      v[2] += e * d1;
-      v[3] += e * (d0 * d0);
-      v[4] += e * (d0 * d1);
-      v[5] += e * (d1 * d1);
+      if (MOM) {
+        const double d0 = th[i].x - k0, d1 = th[i].y - k1;
+        v[1] += e * d0;
+        v[2] += e * d1;
+        v[3] += e * (d0 * d0);
+        v[4] += e * (d0 * d1);
+        v[5] += e * (d1 * d1);
+      }
       v[6] += isfinite(x[i]) ? 1.0 : 0.0;
     }
-    block_sums<V>(v, scratch);
+    if (MOM) {
+      block_sums<V>(v, scratch);
+    } else {  // only the mass and the finite count are summed here (the same per-component tree)
+      double v2[2] = {v[0], v[6]};
+      block_sums<2>(v2, scratch);
+      if (threadIdx.x == 0) {
+        v[0] = v2[0];
+        v[6] = v2[1];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[1 + k] = __ldcg(&mpart[static_cast<size_t>(t) * 5 + k]);
+      }
+    }
     const int g = t / kC5Group;
     const int gsize = min(kC5Group, c.ntiles - g * kC5Group);
     if (threadIdx.x == 0) {
@@ -197,6 +215,65 @@ __global__ void __launch_bounds__(kThreads) k_c5_gather(Ctx c) {
     const unsigned as = __shfl_sync(0xffffffffu, a, slot);
     const long long ns = wbase + slot;
     if (ns < c.N) st_hint(dst + ns * 4 + part, ld_hint(src + static_cast<long long>(as) * 4 + part, pol), pol);
+  }
+}
+
+// The same gather with the NEXT iteration's weighted-moment sums made on the way (the gathered record
+// passes through registers): one CTA per exact-CDF tile, thread j visits the tile's slots
+// i * 256 + j in order - the stats pass's thread layout - so with e = exp(lw - M_t) (M_t: the tile
+// maximum the stats pass of this iteration left in tile_m; lw does not change until the next stats
+// pass or the host invalidates) and the same block tree the five sums are bitwise the stats pass's.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_c5_gather_moments(Ctx c, double* mpart) {
+  constexpr int kTileT = ITEMS * kThreads;
+  constexpr int V = 7;
+  __shared__ double scratch[kWarps * V];
+  if (grid_error(c)) return;
+  const int t = blockIdx.x;
+  const long long base = static_cast<long long>(t) * kTileT;
+  const int lane = threadIdx.x & 31;
+  const int cur = c.st->cur;
+  const double k0 = c.st->mu[0], k1 = c.st->mu[1];  // this iteration's mean: what the next stats pass centres on
+  const double M = __ldcg(&c.tile_m[t]);
+  const double2* src = reinterpret_cast<const double2*>(c.rec[cur]);
+  double2* dst = reinterpret_cast<double2*>(c.rec[cur ^ 1]);
+  const uint64_t pol = l2_policy_stream();
+  double v[V] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+  for (int i = 0; i < ITEMS; ++i) {
+    const long long n = base + i * kThreads + threadIdx.x;
+    const unsigned a = n < c.N ? __ldcs(&c.anc[n]) : 0u;
+    const double x = n < c.N ? __ldcs(&c.lw[n]) : -INFINITY;
+    const long long wbase = n - lane;
+    double2 th = make_double2(0.0, 0.0);  // theta of THIS lane's slot
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+      const int slot = q + lane / 4, part = lane & 3;
+      const unsigned as = __shfl_sync(0xffffffffu, a, slot);
+      const long long ns = wbase + slot;
+      double2 r = make_double2(0.0, 0.0);
+      if (ns < c.N) {
+        r = ld_hint(src + static_cast<long long>(as) * 4 + part, pol);
+        st_hint(dst + ns * 4 + part, r, pol);
+      }
+      // the record's last 16 bytes (theta) sit in lane 4 * (slot % 8) + 3 of this sub-round: hand
+      // them to the slot's own lane
+      const int from = 4 * (lane & 7) + 3;
+      const double tx = __shfl_sync(0xffffffffu, r.x, from), ty = __shfl_sync(0xffffffffu, r.y, from);
+      if ((lane >> 3) == (q >> 3)) th = make_double2(tx, ty);
+    }
+    const double e = isnan(x) ? NAN : (x == -INFINITY ? 0.0 : exp(x - M));
+    const double d0 = th.x - k0, d1 = th.y - k1;
+    v[1] += e * d0;
+    v[2] += e * d1;
+    v[3] += e * (d0 * d0);
+    v[4] += e * (d0 * d1);
+    v[5] += e * (d1 * d1);
+  }
+  block_sums<V>(v, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) mpart[static_cast<size_t>(t) * 5 + k] = v[1 + k];
   }
 }
 
@@ -518,6 +595,7 @@ extern "C" {
 pfsmc_gpu_status pfsmc_gpu_c5_set_logweights(pfsmc_gpu_sampler* s, double sigma, uint64_t key) {
   return guarded([&] {
     if (s->cfg.model != Payload64Model::ID) throw ConfigError("c5: needs the PAYLOAD64 model");
+    s->c5_moments_ready = false;
     k_c5_weights<<<s->grid, kThreads, 0, s->stream>>>(s->ctx, sigma, key);
     CK(cudaGetLastError());
     return PFSMC_GPU_OK;
@@ -533,10 +611,19 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
     c.lg = c.lw;  // the fitness log-weights are the log-weights here
     CK(cudaMemsetAsync(&s->st->error, 0, sizeof(int), s->stream));
     // one wave: 126 (ITEMS 16) / 74 (ITEMS 8) registers => 2 / 3 blocks per SM
-    if (c.tile_log2 == 11)
+    const bool fuse = s->c5_fuse_moments && s->c5_search == PFSMC_GPU_C5_SEARCH_SPLIT;
+    if (fuse && !s->c5_mpart) s->c5_mpart = s->dalloc<double>(static_cast<size_t>(s->ntiles) * 5);
+    if (fuse && s->c5_moments_ready) {  // the previous iteration's gather left this ensemble's moment sums
+      if (c.tile_log2 == 11)
+        k_c5_stats<8, 0, 0><<<std::min(s->ntiles, s->num_sms * 6), kThreads, 0, s->stream>>>(c, s->c5_mpart);
+      else
+        k_c5_stats<16, 0, 0><<<std::min(s->ntiles, s->num_sms * 6), kThreads, 0, s->stream>>>(c, s->c5_mpart);
+    } else if (c.tile_log2 == 11) {
       k_c5_stats<8, 0><<<std::min(s->ntiles, s->num_sms * 3), kThreads, 0, s->stream>>>(c);
-    else
+    } else {
       k_c5_stats<16, 0><<<std::min(s->ntiles, s->num_sms * 2), kThreads, 0, s->stream>>>(c);
+    }
+    s->c5_moments_ready = false;
     launch_scan_single(s, c, s->stream);
     if (s->c5_search == PFSMC_GPU_C5_SEARCH_BUCKETED) {
       const C5Buckets b = c5_buckets(s);
@@ -554,7 +641,13 @@ pfsmc_gpu_status pfsmc_gpu_c5_iteration(pfsmc_gpu_sampler* s, uint64_t j) {
       *s->sp_host = sp;
       CK(cudaMemcpyAsync(s->sp_dev, s->sp_host, sizeof(StepParams), cudaMemcpyHostToDevice, s->stream));
       launch_search_only(c, s->grid, s->stream);
-      k_c5_gather<<<s->grid, kThreads, 0, s->stream>>>(c);
+      if (fuse) {
+        if (c.tile_log2 == 11) k_c5_gather_moments<8><<<s->ntiles, kThreads, 0, s->stream>>>(c, s->c5_mpart);
+        else k_c5_gather_moments<16><<<s->ntiles, kThreads, 0, s->stream>>>(c, s->c5_mpart);
+        s->c5_moments_ready = true;  // until the log-weights, the records or the mean change on the host's side
+      } else {
+        k_c5_gather<<<s->grid, kThreads, 0, s->stream>>>(c);
+      }
       s->c5_anc_pending = false;
     } else {
       k_c5_serve<<<s->grid, kThreads, 0, s->stream>>>(c, j);
@@ -645,6 +738,16 @@ pfsmc_gpu_status pfsmc_gpu_c5_set_search(pfsmc_gpu_sampler* s, int mode) {
     if (mode < PFSMC_GPU_C5_SEARCH_GUIDE || mode > PFSMC_GPU_C5_SEARCH_SPLIT)
       throw ConfigError("c5_set_search: mode must be PFSMC_GPU_C5_SEARCH_GUIDE, _BUCKETED or _SPLIT");
     s->c5_search = mode;
+    s->c5_moments_ready = false;
+    return PFSMC_GPU_OK;
+  });
+}
+
+// Test / A-B knob (not in the public header): 0 = every iteration's stats pass reads theta itself.
+pfsmc_gpu_status pfsmc_gpu_c5_debug_fuse_moments(pfsmc_gpu_sampler* s, int on) {
+  return guarded([&] {
+    s->c5_fuse_moments = on != 0;
+    s->c5_moments_ready = false;
     return PFSMC_GPU_OK;
   });
 }

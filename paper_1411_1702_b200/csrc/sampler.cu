@@ -361,6 +361,7 @@ void raise_pending(pfsmc_gpu_sampler* s) {
 }
 
 void enqueue_step(pfsmc_gpu_sampler* s, const StepParams* host_sp, const StepParams* dev_sp) {
+  s->c5_moments_ready = false;
   if (s->shard_api)
     throw ConfigError("step: a shard handle runs only the sharded phases (pfsmc_gpu_shard_step / shard_*)");
   if (!s->have_ensemble) throw ConfigError("step: no ensemble (call set_ensemble or init_*)");
@@ -660,6 +661,7 @@ pfsmc_gpu_status pfsmc_gpu_set_ensemble(pfsmc_gpu_sampler* s, const double* stat
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaGetLastError());
     s->have_ensemble = true;
+    s->c5_moments_ready = false;
     return PFSMC_GPU_OK;
   });
 }
@@ -718,6 +720,7 @@ static pfsmc_gpu_status do_init(pfsmc_gpu_sampler* s, int kind, const std::vecto
     cudaFree(dprm);
     s->allocs.pop_back();
     s->have_ensemble = true;
+    s->c5_moments_ready = false;
     return PFSMC_GPU_OK;
   });
 }

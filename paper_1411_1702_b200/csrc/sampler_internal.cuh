@@ -172,6 +172,10 @@ struct pfsmc_gpu_sampler {
   double* c5_gall = nullptr;       // sharded: every rank's stats group partials (world * groups * 7)
   bool c5_fitness_is_lw = false;   // sharded scan phases of a config-5 iteration read lw as the fitness
   unsigned long long* c5_remote = nullptr;  // sharded: records pulled from other GPUs (device counter)
+  // config 5, SPLIT search: the gather makes the next iteration's moment sums (c5.cu k_c5_gather_moments)
+  bool c5_fuse_moments = true;
+  bool c5_moments_ready = false;   // c5_mpart holds the current ensemble's sums for the current log-weights
+  double* c5_mpart = nullptr;      // [ntiles][5]
 
   // the Ensemble& boundary's device staging (set / get_ensemble), allocated once
   double* stage_x = nullptr;   // N x d states (AoS, the caller's layout)

@@ -366,6 +366,12 @@ class GpuSampler:
             self._check(self.lib.pfsmc_gpu_c5_debug_bucket_cap(self.h, C.c_longlong(debug_bucket_cap)))
         self._check(self.lib.pfsmc_gpu_c5_set_search(self.h, {"guide": 0, "bucketed": 1, "split": 2}[mode]))
 
+    def c5_fuse_moments(self, on: bool):
+        """A/B and test knob: False makes every config-5 iteration's stats pass read theta itself
+        (default: with the SPLIT search the gather makes the next iteration's moment sums)."""
+        self.lib.pfsmc_gpu_c5_debug_fuse_moments.restype = C.c_int
+        self._check(self.lib.pfsmc_gpu_c5_debug_fuse_moments(self.h, C.c_int(1 if on else 0)))
+
     def set_scan_mode(self, mode: str):
         """'fused' (one-kernel exact scan with decoupled look-back, the default)
         or 'two_pass' (records pass + resolver, CDF pass; include/pfsmc_gpu.h).

@@ -896,6 +896,39 @@ def test_c5_bucketed_search_is_the_slot_order_search(n, cap):
                 assert np.array_equal(x, y), other
 
 
+@pytest.mark.parametrize("n", [1 << 16, (1 << 22) + 4097 * 3 + 5])
+def test_c5_gather_moments_are_the_stats_pass_moments(n):
+    """SPLIT search: from the second iteration on the stats pass takes each
+    tile's weighted-moment sums from the previous iteration's gather
+    (k_c5_gather_moments) instead of reading theta again. Same tiles, thread
+    layout and trees: the mean, covariance, ancestors and records are bitwise
+    those of the pass that reads theta itself, also after the log-weights change."""
+    from paper_1411_1702_b200.sampler import Ensemble, GpuSampler, ObservationModel, PfConfig
+    rng = np.random.default_rng(8)
+    states = rng.standard_normal((n, 6))
+    params = rng.standard_normal((n, 2))
+    out = {}
+    for fuse in (True, False):
+        s = GpuSampler("payload64", PfConfig(particles=n, seed=12), ObservationModel([0], 1.0))
+        s.c5_set_search("split")
+        s.c5_fuse_moments(fuse)
+        s.set_ensemble(Ensemble(states, params, np.zeros(n), np.zeros(2), np.eye(2)))
+        rows = []
+        for sigma, key in ((1.0, 3), (4.0, 9)):
+            s.c5_set_logweights(sigma, key)
+            for it in range(3):
+                s.c5_iteration(10 * key + it)
+                s.synchronize()
+                e = s.get_ensemble()
+                rows.append((e.mean_u.copy(), e.cov_u.copy(), s.step_diagnostics()[0].copy()))
+        e = s.get_ensemble()
+        out[fuse] = (rows, e.states.copy(), e.params_u.copy())
+        s.close()
+    for (m1, c1, a1), (m0, c0, a0) in zip(out[True][0], out[False][0]):
+        assert np.array_equal(m1, m0) and np.array_equal(c1, c0) and np.array_equal(a1, a0)
+    assert np.array_equal(out[True][1], out[False][1]) and np.array_equal(out[True][2], out[False][2])
+
+
 def test_c5_bucket_spill_overflow_raises():
     """More items than bucket capacity + spill list: an internal error at the
     next synchronize, not a silent partial gather."""
